@@ -1,0 +1,259 @@
+"""CPU oracle for Recurrent Arc Consistency (RAC), arXiv 2407.11388.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_2407_11388_b200``) never imports it and
+shares no code with it.
+
+Contents
+  * ``Oracle`` -- ctypes wrapper over ``oracle/oracle.c`` (plain C, built with
+    gcc): O1 naive RAC (Eq. 1, loop of Alg. 1 lines
+    198-210), O2 AC-3 (line 29), the AC definition audit (lines 49-61) and the
+    O4 certificate (Lemma 1, lines 79-82).
+  * ``brute_force_dac`` -- O3: D_ac as the union of all arc-consistent subsets
+    of D, by enumerating every subset (tiny inputs).
+  * ``rac_python`` -- a pure-Python transcription of Eq. 1 (tiny inputs), used
+    to cross-check the C transcription.
+
+Parity status: every function here is pinned by tests/test_oracle.py
+(brute force, closed forms, hand traces from SPEC.md, AC-3 agreement,
+certificate acceptance/rejection, invariants).  No function is unpinned.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+OK = 0
+WIPEOUT = 1
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so with gcc (plain C, -O2, no SIMD intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "..", "synth", "csp_synth.h"))):
+        tmp = _LIB + ".tmp.%d" % os.getpid()
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        u64p = ctypes.POINTER(ctypes.c_uint64)
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        lib.orc_build.restype = P
+        lib.orc_build.argtypes = [ctypes.c_int, i32p, ctypes.c_int, i32p, i32p, u64p, ctypes.c_int]
+        lib.orc_build_synth.restype = P
+        lib.orc_build_synth.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64]
+        lib.orc_free.argtypes = [P]
+        lib.orc_free.restype = None
+        lib.orc_rac.argtypes = [P, u64p, u64p, i32p, i32p, ctypes.c_int]
+        lib.orc_rac.restype = ctypes.c_int
+        lib.orc_ac3.argtypes = [P, u64p, u64p, ctypes.POINTER(ctypes.c_int64)]
+        lib.orc_ac3.restype = ctypes.c_int
+        lib.orc_is_ac.argtypes = [P, u64p]
+        lib.orc_is_ac.restype = ctypes.c_int
+        lib.orc_certify.argtypes = [P, u64p, u64p, i32p, ctypes.c_int]
+        lib.orc_certify.restype = ctypes.c_int
+        lib.orc_support.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, i32p]
+        lib.orc_support.restype = ctypes.c_uint64
+        lib.orc_degree.argtypes = [P, ctypes.c_int]
+        lib.orc_degree.restype = ctypes.c_int
+        lib.orc_row_supported_synth.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
+                                                ctypes.c_uint64, ctypes.c_int, ctypes.c_int, u64p]
+        lib.orc_row_supported_synth.restype = ctypes.c_int
+        lib.orc_domain_size.argtypes = [P, u64p]
+        lib.orc_domain_size.restype = ctypes.c_int64
+        _lib = lib
+    return _lib
+
+
+def _u64p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+class Oracle:
+    """One CSP instance in the oracle's own per-arc layout."""
+
+    def __init__(self, handle, n: int, dom: np.ndarray):
+        self._h = handle
+        self.n = n
+        self.dom = dom
+
+    @classmethod
+    def from_instance(cls, inst) -> "Oracle":
+        lib = _load()
+        dom = np.ascontiguousarray(inst.dom, dtype=np.int32)
+        xs = np.ascontiguousarray(inst.xs, dtype=np.int32)
+        ys = np.ascontiguousarray(inst.ys, dtype=np.int32)
+        rows = np.ascontiguousarray(inst.rows, dtype=np.uint64)
+        stride = rows.shape[1] if rows.ndim == 2 and rows.shape[0] else int(dom.max())
+        if rows.size == 0:
+            rows = np.zeros((1, max(stride, 1)), dtype=np.uint64)
+        h = lib.orc_build(inst.n, _i32p(dom), xs.shape[0], _i32p(xs), _i32p(ys), _u64p(rows), stride)
+        if not h:
+            raise ValueError("invalid instance")
+        return cls(h, inst.n, dom)
+
+    @classmethod
+    def from_synth(cls, n: int, d: int, dens_q32: int, t_q16: int, seed: int) -> "Oracle":
+        lib = _load()
+        h = lib.orc_build_synth(n, d, dens_q32, t_q16, seed)
+        if not h:
+            raise ValueError("invalid synth parameters")
+        return cls(h, n, np.full(n, d, dtype=np.int32))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.orc_free(self._h)
+            self._h = None
+
+    def rac(self, d_in, full: bool = False, with_epochs: bool = True):
+        """O1. Returns (status, d_out, iterations, removed_at[n,64] or None)."""
+        lib = _load()
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        d_out = np.zeros(self.n, dtype=np.uint64)
+        it = np.zeros(1, dtype=np.int32)
+        rem = np.zeros(self.n * 64, dtype=np.int32) if with_epochs else None
+        st = lib.orc_rac(self._h, _u64p(d_in), _u64p(d_out), _i32p(it),
+                         _i32p(rem) if rem is not None else None, 1 if full else 0)
+        return st, d_out, int(it[0]), (rem.reshape(self.n, 64) if rem is not None else None)
+
+    def ac3(self, d_in):
+        """O2. Returns (status, d_out, revisions)."""
+        lib = _load()
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        d_out = np.zeros(self.n, dtype=np.uint64)
+        rev = ctypes.c_int64(0)
+        st = lib.orc_ac3(self._h, _u64p(d_in), _u64p(d_out), ctypes.byref(rev))
+        return st, d_out, int(rev.value)
+
+    def is_ac(self, D) -> bool:
+        D = np.ascontiguousarray(D, dtype=np.uint64)
+        return bool(_load().orc_is_ac(self._h, _u64p(D)))
+
+    def certify(self, d_in, d_out, removed_at, check_ac: bool = True) -> int:
+        """O4. 0 = accepted; nonzero = reason code (see oracle.c)."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        d_out = np.ascontiguousarray(d_out, dtype=np.uint64)
+        rem = np.ascontiguousarray(np.asarray(removed_at, dtype=np.int32).reshape(-1))
+        return int(_load().orc_certify(self._h, _u64p(d_in), _u64p(d_out), _i32p(rem), 1 if check_ac else 0))
+
+    def support(self, x: int, y: int, a: int) -> Tuple[bool, int]:
+        p = ctypes.c_int32(0)
+        s = _load().orc_support(self._h, x, y, a, ctypes.byref(p))
+        return bool(p.value), int(s)
+
+    def degree(self, x: int) -> int:
+        return int(_load().orc_degree(self._h, x))
+
+
+def row_supported_synth(n: int, d: int, dens_q32: int, t_q16: int, seed: int, x: int, a: int, D) -> bool:
+    """Would (x,a) survive one step of Eq. 1 from D?  Straight from the generator."""
+    D = np.ascontiguousarray(D, dtype=np.uint64)
+    return bool(_load().orc_row_supported_synth(n, d, dens_q32, t_q16, seed, x, a, _u64p(D)))
+
+
+# ----------------------------------------------------------------------------- pure Python
+def _support_sets(inst):
+    """{(x,y): {a: set(b)}} for both orientations of every declared constraint."""
+    sup = {}
+    for k in range(inst.n_rel):
+        x, y = int(inst.xs[k]), int(inst.ys[k])
+        fw = {a: set() for a in range(int(inst.dom[x]))}
+        bw = {b: set() for b in range(int(inst.dom[y]))}
+        for a in range(int(inst.dom[x])):
+            r = int(inst.rows[k, a])
+            for b in range(int(inst.dom[y])):
+                if (r >> b) & 1:
+                    fw[a].add(b)
+                    bw[b].add(a)
+        sup[(x, y)] = fw
+        sup[(y, x)] = bw
+    return sup
+
+
+def _to_set(D) -> set:
+    return {(x, a) for x in range(len(D)) for a in range(64) if (int(D[x]) >> a) & 1}
+
+
+def _from_set(S, n) -> np.ndarray:
+    out = np.zeros(n, dtype=np.uint64)
+    for (x, a) in S:
+        out[x] |= np.uint64(1) << np.uint64(a)
+    return out
+
+
+def _is_ac_set(sup, S: set) -> bool:
+    """PAPER.md lines 49-61, literally: ∀(x,a)∈S ∀c_xy∈C_x: c_xy|(x,a) ∩ S ≠ ∅."""
+    for (x, a) in S:
+        for (xx, y), rows in sup.items():
+            if xx != x:
+                continue
+            if not any((y, b) in S for b in rows[a]):
+                return False
+    return True
+
+
+def brute_force_dac(inst, d_in) -> np.ndarray:
+    """O3: D_ac = ⋃{D' ⊆ D : D' arc consistent}, by
+    enumerating all 2^|D| subsets.  Only for |D| <= ~16."""
+    sup = _support_sets(inst)
+    elems = sorted(_to_set(d_in))
+    if len(elems) > 18:
+        raise ValueError("brute force limited to |D| <= 18")
+    union = set()
+    for mask in range(1 << len(elems)):
+        S = {elems[i] for i in range(len(elems)) if (mask >> i) & 1}
+        if _is_ac_set(sup, S):
+            union |= S
+    return _from_set(union, inst.n)
+
+
+def rac_python(inst, d_in, full: bool = False):
+    """Eq. 1 in set notation, pure Python, tiny inputs.
+
+    D~(0) = ∅; D~(k) = D~(k-1) ∪ {(x,a) | ∃y: c_xy|(x,a) ∩ (D \\ D~(k-1)) = ∅}
+    with Alg. 1's loop control (lines 198-210).  Returns (status, d_out, iterations,
+    list of per-step removal sets V^(k))."""
+    sup = _support_sets(inst)
+    D = _to_set(d_in)
+    removed = set()
+    trace: List[set] = []
+    k = 0
+    while True:
+        k += 1
+        live = D - removed
+        new = set()
+        for (x, a) in live:
+            for (xx, y), rows in sup.items():
+                if xx == x and not any((y, b) in live for b in rows[a]):
+                    new.add((x, a))
+                    break
+        removed |= new
+        trace.append(new)
+        cur = D - removed
+        wipe = any(not any((x, a) in cur for a in range(int(inst.dom[x]))) for x in range(inst.n))
+        if wipe and not full:
+            return WIPEOUT, _from_set(cur, inst.n), k, trace
+        if not new:
+            return (WIPEOUT if wipe else OK), _from_set(cur, inst.n), k, trace

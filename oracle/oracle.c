@@ -1,0 +1,453 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for Recurrent Arc
+ * Consistency (RAC), arXiv 2407.11388.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code with the CUDA path (paper_2407_11388_b200/csrc): no
+ * headers, helpers or tables; the only common dependency is the seeded input
+ * generator synth/csp_synth.h, which holds none of the method's arithmetic.
+ *
+ * Layout (deliberately different from the GPU's [x][a][y] masks): a per-arc
+ * adjacency list.  For variable x, nbr[x][k] is the k-th constrained
+ * neighbour y (ascending), and sup[x][k*dom[x] + a] is the support set
+ * c_xy|(x,a) = { tau[y] | tau in rel(c_xy), tau[x] = a }
+ * as a bitset over dom(y).  C_x is { c_{x,nbr[x][k]} }.
+ * Domain states are one uint64 per variable, bit a set iff (x,a) in D.
+ *
+ * Functions:
+ *   orc_rac     -- O1: the RAC recurrence, Eq. 1 run
+ *                  literally and synchronously, with Alg. 1's loop and checks
+ *                  (lines 198-210).  Counts iterations, records removal epochs.
+ *   orc_ac3     -- O2: textbook AC-3 (propagation queue + revision, PAPER.md
+ *                  line 29; SPEC.md ac3_engine lines 262-310), FIFO.
+ *   orc_is_ac   -- the definition of arc consistency.
+ *   orc_certify -- O4: D_out = D_ac certificate: arc-consistency audit plus
+ *                  Lemma 1 (proof 304-308) applied to
+ *                  every removal in epoch order.
+ *   orc_row_supported_synth -- one (x,a) support test against D computed
+ *                  straight from the generator (sampled checks at any size).
+ *
+ * O3 (brute-force union of all arc-consistent subsets)
+ * is in oracle/__init__.py (pure Python, tiny instances).
+ *
+ * Readings of the paper:
+ *   R1  Eq. 1 is read in the intersection form of line 59: (x,a) is removed
+ *       at step k iff some declared c_xy in C_x has c_xy|(x,a) ∩ D_{k-1}(y) = ∅.
+ *   R2  "∃y" ranges over declared constraints only; absent pairs never remove.
+ *   R3  iterations = number of passes executed, including the final no-change
+ *       pass; on wipeout the detecting pass is counted (Alg. 1 loop body count).
+ *   R4  update is synchronous (Jacobi): step k reads only D_{k-1}.
+ *   R5  wipeout is checked before convergence (Alg. 1).
+ *   R6  on wipeout (stop mode) the output is D after the detecting pass.
+ *   R7  an empty row in D_in: one pass runs, then WIPEOUT (iterations = 1).
+ *   FULL mode ignores wipeouts and iterates to the definitional D_ac.
+ *
+ * Parity pins: see tests/test_oracle.py (brute force, closed forms, hand
+ * traces, AC-3 agreement, certificate, invariants).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "../synth/csp_synth.h"
+
+#define ORC_OK 0
+#define ORC_WIPEOUT 1
+#define ORC_EINVAL (-1)
+
+typedef struct {
+  int n;
+  int *dom;        /* dom[x], 1..64                                  */
+  int *deg;        /* number of constrained neighbours of x          */
+  int **nbr;       /* nbr[x][k] ascending                            */
+  int **rev;       /* rev[x][k] = index of x in nbr[nbr[x][k]]       */
+  uint64_t **sup;  /* sup[x][k*dom[x] + a] = c_{x,nbr[x][k]}|(x,a)   */
+} orc_csp;
+
+static uint64_t dom_mask(int k) { return k >= 64 ? ~0ULL : ((1ULL << k) - 1ULL); }
+
+static int popc64(uint64_t v) {
+  int c = 0;
+  while (v) { v &= v - 1; ++c; }
+  return c;
+}
+
+void orc_free(orc_csp *c) {
+  if (!c) return;
+  for (int x = 0; x < c->n; ++x) {
+    if (c->nbr) free(c->nbr[x]);
+    if (c->rev) free(c->rev[x]);
+    if (c->sup) free(c->sup[x]);
+  }
+  free(c->nbr); free(c->rev); free(c->sup); free(c->deg); free(c->dom);
+  free(c);
+}
+
+static orc_csp *alloc_csp(int n, const int *dom) {
+  orc_csp *c = (orc_csp *)calloc(1, sizeof(orc_csp));
+  if (!c) return NULL;
+  c->n = n;
+  c->dom = (int *)calloc((size_t)n, sizeof(int));
+  c->deg = (int *)calloc((size_t)n, sizeof(int));
+  c->nbr = (int **)calloc((size_t)n, sizeof(int *));
+  c->rev = (int **)calloc((size_t)n, sizeof(int *));
+  c->sup = (uint64_t **)calloc((size_t)n, sizeof(uint64_t *));
+  if (!c->dom || !c->deg || !c->nbr || !c->rev || !c->sup) { orc_free(c); return NULL; }
+  for (int x = 0; x < n; ++x) c->dom[x] = dom[x];
+  return c;
+}
+
+/* Index of y in nbr[x] (ascending), or -1. */
+static int arc_index(const orc_csp *c, int x, int y) {
+  int lo = 0, hi = c->deg[x] - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) / 2;
+    if (c->nbr[x][mid] == y) return mid;
+    if (c->nbr[x][mid] < y) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+/* After deg[] is known: allocate per-x arrays. */
+static int alloc_arcs(orc_csp *c) {
+  for (int x = 0; x < c->n; ++x) {
+    size_t k = (size_t)(c->deg[x] > 0 ? c->deg[x] : 1);
+    c->nbr[x] = (int *)malloc(k * sizeof(int));
+    c->rev[x] = (int *)malloc(k * sizeof(int));
+    c->sup[x] = (uint64_t *)calloc(k * (size_t)c->dom[x], sizeof(uint64_t));
+    if (!c->nbr[x] || !c->rev[x] || !c->sup[x]) return -1;
+  }
+  return 0;
+}
+
+static void fill_rev(orc_csp *c) {
+  for (int x = 0; x < c->n; ++x)
+    for (int k = 0; k < c->deg[x]; ++k) c->rev[x][k] = arc_index(c, c->nbr[x][k], x);
+}
+
+static int cmp_int(const void *a, const void *b) {
+  int u = *(const int *)a, v = *(const int *)b;
+  return (u > v) - (u < v);
+}
+
+/*
+ * Build from explicit relations: constraint r is on (xs[r], ys[r]) and
+ * rows[r*row_stride + a] is row a of rel(c_{xs[r],ys[r]}) (bit b set iff
+ * (a,b) allowed).  Either orientation is accepted.  Returns NULL on invalid
+ * input (x == y, out of range, a duplicate unordered pair, bits beyond the
+ * domain sizes).
+ */
+orc_csp *orc_build(int n, const int *dom, int n_rel, const int *xs, const int *ys,
+                   const uint64_t *rows, int row_stride) {
+  if (n < 1) return NULL;
+  for (int x = 0; x < n; ++x)
+    if (dom[x] < 1 || dom[x] > 64) return NULL;
+  orc_csp *c = alloc_csp(n, dom);
+  if (!c) return NULL;
+  for (int r = 0; r < n_rel; ++r) {
+    int x = xs[r], y = ys[r];
+    if (x < 0 || y < 0 || x >= n || y >= n || x == y) { orc_free(c); return NULL; }
+    c->deg[x]++; c->deg[y]++;
+  }
+  if (alloc_arcs(c)) { orc_free(c); return NULL; }
+  int *fill = (int *)calloc((size_t)n, sizeof(int));
+  for (int r = 0; r < n_rel; ++r) {
+    c->nbr[xs[r]][fill[xs[r]]++] = ys[r];
+    c->nbr[ys[r]][fill[ys[r]]++] = xs[r];
+  }
+  free(fill);
+  for (int x = 0; x < n; ++x) {
+    qsort(c->nbr[x], (size_t)c->deg[x], sizeof(int), cmp_int);
+    for (int k = 1; k < c->deg[x]; ++k)
+      if (c->nbr[x][k] == c->nbr[x][k - 1]) { orc_free(c); return NULL; } /* duplicate pair */
+  }
+  for (int r = 0; r < n_rel; ++r) {
+    int x = xs[r], y = ys[r];
+    int kx = arc_index(c, x, y), ky = arc_index(c, y, x);
+    for (int a = 0; a < dom[x]; ++a) {
+      uint64_t row = rows[(size_t)r * (size_t)row_stride + (size_t)a];
+      if (row & ~dom_mask(dom[y])) { orc_free(c); return NULL; }
+      /* arc x -> y: c_xy|(x,a) is row a itself */
+      c->sup[x][(size_t)kx * dom[x] + a] = row;
+      /* arc y -> x: c_yx|(y,b) = { a : (a,b) allowed } -- the transpose */
+      for (int b = 0; b < dom[y]; ++b)
+        if ((row >> b) & 1ULL) c->sup[y][(size_t)ky * dom[y] + b] |= 1ULL << a;
+    }
+    for (int a = dom[x]; a < row_stride; ++a)
+      if (rows[(size_t)r * (size_t)row_stride + (size_t)a]) { orc_free(c); return NULL; }
+  }
+  fill_rev(c);
+  return c;
+}
+
+/* Build the seeded random instance of synth/csp_synth.h (uniform domain d). */
+orc_csp *orc_build_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed) {
+  if (n < 1 || d < 1 || d > 64) return NULL;
+  int *dom = (int *)malloc((size_t)n * sizeof(int));
+  for (int x = 0; x < n; ++x) dom[x] = d;
+  orc_csp *c = alloc_csp(n, dom);
+  free(dom);
+  if (!c) return NULL;
+  /* pass 1: degrees */
+  for (int x = 0; x < n; ++x)
+    for (int y = x + 1; y < n; ++y)
+      if (synth_present(seed, (uint32_t)n, (uint32_t)x, (uint32_t)y, dens_q32)) { c->deg[x]++; c->deg[y]++; }
+  if (alloc_arcs(c)) { orc_free(c); return NULL; }
+  /* pass 2: neighbour lists, ascending in y */
+  int *fill = (int *)calloc((size_t)n, sizeof(int));
+  for (int x = 0; x < n; ++x)
+    for (int y = 0; y < n; ++y) {
+      if (y == x) continue;
+      int lo = x < y ? x : y, hi = x < y ? y : x;
+      if (synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) c->nbr[x][fill[x]++] = y;
+    }
+  free(fill);
+  for (int x = 0; x < n; ++x) {
+    for (int k = 0; k < c->deg[x]; ++k) {
+      int y = c->nbr[x][k];
+      if (x < y) {
+        for (int a = 0; a < d; ++a)
+          c->sup[x][(size_t)k * d + a] =
+              synth_row(seed, (uint32_t)n, (uint32_t)d, (uint32_t)x, (uint32_t)y, (uint32_t)a, t_q16);
+      } else {
+        /* c_xy with x > y is the transpose of c_yx: (a,b) allowed in c_xy iff (b,a) allowed in c_yx */
+        for (int b = 0; b < d; ++b) {
+          uint64_t row_b = synth_row(seed, (uint32_t)n, (uint32_t)d, (uint32_t)y, (uint32_t)x, (uint32_t)b, t_q16);
+          for (int a = 0; a < d; ++a)
+            if ((row_b >> a) & 1ULL) c->sup[x][(size_t)k * d + a] |= 1ULL << b;
+        }
+      }
+    }
+  }
+  fill_rev(c);
+  return c;
+}
+
+int orc_n(const orc_csp *c) { return c->n; }
+int orc_degree(const orc_csp *c, int x) { return c->deg[x]; }
+
+/* c_xy|(x,a) as a bitset over dom(y); *present = 0 (and result 0) if no c_xy. */
+uint64_t orc_support(const orc_csp *c, int x, int y, int a, int *present) {
+  int k = (x == y) ? -1 : arc_index(c, x, y);
+  if (k < 0) { *present = 0; return 0; }
+  *present = 1;
+  return c->sup[x][(size_t)k * c->dom[x] + a];
+}
+
+/*
+ * The definition of arc consistency:
+ *   D is AC  <=>  for all (x,a) in D, for all c_xy in C_x: c_xy|(x,a) ∩ D(y) ≠ ∅.
+ * Returns 1 if D is arc consistent, else 0.
+ */
+int orc_is_ac(const orc_csp *c, const uint64_t *D) {
+  for (int x = 0; x < c->n; ++x)
+    for (int a = 0; a < c->dom[x]; ++a) {
+      if (!((D[x] >> a) & 1ULL)) continue;
+      for (int k = 0; k < c->deg[x]; ++k) {
+        int y = c->nbr[x][k];
+        if ((c->sup[x][(size_t)k * c->dom[x] + a] & D[y]) == 0) return 0;
+      }
+    }
+  return 1;
+}
+
+/*
+ * O1: the RAC recurrence, Eq. 1, run literally.
+ *
+ *   D^(0)_~ac = ∅;  D^(k)_~ac = D^(k-1)_~ac ∪ {(x,a) | ∃ c_xy ∈ C_x: c_xy|(x,a) ⊆ D^(k-1)_~ac}
+ *
+ * in the complement form D_k = D_in \ D^(k)_~ac with the intersection test of
+ * line 59 (reading R1): (x,a) ∈ D_{k-1} is removed at step k iff some declared
+ * c_xy has c_xy|(x,a) ∩ D_{k-1}(y) = ∅.  Step k reads only D_{k-1} (R4): the
+ * result goes into a fresh array.  Loop control follows Alg. 1 tensorAC (lines
+ * 198-210): after each pass, wipeout is checked first (line 203, R5), then
+ * "nothing changed" ends the loop (line 200/206; Prop. 1 end condition,
+ * line 125).  iterations counts every pass executed (R3).
+ *
+ * removed_at (nullable, n*64 int32): removed_at[x*64+a] = k if (x,a) was
+ * removed at step k, 0 otherwise (the per-step sets V^(k) of Prop. 2).
+ * full != 0: do not stop at a wipeout; iterate to the fixpoint (the
+ * definitional D_ac, in which a wiped component is emptied).
+ * Returns ORC_OK or ORC_WIPEOUT.
+ */
+int orc_rac(const orc_csp *c, const uint64_t *d_in, uint64_t *d_out, int *iterations,
+            int32_t *removed_at, int full) {
+  int n = c->n;
+  uint64_t *prev = (uint64_t *)calloc((size_t)n, sizeof(uint64_t));
+  uint64_t *next = (uint64_t *)calloc((size_t)n, sizeof(uint64_t));
+  memcpy(prev, d_in, (size_t)n * sizeof(uint64_t));
+  if (removed_at) memset(removed_at, 0, (size_t)n * 64 * sizeof(int32_t));
+  int k = 0, status = ORC_OK;
+  for (;;) {
+    ++k;
+    /* one step of Eq. 1: every test reads prev (= D_{k-1}) only */
+    for (int x = 0; x < n; ++x) {
+      next[x] = prev[x];
+      for (int a = 0; a < c->dom[x]; ++a) {
+        if (!((prev[x] >> a) & 1ULL)) continue;
+        for (int kk = 0; kk < c->deg[x]; ++kk) {
+          int y = c->nbr[x][kk];
+          uint64_t s = c->sup[x][(size_t)kk * c->dom[x] + a]; /* c_xy|(x,a) */
+          if ((s & prev[y]) == 0) {                            /* ∩ D_{k-1}(y) = ∅ */
+            next[x] &= ~(1ULL << a);
+            if (removed_at) removed_at[x * 64 + a] = k;
+            break;
+          }
+        }
+      }
+    }
+    int wipe = 0, changed = 0;
+    for (int x = 0; x < n; ++x) {
+      if (next[x] == 0) wipe = 1;
+      if (next[x] != prev[x]) changed = 1;
+    }
+    memcpy(prev, next, (size_t)n * sizeof(uint64_t));
+    if (wipe && !full) { status = ORC_WIPEOUT; break; } /* Alg. 1 */
+    if (!changed) { status = wipe ? ORC_WIPEOUT : ORC_OK; break; }
+  }
+  memcpy(d_out, prev, (size_t)n * sizeof(uint64_t));
+  *iterations = k;
+  free(prev); free(next);
+  return status;
+}
+
+/*
+ * O2: AC-3 ("a propagation queue and a revision process";
+ * SPEC.md ac3_engine lines 283-299).  FIFO queue of directed arcs (x,y),
+ * initially every arc in ascending (x, y) order; revise(x,y) removes every
+ * a ∈ D(x) with c_xy|(x,a) ∩ D(y) = ∅; if D(x) shrank, enqueue (z,x) for every
+ * neighbour z ≠ y not already queued.  Plus an upfront empty-domain check
+ * (without it, an empty isolated domain would be reported consistent).
+ * Independent of O1 in algorithm, order and update discipline.
+ * *revisions counts dequeues.  Returns ORC_OK (d_out = D_ac) or ORC_WIPEOUT.
+ */
+int orc_ac3(const orc_csp *c, const uint64_t *d_in, uint64_t *d_out, int64_t *revisions) {
+  int n = c->n;
+  memcpy(d_out, d_in, (size_t)n * sizeof(uint64_t));
+  *revisions = 0;
+  for (int x = 0; x < n; ++x)
+    if (d_out[x] == 0) return ORC_WIPEOUT;
+  size_t n_arcs = 0;
+  size_t *off = (size_t *)malloc(((size_t)n + 1) * sizeof(size_t));
+  for (int x = 0; x < n; ++x) { off[x] = n_arcs; n_arcs += (size_t)c->deg[x]; }
+  off[n] = n_arcs;
+  size_t cap = n_arcs + 1;
+  int *qx = (int *)malloc(cap * sizeof(int));
+  int *qk = (int *)malloc(cap * sizeof(int));
+  char *inq = (char *)calloc(n_arcs + 1, 1);
+  size_t head = 0, count = 0;
+  for (int x = 0; x < n; ++x)
+    for (int k = 0; k < c->deg[x]; ++k) {
+      qx[(head + count) % cap] = x; qk[(head + count) % cap] = k; ++count;
+      inq[off[x] + (size_t)k] = 1;
+    }
+  int status = ORC_OK;
+  while (count) {
+    int x = qx[head], k = qk[head];
+    head = (head + 1) % cap; --count;
+    inq[off[x] + (size_t)k] = 0;
+    ++*revisions;
+    int y = c->nbr[x][k];
+    uint64_t before = d_out[x];
+    for (int a = 0; a < c->dom[x]; ++a) {
+      if (!((d_out[x] >> a) & 1ULL)) continue;
+      if ((c->sup[x][(size_t)k * c->dom[x] + a] & d_out[y]) == 0) d_out[x] &= ~(1ULL << a);
+    }
+    if (d_out[x] != before) {
+      if (d_out[x] == 0) { status = ORC_WIPEOUT; break; }
+      for (int j = 0; j < c->deg[x]; ++j) {
+        int z = c->nbr[x][j];
+        if (z == y) continue;
+        int kz = c->rev[x][j]; /* arc (z, x) */
+        if (!inq[off[z] + (size_t)kz]) {
+          inq[off[z] + (size_t)kz] = 1;
+          qx[(head + count) % cap] = z; qk[(head + count) % cap] = kz; ++count;
+        }
+      }
+    }
+  }
+  free(off); free(qx); free(qk); free(inq);
+  return status;
+}
+
+/*
+ * O4: certificate that d_out is exactly D_ac(d_in) (or, for a stop-mode
+ * wipeout, that every removal is sound).
+ *   (i)  [check_ac] d_out is arc consistent (definition, lines 49-61)
+ *        => d_out ⊆ D_ac (D_ac is the union of all AC subsets, lines 62-63);
+ *   (ii) every removed (x,a) with epoch t has a declared c_xy such that every
+ *        b ∈ c_xy|(x,a) ∩ d_in(y) was removed at an epoch < t.  By induction
+ *        on t with Lemma 1 (lines 79-82) every removed value is in D~ac
+ *        => d_in \ d_out ⊆ D~ac.
+ *   (i)+(ii) give d_out = D_ac.  Also checks d_out ⊆ d_in and that epochs are
+ *   set exactly on removed values.
+ * Returns 0 = accepted; 1 = not AC; 2 = d_out ⊄ d_in; 3 = bad epoch marks;
+ * 4 = a removal without a Lemma-1 justification.
+ */
+int orc_certify(const orc_csp *c, const uint64_t *d_in, const uint64_t *d_out,
+                const int32_t *removed_at, int check_ac) {
+  int n = c->n;
+  for (int x = 0; x < n; ++x)
+    if (d_out[x] & ~d_in[x]) return 2;
+  for (int x = 0; x < n; ++x)
+    for (int a = 0; a < 64; ++a) {
+      int in = (int)((d_in[x] >> a) & 1ULL), out = (int)((d_out[x] >> a) & 1ULL);
+      int32_t t = removed_at[x * 64 + a];
+      if (in && !out) { if (t < 1) return 3; }
+      else if (t != 0) return 3;
+    }
+  if (check_ac && !orc_is_ac(c, d_out)) return 1;
+  for (int x = 0; x < n; ++x)
+    for (int a = 0; a < c->dom[x]; ++a) {
+      if (!((d_in[x] >> a) & 1ULL) || ((d_out[x] >> a) & 1ULL)) continue;
+      int32_t t = removed_at[x * 64 + a];
+      int justified = 0;
+      for (int k = 0; k < c->deg[x] && !justified; ++k) {
+        int y = c->nbr[x][k];
+        uint64_t s = c->sup[x][(size_t)k * c->dom[x] + a] & d_in[y];
+        int all_earlier = 1;
+        for (int b = 0; b < 64; ++b) {
+          if (!((s >> b) & 1ULL)) continue;
+          int32_t tb = ((d_out[y] >> b) & 1ULL) ? 0 : removed_at[y * 64 + b];
+          if (tb < 1 || tb >= t) { all_earlier = 0; break; }
+        }
+        if (all_earlier) justified = 1;
+      }
+      if (!justified) return 4;
+    }
+  return 0;
+}
+
+/*
+ * One support test computed straight from the generator (no instance build):
+ * is (x,a) supported on every declared c_xy in C_x against D?  i.e. would
+ * (x,a) ∈ D survive one step of Eq. 1 from D.  Used for sampled parity at
+ * sizes where building the oracle's instance is too large (C4).
+ * Returns 1 supported, 0 removed.
+ */
+int orc_row_supported_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed,
+                            int x, int a, const uint64_t *D) {
+  for (int y = 0; y < n; ++y) {
+    if (y == x) continue;
+    int lo = x < y ? x : y, hi = x < y ? y : x;
+    if (!synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) continue;
+    uint64_t s = 0; /* c_xy|(x,a) */
+    if (x < y) {
+      s = synth_row(seed, (uint32_t)n, (uint32_t)d, (uint32_t)x, (uint32_t)y, (uint32_t)a, t_q16);
+    } else {
+      for (int b = 0; b < d; ++b)
+        if (synth_allowed(seed, (uint32_t)n, (uint32_t)d, (uint32_t)y, (uint32_t)x, (uint32_t)b, (uint32_t)a, t_q16))
+          s |= 1ULL << b;
+    }
+    if ((s & D[y]) == 0) return 0;
+  }
+  return 1;
+}
+
+/* Number of live values, summed (|D|). */
+int64_t orc_domain_size(const orc_csp *c, const uint64_t *D) {
+  int64_t s = 0;
+  for (int x = 0; x < c->n; ++x) s += popc64(D[x] & dom_mask(c->dom[x]));
+  return s;
+}

@@ -1,0 +1,374 @@
+"""Pins for the CPU oracle (oracle/): each check ties the oracle to something
+other than itself -- the paper's definitions, closed forms, hand traces,
+brute force, an independent algorithm (AC-3), or a textbook routine (BFS).
+
+Citations: PAPER.md line numbers (P:n), SPEC.md line numbers (S:n).
+"""
+from __future__ import annotations
+
+import collections
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import _instances as I
+
+U64 = np.uint64
+
+
+def epochs_to_trace(rem, n, iters):
+    trace = [set() for _ in range(iters)]
+    for x in range(n):
+        for a in range(64):
+            t = int(rem[x, a])
+            if t:
+                trace[t - 1].add((x, a))
+    return trace
+
+
+# ----------------------------------------------------------------------------- hand traces
+@pytest.mark.parametrize("name", I.golden_names())
+def test_golden_hand_traces(name):
+    """EQ2 / PATH3 / WIPE2 / SINGLE hand traces."""
+    doc, inst = I.load_golden(name)
+    exp = doc["expect"]
+    orc = oracle.Oracle.from_instance(inst)
+    d_in = np.asarray(doc["d_in"], dtype=U64)
+    st, d_out, it, rem = orc.rac(d_in)
+    assert st == (oracle.OK if exp["status"] == "OK" else oracle.WIPEOUT)
+    assert [int(v) for v in d_out] == exp["d_out"]
+    assert it == exp["iterations"]
+    trace = epochs_to_trace(rem, inst.n, it)
+    assert trace == [set(map(tuple, s)) for s in exp["trace"]]
+    # the pure-Python transcription agrees
+    st2, d2, it2, tr2 = oracle.rac_python(inst, d_in)
+    assert (st2, [int(v) for v in d2], it2) == (st, [int(v) for v in d_out], it)
+    assert tr2 == trace
+    # AC-3 reaches the same verdict (and D when consistent)
+    st3, d3, _ = orc.ac3(d_in)
+    assert st3 == st
+    if st == oracle.OK:
+        assert np.array_equal(d3, d_out)
+
+
+# ----------------------------------------------------------------------------- brute force
+def test_bruteforce_union_of_ac_subsets():
+    """O3 (union of all AC subsets) == O1 full mode on 300 tiny instances.
+    Inputs: W-root and W-rand domain states."""
+    for k, inst in enumerate(I.tiny_corpus(300)):
+        orc = oracle.Oracle.from_instance(inst)
+        for d_in in (inst.full_domains(), synth.w_rand(inst.dom, 0.8, seed=k)):
+            bf = oracle.brute_force_dac(inst, d_in)
+            st, d_out, it, rem = orc.rac(d_in, full=True)
+            assert np.array_equal(bf, d_out), (k, inst.to_json())
+            assert (st == oracle.WIPEOUT) == bool(np.any(bf == 0))
+
+
+def test_bruteforce_is_ac_definition():
+    """The brute-force AC predicate and the C audit agree on every subset of tiny instances."""
+    for k, inst in enumerate(I.tiny_corpus(40, seed0=3)):
+        if int(inst.dom.sum()) > 10:
+            continue
+        orc = oracle.Oracle.from_instance(inst)
+        sup = oracle._support_sets(inst)
+        elems = sorted(oracle._to_set(inst.full_domains()))
+        for mask in range(1 << len(elems)):
+            S = {elems[i] for i in range(len(elems)) if (mask >> i) & 1}
+            assert oracle._is_ac_set(sup, S) == orc.is_ac(oracle._from_set(S, inst.n))
+
+
+# ----------------------------------------------------------------------------- AC-3 agreement
+def test_rac_agrees_with_ac3_corpus():
+    """S:528 corpus (>=1000 instances, n 2..20, d 1..6): O1 ≡ O2 on verdict, and on D when
+    consistent; O1 full mode has an empty row iff stop mode reports WIPEOUT; stop and full
+    modes coincide when no wipeout happens."""
+    corpus = I.random_corpus(1000)
+    n_wipe = 0
+    for k, inst in enumerate(corpus):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = inst.full_domains() if k % 2 == 0 else synth.w_rand(inst.dom, 0.9, seed=k)
+        st, d_out, it, _ = orc.rac(d_in)
+        st3, d3, _ = orc.ac3(d_in)
+        stf, dfull, itf, _ = orc.rac(d_in, full=True)
+        assert st == st3, k
+        assert (st == oracle.WIPEOUT) == bool(np.any(dfull == 0)), k
+        if st == oracle.OK:
+            assert np.array_equal(d_out, d3), k
+            assert np.array_equal(d_out, dfull) and it == itf, k
+        n_wipe += st == oracle.WIPEOUT
+    assert 50 < n_wipe < 950  # the corpus exercises both outcomes
+
+
+def test_c_and_python_transcriptions_agree():
+    """Two transcriptions of Eq. 1 (C over bitsets, Python over sets) give the same
+    trajectory (per-step removal sets) on 300 random instances, stop and full modes."""
+    for k, inst in enumerate(I.random_corpus(300, seed0=5, n_range=(2, 9), d_range=(1, 5))):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = synth.w_rand(inst.dom, 0.85, seed=k)
+        for full in (False, True):
+            st, d_out, it, rem = orc.rac(d_in, full=full)
+            st2, d2, it2, tr2 = oracle.rac_python(inst, d_in, full=full)
+            assert (st, it) == (st2, it2)
+            assert np.array_equal(d_out, d2)
+            assert epochs_to_trace(rem, inst.n, it) == tr2
+
+
+# ----------------------------------------------------------------------------- certificate
+def test_certificate_accepts_and_rejects():
+    """O4 accepts every correct full-mode result; rejects over-pruned results (a kept value
+    marked removed) and under-pruned ones (a removed value put back)."""
+    rng = np.random.default_rng(11)
+    rejected_over = rejected_under = 0
+    for k, inst in enumerate(I.random_corpus(300, seed0=9)):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = inst.full_domains()
+        st, d_out, it, rem = orc.rac(d_in, full=True)
+        assert orc.certify(d_in, d_out, rem) == 0
+        kept = [(x, a) for x in range(inst.n) for a in range(64) if (int(d_out[x]) >> a) & 1]
+        if kept:
+            x, a = kept[int(rng.integers(len(kept)))]
+            bad = d_out.copy()
+            bad[x] &= ~(U64(1) << U64(a))
+            brem = rem.copy()
+            brem[x, a] = int(rng.integers(1, it + 2))
+            assert orc.certify(d_in, bad, brem) != 0
+            rejected_over += 1
+        removed = [(x, a) for x in range(inst.n) for a in range(64) if rem[x, a]]
+        if removed:
+            x, a = removed[int(rng.integers(len(removed)))]
+            bad = d_out.copy()
+            bad[x] |= U64(1) << U64(a)
+            brem = rem.copy()
+            brem[x, a] = 0
+            assert orc.certify(d_in, bad, brem) != 0
+            rejected_under += 1
+    assert rejected_over > 100 and rejected_under > 100
+
+
+def test_certificate_on_stop_mode_wipeouts():
+    """Stop-mode WIPEOUT results: every removal is sound (Lemma 1 part only)."""
+    seen = 0
+    for k, inst in enumerate(I.random_corpus(400, seed0=13)):
+        orc = oracle.Oracle.from_instance(inst)
+        st, d_out, it, rem = orc.rac(inst.full_domains())
+        if st == oracle.WIPEOUT:
+            assert orc.certify(inst.full_domains(), d_out, rem, check_ac=False) == 0
+            seen += 1
+    assert seen > 20
+
+
+# ----------------------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("n,d", [(1, 1), (5, 3), (17, 8), (40, 64)])
+def test_tightness_zero_is_identity(n, d):
+    """Tightness 0: every relation is universal, nothing is removed, 1 pass."""
+    inst = synth.random_csp(n, d, 1.0, 0.0, seed=3)
+    st, d_out, it, _ = oracle.Oracle.from_instance(inst).rac(inst.full_domains())
+    assert st == oracle.OK and it == 1 and np.array_equal(d_out, inst.full_domains())
+
+
+@pytest.mark.parametrize("n,d", [(2, 1), (3, 5), (4, 64), (9, 2)])
+def test_empty_relation_wipes_in_one_pass(n, d):
+    """An empty relation on a pair wipes both variables in pass 1 (WIPE2)."""
+    cons = [(0, 1, [])] + [(i, i + 1, I.eq_rel(d)) for i in range(1, n - 1)]
+    inst = synth.from_constraints(n, d, cons)
+    st, d_out, it, _ = oracle.Oracle.from_instance(inst).rac(inst.full_domains())
+    assert st == oracle.WIPEOUT and it == 1 and d_out[0] == 0 and d_out[1] == 0
+
+
+@pytest.mark.parametrize("n,d,embed", [(2, 2, False), (7, 3, False), (30, 8, False), (12, 5, True), (25, 32, True)])
+def test_equality_chain_takes_exactly_n_passes(n, d, embed):
+    """Equality chain x_i = x_{i+1}, x_0 = {0}: step k of Eq. 1 removes the nonzero values
+    of x_k only (its sole support chain runs through x_{k-1}), so D_ac = all {0}, reached
+    after n-1 removing steps plus the final quiescent one: exactly n iterations."""
+    inst = I.equality_chain(n, d, embed_complete=embed)
+    d_in = inst.full_domains()
+    d_in[0] = U64(1)
+    st, d_out, it, rem = oracle.Oracle.from_instance(inst).rac(d_in)
+    assert st == oracle.OK and it == n
+    assert np.all(d_out == U64(1))
+    for k in range(1, n):
+        assert all(int(rem[k, a]) == k for a in range(1, d))
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8, 11, 20])
+def test_two_ended_path(n):
+    """x_0 = {0}, x_{n-1} = {1}, equality chain, d = 2: the left wave removes value 1 from
+    x_k at step k, the right wave removes 0 from x_{n-1-k} at step k; they collide at step
+    floor(n/2) -> stop mode WIPEOUT there.  Full mode keeps propagating: every domain
+    ends empty and the n-th pass is the first quiescent one."""
+    inst = I.equality_chain(n, 2)
+    d_in = inst.full_domains()
+    d_in[0] = U64(1)
+    d_in[n - 1] = U64(2)
+    orc = oracle.Oracle.from_instance(inst)
+    st, d_out, it, _ = orc.rac(d_in)
+    assert st == oracle.WIPEOUT and it == n // 2
+    stf, dfull, itf, _ = orc.rac(d_in, full=True)
+    assert stf == oracle.WIPEOUT and itf == n and np.all(dfull == 0)
+
+
+def test_d1_full_mode_is_multisource_bfs():
+    """d = 1: a constraint either allows (0,0) or forbids it.  Endpoints of forbidden
+    constraints lose their only value at step 1; a variable adjacent (by any declared
+    constraint) to a removed one loses its only support one step later.  So the removal
+    epoch of x is 1 + BFS distance from the forbidden endpoints in the constraint graph,
+    and iterations = max depth + 2 (or 1 if nothing is forbidden)."""
+    rng = np.random.default_rng(21)
+    for k in range(300):
+        n = int(rng.integers(1, 30))
+        p = float(rng.uniform(0.05, 0.5))
+        t = float(rng.uniform(0.0, 0.15))
+        inst = synth.random_csp(n, 1, p, t, seed=1000 + k)
+        adj = collections.defaultdict(list)
+        sources = set()
+        for j in range(inst.n_rel):
+            x, y = int(inst.xs[j]), int(inst.ys[j])
+            adj[x].append(y)
+            adj[y].append(x)
+            if int(inst.rows[j, 0]) == 0:
+                sources |= {x, y}
+        dist = {s: 0 for s in sources}
+        q = collections.deque(sources)
+        while q:
+            u = q.popleft()
+            for v in adj[u]:
+                if v not in dist:
+                    dist[v] = dist[u] + 1
+                    q.append(v)
+        st, d_out, it, rem = oracle.Oracle.from_instance(inst).rac(inst.full_domains(), full=True)
+        for x in range(n):
+            if x in dist:
+                assert d_out[x] == 0 and rem[x, 0] == dist[x] + 1
+            else:
+                assert d_out[x] == 1 and rem[x, 0] == 0
+        assert it == (max(dist.values()) + 2 if dist else 1)
+
+
+def test_empty_input_row():
+    """Reading R7: an empty row in D_in -> one pass (only neighbours of the empty
+    variable can lose values), then WIPEOUT with iterations = 1 (Alg. 1)."""
+    inst = synth.from_constraints(4, 2, [(0, 1, [(0, 0), (1, 1)]), (2, 3, [(0, 0), (1, 1)])])
+    d_in = inst.full_domains()
+    d_in[0] = U64(0)
+    st, d_out, it, _ = oracle.Oracle.from_instance(inst).rac(d_in)
+    assert st == oracle.WIPEOUT and it == 1
+    assert [int(v) for v in d_out] == [0, 0, 3, 3]
+    # AC-3's upfront check gives the same verdict
+    assert oracle.Oracle.from_instance(inst).ac3(d_in)[0] == oracle.WIPEOUT
+
+
+# ----------------------------------------------------------------------------- invariants
+def _solutions(inst):
+    doms = [range(int(k)) for k in inst.dom]
+    sols = []
+    for assn in itertools.product(*doms):
+        ok = all((int(inst.rows[j, assn[inst.xs[j]]]) >> assn[inst.ys[j]]) & 1 for j in range(inst.n_rel))
+        if ok:
+            sols.append(assn)
+    return sols
+
+
+def test_invariants_corpus():
+    """Prop. 1/2 and SPEC invariants on 400 random instances:
+    result AC; idempotent (re-enforce -> 1 pass, unchanged); subset of input; iterations
+    <= |D_in| + 1; Prop. 2 cause check; solutions preserved; equivariant under
+    relabelling variables."""
+    rng = np.random.default_rng(17)
+    for k, inst in enumerate(I.random_corpus(400, seed0=19, n_range=(2, 12), d_range=(1, 5))):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = synth.w_rand(inst.dom, 0.9, seed=k)
+        st, d_out, it, rem = orc.rac(d_in, full=True)
+        assert np.all((d_out & ~d_in) == 0)
+        assert orc.is_ac(d_out)
+        assert it <= sum(synth.popcount64(v) for v in d_in) + 1
+        st2, d2, it2, _ = orc.rac(d_out, full=True)
+        assert it2 == 1 and np.array_equal(d2, d_out)
+        # Prop. 2 (2): every value removed at step k >= 2 has a c_xy whose supports
+        # outside D~(k-2) all lie in V^(k-1).
+        for x in range(inst.n):
+            for a in range(64):
+                t = int(rem[x, a])
+                if t < 2:
+                    continue
+                ok = False
+                for y in range(inst.n):
+                    pres, s = orc.support(x, y, a)
+                    if not pres:
+                        continue
+                    rest = [b for b in range(64) if (s >> b) & 1 and (int(d_in[y]) >> b) & 1
+                            and not (1 <= rem[y, b] <= t - 2)]
+                    if all(rem[y, b] == t - 1 for b in rest):
+                        ok = True
+                        break
+                assert ok, (k, x, a)
+        # solutions preserved (tiny only)
+        if np.prod(inst.dom.astype(np.float64)) <= 2e4:
+            for s in _solutions(inst):
+                if all((int(d_in[x]) >> s[x]) & 1 for x in range(inst.n)):
+                    assert all((int(d_out[x]) >> s[x]) & 1 for x in range(inst.n))
+        # equivariance under a variable permutation
+        perm = rng.permutation(inst.n)
+        inv = np.argsort(perm)
+        cons = [(int(perm[inst.xs[j]]), int(perm[inst.ys[j]]),
+                 [(a, b) for a in range(int(inst.dom[inst.xs[j]])) for b in range(int(inst.dom[inst.ys[j]]))
+                  if (int(inst.rows[j, a]) >> b) & 1]) for j in range(inst.n_rel)]
+        pinst = synth.from_constraints(inst.n, inst.dom[inv], cons)
+        pst, pd, pit, _ = oracle.Oracle.from_instance(pinst).rac(d_in[inv], full=True)
+        assert pst == st and pit == it and np.array_equal(pd, d_out[inv])
+
+
+def test_monotone():
+    """D_in ⊆ D_in' => D_ac(D_in) ⊆ D_ac(D_in') (D_ac is the largest AC subset)."""
+    for k, inst in enumerate(I.random_corpus(200, seed0=23, n_range=(2, 12))):
+        orc = oracle.Oracle.from_instance(inst)
+        big = synth.w_rand(inst.dom, 0.95, seed=k)
+        small = big & synth.w_rand(inst.dom, 0.8, seed=k + 7)
+        _, ds, _, _ = orc.rac(small, full=True)
+        _, db, _, _ = orc.rac(big, full=True)
+        assert np.all((ds & ~db) == 0)
+
+
+# ----------------------------------------------------------------------------- generator
+@pytest.mark.parametrize("n,d,p,t,seed", [(7, 5, 0.6, 0.3, 1), (20, 8, 0.5, 0.4, 2), (13, 64, 1.0, 0.5, 3),
+                                          (31, 17, 0.3, 0.7, 4), (9, 1, 1.0, 0.2, 5)])
+def test_generator_numpy_matches_c_header(n, d, p, t, seed):
+    """synth/__init__.py (numpy) and synth/csp_synth.h (used by orc_build_synth) produce the
+    same instance: compare every support set of both orientations."""
+    inst = synth.random_csp(n, d, p, t, seed)
+    a = oracle.Oracle.from_instance(inst)
+    b = oracle.Oracle.from_synth(n, d, synth.quant_density(p), synth.quant_tightness(t), seed)
+    for x in range(n):
+        assert a.degree(x) == b.degree(x)
+        for y in range(n):
+            for v in range(d):
+                assert a.support(x, y, v) == b.support(x, y, v)
+
+
+def test_row_supported_synth_matches_one_step():
+    """The on-the-fly row test equals membership in one step of O1 from D."""
+    n, d, p, t, seed = 30, 12, 0.7, 0.55, 9
+    inst = synth.random_csp(n, d, p, t, seed)
+    orc = oracle.Oracle.from_instance(inst)
+    D = synth.w_rand(inst.dom, 0.8, seed=4)
+    st, d1, it, rem = orc.rac(D)
+    for x in range(n):
+        for a in range(d):
+            if not (int(D[x]) >> a) & 1:
+                continue
+            sup = oracle.row_supported_synth(n, d, synth.quant_density(p), synth.quant_tightness(t), seed, x, a, D)
+            assert sup == (rem[x, a] != 1)
+
+
+def test_generator_statistics():
+    """Constraint count ≈ density·n(n-1)/2 and allowed fraction ≈ 1 - tightness."""
+    inst = synth.random_csp(200, 16, 0.3, 0.25, seed=77)
+    m = inst.n_rel
+    exp = 0.3 * 200 * 199 / 2
+    assert abs(m - exp) < 4 * np.sqrt(exp * 0.7)
+    bits = sum(bin(int(v)).count("1") for v in inst.rows.reshape(-1))
+    cells = m * 16 * 16
+    assert abs(bits / cells - 0.75) < 0.01
+    assert synth.random_csp(3, 4, 1.0, 0.5, seed=1).n_rel == 3
