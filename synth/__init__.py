@@ -31,6 +31,7 @@ TAG_PRES = 0x50524553454E4345
 TAG_CELL = 0x43454C4C42495453
 TAG_KEEP = 0x4B454550424954
 TAG_PICK = 0x5049434B43484F49
+GAMMA = 0x9E3779B97F4A7C15
 
 
 # ----------------------------------------------------------------------------- hashing
@@ -181,12 +182,11 @@ def relation_rows(n: int, d: int, xs, ys, t_q16: int, seed: int) -> np.ndarray:
     kc = U64(key(seed, TAG_CELL))
     rows = np.zeros((xs.shape[0], d), dtype=U64)
     with np.errstate(over="ignore"):
-        base = (xs * U64(n) + ys) * U64(d)
+        pk = mix64(kc ^ mix64(xs * U64(n) + ys))
         for a in range(d):
             acc = np.zeros(xs.shape[0], dtype=U64)
             for bq in range(q):
-                idx = (base + U64(a)) * U64(q) + U64(bq)
-                h = mix64(kc ^ mix64(idx))
+                h = mix64(pk + U64(a * q + bq + 1) * U64(GAMMA))
                 for j in range(4):
                     b = bq * 4 + j
                     if b >= d:

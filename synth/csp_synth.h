@@ -26,8 +26,8 @@
  *   key(seed, tag) = mix64(seed ^ tag)
  *   present(x<y)   = (mix64(key(seed,TAG_PRES) ^ mix64(x*n + y)) >> 32) < dens_q32
  *                    dens_q32 = round(density * 2^32) in [0, 2^32]
- *   allowed(x<y,a,b): q = ceil(d/4); idx = ((x*n + y)*d + a)*q + b/4
- *                    h = mix64(key(seed,TAG_CELL) ^ mix64(idx))
+ *   allowed(x<y,a,b): q = ceil(d/4); pk = mix64(key(seed,TAG_CELL) ^ mix64(x*n + y))
+ *                    h = mix64(pk + (a*q + b/4 + 1) * GAMMA)   (a splitmix64 stream per pair)
  *                    allowed iff ((h >> 16*(b%4)) & 0xFFFF) >= t_q16
  *                    t_q16 = round(tightness * 65536) in [0, 65536]
  *   rel(c_yx) for x<y is the transpose: (b,a) allowed in c_yx iff (a,b) in c_xy.
@@ -49,6 +49,7 @@
 #define SYNTH_TAG_CELL 0x43454C4C42495453ULL /* "CELLBITS" */
 #define SYNTH_TAG_KEEP 0x4B454550424954ULL   /* "KEEPBIT"  */
 #define SYNTH_TAG_PICK 0x5049434B43484F49ULL /* "PICKCHOI" */
+#define SYNTH_GAMMA 0x9E3779B97F4A7C15ULL
 
 SYNTH_FN uint64_t synth_mix64(uint64_t z) {
   z ^= z >> 30;
@@ -67,12 +68,20 @@ SYNTH_FN int synth_present(uint64_t seed, uint32_t n, uint32_t x, uint32_t y, ui
   return (h >> 32) < dens_q32;
 }
 
-/* The 64-bit hash word holding cells (a, 4*(b/4) .. 4*(b/4)+3) of c_xy, x < y. */
+/* Per-pair stream key of c_xy, x < y. */
+SYNTH_FN uint64_t synth_pair_key(uint64_t seed, uint32_t n, uint32_t x, uint32_t y) {
+  return synth_mix64(synth_key(seed, SYNTH_TAG_CELL) ^ synth_mix64((uint64_t)x * n + y));
+}
+
+/* The 64-bit word holding cells (a, 4*bq .. 4*bq+3) of the pair with stream key pk. */
+SYNTH_FN uint64_t synth_cell_word_pk(uint64_t pk, uint32_t d, uint32_t a, uint32_t bq) {
+  uint64_t q = (d + 3u) / 4u;
+  return synth_mix64(pk + ((uint64_t)a * q + bq + 1u) * SYNTH_GAMMA);
+}
+
 SYNTH_FN uint64_t synth_cell_word(uint64_t seed, uint32_t n, uint32_t d, uint32_t x, uint32_t y,
                                   uint32_t a, uint32_t bq) {
-  uint64_t q = (d + 3u) / 4u;
-  uint64_t idx = (((uint64_t)x * n + y) * d + a) * q + bq;
-  return synth_mix64(synth_key(seed, SYNTH_TAG_CELL) ^ synth_mix64(idx));
+  return synth_cell_word_pk(synth_pair_key(seed, n, x, y), d, a, bq);
 }
 
 /* Is (a,b) allowed in rel(c_xy), x < y?  t_q16 in [0, 65536]. */
@@ -87,8 +96,9 @@ SYNTH_FN int synth_allowed(uint64_t seed, uint32_t n, uint32_t d, uint32_t x, ui
 SYNTH_FN uint64_t synth_row(uint64_t seed, uint32_t n, uint32_t d, uint32_t x, uint32_t y,
                             uint32_t a, uint32_t t_q16) {
   uint64_t row = 0;
+  uint64_t pk = synth_pair_key(seed, n, x, y);
   for (uint32_t bq = 0; bq * 4u < d; ++bq) {
-    uint64_t h = synth_cell_word(seed, n, d, x, y, a, bq);
+    uint64_t h = synth_cell_word_pk(pk, d, a, bq);
     for (uint32_t j = 0; j < 4u && bq * 4u + j < d; ++j) {
       uint32_t v = (uint32_t)((h >> (16u * j)) & 0xFFFFu);
       if (v >= t_q16) row |= 1ULL << (bq * 4u + j);
