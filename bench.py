@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""bench.py -- RAC enforcement throughput on B200 (BASELINE.json metric:
+"AC enforcements/sec and relation-tensor GB/s/iter vs HBM peak at 1/2/4/8 B200").
+
+One step = one full enforcement D_in -> D_ac (every §8(a) row: D staged in
+smem, support test over the packed relation masks, AND over C_x, device-side
+loop control to the fixpoint; with N > 1 the per-pass all-gather over NCCL).
+The instance is packed once before timing (rac_create is not per step).
+
+Default workload (configs[2], C3): random binary CSP n=2000, d=32, density
+1.0, tightness 0.5, root enforcement (W-stream: one pass reads every byte of
+the 512 MB mask tensor; inputs larger than the 126 MB L2, so no flush).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3-stream|c3-prop|c2-root|c1-seed|c4-stream|c5-batch]
+  python bench.py --impl reference ...   # the CPU oracle on the same workload
+
+Prints ONE JSON line (rank 0).  Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (input generation only)
+
+METRIC = "AC enforcements/sec"
+UNIT = "enforcements/s"
+FALLBACK_HBM = 6650.0
+
+WORKLOADS = {
+    # name: (n, d, density, tightness, seed, D_in kind, description)
+    "c3-stream": (2000, 32, 1.0, 0.5, 1, "root",
+                  "C3 W-stream: random binary CSP n=2000, d=32, density 1.0, tightness 0.5; root enforcement "
+                  "(full domains; 1 pass over all 512 MB of masks)"),
+    "c3-prop": (2000, 32, 1.0, 0.70, 1, "root",
+                "C3 W-prop: n=2000, d=32, density 1.0, tightness 0.70; root enforcement (~10 passes, consistent)"),
+    "c2-root": (500, 20, 1.0, 0.3, 1, "root",
+                "C2: n=500, d=20, complete graph, tightness 0.3; root enforcement (20 MB, L2-resident)"),
+    "c1-seed": (20, 8, 0.5, 0.4, 1, "seed",
+                "C1 W-seed: n=20, d=8, density 0.5, tightness 0.4; D_ac(root) with one seeded assignment"),
+    "c4-stream": (8000, 64, 1.0, 0.5, 1, "root",
+                  "C4 W-stream: n=8000, d=64, density 1.0, tightness 0.5; root enforcement (32.8 GB of masks)"),
+    "c5-batch": (200, 16, 0.8, 0.3, 1, "dive",
+                 "C5: 1024 W-dive states (search-tree nodes) on n=200, d=16, density 0.8, tightness 0.3; "
+                 "one batched enforcement per step"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(n, d, density_present_deg, live_per_pass):
+    """Σ_t Σ_x |D_{t-1}(x)| · Σ_{y∈C_x} d_y / 8; uniform d."""
+    return sum(live * deg * d for live, deg in zip(live_per_pass, density_present_deg)) / 8.0
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        self.t0 = time.time()
+
+    def stop(self):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+        self.f.flush()
+        rows = []
+        try:
+            with open(self.f.name) as fh:
+                for line in fh:
+                    parts = [s.strip() for s in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        finally:
+            os.unlink(self.f.name)
+        return rows
+
+    @staticmethod
+    def summarize(rows):
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_11388_b200 import rac
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n, d, dens, tight, seed, kind, desc = WORKLOADS[args.workload]
+    dq, tq = synth.quant_density(dens), synth.quant_tightness(tight)
+    uid = None
+    if world > 1:
+        obj = [rac.rac_get_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    t0 = time.time()
+    ctx = rac.RacContext.create_random(n, d, dq, tq, seed, device=local_rank, rank=rank, world=world,
+                                       nccl_unique_id=uid)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    full = synth.full_domains(np.full(n, d))
+    stream = torch.cuda.current_stream()
+
+    # --- D_in
+    if kind == "seed":
+        st, root, _ = ctx.enforce(full)
+        d_in, _, _ = synth.w_seed(root, seed)
+    else:
+        d_in = full
+    S = args.states if kind == "dive" else 1
+    if kind == "dive":
+        st, root, _ = ctx.enforce(full)
+        states = synth.dive_states(root, lambda D: ctx.enforce(D)[:2], S, seed=seed)
+        din_h = np.stack(states)
+    else:
+        din_h = d_in[None, :]
+
+    # --- instrumentation run (outside the timed region): iterations, status, live rows per pass
+    if kind == "dive":
+        res = [ctx.enforce(din_h[s]) for s in range(S)]
+        iters_list = [r[2] for r in res]
+        instr = {"iterations_mean": float(np.mean(iters_list)), "iterations_max": int(np.max(iters_list)),
+                 "wipeout_frac": float(np.mean([r[0] == 1 for r in res]))}
+        alg_bytes = None
+    else:
+        stt, dout, it, rem = (ctx.enforce(din_h[0], removed_at=True) if world == 1 else
+                              (*ctx.enforce(din_h[0]), None))
+        instr = {"iterations": it, "status": "OK" if stt == 0 else "WIPEOUT"}
+        if rem is not None:
+            live0 = np.array([[(int(din_h[0][x]) >> a) & 1 for a in range(d)] for x in range(n)], dtype=bool)
+            remd = rem[:, :d]
+            live_per_pass = [int(np.sum(live0 & ((remd == 0) | (remd >= t)))) for t in range(1, it + 1)]
+        else:
+            live_per_pass = [int(sum(bin(int(v)).count("1") for v in din_h[0]))] + [0] * (it - 1)
+        # complete graph at density 1: deg = n-1; otherwise count present pairs in the generator
+        deg = n - 1 if dens >= 1.0 else None
+        if deg is None:
+            xs, ys = synth.present_pairs(n, dq, seed)
+            degs = np.bincount(np.concatenate([xs, ys]), minlength=n)
+            mean_deg = float(degs.mean())
+        else:
+            mean_deg = float(deg)
+        alg_bytes = sum(l * mean_deg * d for l in live_per_pass) / 8.0
+        instr["live_rows_per_pass"] = live_per_pass
+
+    # --- device buffers
+    din = torch.from_numpy(din_h.view(np.int64).copy()).to(dev)
+    dout = torch.zeros_like(din)
+    its = torch.zeros(S, dtype=torch.int32, device=dev)
+    sts = torch.zeros(S, dtype=torch.int32, device=dev)
+
+    def step():
+        if kind == "dive":
+            ctx.enforce_batch(S, din, dout, its, sts, stream=stream)
+        else:
+            ctx.enforce_async(din, dout, its, sts, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = ctx.last_launch_count
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for k in range(args.steps):
+        step()
+        evs[k + 1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_step = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    # clocks: keep the sampler running for at least ~1.5 s of the same step loop
+    soak = 0
+    while time.time() - clocks.t0 < 1.5:
+        step()
+        soak += 1
+        if soak % 64 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    crow = clocks.stop()
+    clk = ClockSampler.summarize(crow)
+    clk["window"] = "timed region" + (" + %d extra steps of the same loop (>=1.5 s sampling window)" % soak if soak
+                                      else "")
+
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # --- e2e: the public host-buffer call, H2D + D2H inside the timed region
+    e2e = None
+    if kind != "dive":
+        for _ in range(3):
+            ctx.enforce(din_h[0])
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        reps = max(10, min(args.steps, 2000))
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        e0.record(stream)
+        for _ in range(reps):
+            ctx.enforce(din_h[0])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall_ms = (time.perf_counter() - t_wall) * 1e3
+        if world > 1:
+            t = torch.tensor([wall_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall_ms = float(t.item())
+        e2e = {"value": reps / (wall_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": n * 8,
+               "d2h_bytes_per_step": n * 8 + 8,
+               "how": "rac_enforce (host buffers; pinned staging, H2D + enforcement + D2H + sync per call), "
+                      "host wall clock over %d calls, max over ranks" % reps}
+    else:
+        # batched: host states -> device -> batch enforcement -> results back, per step
+        h_in = torch.from_numpy(din_h.view(np.int64).copy()).pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        h_st = torch.empty(S, dtype=torch.int32).pin_memory()
+        reps = max(5, min(args.steps, 200))
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter()
+        for _ in range(reps):
+            din.copy_(h_in, non_blocking=True)
+            step()
+            h_out.copy_(dout, non_blocking=True)
+            h_st.copy_(sts, non_blocking=True)
+            torch.cuda.synchronize()
+        wall_ms = (time.perf_counter() - t_wall) * 1e3
+        e2e = {"value": reps * S / (wall_ms / 1e3), "unit": "states/s", "h2d_bytes_per_step": S * n * 8,
+               "d2h_bytes_per_step": S * n * 8 + S * 4,
+               "how": "pinned host states -> device, rac_enforce_batch, D_out + status -> pinned host, sync"}
+
+    ms_per_step = total_ms / args.steps
+    if kind == "dive":
+        value = S * args.steps / (total_ms / 1e3)
+        unit = "states/s"
+        metric = "AC enforcements/sec (batched search-tree states)"
+    else:
+        value = args.steps / (total_ms / 1e3)
+        unit = UNIT
+        metric = METRIC
+
+    peak, peak_src = measured_peaks()
+    roofline = None
+    if alg_bytes is not None:
+        kern_ms = statistics.median(per_step)
+        achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(args.workload, {}).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "kernel": "rac_fused" if world == 1 else "rac_pass (+ allgather)",
+                    "algorithmic_bytes_per_launch": alg_bytes,
+                    "launch_ms_median": round(kern_ms, 5),
+                    "peak_source": peak_src + ("" if world == 1 else "; per-GPU bytes = total / N")}
+        if world > 1:
+            roofline["achieved"] = round(achieved / world, 1)
+            roofline["frac"] = round(achieved / world / peak, 4)
+    cfg = {"workload": args.workload + ": " + desc, "n": n, "d": d, "density": dens, "tightness": tight,
+           "t_q16": tq, "seed": seed, "states": S if kind == "dive" else 1,
+           "l2": "inputs larger than L2 (no flush)" if n * n * d * d / 8 > 200e6 else
+                 "relation L2-resident (warm; stated, not flushed)",
+           "parallelism": ("row-sharded x%d (NCCL all-gather of D per pass)" % world) if world > 1 else "1 GPU",
+           "instance_generation_s": round(gen_s, 3)}
+    out = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+           "dtype": {1: "u8", 2: "u16", 4: "u32", 8: "u64"}[ctx.mask_bytes] + " bitmasks",
+           "data": "synthetic (seeded counter-based random CSP, synth/csp_synth.h)", "config": cfg,
+           "gpu_launches": int(launches_per_step * args.steps), "clocks": clk, "e2e": e2e,
+           "enforcement": instr, "roofline": roofline}
+    if roofline:
+        out["relation_gbs_per_iter"] = roofline["achieved"] * (world if world > 1 else 1)
+    return out, (n, d, dq, tq, seed, kind, din_h)
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_baseline(n, d, dq, tq, seed, kind, din_h, budget_s=20.0):
+    """The oracle as it stands (single-threaded C, oracle/oracle.c) on a bounded
+    sample of the same workload, on this host."""
+    import oracle
+    t0 = time.time()
+    orc = oracle.Oracle.from_synth(n, d, dq, tq, seed) if kind != "dive" else None
+    if kind == "dive":
+        inst = synth.random_csp(n, d, 0.8, 0.3, seed)
+        orc = oracle.Oracle.from_instance(inst)
+    build_s = time.time() - t0
+    done = 0
+    t1 = time.perf_counter()
+    while True:
+        orc.rac(din_h[done % din_h.shape[0]], with_epochs=False)
+        done += 1
+        el = time.perf_counter() - t1
+        if el > budget_s or done >= max(1, din_h.shape[0]) * 64:
+            break
+    return {"value": done / el, "unit": "states/s" if kind == "dive" else UNIT, "cores": 1, "kind": "oracle",
+            "sample": "%d enforcement(s) of the same D_in%s by orc_rac (O1, 1 thread, gcc -O2) in %.1f s; "
+                      "oracle instance build %.1f s excluded" % (done, " states" if kind == "dive" else "", el,
+                                                                    build_s)}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the same workload (the base contract's
+    reference arm for this tier)."""
+    n, d, dens, tight, seed, kind, desc = WORKLOADS[args.workload]
+    dq, tq = synth.quant_density(dens), synth.quant_tightness(tight)
+    import oracle
+    if kind == "dive":
+        inst = synth.random_csp(n, d, dens, tight, seed)
+        orc = oracle.Oracle.from_instance(inst)
+        _, root, _, _ = orc.rac(inst.full_domains(), with_epochs=False)
+        din_h = np.stack(synth.dive_states(root, lambda D: orc.rac(D, with_epochs=False)[:2], args.states, seed))
+    else:
+        orc = oracle.Oracle.from_synth(n, d, dq, tq, seed)
+        full = synth.full_domains(np.full(n, d))
+        if kind == "seed":
+            _, root, _, _ = orc.rac(full, with_epochs=False)
+            d_in, _, _ = synth.w_seed(root, seed)
+        else:
+            d_in = full
+        din_h = d_in[None, :]
+    # bounded sample: each step = one enforcement (or one state); cap total time
+    t0 = time.perf_counter()
+    orc.rac(din_h[0], with_epochs=False)
+    one = time.perf_counter() - t0
+    budget = 150.0
+    steps = args.steps
+    if one * (args.steps + args.warmup) > budget:
+        steps = max(3, int(budget / max(one, 1e-9)) - args.warmup)
+    for k in range(min(args.warmup, 3)):
+        orc.rac(din_h[k % din_h.shape[0]], with_epochs=False)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        orc.rac(din_h[k % din_h.shape[0]], with_epochs=False)
+    el = time.perf_counter() - t0
+    unit = "states/s" if kind == "dive" else UNIT
+    val = steps / el
+    sample = ("%d of %d requested steps, each one full enforcement by orc_rac (O1, 1 thread)" % (steps, args.steps))
+    return {"metric": METRIC if kind != "dive" else "AC enforcements/sec (batched search-tree states)",
+            "value": val, "unit": unit, "n_gpus": 0, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": el / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64 bitsets", "data": "synthetic (seeded counter-based random CSP, synth/csp_synth.h)",
+            "config": {"workload": args.workload + ": " + desc, "n": n, "d": d, "density": dens,
+                       "tightness": tight, "seed": seed},
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": unit, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--workload", default="c3-stream", choices=sorted(WORKLOADS))
+    ap.add_argument("--states", type=int, default=1024)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        out = run_reference(args)
+        print(json.dumps(out), flush=True)
+        return 0
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out, wl = run_gpu(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                out["cpu_baseline"] = oracle_baseline(*wl, budget_s=args.cpu_budget)
+            except Exception as e:  # report, never hide
+                out["cpu_baseline"] = {"value": None, "error": repr(e)}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,187 @@
+/*
+ * rac.h -- C ABI of librac.so: Recurrent Arc Consistency (RAC) enforcement on
+ * NVIDIA B200 (sm_100a).  arXiv 2407.11388, "Paralleling and Accelerating Arc
+ * Consistency Enforcement with Recurrent Tensor Computations".
+ *
+ * The operation (PAPER.md, reference lines cited as P:n):
+ *   A binary CSP has variables x with domains dom(x) and binary constraints
+ *   c_xy with relations rel(c_xy).  c_xy|(x,a) = { tau[y] | tau in rel(c_xy),
+ *   tau[x] = a } is the support set of (x,a) on c_xy; C_x is the set of
+ *   constraints involving x.  A domain set D is arc consistent iff every
+ *   (x,a) in D has c_xy|(x,a) ∩ D(y) ≠ ∅ for every c_xy in C_x.
+ *   D_ac = the union of all arc-consistent subsets of D.
+ *   rac_enforce computes D_ac by the RAC recurrence, Eq. 1:
+ *     D_0 = D_in;  D_k = { (x,a) in D_{k-1} : ∀ c_xy ∈ C_x, c_xy|(x,a) ∩ D_{k-1}(y) ≠ ∅ }
+ *   (the complement form of D~(k) = D~(k-1) ∪ {(x,a) | ∃y c_xy|(x,a) ⊆ D~(k-1)}),
+ *   iterated with the loop control of Alg. 1 tensorAC: after each
+ *   pass, if some D_k(x) = ∅ stop with RAC_WIPEOUT ("throw inconsistency",
+ *   P:203-204), else if D_k = D_{k-1} stop with RAC_OK (Prop. 1 end condition,
+ *   D_ac = D \ D~(K)).
+ *   The reported iteration count is the number of passes executed, including
+ *   the final no-change pass and the wipeout-detecting pass (the number of
+ *   Alg. 1 loop bodies; reading R3).  Every pass reads only D_{k-1}
+ *   (synchronous / Jacobi update; reading R4).
+ *
+ * Data formats
+ *   Domain state D: uint64_t[n_vars]; bit a of word x set iff (x,a) ∈ D.
+ *     Bits at positions >= dom_sizes[x] must be 0.
+ *   Relation: for a constraint on (x, y), rows[a] (a < dom[x]) is a uint64_t
+ *     whose bit b is set iff (a, b) ∈ rel(c_xy); i.e. rows[a] = c_xy|(x,a).
+ *     Bits >= dom[y] must be 0.  The (y, x) orientation is derived (transpose).
+ *   Domain sizes: 1 <= dom_sizes[x] <= 64 (RAC_MAX_DOM).
+ *
+ * Return values: every int-returning call returns >= 0 on success (RAC_OK or
+ * RAC_WIPEOUT for enforcement calls) and a negative RAC_E* code on error.
+ * Nothing is thrown or aborted across the ABI.  After RAC_ECUDA / RAC_ENCCL
+ * the context is unusable and every later call returns RAC_ESTATE.
+ * rac_last_error(ctx) gives a message (ctx == NULL: the thread's last failed
+ * create).
+ *
+ * Ownership: inputs are borrowed for the duration of the call; rac_create
+ * deep-copies and packs relations, so callers may free them on return.  The
+ * context owns all its device memory (and, for world > 1, its NCCL
+ * communicator).  Callers own every D / iteration / status buffer.  d_out may
+ * equal d_in (in place); any other overlap is undefined.
+ *
+ * Concurrency: calls on one context must be serialized by the caller;
+ * distinct contexts are independent.
+ *
+ * Multi-GPU (world > 1): rac_create* and every rac_enforce* call are
+ * COLLECTIVE over the `world` ranks (one process per GPU).  The relation tensor
+ * is row-sharded: rank r holds the masks of variables [x_lo, x_hi) given by
+ * rac_shard_range.  After each pass the ranks all-gather the new alive
+ * bitvector over NCCL; every rank derives the same stop decision from the
+ * gathered vector, so all ranks return identical d_out, iterations and status.
+ * Every rank must pass identical n_vars, dom_sizes and d_in.
+ */
+#ifndef RAC_H
+#define RAC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ------------------------------------------------------- */
+#define RAC_OK 0             /* fixpoint, no empty domain: d_out == D_ac(d_in)            */
+#define RAC_WIPEOUT 1        /* some domain empty: d_out = D after the detecting pass     */
+#define RAC_EINVAL (-1)      /* invalid argument (see each call)                          */
+#define RAC_ENOMEM (-2)      /* host or device allocation failed                          */
+#define RAC_ECUDA (-3)       /* CUDA error; context now unusable                          */
+#define RAC_ENCCL (-4)       /* NCCL error (or NCCL unavailable for world > 1)            */
+#define RAC_ESTATE (-5)      /* context unusable after an earlier CUDA/NCCL error         */
+#define RAC_EUNSUPPORTED (-6)/* valid request this build does not support                 */
+
+/* ---- flags -------------------------------------------------------------- */
+/* Do not stop at the first wipeout: iterate to the definitional fixpoint D_ac
+ * (in which a wiped component is emptied).  Status is RAC_WIPEOUT iff some
+ * domain of the fixpoint is empty. */
+#define RAC_FULL_FIXPOINT (1u << 0)
+
+#define RAC_MAX_DOM 64
+#define RAC_NCCL_ID_BYTES 128
+
+typedef struct rac_ctx rac_ctx;
+
+/* One binary constraint c_xy.  0 <= x, y < n_vars, x != y; at most one
+ * relation per unordered pair (either orientation).  rows has dom[x] words. */
+typedef struct {
+  int32_t x, y;
+  const uint64_t* rows;
+} rac_relation;
+
+typedef struct {
+  int32_t device;             /* CUDA device ordinal (rank's GPU)                     */
+  uint32_t flags;             /* reserved, must be 0                                  */
+  int32_t rank, world;        /* world <= 1: single GPU                               */
+  const void* nccl_unique_id; /* world > 1: RAC_NCCL_ID_BYTES bytes, identical on all
+                                 ranks (from rac_get_nccl_unique_id on rank 0)        */
+  int32_t virtual_shards;     /* world <= 1 only.  > 1: run the sharded per-pass path
+                                 over this many row blocks on one GPU, a device copy
+                                 standing in for the all-gather (tests the partition
+                                 without NCCL).  0 or 1: fused single-GPU path.      */
+} rac_options;
+
+/* Fill *opt with defaults: device 0, single GPU, fused path. */
+void rac_default_options(rac_options* opt);
+
+/*
+ * Create a context from explicit relations ("Prepare Cons"; Fig. 1).
+ * Packs, on the device, every relation into per-(x,a) support masks (both
+ * orientations) plus a constraint-presence bitmap.
+ * RAC_EINVAL: n_vars < 1; dom size outside [1,64]; x == y or out of range;
+ * duplicate unordered pair; bits beyond the domain sizes; NULL pointers
+ * (rels may be NULL iff n_rel == 0); bad options.
+ */
+int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const rac_relation* rels,
+               const rac_options* opt, rac_ctx** out);
+
+/*
+ * Create a context holding the seeded random CSP of synth/csp_synth.h, generated
+ * directly into the packed layout on the device (no host relation copy; needed at
+ * 30+ GB).  Workload shape: PAPER.md §5.2 P:232-236.  Uniform domain size d.
+ * dens_q32 in [0, 2^32] (pair constrained iff 32-bit draw < dens_q32);
+ * t_q16 in [0, 65536] (value pair forbidden iff 16-bit draw < t_q16).
+ */
+int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed,
+                      const rac_options* opt, rac_ctx** out);
+
+/* Blocking enforcement, host buffers: d_in, d_out = uint64_t[n_vars].
+ * Returns RAC_OK / RAC_WIPEOUT (and *iterations) or an error.
+ * RAC_EINVAL: NULL pointers; bits of d_in beyond dom sizes. */
+int rac_enforce(rac_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations);
+
+/* As rac_enforce, plus flags (RAC_FULL_FIXPOINT) and, if removed_at != NULL,
+ * removed_at[x*64 + a] = the pass that removed (x,a), 0 if kept or absent
+ * (the per-step sets V^(k) of Prop. 2).  removed_at needs world == 1. */
+int rac_enforce_ex(rac_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations,
+                   int32_t* removed_at, uint32_t flags);
+
+/* Asynchronous enforcement, DEVICE buffers, enqueued on `stream`
+ * (a cudaStream_t; NULL = legacy default stream).  Writes *status_dev
+ * (RAC_OK / RAC_WIPEOUT) and *iterations_dev on the device; returns 0 once
+ * enqueued.  Bits of d_in beyond dom sizes are ignored.  removed_at_dev is
+ * nullable ([n_vars*64] int32, world == 1 only).  On the single-GPU fused path
+ * the host is not involved per iteration; on the sharded path (world > 1 or
+ * virtual_shards > 1) the host reads a device flag once per chunk of passes. */
+int rac_enforce_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                      int32_t* iterations_dev, int32_t* status_dev, int32_t* removed_at_dev,
+                      uint32_t flags, void* stream);
+
+/* Batched enforcement of n_states independent domain states (search-tree nodes)
+ * on one instance, DEVICE buffers: d_in_dev/d_out_dev = uint64_t[n_states][n_vars],
+ * iterations_dev/status_dev = int32_t[n_states].  State s's results are exactly
+ * those of rac_enforce on state s alone (each state stops at its own pass).
+ * world == 1 only (batches are sharded by the caller). */
+int rac_enforce_batch(rac_ctx* ctx, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                      int32_t* iterations_dev, int32_t* status_dev, uint32_t flags, void* stream);
+
+/* ---- introspection ------------------------------------------------------ */
+int32_t rac_n_vars(const rac_ctx* ctx);
+int32_t rac_max_dom(const rac_ctx* ctx);
+/* Bytes per packed support mask (1, 2, 4 or 8: the smallest width >= max dom bits). */
+int32_t rac_mask_bytes(const rac_ctx* ctx);
+/* Bytes of packed support masks held by this rank (rows x row stride). */
+int64_t rac_relation_bytes(const rac_ctx* ctx);
+/* Row block [*x_lo, *x_hi) of variables owned by `rank` of `world` (host only,
+ * no GPU needed): contiguous blocks of ceil(n_vars/world). */
+int rac_shard_range(int32_t n_vars, int32_t world, int32_t rank, int32_t* x_lo, int32_t* x_hi);
+/* This context's row block. */
+int rac_local_range(const rac_ctx* ctx, int32_t* x_lo, int32_t* x_hi);
+/* Copy the packed support masks of row (x, a) (x in the local block) to host:
+ * out_masks[y] = mask M[x][a][y] widened to uint64 (all ones for absent pairs and
+ * y == x), out_present[y] = 1 iff c_xy is declared.  Either output may be NULL. */
+int rac_read_row(const rac_ctx* ctx, int32_t x, int32_t a, uint64_t* out_masks, uint8_t* out_present);
+/* NCCL unique id for rac_options.nccl_unique_id (call on rank 0, broadcast). */
+int rac_get_nccl_unique_id(void* out /* RAC_NCCL_ID_BYTES */);
+/* Kernel launches enqueued by the last rac_enforce* call on this context. */
+int64_t rac_last_launch_count(const rac_ctx* ctx);
+
+const char* rac_last_error(const rac_ctx* ctx);
+void rac_destroy(rac_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAC_H */

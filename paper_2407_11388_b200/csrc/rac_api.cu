@@ -1,0 +1,610 @@
+// rac_api.cu -- the C ABI of librac.so (declared and documented in include/rac.h).
+//
+// Host side: validation, device memory ownership, the loop drivers and the
+// NCCL communicator.  Every step of the method runs in the kernels of
+// rac_kernels.cu / rac_pack.cu; there is no CPU fallback.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/rac.h"
+#include "rac_internal.cuh"
+
+using namespace rac;
+
+// ----------------------------------------------------------------------------- NCCL (dlopen)
+namespace {
+
+typedef int ncclResult_t;
+typedef void* ncclComm_t;
+typedef struct { char internal[RAC_NCCL_ID_BYTES]; } ncclUniqueId;
+constexpr int kNcclUint64 = 5;  // ncclUint64 in nccl.h
+
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.loaded) {
+    // Prefer the copy torch already loaded (same soname), else load it.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.loaded = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy;
+    }
+  }
+  return api;
+}
+
+thread_local std::string g_create_error;
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- context
+struct rac_ctx {
+  int device = 0;
+  int rank = 0, world = 1, vshards = 1;
+  int n = 0, dmax = 0, W = 0, nvec = 0;
+  size_t row_stride = 0;
+  int x_lo = 0, x_hi = 0, blk = 0;
+  int pw = 0;
+  std::vector<int32_t> dom;
+  std::vector<uint64_t> dommask_h;
+  // device
+  uint8_t* M = nullptr;
+  uint32_t* P = nullptr;
+  int32_t* dom_d = nullptr;
+  uint64_t* dommask = nullptr;
+  unsigned long long* R3 = nullptr;  // fused: [3][n]
+  unsigned* bar = nullptr;
+  ShardState sh{};
+  uint64_t* buf_in = nullptr;   // blocking-API staging
+  uint64_t* buf_out = nullptr;
+  int32_t* buf_scalars = nullptr;  // [iters, status]
+  int32_t* buf_removed = nullptr;  // [n*64]
+  uint64_t* h_in = nullptr;        // pinned
+  uint64_t* h_out = nullptr;
+  int32_t* h_scalars = nullptr;    // pinned [iters, status, done]
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  int G = 1;
+  int fused_grid = 0;
+  int pass_grid = 0;
+  bool fused_coop = true;
+  ncclComm_t comm = nullptr;
+  int64_t launches = 0;
+  bool broken = false;
+  std::string err;
+};
+
+namespace {
+
+int fail(rac_ctx* c, int code, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (code == RAC_ECUDA || code == RAC_ENCCL) c->broken = true;
+  } else {
+    g_create_error = msg;
+  }
+  return code;
+}
+
+#define CK(ctx, call)                                                                              \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return fail((ctx), RAC_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));           \
+  } while (0)
+
+uint64_t dom_mask(int k) { return k >= 64 ? ~0ull : ((1ull << k) - 1ull); }
+
+int mask_bytes(int dmax) { return dmax <= 8 ? 1 : dmax <= 16 ? 2 : dmax <= 32 ? 4 : 8; }
+
+void free_ctx(rac_ctx* c) {
+  if (!c) return;
+  if (c->device >= 0) cudaSetDevice(c->device);
+  if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
+  cudaFree(c->M);
+  cudaFree(c->P);
+  cudaFree(c->dom_d);
+  cudaFree(c->dommask);
+  cudaFree(c->R3);
+  cudaFree(c->bar);
+  cudaFree(c->sh.Dcur);
+  cudaFree(c->sh.Dg);
+  cudaFree(c->sh.Dw);
+  cudaFree(c->sh.R);
+  cudaFree(c->sh.iters);
+  cudaFree(c->buf_in);
+  cudaFree(c->buf_out);
+  cudaFree(c->buf_scalars);
+  cudaFree(c->buf_removed);
+  cudaFreeHost(c->h_in);
+  cudaFreeHost(c->h_out);
+  cudaFreeHost(c->h_scalars);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+// Common part of rac_create / rac_create_random up to (not including) packing.
+int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt) {
+  rac_options o;
+  rac_default_options(&o);
+  if (opt) o = *opt;
+  if (o.flags != 0) return fail(nullptr, RAC_EINVAL, "options.flags must be 0");
+  c->device = o.device;
+  c->world = o.world < 1 ? 1 : o.world;
+  c->rank = c->world > 1 ? o.rank : 0;
+  c->vshards = (c->world == 1 && o.virtual_shards > 1) ? o.virtual_shards : 1;
+  if (c->world > 1 && (o.rank < 0 || o.rank >= c->world || !o.nccl_unique_id))
+    return fail(nullptr, RAC_EINVAL, "world > 1 needs 0 <= rank < world and nccl_unique_id");
+  if (c->vshards > n) c->vshards = n;
+  c->n = n;
+  c->dom.assign(dom, dom + n);
+  c->dmax = 0;
+  for (int x = 0; x < n; ++x) c->dmax = std::max(c->dmax, (int)dom[x]);
+  c->dommask_h.resize(n);
+  for (int x = 0; x < n; ++x) c->dommask_h[x] = dom_mask(dom[x]);
+  c->W = mask_bytes(c->dmax);
+  c->nvec = (int)(((size_t)n * c->W + 15) / 16);
+  c->row_stride = (size_t)c->nvec * 16;
+  c->pw = (n + 31) / 32;
+  c->blk = (n + c->world - 1) / c->world;
+  rac_shard_range(n, c->world, c->rank, &c->x_lo, &c->x_hi);
+  c->G = choose_group(c->nvec);
+
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(nullptr, RAC_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  if (cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess)
+    return fail(nullptr, RAC_ECUDA, "cudaDeviceGetAttribute");
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(nullptr, RAC_ECUDA, "cudaStreamCreate");
+
+  const size_t local_vars = (size_t)(c->x_hi - c->x_lo);
+  const size_t mbytes = local_vars * c->dmax * c->row_stride;
+#define CKC(call)                                                                                   \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess)                                                                          \
+      return fail(nullptr, e_ == cudaErrorMemoryAllocation ? RAC_ENOMEM : RAC_ECUDA,                \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                              \
+  } while (0)
+  CKC(cudaMalloc(&c->M, std::max<size_t>(mbytes, 16)));
+  CKC(cudaMemsetAsync(c->M, 0xFF, std::max<size_t>(mbytes, 16), c->stream));
+  CKC(cudaMalloc(&c->P, std::max<size_t>(local_vars * c->pw * 4, 4)));
+  CKC(cudaMemsetAsync(c->P, 0, std::max<size_t>(local_vars * c->pw * 4, 4), c->stream));
+  CKC(cudaMalloc(&c->dom_d, (size_t)n * 4));
+  CKC(cudaMemcpyAsync(c->dom_d, dom, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+  CKC(cudaMalloc(&c->dommask, (size_t)n * 8));
+  CKC(cudaMemcpyAsync(c->dommask, c->dommask_h.data(), (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
+  CKC(cudaMalloc(&c->R3, (size_t)3 * n * 8));
+  CKC(cudaMemsetAsync(c->R3, 0, (size_t)3 * n * 8, c->stream));
+  CKC(cudaMalloc(&c->bar, 16));
+  CKC(cudaMemsetAsync(c->bar, 0, 16, c->stream));
+  const size_t gtot = (size_t)c->world * c->blk;
+  CKC(cudaMalloc(&c->sh.Dcur, (size_t)n * 8));
+  CKC(cudaMalloc(&c->sh.Dg, gtot * 8));
+  CKC(cudaMalloc(&c->sh.Dw, c->row_stride));
+  CKC(cudaMalloc(&c->sh.R, (size_t)n * 8));
+  CKC(cudaMemsetAsync(c->sh.R, 0, (size_t)n * 8, c->stream));
+  CKC(cudaMalloc(&c->sh.iters, 16));
+  c->sh.status = c->sh.iters + 1;
+  c->sh.done = c->sh.iters + 2;
+  CKC(cudaMalloc(&c->buf_in, (size_t)n * 8));
+  CKC(cudaMalloc(&c->buf_out, (size_t)n * 8));
+  CKC(cudaMalloc(&c->buf_scalars, 16));
+  CKC(cudaMalloc(&c->buf_removed, (size_t)n * 64 * 4));
+  CKC(cudaMallocHost(&c->h_in, (size_t)n * 8));
+  CKC(cudaMallocHost(&c->h_out, (size_t)n * 8));
+  CKC(cudaMallocHost(&c->h_scalars, 16));
+
+  // Launch geometry.  Fused path: a co-resident grid (cooperative launch),
+  // as many CTAs as fit, but no more than the work can feed.
+  const long rows = (long)n * c->dmax;
+  const long groups_per_cta = (kThreads / 32) * (32 / c->G);
+  int occ = 0;
+  CKC(fused_occupancy(c->W, c->G, c->row_stride, &occ));
+  if (occ < 1) return fail(nullptr, RAC_EUNSUPPORTED, "support-pass kernel does not fit on an SM (n too large)");
+  long want = (rows + groups_per_cta - 1) / groups_per_cta;
+  c->fused_grid = (int)std::max(1L, std::min((long)c->sm_count * occ, want));
+  int pocc = 0;
+  CKC(pass_occupancy(c->W, c->G, c->row_stride, &pocc));
+  c->pass_grid = c->sm_count * std::max(1, pocc);
+  CKC(cudaStreamSynchronize(c->stream));
+#undef CKC
+  return 0;
+}
+
+// Split long rows into segments so that every group gets several items
+// (static round-robin load balance).  Segment length is a multiple of the
+// group's batch (G * kUnroll vectors).
+void set_segments(const rac_ctx* c, PassGeom& g, long rows, long ngroups) {
+  const int batch = c->G * kUnroll;
+  int n_seg = 1;
+  while (rows * n_seg < 12 * ngroups && (c->nvec + n_seg * 2 - 1) / (n_seg * 2) >= batch) n_seg *= 2;
+  int seg = (c->nvec + n_seg - 1) / n_seg;
+  seg = (seg + batch - 1) / batch * batch;
+  g.seg_vecs = seg;
+  g.n_seg = (c->nvec + seg - 1) / seg;
+}
+
+PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi, long ngroups) {
+  PassGeom g{};
+  g.M = c->M;
+  g.row_stride = c->row_stride;
+  g.nvec = c->nvec;
+  g.n = c->n;
+  g.dmax = c->dmax;
+  g.x_lo = x_lo;
+  g.x_hi = x_hi;
+  g.x_lo_alloc = c->x_lo;
+  g.P = c->P;
+  g.pw = c->pw;
+  set_segments(c, g, (long)(x_hi - x_lo) * c->dmax, ngroups);
+  return g;
+}
+
+int check_usable(rac_ctx* c) {
+  if (!c) return RAC_EINVAL;
+  if (c->broken) return RAC_ESTATE;
+  return 0;
+}
+
+int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
+                  int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+  FusedParams p{};
+  const long ngroups = (long)c->fused_grid * (kThreads / 32) * (32 / c->G);
+  p.g = geom_for(c, 0, c->n, ngroups);
+  p.dommask = c->dommask;
+  p.d_in = d_in;
+  p.d_out = d_out;
+  p.iters = iters;
+  p.status = status;
+  p.removed_at = removed_at;
+  p.R = c->R3;
+  p.bar = c->bar;
+  p.flags = flags;
+  if (removed_at) {
+    CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
+    c->launches++;
+  }
+  // R of pass 1 must be clear: R[1] was cleared during the previous call's
+  // last pass or is the initial zero fill... clear it explicitly (tiny).
+  CK(c, cudaMemsetAsync(c->R3 + (size_t)1 * c->n, 0, (size_t)c->n * 8, s));
+  c->launches++;
+  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, c->row_stride, s, c->fused_grid > 1));
+  c->launches++;
+  return 0;
+}
+
+int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
+                    int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+  if (removed_at && c->world > 1) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
+  const int total_g = c->world * c->blk;
+  if (removed_at) {
+    CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
+    c->launches++;
+  }
+  CK(c, launch_shard_init(c->sh, d_in, c->dommask, c->n, c->W, c->row_stride, total_g, s));
+  c->launches++;
+  const long ngroups = (long)c->pass_grid * (kThreads / 32) * (32 / c->G);
+  const int nb = c->world > 1 ? 1 : c->vshards;
+  std::vector<PassParams> pp(nb);
+  for (int b = 0; b < nb; ++b) {
+    int lo, hi;
+    if (c->world > 1) { lo = c->x_lo; hi = c->x_hi; }
+    else rac_shard_range(c->n, c->vshards, b, &lo, &hi);
+    pp[b].g = geom_for(c, lo, std::min(hi, c->n), ngroups);
+    pp[b].s = c->sh;
+    pp[b].removed_at = removed_at;
+  }
+  const long max_passes = (long)c->n * c->dmax + 2;
+  long enq = 0;
+  int chunk = 2;
+  for (;;) {
+    for (int k = 0; k < chunk; ++k) {
+      for (int b = 0; b < nb; ++b) {
+        if (pp[b].g.x_hi <= pp[b].g.x_lo) continue;
+        CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, c->row_stride, s));
+        c->launches++;
+      }
+      if (c->world > 1) {
+        CK(c, launch_shard_slice(c->sh, c->x_lo, c->x_lo + c->blk, c->n, s));
+        c->launches++;
+        ncclResult_t r = nccl().AllGather(c->sh.Dg + (size_t)c->rank * c->blk, c->sh.Dg, (size_t)c->blk,
+                                          kNcclUint64, c->comm, s);
+        if (r != 0)
+          return fail(c, RAC_ENCCL, std::string("ncclAllGather: ") +
+                                        (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
+        c->launches++;
+      } else {
+        CK(c, launch_shard_slice(c->sh, 0, c->n, c->n, s));
+        c->launches++;
+      }
+      CK(c, launch_shard_update(c->sh, c->n, c->W, flags, s));
+      c->launches++;
+    }
+    enq += chunk;
+    CK(c, cudaMemcpyAsync(c->h_scalars + 2, c->sh.done, 4, cudaMemcpyDeviceToHost, s));
+    CK(c, cudaStreamSynchronize(s));
+    if (c->h_scalars[2]) break;
+    if (enq > max_passes) return fail(c, RAC_ECUDA, "sharded loop did not converge (internal error)");
+    chunk = std::min(chunk * 2, 64);
+  }
+  CK(c, launch_shard_finalize(c->sh, c->n, d_out, iters, status, s));
+  c->launches++;
+  return 0;
+}
+
+int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
+                       int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+  if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
+  CK(c, cudaSetDevice(c->device));
+  c->launches = 0;
+  if (c->world > 1 || c->vshards > 1) return enforce_sharded(c, d_in, d_out, iters, status, removed_at, flags, s);
+  return enforce_fused(c, d_in, d_out, iters, status, removed_at, flags, s);
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- C ABI
+extern "C" {
+
+void rac_default_options(rac_options* opt) {
+  if (!opt) return;
+  memset(opt, 0, sizeof(*opt));
+  opt->device = 0;
+  opt->world = 1;
+  opt->rank = 0;
+  opt->virtual_shards = 0;
+}
+
+int rac_shard_range(int32_t n_vars, int32_t world, int32_t rank, int32_t* x_lo, int32_t* x_hi) {
+  if (n_vars < 0 || world < 1 || rank < 0 || rank >= world || !x_lo || !x_hi) return RAC_EINVAL;
+  const int blk = (n_vars + world - 1) / world;
+  *x_lo = std::min(n_vars, rank * blk);
+  *x_hi = std::min(n_vars, (rank + 1) * blk);
+  return 0;
+}
+
+static int init_comm(rac_ctx* c, const rac_options* opt) {
+  if (c->world <= 1) return 0;
+  if (!nccl().loaded) return fail(nullptr, RAC_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  memcpy(id.internal, opt->nccl_unique_id, RAC_NCCL_ID_BYTES);
+  ncclResult_t r = nccl().CommInitRank(&c->comm, c->world, id, c->rank);
+  if (r != 0) {
+    c->comm = nullptr;
+    return fail(nullptr, RAC_ENCCL,
+                std::string("ncclCommInitRank: ") + (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
+  }
+  return 0;
+}
+
+int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const rac_relation* rels,
+               const rac_options* opt, rac_ctx** out) {
+  if (!out) return fail(nullptr, RAC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_vars < 1 || !dom_sizes || n_rel < 0 || (n_rel > 0 && !rels))
+    return fail(nullptr, RAC_EINVAL, "bad n_vars / dom_sizes / rels");
+  for (int x = 0; x < n_vars; ++x)
+    if (dom_sizes[x] < 1 || dom_sizes[x] > RAC_MAX_DOM) return fail(nullptr, RAC_EINVAL, "dom size outside [1,64]");
+  int dmax = 0;
+  for (int x = 0; x < n_vars; ++x) dmax = std::max(dmax, (int)dom_sizes[x]);
+  // validate relations: range, x != y, padding bits, duplicate unordered pairs
+  std::vector<uint64_t> keys(n_rel);
+  std::vector<int32_t> xs(n_rel), ys(n_rel);
+  std::vector<uint64_t> rows((size_t)n_rel * dmax, 0ull);
+  for (int r = 0; r < n_rel; ++r) {
+    const int x = rels[r].x, y = rels[r].y;
+    if (x < 0 || y < 0 || x >= n_vars || y >= n_vars || x == y || !rels[r].rows)
+      return fail(nullptr, RAC_EINVAL, "relation " + std::to_string(r) + ": bad (x, y) or NULL rows");
+    const uint64_t my = dom_mask(dom_sizes[y]);
+    for (int a = 0; a < dom_sizes[x]; ++a) {
+      const uint64_t v = rels[r].rows[a];
+      if (v & ~my) return fail(nullptr, RAC_EINVAL, "relation " + std::to_string(r) + ": bits beyond dom(y)");
+      rows[(size_t)r * dmax + a] = v;
+    }
+    xs[r] = x;
+    ys[r] = y;
+    keys[r] = ((uint64_t)std::min(x, y) << 32) | (uint64_t)std::max(x, y);
+  }
+  {
+    std::vector<uint64_t> k2 = keys;
+    std::sort(k2.begin(), k2.end());
+    if (std::adjacent_find(k2.begin(), k2.end()) != k2.end())
+      return fail(nullptr, RAC_EINVAL, "duplicate constraint on one unordered pair");
+  }
+  rac_ctx* c = new rac_ctx();
+  int rc = setup_ctx(c, n_vars, dom_sizes, opt);
+  if (rc) { free_ctx(c); return rc; }
+  if (n_rel > 0) {
+    int32_t *dxs = nullptr, *dys = nullptr;
+    uint64_t* drows = nullptr;
+    cudaError_t e = cudaMalloc(&dxs, (size_t)n_rel * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&dys, (size_t)n_rel * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&drows, rows.size() * 8);
+    if (e == cudaSuccess) e = cudaMemcpy(dxs, xs.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dys, ys.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice);
+    PackGeom g{c->M, c->row_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
+    if (e == cudaSuccess) e = launch_pack_relations(g, dxs, dys, drows, n_rel, dmax, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(dxs);
+    cudaFree(dys);
+    cudaFree(drows);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(nullptr, RAC_ECUDA, std::string("packing relations: ") + cudaGetErrorString(e));
+    }
+  }
+  rc = init_comm(c, opt);
+  if (rc) { free_ctx(c); return rc; }
+  *out = c;
+  return 0;
+}
+
+int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed,
+                      const rac_options* opt, rac_ctx** out) {
+  if (!out) return fail(nullptr, RAC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_vars < 1 || d < 1 || d > RAC_MAX_DOM || dens_q32 > (1ull << 32) || t_q16 > 65536u)
+    return fail(nullptr, RAC_EINVAL, "bad generator parameters");
+  std::vector<int32_t> dom(n_vars, d);
+  rac_ctx* c = new rac_ctx();
+  int rc = setup_ctx(c, n_vars, dom.data(), opt);
+  if (rc) { free_ctx(c); return rc; }
+  PackGeom g{c->M, c->row_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
+  cudaError_t e = launch_generate(g, d, dens_q32, t_q16, seed, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    free_ctx(c);
+    return fail(nullptr, RAC_ECUDA, std::string("generating instance: ") + cudaGetErrorString(e));
+  }
+  rc = init_comm(c, opt);
+  if (rc) { free_ctx(c); return rc; }
+  *out = c;
+  return 0;
+}
+
+int rac_enforce_async(rac_ctx* c, const uint64_t* d_in_dev, uint64_t* d_out_dev, int32_t* iterations_dev,
+                      int32_t* status_dev, int32_t* removed_at_dev, uint32_t flags, void* stream) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev) return fail(c, RAC_EINVAL, "NULL device buffer");
+  return enforce_async_impl(c, d_in_dev, d_out_dev, iterations_dev, status_dev, removed_at_dev, flags,
+                            (cudaStream_t)stream);
+}
+
+int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations, int32_t* removed_at,
+                   uint32_t flags) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (!d_in || !d_out || !iterations) return fail(c, RAC_EINVAL, "NULL pointer");
+  for (int x = 0; x < c->n; ++x)
+    if (d_in[x] & ~c->dommask_h[x]) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
+  CK(c, cudaSetDevice(c->device));
+  const size_t nb = (size_t)c->n * 8;
+  memcpy(c->h_in, d_in, nb);
+  CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb, cudaMemcpyHostToDevice, c->stream));
+  rc = enforce_async_impl(c, c->buf_in, c->buf_out, c->buf_scalars, c->buf_scalars + 1,
+                          removed_at ? c->buf_removed : nullptr, flags, c->stream);
+  if (rc) return rc;
+  CK(c, cudaMemcpyAsync(c->h_out, c->buf_out, nb, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(c->h_scalars, c->buf_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
+  if (removed_at)
+    CK(c, cudaMemcpyAsync(removed_at, c->buf_removed, (size_t)c->n * 64 * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  memcpy(d_out, c->h_out, nb);
+  *iterations = c->h_scalars[0];
+  const int st = c->h_scalars[1];
+  if (st != RAC_OK && st != RAC_WIPEOUT) return fail(c, RAC_ECUDA, "kernel did not report a status");
+  return st;
+}
+
+int rac_enforce(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations) {
+  return rac_enforce_ex(c, d_in, d_out, iterations, nullptr, 0u);
+}
+
+int rac_enforce_batch(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                      int32_t* iterations_dev, int32_t* status_dev, uint32_t flags, void* stream) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (n_states < 0 || (n_states > 0 && (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev)))
+    return fail(c, RAC_EINVAL, "bad batch arguments");
+  if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
+  if (c->world > 1) return fail(c, RAC_EUNSUPPORTED, "batched mode runs per rank (world == 1 contexts)");
+  c->launches = 0;
+  if (n_states == 0) return 0;
+  CK(c, cudaSetDevice(c->device));
+  BatchParams p{};
+  p.g = geom_for(c, 0, c->n, 1);
+  p.g.n_seg = 1;
+  p.g.seg_vecs = c->nvec;
+  p.dommask = c->dommask;
+  p.d_in = d_in_dev;
+  p.d_out = d_out_dev;
+  p.iters = iterations_dev;
+  p.status = status_dev;
+  p.flags = flags;
+  const size_t smem = c->row_stride + (size_t)c->n * 8;
+  int occ = 0;
+  CK(c, batch_occupancy(c->W, c->G, smem, &occ));
+  if (occ < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");
+  CK(c, launch_batch(c->W, c->G, p, n_states, smem, (cudaStream_t)stream));
+  c->launches = 1;
+  return 0;
+}
+
+int32_t rac_n_vars(const rac_ctx* c) { return c ? c->n : RAC_EINVAL; }
+int32_t rac_max_dom(const rac_ctx* c) { return c ? c->dmax : RAC_EINVAL; }
+int32_t rac_mask_bytes(const rac_ctx* c) { return c ? c->W : RAC_EINVAL; }
+int64_t rac_relation_bytes(const rac_ctx* c) {
+  return c ? (int64_t)(c->x_hi - c->x_lo) * c->dmax * (int64_t)c->row_stride : RAC_EINVAL;
+}
+int64_t rac_last_launch_count(const rac_ctx* c) { return c ? c->launches : RAC_EINVAL; }
+
+int rac_local_range(const rac_ctx* c, int32_t* x_lo, int32_t* x_hi) {
+  if (!c || !x_lo || !x_hi) return RAC_EINVAL;
+  *x_lo = c->x_lo;
+  *x_hi = c->x_hi;
+  return 0;
+}
+
+int rac_read_row(const rac_ctx* cc, int32_t x, int32_t a, uint64_t* out_masks, uint8_t* out_present) {
+  rac_ctx* c = const_cast<rac_ctx*>(cc);
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (x < c->x_lo || x >= c->x_hi || a < 0 || a >= c->dmax) return fail(c, RAC_EINVAL, "row not local");
+  CK(c, cudaSetDevice(c->device));
+  if (out_masks) {
+    std::vector<uint8_t> buf(c->row_stride);
+    const size_t r = (size_t)(x - c->x_lo) * c->dmax + a;
+    CK(c, cudaMemcpy(buf.data(), c->M + r * c->row_stride, c->row_stride, cudaMemcpyDeviceToHost));
+    for (int y = 0; y < c->n; ++y) {
+      uint64_t v = 0;
+      for (int k = 0; k < c->W; ++k) v |= (uint64_t)buf[(size_t)y * c->W + k] << (8 * k);
+      out_masks[y] = v;
+    }
+  }
+  if (out_present) {
+    std::vector<uint32_t> pb(c->pw);
+    CK(c, cudaMemcpy(pb.data(), c->P + (size_t)(x - c->x_lo) * c->pw, (size_t)c->pw * 4, cudaMemcpyDeviceToHost));
+    for (int y = 0; y < c->n; ++y) out_present[y] = (pb[y >> 5] >> (y & 31)) & 1u;
+  }
+  return 0;
+}
+
+int rac_get_nccl_unique_id(void* out) {
+  if (!out) return RAC_EINVAL;
+  if (!nccl().loaded) return fail(nullptr, RAC_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != 0) return fail(nullptr, RAC_ENCCL, "ncclGetUniqueId failed");
+  memcpy(out, id.internal, RAC_NCCL_ID_BYTES);
+  return 0;
+}
+
+const char* rac_last_error(const rac_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+void rac_destroy(rac_ctx* c) { free_ctx(c); }
+
+}  // extern "C"

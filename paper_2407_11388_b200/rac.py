@@ -1,0 +1,284 @@
+"""Thin ctypes binding of librac.so (include/rac.h).  Argument marshalling
+only: every step of the enforcement runs in the library's CUDA kernels.
+
+The functions keep the C names (``rac_create``, ``rac_enforce``, ...).
+``RacContext`` is a small owning wrapper that also accepts torch tensors
+(device memory / streams come from torch: plumbing, not the product).
+
+There is no CPU fallback: if librac.so is missing or cannot be loaded this
+module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librac.so")
+
+RAC_OK = 0
+RAC_WIPEOUT = 1
+RAC_EINVAL = -1
+RAC_ENOMEM = -2
+RAC_ECUDA = -3
+RAC_ENCCL = -4
+RAC_ESTATE = -5
+RAC_EUNSUPPORTED = -6
+RAC_FULL_FIXPOINT = 1
+RAC_MAX_DOM = 64
+RAC_NCCL_ID_BYTES = 128
+
+_ERRNAMES = {RAC_EINVAL: "RAC_EINVAL", RAC_ENOMEM: "RAC_ENOMEM", RAC_ECUDA: "RAC_ECUDA", RAC_ENCCL: "RAC_ENCCL",
+             RAC_ESTATE: "RAC_ESTATE", RAC_EUNSUPPORTED: "RAC_EUNSUPPORTED"}
+
+
+class RacError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__("%s (%d): %s" % (_ERRNAMES.get(code, "RAC_E?"), code, msg))
+        self.code = code
+
+
+class rac_relation(ctypes.Structure):
+    _fields_ = [("x", ctypes.c_int32), ("y", ctypes.c_int32), ("rows", ctypes.POINTER(ctypes.c_uint64))]
+
+
+class rac_options(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p), ("virtual_shards", ctypes.c_int32)]
+
+
+# Every symbol include/rac.h declares (checked by tests/test_abi.py).
+EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforce", "rac_enforce_ex",
+           "rac_enforce_async", "rac_enforce_batch", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
+           "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
+           "rac_last_launch_count", "rac_last_error", "rac_destroy"]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("librac.so not built (%s); run `python -c 'import __graft_entry__ as g; g.build()'`"
+                          % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    P = ctypes.c_void_p
+    i32, u32, i64, u64 = ctypes.c_int32, ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint64
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    sig = {
+        "rac_default_options": (None, [ctypes.POINTER(rac_options)]),
+        "rac_create": (ctypes.c_int, [i32, i32p, i32, ctypes.POINTER(rac_relation), ctypes.POINTER(rac_options),
+                                      ctypes.POINTER(P)]),
+        "rac_create_random": (ctypes.c_int, [i32, i32, u64, u32, u64, ctypes.POINTER(rac_options),
+                                             ctypes.POINTER(P)]),
+        "rac_enforce": (ctypes.c_int, [P, u64p, u64p, i32p]),
+        "rac_enforce_ex": (ctypes.c_int, [P, u64p, u64p, i32p, i32p, u32]),
+        "rac_enforce_async": (ctypes.c_int, [P, P, P, P, P, P, u32, P]),
+        "rac_enforce_batch": (ctypes.c_int, [P, i32, P, P, P, P, u32, P]),
+        "rac_n_vars": (i32, [P]),
+        "rac_max_dom": (i32, [P]),
+        "rac_mask_bytes": (i32, [P]),
+        "rac_relation_bytes": (i64, [P]),
+        "rac_shard_range": (ctypes.c_int, [i32, i32, i32, i32p, i32p]),
+        "rac_local_range": (ctypes.c_int, [P, i32p, i32p]),
+        "rac_read_row": (ctypes.c_int, [P, i32, i32, u64p, ctypes.POINTER(ctypes.c_uint8)]),
+        "rac_get_nccl_unique_id": (ctypes.c_int, [P]),
+        "rac_last_launch_count": (i64, [P]),
+        "rac_last_error": (ctypes.c_char_p, [P]),
+        "rac_destroy": (None, [P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def _u64p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def last_error(ctx=None) -> str:
+    s = lib.rac_last_error(ctx)
+    return s.decode() if s else ""
+
+
+def _check(rc: int, ctx=None) -> int:
+    if rc < 0:
+        raise RacError(rc, last_error(ctx))
+    return rc
+
+
+def rac_shard_range(n_vars: int, world: int, rank: int) -> Tuple[int, int]:
+    lo, hi = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib.rac_shard_range(n_vars, world, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def rac_get_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(RAC_NCCL_ID_BYTES)
+    _check(lib.rac_get_nccl_unique_id(buf))
+    return buf.raw
+
+
+def make_options(device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
+                 virtual_shards: int = 0):
+    o = rac_options()
+    lib.rac_default_options(ctypes.byref(o))
+    o.device, o.rank, o.world, o.virtual_shards = device, rank, world, virtual_shards
+    keep = None
+    if nccl_unique_id is not None:
+        keep = ctypes.create_string_buffer(bytes(nccl_unique_id), RAC_NCCL_ID_BYTES)
+        o.nccl_unique_id = ctypes.cast(keep, ctypes.c_void_p)
+    return o, keep
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        try:
+            import torch
+            return int(torch.cuda.current_stream().cuda_stream)
+        except Exception:  # pragma: no cover - no torch / no cuda
+            return 0
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return 0
+    if isinstance(t, int):
+        return t
+    return int(t.data_ptr())
+
+
+class RacContext:
+    """Owning wrapper of a rac_ctx*."""
+
+    def __init__(self, handle, n: int, dmax: int):
+        self._h = handle
+        self.n = n
+        self.dmax = dmax
+
+    # ---- creation
+    @classmethod
+    def create(cls, n_vars: int, dom_sizes, xs, ys, rows, device: int = 0, rank: int = 0, world: int = 1,
+               nccl_unique_id: Optional[bytes] = None, virtual_shards: int = 0) -> "RacContext":
+        """rac_create from relation arrays: constraint k on (xs[k], ys[k]) with
+        rows[k, a] = c_xy|(x,a) bitsets (uint64)."""
+        dom = np.ascontiguousarray(dom_sizes, dtype=np.int32)
+        xs = np.ascontiguousarray(xs, dtype=np.int32)
+        ys = np.ascontiguousarray(ys, dtype=np.int32)
+        rows = np.ascontiguousarray(rows, dtype=np.uint64)
+        m = xs.shape[0]
+        rel = (rac_relation * max(m, 1))()
+        if m:
+            stride = rows.shape[1] * 8
+            base = rows.ctypes.data
+            arr = np.frombuffer(rel, dtype=np.dtype([("x", np.int32), ("y", np.int32), ("rows", np.uint64)]),
+                                count=m)
+            arr["x"] = xs
+            arr["y"] = ys
+            arr["rows"] = base + stride * np.arange(m, dtype=np.uint64)
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards)
+        h = ctypes.c_void_p()
+        rc = lib.rac_create(n_vars, _i32p(dom), m, rel if m else None, ctypes.byref(opt), ctypes.byref(h))
+        _check(rc)
+        del keep
+        return cls(h, n_vars, int(dom.max()))
+
+    @classmethod
+    def from_instance(cls, inst, **kw) -> "RacContext":
+        return cls.create(inst.n, inst.dom, inst.xs, inst.ys, inst.rows, **kw)
+
+    @classmethod
+    def create_random(cls, n_vars: int, d: int, dens_q32: int, t_q16: int, seed: int, device: int = 0,
+                      rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
+                      virtual_shards: int = 0) -> "RacContext":
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards)
+        h = ctypes.c_void_p()
+        _check(lib.rac_create_random(n_vars, d, dens_q32, t_q16, seed, ctypes.byref(opt), ctypes.byref(h)))
+        del keep
+        return cls(h, n_vars, d)
+
+    def close(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.rac_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- enforcement
+    def enforce(self, d_in, full: bool = False, removed_at: bool = False):
+        """rac_enforce / rac_enforce_ex with host buffers.
+        Returns (status, d_out, iterations[, removed_at[n,64]])."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        if d_in.shape != (self.n,):
+            raise ValueError("d_in must have shape (n_vars,)")
+        d_out = np.zeros(self.n, dtype=np.uint64)
+        it = ctypes.c_int32(0)
+        rem = np.zeros(self.n * 64, dtype=np.int32) if removed_at else None
+        if full or removed_at:
+            rc = lib.rac_enforce_ex(self._h, _u64p(d_in), _u64p(d_out), ctypes.byref(it),
+                                    _i32p(rem) if rem is not None else None, RAC_FULL_FIXPOINT if full else 0)
+        else:
+            rc = lib.rac_enforce(self._h, _u64p(d_in), _u64p(d_out), ctypes.byref(it))
+        _check(rc, self._h)
+        if removed_at:
+            return rc, d_out, it.value, rem.reshape(self.n, 64)
+        return rc, d_out, it.value
+
+    def enforce_async(self, d_in_dev, d_out_dev, iters_dev, status_dev, removed_at_dev=None, full: bool = False,
+                      stream=None) -> None:
+        """rac_enforce_async on device buffers (torch tensors or raw pointers)."""
+        _check(lib.rac_enforce_async(self._h, _ptr(d_in_dev), _ptr(d_out_dev), _ptr(iters_dev), _ptr(status_dev),
+                                     _ptr(removed_at_dev), RAC_FULL_FIXPOINT if full else 0, _stream_ptr(stream)),
+               self._h)
+
+    def enforce_batch(self, n_states: int, d_in_dev, d_out_dev, iters_dev, status_dev, full: bool = False,
+                      stream=None) -> None:
+        """rac_enforce_batch on device buffers: [n_states, n] uint64 states."""
+        _check(lib.rac_enforce_batch(self._h, n_states, _ptr(d_in_dev), _ptr(d_out_dev), _ptr(iters_dev),
+                                     _ptr(status_dev), RAC_FULL_FIXPOINT if full else 0, _stream_ptr(stream)),
+               self._h)
+
+    # ---- introspection
+    @property
+    def mask_bytes(self) -> int:
+        return int(lib.rac_mask_bytes(self._h))
+
+    @property
+    def relation_bytes(self) -> int:
+        return int(lib.rac_relation_bytes(self._h))
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(lib.rac_last_launch_count(self._h))
+
+    def local_range(self) -> Tuple[int, int]:
+        lo, hi = ctypes.c_int32(0), ctypes.c_int32(0)
+        _check(lib.rac_local_range(self._h, ctypes.byref(lo), ctypes.byref(hi)), self._h)
+        return lo.value, hi.value
+
+    def read_row(self, x: int, a: int) -> Tuple[np.ndarray, np.ndarray]:
+        masks = np.zeros(self.n, dtype=np.uint64)
+        pres = np.zeros(self.n, dtype=np.uint8)
+        _check(lib.rac_read_row(self._h, x, a, _u64p(masks), pres.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))),
+               self._h)
+        return masks, pres

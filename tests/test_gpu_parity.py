@@ -1,0 +1,323 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Everything integer: the bar is bit-exact equality of
+status, D_out, iteration count and (where requested) the per-value removal
+epochs.  Expected values come only from oracle/ (never from the CUDA path).
+
+Configs C1..C5 are BASELINE.json configs[0..4]; workloads W-root / W-seed /
+W-rand / W-stream / W-prop / W-dive are defined in DESIGN.md "Input recipe".
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import _instances as I
+
+pytestmark = pytest.mark.gpu
+
+U64 = np.uint64
+
+
+@pytest.fixture(scope="module")
+def rac():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2407_11388_b200 import rac as r
+    return r
+
+
+def assert_same(g, o, what=""):
+    """g = (status, d_out, iters[, removed_at]) from the GPU, o from the oracle."""
+    assert g[0] == o[0], (what, "status", g[0], o[0])
+    assert g[2] == o[2], (what, "iterations", g[2], o[2])
+    assert np.array_equal(g[1], o[1]), (what, "d_out")
+    if len(g) > 3 and len(o) > 3 and o[3] is not None:
+        assert np.array_equal(g[3], o[3]), (what, "removed_at")
+
+
+def both(ctx, orc, d_in, full=False):
+    g = ctx.enforce(d_in, full=full, removed_at=True)
+    o = orc.rac(d_in, full=full)
+    return g, o
+
+
+# ----------------------------------------------------------------------------- hand traces
+@pytest.mark.parametrize("name", I.golden_names())
+def test_golden(rac, name):
+    doc, inst = I.load_golden(name)
+    exp = doc["expect"]
+    ctx = rac.RacContext.from_instance(inst)
+    st, d_out, it, rem = ctx.enforce(np.asarray(doc["d_in"], dtype=U64), removed_at=True)
+    assert st == (rac.RAC_OK if exp["status"] == "OK" else rac.RAC_WIPEOUT)
+    assert [int(v) for v in d_out] == exp["d_out"] and it == exp["iterations"]
+    trace = [set() for _ in range(it)]
+    for x in range(inst.n):
+        for a in range(64):
+            if rem[x, a]:
+                trace[rem[x, a] - 1].add((x, a))
+    assert trace == [set(map(tuple, s)) for s in exp["trace"]]
+
+
+# ----------------------------------------------------------------------------- packer
+@pytest.mark.parametrize("n,d,p,t", [(9, 3, 0.5, 0.3), (33, 8, 0.7, 0.4), (70, 17, 0.3, 0.5), (40, 64, 0.9, 0.6),
+                                     (17, 1, 1.0, 0.2)])
+def test_packer_matches_oracle_layout(rac, n, d, p, t):
+    """Packed masks M[x][a][·] and presence bits equal the oracle's support sets
+    c_xy|(x,a) (both orientations), for host-packed (N1) and device-generated (N7)
+    instances of the same seed."""
+    inst = synth.random_csp(n, d, p, t, seed=5)
+    orc = oracle.Oracle.from_instance(inst)
+    for ctx in (rac.RacContext.from_instance(inst),
+                rac.RacContext.create_random(n, d, synth.quant_density(p), synth.quant_tightness(t), 5)):
+        allones = U64((1 << (8 * ctx.mask_bytes)) - 1)
+        for x in range(n):
+            for a in range(d):
+                masks, pres = ctx.read_row(x, a)
+                for y in range(n):
+                    present, s = orc.support(x, y, a)
+                    assert bool(pres[y]) == present
+                    if present:
+                        assert int(masks[y]) == s, (x, a, y)
+                    else:
+                        assert masks[y] == allones
+
+
+# ----------------------------------------------------------------------------- corpora
+def test_spec_corpus(rac):
+    """SPEC.md acceptance corpus shape: 1000 instances, n 2..20, d 1..6,
+    density 0.1..1, tightness 0..0.9; W-root and W-rand; stop and full modes."""
+    for k, inst in enumerate(I.random_corpus(1000)):
+        ctx = rac.RacContext.from_instance(inst)
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = inst.full_domains() if k % 2 == 0 else synth.w_rand(inst.dom, 0.9, seed=k)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (k, full))
+
+
+def test_nonuniform_domains_and_empty_rows(rac):
+    """Per-variable domain sizes (padded to the max) and empty rows in D_in
+    (reading R7: one pass, presence semantics, then WIPEOUT)."""
+    rng = np.random.default_rng(3)
+    for k in range(200):
+        n = int(rng.integers(2, 14))
+        dom = rng.integers(1, 9, size=n)
+        cons = []
+        for x in range(n):
+            for y in range(x + 1, n):
+                if rng.random() < 0.5:
+                    allowed = [(a, b) for a in range(dom[x]) for b in range(dom[y]) if rng.random() > 0.35]
+                    cons.append((x, y, allowed))
+        inst = synth.from_constraints(n, dom, cons)
+        ctx = rac.RacContext.from_instance(inst)
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = synth.w_rand(inst.dom, 0.85, seed=k)
+        if k % 3 == 0:
+            d_in[int(rng.integers(n))] = U64(0)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (k, full))
+
+
+@pytest.mark.parametrize("d", [8, 16, 32, 64])
+def test_equality_chain_many_passes(rac, d):
+    """Closed form (equality chain embedded in a complete graph): exactly n passes;
+    exercises the device-side loop and grid barrier over hundreds of passes."""
+    n = 300
+    inst = I.equality_chain(n, d, embed_complete=True)
+    ctx = rac.RacContext.from_instance(inst)
+    d_in = inst.full_domains()
+    d_in[0] = U64(1)
+    st, d_out, it = ctx.enforce(d_in)
+    assert st == rac.RAC_OK and it == n and np.all(d_out == U64(1))
+    st, d_out, it = ctx.enforce(d_in, full=True)
+    assert st == rac.RAC_OK and it == n
+
+
+# ----------------------------------------------------------------------------- C1
+def test_c1_many_seeds(rac):
+    """C1: n=20, d=8, density 0.5, t=0.4 (BASELINE configs[0]); 300 instance seeds,
+    W-root, W-seed and W-rand; full removal-epoch parity."""
+    for seed in range(1, 301):
+        inst = synth.random_csp(20, 8, 0.5, 0.4, seed)
+        ctx = rac.RacContext.from_instance(inst)
+        orc = oracle.Oracle.from_instance(inst)
+        root = inst.full_domains()
+        g, o = both(ctx, orc, root)
+        assert_same(g, o, ("root", seed))
+        if o[0] == oracle.OK:
+            ds, _, _ = synth.w_seed(o[1], seed)
+            g, o2 = both(ctx, orc, ds)
+            assert_same(g, o2, ("seed", seed))
+        g, o = both(ctx, orc, synth.w_rand(inst.dom, 0.9, seed))
+        assert_same(g, o, ("rand", seed))
+
+
+# ----------------------------------------------------------------------------- C2
+@pytest.mark.parametrize("t", [0.0119, 0.3])
+def test_c2(rac, t):
+    """C2: n=500, d=20, complete graph (configs[1]); t at the phase-transition
+    estimate and a propagating t=0.3; W-root, W-seed, W-rand."""
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(t)
+    ctx = rac.RacContext.create_random(500, 20, dq, tq, 1)
+    orc = oracle.Oracle.from_synth(500, 20, dq, tq, 1)
+    root = synth.full_domains(np.full(500, 20))
+    g, o = both(ctx, orc, root)
+    assert_same(g, o, "root")
+    if o[0] == oracle.OK:
+        for k in range(3):
+            ds, _, _ = synth.w_seed(o[1], 11, k)
+            g, o2 = both(ctx, orc, ds)
+            assert_same(g, o2, ("seed", k))
+    g, o = both(ctx, orc, synth.w_rand(np.full(500, 20), 0.9, 2))
+    assert_same(g, o, "rand")
+
+
+# ----------------------------------------------------------------------------- C3
+@pytest.mark.parametrize("t,workload", [(0.5, "stream"), (0.70, "prop")])
+def test_c3(rac, t, workload):
+    """C3: n=2000, d=32, density 1 (configs[2], 512 MB of masks); W-stream (1 pass,
+    every byte read) and W-prop (about 10 passes).  Full parity incl. epochs, plus the
+    O4 certificate on the GPU's own removal epochs."""
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(t)
+    ctx = rac.RacContext.create_random(2000, 32, dq, tq, 1)
+    orc = oracle.Oracle.from_synth(2000, 32, dq, tq, 1)
+    root = synth.full_domains(np.full(2000, 32))
+    g, o = both(ctx, orc, root)
+    assert_same(g, o, workload)
+    if workload == "stream":
+        assert g[2] == 1 and np.array_equal(g[1], root)
+    else:
+        assert g[2] > 3
+    assert orc.certify(root, g[1], g[3], check_ac=(g[0] == rac.RAC_OK)) == 0
+
+
+def test_c3_virtual_shards(rac):
+    """The sharded per-pass path (row blocks, TMA-staged D, gather by device copy)
+    gives bit-identical results for 1, 2, 3 and 8 blocks at C3 shape."""
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.70)
+    ref = rac.RacContext.create_random(2000, 32, dq, tq, 1)
+    root = synth.full_domains(np.full(2000, 32))
+    r0 = ref.enforce(root, removed_at=True)
+    for v in (2, 3, 8):
+        ctx = rac.RacContext.create_random(2000, 32, dq, tq, 1, virtual_shards=v)
+        r = ctx.enforce(root, removed_at=True)
+        assert_same(r, r0, v)
+
+
+def test_virtual_shards_corpus(rac):
+    for k, inst in enumerate(I.random_corpus(200, seed0=31)):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = synth.w_rand(inst.dom, 0.9, seed=k)
+        ctx = rac.RacContext.from_instance(inst, virtual_shards=1 + k % 5)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (k, full))
+
+
+# ----------------------------------------------------------------------------- C4
+def test_c4_sampled(rac):
+    """C4 shape on one GPU: n=8000, d=64, density 1 (32.8 GB of masks, generated on
+    device).  W-stream (t=0.5): 1 pass, nothing removed.  A W-rand input at t=0.85
+    removes about half the rows in pass 1; 200 sampled rows' pass-1 verdicts are
+    checked one by one against the oracle computed straight from the generator."""
+    import torch
+    n, d = 8000, 64
+    free, _ = torch.cuda.mem_get_info()
+    if free < 36e9:
+        pytest.skip("needs ~36 GB free device memory")
+    dq = synth.quant_density(1.0)
+    ctx = rac.RacContext.create_random(n, d, dq, synth.quant_tightness(0.5), 1)
+    root = synth.full_domains(np.full(n, d))
+    st, d_out, it = ctx.enforce(root)
+    assert st == rac.RAC_OK and it == 1 and np.array_equal(d_out, root)
+    rng = np.random.default_rng(1)
+    for x, a in zip(rng.integers(0, n, 30), rng.integers(0, d, 30)):
+        assert oracle.row_supported_synth(n, d, dq, synth.quant_tightness(0.5), 1, int(x), int(a), root)
+    ctx.close()
+    del ctx
+    tq = synth.quant_tightness(0.85)
+    ctx = rac.RacContext.create_random(n, d, dq, tq, 2)
+    d_in = synth.w_rand(np.full(n, d), 0.9, 3)
+    st, d_out, it, rem = ctx.enforce(d_in, removed_at=True)
+    live = [(x, a) for x in range(n) for a in range(d) if (int(d_in[x]) >> a) & 1]
+    pick = rng.choice(len(live), 200, replace=False)
+    n_removed = 0
+    for i in pick:
+        x, a = live[i]
+        sup = oracle.row_supported_synth(n, d, dq, tq, 2, x, a, d_in)
+        assert sup == (rem[x, a] != 1), (x, a)
+        n_removed += not sup
+    assert 20 < n_removed < 180
+
+
+# ----------------------------------------------------------------------------- C5 (batched)
+def test_c5_batched(rac):
+    """C5: 1024 W-dive states on n=200, d=16, density 0.8, t=0.3 (configs[4]).  Each
+    state's (status, D_out, iterations) equals the oracle's single-state result; batch
+    composition does not matter (a permuted batch gives permuted results)."""
+    import torch
+    n, d, S = 200, 16, 1024
+    inst = synth.random_csp(n, d, 0.8, 0.3, 1)
+    orc = oracle.Oracle.from_instance(inst)
+    st0, root, _, _ = orc.rac(inst.full_domains())
+    assert st0 == oracle.OK
+
+    def enf(D):
+        s, out, _, _ = orc.rac(D, with_epochs=False)
+        return s, out
+
+    states = np.stack(synth.dive_states(root, enf, S, seed=1))
+    expect = [orc.rac(s, with_epochs=False) for s in states]
+    ctx = rac.RacContext.from_instance(inst)
+    for perm in (np.arange(S), np.random.default_rng(0).permutation(S)):
+        din = torch.from_numpy(states[perm].view(np.int64)).cuda()
+        dout = torch.zeros_like(din)
+        its = torch.zeros(S, dtype=torch.int32, device="cuda")
+        sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+        ctx.enforce_batch(S, din, dout, its, sts)
+        torch.cuda.synchronize()
+        out = dout.cpu().numpy().view(np.uint64)
+        its, sts = its.cpu().numpy(), sts.cpu().numpy()
+        for j, s in enumerate(perm):
+            e = expect[s]
+            assert (sts[j], its[j]) == (e[0], e[2]), (s, sts[j], its[j], e[0], e[2])
+            assert np.array_equal(out[j], e[1]), s
+    iters = np.array([e[2] for e in expect])
+    assert iters.max() > 3 and any(e[0] == oracle.WIPEOUT for e in expect)
+
+
+def test_async_api_and_in_place(rac):
+    """rac_enforce_async on torch device buffers and a torch stream; d_out == d_in."""
+    import torch
+    inst = synth.random_csp(150, 12, 0.6, 0.45, 4)
+    orc = oracle.Oracle.from_instance(inst)
+    ctx = rac.RacContext.from_instance(inst)
+    d_in = synth.w_rand(inst.dom, 0.9, 5)
+    o = orc.rac(d_in)
+    buf = torch.from_numpy(d_in.view(np.int64).copy()).cuda()
+    it = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rem = torch.zeros(150 * 64, dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx.enforce_async(buf, buf, it, st, rem, stream=s)
+    s.synchronize()
+    assert int(st.item()) == o[0] and int(it.item()) == o[2]
+    assert np.array_equal(buf.cpu().numpy().view(np.uint64), o[1])
+    assert np.array_equal(rem.cpu().numpy().reshape(150, 64), o[3])
+    assert ctx.last_launch_count >= 1
+
+
+def test_input_padding_bits_rejected(rac):
+    inst = synth.random_csp(5, 3, 1.0, 0.3, 1)
+    ctx = rac.RacContext.from_instance(inst)
+    bad = inst.full_domains()
+    bad[2] |= U64(1 << 5)
+    with pytest.raises(rac.RacError) as ei:
+        ctx.enforce(bad)
+    assert ei.value.code == rac.RAC_EINVAL
+    # the context stays usable after EINVAL
+    assert ctx.enforce(inst.full_domains())[0] in (rac.RAC_OK, rac.RAC_WIPEOUT)
