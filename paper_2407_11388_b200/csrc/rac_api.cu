@@ -221,7 +221,7 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   const long rows = (long)n * c->dmax;
   const long groups_per_cta = (kThreads / 32) * (32 / c->G);
   int occ = 0;
-  CKC(fused_occupancy(c->W, c->G, c->row_stride, &occ));
+  CKC(fused_occupancy(c->W, c->G, fused_smem(c->nvec), &occ));
   if (occ < 1) return fail(nullptr, RAC_EUNSUPPORTED, "support-pass kernel does not fit on an SM (n too large)");
   long want = (rows + groups_per_cta - 1) / groups_per_cta;
   c->fused_grid = (int)std::max(1L, std::min((long)c->sm_count * occ, want));
@@ -290,7 +290,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   // last pass or is the initial zero fill... clear it explicitly (tiny).
   CK(c, cudaMemsetAsync(c->R3 + (size_t)1 * c->n, 0, (size_t)c->n * 8, s));
   c->launches++;
-  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, c->row_stride, s, c->fused_grid > 1));
+  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, fused_smem(c->nvec), s, c->fused_grid > 1));
   c->launches++;
   return 0;
 }
@@ -545,7 +545,7 @@ int rac_enforce_batch(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   p.iters = iterations_dev;
   p.status = status_dev;
   p.flags = flags;
-  const size_t smem = c->row_stride + (size_t)c->n * 8;
+  const size_t smem = fused_smem(c->nvec) + (size_t)c->n * 8;
   int occ = 0;
   CK(c, batch_occupancy(c->W, c->G, smem, &occ));
   if (occ < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");

@@ -80,6 +80,16 @@ struct BatchParams {
   uint32_t flags;
 };
 
+// Dynamic smem of rac_fused / rac_batch: D (nvec x 16 B), then the incremental
+// vector list (u16[nvec]) and the per-vector "needed" flags (u8[nvec]).
+__host__ __device__ constexpr size_t list_offset(int nvec) { return (size_t)nvec * 16; }
+__host__ __device__ constexpr size_t need_offset(int nvec) {
+  return (size_t)nvec * 16 + (((size_t)nvec * 2 + 15) & ~(size_t)15);
+}
+__host__ __device__ constexpr size_t fused_smem(int nvec) {
+  return need_offset(nvec) + (((size_t)nvec + 15) & ~(size_t)15);
+}
+
 // ---------------------------------------------------------------------------- host launchers
 // (defined in rac_kernels.cu / rac_pack.cu; return cudaError_t of the launch)
 int choose_group(int nvec);  // lanes per row
@@ -219,6 +229,74 @@ __device__ __forceinline__ bool row_fails(const uint4* __restrict__ row, const u
     if (group_any<G>(fail, gmask)) return true;
   }
   return false;
+}
+
+// As row_fails, but only over the 16-byte vectors listed in vl[lb, le)
+// (Prop. 2: after pass 1 a row can only lose support
+// on a constraint whose other variable changed in the previous pass, so only
+// the vectors holding masks of changed variables are re-tested).
+template <int W, int G>
+__device__ __forceinline__ bool row_fails_list(const uint4* __restrict__ row, const uint4* Ds, const uint16_t* vl,
+                                               int lb, int le, int gl, unsigned gmask, int n,
+                                               const uint32_t* Prow) {
+  bool fail = false;
+  for (int i0 = lb; i0 < le; i0 += G * kUnroll) {
+    uint4 m[kUnroll];
+    int vv[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int i = i0 + u * G + gl;
+      vv[u] = i < le ? (int)vl[i] : -1;
+      if (vv[u] >= 0) m[u] = ldg_stream(row + vv[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (vv[u] >= 0) {
+        uint4 d = Ds[vv[u]];
+        if (vec_any_zero<W>(and4(m[u], d))) fail |= vec_real_fail<W>(m[u], d, vv[u], n, Prow);
+      }
+    }
+    if (group_any<G>(fail, gmask)) return true;
+  }
+  return false;
+}
+
+// Block-wide compaction of the flags need[0, cnt) into the ascending index
+// list out[]; clears need[].  Returns the list length (same in every thread).
+__device__ __forceinline__ int block_compact(uint8_t* need, uint16_t* out, int cnt, int* scratch) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const int chunk = (cnt + T - 1) / T;
+  const int b = min(cnt, t * chunk), e = min(cnt, b + chunk);
+  int c = 0;
+  for (int i = b; i < e; ++i) c += need[i] != 0;
+  // inclusive scan over threads: warp shuffles, then warp totals in scratch
+  const int lane = t & 31, w = t >> 5;
+  int v = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) scratch[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int s = lane < (T >> 5) ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += u;
+    }
+    if (lane < (T >> 5)) scratch[lane] = s;  // inclusive warp prefix
+  }
+  __syncthreads();
+  int pos = v - c + (w > 0 ? scratch[w - 1] : 0);
+  for (int i = b; i < e; ++i) {
+    if (need[i]) out[pos++] = (uint16_t)i;
+    need[i] = 0;
+  }
+  const int total = scratch[(T >> 5) - 1];
+  __syncthreads();
+  return total;
 }
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {

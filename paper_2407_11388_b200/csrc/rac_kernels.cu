@@ -54,30 +54,37 @@ __device__ __forceinline__ GroupIds group_ids() {
 
 // Test the rows of variables [g.x_lo, g.x_hi) assigned to this group (static
 // round-robin over (row, segment) items) and record removals into R.
+// vl == nullptr: stream every vector of the row; else only the listed
+// vectors (vl[0, vcnt), Prop. 2 incremental pass).
 template <int W, int G>
 __device__ __forceinline__ void support_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
                                               int32_t* removed_at, int t, long item0, long istep,
-                                              const GroupIds& id) {
+                                              const GroupIds& id, const uint16_t* vl, int vcnt) {
   const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
   const long rows = (long)(g.x_hi - g.x_lo) * g.dmax;
-  const long n_items = rows * g.n_seg;
+  const int n_seg = vl ? 1 : g.n_seg;
+  const long n_items = rows * n_seg;
   const long row0 = (long)(g.x_lo - g.x_lo_alloc) * g.dmax;
   for (long it = item0; it < n_items; it += istep) {
     long r, s;
-    if (g.n_seg == 1) { r = it; s = 0; } else { r = it / g.n_seg; s = it - r * g.n_seg; }
+    if (n_seg == 1) { r = it; s = 0; } else { r = it / n_seg; s = it - r * n_seg; }
     const int xl = (int)(r / g.dmax);
     const int a = (int)(r - (long)xl * g.dmax);
     const int x = g.x_lo + xl;
     if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;  // dead row: (x,a) ∉ D_{t-1}
     const uint4* row = reinterpret_cast<const uint4*>(g.M + (size_t)(row0 + r) * g.row_stride);
-    const int vb = (int)s * g.seg_vecs;
-    const int ve = min(vb + g.seg_vecs, g.nvec);
     const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
-    if (row_fails<W, G>(row, Ds, vb, ve, id.gl, id.gmask, g.n, Prow)) {
-      if (id.gl == 0) {
-        atomicOr(&R[x], 1ull << a);
-        if (removed_at) removed_at[(size_t)x * 64 + a] = t;
-      }
+    bool f;
+    if (vl) {
+      f = row_fails_list<W, G>(row, Ds, vl, 0, vcnt, id.gl, id.gmask, g.n, Prow);
+    } else {
+      const int vb = (int)s * g.seg_vecs;
+      const int ve = min(vb + g.seg_vecs, g.nvec);
+      f = row_fails<W, G>(row, Ds, vb, ve, id.gl, id.gmask, g.n, Prow);
+    }
+    if (f && id.gl == 0) {
+      atomicOr(&R[x], 1ull << a);
+      if (removed_at) removed_at[(size_t)x * 64 + a] = t;
     }
   }
 }
@@ -97,12 +104,16 @@ __device__ __forceinline__ void stage_from_u64(uint4* Ds, const uint64_t* src, c
 template <int W, int G>
 __global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
   extern __shared__ uint4 Ds[];
+  __shared__ int scratch[kThreads / 32];
   const PassGeom& g = p.g;
+  uint16_t* vlist = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(Ds) + list_offset(g.nvec));
+  uint8_t* vneed = reinterpret_cast<uint8_t*>(Ds) + need_offset(g.nvec);
+  for (int i = threadIdx.x; i < g.nvec; i += blockDim.x) vneed[i] = 0;
   stage_from_u64<W>(Ds, p.d_in, p.dommask, g.n, g.nvec);
   uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
   const GroupIds id = group_ids<G>();
   const bool full = (p.flags & kFull) != 0;
-  int t = 0, status = kOK;
+  int t = 0, status = kOK, vcnt = g.nvec;
   unsigned epoch = 0;
   for (;;) {
     ++t;
@@ -110,7 +121,10 @@ __global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
     unsigned long long* Rn = p.R + (size_t)((t + 1) % 3) * g.n;
     // R of pass t+1 was last read before the previous barrier: clear it now.
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
-    support_sweep<W, G>(g, Ds, Rc, p.removed_at, t, id.gidx, id.ngroups, id);
+    // pass 1 (and any pass where many variables changed) streams whole rows;
+    // otherwise only the vectors of variables changed in the previous pass.
+    const bool use_list = t > 1 && 2 * vcnt <= g.nvec && g.nvec <= 65535;
+    support_sweep<W, G>(g, Ds, Rc, p.removed_at, t, id.gidx, id.ngroups, id, use_list ? vlist : nullptr, vcnt);
     grid_sync(p.bar, gridDim.x, ++epoch);
     // D_t = D_{t-1} & ~R (every CTA, redundantly); flags for Alg. 1's checks.
     int changed = 0, wipe = 0;
@@ -119,11 +133,14 @@ __global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
       const uint64_t dv = load_w<W>(Db + x * W);
       const uint64_t nd = dv & ~r;
       store_w<W>(Db + x * W, nd);
-      changed |= (dv & r) != 0;
+      const bool chx = (dv & r) != 0;
+      changed |= chx;
       wipe |= nd == 0;
+      if (chx) vneed[(x * W) >> 4] = 1;
     }
     changed = __syncthreads_or(changed);
     wipe = __syncthreads_or(wipe);
+    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
     if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
     if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
   }
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2) rac_pass(PassParams p) {
   tma_stage(Ds, p.s.Dw, (uint32_t)p.g.row_stride, &mbar);
   const int t = *p.s.iters + 1;
   const GroupIds id = group_ids<G>();
-  support_sweep<W, G>(p.g, Ds, p.s.R, p.removed_at, t, id.gidx, id.ngroups, id);
+  support_sweep<W, G>(p.g, Ds, p.s.R, p.removed_at, t, id.gidx, id.ngroups, id, nullptr, 0);
 }
 
 __global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
@@ -264,9 +281,13 @@ __global__ void rac_shard_finalize(ShardState s, int n, uint64_t* d_out, int32_t
 template <int W, int G>
 __global__ void __launch_bounds__(kThreads, 2) rac_batch(BatchParams p) {
   extern __shared__ uint4 Ds[];
+  __shared__ int scratch[kThreads / 32];
   const PassGeom& g = p.g;
   const int s = blockIdx.x;
-  unsigned long long* R = reinterpret_cast<unsigned long long*>(Ds + g.nvec);
+  uint16_t* vlist = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(Ds) + list_offset(g.nvec));
+  uint8_t* vneed = reinterpret_cast<uint8_t*>(Ds) + need_offset(g.nvec);
+  unsigned long long* R = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(Ds) + fused_smem(g.nvec));
+  for (int i = threadIdx.x; i < g.nvec; i += blockDim.x) vneed[i] = 0;
   stage_from_u64<W>(Ds, p.d_in + (size_t)s * g.n, p.dommask, g.n, g.nvec);
   uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gw = lane / G;
@@ -276,20 +297,22 @@ __global__ void __launch_bounds__(kThreads, 2) rac_batch(BatchParams p) {
   id.gidx = warp * (32 / G) + gw;
   id.ngroups = (long)(blockDim.x / 32) * (32 / G);
   const bool full = (p.flags & kFull) != 0;
-  int t = 0, status = kOK;
+  int t = 0, status = kOK, vcnt = g.nvec;
   for (;;) {
     ++t;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) R[x] = 0ull;
     __syncthreads();
-    // R in smem: atomicOr on shared u64
+    const bool use_list = t > 1 && 2 * vcnt <= g.nvec && g.nvec <= 65535;
     {
       const long rows = (long)g.n * g.dmax;
       for (long r = id.gidx; r < rows; r += id.ngroups) {
         const int x = (int)(r / g.dmax), a = (int)(r - (long)x * g.dmax);
         if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;
         const uint4* row = reinterpret_cast<const uint4*>(g.M + (size_t)r * g.row_stride);
-        if (row_fails<W, G>(row, Ds, 0, g.nvec, id.gl, id.gmask, g.n, g.P + (size_t)x * g.pw))
-          if (id.gl == 0) atomicOr(&R[x], 1ull << a);
+        const uint32_t* Prow = g.P + (size_t)x * g.pw;
+        const bool f = use_list ? row_fails_list<W, G>(row, Ds, vlist, 0, vcnt, id.gl, id.gmask, g.n, Prow)
+                                : row_fails<W, G>(row, Ds, 0, g.nvec, id.gl, id.gmask, g.n, Prow);
+        if (f && id.gl == 0) atomicOr(&R[x], 1ull << a);  // shared-memory u64 atomic
       }
     }
     __syncthreads();
@@ -299,11 +322,14 @@ __global__ void __launch_bounds__(kThreads, 2) rac_batch(BatchParams p) {
       const uint64_t dv = load_w<W>(Db + x * W);
       const uint64_t nd = dv & ~r;
       store_w<W>(Db + x * W, nd);
-      changed |= (dv & r) != 0;
+      const bool chx = (dv & r) != 0;
+      changed |= chx;
       wipe |= nd == 0;
+      if (chx) vneed[(x * W) >> 4] = 1;
     }
     changed = __syncthreads_or(changed);
     wipe = __syncthreads_or(wipe);
+    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
     if (wipe && !full) { status = kWIPEOUT; break; }
     if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }
   }
