@@ -77,6 +77,11 @@ def _load():
         lib.orc_row_supported_synth.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
                                                 ctypes.c_uint64, ctypes.c_int, ctypes.c_int, u64p]
         lib.orc_row_supported_synth.restype = ctypes.c_int
+        lib.orc_build_synth_block.restype = P
+        lib.orc_build_synth_block.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
+                                              ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
+        lib.orc_pass_block.restype = ctypes.c_int64
+        lib.orc_pass_block.argtypes = [P, u64p, ctypes.c_int, ctypes.c_int, u64p]
         lib.orc_domain_size.argtypes = [P, u64p]
         lib.orc_domain_size.restype = ctypes.c_int64
         _lib = lib
@@ -121,6 +126,24 @@ class Oracle:
         if not h:
             raise ValueError("invalid synth parameters")
         return cls(h, n, np.full(n, d, dtype=np.int32))
+
+    @classmethod
+    def from_synth_block(cls, n: int, d: int, dens_q32: int, t_q16: int, seed: int, x_lo: int, x_hi: int):
+        """Arcs of variables [x_lo, x_hi) only (sampled timing at C4 size); use pass_block only."""
+        lib = _load()
+        h = lib.orc_build_synth_block(n, d, dens_q32, t_q16, seed, x_lo, x_hi)
+        if not h:
+            raise ValueError("invalid synth parameters")
+        o = cls(h, n, np.full(n, d, dtype=np.int32))
+        o.block = (x_lo, x_hi)
+        return o
+
+    def pass_block(self, D, x_lo: int, x_hi: int):
+        """One Eq. 1 step for rows of [x_lo, x_hi): (new words, number removed)."""
+        D = np.ascontiguousarray(D, dtype=np.uint64)
+        out = np.zeros(max(x_hi - x_lo, 1), dtype=np.uint64)
+        r = _load().orc_pass_block(self._h, _u64p(D), x_lo, x_hi, _u64p(out))
+        return out[: x_hi - x_lo], int(r)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

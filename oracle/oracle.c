@@ -224,6 +224,71 @@ orc_csp *orc_build_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64
   return c;
 }
 
+/*
+ * Partial build for sampled CPU timing at sizes the full oracle instance does
+ * not fit (C4): arcs only for variables x in [x_lo, x_hi) (all their
+ * neighbours y), other variables get no arcs.  Only orc_pass_block may be used
+ * on it.
+ */
+orc_csp *orc_build_synth_block(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed, int x_lo, int x_hi) {
+  if (n < 1 || d < 1 || d > 64 || x_lo < 0 || x_hi > n || x_lo > x_hi) return NULL;
+  int *dom = (int *)malloc((size_t)n * sizeof(int));
+  for (int x = 0; x < n; ++x) dom[x] = d;
+  orc_csp *c = alloc_csp(n, dom);
+  free(dom);
+  if (!c) return NULL;
+  for (int x = x_lo; x < x_hi; ++x)
+    for (int y = 0; y < n; ++y) {
+      if (y == x) continue;
+      int lo = x < y ? x : y, hi = x < y ? y : x;
+      if (synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) c->deg[x]++;
+    }
+  if (alloc_arcs(c)) { orc_free(c); return NULL; }
+  for (int x = x_lo; x < x_hi; ++x) {
+    int k = 0;
+    for (int y = 0; y < n; ++y) {
+      if (y == x) continue;
+      int lo = x < y ? x : y, hi = x < y ? y : x;
+      if (!synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) continue;
+      c->nbr[x][k] = y;
+      if (x < y) {
+        for (int a = 0; a < d; ++a)
+          c->sup[x][(size_t)k * d + a] =
+              synth_row(seed, (uint32_t)n, (uint32_t)d, (uint32_t)x, (uint32_t)y, (uint32_t)a, t_q16);
+      } else {
+        for (int b = 0; b < d; ++b) {
+          uint64_t row_b = synth_row(seed, (uint32_t)n, (uint32_t)d, (uint32_t)y, (uint32_t)x, (uint32_t)b, t_q16);
+          for (int a = 0; a < d; ++a)
+            if ((row_b >> a) & 1ULL) c->sup[x][(size_t)k * d + a] |= 1ULL << b;
+        }
+      }
+      ++k;
+    }
+  }
+  return c;
+}
+
+/*
+ * One step of Eq. 1 restricted to the rows of variables [x_lo, x_hi):
+ * out[x - x_lo] = { a ∈ D(x) : ∀ c_xy ∈ C_x  c_xy|(x,a) ∩ D(y) ≠ ∅ }.
+ * Same loop as orc_rac's step.  Returns the number of values removed.
+ */
+int64_t orc_pass_block(const orc_csp *c, const uint64_t *D, int x_lo, int x_hi, uint64_t *out) {
+  int64_t removed = 0;
+  for (int x = x_lo; x < x_hi; ++x) {
+    uint64_t nx = D[x];
+    for (int a = 0; a < c->dom[x]; ++a) {
+      if (!((D[x] >> a) & 1ULL)) continue;
+      for (int kk = 0; kk < c->deg[x]; ++kk) {
+        int y = c->nbr[x][kk];
+        if ((c->sup[x][(size_t)kk * c->dom[x] + a] & D[y]) == 0) { nx &= ~(1ULL << a); ++removed; break; }
+      }
+    }
+    out[x - x_lo] = nx;
+  }
+  return removed;
+}
+
 int orc_n(const orc_csp *c) { return c->n; }
 int orc_degree(const orc_csp *c, int x) { return c->deg[x]; }
 

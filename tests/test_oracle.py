@@ -372,3 +372,17 @@ def test_generator_statistics():
     cells = m * 16 * 16
     assert abs(bits / cells - 0.75) < 0.01
     assert synth.random_csp(3, 4, 1.0, 0.5, seed=1).n_rel == 3
+
+
+def test_pass_block_matches_one_step():
+    """The block-restricted step (used for sampled CPU timing) equals one O1 step."""
+    n, d, p, t, seed = 40, 9, 0.8, 0.5, 12
+    inst = synth.random_csp(n, d, p, t, seed)
+    D = synth.w_rand(inst.dom, 0.85, seed=3)
+    st, d1, it, rem = oracle.Oracle.from_instance(inst).rac(D)
+    blk = oracle.Oracle.from_synth_block(n, d, synth.quant_density(p), synth.quant_tightness(t), seed, 7, 23)
+    out, removed = blk.pass_block(D, 7, 23)
+    for x in range(7, 23):
+        expect = int(D[x]) & ~sum(1 << a for a in range(64) if rem[x, a] == 1)
+        assert int(out[x - 7]) == expect
+    assert removed == int(np.sum(rem[7:23] == 1))
