@@ -157,6 +157,34 @@ int rac_enforce_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d_out_de
 int rac_enforce_batch(rac_ctx* ctx, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                       int32_t* iterations_dev, int32_t* status_dev, uint32_t flags, void* stream);
 
+/* Seeded (incremental) enforcement: Alg. 1 tensorAC(Vars, @changed = seeds)
+ * (P:198-221), the paper's per-assignment call tensorAC(Vars, [idx]).
+ * PRECONDITION: d_in is arc consistent on every constraint c_xy whose y is not
+ * a seed -- e.g. the D_ac of a parent search node after the seed variables'
+ * domains were reduced (an assignment).  Under it the result
+ * (status, d_out, iterations) equals rac_enforce(d_in): by Prop. 2
+ * the trajectory is the same, but pass 1 reads only the masks of the seed
+ * variables instead of the whole relation tensor.  Without the precondition the
+ * result is sound (every removal is justified by Lemma 1) but may keep values
+ * D_ac removes.  n_seeds == 0: no pass, iterations = 0, status RAC_WIPEOUT iff
+ * some domain of d_in is empty.  seeds: host int32[n_seeds], each in [0, n). */
+int rac_enforce_seeded(rac_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations,
+                       const int32_t* seeds, int32_t n_seeds, uint32_t flags);
+
+/* As rac_enforce_seeded, device buffers (seeds_dev: device int32[n_seeds]),
+ * asynchronous on `stream` like rac_enforce_async. */
+int rac_enforce_seeded_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d_out_dev, int32_t* iterations_dev,
+                             int32_t* status_dev, const int32_t* seeds_dev, int32_t n_seeds, uint32_t flags,
+                             void* stream);
+
+/* Batched seeded enforcement: state s is seeded with the single variable
+ * seed_var_dev[s] (device int32[n_states]; -1 = all variables, i.e. a root
+ * call), under the precondition above (search-tree children after one
+ * assignment each).  Results equal rac_enforce of each state alone. */
+int rac_enforce_batch_seeded(rac_ctx* ctx, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                             int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev,
+                             uint32_t flags, void* stream);
+
 /* ---- introspection ------------------------------------------------------ */
 int32_t rac_n_vars(const rac_ctx* ctx);
 int32_t rac_max_dom(const rac_ctx* ctx);

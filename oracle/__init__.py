@@ -12,6 +12,8 @@ Contents
     O4 certificate (Lemma 1, lines 79-82).
   * ``brute_force_dac`` -- O3: D_ac as the union of all arc-consistent subsets
     of D, by enumerating every subset (tiny inputs).
+  * ``Oracle.rac_seeded`` -- O5: Alg. 1 tensorAC(Vars, @changed) as written
+    (lines 198-221), the paper's incremental per-assignment call (line 392).
   * ``rac_python`` -- a pure-Python transcription of Eq. 1 (tiny inputs), used
     to cross-check the C transcription.
 
@@ -64,6 +66,8 @@ def _load():
         lib.orc_free.restype = None
         lib.orc_rac.argtypes = [P, u64p, u64p, i32p, i32p, ctypes.c_int]
         lib.orc_rac.restype = ctypes.c_int
+        lib.orc_rac_seeded.argtypes = [P, u64p, i32p, ctypes.c_int, u64p, i32p, i32p, ctypes.c_int]
+        lib.orc_rac_seeded.restype = ctypes.c_int
         lib.orc_ac3.argtypes = [P, u64p, u64p, ctypes.POINTER(ctypes.c_int64)]
         lib.orc_ac3.restype = ctypes.c_int
         lib.orc_is_ac.argtypes = [P, u64p]
@@ -159,6 +163,18 @@ class Oracle:
         rem = np.zeros(self.n * 64, dtype=np.int32) if with_epochs else None
         st = lib.orc_rac(self._h, _u64p(d_in), _u64p(d_out), _i32p(it),
                          _i32p(rem) if rem is not None else None, 1 if full else 0)
+        return st, d_out, int(it[0]), (rem.reshape(self.n, 64) if rem is not None else None)
+
+    def rac_seeded(self, d_in, seeds, full: bool = False, with_epochs: bool = True):
+        """O5: Alg. 1 tensorAC(Vars, @changed = seeds) as written.  Returns like rac()."""
+        lib = _load()
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int32).reshape(-1))
+        d_out = np.zeros(self.n, dtype=np.uint64)
+        it = np.zeros(1, dtype=np.int32)
+        rem = np.zeros(self.n * 64, dtype=np.int32) if with_epochs else None
+        st = lib.orc_rac_seeded(self._h, _u64p(d_in), _i32p(seeds) if seeds.size else None, int(seeds.size),
+                                _u64p(d_out), _i32p(it), _i32p(rem) if rem is not None else None, 1 if full else 0)
         return st, d_out, int(it[0]), (rem.reshape(self.n, 64) if rem is not None else None)
 
     def ac3(self, d_in):

@@ -378,6 +378,67 @@ int orc_rac(const orc_csp *c, const uint64_t *d_in, uint64_t *d_out, int *iterat
 }
 
 /*
+ * O5: Alg. 1 tensorAC(Vars, @changed) as written:
+ *   while |@changed| != 0:
+ *     Vars = tensorRevise(Vars, @changed)   -- (x,a) kept iff for every y in
+ *         @changed (with a declared c_xy, reading R2) c_xy|(x,a) ∩ D(y) ≠ ∅
+ *     if some #Vals == 0: inconsistency      -- checked first (R5)
+ *     @changed = { x : #Vals(x) != #Vals_pre(x) }
+ * seeds = the initial @changed (P:392 calls it with [idx] after an
+ * assignment; the root call P:381 passes all variables).  An empty seed list
+ * runs no pass (iterations = 0).  Same outputs as orc_rac.
+ */
+int orc_rac_seeded(const orc_csp *c, const uint64_t *d_in, const int32_t *seeds, int n_seeds, uint64_t *d_out,
+                   int *iterations, int32_t *removed_at, int full) {
+  int n = c->n;
+  uint64_t *prev = (uint64_t *)calloc((size_t)n, sizeof(uint64_t));
+  uint64_t *next = (uint64_t *)calloc((size_t)n, sizeof(uint64_t));
+  char *chg = (char *)calloc((size_t)n, 1);
+  memcpy(prev, d_in, (size_t)n * sizeof(uint64_t));
+  if (removed_at) memset(removed_at, 0, (size_t)n * 64 * sizeof(int32_t));
+  int n_chg = 0;
+  for (int i = 0; i < n_seeds; ++i)
+    if (seeds[i] >= 0 && seeds[i] < n && !chg[seeds[i]]) { chg[seeds[i]] = 1; ++n_chg; }
+  int k = 0, status = ORC_OK;
+  while (n_chg != 0) {
+    ++k;
+    for (int x = 0; x < n; ++x) {
+      next[x] = prev[x];
+      for (int a = 0; a < c->dom[x]; ++a) {
+        if (!((prev[x] >> a) & 1ULL)) continue;
+        for (int kk = 0; kk < c->deg[x]; ++kk) {
+          int y = c->nbr[x][kk];
+          if (!chg[y]) continue; /* Cons[*, @changed] only */
+          if ((c->sup[x][(size_t)kk * c->dom[x] + a] & prev[y]) == 0) {
+            next[x] &= ~(1ULL << a);
+            if (removed_at) removed_at[x * 64 + a] = k;
+            break;
+          }
+        }
+      }
+    }
+    int wipe = 0;
+    n_chg = 0;
+    for (int x = 0; x < n; ++x) {
+      if (next[x] == 0) wipe = 1;
+      chg[x] = next[x] != prev[x];
+      n_chg += chg[x];
+    }
+    memcpy(prev, next, (size_t)n * sizeof(uint64_t));
+    if (wipe && !full) { status = ORC_WIPEOUT; break; }
+    if (n_chg == 0 && wipe) status = ORC_WIPEOUT;
+  }
+  if (k == 0) {
+    for (int x = 0; x < n; ++x)
+      if (prev[x] == 0) status = ORC_WIPEOUT;
+  }
+  memcpy(d_out, prev, (size_t)n * sizeof(uint64_t));
+  *iterations = k;
+  free(prev); free(next); free(chg);
+  return status;
+}
+
+/*
  * O2: AC-3 ("a propagation queue and a revision process";
  * SPEC.md ac3_engine lines 283-299).  FIFO queue of directed arcs (x,y),
  * initially every arc in ascending (x, y) order; revise(x,y) removes every

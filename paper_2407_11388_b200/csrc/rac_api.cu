@@ -80,6 +80,8 @@ struct rac_ctx {
   uint64_t* buf_out = nullptr;
   int32_t* buf_scalars = nullptr;  // [iters, status]
   int32_t* buf_removed = nullptr;  // [n*64]
+  int32_t* buf_seeds = nullptr;    // [seed_cap]
+  size_t seed_cap = 0;
   uint64_t* h_in = nullptr;        // pinned
   uint64_t* h_out = nullptr;
   int32_t* h_scalars = nullptr;    // pinned [iters, status, done]
@@ -133,10 +135,12 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->sh.Dw);
   cudaFree(c->sh.R);
   cudaFree(c->sh.iters);
+  cudaFree(c->sh.vlist);
   cudaFree(c->buf_in);
   cudaFree(c->buf_out);
   cudaFree(c->buf_scalars);
   cudaFree(c->buf_removed);
+  cudaFree(c->buf_seeds);
   cudaFreeHost(c->h_in);
   cudaFreeHost(c->h_out);
   cudaFreeHost(c->h_scalars);
@@ -208,6 +212,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   CKC(cudaMalloc(&c->sh.iters, 16));
   c->sh.status = c->sh.iters + 1;
   c->sh.done = c->sh.iters + 2;
+  c->sh.vcnt = c->sh.iters + 3;
+  CKC(cudaMalloc(&c->sh.vlist, (size_t)c->nvec * 2 + 16));
   CKC(cudaMalloc(&c->buf_in, (size_t)n * 8));
   CKC(cudaMalloc(&c->buf_out, (size_t)n * 8));
   CKC(cudaMalloc(&c->buf_scalars, 16));
@@ -226,7 +232,7 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   long want = (rows + groups_per_cta - 1) / groups_per_cta;
   c->fused_grid = (int)std::max(1L, std::min((long)c->sm_count * occ, want));
   int pocc = 0;
-  CKC(pass_occupancy(c->W, c->G, c->row_stride, &pocc));
+  CKC(pass_occupancy(c->W, c->G, fused_smem(c->nvec), &pocc));
   c->pass_grid = c->sm_count * std::max(1, pocc);
   CKC(cudaStreamSynchronize(c->stream));
 #undef CKC
@@ -269,7 +275,8 @@ int check_usable(rac_ctx* c) {
 }
 
 int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
-                  int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+                  int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
+                  int n_seeds = 0) {
   FusedParams p{};
   const long ngroups = (long)c->fused_grid * (kThreads / 32) * (32 / c->G);
   p.g = geom_for(c, 0, c->n, ngroups);
@@ -282,14 +289,11 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.R = c->R3;
   p.bar = c->bar;
   p.flags = flags;
-  if (removed_at) {
-    CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
-    c->launches++;
-  }
-  // R of pass 1 must be clear: R[1] was cleared during the previous call's
-  // last pass or is the initial zero fill... clear it explicitly (tiny).
-  CK(c, cudaMemsetAsync(c->R3 + (size_t)1 * c->n, 0, (size_t)c->n * 8, s));
-  c->launches++;
+  p.seeds = seeds;
+  p.n_seeds = n_seeds;
+  if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
+  // R[1] (pass 1's removal buffer) is clean: zeroed at create and by the last
+  // CTA of every previous launch.
   CK(c, launch_fused(c->W, c->G, p, c->fused_grid, fused_smem(c->nvec), s, c->fused_grid > 1));
   c->launches++;
   return 0;
@@ -299,10 +303,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
                     int32_t* removed_at, uint32_t flags, cudaStream_t s) {
   if (removed_at && c->world > 1) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
   const int total_g = c->world * c->blk;
-  if (removed_at) {
-    CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
-    c->launches++;
-  }
+  if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
   CK(c, launch_shard_init(c->sh, d_in, c->dommask, c->n, c->W, c->row_stride, total_g, s));
   c->launches++;
   const long ngroups = (long)c->pass_grid * (kThreads / 32) * (32 / c->G);
@@ -323,7 +324,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
     for (int k = 0; k < chunk; ++k) {
       for (int b = 0; b < nb; ++b) {
         if (pp[b].g.x_hi <= pp[b].g.x_lo) continue;
-        CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, c->row_stride, s));
+        CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, fused_smem(c->nvec), s));
         c->launches++;
       }
       if (c->world > 1) {
@@ -334,12 +335,11 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
         if (r != 0)
           return fail(c, RAC_ENCCL, std::string("ncclAllGather: ") +
                                         (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
-        c->launches++;
       } else {
         CK(c, launch_shard_slice(c->sh, 0, c->n, c->n, s));
         c->launches++;
       }
-      CK(c, launch_shard_update(c->sh, c->n, c->W, flags, s));
+      CK(c, launch_shard_update(c->sh, c->n, c->W, c->nvec, flags, s));
       c->launches++;
     }
     enq += chunk;
@@ -355,12 +355,19 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
 }
 
 int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
-                       int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+                       int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
+                       int n_seeds = -1) {
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
-  if (c->world > 1 || c->vshards > 1) return enforce_sharded(c, d_in, d_out, iters, status, removed_at, flags, s);
-  return enforce_fused(c, d_in, d_out, iters, status, removed_at, flags, s);
+  if (c->world > 1 || c->vshards > 1) {
+    // the sharded driver has no seeded pass 1: a full pass 1 is the superset
+    // check (valid under the precondition; identical trajectory, Prop. 2)
+    if (n_seeds == 0) return fail(c, RAC_EUNSUPPORTED, "empty seed list on the sharded path");
+    return enforce_sharded(c, d_in, d_out, iters, status, removed_at, flags, s);
+  }
+  return enforce_fused(c, d_in, d_out, iters, status, removed_at, flags, s, n_seeds >= 0 ? seeds : nullptr,
+                       n_seeds >= 0 ? n_seeds : 0);
 }
 
 }  // namespace
@@ -524,8 +531,71 @@ int rac_enforce(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iter
   return rac_enforce_ex(c, d_in, d_out, iterations, nullptr, 0u);
 }
 
+int rac_enforce_seeded_async(rac_ctx* c, const uint64_t* d_in_dev, uint64_t* d_out_dev, int32_t* iterations_dev,
+                             int32_t* status_dev, const int32_t* seeds_dev, int32_t n_seeds, uint32_t flags,
+                             void* stream) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev || n_seeds < 0 || (n_seeds > 0 && !seeds_dev))
+    return fail(c, RAC_EINVAL, "bad seeded-enforcement arguments");
+  return enforce_async_impl(c, d_in_dev, d_out_dev, iterations_dev, status_dev, nullptr, flags,
+                            (cudaStream_t)stream, seeds_dev, n_seeds);
+}
+
+int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations, const int32_t* seeds,
+                       int32_t n_seeds, uint32_t flags) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (!d_in || !d_out || !iterations || n_seeds < 0 || (n_seeds > 0 && !seeds))
+    return fail(c, RAC_EINVAL, "bad seeded-enforcement arguments");
+  for (int i = 0; i < n_seeds; ++i)
+    if (seeds[i] < 0 || seeds[i] >= c->n) return fail(c, RAC_EINVAL, "seed out of range");
+  for (int x = 0; x < c->n; ++x)
+    if (d_in[x] & ~c->dommask_h[x]) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
+  CK(c, cudaSetDevice(c->device));
+  const size_t nb = (size_t)c->n * 8;
+  if ((size_t)n_seeds > c->seed_cap) {
+    cudaFree(c->buf_seeds);
+    c->buf_seeds = nullptr;
+    CK(c, cudaMalloc(&c->buf_seeds, (size_t)n_seeds * 4));
+    c->seed_cap = (size_t)n_seeds;
+  }
+  memcpy(c->h_in, d_in, nb);
+  CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb, cudaMemcpyHostToDevice, c->stream));
+  if (n_seeds > 0)
+    CK(c, cudaMemcpyAsync(c->buf_seeds, seeds, (size_t)n_seeds * 4, cudaMemcpyHostToDevice, c->stream));
+  rc = enforce_async_impl(c, c->buf_in, c->buf_out, c->buf_scalars, c->buf_scalars + 1, nullptr, flags, c->stream,
+                          c->buf_seeds, n_seeds);
+  if (rc) return rc;
+  CK(c, cudaMemcpyAsync(c->h_out, c->buf_out, nb, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(c->h_scalars, c->buf_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  memcpy(d_out, c->h_out, nb);
+  *iterations = c->h_scalars[0];
+  const int st = c->h_scalars[1];
+  if (st != RAC_OK && st != RAC_WIPEOUT) return fail(c, RAC_ECUDA, "kernel did not report a status");
+  return st;
+}
+
+static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                      int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev, uint32_t flags,
+                      void* stream);
+
+int rac_enforce_batch_seeded(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                             int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev,
+                             uint32_t flags, void* stream) {
+  if (n_states > 0 && !seed_var_dev) return fail(c, RAC_EINVAL, "seed_var_dev is NULL");
+  return batch_impl(c, n_states, d_in_dev, d_out_dev, iterations_dev, status_dev, seed_var_dev, flags, stream);
+}
+
 int rac_enforce_batch(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                       int32_t* iterations_dev, int32_t* status_dev, uint32_t flags, void* stream) {
+  return batch_impl(c, n_states, d_in_dev, d_out_dev, iterations_dev, status_dev, nullptr, flags, stream);
+}
+
+static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                      int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev, uint32_t flags,
+                      void* stream) {
   int rc = check_usable(c);
   if (rc) return rc;
   if (n_states < 0 || (n_states > 0 && (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev)))
@@ -544,6 +614,7 @@ int rac_enforce_batch(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   p.d_out = d_out_dev;
   p.iters = iterations_dev;
   p.status = status_dev;
+  p.seed_var = seed_var_dev;
   p.flags = flags;
   const size_t smem = fused_smem(c->nvec) + (size_t)c->n * 8;
   int occ = 0;

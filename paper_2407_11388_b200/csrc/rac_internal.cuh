@@ -51,6 +51,8 @@ struct FusedParams {
   int32_t* removed_at;      // nullable [n*64], pre-zeroed
   unsigned long long* R;    // [3][n] removal masks (rotating)
   unsigned* bar;            // grid barrier words [4]
+  const int32_t* seeds;     // nullable device [n_seeds]: Alg. 1 initial @changed
+  int n_seeds;
   uint32_t flags;
 };
 
@@ -62,6 +64,8 @@ struct ShardState {
   int32_t* iters;            // device scalars
   int32_t* status;
   int32_t* done;
+  int32_t* vcnt;             // length of vlist (vectors changed in the last pass)
+  uint16_t* vlist;           // [nvec] Prop. 2 incremental vector list
 };
 
 struct PassParams {
@@ -77,6 +81,7 @@ struct BatchParams {
   uint64_t* d_out;        // [S][n]
   int32_t* iters;         // [S]
   int32_t* status;        // [S]
+  const int32_t* seed_var;  // nullable [S]: per-state seed variable (-1 = all)
   uint32_t flags;
 };
 
@@ -100,7 +105,7 @@ cudaError_t pass_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
 cudaError_t launch_shard_init(const ShardState& s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
                               size_t row_stride, int total_g, cudaStream_t st);
 cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, cudaStream_t st);
-cudaError_t launch_shard_update(const ShardState& s, int n, int W, uint32_t flags, cudaStream_t st);
+cudaError_t launch_shard_update(const ShardState& s, int n, int W, int nvec, uint32_t flags, cudaStream_t st);
 cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, int32_t* iters, int32_t* status,
                                   cudaStream_t st);
 cudaError_t launch_batch(int W, int G, const BatchParams& p, int n_states, size_t smem, cudaStream_t s);

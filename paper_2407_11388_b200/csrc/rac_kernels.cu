@@ -96,7 +96,20 @@ __device__ __forceinline__ void stage_from_u64(uint4* Ds, const uint64_t* src, c
   for (int i = threadIdx.x; i < nvec * 4; i += blockDim.x) w[i] = 0xffffffffu;
   __syncthreads();
   uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
-  for (int x = threadIdx.x; x < n; x += blockDim.x) store_w<W>(Db + x * W, src[x] & dommask[x]);
+  // 4 independent loads per thread in flight (the whole of D for n <= 2048)
+  for (int x0 = threadIdx.x; x0 < n; x0 += 4 * blockDim.x) {
+    uint64_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int x = x0 + k * blockDim.x;
+      v[k] = x < n ? __ldg(src + x) & __ldg(dommask + x) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int x = x0 + k * blockDim.x;
+      if (x < n) store_w<W>(Db + x * W, v[k]);
+    }
+  }
   __syncthreads();
 }
 
@@ -115,7 +128,23 @@ __global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
   const bool full = (p.flags & kFull) != 0;
   int t = 0, status = kOK, vcnt = g.nvec;
   unsigned epoch = 0;
-  for (;;) {
+  // Seeded call (Alg. 1 with @changed = seeds): pass 1 only re-tests the
+  // vectors holding the seed variables.
+  bool seeded = p.seeds != nullptr;
+  if (seeded) {
+    for (int i = threadIdx.x; i < p.n_seeds; i += blockDim.x) {
+      const int y = p.seeds[i];
+      if (y >= 0 && y < g.n) vneed[(y * W) >> 4] = 1;
+    }
+    __syncthreads();
+    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
+  }
+  if (seeded && vcnt == 0) {  // empty @changed: no pass (status from D_in)
+    int wipe = 0;
+    for (int x = threadIdx.x; x < g.n; x += blockDim.x) wipe |= load_w<W>(Db + x * W) == 0;
+    wipe = __syncthreads_or(wipe);
+    status = wipe ? kWIPEOUT : kOK;
+  } else for (;;) {
     ++t;
     unsigned long long* Rc = p.R + (size_t)(t % 3) * g.n;
     unsigned long long* Rn = p.R + (size_t)((t + 1) % 3) * g.n;
@@ -123,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
     // pass 1 (and any pass where many variables changed) streams whole rows;
     // otherwise only the vectors of variables changed in the previous pass.
-    const bool use_list = t > 1 && 2 * vcnt <= g.nvec && g.nvec <= 65535;
+    const bool use_list = (t > 1 || seeded) && 2 * vcnt <= g.nvec && g.nvec <= 65535;
     support_sweep<W, G>(g, Ds, Rc, p.removed_at, t, id.gidx, id.ngroups, id, use_list ? vlist : nullptr, vcnt);
     grid_sync(p.bar, gridDim.x, ++epoch);
     // D_t = D_{t-1} & ~R (every CTA, redundantly); flags for Alg. 1's checks.
@@ -148,16 +177,24 @@ __global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.d_out[x] = load_w<W>(Db + x * W);
     if (threadIdx.x == 0) { *p.iters = t; *p.status = status; }
   }
-  // The last CTA out resets the barrier words for the next launch.
-  if (threadIdx.x == 0 && gridDim.x > 1) {
+  // The last CTA out resets the barrier words and clears R[1] (the removal
+  // buffer pass 1 of the next launch writes): every other CTA has finished
+  // reading by the time it counts itself out.
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
     __threadfence();
-    unsigned e = atomicAdd(&p.bar[2], 1u);
-    if (e + 1u == gridDim.x) {
+    s_last = gridDim.x == 1 ? 1 : (atomicAdd(&p.bar[2], 1u) + 1u == gridDim.x);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.R[(size_t)g.n + x] = 0ull;
+    if (threadIdx.x == 0 && gridDim.x > 1) {
       p.bar[0] = 0u;
       p.bar[1] = 0u;
       p.bar[2] = 0u;
-      __threadfence();
     }
+    __threadfence();
   }
 }
 
@@ -202,8 +239,15 @@ __global__ void __launch_bounds__(kThreads, 2) rac_pass(PassParams p) {
   if (*reinterpret_cast<volatile int32_t*>(p.s.done)) return;  // converged: speculative pass is a no-op
   tma_stage(Ds, p.s.Dw, (uint32_t)p.g.row_stride, &mbar);
   const int t = *p.s.iters + 1;
+  const int vcnt = *p.s.vcnt;
+  const bool use_list = t > 1 && 2 * vcnt <= p.g.nvec && p.g.nvec <= 65535;
+  uint16_t* vlist = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(Ds) + list_offset(p.g.nvec));
+  if (use_list) {
+    for (int i = threadIdx.x; i < vcnt; i += blockDim.x) vlist[i] = p.s.vlist[i];
+    __syncthreads();
+  }
   const GroupIds id = group_ids<G>();
-  support_sweep<W, G>(p.g, Ds, p.s.R, p.removed_at, t, id.gidx, id.ngroups, id, nullptr, 0);
+  support_sweep<W, G>(p.g, Ds, p.s.R, p.removed_at, t, id.gidx, id.ngroups, id, use_list ? vlist : nullptr, vcnt);
 }
 
 __global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
@@ -223,6 +267,7 @@ __global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_
     *s.iters = 0;
     *s.status = -1;
     *s.done = 0;
+    *s.vcnt = 0;
   }
 }
 
@@ -241,20 +286,30 @@ __global__ void rac_shard_slice(ShardState s, int x_lo, int x_hi, int n) {
 }
 
 // After the exchange: every rank derives the same flags from the gathered
-// vector (changed = D_t != D_{t-1}, wipe = some D_t(x) empty) and advances.
-__global__ void __launch_bounds__(1024) rac_shard_update(ShardState s, int n, int W, uint32_t flags) {
+// vector (changed = D_t != D_{t-1}, wipe = some D_t(x) empty), the list of
+// vectors holding changed variables (Prop. 2 incremental next pass), and
+// advances.  One CTA; dynamic smem = nvec flag bytes.
+__global__ void __launch_bounds__(1024) rac_shard_update(ShardState s, int n, int W, int nvec, uint32_t flags) {
+  extern __shared__ uint8_t need[];
+  __shared__ int scratch[32];
   if (*reinterpret_cast<volatile int32_t*>(s.done)) return;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) need[i] = 0;
+  __syncthreads();
   int changed = 0, wipe = 0;
   for (int x = threadIdx.x; x < n; x += blockDim.x) {
     const uint64_t nv = s.Dg[x];
-    changed |= nv != s.Dcur[x];
+    const bool chx = nv != s.Dcur[x];
+    changed |= chx;
     wipe |= nv == 0;
+    if (chx) need[(x * W) >> 4] = 1;
     s.Dcur[x] = nv;
     for (int k = 0; k < W; ++k) s.Dw[(size_t)x * W + k] = (uint8_t)(nv >> (8 * k));
   }
   changed = __syncthreads_or(changed);
   wipe = __syncthreads_or(wipe);
+  const int cnt = nvec <= 65535 ? block_compact(need, s.vlist, nvec, scratch) : nvec;
   if (threadIdx.x == 0) {
+    *s.vcnt = cnt;
     *s.iters += 1;
     if (wipe && !(flags & kFull)) {
       *s.status = kWIPEOUT;
@@ -298,11 +353,18 @@ __global__ void __launch_bounds__(kThreads, 2) rac_batch(BatchParams p) {
   id.ngroups = (long)(blockDim.x / 32) * (32 / G);
   const bool full = (p.flags & kFull) != 0;
   int t = 0, status = kOK, vcnt = g.nvec;
+  const int seed = p.seed_var ? p.seed_var[s] : -1;
+  const bool seeded = seed >= 0 && seed < g.n;
+  if (seeded) {
+    if (threadIdx.x == 0) vneed[(seed * W) >> 4] = 1;
+    __syncthreads();
+    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
+  }
   for (;;) {
     ++t;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) R[x] = 0ull;
     __syncthreads();
-    const bool use_list = t > 1 && 2 * vcnt <= g.nvec && g.nvec <= 65535;
+    const bool use_list = (t > 1 || seeded) && 2 * vcnt <= g.nvec && g.nvec <= 65535;
     {
       const long rows = (long)g.n * g.dmax;
       for (long r = id.gidx; r < rows; r += id.ngroups) {
@@ -467,8 +529,12 @@ cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, c
   rac_shard_slice<<<grid, 256, 0, st>>>(s, x_lo, x_hi, n);
   return cudaGetLastError();
 }
-cudaError_t launch_shard_update(const ShardState& s, int n, int W, uint32_t flags, cudaStream_t st) {
-  rac_shard_update<<<1, 1024, 0, st>>>(s, n, W, flags);
+cudaError_t launch_shard_update(const ShardState& s, int n, int W, int nvec, uint32_t flags, cudaStream_t st) {
+  if (nvec > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(rac_shard_update, cudaFuncAttributeMaxDynamicSharedMemorySize, nvec);
+    if (e != cudaSuccess) return e;
+  }
+  rac_shard_update<<<1, 1024, nvec, st>>>(s, n, W, nvec, flags);
   return cudaGetLastError();
 }
 cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, int32_t* iters, int32_t* status,

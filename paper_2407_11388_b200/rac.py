@@ -52,7 +52,8 @@ class rac_options(ctypes.Structure):
 
 # Every symbol include/rac.h declares (checked by tests/test_abi.py).
 EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforce", "rac_enforce_ex",
-           "rac_enforce_async", "rac_enforce_batch", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
+           "rac_enforce_async", "rac_enforce_batch", "rac_enforce_seeded", "rac_enforce_seeded_async",
+           "rac_enforce_batch_seeded", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
            "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
            "rac_last_launch_count", "rac_last_error", "rac_destroy"]
 
@@ -76,6 +77,9 @@ def _load() -> ctypes.CDLL:
         "rac_enforce_ex": (ctypes.c_int, [P, u64p, u64p, i32p, i32p, u32]),
         "rac_enforce_async": (ctypes.c_int, [P, P, P, P, P, P, u32, P]),
         "rac_enforce_batch": (ctypes.c_int, [P, i32, P, P, P, P, u32, P]),
+        "rac_enforce_seeded": (ctypes.c_int, [P, u64p, u64p, i32p, i32p, i32, u32]),
+        "rac_enforce_seeded_async": (ctypes.c_int, [P, P, P, P, P, P, i32, u32, P]),
+        "rac_enforce_batch_seeded": (ctypes.c_int, [P, i32, P, P, P, P, P, u32, P]),
         "rac_n_vars": (i32, [P]),
         "rac_max_dom": (i32, [P]),
         "rac_mask_bytes": (i32, [P]),
@@ -243,6 +247,32 @@ class RacContext:
         if removed_at:
             return rc, d_out, it.value, rem.reshape(self.n, 64)
         return rc, d_out, it.value
+
+    def enforce_seeded(self, d_in, seeds, full: bool = False):
+        """rac_enforce_seeded (Alg. 1 tensorAC(Vars, @changed = seeds)), host buffers.
+        Returns (status, d_out, iterations)."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int32).reshape(-1))
+        d_out = np.zeros(self.n, dtype=np.uint64)
+        it = ctypes.c_int32(0)
+        rc = lib.rac_enforce_seeded(self._h, _u64p(d_in), _u64p(d_out), ctypes.byref(it),
+                                    _i32p(seeds) if seeds.size else None, int(seeds.size),
+                                    RAC_FULL_FIXPOINT if full else 0)
+        _check(rc, self._h)
+        return rc, d_out, it.value
+
+    def enforce_seeded_async(self, d_in_dev, d_out_dev, iters_dev, status_dev, seeds_dev, n_seeds: int,
+                             full: bool = False, stream=None) -> None:
+        _check(lib.rac_enforce_seeded_async(self._h, _ptr(d_in_dev), _ptr(d_out_dev), _ptr(iters_dev),
+                                            _ptr(status_dev), _ptr(seeds_dev), n_seeds,
+                                            RAC_FULL_FIXPOINT if full else 0, _stream_ptr(stream)), self._h)
+
+    def enforce_batch_seeded(self, n_states: int, d_in_dev, d_out_dev, iters_dev, status_dev, seed_var_dev,
+                             full: bool = False, stream=None) -> None:
+        """rac_enforce_batch_seeded: state s seeded with variable seed_var_dev[s] (-1 = all)."""
+        _check(lib.rac_enforce_batch_seeded(self._h, n_states, _ptr(d_in_dev), _ptr(d_out_dev), _ptr(iters_dev),
+                                            _ptr(status_dev), _ptr(seed_var_dev), RAC_FULL_FIXPOINT if full else 0,
+                                            _stream_ptr(stream)), self._h)
 
     def enforce_async(self, d_in_dev, d_out_dev, iters_dev, status_dev, removed_at_dev=None, full: bool = False,
                       stream=None) -> None:

@@ -270,13 +270,15 @@ def w_seed(D_root: np.ndarray, seed: int, k: int = 0) -> Tuple[np.ndarray, int, 
 
 
 def dive_states(D_root: np.ndarray, enforce: Callable[[np.ndarray], Tuple[int, np.ndarray]],
-                n_states: int, seed: int) -> List[np.ndarray]:
+                n_states: int, seed: int, return_seeds: bool = False):
     """W-dive: chains of assignments (min-domain variable, lowest index tie-break,
     seeded random live value), each state being the input of one enforcement; restart
-    from D_root after a wipeout or a complete assignment.  `enforce(D) -> (status, D_out)`
+    from D_root after a wipeout or a complete assignment.  With return_seeds, also the
+    assigned variable of each state (its Alg. 1 seed).  `enforce(D) -> (status, D_out)`
     is supplied by the caller (oracle in tests, the GPU path in bench), so this
     function holds none of the method's arithmetic."""
     states = []
+    seeds = []
     cur = np.array(D_root, dtype=U64, copy=True)
     k = 0
     while len(states) < n_states:
@@ -291,6 +293,7 @@ def dive_states(D_root: np.ndarray, enforce: Callable[[np.ndarray], Tuple[int, n
         k += 1
         s = assign(cur, x, v)
         states.append(s)
+        seeds.append(x)
         status, out = enforce(s)
         cur = np.array(D_root if status != 0 else out, dtype=U64, copy=True)
-    return states
+    return (states, seeds) if return_seeds else states

@@ -321,3 +321,77 @@ def test_input_padding_bits_rejected(rac):
     assert ei.value.code == rac.RAC_EINVAL
     # the context stays usable after EINVAL
     assert ctx.enforce(inst.full_domains())[0] in (rac.RAC_OK, rac.RAC_WIPEOUT)
+
+
+# ----------------------------------------------------------------------------- seeded (NEXT-1)
+def test_seeded_c1_and_corpus(rac):
+    """Seeded enforcement (Alg. 1 tensorAC(Vars, [idx])) on W-seed inputs: equal to
+    the oracle's full recurrence O1 and to the literal Alg. 1 O5 (status, D, iterations)."""
+    n_checked = 0
+    for seed in range(1, 201):
+        inst = synth.random_csp(20, 8, 0.5, 0.4, seed) if seed % 2 else \
+            I.random_corpus(1, seed0=seed, n_range=(3, 20))[0]
+        orc = oracle.Oracle.from_instance(inst)
+        st, root, _, _ = orc.rac(inst.full_domains())
+        if st != oracle.OK:
+            continue
+        ctx = rac.RacContext.from_instance(inst)
+        for j in range(2):
+            s, x, v = synth.w_seed(root, seed, j)
+            g = ctx.enforce_seeded(s, [x])
+            o = orc.rac(s)
+            o5 = orc.rac_seeded(s, [x])
+            assert (g[0], g[2]) == (o[0], o[2]) == (o5[0], o5[2]), (seed, j)
+            assert np.array_equal(g[1], o[1]) and np.array_equal(g[1], o5[1])
+            n_checked += 1
+        g = ctx.enforce_seeded(root, [])
+        assert g[0] == rac.RAC_OK and g[2] == 0 and np.array_equal(g[1], root)
+    assert n_checked > 100
+
+
+def test_seeded_c3(rac):
+    """C3 W-seed (n=2000, d=32, t=0.5): the seeded call reads only the assigned variable's
+    masks in pass 1 and equals the oracle's full recurrence."""
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.5)
+    ctx = rac.RacContext.create_random(2000, 32, dq, tq, 1)
+    orc = oracle.Oracle.from_synth(2000, 32, dq, tq, 1)
+    root = synth.full_domains(np.full(2000, 32))
+    st, droot, _, _ = orc.rac(root)
+    assert st == oracle.OK
+    for j in range(3):
+        s, x, v = synth.w_seed(droot, 5, j)
+        g = ctx.enforce_seeded(s, [x])
+        o = orc.rac(s, with_epochs=False)
+        assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1])
+
+
+def test_c5_batched_seeded(rac):
+    """C5 dive states with their assigned variable as the per-state seed: equal to the
+    oracle's single-state full recurrence."""
+    import torch
+    n, d, S = 200, 16, 1024
+    inst = synth.random_csp(n, d, 0.8, 0.3, 1)
+    orc = oracle.Oracle.from_instance(inst)
+    _, root, _, _ = orc.rac(inst.full_domains())
+
+    def enf(D):
+        s, out, _, _ = orc.rac(D, with_epochs=False)
+        return s, out
+
+    states, seeds = synth.dive_states(root, enf, S, seed=2, return_seeds=True)
+    states = np.stack(states)
+    seeds = np.asarray(seeds, dtype=np.int32)
+    seeds[::7] = -1  # some states as root calls
+    ctx = rac.RacContext.from_instance(inst)
+    din = torch.from_numpy(states.view(np.int64)).cuda()
+    dout = torch.zeros_like(din)
+    its = torch.zeros(S, dtype=torch.int32, device="cuda")
+    sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+    sv = torch.from_numpy(seeds).cuda()
+    ctx.enforce_batch_seeded(S, din, dout, its, sts, sv)
+    torch.cuda.synchronize()
+    out = dout.cpu().numpy().view(np.uint64)
+    its, sts = its.cpu().numpy(), sts.cpu().numpy()
+    for s in range(S):
+        e = orc.rac(states[s], with_epochs=False)
+        assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), s

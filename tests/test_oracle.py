@@ -386,3 +386,52 @@ def test_pass_block_matches_one_step():
         expect = int(D[x]) & ~sum(1 << a for a in range(64) if rem[x, a] == 1)
         assert int(out[x - 7]) == expect
     assert removed == int(np.sum(rem[7:23] == 1))
+
+
+# ----------------------------------------------------------------------------- Alg. 1 (seeded)
+def test_seeded_all_equals_root():
+    """tensorAC(Vars, all variables) is the root call: identical to O1."""
+    for k, inst in enumerate(I.random_corpus(200, seed0=41)):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = synth.w_rand(inst.dom, 0.9, seed=k)
+        for full in (False, True):
+            a = orc.rac(d_in, full=full)
+            b = orc.rac_seeded(d_in, np.arange(inst.n), full=full)
+            assert a[0] == b[0] and a[2] == b[2] and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
+
+
+def test_seeded_after_assignment_matches_full_trajectory():
+    """Prop. 2: after an assignment to x on an AC state (W-seed), Alg. 1 seeded
+    with [x] follows exactly the same trajectory as the full recurrence: same
+    status, D, iteration count and per-step removal sets.  Checked on W-seed and W-dive
+    states (the precondition: D_in is AC on every c_xy with y not a seed)."""
+    n_checked = 0
+    for k, inst in enumerate(I.random_corpus(300, seed0=43, n_range=(3, 20))):
+        orc = oracle.Oracle.from_instance(inst)
+        st, root, _, _ = orc.rac(inst.full_domains())
+        if st != oracle.OK:
+            continue
+        for j in range(3):
+            s, x, v = synth.w_seed(root, k, j)
+            a = orc.rac(s)
+            b = orc.rac_seeded(s, [x])
+            assert a[0] == b[0] and a[2] == b[2], (k, j)
+            assert np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
+            n_checked += 1
+    assert n_checked > 200
+
+
+def test_seeded_empty_and_precondition_violated():
+    """Empty @changed: no pass.  Without the precondition the seeded call can keep
+    values the full recurrence removes (it only looks at the changed columns)."""
+    inst = synth.from_constraints(2, 2, [(0, 1, [(0, 0)])])
+    orc = oracle.Oracle.from_instance(inst)
+    st, d, it, _ = orc.rac_seeded(inst.full_domains(), [])
+    assert it == 0 and st == oracle.OK and np.array_equal(d, inst.full_domains())
+    # EQ2 seeded with [0] (precondition violated: full domains are not AC on c_01):
+    # pass 1 tests only column x0 -> removes (1,1); pass 2 tests column x1 -> removes (0,1);
+    # pass 3 tests column x0 -> nothing.  Same D as the full recurrence, 3 passes instead of 2.
+    st, d, it, rem = orc.rac_seeded(inst.full_domains(), [0])
+    assert (st, it, [int(v) for v in d]) == (oracle.OK, 3, [1, 1])
+    assert rem[1, 1] == 1 and rem[0, 1] == 2
+    assert orc.rac(inst.full_domains())[2] == 2
