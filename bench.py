@@ -49,12 +49,16 @@ WORKLOADS = {
     "c2-root": (500, 20, 1.0, 0.3, 1, "root",
                 "C2: n=500, d=20, complete graph, tightness 0.3; root enforcement (20 MB, L2-resident)"),
     "c1-seed": (20, 8, 0.5, 0.4, 1, "seed",
-                "C1 W-seed: n=20, d=8, density 0.5, tightness 0.4; D_ac(root) with one seeded assignment"),
+                "C1 W-seed: n=20, d=8, density 0.5, tightness 0.4; D_ac(root) with one seeded assignment, "
+                "seeded enforcement (Alg. 1 tensorAC(Vars, [idx]), P:392)"),
+    "c3-seed": (2000, 32, 1.0, 0.5, 1, "seed",
+                "C3 W-seed: n=2000, d=32, density 1.0, tightness 0.5; D_ac(root) with one seeded assignment, "
+                "seeded enforcement (Alg. 1 tensorAC(Vars, [idx]), P:392)"),
     "c4-stream": (8000, 64, 1.0, 0.5, 1, "root",
                   "C4 W-stream: n=8000, d=64, density 1.0, tightness 0.5; root enforcement (32.8 GB of masks)"),
     "c5-batch": (200, 16, 0.8, 0.3, 1, "dive",
                  "C5: 1024 W-dive states (search-tree nodes) on n=200, d=16, density 0.8, tightness 0.3; "
-                 "one batched enforcement per step"),
+                 "one batched seeded enforcement per step (each state seeded with its assigned variable)"),
 }
 
 
@@ -159,16 +163,19 @@ def run_gpu(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     # --- D_in
+    seed_vars = None
     if kind == "seed":
         st, root, _ = ctx.enforce(full)
-        d_in, _, _ = synth.w_seed(root, seed)
+        d_in, sx, _ = synth.w_seed(root, seed)
+        seed_vars = np.array([sx], dtype=np.int32)
     else:
         d_in = full
     S = args.states if kind == "dive" else 1
     if kind == "dive":
         st, root, _ = ctx.enforce(full)
-        states = synth.dive_states(root, lambda D: ctx.enforce(D)[:2], S, seed=seed)
+        states, svars = synth.dive_states(root, lambda D: ctx.enforce(D)[:2], S, seed=seed, return_seeds=True)
         din_h = np.stack(states)
+        seed_vars = np.asarray(svars, dtype=np.int32)
     else:
         din_h = d_in[None, :]
 
@@ -183,21 +190,40 @@ def run_gpu(args, rank, world, local_rank):
         stt, dout, it, rem = (ctx.enforce(din_h[0], removed_at=True) if world == 1 else
                               (*ctx.enforce(din_h[0]), None))
         instr = {"iterations": it, "status": "OK" if stt == 0 else "WIPEOUT"}
+        # Algorithmic bytes of Alg. 1: pass t tests every live (x,a)
+        # against the constraints c_xy with y changed in pass t-1 (all y in
+        # pass 1 of a root call; the seed variables in pass 1 of a seeded call):
+        #   bytes_t = Σ_x |D_{t-1}(x)| · |{y ∈ C_x : y ∈ changed_{t-1}}| · d / 8
+        # (equal to SURVEY §8(d)'s full-check figure for one-pass workloads).
         if rem is not None:
-            live0 = np.array([[(int(din_h[0][x]) >> a) & 1 for a in range(d)] for x in range(n)], dtype=bool)
             remd = rem[:, :d]
-            live_per_pass = [int(np.sum(live0 & ((remd == 0) | (remd >= t)))) for t in range(1, it + 1)]
+            live0 = np.array([[(int(din_h[0][x]) >> a) & 1 for a in range(d)] for x in range(n)], dtype=bool)
+            if dens >= 1.0:
+                def nbr_count(chg):
+                    return chg.sum() - chg.astype(np.int64)
+            else:
+                xs, ys = synth.present_pairs(n, dq, seed)
+
+                def nbr_count(chg):
+                    c = np.zeros(n, dtype=np.int64)
+                    np.add.at(c, xs, chg[ys].astype(np.int64))
+                    np.add.at(c, ys, chg[xs].astype(np.int64))
+                    return c
+            chg = np.zeros(n, dtype=bool)
+            if kind == "seed":
+                chg[seed_vars] = True
+            else:
+                chg[:] = True
+            live_per_pass, alg_bytes = [], 0.0
+            for t in range(1, it + 1):
+                alive = live0 & ((remd == 0) | (remd >= t))
+                lv = alive.sum(axis=1)
+                live_per_pass.append(int(lv.sum()))
+                alg_bytes += float((lv * nbr_count(chg)).sum()) * d / 8.0
+                chg = (remd == t).any(axis=1)
         else:
             live_per_pass = [int(sum(bin(int(v)).count("1") for v in din_h[0]))] + [0] * (it - 1)
-        # complete graph at density 1: deg = n-1; otherwise count present pairs in the generator
-        deg = n - 1 if dens >= 1.0 else None
-        if deg is None:
-            xs, ys = synth.present_pairs(n, dq, seed)
-            degs = np.bincount(np.concatenate([xs, ys]), minlength=n)
-            mean_deg = float(degs.mean())
-        else:
-            mean_deg = float(deg)
-        alg_bytes = sum(l * mean_deg * d for l in live_per_pass) / 8.0
+            alg_bytes = live_per_pass[0] * (n - 1) * d / 8.0 if it == 1 else None
         instr["live_rows_per_pass"] = live_per_pass
 
     # --- device buffers
@@ -205,10 +231,13 @@ def run_gpu(args, rank, world, local_rank):
     dout = torch.zeros_like(din)
     its = torch.zeros(S, dtype=torch.int32, device=dev)
     sts = torch.zeros(S, dtype=torch.int32, device=dev)
+    sv = torch.from_numpy(seed_vars).to(dev) if seed_vars is not None else None
 
     def step():
         if kind == "dive":
-            ctx.enforce_batch(S, din, dout, its, sts, stream=stream)
+            ctx.enforce_batch_seeded(S, din, dout, its, sts, sv, stream=stream)
+        elif kind == "seed":
+            ctx.enforce_seeded_async(din, dout, its, sts, sv, 1, stream=stream)
         else:
             ctx.enforce_async(din, dout, its, sts, stream=stream)
 
@@ -253,8 +282,10 @@ def run_gpu(args, rank, world, local_rank):
     # --- e2e: the public host-buffer call, H2D + D2H inside the timed region
     e2e = None
     if kind != "dive":
+        host_call = (lambda: ctx.enforce_seeded(din_h[0], seed_vars)) if kind == "seed" else \
+            (lambda: ctx.enforce(din_h[0]))
         for _ in range(3):
-            ctx.enforce(din_h[0])
+            host_call()
         if world > 1:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -264,7 +295,7 @@ def run_gpu(args, rank, world, local_rank):
         t_wall = time.perf_counter()
         e0.record(stream)
         for _ in range(reps):
-            ctx.enforce(din_h[0])
+            host_call()
         e1.record(stream)
         torch.cuda.synchronize()
         wall_ms = (time.perf_counter() - t_wall) * 1e3
@@ -272,9 +303,9 @@ def run_gpu(args, rank, world, local_rank):
             t = torch.tensor([wall_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall_ms = float(t.item())
-        e2e = {"value": reps / (wall_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": n * 8,
-               "d2h_bytes_per_step": n * 8 + 8,
-               "how": "rac_enforce (host buffers; pinned staging, H2D + enforcement + D2H + sync per call), "
+        e2e = {"value": reps / (wall_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": n * 8 + (4 if kind == "seed" else 0), "d2h_bytes_per_step": n * 8 + 8,
+               "how": ("rac_enforce_seeded" if kind == "seed" else "rac_enforce") + " (host buffers; pinned staging, H2D + enforcement + D2H + sync per call), "
                       "host wall clock over %d calls, max over ranks" % reps}
     else:
         # batched: host states -> device -> batch enforcement -> results back, per step

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -82,6 +83,10 @@ struct rac_ctx {
   int32_t* buf_removed = nullptr;  // [n*64]
   int32_t* buf_seeds = nullptr;    // [seed_cap]
   size_t seed_cap = 0;
+  uint32_t* bs_X2 = nullptr;       // bit-sliced batch exchange buffers
+  size_t bs_X2_cap = 0;            // bytes
+  unsigned* bs_bar = nullptr;      // per-word barrier words
+  size_t bs_bar_cap = 0;           // words
   uint64_t* h_in = nullptr;        // pinned
   uint64_t* h_out = nullptr;
   int32_t* h_scalars = nullptr;    // pinned [iters, status, done]
@@ -141,6 +146,8 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->buf_scalars);
   cudaFree(c->buf_removed);
   cudaFree(c->buf_seeds);
+  cudaFree(c->bs_X2);
+  cudaFree(c->bs_bar);
   cudaFreeHost(c->h_in);
   cudaFreeHost(c->h_out);
   cudaFreeHost(c->h_scalars);
@@ -556,6 +563,8 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   const size_t nb = (size_t)c->n * 8;
   if ((size_t)n_seeds > c->seed_cap) {
     cudaFree(c->buf_seeds);
+  cudaFree(c->bs_X2);
+  cudaFree(c->bs_bar);
     c->buf_seeds = nullptr;
     CK(c, cudaMalloc(&c->buf_seeds, (size_t)n_seeds * 4));
     c->seed_cap = (size_t)n_seeds;
@@ -605,6 +614,61 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   c->launches = 0;
   if (n_states == 0) return 0;
   CK(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  // Bit-sliced path (N5): 32 states per 32-bit word, per-word CTA groups.
+  const char* impl = getenv("RAC_BATCH_IMPL");
+  const bool want_bs = !(impl && strcmp(impl, "state") == 0);
+  const int rows = c->n * c->dmax;
+  const int RB = (rows + 255) / 256;
+  bool use_table = batch_bs_smem(c->n, c->dmax, c->W, true) <= 96 * 1024;
+  const size_t smem = batch_bs_smem(c->n, c->dmax, c->W, use_table);
+  int occ = 0;
+  if (want_bs && smem <= 200 * 1024) CK(c, batch_bs_occupancy(c->W, smem, &occ));
+  const int words_per_launch = occ > 0 ? (c->sm_count * occ) / RB : 0;
+  if (want_bs && words_per_launch >= 1) {
+    const int NWmax = std::min(words_per_launch, (n_states + 31) / 32);
+    const size_t x2_bytes = (size_t)2 * NWmax * rows * 4;
+    if (x2_bytes > c->bs_X2_cap) {
+      cudaFree(c->bs_X2);
+      c->bs_X2 = nullptr;
+      CK(c, cudaMalloc(&c->bs_X2, x2_bytes));
+      c->bs_X2_cap = x2_bytes;
+    }
+    if ((size_t)NWmax * 4 > c->bs_bar_cap) {
+      cudaFree(c->bs_bar);
+      c->bs_bar = nullptr;
+      CK(c, cudaMalloc(&c->bs_bar, (size_t)NWmax * 16));
+      CK(c, cudaMemsetAsync(c->bs_bar, 0, (size_t)NWmax * 16, st));
+      c->bs_bar_cap = (size_t)NWmax * 4;
+    }
+    for (int s0 = 0; s0 < n_states; s0 += 32 * NWmax) {
+      BatchBSParams b{};
+      b.M = c->M;
+      b.row_stride = c->row_stride;
+      b.n = c->n;
+      b.dmax = c->dmax;
+      b.P = c->P;
+      b.pw = c->pw;
+      b.dommask = c->dommask;
+      b.d_in = d_in_dev;
+      b.d_out = d_out_dev;
+      b.iters = iterations_dev;
+      b.status = status_dev;
+      b.seed_var = seed_var_dev;
+      b.S = std::min(n_states - s0, 32 * NWmax);
+      b.s0 = s0;
+      b.NW = (b.S + 31) / 32;
+      b.RB = RB;
+      b.use_table = use_table;
+      b.X2 = c->bs_X2;
+      b.bar = c->bs_bar;
+      b.flags = flags;
+      CK(c, launch_batch_bs(c->W, b, b.NW * RB, smem, st));
+      c->launches++;
+    }
+    return 0;
+  }
+  // Per-state path: one CTA per state (reference design for comparison).
   BatchParams p{};
   p.g = geom_for(c, 0, c->n, 1);
   p.g.n_seg = 1;
@@ -616,11 +680,11 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   p.status = status_dev;
   p.seed_var = seed_var_dev;
   p.flags = flags;
-  const size_t smem = fused_smem(c->nvec) + (size_t)c->n * 8;
-  int occ = 0;
-  CK(c, batch_occupancy(c->W, c->G, smem, &occ));
-  if (occ < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");
-  CK(c, launch_batch(c->W, c->G, p, n_states, smem, (cudaStream_t)stream));
+  const size_t smem1 = fused_smem(c->nvec) + (size_t)c->n * 8;
+  int occ1 = 0;
+  CK(c, batch_occupancy(c->W, c->G, smem1, &occ1));
+  if (occ1 < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");
+  CK(c, launch_batch(c->W, c->G, p, n_states, smem1, st));
   c->launches = 1;
   return 0;
 }

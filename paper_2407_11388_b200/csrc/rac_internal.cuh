@@ -85,6 +85,28 @@ struct BatchParams {
   uint32_t flags;
 };
 
+struct BatchBSParams {
+  const uint8_t* M;
+  size_t row_stride;
+  int n, dmax;
+  const uint32_t* P;
+  int pw;
+  const uint64_t* dommask;
+  const uint64_t* d_in;     // [.][n] caller's states
+  uint64_t* d_out;
+  int32_t* iters;
+  int32_t* status;
+  const int32_t* seed_var;  // nullable [.]
+  int S;                    // states in this launch
+  int s0;                   // index of the first state in the caller's arrays
+  int NW;                   // words (32 states) in this launch
+  int RB;                   // CTAs per word
+  bool use_table;
+  uint32_t* X2;             // [2][NW][n*dmax] exchange buffers
+  unsigned* bar;            // [NW][4] per-word barrier words (zero between launches)
+  uint32_t flags;
+};
+
 // Dynamic smem of rac_fused / rac_batch: D (nvec x 16 B), then the incremental
 // vector list (u16[nvec]) and the per-vector "needed" flags (u8[nvec]).
 __host__ __device__ constexpr size_t list_offset(int nvec) { return (size_t)nvec * 16; }
@@ -110,6 +132,9 @@ cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, i
                                   cudaStream_t st);
 cudaError_t launch_batch(int W, int G, const BatchParams& p, int n_states, size_t smem, cudaStream_t s);
 cudaError_t batch_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
+size_t batch_bs_smem(int n, int dmax, int W, bool use_table);
+cudaError_t batch_bs_occupancy(int W, size_t smem, int* blocks_per_sm);
+cudaError_t launch_batch_bs(int W, const BatchBSParams& p, int grid, size_t smem, cudaStream_t s);
 
 struct PackGeom {
   uint8_t* M;             // local rows
