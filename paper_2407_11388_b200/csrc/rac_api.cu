@@ -63,8 +63,10 @@ thread_local std::string g_create_error;
 struct rac_ctx {
   int device = 0;
   int rank = 0, world = 1, vshards = 1;
-  int n = 0, dmax = 0, W = 0, nvec = 0;
-  size_t row_stride = 0;
+  int n = 0, dmax = 0, W = 0;
+  int rows_pad = 0;        // local rows padded to a warp slab
+  size_t col_stride = 0;   // bytes per column of the mask tensor
+  int dbytes = 0;          // bytes of D in smem
   int x_lo = 0, x_hi = 0, blk = 0;
   int pw = 0;
   std::vector<int32_t> dom;
@@ -87,12 +89,12 @@ struct rac_ctx {
   size_t bs_X2_cap = 0;            // bytes
   unsigned* bs_bar = nullptr;      // per-word barrier words
   size_t bs_bar_cap = 0;           // words
+  unsigned long long* dbg = nullptr;  // RAC_DEBUG_TIMELINE phase timestamps [256]
   uint64_t* h_in = nullptr;        // pinned
   uint64_t* h_out = nullptr;
   int32_t* h_scalars = nullptr;    // pinned [iters, status, done]
   cudaStream_t stream = nullptr;
   int sm_count = 0;
-  int G = 1;
   int fused_grid = 0;
   int pass_grid = 0;
   bool fused_coop = true;
@@ -148,6 +150,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->buf_seeds);
   cudaFree(c->bs_X2);
   cudaFree(c->bs_bar);
+  cudaFree(c->dbg);
   cudaFreeHost(c->h_in);
   cudaFreeHost(c->h_out);
   cudaFreeHost(c->h_scalars);
@@ -175,12 +178,17 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   c->dommask_h.resize(n);
   for (int x = 0; x < n; ++x) c->dommask_h[x] = dom_mask(dom[x]);
   c->W = mask_bytes(c->dmax);
-  c->nvec = (int)(((size_t)n * c->W + 15) / 16);
-  c->row_stride = (size_t)c->nvec * 16;
+  c->dbytes = (int)(((size_t)n * c->W + 15) / 16 * 16);
   c->pw = (n + 31) / 32;
   c->blk = (n + c->world - 1) / c->world;
   rac_shard_range(n, c->world, c->rank, &c->x_lo, &c->x_hi);
-  c->G = choose_group(c->nvec);
+  {
+    const int rows = (c->x_hi - c->x_lo) * c->dmax;
+    const int slab = slab_rows(c->W);
+    c->rows_pad = std::max(slab, (rows + slab - 1) / slab * slab);
+    c->col_stride = (size_t)c->rows_pad * c->W;
+  }
+  if (n > 65535) return fail(nullptr, RAC_EUNSUPPORTED, "n_vars > 65535");
 
   cudaError_t e = cudaSetDevice(c->device);
   if (e != cudaSuccess) return fail(nullptr, RAC_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
@@ -190,7 +198,7 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
     return fail(nullptr, RAC_ECUDA, "cudaStreamCreate");
 
   const size_t local_vars = (size_t)(c->x_hi - c->x_lo);
-  const size_t mbytes = local_vars * c->dmax * c->row_stride;
+  const size_t mbytes = (size_t)n * c->col_stride;
 #define CKC(call)                                                                                   \
   do {                                                                                              \
     cudaError_t e_ = (call);                                                                        \
@@ -213,14 +221,14 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   const size_t gtot = (size_t)c->world * c->blk;
   CKC(cudaMalloc(&c->sh.Dcur, (size_t)n * 8));
   CKC(cudaMalloc(&c->sh.Dg, gtot * 8));
-  CKC(cudaMalloc(&c->sh.Dw, c->row_stride));
+  CKC(cudaMalloc(&c->sh.Dw, (size_t)c->dbytes));
   CKC(cudaMalloc(&c->sh.R, (size_t)n * 8));
   CKC(cudaMemsetAsync(c->sh.R, 0, (size_t)n * 8, c->stream));
   CKC(cudaMalloc(&c->sh.iters, 16));
   c->sh.status = c->sh.iters + 1;
   c->sh.done = c->sh.iters + 2;
   c->sh.vcnt = c->sh.iters + 3;
-  CKC(cudaMalloc(&c->sh.vlist, (size_t)c->nvec * 2 + 16));
+  CKC(cudaMalloc(&c->sh.vlist, (size_t)n * 2 + 16));
   CKC(cudaMalloc(&c->buf_in, (size_t)n * 8));
   CKC(cudaMalloc(&c->buf_out, (size_t)n * 8));
   CKC(cudaMalloc(&c->buf_scalars, 16));
@@ -230,40 +238,28 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   CKC(cudaMallocHost(&c->h_scalars, 16));
 
   // Launch geometry.  Fused path: a co-resident grid (cooperative launch),
-  // as many CTAs as fit, but no more than the work can feed.
-  const long rows = (long)n * c->dmax;
-  const long groups_per_cta = (kThreads / 32) * (32 / c->G);
+  // as many CTAs as fit, but no more than the work of a full pass can feed
+  // (about 4 items of kUnroll columns x one 512-byte slab per warp).
+  const long slabs = c->rows_pad / slab_rows(c->W);
+  const long items = slabs * ((n + kUnroll - 1) / kUnroll);
   int occ = 0;
-  CKC(fused_occupancy(c->W, c->G, fused_smem(c->nvec), &occ));
+  CKC(fused_occupancy(c->W, fused_smem(c->dbytes, n), &occ));
   if (occ < 1) return fail(nullptr, RAC_EUNSUPPORTED, "support-pass kernel does not fit on an SM (n too large)");
-  long want = (rows + groups_per_cta - 1) / groups_per_cta;
+  // about one item per warp (small problems are latency-bound: spread them)
+  const long want = (items + (kThreads / 32) - 1) / (kThreads / 32);
   c->fused_grid = (int)std::max(1L, std::min((long)c->sm_count * occ, want));
   int pocc = 0;
-  CKC(pass_occupancy(c->W, c->G, fused_smem(c->nvec), &pocc));
-  c->pass_grid = c->sm_count * std::max(1, pocc);
+  CKC(pass_occupancy(c->W, fused_smem(c->dbytes, n), &pocc));
+  c->pass_grid = (int)std::max(1L, std::min((long)c->sm_count * std::max(1, pocc), want));
   CKC(cudaStreamSynchronize(c->stream));
 #undef CKC
   return 0;
 }
 
-// Split long rows into segments so that every group gets several items
-// (static round-robin load balance).  Segment length is a multiple of the
-// group's batch (G * kUnroll vectors).
-void set_segments(const rac_ctx* c, PassGeom& g, long rows, long ngroups) {
-  const int batch = c->G * kUnroll;
-  int n_seg = 1;
-  while (rows * n_seg < 12 * ngroups && (c->nvec + n_seg * 2 - 1) / (n_seg * 2) >= batch) n_seg *= 2;
-  int seg = (c->nvec + n_seg - 1) / n_seg;
-  seg = (seg + batch - 1) / batch * batch;
-  g.seg_vecs = seg;
-  g.n_seg = (c->nvec + seg - 1) / seg;
-}
-
-PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi, long ngroups) {
+PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi) {
   PassGeom g{};
   g.M = c->M;
-  g.row_stride = c->row_stride;
-  g.nvec = c->nvec;
+  g.col_stride = c->col_stride;
   g.n = c->n;
   g.dmax = c->dmax;
   g.x_lo = x_lo;
@@ -271,7 +267,7 @@ PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi, long ngroups) {
   g.x_lo_alloc = c->x_lo;
   g.P = c->P;
   g.pw = c->pw;
-  set_segments(c, g, (long)(x_hi - x_lo) * c->dmax, ngroups);
+  g.dbytes = c->dbytes;
   return g;
 }
 
@@ -285,8 +281,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
                   int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
                   int n_seeds = 0) {
   FusedParams p{};
-  const long ngroups = (long)c->fused_grid * (kThreads / 32) * (32 / c->G);
-  p.g = geom_for(c, 0, c->n, ngroups);
+  p.g = geom_for(c, 0, c->n);
   p.dommask = c->dommask;
   p.d_in = d_in;
   p.d_out = d_out;
@@ -298,10 +293,13 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.flags = flags;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
+  if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, 256 * 8));
+  p.dbg = c->dbg;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
   // R[1] (pass 1's removal buffer) is clean: zeroed at create and by the last
   // CTA of every previous launch.
-  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, fused_smem(c->nvec), s, c->fused_grid > 1));
+  static const bool no_coop = getenv("RAC_NO_COOP") != nullptr;  // A/B knob (tooling only)
+  CK(c, launch_fused(c->W, p, c->fused_grid, fused_smem(c->dbytes, c->n), s, c->fused_grid > 1 && !no_coop));
   c->launches++;
   return 0;
 }
@@ -311,16 +309,15 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
   if (removed_at && c->world > 1) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
   const int total_g = c->world * c->blk;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
-  CK(c, launch_shard_init(c->sh, d_in, c->dommask, c->n, c->W, c->row_stride, total_g, s));
+  CK(c, launch_shard_init(c->sh, d_in, c->dommask, c->n, c->W, c->dbytes, total_g, s));
   c->launches++;
-  const long ngroups = (long)c->pass_grid * (kThreads / 32) * (32 / c->G);
   const int nb = c->world > 1 ? 1 : c->vshards;
   std::vector<PassParams> pp(nb);
   for (int b = 0; b < nb; ++b) {
     int lo, hi;
     if (c->world > 1) { lo = c->x_lo; hi = c->x_hi; }
     else rac_shard_range(c->n, c->vshards, b, &lo, &hi);
-    pp[b].g = geom_for(c, lo, std::min(hi, c->n), ngroups);
+    pp[b].g = geom_for(c, lo, std::min(hi, c->n));
     pp[b].s = c->sh;
     pp[b].removed_at = removed_at;
   }
@@ -331,7 +328,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
     for (int k = 0; k < chunk; ++k) {
       for (int b = 0; b < nb; ++b) {
         if (pp[b].g.x_hi <= pp[b].g.x_lo) continue;
-        CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, fused_smem(c->nvec), s));
+        CK(c, launch_pass(c->W, pp[b], c->pass_grid, fused_smem(c->dbytes, c->n), s));
         c->launches++;
       }
       if (c->world > 1) {
@@ -346,7 +343,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
         CK(c, launch_shard_slice(c->sh, 0, c->n, c->n, s));
         c->launches++;
       }
-      CK(c, launch_shard_update(c->sh, c->n, c->W, c->nvec, flags, s));
+      CK(c, launch_shard_update(c->sh, c->n, c->W, flags, s));
       c->launches++;
     }
     enq += chunk;
@@ -459,7 +456,7 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
     if (e == cudaSuccess) e = cudaMemcpy(dxs, xs.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(dys, ys.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice);
-    PackGeom g{c->M, c->row_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
+    PackGeom g{c->M, c->col_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
     if (e == cudaSuccess) e = launch_pack_relations(g, dxs, dys, drows, n_rel, dmax, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     cudaFree(dxs);
@@ -486,7 +483,7 @@ int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q
   rac_ctx* c = new rac_ctx();
   int rc = setup_ctx(c, n_vars, dom.data(), opt);
   if (rc) { free_ctx(c); return rc; }
-  PackGeom g{c->M, c->row_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
+  PackGeom g{c->M, c->col_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
   cudaError_t e = launch_generate(g, d, dens_q32, t_q16, seed, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
@@ -565,6 +562,7 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
     cudaFree(c->buf_seeds);
   cudaFree(c->bs_X2);
   cudaFree(c->bs_bar);
+  cudaFree(c->dbg);
     c->buf_seeds = nullptr;
     CK(c, cudaMalloc(&c->buf_seeds, (size_t)n_seeds * 4));
     c->seed_cap = (size_t)n_seeds;
@@ -636,6 +634,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     }
     if ((size_t)NWmax * 4 > c->bs_bar_cap) {
       cudaFree(c->bs_bar);
+  cudaFree(c->dbg);
       c->bs_bar = nullptr;
       CK(c, cudaMalloc(&c->bs_bar, (size_t)NWmax * 16));
       CK(c, cudaMemsetAsync(c->bs_bar, 0, (size_t)NWmax * 16, st));
@@ -644,7 +643,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     for (int s0 = 0; s0 < n_states; s0 += 32 * NWmax) {
       BatchBSParams b{};
       b.M = c->M;
-      b.row_stride = c->row_stride;
+      b.col_stride = c->col_stride;
       b.n = c->n;
       b.dmax = c->dmax;
       b.P = c->P;
@@ -670,9 +669,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   }
   // Per-state path: one CTA per state (reference design for comparison).
   BatchParams p{};
-  p.g = geom_for(c, 0, c->n, 1);
-  p.g.n_seg = 1;
-  p.g.seg_vecs = c->nvec;
+  p.g = geom_for(c, 0, c->n);
   p.dommask = c->dommask;
   p.d_in = d_in_dev;
   p.d_out = d_out_dev;
@@ -680,11 +677,11 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   p.status = status_dev;
   p.seed_var = seed_var_dev;
   p.flags = flags;
-  const size_t smem1 = fused_smem(c->nvec) + (size_t)c->n * 8;
+  const size_t smem1 = fused_smem(c->dbytes, c->n) + (size_t)c->n * 8;
   int occ1 = 0;
-  CK(c, batch_occupancy(c->W, c->G, smem1, &occ1));
+  CK(c, batch_occupancy(c->W, smem1, &occ1));
   if (occ1 < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");
-  CK(c, launch_batch(c->W, c->G, p, n_states, smem1, st));
+  CK(c, launch_batch(c->W, p, n_states, smem1, st));
   c->launches = 1;
   return 0;
 }
@@ -693,7 +690,7 @@ int32_t rac_n_vars(const rac_ctx* c) { return c ? c->n : RAC_EINVAL; }
 int32_t rac_max_dom(const rac_ctx* c) { return c ? c->dmax : RAC_EINVAL; }
 int32_t rac_mask_bytes(const rac_ctx* c) { return c ? c->W : RAC_EINVAL; }
 int64_t rac_relation_bytes(const rac_ctx* c) {
-  return c ? (int64_t)(c->x_hi - c->x_lo) * c->dmax * (int64_t)c->row_stride : RAC_EINVAL;
+  return c ? (int64_t)c->n * (int64_t)c->col_stride : RAC_EINVAL;
 }
 int64_t rac_last_launch_count(const rac_ctx* c) { return c ? c->launches : RAC_EINVAL; }
 
@@ -711,9 +708,10 @@ int rac_read_row(const rac_ctx* cc, int32_t x, int32_t a, uint64_t* out_masks, u
   if (x < c->x_lo || x >= c->x_hi || a < 0 || a >= c->dmax) return fail(c, RAC_EINVAL, "row not local");
   CK(c, cudaSetDevice(c->device));
   if (out_masks) {
-    std::vector<uint8_t> buf(c->row_stride);
+    // column-major: the row's n masks are strided by col_stride
+    std::vector<uint8_t> buf((size_t)c->n * c->W);
     const size_t r = (size_t)(x - c->x_lo) * c->dmax + a;
-    CK(c, cudaMemcpy(buf.data(), c->M + r * c->row_stride, c->row_stride, cudaMemcpyDeviceToHost));
+    CK(c, cudaMemcpy2D(buf.data(), c->W, c->M + r * c->W, c->col_stride, c->W, c->n, cudaMemcpyDeviceToHost));
     for (int y = 0; y < c->n; ++y) {
       uint64_t v = 0;
       for (int k = 0; k < c->W; ++k) v |= (uint64_t)buf[(size_t)y * c->W + k] << (8 * k);
@@ -726,6 +724,17 @@ int rac_read_row(const rac_ctx* cc, int32_t x, int32_t a, uint64_t* out_masks, u
     for (int y = 0; y < c->n; ++y) out_present[y] = (pb[y >> 5] >> (y & 31)) & 1u;
   }
   return 0;
+}
+
+// Tooling (not part of include/rac.h): phase timestamps of the last fused
+// launch when RAC_DEBUG_TIMELINE is set.  Returns the number written.
+int rac_debug_timeline(rac_ctx* c, unsigned long long* out, int cap) {
+  if (!c || !c->dbg || !out) return 0;
+  unsigned long long buf[256];
+  if (cudaMemcpy(buf, c->dbg, sizeof(buf), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  int n = (int)std::min<unsigned long long>(buf[0], (unsigned long long)cap);
+  for (int i = 0; i < n; ++i) out[i] = buf[1 + i];
+  return n;
 }
 
 int rac_get_nccl_unique_id(void* out) {

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
   const int row = rb * kBT + threadIdx.x;
   const int x = row < rows ? row / p.dmax : 0;
   const int a = row - x * p.dmax;
-  const uint8_t* Mrow = p.M + (size_t)row * p.row_stride;
+  const uint8_t* Mrow = p.M + (size_t)row * W;  // + y * col_stride: column-major masks
   const uint32_t* Prow = p.P + (size_t)x * p.pw;
   int t = 0;
   unsigned epoch = 0;
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
           const int y = list[k];
           uint32_t sup = 0;
           if constexpr (W == 8) {
-            const uint64_t m = load_mask64(Mrow + (size_t)y * 8);
+            const uint64_t m = load_mask64(Mrow + (size_t)y * p.col_stride);
             if (p.use_table) {
 #pragma unroll
               for (int q = 0; q < NQ; ++q) sup |= T[((size_t)y * NQ + q) * 16 + ((m >> (4 * q)) & 15u)];
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
               }
             }
           } else {
-            const uint32_t m = load_mask<W>(Mrow + (size_t)y * W);
+            const uint32_t m = load_mask<W>(Mrow + (size_t)y * p.col_stride);
             if (p.use_table) {
 #pragma unroll
               for (int q = 0; q < NQ; ++q) sup |= T[((size_t)y * NQ + q) * 16 + ((m >> (4 * q)) & 15u)];

@@ -2,18 +2,18 @@
 //
 // Data layout in HBM:
 //   W          bytes per support mask: 1, 2, 4 or 8 (smallest >= max dom bits).
-//   nvec       ceil(n*W / 16): 16-byte vectors per (x,a) row.
-//   row_stride nvec*16 bytes.
-//   M          [local rows][row_stride] bytes; local row r = (x - x_lo)*dmax + a.
-//              Bytes [y*W, y*W+W) of row (x,a) hold the support mask
-//              c_xy|(x,a) as a d_y-bit set; absent pairs
-//              and y == x hold all-ones; bytes beyond n*W hold 0xFF.
+//   rows       local rows (x,a): r = (x - x_lo)*dmax + a, padded to a multiple of
+//              kSlabRows(W) = 32 lanes x 16/W rows (one warp-wide 512-byte slab).
+//   M          COLUMN-major: column y (every variable y = 0..n-1) is a contiguous
+//              array of `rows` W-byte masks, M + y*col_stride + r*W holds
+//              c_xy|(x,a) as a d_y-bit set.  Absent pairs and
+//              y == x hold all-ones; padding rows hold 0xFF.  Reading the columns
+//              of the changed variables is Alg. 1's Cons[:, @changed] gather
+//               as contiguous streams.
 //   P          presence bitmap, [local x][pw = ceil(n/32)] u32; bit y of
 //              variable x set iff c_xy is declared (C_x).
-//   D (smem)   the alive bitvector D_t in the same W-byte layout as a row
-//              (variable x at bytes [x*W, x*W+W)), padded with 0xFF to
-//              row_stride bytes, so 16-byte vector v of a row lines up with
-//              16-byte vector v of D.
+//   D (smem)   the alive bitvector D_t, variable y at bytes [y*W, y*W+W),
+//              padded to 16 bytes (dbytes).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -23,22 +23,25 @@
 
 namespace rac {
 
-constexpr int kThreads = 512;  // CTA size of the support-pass kernels
-constexpr int kUnroll = 4;     // 16-byte loads in flight per lane per batch
+#ifndef RAC_THREADS
+#define RAC_THREADS 512
+#endif
+constexpr int kThreads = RAC_THREADS;  // CTA size of the support-pass kernels
+constexpr int kUnroll = 8;     // 16-byte column loads in flight per lane
+
+__host__ __device__ constexpr int slab_rows(int W) { return 32 * (16 / W); }
 
 // ---------------------------------------------------------------------------- params
 struct PassGeom {
-  const uint8_t* M;       // first local row
-  size_t row_stride;      // bytes
-  int nvec;               // 16-byte vectors per row
-  int n;                  // variables
+  const uint8_t* M;       // column-major masks of the local rows
+  size_t col_stride;      // bytes per column = rows_pad * W
+  int n;                  // variables (= columns)
   int dmax;               // rows per variable
-  int x_lo, x_hi;         // rows of variables [x_lo, x_hi) are processed (M indexed from x_lo_alloc)
-  int x_lo_alloc;         // first variable whose rows M points at
+  int x_lo, x_hi;         // rows of variables [x_lo, x_hi) are tested
+  int x_lo_alloc;         // first variable of the local row block
   const uint32_t* P;      // presence bits of variable x_lo_alloc onward
   int pw;                 // u32 words per presence row
-  int seg_vecs;           // vectors per work item (a row is split into n_seg segments)
-  int n_seg;
+  int dbytes;             // bytes of D in smem (n*W rounded up to 16)
 };
 
 struct FusedParams {
@@ -54,18 +57,19 @@ struct FusedParams {
   const int32_t* seeds;     // nullable device [n_seeds]: Alg. 1 initial @changed
   int n_seeds;
   uint32_t flags;
+  unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
 };
 
 struct ShardState {
   uint64_t* Dcur;            // [n] current D_t (u64 per variable)
   uint64_t* Dg;              // [world*blk] gathered D_{t+1}
-  uint8_t* Dw;               // [row_stride] D_t in the W-byte smem layout (TMA source)
+  uint8_t* Dw;               // [dbytes] D_t in the W-byte smem layout (TMA source)
   unsigned long long* R;     // [n] removal masks of the current pass
   int32_t* iters;            // device scalars
   int32_t* status;
   int32_t* done;
-  int32_t* vcnt;             // length of vlist (vectors changed in the last pass)
-  uint16_t* vlist;           // [nvec] Prop. 2 incremental vector list
+  int32_t* vcnt;             // length of vlist (variables changed in the last pass)
+  uint16_t* vlist;           // [n] Prop. 2 incremental column list
 };
 
 struct PassParams {
@@ -87,7 +91,7 @@ struct BatchParams {
 
 struct BatchBSParams {
   const uint8_t* M;
-  size_t row_stride;
+  size_t col_stride;
   int n, dmax;
   const uint32_t* P;
   int pw;
@@ -107,38 +111,37 @@ struct BatchBSParams {
   uint32_t flags;
 };
 
-// Dynamic smem of rac_fused / rac_batch: D (nvec x 16 B), then the incremental
-// vector list (u16[nvec]) and the per-vector "needed" flags (u8[nvec]).
-__host__ __device__ constexpr size_t list_offset(int nvec) { return (size_t)nvec * 16; }
-__host__ __device__ constexpr size_t need_offset(int nvec) {
-  return (size_t)nvec * 16 + (((size_t)nvec * 2 + 15) & ~(size_t)15);
+// Dynamic smem of rac_fused / rac_pass / rac_batch: D (dbytes), then the
+// incremental column list (u16[n]) and the per-variable "changed" flags (u8[n]).
+__host__ __device__ constexpr size_t list_offset(int dbytes) { return (size_t)dbytes; }
+__host__ __device__ constexpr size_t need_offset(int dbytes, int n) {
+  return (size_t)dbytes + (((size_t)n * 2 + 15) & ~(size_t)15);
 }
-__host__ __device__ constexpr size_t fused_smem(int nvec) {
-  return need_offset(nvec) + (((size_t)nvec + 15) & ~(size_t)15);
+__host__ __device__ constexpr size_t fused_smem(int dbytes, int n) {
+  return need_offset(dbytes, n) + (((size_t)n + 15) & ~(size_t)15);
 }
 
 // ---------------------------------------------------------------------------- host launchers
 // (defined in rac_kernels.cu / rac_pack.cu; return cudaError_t of the launch)
-int choose_group(int nvec);  // lanes per row
-cudaError_t launch_fused(int W, int G, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool cooperative);
-cudaError_t fused_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
-cudaError_t launch_pass(int W, int G, const PassParams& p, int grid, size_t smem, cudaStream_t s);
-cudaError_t pass_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
+cudaError_t launch_fused(int W, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool cooperative);
+cudaError_t fused_occupancy(int W, size_t smem, int* blocks_per_sm);
+cudaError_t launch_pass(int W, const PassParams& p, int grid, size_t smem, cudaStream_t s);
+cudaError_t pass_occupancy(int W, size_t smem, int* blocks_per_sm);
 cudaError_t launch_shard_init(const ShardState& s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
-                              size_t row_stride, int total_g, cudaStream_t st);
+                              int dbytes, int total_g, cudaStream_t st);
 cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, cudaStream_t st);
-cudaError_t launch_shard_update(const ShardState& s, int n, int W, int nvec, uint32_t flags, cudaStream_t st);
+cudaError_t launch_shard_update(const ShardState& s, int n, int W, uint32_t flags, cudaStream_t st);
 cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, int32_t* iters, int32_t* status,
                                   cudaStream_t st);
-cudaError_t launch_batch(int W, int G, const BatchParams& p, int n_states, size_t smem, cudaStream_t s);
-cudaError_t batch_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
+cudaError_t launch_batch(int W, const BatchParams& p, int n_states, size_t smem, cudaStream_t s);
+cudaError_t batch_occupancy(int W, size_t smem, int* blocks_per_sm);
 size_t batch_bs_smem(int n, int dmax, int W, bool use_table);
 cudaError_t batch_bs_occupancy(int W, size_t smem, int* blocks_per_sm);
 cudaError_t launch_batch_bs(int W, const BatchBSParams& p, int grid, size_t smem, cudaStream_t s);
 
 struct PackGeom {
-  uint8_t* M;             // local rows
-  size_t row_stride;
+  uint8_t* M;             // column-major masks of the local rows
+  size_t col_stride;
   int W;
   int n, dmax;
   int x_lo, x_hi;         // local block
@@ -162,20 +165,6 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   return r;
 }
 
-// Does any W-byte lane of t equal zero?  (t = mask & D, 16 bytes = 16/W masks)
-template <int W>
-__device__ __forceinline__ bool vec_any_zero(uint4 t) {
-  if constexpr (W == 8) {
-    return ((t.x | t.y) == 0u) | ((t.z | t.w) == 0u);
-  } else if constexpr (W == 4) {
-    return (t.x == 0u) | (t.y == 0u) | (t.z == 0u) | (t.w == 0u);
-  } else if constexpr (W == 2) {
-    return (__vcmpeq2(t.x, 0u) | __vcmpeq2(t.y, 0u) | __vcmpeq2(t.z, 0u) | __vcmpeq2(t.w, 0u)) != 0u;
-  } else {
-    return (__vcmpeq4(t.x, 0u) | __vcmpeq4(t.y, 0u) | __vcmpeq4(t.z, 0u) | __vcmpeq4(t.w, 0u)) != 0u;
-  }
-}
-
 __device__ __forceinline__ uint4 and4(uint4 a, uint4 b) {
   return make_uint4(a.x & b.x, a.y & b.y, a.z & b.z, a.w & b.w);
 }
@@ -196,99 +185,66 @@ __device__ __forceinline__ void store_w(uint8_t* p, uint64_t v) {
   else *p = (uint8_t)v;
 }
 
-__device__ __forceinline__ uint64_t extract_w(const uint4& v, int i, int W) {
-  // i-th W-byte lane of a 16-byte vector
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  if (W == 8) return (uint64_t)w[2 * i] | ((uint64_t)w[2 * i + 1] << 32);
-  if (W == 4) return w[i];
-  if (W == 2) return (w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-  return (w[i >> 2] >> (8 * (i & 3))) & 0xFFu;
-}
-
-// A 16-byte vector had some mask & D == 0.  Decide whether that is a real
-// loss of support: mask_y & D(y) == 0 removes (x,a) iff c_xy is declared
-// (reading R2) -- absent pairs store all-ones, so they only "fail" when D(y)
-// is empty, and then P decides.  Padding lanes (y >= n) never fail.
+// D(y) replicated over the 16/W lanes of a 16-byte vector.
 template <int W>
-__device__ __noinline__ bool vec_real_fail(uint4 m, uint4 d, int v, int n, const uint32_t* Prow) {
-  constexpr int L = 16 / W;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    int y = v * L + i;
-    if (y >= n) break;
-    uint64_t mi = extract_w(m, i, W), di = extract_w(d, i, W);
-    if ((mi & di) == 0) {
-      if (di != 0) return true;
-      if ((Prow[y >> 5] >> (y & 31)) & 1u) return true;
-    }
+__device__ __forceinline__ uint4 rep16(uint64_t d) {
+  if constexpr (W == 8) {
+    const uint32_t lo = (uint32_t)d, hi = (uint32_t)(d >> 32);
+    return make_uint4(lo, hi, lo, hi);
+  } else {
+    uint32_t v = (uint32_t)d;
+    if constexpr (W == 2) v = v | (v << 16);
+    if constexpr (W == 1) v = v * 0x01010101u;
+    return make_uint4(v, v, v, v);
   }
-  return false;
 }
 
-template <int G>
-__device__ __forceinline__ bool group_any(bool f, unsigned gmask) {
-  if constexpr (G == 32) return __any_sync(0xffffffffu, f);
-  else if constexpr (G == 1) return f;
-  else return (__ballot_sync(gmask, f) & gmask) != 0u;
+// Bit i set iff the i-th W-byte lane of t is zero (16/W lanes).
+template <int W>
+__device__ __forceinline__ uint32_t zero_lanes(uint4 t) {
+  if constexpr (W == 8) {
+    return (uint32_t)((t.x | t.y) == 0u) | ((uint32_t)((t.z | t.w) == 0u) << 1);
+  } else if constexpr (W == 4) {
+    return (uint32_t)(t.x == 0u) | ((uint32_t)(t.y == 0u) << 1) | ((uint32_t)(t.z == 0u) << 2) |
+           ((uint32_t)(t.w == 0u) << 3);
+  } else if constexpr (W == 2) {
+    const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = __vcmpeq2(w4[k], 0u);
+      m |= ((c & 1u) | ((c >> 15) & 2u)) << (2 * k);
+    }
+    return m;
+  } else {
+    const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = __vcmpeq4(w4[k], 0u);
+      m |= ((c & 1u) | ((c >> 7) & 2u) | ((c >> 14) & 4u) | ((c >> 21) & 8u)) << (4 * k);
+    }
+    return m;
+  }
 }
 
-// Support test of one (x,a) row segment [vb, ve) against D in smem:
-// returns true iff some declared c_xy has c_xy|(x,a) ∩ D(y) = ∅ for y in the
-// segment (Eq. 1 condition, intersection form of line 59).
-// G lanes cooperate; kUnroll 16-byte streaming loads per lane are in flight
-// before the AND/test; the group exits early once a failure is seen.
-template <int W, int G>
-__device__ __forceinline__ bool row_fails(const uint4* __restrict__ row, const uint4* Ds, int vb, int ve, int gl,
-                                          unsigned gmask, int n, const uint32_t* Prow) {
-  bool fail = false;
-  for (int v0 = vb; v0 < ve; v0 += G * kUnroll) {
-    uint4 m[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      int v = v0 + u * G + gl;
-      if (v < ve) m[u] = ldg_stream(row + v);
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      int v = v0 + u * G + gl;
-      if (v < ve) {
-        uint4 d = Ds[v];
-        if (vec_any_zero<W>(and4(m[u], d))) fail |= vec_real_fail<W>(m[u], d, v, n, Prow);
-      }
-    }
-    if (group_any<G>(fail, gmask)) return true;
+// Support test of column y for the 16/W rows r0.. of one lane against D(y):
+// returns the rows (bits) among `cand` that lose support, i.e. whose mask &
+// D(y) == 0 (Eq. 1 condition, intersection form of line
+// 59) -- but only on a declared c_xy (reading R2): absent pairs store
+// all-ones, so they can only "fail" when D(y) is empty, and then P decides.
+template <int W>
+__device__ __forceinline__ uint32_t column_fail(uint4 m, uint64_t d, uint32_t cand, int y, int r0, int dmax,
+                                                const uint32_t* P, int pw) {
+  const uint32_t z = zero_lanes<W>(and4(m, rep16<W>(d))) & cand;
+  if (z == 0u || d != 0ull) return z;
+  uint32_t f = 0;
+  for (uint32_t zz = z; zz; zz &= zz - 1u) {
+    const int i = __ffs(zz) - 1;
+    const int xl = (r0 + i) / dmax;  // local variable of row r0+i
+    if ((P[(size_t)xl * pw + (y >> 5)] >> (y & 31)) & 1u) f |= 1u << i;
   }
-  return false;
-}
-
-// As row_fails, but only over the 16-byte vectors listed in vl[lb, le)
-// (Prop. 2: after pass 1 a row can only lose support
-// on a constraint whose other variable changed in the previous pass, so only
-// the vectors holding masks of changed variables are re-tested).
-template <int W, int G>
-__device__ __forceinline__ bool row_fails_list(const uint4* __restrict__ row, const uint4* Ds, const uint16_t* vl,
-                                               int lb, int le, int gl, unsigned gmask, int n,
-                                               const uint32_t* Prow) {
-  bool fail = false;
-  for (int i0 = lb; i0 < le; i0 += G * kUnroll) {
-    uint4 m[kUnroll];
-    int vv[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int i = i0 + u * G + gl;
-      vv[u] = i < le ? (int)vl[i] : -1;
-      if (vv[u] >= 0) m[u] = ldg_stream(row + vv[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (vv[u] >= 0) {
-        uint4 d = Ds[vv[u]];
-        if (vec_any_zero<W>(and4(m[u], d))) fail |= vec_real_fail<W>(m[u], d, vv[u], n, Prow);
-      }
-    }
-    if (group_any<G>(fail, gmask)) return true;
-  }
-  return false;
+  return f;
 }
 
 // Block-wide compaction of the flags need[0, cnt) into the ascending index
@@ -327,6 +283,12 @@ __device__ __forceinline__ int block_compact(uint8_t* need, uint16_t* out, int c
   const int total = scratch[(T >> 5) - 1];
   __syncthreads();
   return total;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {

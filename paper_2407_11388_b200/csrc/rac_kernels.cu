@@ -3,12 +3,16 @@
 // One pass of the recurrence, Eq. 1, read in the
 // intersection form of line 59:
 //   D_t(x,a) = D_{t-1}(x,a) ∧ ∧_{c_xy ∈ C_x} [ c_xy|(x,a) ∩ D_{t-1}(y) ≠ ∅ ]
-// For each live row (x,a) the kernel streams the packed masks M[x][a][·]
-// (coalesced 128-bit loads), ANDs them with D_{t-1} held in shared memory and
-// reduces "some mask & D == 0" across the lanes of the row with warp votes
-// (early exit on the first failure).  Removed values are OR-ed into a removal
-// bitvector R; D_t = D_{t-1} & ~R.  Loop control (Alg. 1 tensorAC, lines
-// 198-210): wipeout checked first, then "nothing changed".
+// evaluated column by column: for every tested column y (all y in a full
+// pass; the variables changed in the previous pass otherwise -- Alg. 1's
+// Cons[:, @changed], justified by Prop. 2)
+// a warp streams 512 contiguous bytes of column y (16 bytes = 16/W masks per
+// lane, 128-bit loads, kUnroll columns in flight per lane), ANDs each mask
+// with D_{t-1}(y) held in shared memory and ORs "mask & D == 0" into a
+// per-lane failure set; a lane stops as soon as all its live rows failed;
+// dead rows are skipped.  Failing rows are OR-ed into a removal bitvector R
+// (the only atomics; rare), and D_t = D_{t-1} & ~R.  Loop control (Alg. 1
+// tensorAC, lines 198-210): wipeout checked first, then "nothing changed".
 //
 // Kernels:
 //   rac_fused  -- whole enforcement in one cooperative launch: every CTA keeps
@@ -19,7 +23,8 @@
 //                 TMA bulk copy (cp.async.bulk + mbarrier).  Used by the
 //                 row-sharded multi-GPU path (and virtual shards on one GPU)
 //                 together with rac_shard_{init,slice,update,finalize}.
-//   rac_batch  -- one CTA per domain state (batched mode).
+//   rac_batch  -- one CTA per domain state (batched mode, per-state design;
+//                 the default batched path is the bit-sliced rac_batch_bs).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,57 +37,73 @@ namespace {
 constexpr uint32_t kFull = 1u;  // RAC_FULL_FIXPOINT
 constexpr int kOK = 0, kWIPEOUT = 1;
 
-struct GroupIds {
-  int gl;          // lane within the group
-  unsigned gmask;  // lanes of this group within the warp
-  long gidx;       // global group index
-  long ngroups;    // total groups in the grid
-};
-
-template <int G>
-__device__ __forceinline__ GroupIds group_ids() {
-  GroupIds r;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gw = lane / G;
-  r.gl = lane % G;
-  r.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
-  const long per_cta = (long)(blockDim.x / 32) * (32 / G);
-  r.gidx = (long)blockIdx.x * per_cta + warp * (32 / G) + gw;
-  r.ngroups = (long)gridDim.x * per_cta;
-  return r;
-}
-
-// Test the rows of variables [g.x_lo, g.x_hi) assigned to this group (static
-// round-robin over (row, segment) items) and record removals into R.
-// vl == nullptr: stream every vector of the row; else only the listed
-// vectors (vl[0, vcnt), Prop. 2 incremental pass).
-template <int W, int G>
-__device__ __forceinline__ void support_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
-                                              int32_t* removed_at, int t, long item0, long istep,
-                                              const GroupIds& id, const uint16_t* vl, int vcnt) {
-  const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
-  const long rows = (long)(g.x_hi - g.x_lo) * g.dmax;
-  const int n_seg = vl ? 1 : g.n_seg;
-  const long n_items = rows * n_seg;
-  const long row0 = (long)(g.x_lo - g.x_lo_alloc) * g.dmax;
-  for (long it = item0; it < n_items; it += istep) {
-    long r, s;
-    if (n_seg == 1) { r = it; s = 0; } else { r = it / n_seg; s = it - r * n_seg; }
-    const int xl = (int)(r / g.dmax);
-    const int a = (int)(r - (long)xl * g.dmax);
-    const int x = g.x_lo + xl;
-    if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;  // dead row: (x,a) ∉ D_{t-1}
-    const uint4* row = reinterpret_cast<const uint4*>(g.M + (size_t)(row0 + r) * g.row_stride);
-    const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
-    bool f;
-    if (vl) {
-      f = row_fails_list<W, G>(row, Ds, vl, 0, vcnt, id.gl, id.gmask, g.n, Prow);
-    } else {
-      const int vb = (int)s * g.seg_vecs;
-      const int ve = min(vb + g.seg_vecs, g.nvec);
-      f = row_fails<W, G>(row, Ds, vb, ve, id.gl, id.gmask, g.n, Prow);
+// Test the rows of variables [g.x_lo, g.x_hi) against the columns
+// cols[0, ncol) (cols == nullptr: columns 0..ncol-1) and OR removals into R.
+// Work items = (slab of 32*(16/W) rows, chunk of columns), one warp per item,
+// static round-robin over the warps [warp0, warp0 + nwarps) of the launch.
+template <int W>
+__device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
+                                             int32_t* removed_at, int t, long warp0, long nwarps,
+                                             const uint16_t* cols, int ncol) {
+  constexpr int RPL = 16 / W, RPW = 32 * RPL;
+  const int lane = threadIdx.x & 31;
+  const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
+  const int r_hi = (g.x_hi - g.x_lo_alloc) * g.dmax;
+  if (r_hi <= r_lo || ncol <= 0) return;
+  const int s_lo = r_lo / RPW, s_hi = (r_hi + RPW - 1) / RPW;
+  const int nslab = s_hi - s_lo;
+  // about 4 items per warp, each at least kUnroll columns long (32-bit
+  // arithmetic only: 64-bit division is a long software sequence)
+  const int nw = (int)nwarps;
+  int nchunk = (4 * nw + nslab - 1) / nslab;
+  const int maxchunk = (ncol + kUnroll - 1) / kUnroll;
+  if (nchunk > maxchunk) nchunk = maxchunk;
+  if (nchunk < 1) nchunk = 1;
+  const int yc = (ncol + nchunk - 1) / nchunk;
+  nchunk = (ncol + yc - 1) / yc;
+  const int items = nslab * nchunk;
+  for (int it = (int)warp0; it < items; it += nw) {
+    const int chunk = it / nslab;
+    const int slab = s_lo + (it - chunk * nslab);
+    const int r0 = slab * RPW + lane * RPL;  // first local row of this lane
+    uint32_t cand = 0;                       // live rows of this lane
+    {
+      // walk (x, a) incrementally from one division
+      int xl = r0 / g.dmax, a = r0 - xl * g.dmax;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = r0 + i;
+        if (r >= r_lo && r < r_hi) {
+          const int x = g.x_lo_alloc + xl;
+          if ((Db[x * W + (a >> 3)] >> (a & 7)) & 1u) cand |= 1u << i;
+        }
+        if (++a == g.dmax) { a = 0; ++xl; }
+      }
     }
-    if (f && id.gl == 0) {
+    uint32_t fail = 0;
+    const int c0 = chunk * yc, c1 = min(c0 + yc, ncol);
+    const uint8_t* base = g.M + (size_t)r0 * W;
+    for (int c = c0; c < c1 && fail != cand; c += kUnroll) {
+      uint4 m[kUnroll];
+      int yy[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int cc = c + u;
+        yy[u] = cc < c1 ? (cols ? (int)cols[cc] : cc) : -1;
+        if (yy[u] >= 0) m[u] = ldg_stream(reinterpret_cast<const uint4*>(base + (size_t)yy[u] * g.col_stride));
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (yy[u] >= 0) {
+          const uint64_t d = load_w<W>(Db + yy[u] * W);
+          fail |= column_fail<W>(m[u], d, cand & ~fail, yy[u], r0, g.dmax, g.P, g.pw);
+        }
+      }
+    }
+    for (uint32_t f = fail; f; f &= f - 1u) {
+      const int r = r0 + __ffs(f) - 1;
+      const int xl = r / g.dmax, a = r - xl * g.dmax;
+      const int x = g.x_lo_alloc + xl;
       atomicOr(&R[x], 1ull << a);
       if (removed_at) removed_at[(size_t)x * 64 + a] = t;
     }
@@ -90,12 +111,11 @@ __device__ __forceinline__ void support_sweep(const PassGeom& g, const uint4* Ds
 }
 
 template <int W>
-__device__ __forceinline__ void stage_from_u64(uint4* Ds, const uint64_t* src, const uint64_t* dommask, int n,
-                                               int nvec) {
-  uint32_t* w = reinterpret_cast<uint32_t*>(Ds);
-  for (int i = threadIdx.x; i < nvec * 4; i += blockDim.x) w[i] = 0xffffffffu;
+__device__ __forceinline__ void stage_from_u64(uint8_t* Db, const uint64_t* src, const uint64_t* dommask, int n,
+                                               int dbytes) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(Db);
+  for (int i = threadIdx.x; i < dbytes / 4; i += blockDim.x) w[i] = 0xffffffffu;
   __syncthreads();
-  uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
   // 4 independent loads per thread in flight (the whole of D for n <= 2048)
   for (int x0 = threadIdx.x; x0 < n; x0 += 4 * blockDim.x) {
     uint64_t v[4];
@@ -114,73 +134,88 @@ __device__ __forceinline__ void stage_from_u64(uint4* Ds, const uint64_t* src, c
 }
 
 // ---------------------------------------------------------------------------- fused
-template <int W, int G>
-__global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_fused(FusedParams p) {
   extern __shared__ uint4 Ds[];
   __shared__ int scratch[kThreads / 32];
+  __shared__ int s_last;
   const PassGeom& g = p.g;
-  uint16_t* vlist = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(Ds) + list_offset(g.nvec));
-  uint8_t* vneed = reinterpret_cast<uint8_t*>(Ds) + need_offset(g.nvec);
-  for (int i = threadIdx.x; i < g.nvec; i += blockDim.x) vneed[i] = 0;
-  stage_from_u64<W>(Ds, p.d_in, p.dommask, g.n, g.nvec);
   uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
-  const GroupIds id = group_ids<G>();
+  uint16_t* vlist = reinterpret_cast<uint16_t*>(Db + list_offset(g.dbytes));
+  uint8_t* vneed = Db + need_offset(g.dbytes, g.n);
+  // phase timestamps (debug): thread 0 of CTA 0 records %globaltimer
+  int nd = 0;
+  const bool dbg = p.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+#define RAC_MARK() do { if (dbg && nd < 255) p.dbg[1 + nd++] = globaltimer(); } while (0)
+  RAC_MARK();
+  for (int i = threadIdx.x; i < g.n; i += blockDim.x) vneed[i] = 0;
+  stage_from_u64<W>(Db, p.d_in, p.dommask, g.n, g.dbytes);
+  RAC_MARK();
+  const long warp0 = (long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const long nwarps = (long)gridDim.x * (blockDim.x / 32);
   const bool full = (p.flags & kFull) != 0;
-  int t = 0, status = kOK, vcnt = g.nvec;
+  int t = 0, status = kOK, vcnt = g.n;
   unsigned epoch = 0;
-  // Seeded call (Alg. 1 with @changed = seeds): pass 1 only re-tests the
-  // vectors holding the seed variables.
-  bool seeded = p.seeds != nullptr;
+  // Seeded call (Alg. 1 with @changed = seeds): pass 1 tests only the seed columns.
+  const bool seeded = p.seeds != nullptr;
   if (seeded) {
     for (int i = threadIdx.x; i < p.n_seeds; i += blockDim.x) {
       const int y = p.seeds[i];
-      if (y >= 0 && y < g.n) vneed[(y * W) >> 4] = 1;
+      if (y >= 0 && y < g.n) vneed[y] = 1;
     }
     __syncthreads();
-    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
+    vcnt = block_compact(vneed, vlist, g.n, scratch);
   }
   if (seeded && vcnt == 0) {  // empty @changed: no pass (status from D_in)
     int wipe = 0;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) wipe |= load_w<W>(Db + x * W) == 0;
     wipe = __syncthreads_or(wipe);
     status = wipe ? kWIPEOUT : kOK;
-  } else for (;;) {
-    ++t;
-    unsigned long long* Rc = p.R + (size_t)(t % 3) * g.n;
-    unsigned long long* Rn = p.R + (size_t)((t + 1) % 3) * g.n;
-    // R of pass t+1 was last read before the previous barrier: clear it now.
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
-    // pass 1 (and any pass where many variables changed) streams whole rows;
-    // otherwise only the vectors of variables changed in the previous pass.
-    const bool use_list = (t > 1 || seeded) && 2 * vcnt <= g.nvec && g.nvec <= 65535;
-    support_sweep<W, G>(g, Ds, Rc, p.removed_at, t, id.gidx, id.ngroups, id, use_list ? vlist : nullptr, vcnt);
-    grid_sync(p.bar, gridDim.x, ++epoch);
-    // D_t = D_{t-1} & ~R (every CTA, redundantly); flags for Alg. 1's checks.
-    int changed = 0, wipe = 0;
-    for (int x = threadIdx.x; x < g.n; x += blockDim.x) {
-      const uint64_t r = __ldcg(&Rc[x]);
-      const uint64_t dv = load_w<W>(Db + x * W);
-      const uint64_t nd = dv & ~r;
-      store_w<W>(Db + x * W, nd);
-      const bool chx = (dv & r) != 0;
-      changed |= chx;
-      wipe |= nd == 0;
-      if (chx) vneed[(x * W) >> 4] = 1;
+  } else {
+    for (;;) {
+      ++t;
+      unsigned long long* Rc = p.R + (size_t)(t % 3) * g.n;
+      unsigned long long* Rn = p.R + (size_t)((t + 1) % 3) * g.n;
+      // R of pass t+1 was last read before the previous barrier: clear it now.
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
+      const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
+      RAC_MARK();
+      column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
+      RAC_MARK();
+      grid_sync(p.bar, gridDim.x, ++epoch);
+      RAC_MARK();
+      // D_t = D_{t-1} & ~R (every CTA, redundantly); flags for Alg. 1's checks;
+      // the changed variables are the next pass's columns.
+      int changed = 0, wipe = 0;
+      for (int x = threadIdx.x; x < g.n; x += blockDim.x) {
+        const uint64_t r = __ldcg(&Rc[x]);
+        const uint64_t dv = load_w<W>(Db + x * W);
+        const uint64_t nd = dv & ~r;
+        store_w<W>(Db + x * W, nd);
+        const bool chx = (dv & r) != 0;
+        changed |= chx;
+        wipe |= nd == 0;
+        if (chx) vneed[x] = 1;
+      }
+      changed = __syncthreads_or(changed);
+      wipe = __syncthreads_or(wipe);
+      RAC_MARK();
+      vcnt = block_compact(vneed, vlist, g.n, scratch);
+      RAC_MARK();
+      if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
+      if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
     }
-    changed = __syncthreads_or(changed);
-    wipe = __syncthreads_or(wipe);
-    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
-    if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
-    if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
   }
   if (blockIdx.x == 0) {
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.d_out[x] = load_w<W>(Db + x * W);
     if (threadIdx.x == 0) { *p.iters = t; *p.status = status; }
   }
+  RAC_MARK();
+  if (dbg) p.dbg[0] = nd;
+#undef RAC_MARK
   // The last CTA out resets the barrier words and clears R[1] (the removal
   // buffer pass 1 of the next launch writes): every other CTA has finished
   // reading by the time it counts itself out.
-  __shared__ int s_last;
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = gridDim.x == 1 ? 1 : (atomicAdd(&p.bar[2], 1u) + 1u == gridDim.x);
@@ -199,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 2) rac_fused(FusedParams p) {
 }
 
 // ---------------------------------------------------------------------------- per-pass (sharded)
-__device__ __forceinline__ void tma_stage(uint4* dst, const uint8_t* src, uint32_t bytes, uint64_t* mbar) {
+__device__ __forceinline__ void tma_stage(uint8_t* dst, const uint8_t* src, uint32_t bytes, uint64_t* mbar) {
   // One elected thread arms the mbarrier with the byte count and issues bulk
   // copies (<= 32 KB each); every thread waits on phase 0.
   const uint32_t mb = (uint32_t)__cvta_generic_to_shared(mbar);
@@ -232,26 +267,28 @@ __device__ __forceinline__ void tma_stage(uint4* dst, const uint8_t* src, uint32
   }
 }
 
-template <int W, int G>
-__global__ void __launch_bounds__(kThreads, 2) rac_pass(PassParams p) {
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_pass(PassParams p) {
   extern __shared__ uint4 Ds[];
   __shared__ alignas(8) uint64_t mbar;
   if (*reinterpret_cast<volatile int32_t*>(p.s.done)) return;  // converged: speculative pass is a no-op
-  tma_stage(Ds, p.s.Dw, (uint32_t)p.g.row_stride, &mbar);
+  uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
+  tma_stage(Db, p.s.Dw, (uint32_t)p.g.dbytes, &mbar);
   const int t = *p.s.iters + 1;
   const int vcnt = *p.s.vcnt;
-  const bool use_list = t > 1 && 2 * vcnt <= p.g.nvec && p.g.nvec <= 65535;
-  uint16_t* vlist = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(Ds) + list_offset(p.g.nvec));
-  if (use_list) {
+  const bool lst = t > 1;
+  uint16_t* vlist = reinterpret_cast<uint16_t*>(Db + list_offset(p.g.dbytes));
+  if (lst) {
     for (int i = threadIdx.x; i < vcnt; i += blockDim.x) vlist[i] = p.s.vlist[i];
     __syncthreads();
   }
-  const GroupIds id = group_ids<G>();
-  support_sweep<W, G>(p.g, Ds, p.s.R, p.removed_at, t, id.gidx, id.ngroups, id, use_list ? vlist : nullptr, vcnt);
+  const long warp0 = (long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const long nwarps = (long)gridDim.x * (blockDim.x / 32);
+  column_sweep<W>(p.g, Db, p.s.R, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : p.g.n);
 }
 
-__global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
-                               int row_stride, int total_g) {
+__global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_t* dommask, int n, int W, int dbytes,
+                               int total_g) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total_g; i += gridDim.x * blockDim.x) {
     if (i < n) {
       const uint64_t v = d_in[i] & dommask[i];
@@ -261,7 +298,7 @@ __global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_
     }
     s.Dg[i] = 0ull;
   }
-  for (int b = n * W + blockIdx.x * blockDim.x + threadIdx.x; b < row_stride; b += gridDim.x * blockDim.x)
+  for (int b = n * W + blockIdx.x * blockDim.x + threadIdx.x; b < dbytes; b += gridDim.x * blockDim.x)
     s.Dw[b] = 0xffu;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *s.iters = 0;
@@ -287,13 +324,13 @@ __global__ void rac_shard_slice(ShardState s, int x_lo, int x_hi, int n) {
 
 // After the exchange: every rank derives the same flags from the gathered
 // vector (changed = D_t != D_{t-1}, wipe = some D_t(x) empty), the list of
-// vectors holding changed variables (Prop. 2 incremental next pass), and
-// advances.  One CTA; dynamic smem = nvec flag bytes.
-__global__ void __launch_bounds__(1024) rac_shard_update(ShardState s, int n, int W, int nvec, uint32_t flags) {
+// changed variables (the next pass's columns, Prop. 2), and advances.
+// One CTA; dynamic smem = n flag bytes.
+__global__ void __launch_bounds__(1024) rac_shard_update(ShardState s, int n, int W, uint32_t flags) {
   extern __shared__ uint8_t need[];
   __shared__ int scratch[32];
   if (*reinterpret_cast<volatile int32_t*>(s.done)) return;
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) need[i] = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) need[i] = 0;
   __syncthreads();
   int changed = 0, wipe = 0;
   for (int x = threadIdx.x; x < n; x += blockDim.x) {
@@ -301,13 +338,13 @@ __global__ void __launch_bounds__(1024) rac_shard_update(ShardState s, int n, in
     const bool chx = nv != s.Dcur[x];
     changed |= chx;
     wipe |= nv == 0;
-    if (chx) need[(x * W) >> 4] = 1;
+    if (chx) need[x] = 1;
     s.Dcur[x] = nv;
     for (int k = 0; k < W; ++k) s.Dw[(size_t)x * W + k] = (uint8_t)(nv >> (8 * k));
   }
   changed = __syncthreads_or(changed);
   wipe = __syncthreads_or(wipe);
-  const int cnt = nvec <= 65535 ? block_compact(need, s.vlist, nvec, scratch) : nvec;
+  const int cnt = block_compact(need, s.vlist, n, scratch);
   if (threadIdx.x == 0) {
     *s.vcnt = cnt;
     *s.iters += 1;
@@ -329,54 +366,38 @@ __global__ void rac_shard_finalize(ShardState s, int n, uint64_t* d_out, int32_t
   }
 }
 
-// ---------------------------------------------------------------------------- batched
-// One CTA per state: D and R live in smem, __syncthreads is the pass barrier,
-// each state stops at its own pass (freeze-on-stop).  The relation rows are
-// shared by all states and stay L2-resident.
-template <int W, int G>
-__global__ void __launch_bounds__(kThreads, 2) rac_batch(BatchParams p) {
+// ---------------------------------------------------------------------------- batched (per state)
+// One CTA per state: D, the column list and R live in smem, __syncthreads is
+// the pass barrier, each state stops at its own pass (freeze-on-stop).  The
+// relation is shared by all states and stays L2-resident.
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_batch(BatchParams p) {
   extern __shared__ uint4 Ds[];
   __shared__ int scratch[kThreads / 32];
   const PassGeom& g = p.g;
   const int s = blockIdx.x;
-  uint16_t* vlist = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(Ds) + list_offset(g.nvec));
-  uint8_t* vneed = reinterpret_cast<uint8_t*>(Ds) + need_offset(g.nvec);
-  unsigned long long* R = reinterpret_cast<unsigned long long*>(reinterpret_cast<uint8_t*>(Ds) + fused_smem(g.nvec));
-  for (int i = threadIdx.x; i < g.nvec; i += blockDim.x) vneed[i] = 0;
-  stage_from_u64<W>(Ds, p.d_in + (size_t)s * g.n, p.dommask, g.n, g.nvec);
   uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gw = lane / G;
-  GroupIds id;
-  id.gl = lane % G;
-  id.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (gw * G));
-  id.gidx = warp * (32 / G) + gw;
-  id.ngroups = (long)(blockDim.x / 32) * (32 / G);
+  uint16_t* vlist = reinterpret_cast<uint16_t*>(Db + list_offset(g.dbytes));
+  uint8_t* vneed = Db + need_offset(g.dbytes, g.n);
+  unsigned long long* R = reinterpret_cast<unsigned long long*>(Db + fused_smem(g.dbytes, g.n));
+  for (int i = threadIdx.x; i < g.n; i += blockDim.x) vneed[i] = 0;
+  stage_from_u64<W>(Db, p.d_in + (size_t)s * g.n, p.dommask, g.n, g.dbytes);
+  const long warp0 = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const bool full = (p.flags & kFull) != 0;
-  int t = 0, status = kOK, vcnt = g.nvec;
+  int t = 0, status = kOK, vcnt = g.n;
   const int seed = p.seed_var ? p.seed_var[s] : -1;
   const bool seeded = seed >= 0 && seed < g.n;
   if (seeded) {
-    if (threadIdx.x == 0) vneed[(seed * W) >> 4] = 1;
+    if (threadIdx.x == 0) vneed[seed] = 1;
     __syncthreads();
-    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
+    vcnt = block_compact(vneed, vlist, g.n, scratch);
   }
   for (;;) {
     ++t;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) R[x] = 0ull;
     __syncthreads();
-    const bool use_list = (t > 1 || seeded) && 2 * vcnt <= g.nvec && g.nvec <= 65535;
-    {
-      const long rows = (long)g.n * g.dmax;
-      for (long r = id.gidx; r < rows; r += id.ngroups) {
-        const int x = (int)(r / g.dmax), a = (int)(r - (long)x * g.dmax);
-        if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;
-        const uint4* row = reinterpret_cast<const uint4*>(g.M + (size_t)r * g.row_stride);
-        const uint32_t* Prow = g.P + (size_t)x * g.pw;
-        const bool f = use_list ? row_fails_list<W, G>(row, Ds, vlist, 0, vcnt, id.gl, id.gmask, g.n, Prow)
-                                : row_fails<W, G>(row, Ds, 0, g.nvec, id.gl, id.gmask, g.n, Prow);
-        if (f && id.gl == 0) atomicOr(&R[x], 1ull << a);  // shared-memory u64 atomic
-      }
-    }
+    const bool lst = seeded || t > 1;
+    column_sweep<W>(g, Db, R, nullptr, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
     __syncthreads();
     int changed = 0, wipe = 0;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) {
@@ -387,11 +408,11 @@ __global__ void __launch_bounds__(kThreads, 2) rac_batch(BatchParams p) {
       const bool chx = (dv & r) != 0;
       changed |= chx;
       wipe |= nd == 0;
-      if (chx) vneed[(x * W) >> 4] = 1;
+      if (chx) vneed[x] = 1;
     }
     changed = __syncthreads_or(changed);
     wipe = __syncthreads_or(wipe);
-    vcnt = block_compact(vneed, vlist, g.nvec, scratch);
+    vcnt = block_compact(vneed, vlist, g.n, scratch);
     if (wipe && !full) { status = kWIPEOUT; break; }
     if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }
   }
@@ -402,124 +423,82 @@ __global__ void __launch_bounds__(kThreads, 2) rac_batch(BatchParams p) {
   }
 }
 
-template <template <int, int> class F, typename... A>
-cudaError_t dispatch(int W, int G, A&&... a) {
-#define RAC_CASE_G(WW)                                        \
-  switch (G) {                                                \
-    case 1: return F<WW, 1>::run(a...);                       \
-    case 2: return F<WW, 2>::run(a...);                       \
-    case 4: return F<WW, 4>::run(a...);                       \
-    case 8: return F<WW, 8>::run(a...);                       \
-    case 16: return F<WW, 16>::run(a...);                     \
-    case 32: return F<WW, 32>::run(a...);                     \
-    default: return cudaErrorInvalidValue;                    \
-  }
-  switch (W) {
-    case 1: RAC_CASE_G(1)
-    case 2: RAC_CASE_G(2)
-    case 4: RAC_CASE_G(4)
-    case 8: RAC_CASE_G(8)
-    default: return cudaErrorInvalidValue;
-  }
-#undef RAC_CASE_G
+template <typename K>
+cudaError_t set_smem(K k, size_t smem) {
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <int W, int G>
-struct FusedLaunch {
-  static cudaError_t run(const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
-    auto k = rac_fused<W, G>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (coop) {
-      FusedParams pp = p;
-      void* args[] = {&pp};
-      return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kThreads), args, smem, s);
-    }
-    k<<<grid, kThreads, smem, s>>>(p);
-    return cudaGetLastError();
+template <int W>
+cudaError_t launch_fused_w(const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
+  auto k = rac_fused<W>;
+  cudaError_t e = set_smem(k, smem);
+  if (e != cudaSuccess) return e;
+  if (coop) {
+    FusedParams pp = p;
+    void* args[] = {&pp};
+    return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kThreads), args, smem, s);
   }
-};
+  k<<<grid, kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
 
-template <int W, int G>
-struct FusedOcc {
-  static cudaError_t run(size_t smem, int* out) {
-    auto k = rac_fused<W, G>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
-  }
-};
+template <int W>
+cudaError_t occ_w(int which, size_t smem, int* out) {
+  const void* k = which == 0 ? (const void*)rac_fused<W> : which == 1 ? (const void*)rac_pass<W>
+                                                                      : (const void*)rac_batch<W>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
+}
 
-template <int W, int G>
-struct PassLaunch {
-  static cudaError_t run(const PassParams& p, int grid, size_t smem, cudaStream_t s) {
-    auto k = rac_pass<W, G>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k<<<grid, kThreads, smem, s>>>(p);
-    return cudaGetLastError();
-  }
-};
+template <int W>
+cudaError_t launch_pass_w(const PassParams& p, int grid, size_t smem, cudaStream_t s) {
+  auto k = rac_pass<W>;
+  cudaError_t e = set_smem(k, smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
 
-template <int W, int G>
-struct PassOcc {
-  static cudaError_t run(size_t smem, int* out) {
-    auto k = rac_pass<W, G>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
-  }
-};
-
-template <int W, int G>
-struct BatchLaunch {
-  static cudaError_t run(const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
-    auto k = rac_batch<W, G>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k<<<n_states, kThreads, smem, s>>>(p);
-    return cudaGetLastError();
-  }
-};
-
-template <int W, int G>
-struct BatchOcc {
-  static cudaError_t run(size_t smem, int* out) {
-    auto k = rac_batch<W, G>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
-  }
-};
+template <int W>
+cudaError_t launch_batch_w(const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
+  auto k = rac_batch<W>;
+  cudaError_t e = set_smem(k, smem);
+  if (e != cudaSuccess) return e;
+  k<<<n_states, kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
 
 }  // namespace
 
-int choose_group(int nvec) {
-  // smallest power of two G with G * kUnroll >= nvec, capped at a warp
-  int G = 1;
-  while (G < 32 && G * kUnroll < nvec) G *= 2;
-  return G;
-}
+#define RAC_W_SWITCH(W, EXPR_T)                          \
+  switch (W) {                                           \
+    case 1: { constexpr int WW = 1; return EXPR_T; }     \
+    case 2: { constexpr int WW = 2; return EXPR_T; }     \
+    case 4: { constexpr int WW = 4; return EXPR_T; }     \
+    case 8: { constexpr int WW = 8; return EXPR_T; }     \
+    default: return cudaErrorInvalidValue;               \
+  }
 
-cudaError_t launch_fused(int W, int G, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
-  return dispatch<FusedLaunch>(W, G, p, grid, smem, s, coop);
+cudaError_t launch_fused(int W, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
+  RAC_W_SWITCH(W, launch_fused_w<WW>(p, grid, smem, s, coop))
 }
-cudaError_t fused_occupancy(int W, int G, size_t smem, int* out) { return dispatch<FusedOcc>(W, G, smem, out); }
-cudaError_t launch_pass(int W, int G, const PassParams& p, int grid, size_t smem, cudaStream_t s) {
-  return dispatch<PassLaunch>(W, G, p, grid, smem, s);
+cudaError_t fused_occupancy(int W, size_t smem, int* out) { RAC_W_SWITCH(W, occ_w<WW>(0, smem, out)) }
+cudaError_t launch_pass(int W, const PassParams& p, int grid, size_t smem, cudaStream_t s) {
+  RAC_W_SWITCH(W, launch_pass_w<WW>(p, grid, smem, s))
 }
-cudaError_t pass_occupancy(int W, int G, size_t smem, int* out) { return dispatch<PassOcc>(W, G, smem, out); }
-cudaError_t launch_batch(int W, int G, const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
-  return dispatch<BatchLaunch>(W, G, p, n_states, smem, s);
+cudaError_t pass_occupancy(int W, size_t smem, int* out) { RAC_W_SWITCH(W, occ_w<WW>(1, smem, out)) }
+cudaError_t launch_batch(int W, const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
+  RAC_W_SWITCH(W, launch_batch_w<WW>(p, n_states, smem, s))
 }
-cudaError_t batch_occupancy(int W, int G, size_t smem, int* out) { return dispatch<BatchOcc>(W, G, smem, out); }
+cudaError_t batch_occupancy(int W, size_t smem, int* out) { RAC_W_SWITCH(W, occ_w<WW>(2, smem, out)) }
 
 cudaError_t launch_shard_init(const ShardState& s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
-                              size_t row_stride, int total_g, cudaStream_t st) {
-  int work = total_g > (int)row_stride ? total_g : (int)row_stride;
+                              int dbytes, int total_g, cudaStream_t st) {
+  int work = total_g > dbytes ? total_g : dbytes;
   int grid = (work + 255) / 256;
   if (grid > 1024) grid = 1024;
-  rac_shard_init<<<grid, 256, 0, st>>>(s, d_in, dommask, n, W, (int)row_stride, total_g);
+  rac_shard_init<<<grid, 256, 0, st>>>(s, d_in, dommask, n, W, dbytes, total_g);
   return cudaGetLastError();
 }
 cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, cudaStream_t st) {
@@ -529,12 +508,12 @@ cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, c
   rac_shard_slice<<<grid, 256, 0, st>>>(s, x_lo, x_hi, n);
   return cudaGetLastError();
 }
-cudaError_t launch_shard_update(const ShardState& s, int n, int W, int nvec, uint32_t flags, cudaStream_t st) {
-  if (nvec > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(rac_shard_update, cudaFuncAttributeMaxDynamicSharedMemorySize, nvec);
+cudaError_t launch_shard_update(const ShardState& s, int n, int W, uint32_t flags, cudaStream_t st) {
+  if (n > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(rac_shard_update, cudaFuncAttributeMaxDynamicSharedMemorySize, n);
     if (e != cudaSuccess) return e;
   }
-  rac_shard_update<<<1, 1024, nvec, st>>>(s, n, W, nvec, flags);
+  rac_shard_update<<<1, 1024, n, st>>>(s, n, W, flags);
   return cudaGetLastError();
 }
 cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, int32_t* iters, int32_t* status,

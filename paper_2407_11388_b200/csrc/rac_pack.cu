@@ -2,7 +2,8 @@
 //
 // "Prepare Cons" (Fig. 1): the paper stores
 // Cons ∈ {0,1}^{n×n×d×d} in fp32.  Here each support set c_xy|(x,a)
-// (line 45) becomes one W-byte mask M[x][a][y]; both orientations are stored,
+// (line 45) becomes one W-byte mask in column y at row (x,a) of the column-major
+// tensor (rac_internal.cuh); both orientations are stored,
 // the (y,x) one being the bit-transpose built with warp ballots.  Absent pairs
 // and y == x keep the all-ones fill (cudaMemset 0xFF) and presence bit 0.
 #include <cuda_runtime.h>
@@ -15,8 +16,9 @@ namespace rac {
 
 namespace {
 
+// column-major: mask c_xy|(x,a) lives in column y at local row (x - x_lo)*dmax + a
 __device__ __forceinline__ void store_mask(const PackGeom& g, int x, int a, int y, uint64_t m) {
-  uint8_t* p = g.M + ((size_t)(x - g.x_lo) * g.dmax + a) * g.row_stride + (size_t)y * g.W;
+  uint8_t* p = g.M + (size_t)y * g.col_stride + ((size_t)(x - g.x_lo) * g.dmax + a) * g.W;
   switch (g.W) {
     case 8: *reinterpret_cast<uint64_t*>(p) = m; break;
     case 4: *reinterpret_cast<uint32_t*>(p) = (uint32_t)m; break;

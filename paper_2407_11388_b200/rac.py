@@ -17,7 +17,7 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librac.so")
+LIB_PATH = os.environ.get("RAC_LIB_PATH") or os.path.join(_HERE, "librac.so")  # override: A/B tooling
 
 RAC_OK = 0
 RAC_WIPEOUT = 1
