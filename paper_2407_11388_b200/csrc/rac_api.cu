@@ -72,7 +72,10 @@ struct rac_ctx {
   std::vector<int32_t> dom;
   std::vector<uint64_t> dommask_h;
   // device
-  uint8_t* M = nullptr;
+  uint8_t* M = nullptr;     // column-major masks
+  uint8_t* Mr = nullptr;    // row-major copy (nullable)
+  int G = 1;                // lanes per row of the row-major sweep
+  int force_layout = 0;     // RAC_FORCE_LAYOUT=rows|cols (testing knob)
   uint32_t* P = nullptr;
   int32_t* dom_d = nullptr;
   uint64_t* dommask = nullptr;
@@ -132,6 +135,7 @@ void free_ctx(rac_ctx* c) {
   if (c->device >= 0) cudaSetDevice(c->device);
   if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
   cudaFree(c->M);
+  cudaFree(c->Mr);
   cudaFree(c->P);
   cudaFree(c->dom_d);
   cudaFree(c->dommask);
@@ -208,6 +212,23 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   } while (0)
   CKC(cudaMalloc(&c->M, std::max<size_t>(mbytes, 16)));
   CKC(cudaMemsetAsync(c->M, 0xFF, std::max<size_t>(mbytes, 16), c->stream));
+  {
+    // Row-major copy for full passes (dead-row skip, early exit).  Optional:
+    // without room for it every pass uses the column-major tensor.
+    const size_t rbytes = (size_t)c->rows_pad * c->dbytes;
+    const char* fl = getenv("RAC_FORCE_LAYOUT");
+    c->force_layout = fl ? (strcmp(fl, "rows") == 0 ? 1 : strcmp(fl, "cols") == 0 ? 2 : 0) : 0;
+    const char* nr = getenv("RAC_NO_ROW_LAYOUT");
+    if (!(nr && *nr && strcmp(nr, "0") != 0) && c->force_layout != 2) {
+      if (cudaMalloc(&c->Mr, rbytes) != cudaSuccess) {
+        cudaGetLastError();
+        c->Mr = nullptr;
+      } else {
+        CKC(cudaMemsetAsync(c->Mr, 0xFF, rbytes, c->stream));
+      }
+    }
+    c->G = choose_group(c->dbytes / 16);
+  }
   CKC(cudaMalloc(&c->P, std::max<size_t>(local_vars * c->pw * 4, 4)));
   CKC(cudaMemsetAsync(c->P, 0, std::max<size_t>(local_vars * c->pw * 4, 4), c->stream));
   CKC(cudaMalloc(&c->dom_d, (size_t)n * 4));
@@ -243,13 +264,13 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   const long slabs = c->rows_pad / slab_rows(c->W);
   const long items = slabs * ((n + kUnroll - 1) / kUnroll);
   int occ = 0;
-  CKC(fused_occupancy(c->W, fused_smem(c->dbytes, n), &occ));
+  CKC(fused_occupancy(c->W, c->G, fused_smem(c->dbytes, n), &occ));
   if (occ < 1) return fail(nullptr, RAC_EUNSUPPORTED, "support-pass kernel does not fit on an SM (n too large)");
   // about one item per warp (small problems are latency-bound: spread them)
   const long want = (items + (kThreads / 32) - 1) / (kThreads / 32);
   c->fused_grid = (int)std::max(1L, std::min((long)c->sm_count * occ, want));
   int pocc = 0;
-  CKC(pass_occupancy(c->W, fused_smem(c->dbytes, n), &pocc));
+  CKC(pass_occupancy(c->W, c->G, fused_smem(c->dbytes, n), &pocc));
   c->pass_grid = (int)std::max(1L, std::min((long)c->sm_count * std::max(1, pocc), want));
   CKC(cudaStreamSynchronize(c->stream));
 #undef CKC
@@ -260,6 +281,8 @@ PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi) {
   PassGeom g{};
   g.M = c->M;
   g.col_stride = c->col_stride;
+  g.Mr = c->Mr;
+  g.force = c->force_layout;
   g.n = c->n;
   g.dmax = c->dmax;
   g.x_lo = x_lo;
@@ -299,7 +322,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   // R[1] (pass 1's removal buffer) is clean: zeroed at create and by the last
   // CTA of every previous launch.
   static const bool no_coop = getenv("RAC_NO_COOP") != nullptr;  // A/B knob (tooling only)
-  CK(c, launch_fused(c->W, p, c->fused_grid, fused_smem(c->dbytes, c->n), s, c->fused_grid > 1 && !no_coop));
+  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, fused_smem(c->dbytes, c->n), s, c->fused_grid > 1 && !no_coop));
   c->launches++;
   return 0;
 }
@@ -328,7 +351,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
     for (int k = 0; k < chunk; ++k) {
       for (int b = 0; b < nb; ++b) {
         if (pp[b].g.x_hi <= pp[b].g.x_lo) continue;
-        CK(c, launch_pass(c->W, pp[b], c->pass_grid, fused_smem(c->dbytes, c->n), s));
+        CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, fused_smem(c->dbytes, c->n), s));
         c->launches++;
       }
       if (c->world > 1) {
@@ -456,7 +479,8 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
     if (e == cudaSuccess) e = cudaMemcpy(dxs, xs.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(dys, ys.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice);
-    PackGeom g{c->M, c->col_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
+    PackGeom g{c->M, c->col_stride, c->Mr, (size_t)c->dbytes, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw,
+               c->dom_d};
     if (e == cudaSuccess) e = launch_pack_relations(g, dxs, dys, drows, n_rel, dmax, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     cudaFree(dxs);
@@ -483,7 +507,8 @@ int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q
   rac_ctx* c = new rac_ctx();
   int rc = setup_ctx(c, n_vars, dom.data(), opt);
   if (rc) { free_ctx(c); return rc; }
-  PackGeom g{c->M, c->col_stride, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw, c->dom_d};
+  PackGeom g{c->M, c->col_stride, c->Mr, (size_t)c->dbytes, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw,
+               c->dom_d};
   cudaError_t e = launch_generate(g, d, dens_q32, t_q16, seed, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
@@ -679,9 +704,9 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   p.flags = flags;
   const size_t smem1 = fused_smem(c->dbytes, c->n) + (size_t)c->n * 8;
   int occ1 = 0;
-  CK(c, batch_occupancy(c->W, smem1, &occ1));
+  CK(c, batch_occupancy(c->W, c->G, smem1, &occ1));
   if (occ1 < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");
-  CK(c, launch_batch(c->W, p, n_states, smem1, st));
+  CK(c, launch_batch(c->W, c->G, p, n_states, smem1, st));
   c->launches = 1;
   return 0;
 }
@@ -690,7 +715,7 @@ int32_t rac_n_vars(const rac_ctx* c) { return c ? c->n : RAC_EINVAL; }
 int32_t rac_max_dom(const rac_ctx* c) { return c ? c->dmax : RAC_EINVAL; }
 int32_t rac_mask_bytes(const rac_ctx* c) { return c ? c->W : RAC_EINVAL; }
 int64_t rac_relation_bytes(const rac_ctx* c) {
-  return c ? (int64_t)c->n * (int64_t)c->col_stride : RAC_EINVAL;
+  return c ? (int64_t)c->n * (int64_t)c->col_stride + (c->Mr ? (int64_t)c->rows_pad * c->dbytes : 0) : RAC_EINVAL;
 }
 int64_t rac_last_launch_count(const rac_ctx* c) { return c ? c->launches : RAC_EINVAL; }
 

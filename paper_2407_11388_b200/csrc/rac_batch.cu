@@ -155,11 +155,25 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
       nb = cur;
       if (live) {
         uint32_t acc = 0xffffffffu;
-        for (int k = 0; k < ncol; ++k) {
-          const int y = list[k];
-          uint32_t sup = 0;
-          if constexpr (W == 8) {
-            const uint64_t m = load_mask64(Mrow + (size_t)y * p.col_stride);
+        // kBU mask loads in flight per thread, then the table lookups
+        constexpr int kBU = 8;
+        for (int k0 = 0; k0 < ncol && (acc & live) != 0; k0 += kBU) {
+          uint64_t mv[kBU];
+          int yv[kBU];
+#pragma unroll
+          for (int u = 0; u < kBU; ++u) {
+            yv[u] = k0 + u < ncol ? list[k0 + u] : -1;
+            if (yv[u] >= 0) {
+              if constexpr (W == 8) mv[u] = load_mask64(Mrow + (size_t)yv[u] * p.col_stride);
+              else mv[u] = load_mask<W>(Mrow + (size_t)yv[u] * p.col_stride);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kBU; ++u) {
+            const int y = yv[u];
+            if (y < 0) continue;
+            const uint64_t m = mv[u];
+            uint32_t sup = 0;
             if (p.use_table) {
 #pragma unroll
               for (int q = 0; q < NQ; ++q) sup |= T[((size_t)y * NQ + q) * 16 + ((m >> (4 * q)) & 15u)];
@@ -171,27 +185,13 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
                 mm &= mm - 1;
               }
             }
-          } else {
-            const uint32_t m = load_mask<W>(Mrow + (size_t)y * p.col_stride);
-            if (p.use_table) {
-#pragma unroll
-              for (int q = 0; q < NQ; ++q) sup |= T[((size_t)y * NQ + q) * 16 + ((m >> (4 * q)) & 15u)];
-            } else {
-              uint32_t mm = m & (p.dmax >= 32 ? ~0u : ((1u << p.dmax) - 1u));
-              while (mm) {
-                const int b = __ffs(mm) - 1;
-                sup |= X[y * p.dmax + b];
-                mm &= mm - 1;
-              }
+            if ((sup & live) != live) {
+              // some live state lost support on column y: only a declared c_xy
+              // removes (absent pairs and y == x store all-ones; reading R2)
+              if (!((__ldg(Prow + (y >> 5)) >> (y & 31)) & 1u)) sup = 0xffffffffu;
             }
+            acc &= sup;
           }
-          if ((sup & live) != live) {
-            // some live state lost support on column y: only a declared c_xy
-            // removes (absent pairs and y == x store all-ones; reading R2)
-            if (!((__ldg(Prow + (y >> 5)) >> (y & 31)) & 1u)) sup = 0xffffffffu;
-          }
-          acc &= sup;
-          if ((acc & live) == 0) break;
         }
         nb = cur & (acc | ~active);
       }

@@ -10,6 +10,11 @@
 //              y == x hold all-ones; padding rows hold 0xFF.  Reading the columns
 //              of the changed variables is Alg. 1's Cons[:, @changed] gather
 //               as contiguous streams.
+//   Mr         optional ROW-major copy: row r = n W-byte masks M[(x,a)][y], padded
+//              to dbytes (16-byte multiple, 0xFF); a full pass over the live rows
+//              streams whole rows with per-row early exit and dead-row skip.
+//              Each pass picks the layout that reads fewer bytes (live rows x n
+//              vs all rows x changed columns).
 //   P          presence bitmap, [local x][pw = ceil(n/32)] u32; bit y of
 //              variable x set iff c_xy is declared (C_x).
 //   D (smem)   the alive bitvector D_t, variable y at bytes [y*W, y*W+W),
@@ -27,7 +32,22 @@ namespace rac {
 #define RAC_THREADS 512
 #endif
 constexpr int kThreads = RAC_THREADS;  // CTA size of the support-pass kernels
-constexpr int kUnroll = 8;     // 16-byte column loads in flight per lane
+#ifndef RAC_MIN_BLOCKS
+#define RAC_MIN_BLOCKS 1
+#endif
+constexpr int kMinBlocks = RAC_MIN_BLOCKS;  // CTAs per SM the register budget is sized for
+#ifndef RAC_UNROLL_C
+#define RAC_UNROLL_C 8
+#endif
+#ifndef RAC_UNROLL_L
+#define RAC_UNROLL_L 8
+#endif
+constexpr int kUnroll = RAC_UNROLL_C;   // 16-byte column loads in flight per lane (contiguous columns)
+constexpr int kUnrollL = RAC_UNROLL_L;  // ... listed columns (an index each)
+#ifndef RAC_UNROLL_R
+#define RAC_UNROLL_R 8
+#endif
+constexpr int kUnrollR = RAC_UNROLL_R;  // 16-byte row loads in flight per lane (row-major sweep)
 
 __host__ __device__ constexpr int slab_rows(int W) { return 32 * (16 / W); }
 
@@ -35,6 +55,8 @@ __host__ __device__ constexpr int slab_rows(int W) { return 32 * (16 / W); }
 struct PassGeom {
   const uint8_t* M;       // column-major masks of the local rows
   size_t col_stride;      // bytes per column = rows_pad * W
+  const uint8_t* Mr;      // nullable: row-major copy (row stride dbytes)
+  int force;              // 0 = pick per pass, 1 = rows, 2 = columns (testing knob)
   int n;                  // variables (= columns)
   int dmax;               // rows per variable
   int x_lo, x_hi;         // rows of variables [x_lo, x_hi) are tested
@@ -123,18 +145,19 @@ __host__ __device__ constexpr size_t fused_smem(int dbytes, int n) {
 
 // ---------------------------------------------------------------------------- host launchers
 // (defined in rac_kernels.cu / rac_pack.cu; return cudaError_t of the launch)
-cudaError_t launch_fused(int W, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool cooperative);
-cudaError_t fused_occupancy(int W, size_t smem, int* blocks_per_sm);
-cudaError_t launch_pass(int W, const PassParams& p, int grid, size_t smem, cudaStream_t s);
-cudaError_t pass_occupancy(int W, size_t smem, int* blocks_per_sm);
+int choose_group(int nvec);  // lanes per row of the row-major sweep
+cudaError_t launch_fused(int W, int G, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool cooperative);
+cudaError_t fused_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
+cudaError_t launch_pass(int W, int G, const PassParams& p, int grid, size_t smem, cudaStream_t s);
+cudaError_t pass_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
 cudaError_t launch_shard_init(const ShardState& s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
                               int dbytes, int total_g, cudaStream_t st);
 cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, cudaStream_t st);
 cudaError_t launch_shard_update(const ShardState& s, int n, int W, uint32_t flags, cudaStream_t st);
 cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, int32_t* iters, int32_t* status,
                                   cudaStream_t st);
-cudaError_t launch_batch(int W, const BatchParams& p, int n_states, size_t smem, cudaStream_t s);
-cudaError_t batch_occupancy(int W, size_t smem, int* blocks_per_sm);
+cudaError_t launch_batch(int W, int G, const BatchParams& p, int n_states, size_t smem, cudaStream_t s);
+cudaError_t batch_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
 size_t batch_bs_smem(int n, int dmax, int W, bool use_table);
 cudaError_t batch_bs_occupancy(int W, size_t smem, int* blocks_per_sm);
 cudaError_t launch_batch_bs(int W, const BatchBSParams& p, int grid, size_t smem, cudaStream_t s);
@@ -142,6 +165,8 @@ cudaError_t launch_batch_bs(int W, const BatchBSParams& p, int grid, size_t smem
 struct PackGeom {
   uint8_t* M;             // column-major masks of the local rows
   size_t col_stride;
+  uint8_t* Mr;            // nullable row-major copy
+  size_t row_bytes;       // = dbytes
   int W;
   int n, dmax;
   int x_lo, x_hi;         // local block
@@ -245,6 +270,83 @@ __device__ __forceinline__ uint32_t column_fail(uint4 m, uint64_t d, uint32_t ca
     if ((P[(size_t)xl * pw + (y >> 5)] >> (y & 31)) & 1u) f |= 1u << i;
   }
   return f;
+}
+
+// ---- row-major sweep helpers
+// Does any W-byte lane of t equal zero?  (t = mask & D, 16 bytes = 16/W masks)
+template <int W>
+__device__ __forceinline__ bool vec_any_zero(uint4 t) {
+  if constexpr (W == 8) {
+    return ((t.x | t.y) == 0u) | ((t.z | t.w) == 0u);
+  } else if constexpr (W == 4) {
+    return (t.x == 0u) | (t.y == 0u) | (t.z == 0u) | (t.w == 0u);
+  } else if constexpr (W == 2) {
+    return (__vcmpeq2(t.x, 0u) | __vcmpeq2(t.y, 0u) | __vcmpeq2(t.z, 0u) | __vcmpeq2(t.w, 0u)) != 0u;
+  } else {
+    return (__vcmpeq4(t.x, 0u) | __vcmpeq4(t.y, 0u) | __vcmpeq4(t.z, 0u) | __vcmpeq4(t.w, 0u)) != 0u;
+  }
+}
+
+// A 16-byte vector v of row (x,a) had some mask & D == 0: is it a real loss of
+// support?  Only on a declared c_xy (reading R2); padding lanes never fail.
+template <int W>
+__device__ __noinline__ bool vec_real_fail(uint4 m, uint4 d, int v, int n, const uint32_t* Prow) {
+  constexpr int L = 16 / W;
+  const uint32_t mw[4] = {m.x, m.y, m.z, m.w}, dw[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const int y = v * L + i;
+    if (y >= n) break;
+    uint64_t mi, di;
+    if (W == 8) {
+      mi = (uint64_t)mw[2 * i] | ((uint64_t)mw[2 * i + 1] << 32);
+      di = (uint64_t)dw[2 * i] | ((uint64_t)dw[2 * i + 1] << 32);
+    } else {
+      const int sh = (8 * W * i) & 31, k = (W * i) >> 2;
+      const uint32_t msk = W == 4 ? 0xffffffffu : ((1u << (8 * W)) - 1u);
+      mi = (mw[k] >> sh) & msk;
+      di = (dw[k] >> sh) & msk;
+    }
+    if ((mi & di) == 0) {
+      if (di != 0) return true;
+      if ((Prow[y >> 5] >> (y & 31)) & 1u) return true;
+    }
+  }
+  return false;
+}
+
+template <int G>
+__device__ __forceinline__ bool group_any(bool f, unsigned gmask) {
+  if constexpr (G == 32) return __any_sync(0xffffffffu, f);
+  else if constexpr (G == 1) return f;
+  else return (__ballot_sync(gmask, f) & gmask) != 0u;
+}
+
+// Support test of one (x,a) row segment [vb, ve) (16-byte vectors) against D
+// in smem: true iff some declared c_xy has c_xy|(x,a) ∩ D(y) = ∅ (Eq. 1
+// condition).  G lanes cooperate, kUnrollR loads per lane in flight, early exit.
+template <int W, int G>
+__device__ __forceinline__ bool row_fails(const uint4* __restrict__ row, const uint4* Ds, int vb, int ve, int gl,
+                                          unsigned gmask, int n, const uint32_t* Prow) {
+  bool fail = false;
+  for (int v0 = vb; v0 < ve; v0 += G * kUnrollR) {
+    uint4 m[kUnrollR];
+#pragma unroll
+    for (int u = 0; u < kUnrollR; ++u) {
+      const int v = v0 + u * G + gl;
+      if (v < ve) m[u] = ldg_stream(row + v);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnrollR; ++u) {
+      const int v = v0 + u * G + gl;
+      if (v < ve) {
+        const uint4 d = Ds[v];
+        if (vec_any_zero<W>(and4(m[u], d))) fail |= vec_real_fail<W>(m[u], d, v, n, Prow);
+      }
+    }
+    if (group_any<G>(fail, gmask)) return true;
+  }
+  return false;
 }
 
 // Block-wide compaction of the flags need[0, cnt) into the ascending index

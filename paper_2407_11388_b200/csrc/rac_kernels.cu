@@ -83,20 +83,42 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
     uint32_t fail = 0;
     const int c0 = chunk * yc, c1 = min(c0 + yc, ncol);
     const uint8_t* base = g.M + (size_t)r0 * W;
-    for (int c = c0; c < c1 && fail != cand; c += kUnroll) {
-      uint4 m[kUnroll];
-      int yy[kUnroll];
+    if (cols == nullptr) {
+      // contiguous columns c0..c1-1: running pointer, no index array
+      const uint8_t* pc = base + (size_t)c0 * g.col_stride;
+      for (int c = c0; c < c1 && fail != cand; c += kUnroll) {
+        uint4 m[kUnroll];
+        const uint8_t* q = pc;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int cc = c + u;
-        yy[u] = cc < c1 ? (cols ? (int)cols[cc] : cc) : -1;
-        if (yy[u] >= 0) m[u] = ldg_stream(reinterpret_cast<const uint4*>(base + (size_t)yy[u] * g.col_stride));
+        for (int u = 0; u < kUnroll; ++u) {
+          if (c + u < c1) m[u] = ldg_stream(reinterpret_cast<const uint4*>(q));
+          q += g.col_stride;
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          if (c + u < c1) {
+            const uint64_t d = load_w<W>(Db + (c + u) * W);
+            fail |= column_fail<W>(m[u], d, cand & ~fail, c + u, r0, g.dmax, g.P, g.pw);
+          }
+        }
+        pc = q;
       }
+    } else {
+      constexpr int UL = kUnrollL;  // listed columns: an index each
+      for (int c = c0; c < c1 && fail != cand; c += UL) {
+        uint4 m[UL];
+        int yy[UL];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        if (yy[u] >= 0) {
-          const uint64_t d = load_w<W>(Db + yy[u] * W);
-          fail |= column_fail<W>(m[u], d, cand & ~fail, yy[u], r0, g.dmax, g.P, g.pw);
+        for (int u = 0; u < UL; ++u) {
+          yy[u] = c + u < c1 ? (int)cols[c + u] : -1;
+          if (yy[u] >= 0) m[u] = ldg_stream(reinterpret_cast<const uint4*>(base + (size_t)yy[u] * g.col_stride));
+        }
+#pragma unroll
+        for (int u = 0; u < UL; ++u) {
+          if (yy[u] >= 0) {
+            const uint64_t d = load_w<W>(Db + yy[u] * W);
+            fail |= column_fail<W>(m[u], d, cand & ~fail, yy[u], r0, g.dmax, g.P, g.pw);
+          }
         }
       }
     }
@@ -108,6 +130,68 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
       if (removed_at) removed_at[(size_t)x * 64 + a] = t;
     }
   }
+}
+
+// Row-major sweep: every live row (x,a) of variables [g.x_lo, g.x_hi) is
+// streamed whole (all n columns) by a group of G lanes, with early exit on
+// the first failing column and dead-row skip.  Rows are split into n_seg
+// segments so that every group gets several items.
+template <int W, int G>
+__device__ __forceinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
+                                          int32_t* removed_at, int t, long gidx, long ngroups) {
+  const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((lane / G) * G));
+  const int nvec = g.dbytes / 16;
+  const int rows = (g.x_hi - g.x_lo) * g.dmax;
+  const int row0 = (g.x_lo - g.x_lo_alloc) * g.dmax;
+  const int ng = (int)ngroups;
+  int n_seg = 1;
+  while ((long)rows * n_seg < 8L * ng && (nvec + 2 * n_seg - 1) / (2 * n_seg) >= G * kUnrollR) n_seg *= 2;
+  const int seg = ((nvec + n_seg - 1) / n_seg + G * kUnrollR - 1) / (G * kUnrollR) * (G * kUnrollR);
+  n_seg = (nvec + seg - 1) / seg;
+  const int items = rows * n_seg;
+  for (int it = (int)gidx; it < items; it += ng) {
+    int r = it, sgi = 0;
+    if (n_seg > 1) { r = it / n_seg; sgi = it - r * n_seg; }
+    const int xl = r / g.dmax, a = r - xl * g.dmax;
+    const int x = g.x_lo + xl;
+    if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;  // dead row: (x,a) ∉ D_{t-1}
+    const uint4* row = reinterpret_cast<const uint4*>(g.Mr + (size_t)(row0 + r) * g.dbytes);
+    const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
+    const int vb = sgi * seg, ve = min(vb + seg, nvec);
+    if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
+      atomicOr(&R[x], 1ull << a);
+      if (removed_at) removed_at[(size_t)x * 64 + a] = t;
+    }
+  }
+}
+
+// Which layout reads fewer bytes this pass?  rows: every live row in full
+// (live x n masks); columns: every row of the tested columns (rows x ncol).
+__device__ __forceinline__ bool pick_rows(const PassGeom& g, long long live, int ncol) {
+  if (g.Mr == nullptr || g.force == 2) return false;
+  if (g.force == 1) return true;
+  const long long rows = (long long)(g.x_hi - g.x_lo) * g.dmax;
+  // tiny tensors are latency-bound: whole rows are fewer, simpler work items
+  if (rows * (long long)g.dbytes <= (256ll << 10)) return true;
+  return live * (long long)g.n <= rows * (long long)ncol;
+}
+
+// Live rows (x,a) of variables [x_lo, x_hi) in D (every thread of the CTA gets it).
+template <int W>
+__device__ __forceinline__ long long count_live(const uint8_t* Db, int x_lo, int x_hi, int* scratch) {
+  int c = 0;
+  for (int x = x_lo + threadIdx.x; x < x_hi; x += blockDim.x) c += __popcll(load_w<W>(Db + x * W));
+  c = __reduce_add_sync(0xffffffffu, c);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = c;
+  __syncthreads();
+  long long tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += scratch[w];
+  __syncthreads();
+  return tot;
 }
 
 template <int W>
@@ -134,8 +218,8 @@ __device__ __forceinline__ void stage_from_u64(uint8_t* Db, const uint64_t* src,
 }
 
 // ---------------------------------------------------------------------------- fused
-template <int W>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_fused(FusedParams p) {
+template <int W, int G>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p) {
   extern __shared__ uint4 Ds[];
   __shared__ int scratch[kThreads / 32];
   __shared__ int s_last;
@@ -153,9 +237,11 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_fused(FusedPara
   RAC_MARK();
   const long warp0 = (long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const long nwarps = (long)gridDim.x * (blockDim.x / 32);
+  const long gidx = warp0 * (32 / G) + (threadIdx.x & 31) / G, ngroups = nwarps * (32 / G);
   const bool full = (p.flags & kFull) != 0;
   int t = 0, status = kOK, vcnt = g.n;
   unsigned epoch = 0;
+  long long live = count_live<W>(Db, 0, g.n, scratch);
   // Seeded call (Alg. 1 with @changed = seeds): pass 1 tests only the seed columns.
   const bool seeded = p.seeds != nullptr;
   if (seeded) {
@@ -180,7 +266,10 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_fused(FusedPara
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
-      column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
+      if (pick_rows(g, live, lst ? vcnt : g.n))
+        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups);
+      else
+        column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
       RAC_MARK();
       grid_sync(p.bar, gridDim.x, ++epoch);
       RAC_MARK();
@@ -201,6 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_fused(FusedPara
       wipe = __syncthreads_or(wipe);
       RAC_MARK();
       vcnt = block_compact(vneed, vlist, g.n, scratch);
+      live = count_live<W>(Db, 0, g.n, scratch);
       RAC_MARK();
       if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
       if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
@@ -267,8 +357,8 @@ __device__ __forceinline__ void tma_stage(uint8_t* dst, const uint8_t* src, uint
   }
 }
 
-template <int W>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_pass(PassParams p) {
+template <int W, int G>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) rac_pass(PassParams p) {
   extern __shared__ uint4 Ds[];
   __shared__ alignas(8) uint64_t mbar;
   if (*reinterpret_cast<volatile int32_t*>(p.s.done)) return;  // converged: speculative pass is a no-op
@@ -284,7 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_pass(PassParams
   }
   const long warp0 = (long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const long nwarps = (long)gridDim.x * (blockDim.x / 32);
-  column_sweep<W>(p.g, Db, p.s.R, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : p.g.n);
+  __shared__ int scratch[kThreads / 32];
+  const long long live = count_live<W>(Db, p.g.x_lo, p.g.x_hi, scratch);
+  if (pick_rows(p.g, live, lst ? vcnt : p.g.n))
+    row_sweep<W, G>(p.g, Ds, p.s.R, p.removed_at, t, warp0 * (32 / G) + (threadIdx.x & 31) / G, nwarps * (32 / G));
+  else
+    column_sweep<W>(p.g, Db, p.s.R, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : p.g.n);
 }
 
 __global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_t* dommask, int n, int W, int dbytes,
@@ -370,8 +465,8 @@ __global__ void rac_shard_finalize(ShardState s, int n, uint64_t* d_out, int32_t
 // One CTA per state: D, the column list and R live in smem, __syncthreads is
 // the pass barrier, each state stops at its own pass (freeze-on-stop).  The
 // relation is shared by all states and stays L2-resident.
-template <int W>
-__global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_batch(BatchParams p) {
+template <int W, int G>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) rac_batch(BatchParams p) {
   extern __shared__ uint4 Ds[];
   __shared__ int scratch[kThreads / 32];
   const PassGeom& g = p.g;
@@ -383,8 +478,10 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_batch(BatchPara
   for (int i = threadIdx.x; i < g.n; i += blockDim.x) vneed[i] = 0;
   stage_from_u64<W>(Db, p.d_in + (size_t)s * g.n, p.dommask, g.n, g.dbytes);
   const long warp0 = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const long gidx = warp0 * (32 / G) + (threadIdx.x & 31) / G, ngroups = nwarps * (32 / G);
   const bool full = (p.flags & kFull) != 0;
   int t = 0, status = kOK, vcnt = g.n;
+  long long live = count_live<W>(Db, 0, g.n, scratch);
   const int seed = p.seed_var ? p.seed_var[s] : -1;
   const bool seeded = seed >= 0 && seed < g.n;
   if (seeded) {
@@ -397,7 +494,10 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_batch(BatchPara
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) R[x] = 0ull;
     __syncthreads();
     const bool lst = seeded || t > 1;
-    column_sweep<W>(g, Db, R, nullptr, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
+    if (pick_rows(g, live, lst ? vcnt : g.n))
+      row_sweep<W, G>(g, Ds, R, nullptr, t, gidx, ngroups);
+    else
+      column_sweep<W>(g, Db, R, nullptr, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
     __syncthreads();
     int changed = 0, wipe = 0;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) {
@@ -413,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) rac_batch(BatchPara
     changed = __syncthreads_or(changed);
     wipe = __syncthreads_or(wipe);
     vcnt = block_compact(vneed, vlist, g.n, scratch);
+    live = count_live<W>(Db, 0, g.n, scratch);
     if (wipe && !full) { status = kWIPEOUT; break; }
     if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }
   }
@@ -428,70 +529,83 @@ cudaError_t set_smem(K k, size_t smem) {
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <int W>
-cudaError_t launch_fused_w(const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
-  auto k = rac_fused<W>;
-  cudaError_t e = set_smem(k, smem);
-  if (e != cudaSuccess) return e;
-  if (coop) {
-    FusedParams pp = p;
-    void* args[] = {&pp};
-    return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kThreads), args, smem, s);
+template <int W, int G>
+struct Launch {
+  static cudaError_t fused(const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
+    auto k = rac_fused<W, G>;
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    if (coop) {
+      FusedParams pp = p;
+      void* args[] = {&pp};
+      return cudaLaunchCooperativeKernel((const void*)k, dim3(grid), dim3(kThreads), args, smem, s);
+    }
+    k<<<grid, kThreads, smem, s>>>(p);
+    return cudaGetLastError();
   }
-  k<<<grid, kThreads, smem, s>>>(p);
-  return cudaGetLastError();
-}
-
-template <int W>
-cudaError_t occ_w(int which, size_t smem, int* out) {
-  const void* k = which == 0 ? (const void*)rac_fused<W> : which == 1 ? (const void*)rac_pass<W>
-                                                                      : (const void*)rac_batch<W>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
-}
-
-template <int W>
-cudaError_t launch_pass_w(const PassParams& p, int grid, size_t smem, cudaStream_t s) {
-  auto k = rac_pass<W>;
-  cudaError_t e = set_smem(k, smem);
-  if (e != cudaSuccess) return e;
-  k<<<grid, kThreads, smem, s>>>(p);
-  return cudaGetLastError();
-}
-
-template <int W>
-cudaError_t launch_batch_w(const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
-  auto k = rac_batch<W>;
-  cudaError_t e = set_smem(k, smem);
-  if (e != cudaSuccess) return e;
-  k<<<n_states, kThreads, smem, s>>>(p);
-  return cudaGetLastError();
-}
+  static cudaError_t pass(const PassParams& p, int grid, size_t smem, cudaStream_t s) {
+    auto k = rac_pass<W, G>;
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<grid, kThreads, smem, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t batch(const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
+    auto k = rac_batch<W, G>;
+    cudaError_t e = set_smem(k, smem);
+    if (e != cudaSuccess) return e;
+    k<<<n_states, kThreads, smem, s>>>(p);
+    return cudaGetLastError();
+  }
+  static cudaError_t occ(int which, size_t smem, int* out) {
+    const void* k = which == 0 ? (const void*)rac_fused<W, G>
+                    : which == 1 ? (const void*)rac_pass<W, G> : (const void*)rac_batch<W, G>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
+  }
+};
 
 }  // namespace
 
-#define RAC_W_SWITCH(W, EXPR_T)                          \
-  switch (W) {                                           \
-    case 1: { constexpr int WW = 1; return EXPR_T; }     \
-    case 2: { constexpr int WW = 2; return EXPR_T; }     \
-    case 4: { constexpr int WW = 4; return EXPR_T; }     \
-    case 8: { constexpr int WW = 8; return EXPR_T; }     \
-    default: return cudaErrorInvalidValue;               \
+#define RAC_G_SWITCH(WW, G, CALL)                                  \
+  switch (G) {                                                     \
+    case 1: return Launch<WW, 1>::CALL;                            \
+    case 2: return Launch<WW, 2>::CALL;                            \
+    case 4: return Launch<WW, 4>::CALL;                            \
+    case 8: return Launch<WW, 8>::CALL;                            \
+    case 16: return Launch<WW, 16>::CALL;                          \
+    case 32: return Launch<WW, 32>::CALL;                          \
+    default: return cudaErrorInvalidValue;                         \
+  }
+#define RAC_WG_SWITCH(W, G, CALL)                                  \
+  switch (W) {                                                     \
+    case 1: RAC_G_SWITCH(1, G, CALL)                               \
+    case 2: RAC_G_SWITCH(2, G, CALL)                               \
+    case 4: RAC_G_SWITCH(4, G, CALL)                               \
+    case 8: RAC_G_SWITCH(8, G, CALL)                               \
+    default: return cudaErrorInvalidValue;                         \
   }
 
-cudaError_t launch_fused(int W, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
-  RAC_W_SWITCH(W, launch_fused_w<WW>(p, grid, smem, s, coop))
+int choose_group(int nvec) {
+  // smallest power of two G with G * kUnrollR >= nvec, capped at a warp
+  int G = 1;
+  while (G < 32 && G * kUnrollR < nvec) G *= 2;
+  return G;
 }
-cudaError_t fused_occupancy(int W, size_t smem, int* out) { RAC_W_SWITCH(W, occ_w<WW>(0, smem, out)) }
-cudaError_t launch_pass(int W, const PassParams& p, int grid, size_t smem, cudaStream_t s) {
-  RAC_W_SWITCH(W, launch_pass_w<WW>(p, grid, smem, s))
+
+cudaError_t launch_fused(int W, int G, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
+  RAC_WG_SWITCH(W, G, fused(p, grid, smem, s, coop))
 }
-cudaError_t pass_occupancy(int W, size_t smem, int* out) { RAC_W_SWITCH(W, occ_w<WW>(1, smem, out)) }
-cudaError_t launch_batch(int W, const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
-  RAC_W_SWITCH(W, launch_batch_w<WW>(p, n_states, smem, s))
+cudaError_t fused_occupancy(int W, int G, size_t smem, int* out) { RAC_WG_SWITCH(W, G, occ(0, smem, out)) }
+cudaError_t launch_pass(int W, int G, const PassParams& p, int grid, size_t smem, cudaStream_t s) {
+  RAC_WG_SWITCH(W, G, pass(p, grid, smem, s))
 }
-cudaError_t batch_occupancy(int W, size_t smem, int* out) { RAC_W_SWITCH(W, occ_w<WW>(2, smem, out)) }
+cudaError_t pass_occupancy(int W, int G, size_t smem, int* out) { RAC_WG_SWITCH(W, G, occ(1, smem, out)) }
+cudaError_t launch_batch(int W, int G, const BatchParams& p, int n_states, size_t smem, cudaStream_t s) {
+  RAC_WG_SWITCH(W, G, batch(p, n_states, smem, s))
+}
+cudaError_t batch_occupancy(int W, int G, size_t smem, int* out) { RAC_WG_SWITCH(W, G, occ(2, smem, out)) }
 
 cudaError_t launch_shard_init(const ShardState& s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
                               int dbytes, int total_g, cudaStream_t st) {

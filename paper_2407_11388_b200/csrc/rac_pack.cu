@@ -16,15 +16,21 @@ namespace rac {
 
 namespace {
 
-// column-major: mask c_xy|(x,a) lives in column y at local row (x - x_lo)*dmax + a
-__device__ __forceinline__ void store_mask(const PackGeom& g, int x, int a, int y, uint64_t m) {
-  uint8_t* p = g.M + (size_t)y * g.col_stride + ((size_t)(x - g.x_lo) * g.dmax + a) * g.W;
-  switch (g.W) {
+__device__ __forceinline__ void put_w(uint8_t* p, int W, uint64_t m) {
+  switch (W) {
     case 8: *reinterpret_cast<uint64_t*>(p) = m; break;
     case 4: *reinterpret_cast<uint32_t*>(p) = (uint32_t)m; break;
     case 2: *reinterpret_cast<uint16_t*>(p) = (uint16_t)m; break;
     default: *p = (uint8_t)m; break;
   }
+}
+
+// Mask c_xy|(x,a): column-major copy (column y, local row (x - x_lo)*dmax + a)
+// and, when present, the row-major copy (that row, byte offset y*W).
+__device__ __forceinline__ void store_mask(const PackGeom& g, int x, int a, int y, uint64_t m) {
+  const size_t r = (size_t)(x - g.x_lo) * g.dmax + a;
+  put_w(g.M + (size_t)y * g.col_stride + r * g.W, g.W, m);
+  if (g.Mr) put_w(g.Mr + r * g.row_bytes + (size_t)y * g.W, g.W, m);
 }
 
 __device__ __forceinline__ void set_present(const PackGeom& g, int x, int y) {

@@ -395,3 +395,35 @@ def test_c5_batched_seeded(rac):
     for s in range(S):
         e = orc.rac(states[s], with_epochs=False)
         assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), s
+
+
+# ----------------------------------------------------------------------------- layouts
+@pytest.mark.parametrize("layout", ["rows", "cols"])
+def test_forced_layouts(rac, layout, monkeypatch):
+    """Every pass on the row-major copy only, or on the column-major tensor only
+    (RAC_FORCE_LAYOUT), gives the oracle's results: both sweeps are exact."""
+    monkeypatch.setenv("RAC_FORCE_LAYOUT", layout)
+    for k, inst in enumerate(I.random_corpus(150, seed0=61)):
+        ctx = rac.RacContext.from_instance(inst)
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = synth.w_rand(inst.dom, 0.9, seed=k)
+        if k % 4 == 0:
+            d_in[k % inst.n] = U64(0)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (layout, k, full))
+    dq = synth.quant_density(1.0)
+    for t, kind in ((0.70, "root"), (0.5, "seed")):
+        tq = synth.quant_tightness(t)
+        ctx = rac.RacContext.create_random(2000, 32, dq, tq, 1)
+        orc = oracle.Oracle.from_synth(2000, 32, dq, tq, 1)
+        root = synth.full_domains(np.full(2000, 32))
+        if kind == "root":
+            g, o = both(ctx, orc, root)
+            assert_same(g, o, (layout, kind))
+        else:
+            _, droot, _, _ = orc.rac(root, with_epochs=False)
+            s, x, v = synth.w_seed(droot, 7)
+            g = ctx.enforce_seeded(s, [x])
+            o = orc.rac(s, with_epochs=False)
+            assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1])
