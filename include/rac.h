@@ -66,6 +66,7 @@ extern "C" {
 /* ---- return codes ------------------------------------------------------- */
 #define RAC_OK 0             /* fixpoint, no empty domain: d_out == D_ac(d_in)            */
 #define RAC_WIPEOUT 1        /* some domain empty: d_out = D after the detecting pass     */
+#define RAC_BUDGET 2         /* rac_search: assignment budget exhausted before a verdict  */
 #define RAC_EINVAL (-1)      /* invalid argument (see each call)                          */
 #define RAC_ENOMEM (-2)      /* host or device allocation failed                          */
 #define RAC_ECUDA (-3)       /* CUDA error; context now unusable                          */
@@ -184,6 +185,35 @@ int rac_enforce_seeded_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d
 int rac_enforce_batch_seeded(rac_ctx* ctx, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                              int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev,
                              uint32_t flags, void* stream);
+
+/* ---- search (Alg. 2) ---------------------------------------- */
+typedef struct {
+  int64_t assignments;      /* assign + seeded enforcement events (Table 1's unit) */
+  int64_t recurrences;      /* sum of their iteration counts (Table 1's #Recurrence x assignments) */
+  int64_t wipeouts;         /* assignments whose enforcement ended in RAC_WIPEOUT               */
+  int64_t solutions;        /* complete assignments reached                                    */
+  int64_t max_depth;        /* deepest level reached                                            */
+  int32_t root_iterations;  /* passes of the root enforcement tensorAC(Vars, all)       */
+  int32_t root_status;
+  double enforce_seconds;   /* host wall time spent in the per-assignment enforcements          */
+} rac_search_stats;
+
+#define RAC_SEARCH_ALL (1u << 8) /* count every solution instead of stopping at the first */
+
+/* Backtracking search maintaining arc consistency (Alg. 2) on the
+ * device-resident instance: root enforcement tensorAC(Vars, all),
+ * then depth-first: pick the unassigned variable with the smallest current
+ * domain (lowest index on ties -- the paper leaves heuristics() open, P:389;
+ * SPEC S:396-404), try its values in ascending order, assign (row overwrite,
+ * P:410-416) on a copy of the parent's domains, enforce with @changed = [idx]
+ * (rac_enforce_seeded), recurse unless wiped out.
+ * Returns RAC_OK (a solution: solution[x] = value of x, unless NULL;
+ * with RAC_SEARCH_ALL the whole tree is explored and RAC_OK means >= 1
+ * solution), RAC_WIPEOUT (unsatisfiable: tree exhausted with no solution) or
+ * RAC_BUDGET (max_assignments reached first; max_assignments <= 0 = no limit).
+ * d_in: host uint64_t[n_vars].  world == 1 only. */
+int rac_search(rac_ctx* ctx, const uint64_t* d_in, int64_t max_assignments, uint32_t flags, int32_t* solution,
+               rac_search_stats* stats);
 
 /* ---- introspection ------------------------------------------------------ */
 int32_t rac_n_vars(const rac_ctx* ctx);

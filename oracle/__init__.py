@@ -14,6 +14,8 @@ Contents
     of D, by enumerating every subset (tiny inputs).
   * ``Oracle.rac_seeded`` -- O5: Alg. 1 tensorAC(Vars, @changed) as written
     (lines 198-221), the paper's incremental per-assignment call (line 392).
+  * ``Oracle.search`` -- O6: Alg. 2 backtracking search (lines 369-417) over
+    O5 / O1 / O2 enforcement.
   * ``rac_python`` -- a pure-Python transcription of Eq. 1 (tiny inputs), used
     to cross-check the C transcription.
 
@@ -68,6 +70,9 @@ def _load():
         lib.orc_rac.restype = ctypes.c_int
         lib.orc_rac_seeded.argtypes = [P, u64p, i32p, ctypes.c_int, u64p, i32p, i32p, ctypes.c_int]
         lib.orc_rac_seeded.restype = ctypes.c_int
+        lib.orc_search.argtypes = [P, u64p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, i32p,
+                                   ctypes.POINTER(ctypes.c_int64)]
+        lib.orc_search.restype = ctypes.c_int
         lib.orc_ac3.argtypes = [P, u64p, u64p, ctypes.POINTER(ctypes.c_int64)]
         lib.orc_ac3.restype = ctypes.c_int
         lib.orc_is_ac.argtypes = [P, u64p]
@@ -176,6 +181,20 @@ class Oracle:
         st = lib.orc_rac_seeded(self._h, _u64p(d_in), _i32p(seeds) if seeds.size else None, int(seeds.size),
                                 _u64p(d_out), _i32p(it), _i32p(rem) if rem is not None else None, 1 if full else 0)
         return st, d_out, int(it[0]), (rem.reshape(self.n, 64) if rem is not None else None)
+
+    def search(self, d_in, max_assignments: int = 0, engine: str = "seeded", all_solutions: bool = False,
+               full: bool = False):
+        """O6: Alg. 2 backtracking search.  Returns (result, solution, stats) with result 0 = solution,
+        1 = unsat, 2 = budget; stats keys as in rac_search_stats."""
+        lib = _load()
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        sol = np.full(self.n, -1, dtype=np.int32)
+        st = (ctypes.c_int64 * 6)()
+        eng = {"seeded": 0, "full": 1, "ac3": 2}[engine]
+        r = lib.orc_search(self._h, _u64p(d_in), int(max_assignments), eng, 1 if all_solutions else 0,
+                           1 if full else 0, _i32p(sol), st)
+        keys = ["assignments", "recurrences", "wipeouts", "solutions", "max_depth", "root_iterations"]
+        return r, sol, dict(zip(keys, [int(v) for v in st]))
 
     def ac3(self, d_in):
         """O2. Returns (status, d_out, revisions)."""

@@ -439,6 +439,97 @@ int orc_rac_seeded(const orc_csp *c, const uint64_t *d_in, const int32_t *seeds,
 }
 
 /*
+ * O6: Alg. 2 backtracking search, written
+ * recursively: dfs(level, Vars) picks idx = heuristics() -- the unassigned
+ * variable with the fewest values, lowest index on ties (the
+ * paper leaves it open, line 389) -- and for each Val in Var[idx].nonzero()
+ * (ascending) assigns it on a COPY of the parent's domains (the paper's
+ * pseudocode reuses Vars across siblings, lines 390-393, reading R13) and
+ * enforces.  engine 0: O5 tensorAC(Vars, [idx]) (line 392); 1: O1 full
+ * recurrence; 2: O2 AC-3.  stats[0] assignments,
+ * [1] sum of iterations (engine 2: of AC-3 revisions), [2] wipeouts, [3] solutions, [4] max depth,
+ * [5] root iterations.  Returns 0 solution found (first one in solution[]),
+ * 1 unsatisfiable, 2 budget exhausted.  all != 0: explore the whole tree.
+ */
+int orc_ac3(const orc_csp *c, const uint64_t *d_in, uint64_t *d_out, int64_t *revisions);
+
+typedef struct {
+  const orc_csp *c;
+  int64_t budget;
+  int engine, all, full;
+  int64_t *stats;
+  int32_t *solution;
+  char *assigned;
+  int found, out_of_budget;
+} orc_search_ctx;
+
+static int orc_enforce_engine(orc_search_ctx *s, const uint64_t *din, uint64_t *dout, int seed, int *iters) {
+  if (s->engine == 0) return orc_rac_seeded(s->c, din, &seed, 1, dout, iters, NULL, s->full);
+  if (s->engine == 1) return orc_rac(s->c, din, dout, iters, NULL, s->full);
+  int64_t rev = 0;
+  int st = orc_ac3(s->c, din, dout, &rev);
+  *iters = (int)rev; /* engine 2 sums AC-3 revisions (Table 1's #Revision) */
+  return st;
+}
+
+static int orc_dfs(orc_search_ctx *s, const uint64_t *D, int level) {
+  const orc_csp *c = s->c;
+  int n = c->n;
+  int idx = -1, best = 65;
+  for (int x = 0; x < n; ++x)
+    if (!s->assigned[x] && popc64(D[x]) < best) { best = popc64(D[x]); idx = x; }
+  s->assigned[idx] = 1;
+  uint64_t *child = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+  uint64_t *out = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+  int stop = 0;
+  for (int v = 0; v < 64 && !stop; ++v) {
+    if (!((D[idx] >> v) & 1ULL)) continue;
+    if (s->budget > 0 && s->stats[0] >= s->budget) { s->out_of_budget = 1; stop = 1; break; }
+    memcpy(child, D, (size_t)n * sizeof(uint64_t));
+    child[idx] = 1ULL << v; /* assign, lines 410-416 */
+    int it = 0;
+    int st = orc_enforce_engine(s, child, out, idx, &it);
+    s->stats[0]++;
+    s->stats[1] += it;
+    if (st == ORC_WIPEOUT) { s->stats[2]++; continue; }
+    if (level + 1 > s->stats[4]) s->stats[4] = level + 1;
+    if (level + 1 == n) {
+      s->stats[3]++;
+      if (!s->found && s->solution)
+        for (int x = 0; x < n; ++x)
+          for (int b = 0; b < 64; ++b)
+            if ((out[x] >> b) & 1ULL) { s->solution[x] = b; break; }
+      s->found = 1;
+      if (!s->all) stop = 1;
+      continue;
+    }
+    if (orc_dfs(s, out, level + 1)) stop = 1;
+  }
+  free(child); free(out);
+  s->assigned[idx] = 0;
+  return stop;
+}
+
+int orc_search(const orc_csp *c, const uint64_t *d_in, int64_t max_assignments, int engine, int all, int full,
+               int32_t *solution, int64_t *stats) {
+  int n = c->n;
+  for (int k = 0; k < 6; ++k) stats[k] = 0;
+  uint64_t *root = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+  int it = 0, st;
+  if (engine == 2) { int64_t rev; st = orc_ac3(c, d_in, root, &rev); }
+  else st = orc_rac(c, d_in, root, &it, NULL, full);
+  stats[5] = it;
+  if (st == ORC_WIPEOUT) { free(root); return 1; }
+  orc_search_ctx s = {c, max_assignments, engine, all, full, stats, solution, NULL, 0, 0};
+  s.assigned = (char *)calloc((size_t)n, 1);
+  orc_dfs(&s, root, 0);
+  free(s.assigned);
+  free(root);
+  if (s.out_of_budget) return 2;
+  return s.found ? 0 : 1;
+}
+
+/*
  * O2: AC-3 ("a propagation queue and a revision process";
  * SPEC.md ac3_engine lines 283-299).  FIFO queue of directed arcs (x,y),
  * initially every arc in ascending (x, y) order; revise(x,y) removes every

@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -76,6 +77,7 @@ struct rac_ctx {
   uint8_t* Mr = nullptr;    // row-major copy (nullable)
   int G = 1;                // lanes per row of the row-major sweep
   int force_layout = 0;     // RAC_FORCE_LAYOUT=rows|cols (testing knob)
+  bool use_ring = false;    // column sweep through per-warp TMA rings
   uint32_t* P = nullptr;
   int32_t* dom_d = nullptr;
   uint64_t* dommask = nullptr;
@@ -160,6 +162,10 @@ void free_ctx(rac_ctx* c) {
   cudaFreeHost(c->h_scalars);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+}
+
+size_t kernel_smem(const rac_ctx* c) {
+  return fused_smem(c->dbytes, c->n) + (c->use_ring ? ring_bytes(kThreads / 32) : 0);
 }
 
 // Common part of rac_create / rac_create_random up to (not including) packing.
@@ -261,16 +267,22 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   // Launch geometry.  Fused path: a co-resident grid (cooperative launch),
   // as many CTAs as fit, but no more than the work of a full pass can feed
   // (about 4 items of kUnroll columns x one 512-byte slab per warp).
+  {
+    // TMA rings for the column sweep when they fit next to D (RAC_NO_RING: A/B knob)
+    const char* nr = getenv("RAC_NO_RING");
+    c->use_ring = !(nr && *nr && strcmp(nr, "0") != 0) &&
+                  fused_smem(c->dbytes, n) + ring_bytes(kThreads / 32) <= 220 * 1024;
+  }
   const long slabs = c->rows_pad / slab_rows(c->W);
   const long items = slabs * ((n + kUnroll - 1) / kUnroll);
   int occ = 0;
-  CKC(fused_occupancy(c->W, c->G, fused_smem(c->dbytes, n), &occ));
+  CKC(fused_occupancy(c->W, c->G, kernel_smem(c), &occ));
   if (occ < 1) return fail(nullptr, RAC_EUNSUPPORTED, "support-pass kernel does not fit on an SM (n too large)");
   // about one item per warp (small problems are latency-bound: spread them)
   const long want = (items + (kThreads / 32) - 1) / (kThreads / 32);
   c->fused_grid = (int)std::max(1L, std::min((long)c->sm_count * occ, want));
   int pocc = 0;
-  CKC(pass_occupancy(c->W, c->G, fused_smem(c->dbytes, n), &pocc));
+  CKC(pass_occupancy(c->W, c->G, kernel_smem(c), &pocc));
   c->pass_grid = (int)std::max(1L, std::min((long)c->sm_count * std::max(1, pocc), want));
   CKC(cudaStreamSynchronize(c->stream));
 #undef CKC
@@ -291,8 +303,11 @@ PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi) {
   g.P = c->P;
   g.pw = c->pw;
   g.dbytes = c->dbytes;
+  g.ring_off = c->use_ring ? (int)fused_smem(c->dbytes, c->n) : 0;
   return g;
 }
+
+
 
 int check_usable(rac_ctx* c) {
   if (!c) return RAC_EINVAL;
@@ -322,7 +337,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   // R[1] (pass 1's removal buffer) is clean: zeroed at create and by the last
   // CTA of every previous launch.
   static const bool no_coop = getenv("RAC_NO_COOP") != nullptr;  // A/B knob (tooling only)
-  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, fused_smem(c->dbytes, c->n), s, c->fused_grid > 1 && !no_coop));
+  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, kernel_smem(c), s, c->fused_grid > 1 && !no_coop));
   c->launches++;
   return 0;
 }
@@ -351,7 +366,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
     for (int k = 0; k < chunk; ++k) {
       for (int b = 0; b < nb; ++b) {
         if (pp[b].g.x_hi <= pp[b].g.x_lo) continue;
-        CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, fused_smem(c->dbytes, c->n), s));
+        CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, kernel_smem(c), s));
         c->launches++;
       }
       if (c->world > 1) {
@@ -702,13 +717,105 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   p.status = status_dev;
   p.seed_var = seed_var_dev;
   p.flags = flags;
-  const size_t smem1 = fused_smem(c->dbytes, c->n) + (size_t)c->n * 8;
+  // per-state kernel: rings (if any) after R
+  if (c->use_ring) p.g.ring_off = (int)(fused_smem(c->dbytes, c->n) + (size_t)c->n * 8);
+  const size_t smem1 = fused_smem(c->dbytes, c->n) + (size_t)c->n * 8 + (c->use_ring ? ring_bytes(kThreads / 32) : 0);
   int occ1 = 0;
   CK(c, batch_occupancy(c->W, c->G, smem1, &occ1));
   if (occ1 < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");
   CK(c, launch_batch(c->W, c->G, p, n_states, smem1, st));
   c->launches = 1;
   return 0;
+}
+
+int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32_t flags, int32_t* solution,
+               rac_search_stats* stats) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (!d_in) return fail(c, RAC_EINVAL, "d_in is NULL");
+  if (flags & ~(RAC_SEARCH_ALL | RAC_FULL_FIXPOINT)) return fail(c, RAC_EINVAL, "unknown flags");
+  if (c->world > 1 || c->vshards > 1) return fail(c, RAC_EUNSUPPORTED, "rac_search runs on single-GPU contexts");
+  const int n = c->n;
+  rac_search_stats st;
+  memset(&st, 0, sizeof(st));
+  const uint32_t ef = flags & RAC_FULL_FIXPOINT;
+  // root: tensorAC(Vars, [0 : |Vars|])
+  std::vector<uint64_t> root(n);
+  int32_t it = 0;
+  rc = rac_enforce_ex(c, d_in, root.data(), &it, nullptr, ef);
+  if (rc < 0) return rc;
+  st.root_iterations = it;
+  st.root_status = rc;
+  if (rc == RAC_WIPEOUT) {
+    if (stats) *stats = st;
+    return RAC_WIPEOUT;
+  }
+  // explicit DFS stack: frame k holds the domains of depth k and the variable
+  // chosen there with its untried values
+  struct Frame {
+    int var;
+    uint64_t todo;
+  };
+  std::vector<uint64_t> doms((size_t)(n + 1) * n);
+  std::vector<Frame> frames(n + 1);
+  std::vector<char> assigned(n, 0);
+  auto pick = [&](const uint64_t* D) {
+    int best = -1, bc = 65;
+    for (int x = 0; x < n; ++x) {
+      if (assigned[x]) continue;
+      const int cnt = __builtin_popcountll(D[x]);
+      if (cnt < bc) { bc = cnt; best = x; }
+    }
+    return best;
+  };
+  std::copy(root.begin(), root.end(), doms.begin());
+  int depth = 0;
+  frames[0].var = pick(doms.data());
+  frames[0].todo = doms[frames[0].var];
+  assigned[frames[0].var] = 1;
+  bool found = false;
+  int result = RAC_WIPEOUT;
+  std::vector<uint64_t> child(n);
+  while (depth >= 0) {
+    Frame& f = frames[depth];
+    if (f.todo == 0) {  // all values of f.var tried: backtrack
+      assigned[f.var] = 0;
+      --depth;
+      continue;
+    }
+    if (max_assignments > 0 && st.assignments >= max_assignments) { result = RAC_BUDGET; break; }
+    const int val = __builtin_ctzll(f.todo);
+    f.todo &= f.todo - 1;
+    const uint64_t* parent = doms.data() + (size_t)depth * n;
+    std::copy(parent, parent + n, child.begin());
+    child[f.var] = 1ull << val;  // assign: row overwrite
+    int32_t seed = f.var;
+    int32_t cit = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    rc = rac_enforce_seeded(c, child.data(), child.data(), &cit, &seed, 1, ef);
+    st.enforce_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc < 0) return rc;
+    st.assignments++;
+    st.recurrences += cit;
+    if (rc == RAC_WIPEOUT) { st.wipeouts++; continue; }
+    if (depth + 1 > st.max_depth) st.max_depth = depth + 1;
+    if (depth + 1 == n) {  // every variable assigned: a solution (Alg. 2 "find answer")
+      st.solutions++;
+      if (!found && solution)
+        for (int x = 0; x < n; ++x) solution[x] = __builtin_ctzll(child[x]);
+      found = true;
+      if (!(flags & RAC_SEARCH_ALL)) { result = RAC_OK; break; }
+      continue;
+    }
+    ++depth;
+    std::copy(child.begin(), child.end(), doms.begin() + (size_t)depth * n);
+    frames[depth].var = pick(child.data());
+    frames[depth].todo = child[frames[depth].var];
+    assigned[frames[depth].var] = 1;
+  }
+  if (result != RAC_BUDGET && found) result = RAC_OK;
+  if (stats) *stats = st;
+  return result;
 }
 
 int32_t rac_n_vars(const rac_ctx* c) { return c ? c->n : RAC_EINVAL; }

@@ -64,7 +64,14 @@ struct PassGeom {
   const uint32_t* P;      // presence bits of variable x_lo_alloc onward
   int pw;                 // u32 words per presence row
   int dbytes;             // bytes of D in smem (n*W rounded up to 16)
+  int ring_off;           // > 0: byte offset in dynamic smem of the per-warp TMA rings
 };
+
+// Per-warp TMA ring of the column sweep: 2 stages x kRingCols columns x one
+// 512-byte slab, filled by cp.async.bulk and tracked by one mbarrier per stage.
+constexpr int kRingCols = 8;
+constexpr int kRingWarpBytes = 2 * kRingCols * 512;
+__host__ __device__ constexpr size_t ring_bytes(int warps) { return (size_t)warps * kRingWarpBytes + (size_t)warps * 16; }
 
 struct FusedParams {
   PassGeom g;
@@ -385,6 +392,38 @@ __device__ __forceinline__ int block_compact(uint8_t* need, uint16_t* out, int c
   const int total = scratch[(T >> 5) - 1];
   __syncthreads();
   return total;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(mb)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(mb);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
+// One elected lane: arm `mb` for `bytes` and start `cnt` 512-byte bulk copies.
+__device__ __forceinline__ void bulk_arm(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(mb)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy_512(void* dst, const void* src, uint64_t* mb) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"((uint32_t)__cvta_generic_to_shared(mb))
+      : "memory");
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {

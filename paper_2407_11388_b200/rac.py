@@ -21,6 +21,8 @@ LIB_PATH = os.environ.get("RAC_LIB_PATH") or os.path.join(_HERE, "librac.so")  #
 
 RAC_OK = 0
 RAC_WIPEOUT = 1
+RAC_BUDGET = 2
+RAC_SEARCH_ALL = 1 << 8
 RAC_EINVAL = -1
 RAC_ENOMEM = -2
 RAC_ECUDA = -3
@@ -45,6 +47,12 @@ class rac_relation(ctypes.Structure):
     _fields_ = [("x", ctypes.c_int32), ("y", ctypes.c_int32), ("rows", ctypes.POINTER(ctypes.c_uint64))]
 
 
+class rac_search_stats(ctypes.Structure):
+    _fields_ = [("assignments", ctypes.c_int64), ("recurrences", ctypes.c_int64), ("wipeouts", ctypes.c_int64),
+                ("solutions", ctypes.c_int64), ("max_depth", ctypes.c_int64), ("root_iterations", ctypes.c_int32),
+                ("root_status", ctypes.c_int32), ("enforce_seconds", ctypes.c_double)]
+
+
 class rac_options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
                 ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p), ("virtual_shards", ctypes.c_int32)]
@@ -53,7 +61,7 @@ class rac_options(ctypes.Structure):
 # Every symbol include/rac.h declares (checked by tests/test_abi.py).
 EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforce", "rac_enforce_ex",
            "rac_enforce_async", "rac_enforce_batch", "rac_enforce_seeded", "rac_enforce_seeded_async",
-           "rac_enforce_batch_seeded", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
+           "rac_enforce_batch_seeded", "rac_search", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
            "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
            "rac_last_launch_count", "rac_last_error", "rac_destroy"]
 
@@ -80,6 +88,7 @@ def _load() -> ctypes.CDLL:
         "rac_enforce_seeded": (ctypes.c_int, [P, u64p, u64p, i32p, i32p, i32, u32]),
         "rac_enforce_seeded_async": (ctypes.c_int, [P, P, P, P, P, P, i32, u32, P]),
         "rac_enforce_batch_seeded": (ctypes.c_int, [P, i32, P, P, P, P, P, u32, P]),
+        "rac_search": (ctypes.c_int, [P, u64p, ctypes.c_int64, u32, i32p, ctypes.POINTER(rac_search_stats)]),
         "rac_n_vars": (i32, [P]),
         "rac_max_dom": (i32, [P]),
         "rac_mask_bytes": (i32, [P]),
@@ -273,6 +282,18 @@ class RacContext:
         _check(lib.rac_enforce_batch_seeded(self._h, n_states, _ptr(d_in_dev), _ptr(d_out_dev), _ptr(iters_dev),
                                             _ptr(status_dev), _ptr(seed_var_dev), RAC_FULL_FIXPOINT if full else 0,
                                             _stream_ptr(stream)), self._h)
+
+    def search(self, d_in, max_assignments: int = 0, all_solutions: bool = False, full: bool = False):
+        """rac_search: Alg. 2 backtracking search with seeded enforcement per assignment.
+        Returns (result, solution or None, stats dict)."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        sol = np.full(self.n, -1, dtype=np.int32)
+        st = rac_search_stats()
+        flags = (RAC_SEARCH_ALL if all_solutions else 0) | (RAC_FULL_FIXPOINT if full else 0)
+        rc = lib.rac_search(self._h, _u64p(d_in), int(max_assignments), flags, _i32p(sol), ctypes.byref(st))
+        _check(rc, self._h)
+        stats = {k: getattr(st, k) for k, _ in rac_search_stats._fields_}
+        return rc, (sol if rc == RAC_OK else None), stats
 
     def enforce_async(self, d_in_dev, d_out_dev, iters_dev, status_dev, removed_at_dev=None, full: bool = False,
                       stream=None) -> None:

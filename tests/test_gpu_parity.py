@@ -427,3 +427,25 @@ def test_forced_layouts(rac, layout, monkeypatch):
             g = ctx.enforce_seeded(s, [x])
             o = orc.rac(s, with_epochs=False)
             assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1])
+
+
+# ----------------------------------------------------------------------------- search (NEXT-2)
+def test_search_parity(rac):
+    """rac_search (Alg. 2 with seeded enforcement per assignment) explores the
+    same tree as the oracle's O6: identical verdict, first solution, assignments, summed
+    #Recurrence, wipeouts and depth -- on the tiny corpus (whole trees, all solutions),
+    C1 instances and a C5-shaped instance under an assignment budget."""
+    keys = ("assignments", "recurrences", "wipeouts", "solutions", "max_depth", "root_iterations")
+    cases = [(inst, 0, True) for inst in I.random_corpus(120, seed0=81, n_range=(1, 8), d_range=(1, 4))]
+    cases += [(synth.random_csp(20, 8, 0.5, 0.4, s), 3000, False) for s in range(1, 21)]
+    cases += [(synth.random_csp(200, 16, 0.8, 0.3, 1), 1500, False), (synth.random_csp(100, 20, 0.25, 0.3, 2), 1500, False)]
+    for k, (inst, budget, all_sol) in enumerate(cases):
+        orc = oracle.Oracle.from_instance(inst)
+        ctx = rac.RacContext.from_instance(inst)
+        r_o, sol_o, st_o = orc.search(inst.full_domains(), max_assignments=budget, all_solutions=all_sol)
+        r_g, sol_g, st_g = ctx.search(inst.full_domains(), max_assignments=budget, all_solutions=all_sol)
+        assert r_g == r_o, (k, r_g, r_o)
+        for key in keys:
+            assert st_g[key] == st_o[key], (k, key, st_g[key], st_o[key])
+        if r_o == 0:
+            assert np.array_equal(sol_g, sol_o)

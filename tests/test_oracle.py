@@ -435,3 +435,53 @@ def test_seeded_empty_and_precondition_violated():
     assert (st, it, [int(v) for v in d]) == (oracle.OK, 3, [1, 1])
     assert rem[1, 1] == 1 and rem[0, 1] == 2
     assert orc.rac(inst.full_domains())[2] == 2
+
+
+# ----------------------------------------------------------------------------- Alg. 2 search
+def _enumerate(inst):
+    return _solutions(inst)
+
+
+def test_search_matches_enumeration():
+    """O6 (Alg. 2) on 200 tiny instances: Solution iff the brute-force
+    enumeration is non-empty; the solution satisfies every constraint and is one of the
+    enumerated ones; with all_solutions the count equals the enumeration's (AC never
+    removes a solution value, and every complete assignment reached is a solution)."""
+    for k, inst in enumerate(I.random_corpus(200, seed0=71, n_range=(1, 7), d_range=(1, 4))):
+        sols = _enumerate(inst)
+        orc = oracle.Oracle.from_instance(inst)
+        r, sol, st = orc.search(inst.full_domains())
+        assert r == (0 if sols else 1), k
+        if sols:
+            assert tuple(int(v) for v in sol) in set(sols)
+        r2, _, st2 = orc.search(inst.full_domains(), all_solutions=True)
+        assert st2["solutions"] == len(sols)
+
+
+def test_search_engines_agree():
+    """The search tree depends only on D_ac at each node: O5 (seeded, the paper's call),
+    O1 (full recurrence) and O2 (AC-3) explore identical trees (assignments, wipeouts,
+    solution); O5 and O1 also give the same #Recurrence sum (Prop. 2 precondition holds
+    at every node)."""
+    for k, inst in enumerate(I.random_corpus(150, seed0=73, n_range=(3, 16), d_range=(2, 6))):
+        orc = oracle.Oracle.from_instance(inst)
+        res = {e: orc.search(inst.full_domains(), max_assignments=400, engine=e) for e in ("seeded", "full", "ac3")}
+        for e in ("full", "ac3"):
+            assert res[e][0] == res["seeded"][0]
+            for key in ("assignments", "wipeouts", "solutions", "max_depth"):
+                assert res[e][2][key] == res["seeded"][2][key], (k, e, key)
+            assert np.array_equal(res[e][1], res["seeded"][1])
+        assert res["full"][2]["recurrences"] == res["seeded"][2]["recurrences"]
+
+
+def test_search_hand_cases():
+    """SPEC mac_search examples (S:388-390): EQ2 -> x0=0, x1=0; WIPE2 -> unsat at the root;
+    unconstrained n=3, d=2 -> (0,0,0)."""
+    _, eq2 = I.load_golden("eq2.json")
+    r, sol, st = oracle.Oracle.from_instance(eq2).search(eq2.full_domains())
+    assert r == 0 and list(sol) == [0, 0]
+    _, w2 = I.load_golden("wipe2.json")
+    assert oracle.Oracle.from_instance(w2).search(w2.full_domains())[0] == 1
+    free = synth.from_constraints(3, 2, [])
+    r, sol, st = oracle.Oracle.from_instance(free).search(free.full_domains())
+    assert r == 0 and list(sol) == [0, 0, 0] and st["assignments"] == 3
