@@ -77,7 +77,6 @@ struct rac_ctx {
   uint8_t* Mr = nullptr;    // row-major copy (nullable)
   int G = 1;                // lanes per row of the row-major sweep
   int force_layout = 0;     // RAC_FORCE_LAYOUT=rows|cols (testing knob)
-  bool use_ring = false;    // column sweep through per-warp TMA rings
   uint32_t* P = nullptr;
   int32_t* dom_d = nullptr;
   uint64_t* dommask = nullptr;
@@ -165,7 +164,7 @@ void free_ctx(rac_ctx* c) {
 }
 
 size_t kernel_smem(const rac_ctx* c) {
-  return fused_smem(c->dbytes, c->n) + (c->use_ring ? ring_bytes(kThreads / 32) : 0);
+  return fused_smem(c->dbytes, c->n);
 }
 
 // Common part of rac_create / rac_create_random up to (not including) packing.
@@ -267,12 +266,6 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   // Launch geometry.  Fused path: a co-resident grid (cooperative launch),
   // as many CTAs as fit, but no more than the work of a full pass can feed
   // (about 4 items of kUnroll columns x one 512-byte slab per warp).
-  {
-    // TMA rings for the column sweep when they fit next to D (RAC_NO_RING: A/B knob)
-    const char* nr = getenv("RAC_NO_RING");
-    c->use_ring = !(nr && *nr && strcmp(nr, "0") != 0) &&
-                  fused_smem(c->dbytes, n) + ring_bytes(kThreads / 32) <= 220 * 1024;
-  }
   const long slabs = c->rows_pad / slab_rows(c->W);
   const long items = slabs * ((n + kUnroll - 1) / kUnroll);
   int occ = 0;
@@ -303,7 +296,6 @@ PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi) {
   g.P = c->P;
   g.pw = c->pw;
   g.dbytes = c->dbytes;
-  g.ring_off = c->use_ring ? (int)fused_smem(c->dbytes, c->n) : 0;
   return g;
 }
 
@@ -717,9 +709,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   p.status = status_dev;
   p.seed_var = seed_var_dev;
   p.flags = flags;
-  // per-state kernel: rings (if any) after R
-  if (c->use_ring) p.g.ring_off = (int)(fused_smem(c->dbytes, c->n) + (size_t)c->n * 8);
-  const size_t smem1 = fused_smem(c->dbytes, c->n) + (size_t)c->n * 8 + (c->use_ring ? ring_bytes(kThreads / 32) : 0);
+  const size_t smem1 = fused_smem(c->dbytes, c->n) + (size_t)c->n * 8;
   int occ1 = 0;
   CK(c, batch_occupancy(c->W, c->G, smem1, &occ1));
   if (occ1 < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");

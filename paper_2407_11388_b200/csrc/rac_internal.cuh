@@ -64,14 +64,7 @@ struct PassGeom {
   const uint32_t* P;      // presence bits of variable x_lo_alloc onward
   int pw;                 // u32 words per presence row
   int dbytes;             // bytes of D in smem (n*W rounded up to 16)
-  int ring_off;           // > 0: byte offset in dynamic smem of the per-warp TMA rings
 };
-
-// Per-warp TMA ring of the column sweep: 2 stages x kRingCols columns x one
-// 512-byte slab, filled by cp.async.bulk and tracked by one mbarrier per stage.
-constexpr int kRingCols = 8;
-constexpr int kRingWarpBytes = 2 * kRingCols * 512;
-__host__ __device__ constexpr size_t ring_bytes(int warps) { return (size_t)warps * kRingWarpBytes + (size_t)warps * 16; }
 
 struct FusedParams {
   PassGeom g;
@@ -425,6 +418,14 @@ __device__ __forceinline__ void bulk_copy_512(void* dst, const void* src, uint64
       "l"(src), "r"((uint32_t)__cvta_generic_to_shared(mb))
       : "memory");
 }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;

@@ -44,7 +44,7 @@ constexpr int kOK = 0, kWIPEOUT = 1;
 template <int W>
 __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                              int32_t* removed_at, int t, long warp0, long nwarps,
-                                             const uint16_t* cols, int ncol, uint32_t& ring_state) {
+                                             const uint16_t* cols, int ncol) {
   constexpr int RPL = 16 / W, RPW = 32 * RPL;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
@@ -83,64 +83,7 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
     uint32_t fail = 0;
     const int c0 = chunk * yc, c1 = min(c0 + yc, ncol);
     const uint8_t* base = g.M + (size_t)r0 * W;
-    if (g.ring_off > 0) {
-      // TMA ring: lane 0 streams groups of kRingCols column slabs (512 B each)
-      // into a 2-stage per-warp smem ring with cp.async.bulk; every lane tests
-      // its 16 bytes from smem.  ring_state: bit 0-1 = mbarrier parities of the
-      // two stages, bits 2.. = stage counter (persist across items and passes).
-      if (__all_sync(0xffffffffu, cand == 0u)) continue;  // the whole slab is dead
-      const int wl = threadIdx.x >> 5;
-      uint8_t* ring = const_cast<uint8_t*>(Db) + g.ring_off + (size_t)wl * kRingWarpBytes;
-      uint64_t* mbar = reinterpret_cast<uint64_t*>(const_cast<uint8_t*>(Db) + g.ring_off +
-                                                   (size_t)(blockDim.x >> 5) * kRingWarpBytes) + 2 * wl;
-      const uint8_t* slab_base = g.M + (size_t)slab * RPW * W;
-      const int ngr = (c1 - c0 + kRingCols - 1) / kRingCols;
-      auto issue = [&](int gi, int stg) {
-        if (lane == 0) {
-          const int cb = c0 + gi * kRingCols, cnt = min(kRingCols, c1 - cb);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          bulk_arm(mbar + stg, (uint32_t)cnt * 512u);
-          for (int u = 0; u < cnt; ++u) {
-            const int y = cols ? (int)cols[cb + u] : cb + u;
-            bulk_copy_512(ring + (size_t)(stg * kRingCols + u) * 512, slab_base + (size_t)y * g.col_stride, mbar + stg);
-          }
-        }
-      };
-      uint32_t ph = ring_state & 3u, st = ring_state >> 2;
-      __syncwarp();
-      issue(0, st & 1u);
-      for (int gi = 0; gi < ngr; ++gi) {
-        const int cur = (int)((st + gi) & 1u);
-        if (gi + 1 < ngr) {
-          __syncwarp();  // every lane has finished reading the other stage
-          issue(gi + 1, cur ^ 1);
-        }
-        mbar_wait(mbar + cur, (ph >> cur) & 1u);
-        ph ^= 1u << cur;
-        const int cb = c0 + gi * kRingCols, cnt = min(kRingCols, c1 - cb);
-        const uint8_t* buf = ring + (size_t)cur * kRingCols * 512 + lane * 16;
-        for (int u = 0; u < cnt; ++u) {
-          const int y = cols ? (int)cols[cb + u] : cb + u;
-          const uint4 m = *reinterpret_cast<const uint4*>(buf + u * 512);
-          const uint64_t d = load_w<W>(Db + y * W);
-          fail |= column_fail<W>(m, d, cand & ~fail, y, r0, g.dmax, g.P, g.pw);
-        }
-        if (__all_sync(0xffffffffu, fail == cand)) {
-          if (gi + 1 < ngr) {  // drain the group in flight before leaving the item
-            const int nx = cur ^ 1;
-            mbar_wait(mbar + nx, (ph >> nx) & 1u);
-            ph ^= 1u << nx;
-          }
-          st += (uint32_t)min(gi + 2, ngr);
-          ring_state = (st << 2) | ph;
-          goto ring_done;
-        }
-      }
-      st += ngr;
-      ring_state = (st << 2) | ph;
-    ring_done:
-      __syncwarp();
-    } else if (cols == nullptr) {
+    if (cols == nullptr) {
       // contiguous columns c0..c1-1: running pointer, no index array
       const uint8_t* pc = base + (size_t)c0 * g.col_stride;
       for (int c = c0; c < c1 && fail != cand; c += kUnroll) {
@@ -225,19 +168,6 @@ __device__ __forceinline__ void row_sweep(const PassGeom& g, const uint4* Ds, un
   }
 }
 
-// Initialise the per-warp ring mbarriers (two per warp) of a kernel whose
-// dynamic smem carries TMA rings at g.ring_off.
-__device__ __forceinline__ void ring_init(const PassGeom& g, uint8_t* Db) {
-  if (g.ring_off > 0 && (threadIdx.x & 31) == 0) {
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(Db + g.ring_off + (size_t)(blockDim.x >> 5) * kRingWarpBytes) +
-                     2 * (threadIdx.x >> 5);
-    mbar_init(mbar, 1);
-    mbar_init(mbar + 1, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-}
-
 // Which layout reads fewer bytes this pass?  rows: every live row in full
 // (live x n masks); columns: every row of the tested columns (rows x ncol).
 __device__ __forceinline__ bool pick_rows(const PassGeom& g, long long live, int ncol) {
@@ -303,8 +233,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
 #define RAC_MARK() do { if (dbg && nd < 255) p.dbg[1 + nd++] = globaltimer(); } while (0)
   RAC_MARK();
   for (int i = threadIdx.x; i < g.n; i += blockDim.x) vneed[i] = 0;
-  ring_init(g, Db);
-  uint32_t ring_state = 0;
   stage_from_u64<W>(Db, p.d_in, p.dommask, g.n, g.dbytes);
   RAC_MARK();
   const long warp0 = (long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -341,8 +269,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
       if (pick_rows(g, live, lst ? vcnt : g.n))
         row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups);
       else
-        column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
-                        ring_state);
+        column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
       RAC_MARK();
       grid_sync(p.bar, gridDim.x, ++epoch);
       RAC_MARK();
@@ -436,8 +363,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_pass(PassParams p) {
   __shared__ alignas(8) uint64_t mbar;
   if (*reinterpret_cast<volatile int32_t*>(p.s.done)) return;  // converged: speculative pass is a no-op
   uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
-  ring_init(p.g, Db);
-  uint32_t ring_state = 0;
   tma_stage(Db, p.s.Dw, (uint32_t)p.g.dbytes, &mbar);
   const int t = *p.s.iters + 1;
   const int vcnt = *p.s.vcnt;
@@ -454,8 +379,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_pass(PassParams p) {
   if (pick_rows(p.g, live, lst ? vcnt : p.g.n))
     row_sweep<W, G>(p.g, Ds, p.s.R, p.removed_at, t, warp0 * (32 / G) + (threadIdx.x & 31) / G, nwarps * (32 / G));
   else
-    column_sweep<W>(p.g, Db, p.s.R, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : p.g.n,
-                    ring_state);
+    column_sweep<W>(p.g, Db, p.s.R, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : p.g.n);
 }
 
 __global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_t* dommask, int n, int W, int dbytes,
@@ -552,8 +476,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_batch(BatchParams p)
   uint8_t* vneed = Db + need_offset(g.dbytes, g.n);
   unsigned long long* R = reinterpret_cast<unsigned long long*>(Db + fused_smem(g.dbytes, g.n));
   for (int i = threadIdx.x; i < g.n; i += blockDim.x) vneed[i] = 0;
-  ring_init(g, Db);
-  uint32_t ring_state = 0;
   stage_from_u64<W>(Db, p.d_in + (size_t)s * g.n, p.dommask, g.n, g.dbytes);
   const long warp0 = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const long gidx = warp0 * (32 / G) + (threadIdx.x & 31) / G, ngroups = nwarps * (32 / G);
@@ -575,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_batch(BatchParams p)
     if (pick_rows(g, live, lst ? vcnt : g.n))
       row_sweep<W, G>(g, Ds, R, nullptr, t, gidx, ngroups);
     else
-      column_sweep<W>(g, Db, R, nullptr, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ring_state);
+      column_sweep<W>(g, Db, R, nullptr, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
     __syncthreads();
     int changed = 0, wipe = 0;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) {
