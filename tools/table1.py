@@ -47,11 +47,11 @@ def main():
                    "wipeout_frac": st["wipeouts"] / a, "us_per_assignment_gpu": st["enforce_seconds"] / a * 1e6,
                    "root_iterations": st["root_iterations"], "paper_recurrence": PAPER[(n, p)][1],
                    "paper_revision": PAPER[(n, p)][0], "search_wall_s": round(wall, 3)}
-            if with_ac3 and n <= 500:
+            if with_ac3 and n <= 250:
                 import oracle
                 inst = synth.random_csp(n, d, p, t, 1)
                 orc = oracle.Oracle.from_instance(inst)
-                ro, _, so = orc.search(full, max_assignments=min(K, 500), engine="ac3")
+                ro, _, so = orc.search(full, max_assignments=min(K, 300), engine="ac3")
                 row["revision_per_assignment_ac3"] = so["recurrences"] / max(so["assignments"], 1)
                 row["ac3_assignments"] = so["assignments"]
             rows.append(row)
