@@ -92,9 +92,14 @@ typedef struct {
   const uint64_t* rows;
 } rac_relation;
 
+/* rac_options.flags: run a world == 1 context through the multi-GPU exchange
+ * path with a one-rank NCCL communicator (exercises the NCCL all-gather leg on
+ * a single GPU; results are identical to the fused path). */
+#define RAC_OPT_NCCL_SELF (1u << 0)
+
 typedef struct {
   int32_t device;             /* CUDA device ordinal (rank's GPU)                     */
-  uint32_t flags;             /* reserved, must be 0                                  */
+  uint32_t flags;             /* 0 or RAC_OPT_NCCL_SELF                               */
   int32_t rank, world;        /* world <= 1: single GPU                               */
   const void* nccl_unique_id; /* world > 1: RAC_NCCL_ID_BYTES bytes, identical on all
                                  ranks (from rac_get_nccl_unique_id on rank 0)        */

@@ -64,6 +64,8 @@ thread_local std::string g_create_error;
 struct rac_ctx {
   int device = 0;
   int rank = 0, world = 1, vshards = 1;
+  bool nccl_self = false;  // world == 1 through the NCCL exchange path (RAC_OPT_NCCL_SELF)
+  bool use_nccl() const { return world > 1 || nccl_self; }
   int n = 0, dmax = 0, W = 0;
   int rows_pad = 0;        // local rows padded to a warp slab
   size_t col_stride = 0;   // bytes per column of the mask tensor
@@ -94,6 +96,8 @@ struct rac_ctx {
   unsigned* bs_bar = nullptr;      // per-word barrier words
   size_t bs_bar_cap = 0;           // words
   unsigned long long* dbg = nullptr;  // RAC_DEBUG_TIMELINE phase timestamps [256]
+  unsigned long long* bs_dbg = nullptr;  // bit-sliced batch: [ctas][64] pass-end timestamps
+  int bs_dbg_ctas = 0;
   uint64_t* h_in = nullptr;        // pinned
   uint64_t* h_out = nullptr;
   int32_t* h_scalars = nullptr;    // pinned [iters, status, done]
@@ -156,6 +160,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->bs_X2);
   cudaFree(c->bs_bar);
   cudaFree(c->dbg);
+  cudaFree(c->bs_dbg);
   cudaFreeHost(c->h_in);
   cudaFreeHost(c->h_out);
   cudaFreeHost(c->h_scalars);
@@ -172,7 +177,9 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   rac_options o;
   rac_default_options(&o);
   if (opt) o = *opt;
-  if (o.flags != 0) return fail(nullptr, RAC_EINVAL, "options.flags must be 0");
+  if (o.flags & ~RAC_OPT_NCCL_SELF) return fail(nullptr, RAC_EINVAL, "unknown options.flags");
+  if ((o.flags & RAC_OPT_NCCL_SELF) && o.world > 1) return fail(nullptr, RAC_EINVAL, "RAC_OPT_NCCL_SELF needs world == 1");
+  c->nccl_self = (o.flags & RAC_OPT_NCCL_SELF) != 0;
   c->device = o.device;
   c->world = o.world < 1 ? 1 : o.world;
   c->rank = c->world > 1 ? o.rank : 0;
@@ -326,6 +333,24 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, 256 * 8));
   p.dbg = c->dbg;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
+  if (c->fused_grid == 1 && (seeds == nullptr || n_seeds == 1)) {
+    // One CTA is enough: run the single-CTA variant (removal bits in shared
+    // memory, __syncthreads as the pass barrier) -- the batched per-state
+    // kernel with one state.
+    BatchParams b{};
+    b.g = geom_for(c, 0, c->n);
+    b.dommask = c->dommask;
+    b.d_in = d_in;
+    b.d_out = d_out;
+    b.iters = iters;
+    b.status = status;
+    b.seed_var = seeds;  // one seed (or NULL = root call)
+    b.removed_at = removed_at;
+    b.flags = flags;
+    CK(c, launch_batch(c->W, c->G, b, 1, fused_smem(c->dbytes, c->n) + (size_t)c->n * 8, s));
+    c->launches++;
+    return 0;
+  }
   // R[1] (pass 1's removal buffer) is clean: zeroed at create and by the last
   // CTA of every previous launch.
   static const bool no_coop = getenv("RAC_NO_COOP") != nullptr;  // A/B knob (tooling only)
@@ -341,11 +366,11 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
   CK(c, launch_shard_init(c->sh, d_in, c->dommask, c->n, c->W, c->dbytes, total_g, s));
   c->launches++;
-  const int nb = c->world > 1 ? 1 : c->vshards;
+  const int nb = c->use_nccl() ? 1 : c->vshards;
   std::vector<PassParams> pp(nb);
   for (int b = 0; b < nb; ++b) {
     int lo, hi;
-    if (c->world > 1) { lo = c->x_lo; hi = c->x_hi; }
+    if (c->use_nccl()) { lo = c->x_lo; hi = c->x_hi; }
     else rac_shard_range(c->n, c->vshards, b, &lo, &hi);
     pp[b].g = geom_for(c, lo, std::min(hi, c->n));
     pp[b].s = c->sh;
@@ -361,7 +386,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
         CK(c, launch_pass(c->W, c->G, pp[b], c->pass_grid, kernel_smem(c), s));
         c->launches++;
       }
-      if (c->world > 1) {
+      if (c->use_nccl()) {
         CK(c, launch_shard_slice(c->sh, c->x_lo, c->x_lo + c->blk, c->n, s));
         c->launches++;
         ncclResult_t r = nccl().AllGather(c->sh.Dg + (size_t)c->rank * c->blk, c->sh.Dg, (size_t)c->blk,
@@ -394,7 +419,7 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
-  if (c->world > 1 || c->vshards > 1) {
+  if (c->use_nccl() || c->vshards > 1) {
     // the sharded driver has no seeded pass 1: a full pass 1 is the superset
     // check (valid under the precondition; identical trajectory, Prop. 2)
     if (n_seeds == 0) return fail(c, RAC_EUNSUPPORTED, "empty seed list on the sharded path");
@@ -427,10 +452,14 @@ int rac_shard_range(int32_t n_vars, int32_t world, int32_t rank, int32_t* x_lo, 
 }
 
 static int init_comm(rac_ctx* c, const rac_options* opt) {
-  if (c->world <= 1) return 0;
+  if (!c->use_nccl()) return 0;
   if (!nccl().loaded) return fail(nullptr, RAC_ENCCL, "libnccl.so.2 not loadable");
   ncclUniqueId id;
-  memcpy(id.internal, opt->nccl_unique_id, RAC_NCCL_ID_BYTES);
+  if (c->nccl_self) {
+    if (nccl().GetUniqueId(&id) != 0) return fail(nullptr, RAC_ENCCL, "ncclGetUniqueId failed");
+  } else {
+    memcpy(id.internal, opt->nccl_unique_id, RAC_NCCL_ID_BYTES);
+  }
   ncclResult_t r = nccl().CommInitRank(&c->comm, c->world, id, c->rank);
   if (r != 0) {
     c->comm = nullptr;
@@ -595,6 +624,7 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   cudaFree(c->bs_X2);
   cudaFree(c->bs_bar);
   cudaFree(c->dbg);
+  cudaFree(c->bs_dbg);
     c->buf_seeds = nullptr;
     CK(c, cudaMalloc(&c->buf_seeds, (size_t)n_seeds * 4));
     c->seed_cap = (size_t)n_seeds;
@@ -657,7 +687,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   const int words_per_launch = occ > 0 ? (c->sm_count * occ) / RB : 0;
   if (want_bs && words_per_launch >= 1) {
     const int NWmax = std::min(words_per_launch, (n_states + 31) / 32);
-    const size_t x2_bytes = (size_t)2 * NWmax * rows * 4;
+    const size_t x2_bytes = (size_t)2 * NWmax * ((rows + 3) & ~3) * 4;
     if (x2_bytes > c->bs_X2_cap) {
       cudaFree(c->bs_X2);
       c->bs_X2 = nullptr;
@@ -667,6 +697,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     if ((size_t)NWmax * 4 > c->bs_bar_cap) {
       cudaFree(c->bs_bar);
   cudaFree(c->dbg);
+  cudaFree(c->bs_dbg);
       c->bs_bar = nullptr;
       CK(c, cudaMalloc(&c->bs_bar, (size_t)NWmax * 16));
       CK(c, cudaMemsetAsync(c->bs_bar, 0, (size_t)NWmax * 16, st));
@@ -676,6 +707,8 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       BatchBSParams b{};
       b.M = c->M;
       b.col_stride = c->col_stride;
+      b.Mr = c->Mr;
+      b.row_bytes = c->dbytes;
       b.n = c->n;
       b.dmax = c->dmax;
       b.P = c->P;
@@ -694,6 +727,12 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       b.X2 = c->bs_X2;
       b.bar = c->bs_bar;
       b.flags = flags;
+      if (getenv("RAC_DEBUG_TIMELINE")) {
+        if (!c->bs_dbg) CK(c, cudaMalloc(&c->bs_dbg, (size_t)4096 * 64 * 8));
+        CK(c, cudaMemsetAsync(c->bs_dbg, 0, (size_t)4096 * 64 * 8, st));
+        b.dbg = (size_t)b.NW * RB <= 4096 ? c->bs_dbg : nullptr;
+        c->bs_dbg_ctas = b.NW * RB;
+      }
       CK(c, launch_batch_bs(c->W, b, b.NW * RB, smem, st));
       c->launches++;
     }
@@ -724,7 +763,7 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
   if (rc) return rc;
   if (!d_in) return fail(c, RAC_EINVAL, "d_in is NULL");
   if (flags & ~(RAC_SEARCH_ALL | RAC_FULL_FIXPOINT)) return fail(c, RAC_EINVAL, "unknown flags");
-  if (c->world > 1 || c->vshards > 1) return fail(c, RAC_EUNSUPPORTED, "rac_search runs on single-GPU contexts");
+  if (c->use_nccl() || c->vshards > 1) return fail(c, RAC_EUNSUPPORTED, "rac_search runs on fused single-GPU contexts");
   const int n = c->n;
   rac_search_stats st;
   memset(&st, 0, sizeof(st));
@@ -857,6 +896,14 @@ int rac_debug_timeline(rac_ctx* c, unsigned long long* out, int cap) {
   int n = (int)std::min<unsigned long long>(buf[0], (unsigned long long)cap);
   for (int i = 0; i < n; ++i) out[i] = buf[1 + i];
   return n;
+}
+
+// Tooling: per-CTA pass-end timestamps of the last bit-sliced batch launch.
+int rac_debug_batch_timeline(rac_ctx* c, unsigned long long* out, int cap) {
+  if (!c || !c->bs_dbg || !out) return 0;
+  const int cnt = std::min(cap, c->bs_dbg_ctas * 64);
+  if (cudaMemcpy(out, c->bs_dbg, (size_t)cnt * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return cnt;
 }
 
 int rac_get_nccl_unique_id(void* out) {

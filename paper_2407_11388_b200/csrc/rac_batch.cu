@@ -39,7 +39,7 @@ __device__ __forceinline__ void word_sync(unsigned* bar, unsigned nblocks, unsig
     if (prev + 1u == nblocks * epoch) {
       st_release_gpu(&bar[1], epoch);
     } else {
-      while (ld_acquire_gpu(&bar[1]) < epoch) __nanosleep(32);
+      while (ld_acquire_gpu(&bar[1]) < epoch) __nanosleep(128);
     }
     __threadfence();
   }
@@ -62,16 +62,18 @@ __device__ __forceinline__ uint64_t load_mask64(const uint8_t* p) {
 }  // namespace
 
 template <int W>
-__global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
+__global__ void __launch_bounds__(kBT, 3) rac_batch_bs(BatchBSParams p) {
   extern __shared__ uint32_t sm[];
   constexpr int NQ = 2 * W;  // nibbles per mask (d <= 8W)
   const int rows = p.n * p.dmax;
+  const int rows4 = (rows + 3) & ~3;  // per-word stride of the exchange buffers (16-B aligned)
   const int w = blockIdx.x / p.RB;
   const int rb = blockIdx.x - w * p.RB;
   uint32_t* X = sm;                                                   // [rows]
-  uint32_t* T = X + rows;                                             // [n][NQ][16] (if p.use_table)
+  uint32_t* T = X + ((rows + 3) & ~3);                                // [n][NQ][16] (if p.use_table), 16-B aligned
   int* list = reinterpret_cast<int*>(T + (p.use_table ? (size_t)p.n * NQ * 16 : 0));  // [n]
   uint8_t* need = reinterpret_cast<uint8_t*>(list + p.n);             // [n]
+  uint8_t* inlist = need + ((p.n + 15) & ~15);                         // [n] columns of this pass
   __shared__ int s_iters[32], s_status[32];
   __shared__ uint32_t s_or, s_and;
   __shared__ int s_cnt;
@@ -119,12 +121,15 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
   const uint32_t* Prow = p.P + (size_t)x * p.pw;
   int t = 0;
   unsigned epoch = 0;
+  unsigned long long* dbg = (p.dbg && threadIdx.x == 0) ? p.dbg + (size_t)blockIdx.x * 64 : nullptr;
+  if (dbg) dbg[0] = globaltimer();
   for (;;) {
     ++t;
     // column list for this pass from need[] (ascending), need[] cleared
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
+      inlist[i] = need[i];
       if (need[i]) {
         list[atomicAdd(&s_cnt, 1)] = i;
         need[i] = 0;
@@ -132,18 +137,22 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
     }
     __syncthreads();
     const int ncol = s_cnt;
-    // nibble tables for the listed columns
+    // nibble tables for the listed columns: one thread per (column, nibble q)
+    // loads the 4 slices X[(y, 4q..4q+3)] and writes the 16 OR-combinations
     if (p.use_table) {
-      for (int i = threadIdx.x; i < ncol * NQ * 16; i += blockDim.x) {
-        const int k = i / (NQ * 16), r = i - k * (NQ * 16), q = r >> 4, v = r & 15;
+      for (int i = threadIdx.x; i < ncol * NQ; i += blockDim.x) {
+        const int k = i / NQ, q = i - k * NQ;
         const int y = list[k];
-        uint32_t o = 0;
+        uint32_t xb[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int b = 4 * q + j;
-          if (((v >> j) & 1) && b < p.dmax) o |= X[y * p.dmax + b];
-        }
-        T[((size_t)y * NQ + q) * 16 + v] = o;
+        for (int j = 0; j < 4; ++j) xb[j] = (4 * q + j < p.dmax) ? X[y * p.dmax + 4 * q + j] : 0u;
+        uint32_t tv[16];
+        tv[0] = 0u;
+#pragma unroll
+        for (int v = 1; v < 16; ++v) tv[v] = tv[v & (v - 1)] | xb[__ffs(v) - 1];
+        uint4* dst = reinterpret_cast<uint4*>(T + (y * NQ + q) * 16);
+#pragma unroll
+        for (int v = 0; v < 16; v += 4) dst[v >> 2] = make_uint4(tv[v], tv[v + 1], tv[v + 2], tv[v + 3]);
       }
       __syncthreads();
     }
@@ -155,13 +164,55 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
       nb = cur;
       if (live) {
         uint32_t acc = 0xffffffffu;
-        // kBU mask loads in flight per thread, then the table lookups
-        constexpr int kBU = 8;
-        for (int k0 = 0; k0 < ncol && (acc & live) != 0; k0 += kBU) {
-          uint64_t mv[kBU];
-          int yv[kBU];
+        const int nvecr = p.row_bytes / 16;
+        if (p.Mr != nullptr && ncol >= nvecr && W < 8) {
+          // dense column list: stream the row-major copy of my row, 16 bytes =
+          // 16/W masks per load, kRV loads in flight; listed columns only.
+          constexpr int L = 16 / W, kRV = 8;
+          const bool all_cols = ncol == p.n;
+          const uint4* rowv = reinterpret_cast<const uint4*>(p.Mr + (size_t)row * p.row_bytes);
+          for (int v0 = 0; v0 < nvecr && (acc & live) != 0; v0 += kRV) {
+            uint4 mv[kRV];
 #pragma unroll
-          for (int u = 0; u < kBU; ++u) {
+            for (int u = 0; u < kRV; ++u)
+              if (v0 + u < nvecr) mv[u] = __ldg(rowv + v0 + u);
+#pragma unroll
+            for (int u = 0; u < kRV; ++u) {
+              if (v0 + u >= nvecr) continue;
+              const uint32_t w4[4] = {mv[u].x, mv[u].y, mv[u].z, mv[u].w};
+#pragma unroll
+              for (int i = 0; i < L; ++i) {
+                const int y = (v0 + u) * L + i;
+                if (y >= p.n) break;
+                if (!all_cols && !inlist[y]) continue;
+                const uint32_t m = (w4[(i * W) >> 2] >> ((8 * W * i) & 31));
+                uint32_t sup = 0;
+                if (p.use_table) {
+                  const uint32_t* Ty = T + y * (NQ * 16);
+#pragma unroll
+                  for (int q = 0; q < NQ; ++q) sup |= Ty[q * 16 + ((m >> (4 * q)) & 15u)];
+                } else {
+                  uint32_t mm = m & (p.dmax >= 32 ? ~0u : ((1u << p.dmax) - 1u));
+                  while (mm) {
+                    const int b = __ffs(mm) - 1;
+                    sup |= X[y * p.dmax + b];
+                    mm &= mm - 1;
+                  }
+                }
+                if ((sup & live) != live) {
+                  if (!((__ldg(Prow + (y >> 5)) >> (y & 31)) & 1u)) sup = 0xffffffffu;
+                }
+                acc &= sup;
+              }
+            }
+          }
+        } else
+        // kBU mask loads in flight per thread, then the table lookups
+        for (int k0 = 0, kBU = 8; k0 < ncol && (acc & live) != 0; k0 += kBU) {
+          uint64_t mv[8];
+          int yv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
             yv[u] = k0 + u < ncol ? list[k0 + u] : -1;
             if (yv[u] >= 0) {
               if constexpr (W == 8) mv[u] = load_mask64(Mrow + (size_t)yv[u] * p.col_stride);
@@ -169,14 +220,14 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
             }
           }
 #pragma unroll
-          for (int u = 0; u < kBU; ++u) {
+          for (int u = 0; u < 8; ++u) {
             const int y = yv[u];
             if (y < 0) continue;
             const uint64_t m = mv[u];
             uint32_t sup = 0;
             if (p.use_table) {
 #pragma unroll
-              for (int q = 0; q < NQ; ++q) sup |= T[((size_t)y * NQ + q) * 16 + ((m >> (4 * q)) & 15u)];
+              for (int q = 0; q < NQ; ++q) sup |= T[(y * NQ + q) * 16 + (uint32_t)((m >> (4 * q)) & 15u)];
             } else {
               uint64_t mm = m & (p.dmax >= 64 ? ~0ull : ((1ull << p.dmax) - 1ull));
               while (mm) {
@@ -195,7 +246,7 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
         }
         nb = cur & (acc | ~active);
       }
-      p.X2[((size_t)(t & 1) * p.NW + w) * rows + row] = nb;
+      p.X2[((size_t)(t & 1) * p.NW + w) * rows4 + row] = nb;
     }
     word_sync(bar, p.RB, ++epoch);
     // ---- gather the word's new rows; per-state flags (every CTA redundantly)
@@ -205,12 +256,36 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
     }
     __syncthreads();
     uint32_t diff = 0;
-    const uint32_t* Xg = p.X2 + ((size_t)(t & 1) * p.NW + w) * rows;
-    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-      const uint32_t o = X[i], nw = __ldcg(Xg + i);
-      diff |= o ^ nw;
-      if (o ^ nw) need[i / p.dmax] = 1;
-      X[i] = nw;
+    const uint32_t* Xg = p.X2 + ((size_t)(t & 1) * p.NW + w) * rows4;
+    {
+      // 16-byte loads, all issued before use; the last partial group of 4
+      // rows is read past `rows` (the stride is rows4) and ignored
+      const uint4* Xg4 = reinterpret_cast<const uint4*>(Xg);
+      const int r4 = rows4 >> 2;
+      constexpr int U = 4;
+      for (int i0 = threadIdx.x; i0 < r4; i0 += U * blockDim.x) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * blockDim.x;
+          if (i < r4) v[u] = __ldcg(Xg4 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * blockDim.x;
+          if (i >= r4) continue;
+          const uint32_t nw4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int r = 4 * i + k;
+            if (r >= rows) break;
+            const uint32_t o = X[r], nw = nw4[k];
+            diff |= o ^ nw;
+            if (o ^ nw) need[r / p.dmax] = 1;
+            X[r] = nw;
+          }
+        }
+      }
     }
     diff = __reduce_or_sync(0xffffffffu, diff);
     if (lane == 0 && diff) atomicOr(&s_or, diff);
@@ -234,6 +309,7 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
       if (stop_conv & bit) s_status[threadIdx.x] = (wipe & bit) ? 1 : 0;
     }
     active &= ~(stop_wipe | stop_conv);
+    if (dbg && t < 63) dbg[t] = globaltimer();
     __syncthreads();
     if (active == 0) break;
   }
@@ -263,7 +339,8 @@ __global__ void __launch_bounds__(kBT) rac_batch_bs(BatchBSParams p) {
 
 size_t batch_bs_smem(int n, int dmax, int W, bool use_table) {
   const size_t rows = (size_t)n * dmax;
-  return rows * 4 + (use_table ? (size_t)n * (2 * W) * 16 * 4 : 0) + (size_t)n * 4 + (((size_t)n + 15) & ~(size_t)15);
+  return ((rows + 3) & ~(size_t)3) * 4 + (use_table ? (size_t)n * (2 * W) * 16 * 4 : 0) + (size_t)n * 4 +
+         2 * (((size_t)n + 15) & ~(size_t)15);
 }
 
 cudaError_t batch_bs_occupancy(int W, size_t smem, int* out) {

@@ -108,12 +108,15 @@ struct BatchParams {
   int32_t* iters;         // [S]
   int32_t* status;        // [S]
   const int32_t* seed_var;  // nullable [S]: per-state seed variable (-1 = all)
+  int32_t* removed_at;      // nullable, single-state launches only: [n*64] removal epochs (pre-zeroed)
   uint32_t flags;
 };
 
 struct BatchBSParams {
   const uint8_t* M;
   size_t col_stride;
+  const uint8_t* Mr;        // nullable row-major copy (row stride row_bytes)
+  int row_bytes;
   int n, dmax;
   const uint32_t* P;
   int pw;
@@ -131,6 +134,7 @@ struct BatchBSParams {
   uint32_t* X2;             // [2][NW][n*dmax] exchange buffers
   unsigned* bar;            // [NW][4] per-word barrier words (zero between launches)
   uint32_t flags;
+  unsigned long long* dbg;  // nullable: [grid][64] per-CTA pass-end timestamps (RAC_DEBUG_TIMELINE)
 };
 
 // Dynamic smem of rac_fused / rac_pass / rac_batch: D (dbytes), then the

@@ -495,9 +495,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_batch(BatchParams p)
     __syncthreads();
     const bool lst = seeded || t > 1;
     if (pick_rows(g, live, lst ? vcnt : g.n))
-      row_sweep<W, G>(g, Ds, R, nullptr, t, gidx, ngroups);
+      row_sweep<W, G>(g, Ds, R, p.removed_at, t, gidx, ngroups);
     else
-      column_sweep<W>(g, Db, R, nullptr, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
+      column_sweep<W>(g, Db, R, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
     __syncthreads();
     int changed = 0, wipe = 0;
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) {

@@ -30,6 +30,7 @@ RAC_ENCCL = -4
 RAC_ESTATE = -5
 RAC_EUNSUPPORTED = -6
 RAC_FULL_FIXPOINT = 1
+RAC_OPT_NCCL_SELF = 1
 RAC_MAX_DOM = 64
 RAC_NCCL_ID_BYTES = 128
 
@@ -143,10 +144,11 @@ def rac_get_nccl_unique_id() -> bytes:
 
 
 def make_options(device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
-                 virtual_shards: int = 0):
+                 virtual_shards: int = 0, nccl_self: bool = False):
     o = rac_options()
     lib.rac_default_options(ctypes.byref(o))
     o.device, o.rank, o.world, o.virtual_shards = device, rank, world, virtual_shards
+    o.flags = RAC_OPT_NCCL_SELF if nccl_self else 0
     keep = None
     if nccl_unique_id is not None:
         keep = ctypes.create_string_buffer(bytes(nccl_unique_id), RAC_NCCL_ID_BYTES)
@@ -185,7 +187,8 @@ class RacContext:
     # ---- creation
     @classmethod
     def create(cls, n_vars: int, dom_sizes, xs, ys, rows, device: int = 0, rank: int = 0, world: int = 1,
-               nccl_unique_id: Optional[bytes] = None, virtual_shards: int = 0) -> "RacContext":
+               nccl_unique_id: Optional[bytes] = None, virtual_shards: int = 0,
+               nccl_self: bool = False) -> "RacContext":
         """rac_create from relation arrays: constraint k on (xs[k], ys[k]) with
         rows[k, a] = c_xy|(x,a) bitsets (uint64)."""
         dom = np.ascontiguousarray(dom_sizes, dtype=np.int32)
@@ -202,7 +205,7 @@ class RacContext:
             arr["x"] = xs
             arr["y"] = ys
             arr["rows"] = base + stride * np.arange(m, dtype=np.uint64)
-        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards)
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self)
         h = ctypes.c_void_p()
         rc = lib.rac_create(n_vars, _i32p(dom), m, rel if m else None, ctypes.byref(opt), ctypes.byref(h))
         _check(rc)
@@ -216,8 +219,8 @@ class RacContext:
     @classmethod
     def create_random(cls, n_vars: int, d: int, dens_q32: int, t_q16: int, seed: int, device: int = 0,
                       rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
-                      virtual_shards: int = 0) -> "RacContext":
-        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards)
+                      virtual_shards: int = 0, nccl_self: bool = False) -> "RacContext":
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self)
         h = ctypes.c_void_p()
         _check(lib.rac_create_random(n_vars, d, dens_q32, t_q16, seed, ctypes.byref(opt), ctypes.byref(h)))
         del keep

@@ -94,3 +94,5 @@ def test_world_options_validation():
     dom = np.full(4, 2, dtype=np.int32)
     rc = rac.lib.rac_create(4, rac._i32p(dom), 0, None, ctypes.byref(o), ctypes.byref(h))
     assert rc == rac.RAC_EINVAL  # world > 1 without a unique id
+    o2, _ = rac.make_options(world=2, rank=0, nccl_unique_id=b"x" * 128, nccl_self=True)
+    assert rac.lib.rac_create(4, rac._i32p(dom), 0, None, ctypes.byref(o2), ctypes.byref(h)) == rac.RAC_EINVAL

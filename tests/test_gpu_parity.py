@@ -449,3 +449,63 @@ def test_search_parity(rac):
             assert st_g[key] == st_o[key], (k, key, st_g[key], st_o[key])
         if r_o == 0:
             assert np.array_equal(sol_g, sol_o)
+
+
+def test_batched_corpus(rac):
+    """Batched enforcement (bit-sliced, and the per-state kernel via RAC_BATCH_IMPL=state) on
+    random instances with odd row counts and non-uniform domains: every state equals the
+    oracle's single-state result; seeded and unseeded; batch sizes not multiples of 32."""
+    import os
+    import torch
+    rng = np.random.default_rng(5)
+    for impl in ("bs", "state"):
+        if impl == "state":
+            os.environ["RAC_BATCH_IMPL"] = "state"
+        try:
+            for k, inst in enumerate(I.random_corpus(40, seed0=91, n_range=(2, 15), d_range=(1, 7))):
+                orc = oracle.Oracle.from_instance(inst)
+                S = int(rng.integers(1, 70))
+                states = np.stack([synth.w_rand(inst.dom, 0.85, seed=1000 * k + s) for s in range(S)])
+                seeds = np.full(S, -1, dtype=np.int32)
+                st_root, root, _, _ = orc.rac(inst.full_domains(), with_epochs=False)
+                if st_root == oracle.OK:  # some states as assignments on the root fixpoint (seeded)
+                    for s in range(0, S, 2):
+                        ds, x, v = synth.w_seed(root, k, s)
+                        states[s], seeds[s] = ds, x
+                ctx = rac.RacContext.from_instance(inst)
+                din = torch.from_numpy(states.view(np.int64)).cuda()
+                dout = torch.zeros_like(din)
+                its = torch.zeros(S, dtype=torch.int32, device="cuda")
+                sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+                for seeded in (False, True):
+                    if seeded:
+                        ctx.enforce_batch_seeded(S, din, dout, its, sts, torch.from_numpy(seeds).cuda())
+                    else:
+                        ctx.enforce_batch(S, din, dout, its, sts)
+                    torch.cuda.synchronize()
+                    out = dout.cpu().numpy().view(np.uint64)
+                    it_h, st_h = its.cpu().numpy(), sts.cpu().numpy()
+                    for s in range(S):
+                        e = orc.rac(states[s], with_epochs=False)
+                        assert (st_h[s], it_h[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (impl, k, s, seeded)
+        finally:
+            os.environ.pop("RAC_BATCH_IMPL", None)
+
+
+def test_nccl_exchange_leg_single_rank(rac):
+    """The multi-GPU path with its real NCCL all-gather (a one-rank communicator,
+    RAC_OPT_NCCL_SELF) gives the oracle's results: exercises dlopen of libnccl, comm init,
+    the in-place ncclAllGather on the enforcement stream and the chunked host loop."""
+    for k, inst in enumerate(I.random_corpus(60, seed0=97)):
+        orc = oracle.Oracle.from_instance(inst)
+        ctx = rac.RacContext.from_instance(inst, nccl_self=True)
+        d_in = synth.w_rand(inst.dom, 0.9, seed=k)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (k, full))
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.70)
+    ctx = rac.RacContext.create_random(2000, 32, dq, tq, 1, nccl_self=True)
+    orc = oracle.Oracle.from_synth(2000, 32, dq, tq, 1)
+    root = synth.full_domains(np.full(2000, 32))
+    g, o = both(ctx, orc, root)
+    assert_same(g, o, "c3-prop nccl")
