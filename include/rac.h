@@ -191,6 +191,16 @@ int rac_enforce_batch_seeded(rac_ctx* ctx, int32_t n_states, const uint64_t* d_i
                              int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev,
                              uint32_t flags, void* stream);
 
+/* Measurement of the batched contraction alone: ONE pass of Eq. 1 (every
+ * column tested, no loop control) for n_states device states, d_out[s] = D_1.
+ * impl 0 = bit-sliced ALU pass (32 states per u32 OR); impl 1 = tcgen05
+ * tensor-core pass (tcgen05.mma.kind::f16: per column y, 128 rows x 16 mask
+ * bits times 16 values x 256 states, fp32 counts in TMEM, count > 0 tested in
+ * the epilogue).  impl 1 needs max dom <= 16.  world == 1 only.  This is the
+ * A/B behind the batched-mode choice, not an enforcement API. */
+int rac_batch_pass_eval(rac_ctx* ctx, int32_t impl, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                        void* stream);
+
 /* ---- search (Alg. 2) ---------------------------------------- */
 typedef struct {
   int64_t assignments;      /* assign + seeded enforcement events (Table 1's unit) */

@@ -97,6 +97,8 @@ struct rac_ctx {
   size_t bs_bar_cap = 0;           // words
   unsigned long long* dbg = nullptr;  // RAC_DEBUG_TIMELINE phase timestamps [256]
   unsigned long long* bs_dbg = nullptr;  // bit-sliced batch: [ctas][64] pass-end timestamps
+  uint32_t* eval_buf = nullptr;          // rac_batch_pass_eval scratch
+  size_t eval_cap = 0;
   int bs_dbg_ctas = 0;
   uint64_t* h_in = nullptr;        // pinned
   uint64_t* h_out = nullptr;
@@ -161,6 +163,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->bs_bar);
   cudaFree(c->dbg);
   cudaFree(c->bs_dbg);
+  cudaFree(c->eval_buf);
   cudaFreeHost(c->h_in);
   cudaFreeHost(c->h_out);
   cudaFreeHost(c->h_scalars);
@@ -625,6 +628,7 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   cudaFree(c->bs_bar);
   cudaFree(c->dbg);
   cudaFree(c->bs_dbg);
+  cudaFree(c->eval_buf);
     c->buf_seeds = nullptr;
     CK(c, cudaMalloc(&c->buf_seeds, (size_t)n_seeds * 4));
     c->seed_cap = (size_t)n_seeds;
@@ -698,6 +702,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       cudaFree(c->bs_bar);
   cudaFree(c->dbg);
   cudaFree(c->bs_dbg);
+  cudaFree(c->eval_buf);
       c->bs_bar = nullptr;
       CK(c, cudaMalloc(&c->bs_bar, (size_t)NWmax * 16));
       CK(c, cudaMemsetAsync(c->bs_bar, 0, (size_t)NWmax * 16, st));
@@ -754,6 +759,40 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   if (occ1 < 1) return fail(c, RAC_EUNSUPPORTED, "batched kernel does not fit on an SM (n too large)");
   CK(c, launch_batch(c->W, c->G, p, n_states, smem1, st));
   c->launches = 1;
+  return 0;
+}
+
+int rac_batch_pass_eval(rac_ctx* c, int32_t impl, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
+                        void* stream) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (n_states < 1 || !d_in_dev || !d_out_dev || (impl != 0 && impl != 1)) return fail(c, RAC_EINVAL, "bad arguments");
+  if (c->use_nccl() || c->x_lo != 0 || c->x_hi != c->n) return fail(c, RAC_EUNSUPPORTED, "single-GPU contexts only");
+  if (impl == 1 && c->dmax > 16) return fail(c, RAC_EUNSUPPORTED, "tensor-core pass needs max dom <= 16");
+  CK(c, cudaSetDevice(c->device));
+  const int rows = c->n * c->dmax, rows4 = (rows + 3) & ~3, NW = (n_states + 31) / 32;
+  const size_t need = (size_t)2 * NW * rows4 * 4;
+  if (need > c->eval_cap) {
+    cudaFree(c->eval_buf);
+    c->eval_buf = nullptr;
+    CK(c, cudaMalloc(&c->eval_buf, need));
+    c->eval_cap = need;
+  }
+  TcPassParams p{};
+  p.M = c->M;
+  p.col_stride = c->col_stride;
+  p.W = c->W;
+  p.n = c->n;
+  p.dmax = c->dmax;
+  p.rows = rows;
+  p.P = c->P;
+  p.pw = c->pw;
+  p.Xin = c->eval_buf;
+  p.Xout = c->eval_buf + (size_t)NW * rows4;
+  p.rows4 = rows4;
+  p.NW = NW;
+  CK(c, launch_batch_pass_eval(impl, p, d_in_dev, c->dommask, n_states, d_out_dev, (cudaStream_t)stream));
+  c->launches = 3;
   return 0;
 }
 

@@ -137,6 +137,18 @@ struct BatchBSParams {
   unsigned long long* dbg;  // nullable: [grid][64] per-CTA pass-end timestamps (RAC_DEBUG_TIMELINE)
 };
 
+struct TcPassParams {
+  const uint8_t* M;        // column-major masks
+  size_t col_stride;
+  int W;
+  int n, dmax, rows;
+  const uint32_t* P;
+  int pw;
+  const uint32_t* Xin;     // [NW][rows4] state bit slices
+  uint32_t* Xout;          // [NW][rows4]
+  int rows4, NW;
+};
+
 // Dynamic smem of rac_fused / rac_pass / rac_batch: D (dbytes), then the
 // incremental column list (u16[n]) and the per-variable "changed" flags (u8[n]).
 __host__ __device__ constexpr size_t list_offset(int dbytes) { return (size_t)dbytes; }
@@ -163,6 +175,9 @@ cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, i
 cudaError_t launch_batch(int W, int G, const BatchParams& p, int n_states, size_t smem, cudaStream_t s);
 cudaError_t batch_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
 size_t batch_bs_smem(int n, int dmax, int W, bool use_table);
+struct TcPassParams;
+cudaError_t launch_batch_pass_eval(int impl, const TcPassParams& p, const uint64_t* d_in, const uint64_t* dommask,
+                                   int S, uint64_t* d_out, cudaStream_t st);
 cudaError_t batch_bs_occupancy(int W, size_t smem, int* blocks_per_sm);
 cudaError_t launch_batch_bs(int W, const BatchBSParams& p, int grid, size_t smem, cudaStream_t s);
 

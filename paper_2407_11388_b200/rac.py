@@ -62,7 +62,7 @@ class rac_options(ctypes.Structure):
 # Every symbol include/rac.h declares (checked by tests/test_abi.py).
 EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforce", "rac_enforce_ex",
            "rac_enforce_async", "rac_enforce_batch", "rac_enforce_seeded", "rac_enforce_seeded_async",
-           "rac_enforce_batch_seeded", "rac_search", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
+           "rac_enforce_batch_seeded", "rac_search", "rac_batch_pass_eval", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
            "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
            "rac_last_launch_count", "rac_last_error", "rac_destroy"]
 
@@ -90,6 +90,7 @@ def _load() -> ctypes.CDLL:
         "rac_enforce_seeded_async": (ctypes.c_int, [P, P, P, P, P, P, i32, u32, P]),
         "rac_enforce_batch_seeded": (ctypes.c_int, [P, i32, P, P, P, P, P, u32, P]),
         "rac_search": (ctypes.c_int, [P, u64p, ctypes.c_int64, u32, i32p, ctypes.POINTER(rac_search_stats)]),
+        "rac_batch_pass_eval": (ctypes.c_int, [P, i32, i32, P, P, P]),
         "rac_n_vars": (i32, [P]),
         "rac_max_dom": (i32, [P]),
         "rac_mask_bytes": (i32, [P]),
@@ -297,6 +298,11 @@ class RacContext:
         _check(rc, self._h)
         stats = {k: getattr(st, k) for k, _ in rac_search_stats._fields_}
         return rc, (sol if rc == RAC_OK else None), stats
+
+    def batch_pass_eval(self, impl: int, n_states: int, d_in_dev, d_out_dev, stream=None) -> None:
+        """rac_batch_pass_eval: one Eq. 1 pass for n_states states (0 = bit-sliced, 1 = tcgen05)."""
+        _check(lib.rac_batch_pass_eval(self._h, impl, n_states, _ptr(d_in_dev), _ptr(d_out_dev),
+                                       _stream_ptr(stream)), self._h)
 
     def enforce_async(self, d_in_dev, d_out_dev, iters_dev, status_dev, removed_at_dev=None, full: bool = False,
                       stream=None) -> None:

@@ -509,3 +509,40 @@ def test_nccl_exchange_leg_single_rank(rac):
     root = synth.full_domains(np.full(2000, 32))
     g, o = both(ctx, orc, root)
     assert_same(g, o, "c3-prop nccl")
+
+
+# ----------------------------------------------------------------------------- batched contraction A/B
+def test_batch_pass_eval_tc_and_bitsliced(rac):
+    """One Eq. 1 pass for many states by the bit-sliced ALU contraction (impl 0) and the
+    tcgen05 tensor-core contraction (impl 1): both equal the oracle's first step (values
+    with removal epoch 1), on C5 dive states and on random instances with d <= 16."""
+    import torch
+    cases = []
+    inst = synth.random_csp(200, 16, 0.8, 0.3, 1)
+    orc = oracle.Oracle.from_instance(inst)
+    _, root, _, _ = orc.rac(inst.full_domains(), with_epochs=False)
+    states = synth.dive_states(root, lambda D: orc.rac(D, with_epochs=False)[:2], 300, seed=3)
+    cases.append((inst, np.stack(states)))
+    for k, ins in enumerate(I.random_corpus(20, seed0=101, n_range=(2, 40), d_range=(1, 16))):
+        cases.append((ins, np.stack([synth.w_rand(ins.dom, 0.8, seed=50 * k + s) for s in range(37)])))
+    for ci, (ins, st) in enumerate(cases):
+        orc = oracle.Oracle.from_instance(ins)
+        ctx = rac.RacContext.from_instance(ins)
+        S = st.shape[0]
+        din = torch.from_numpy(st.view(np.int64)).cuda()
+        expect = []
+        for s in range(S):
+            _, _, _, rem = orc.rac(st[s])
+            one = st[s].copy()
+            for x in range(ins.n):
+                for a in range(64):
+                    if rem[x, a] == 1:
+                        one[x] &= ~U64(1 << a)
+            expect.append(one)
+        for impl in (0, 1):
+            dout = torch.zeros_like(din)
+            ctx.batch_pass_eval(impl, S, din, dout)
+            torch.cuda.synchronize()
+            out = dout.cpu().numpy().view(np.uint64)
+            for s in range(S):
+                assert np.array_equal(out[s], expect[s]), (ci, impl, s)
