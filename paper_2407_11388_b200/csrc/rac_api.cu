@@ -252,8 +252,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   CKC(cudaMemcpyAsync(c->dommask, c->dommask_h.data(), (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
   CKC(cudaMalloc(&c->R3, (size_t)3 * n * 8));
   CKC(cudaMemsetAsync(c->R3, 0, (size_t)3 * n * 8, c->stream));
-  CKC(cudaMalloc(&c->bar, 16));
-  CKC(cudaMemsetAsync(c->bar, 0, 16, c->stream));
+  CKC(cudaMalloc(&c->bar, 32));
+  CKC(cudaMemsetAsync(c->bar, 0, 32, c->stream));  // [0..3] grid barrier, [4..6] row counters
   const size_t gtot = (size_t)c->world * c->blk;
   CKC(cudaMalloc(&c->sh.Dcur, (size_t)n * 8));
   CKC(cudaMalloc(&c->sh.Dg, gtot * 8));
@@ -330,6 +330,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.removed_at = removed_at;
   p.R = c->R3;
   p.bar = c->bar;
+  p.wctr = c->bar + 4;
   p.flags = flags;
   p.seeds = seeds;
   p.n_seeds = n_seeds;

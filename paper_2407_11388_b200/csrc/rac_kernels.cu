@@ -138,7 +138,8 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
 // segments so that every group gets several items.
 template <int W, int G>
 __device__ __forceinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
-                                          int32_t* removed_at, int t, long gidx, long ngroups) {
+                                          int32_t* removed_at, int t, long gidx, long ngroups,
+                                          unsigned* wctr = nullptr) {
   const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
@@ -152,18 +153,44 @@ __device__ __forceinline__ void row_sweep(const PassGeom& g, const uint4* Ds, un
   const int seg = ((nvec + n_seg - 1) / n_seg + G * kUnrollR - 1) / (G * kUnrollR) * (G * kUnrollR);
   n_seg = (nvec + seg - 1) / seg;
   const int items = rows * n_seg;
-  for (int it = (int)gidx; it < items; it += ng) {
+  // Work items: static round robin, or (wctr != nullptr) claimed dynamically
+  // in chunks by each warp so that the pass ends within about one item.
+  constexpr int kClaim = 4;  // items per group per claim
+  const int gpw = 32 / G, gw = lane / G;
+  int it = (int)gidx, chunk_end = 0;
+  if (wctr) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(wctr, (unsigned)(kClaim * gpw));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    it = (int)base + gw;
+    chunk_end = (int)base + kClaim * gpw;
+  }
+  // the loop exit is warp-uniform (groups of a warp share the claims)
+  while (!__all_sync(0xffffffffu, it >= items)) {
     int r = it, sgi = 0;
     if (n_seg > 1) { r = it / n_seg; sgi = it - r * n_seg; }
     const int xl = r / g.dmax, a = r - xl * g.dmax;
     const int x = g.x_lo + xl;
-    if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;  // dead row: (x,a) ∉ D_{t-1}
-    const uint4* row = reinterpret_cast<const uint4*>(g.Mr + (size_t)(row0 + r) * g.dbytes);
-    const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
-    const int vb = sgi * seg, ve = min(vb + seg, nvec);
-    if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
-      atomicOr(&R[x], 1ull << a);
-      if (removed_at) removed_at[(size_t)x * 64 + a] = t;
+    if (it < items && ((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) {  // dead rows ((x,a) ∉ D_{t-1}) are skipped
+      const uint4* row = reinterpret_cast<const uint4*>(g.Mr + (size_t)(row0 + r) * g.dbytes);
+      const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
+      const int vb = sgi * seg, ve = min(vb + seg, nvec);
+      if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
+        atomicOr(&R[x], 1ull << a);
+        if (removed_at) removed_at[(size_t)x * 64 + a] = t;
+      }
+    }
+    if (wctr) {
+      it += gpw;
+      if (it >= chunk_end) {  // warp-uniform: every group of the warp runs out together
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(wctr, (unsigned)(kClaim * gpw));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        it = (int)base + gw;
+        chunk_end = (int)base + kClaim * gpw;
+      }
+    } else {
+      it += ng;
     }
   }
 }
@@ -176,7 +203,9 @@ __device__ __forceinline__ bool pick_rows(const PassGeom& g, long long live, int
   const long long rows = (long long)(g.x_hi - g.x_lo) * g.dmax;
   // tiny tensors are latency-bound: whole rows are fewer, simpler work items
   if (rows * (long long)g.dbytes <= (256ll << 10)) return true;
-  return live * (long long)g.n <= rows * (long long)ncol;
+  // bytes of each layout, the column stream weighted by its measured rate
+  // (~3.7 vs ~6.5 TB/s at C3, profiles/r01d timeline): 7 col bytes ~ 4 row bytes
+  return 4 * live * (long long)g.n <= 7 * rows * (long long)ncol;
 }
 
 // Live rows (x,a) of variables [x_lo, x_hi) in D (every thread of the CTA gets it).
@@ -262,12 +291,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
       ++t;
       unsigned long long* Rc = p.R + (size_t)(t % 3) * g.n;
       unsigned long long* Rn = p.R + (size_t)((t + 1) % 3) * g.n;
-      // R of pass t+1 was last read before the previous barrier: clear it now.
+      // R (and the row counter) of pass t+1 were last used before the
+      // previous barrier: clear them now.
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.wctr[(t + 1) % 3] = 0u;
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
       if (pick_rows(g, live, lst ? vcnt : g.n))
-        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups);
+        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr + (t % 3));
       else
         column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
       RAC_MARK();
@@ -289,11 +320,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
       changed = __syncthreads_or(changed);
       wipe = __syncthreads_or(wipe);
       RAC_MARK();
-      vcnt = block_compact(vneed, vlist, g.n, scratch);
-      live = count_live<W>(Db, 0, g.n, scratch);
-      RAC_MARK();
       if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
       if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
+      vcnt = block_compact(vneed, vlist, g.n, scratch);        // next pass's columns
+      live = count_live<W>(Db, 0, g.n, scratch);
+      RAC_MARK();
     }
   }
   if (blockIdx.x == 0) {
@@ -314,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   if (s_last) {
     __threadfence();
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.R[(size_t)g.n + x] = 0ull;
+    if (threadIdx.x == 0) p.wctr[1] = 0u;
     if (threadIdx.x == 0 && gridDim.x > 1) {
       p.bar[0] = 0u;
       p.bar[1] = 0u;
