@@ -252,8 +252,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   CKC(cudaMemcpyAsync(c->dommask, c->dommask_h.data(), (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
   CKC(cudaMalloc(&c->R3, (size_t)3 * n * 8));
   CKC(cudaMemsetAsync(c->R3, 0, (size_t)3 * n * 8, c->stream));
-  CKC(cudaMalloc(&c->bar, 32));
-  CKC(cudaMemsetAsync(c->bar, 0, 32, c->stream));  // [0..3] grid barrier, [4..6] row counters
+  CKC(cudaMalloc(&c->bar, 64));
+  CKC(cudaMemsetAsync(c->bar, 0, 64, c->stream));  // [0..3] grid barrier, [4..6] row counters, [8..10] removal flags
   const size_t gtot = (size_t)c->world * c->blk;
   CKC(cudaMalloc(&c->sh.Dcur, (size_t)n * 8));
   CKC(cudaMalloc(&c->sh.Dg, gtot * 8));
@@ -331,10 +331,11 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.R = c->R3;
   p.bar = c->bar;
   p.wctr = c->bar + 4;
+  p.rflag = c->bar + 8;
   p.flags = flags;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
-  if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, 256 * 8));
+  if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
   p.dbg = c->dbg;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
   if (c->fused_grid == 1 && (seeds == nullptr || n_seeds == 1)) {
@@ -936,6 +937,14 @@ int rac_debug_timeline(rac_ctx* c, unsigned long long* out, int cap) {
   int n = (int)std::min<unsigned long long>(buf[0], (unsigned long long)cap);
   for (int i = 0; i < n; ++i) out[i] = buf[1 + i];
   return n;
+}
+
+// Tooling: per-CTA (start, first-barrier arrival, end) stamps of the last fused launch.
+int rac_debug_cta_stamps(rac_ctx* c, unsigned long long* out, int cap) {
+  if (!c || !c->dbg || !out) return 0;
+  const int cnt = std::min(cap, 3 * c->fused_grid);
+  if (cudaMemcpy(out, c->dbg + 256, (size_t)cnt * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return cnt;
 }
 
 // Tooling: per-CTA pass-end timestamps of the last bit-sliced batch launch.

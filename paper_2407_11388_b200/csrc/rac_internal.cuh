@@ -77,6 +77,7 @@ struct FusedParams {
   unsigned long long* R;    // [3][n] removal masks (rotating)
   unsigned* bar;            // grid barrier words [4]
   unsigned* wctr;           // [3] per-pass dynamic row counters (rotating like R)
+  unsigned* rflag;          // [3] per-pass "some value was removed" flags (rotating like R)
   const int32_t* seeds;     // nullable device [n_seeds]: Alg. 1 initial @changed
   int n_seeds;
   uint32_t flags;

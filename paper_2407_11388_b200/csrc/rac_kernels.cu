@@ -44,7 +44,7 @@ constexpr int kOK = 0, kWIPEOUT = 1;
 template <int W>
 __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                              int32_t* removed_at, int t, long warp0, long nwarps,
-                                             const uint16_t* cols, int ncol) {
+                                             const uint16_t* cols, int ncol, unsigned* rflag = nullptr) {
   constexpr int RPL = 16 / W, RPW = 32 * RPL;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
@@ -122,6 +122,7 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
         }
       }
     }
+    if (fail && rflag) atomicOr(rflag, 1u);  // this pass removed something
     for (uint32_t f = fail; f; f &= f - 1u) {
       const int r = r0 + __ffs(f) - 1;
       const int xl = r / g.dmax, a = r - xl * g.dmax;
@@ -139,7 +140,7 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
 template <int W, int G>
 __device__ __forceinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
                                           int32_t* removed_at, int t, long gidx, long ngroups,
-                                          unsigned* wctr = nullptr) {
+                                          unsigned* wctr = nullptr, unsigned* rflag = nullptr) {
   const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
@@ -153,45 +154,47 @@ __device__ __forceinline__ void row_sweep(const PassGeom& g, const uint4* Ds, un
   const int seg = ((nvec + n_seg - 1) / n_seg + G * kUnrollR - 1) / (G * kUnrollR) * (G * kUnrollR);
   n_seg = (nvec + seg - 1) / seg;
   const int items = rows * n_seg;
-  // Work items: static round robin, or (wctr != nullptr) claimed dynamically
-  // in chunks by each warp so that the pass ends within about one item.
-  constexpr int kClaim = 4;  // items per group per claim
+  // Work items: static round robin; with wctr the first ~7/8 are static and the
+  // rest are claimed one item per group (a warp claims for its groups, the next
+  // claim in flight while the current item streams), so SMs that drain HBM
+  // faster take more of the tail and the pass ends within about one row.
   const int gpw = 32 / G, gw = lane / G;
-  int it = (int)gidx, chunk_end = 0;
-  if (wctr) {
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(wctr, (unsigned)(kClaim * gpw));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    it = (int)base + gw;
-    chunk_end = (int)base + kClaim * gpw;
-  }
-  // the loop exit is warp-uniform (groups of a warp share the claims)
-  while (!__all_sync(0xffffffffu, it >= items)) {
+  auto process = [&](int it) {
     int r = it, sgi = 0;
     if (n_seg > 1) { r = it / n_seg; sgi = it - r * n_seg; }
     const int xl = r / g.dmax, a = r - xl * g.dmax;
     const int x = g.x_lo + xl;
-    if (it < items && ((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) {  // dead rows ((x,a) ∉ D_{t-1}) are skipped
-      const uint4* row = reinterpret_cast<const uint4*>(g.Mr + (size_t)(row0 + r) * g.dbytes);
-      const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
-      const int vb = sgi * seg, ve = min(vb + seg, nvec);
-      if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
-        atomicOr(&R[x], 1ull << a);
-        if (removed_at) removed_at[(size_t)x * 64 + a] = t;
-      }
+    if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) return;  // dead row: (x,a) ∉ D_{t-1}
+    const uint4* row = reinterpret_cast<const uint4*>(g.Mr + (size_t)(row0 + r) * g.dbytes);
+    const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
+    const int vb = sgi * seg, ve = min(vb + seg, nvec);
+    if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
+      atomicOr(&R[x], 1ull << a);
+      if (rflag) atomicOr(rflag, 1u);  // this pass removed something
+      if (removed_at) removed_at[(size_t)x * 64 + a] = t;
     }
-    if (wctr) {
-      it += gpw;
-      if (it >= chunk_end) {  // warp-uniform: every group of the warp runs out together
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(wctr, (unsigned)(kClaim * gpw));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        it = (int)base + gw;
-        chunk_end = (int)base + kClaim * gpw;
-      }
+  };
+  const int per = wctr ? (items - items / 8) / ng : (items + ng - 1) / ng;
+  const int S = wctr ? per * ng : items;
+  auto claim = [&]() {
+    unsigned b = 0;
+    if (lane == 0) b = atomicAdd(wctr, (unsigned)gpw);
+    return S + (int)__shfl_sync(0xffffffffu, b, 0) + gw;
+  };
+  int k = 0, pending = (wctr && per == 0) ? claim() : 0;
+  for (;;) {  // one loop body (one copy of the row test): static items, then claims
+    int it;
+    if (k < per) {
+      it = (int)gidx + k * ng;
+      if (++k == per && wctr) pending = claim();  // first claim in flight during the last static item
+    } else if (wctr) {
+      it = pending;
+      if (__all_sync(0xffffffffu, it >= items)) break;  // warp-uniform exit
+      pending = claim();
     } else {
-      it += ng;
+      break;
     }
+    if (it < items) process(it);
   }
 }
 
@@ -260,6 +263,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   int nd = 0;
   const bool dbg = p.dbg != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
 #define RAC_MARK() do { if (dbg && nd < 255) p.dbg[1 + nd++] = globaltimer(); } while (0)
+  // per-CTA stamps (debug): [256 + 3*cta] start, first barrier arrival, end
+  const bool dbg_cta = p.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 1000;
+  if (dbg_cta) p.dbg[256 + 3 * blockIdx.x] = globaltimer();
   RAC_MARK();
   for (int i = threadIdx.x; i < g.n; i += blockDim.x) vneed[i] = 0;
   stage_from_u64<W>(Db, p.d_in, p.dommask, g.n, g.dbytes);
@@ -271,6 +277,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   int t = 0, status = kOK, vcnt = g.n;
   unsigned epoch = 0;
   long long live = count_live<W>(Db, 0, g.n, scratch);
+  int has_empty = 0;  // some D(x) empty (block-uniform)
+  for (int x = threadIdx.x; x < g.n; x += blockDim.x) has_empty |= load_w<W>(Db + x * W) == 0;
+  has_empty = __syncthreads_or(has_empty);
   // Seeded call (Alg. 1 with @changed = seeds): pass 1 tests only the seed columns.
   const bool seeded = p.seeds != nullptr;
   if (seeded) {
@@ -294,31 +303,56 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
       // R (and the row counter) of pass t+1 were last used before the
       // previous barrier: clear them now.
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
-      if (blockIdx.x == 0 && threadIdx.x == 0) p.wctr[(t + 1) % 3] = 0u;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.wctr[(t + 1) % 3] = 0u;
+        p.rflag[(t + 1) % 3] = 0u;
+      }
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
       if (pick_rows(g, live, lst ? vcnt : g.n))
-        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr + (t % 3));
+        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr + (t % 3), p.rflag + (t % 3));
       else
-        column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n);
+        column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
+                        p.rflag + (t % 3));
       RAC_MARK();
+      if (p.dbg != nullptr && t == 1) {  // block-uniform condition: the barrier is safe
+        __syncthreads();
+        if (dbg_cta) p.dbg[256 + 3 * blockIdx.x + 1] = globaltimer();
+      }
       grid_sync(p.bar, gridDim.x, ++epoch);
       RAC_MARK();
       // D_t = D_{t-1} & ~R (every CTA, redundantly); flags for Alg. 1's checks;
-      // the changed variables are the next pass's columns.
+      // the changed variables are the next pass's columns.  A pass that
+      // removed nothing (the per-pass flag is still 0) leaves D as it was:
+      // changed = 0, wipe = "D already had an empty row", no R read.
       int changed = 0, wipe = 0;
-      for (int x = threadIdx.x; x < g.n; x += blockDim.x) {
-        const uint64_t r = __ldcg(&Rc[x]);
-        const uint64_t dv = load_w<W>(Db + x * W);
-        const uint64_t nd = dv & ~r;
-        store_w<W>(Db + x * W, nd);
-        const bool chx = (dv & r) != 0;
-        changed |= chx;
-        wipe |= nd == 0;
-        if (chx) vneed[x] = 1;
+      if (__ldcg(p.rflag + (t % 3)) == 0u) {
+        wipe = has_empty;
+      } else {
+        for (int x0 = threadIdx.x; x0 < g.n; x0 += 4 * blockDim.x) {
+          uint64_t rv[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int x = x0 + k * blockDim.x;
+            rv[k] = x < g.n ? __ldcg(&Rc[x]) : 0ull;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int x = x0 + k * blockDim.x;
+            if (x >= g.n) break;
+            const uint64_t dv = load_w<W>(Db + x * W);
+            const uint64_t nd = dv & ~rv[k];
+            store_w<W>(Db + x * W, nd);
+            const bool chx = (dv & rv[k]) != 0;
+            changed |= chx;
+            wipe |= nd == 0;
+            if (chx) vneed[x] = 1;
+          }
+        }
       }
       changed = __syncthreads_or(changed);
       wipe = __syncthreads_or(wipe);
+      has_empty = wipe;
       RAC_MARK();
       if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
       if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
@@ -333,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   }
   RAC_MARK();
   if (dbg) p.dbg[0] = nd;
+  if (dbg_cta) p.dbg[256 + 3 * blockIdx.x + 2] = globaltimer();
 #undef RAC_MARK
   // The last CTA out resets the barrier words and clears R[1] (the removal
   // buffer pass 1 of the next launch writes): every other CTA has finished
@@ -345,7 +380,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   if (s_last) {
     __threadfence();
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.R[(size_t)g.n + x] = 0ull;
-    if (threadIdx.x == 0) p.wctr[1] = 0u;
+    if (threadIdx.x == 0) {
+      p.wctr[1] = 0u;
+      p.rflag[1] = 0u;
+    }
     if (threadIdx.x == 0 && gridDim.x > 1) {
       p.bar[0] = 0u;
       p.bar[1] = 0u;
