@@ -107,7 +107,6 @@ struct rac_ctx {
   int sm_count = 0;
   int fused_grid = 0;
   int pass_grid = 0;
-  bool fused_coop = true;
   ncclComm_t comm = nullptr;
   int64_t launches = 0;
   bool broken = false;
@@ -383,7 +382,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
   }
   const long max_passes = (long)c->n * c->dmax + 2;
   long enq = 0;
-  int chunk = 2;
+  int chunk = 1;  // a one-pass enforcement (W-stream) needs no speculative pass
   for (;;) {
     for (int k = 0; k < chunk; ++k) {
       for (int b = 0; b < nb; ++b) {

@@ -23,8 +23,11 @@
 //                 TMA bulk copy (cp.async.bulk + mbarrier).  Used by the
 //                 row-sharded multi-GPU path (and virtual shards on one GPU)
 //                 together with rac_shard_{init,slice,update,finalize}.
-//   rac_batch  -- one CTA per domain state (batched mode, per-state design;
-//                 the default batched path is the bit-sliced rac_batch_bs).
+//   rac_batch  -- one CTA per domain state, removal bits in smem and
+//                 __syncthreads as the pass barrier: the single-CTA enforcement
+//                 of small instances (one state) and the per-state batched
+//                 design kept for comparison (the default batched path is the
+//                 bit-sliced rac_batch_bs).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
