@@ -32,8 +32,8 @@
  *
  * Return values: every int-returning call returns >= 0 on success (RAC_OK or
  * RAC_WIPEOUT for enforcement calls) and a negative RAC_E* code on error.
- * Nothing is thrown or aborted across the ABI.  After RAC_ECUDA / RAC_ENCCL
- * the context is unusable and every later call returns RAC_ESTATE.
+ * Nothing is thrown or aborted across the ABI.  After RAC_ECUDA / RAC_ENCCL /
+ * RAC_EPEER the context is unusable and every later call returns RAC_ESTATE.
  * rac_last_error(ctx) gives a message (ctx == NULL: the thread's last failed
  * create).
  *
@@ -49,10 +49,21 @@
  * Multi-GPU (world > 1): rac_create* and every rac_enforce* call are
  * COLLECTIVE over the `world` ranks (one process per GPU).  The relation tensor
  * is row-sharded: rank r holds the masks of variables [x_lo, x_hi) given by
- * rac_shard_range.  After each pass the ranks all-gather the new alive
- * bitvector over NCCL; every rank derives the same stop decision from the
- * gathered vector, so all ranks return identical d_out, iterations and status.
- * Every rank must pass identical n_vars, dom_sizes and d_in.
+ * rac_shard_range.  Two exchange paths (neither is in the paper, which is
+ * single-GPU; BASELINE.json north_star asks for the row sharding):
+ *   NCCL (default): one rac_pass launch per pass over the local rows, then an
+ *     NCCL all-gather of the new alive bitvector; the host polls a done flag.
+ *   Peer memory (RAC_OPT_PEER): the whole enforcement is ONE persistent kernel
+ *     per rank.  Every removal bit found on the local rows is also OR-ed into
+ *     the same word of every peer's removal buffer (NVLink P2P atomics), and
+ *     the grid barrier between passes is extended across ranks with
+ *     system-scope release/acquire arrival words; no host round trip and no
+ *     separate collective per pass.  Needs rac_connect_peers (one process per
+ *     GPU, IPC handles) or rac_connect_peers_local (one process driving
+ *     several ranks) before the first enforcement.
+ * Every rank derives the same stop decision from the same data, so all ranks
+ * return identical d_out, iterations and status.  Every rank must pass
+ * identical n_vars, dom_sizes and d_in, and make the same sequence of calls.
  */
 #ifndef RAC_H
 #define RAC_H
@@ -73,6 +84,9 @@ extern "C" {
 #define RAC_ENCCL (-4)       /* NCCL error (or NCCL unavailable for world > 1)            */
 #define RAC_ESTATE (-5)      /* context unusable after an earlier CUDA/NCCL error         */
 #define RAC_EUNSUPPORTED (-6)/* valid request this build does not support                 */
+#define RAC_EPEER (-7)       /* peer-memory exchange failed (IPC open, or a rank did not
+                                arrive within RAC_PEER_TIMEOUT_MS, default 20000 ms);
+                                context now unusable                                     */
 
 /* ---- flags -------------------------------------------------------------- */
 /* Do not stop at the first wipeout: iterate to the definitional fixpoint D_ac
@@ -96,6 +110,11 @@ typedef struct {
  * path with a one-rank NCCL communicator (exercises the NCCL all-gather leg on
  * a single GPU; results are identical to the fused path). */
 #define RAC_OPT_NCCL_SELF (1u << 0)
+/* rac_options.flags: world > 1 exchanges through peer memory inside the fused
+ * kernel instead of NCCL (see "Multi-GPU" above); 2 <= world <= RAC_MAX_RANKS. */
+#define RAC_OPT_PEER (1u << 1)
+#define RAC_MAX_RANKS 8
+#define RAC_IPC_HANDLE_BYTES 64
 
 typedef struct {
   int32_t device;             /* CUDA device ordinal (rank's GPU)                     */
@@ -107,6 +126,11 @@ typedef struct {
                                  over this many row blocks on one GPU, a device copy
                                  standing in for the all-gather (tests the partition
                                  without NCCL).  0 or 1: fused single-GPU path.      */
+  int32_t max_ctas;           /* > 0: cap the CTAs of the enforcement kernels (and
+                                 launch the fused kernel without the cooperative
+                                 API): lets several RAC_OPT_PEER ranks share one GPU,
+                                 whose grids must then fit on it together.  0: all
+                                 SMs.                                                */
 } rac_options;
 
 /* Fill *opt with defaults: device 0, single GPU, fused path. */
@@ -248,6 +272,25 @@ int rac_local_range(const rac_ctx* ctx, int32_t* x_lo, int32_t* x_hi);
 int rac_read_row(const rac_ctx* ctx, int32_t x, int32_t a, uint64_t* out_masks, uint8_t* out_present);
 /* NCCL unique id for rac_options.nccl_unique_id (call on rank 0, broadcast). */
 int rac_get_nccl_unique_id(void* out /* RAC_NCCL_ID_BYTES */);
+/* Peer-memory exchange (RAC_OPT_PEER contexts).  Each rank exposes one device
+ * region (its removal buffers, removal flags, arrival words and pass counter;
+ * layout private to the library, identical on all ranks).
+ * rac_peer_handle: the region's CUDA IPC handle (RAC_IPC_HANDLE_BYTES bytes) to
+ *   all-gather over the host transport (e.g. torch.distributed).
+ * rac_connect_peers: handles = world x RAC_IPC_HANDLE_BYTES bytes in rank order
+ *   (own entry ignored); opens every peer's region (cudaIpcOpenMemHandle, peer
+ *   access enabled lazily).  RAC_EPEER if a handle cannot be opened.
+ * rac_peer_region / rac_connect_peers_local: the same for ranks driven by ONE
+ *   process: regions[q] = rank q's region pointer (rac_peer_region), devices[q]
+ *   = its device; enables peer access between distinct devices
+ *   (RAC_EUNSUPPORTED if the devices cannot access each other).  Ranks may
+ *   share a device (then size max_ctas so that all grids fit together).
+ * Connect once, before the first enforcement; destroy the ranks' contexts only
+ * after every rank's work has completed. */
+int rac_peer_handle(const rac_ctx* ctx, void* out /* RAC_IPC_HANDLE_BYTES */);
+int rac_connect_peers(rac_ctx* ctx, const void* handles /* world x RAC_IPC_HANDLE_BYTES */);
+int rac_peer_region(const rac_ctx* ctx, void** region_dev);
+int rac_connect_peers_local(rac_ctx* ctx, void* const* regions /* [world] */, const int32_t* devices /* [world] */);
 /* Kernel launches enqueued by the last rac_enforce* call on this context. */
 int64_t rac_last_launch_count(const rac_ctx* ctx);
 

@@ -65,7 +65,10 @@ struct rac_ctx {
   int device = 0;
   int rank = 0, world = 1, vshards = 1;
   bool nccl_self = false;  // world == 1 through the NCCL exchange path (RAC_OPT_NCCL_SELF)
-  bool use_nccl() const { return world > 1 || nccl_self; }
+  bool peer = false;       // world > 1 through the fused kernel + peer-memory exchange (RAC_OPT_PEER)
+  bool connected = false;  // peer regions known (rac_connect_peers*)
+  int max_ctas = 0;        // rac_options.max_ctas
+  bool use_nccl() const { return (world > 1 && !peer) || nccl_self; }
   int n = 0, dmax = 0, W = 0;
   int rows_pad = 0;        // local rows padded to a warp slab
   size_t col_stride = 0;   // bytes per column of the mask tensor
@@ -82,7 +85,13 @@ struct rac_ctx {
   uint32_t* P = nullptr;
   int32_t* dom_d = nullptr;
   uint64_t* dommask = nullptr;
-  unsigned long long* R3 = nullptr;  // fused: [3][n]
+  // Exchange region (one allocation so that one IPC handle maps it): the
+  // fused kernel's rotating removal buffers R[3][n], per-pass removal flags,
+  // the arrival words peers write, and the global pass counter.
+  uint8_t* xr = nullptr;
+  unsigned long long* R3 = nullptr;  // = xr
+  uint8_t* peer_base[RAC_MAX_RANKS] = {};  // every rank's region as seen from this device (self = xr)
+  bool peer_ipc[RAC_MAX_RANKS] = {};       // opened with cudaIpcOpenMemHandle (closed at destroy)
   unsigned* bar = nullptr;
   ShardState sh{};
   uint64_t* buf_in = nullptr;   // blocking-API staging
@@ -118,7 +127,7 @@ namespace {
 int fail(rac_ctx* c, int code, const std::string& msg) {
   if (c) {
     c->err = msg;
-    if (code == RAC_ECUDA || code == RAC_ENCCL) c->broken = true;
+    if (code == RAC_ECUDA || code == RAC_ENCCL || code == RAC_EPEER) c->broken = true;
   } else {
     g_create_error = msg;
   }
@@ -140,12 +149,14 @@ void free_ctx(rac_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
   if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
+  for (int q = 0; q < RAC_MAX_RANKS; ++q)
+    if (c->peer_ipc[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
   cudaFree(c->M);
   cudaFree(c->Mr);
   cudaFree(c->P);
   cudaFree(c->dom_d);
   cudaFree(c->dommask);
-  cudaFree(c->R3);
+  cudaFree(c->xr);
   cudaFree(c->bar);
   cudaFree(c->sh.Dcur);
   cudaFree(c->sh.Dg);
@@ -170,6 +181,12 @@ void free_ctx(rac_ctx* c) {
   delete c;
 }
 
+// Exchange region layout (identical on every rank: it depends on n only).
+size_t xr_rflag_off(int n) { return (size_t)3 * n * 8; }                 // u32[4]
+size_t xr_arrive_off(int n) { return xr_rflag_off(n) + 16; }             // u64[RAC_MAX_RANKS]
+size_t xr_seq_off(int n) { return xr_arrive_off(n) + 8 * RAC_MAX_RANKS; }  // u64
+size_t xr_bytes(int n) { return xr_seq_off(n) + 8; }
+
 size_t kernel_smem(const rac_ctx* c) {
   return fused_smem(c->dbytes, c->n);
 }
@@ -179,15 +196,22 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   rac_options o;
   rac_default_options(&o);
   if (opt) o = *opt;
-  if (o.flags & ~RAC_OPT_NCCL_SELF) return fail(nullptr, RAC_EINVAL, "unknown options.flags");
+  if (o.flags & ~(RAC_OPT_NCCL_SELF | RAC_OPT_PEER)) return fail(nullptr, RAC_EINVAL, "unknown options.flags");
   if ((o.flags & RAC_OPT_NCCL_SELF) && o.world > 1) return fail(nullptr, RAC_EINVAL, "RAC_OPT_NCCL_SELF needs world == 1");
+  if ((o.flags & RAC_OPT_PEER) && (o.world < 2 || o.world > RAC_MAX_RANKS))
+    return fail(nullptr, RAC_EINVAL, "RAC_OPT_PEER needs 2 <= world <= RAC_MAX_RANKS");
+  if (o.max_ctas < 0) return fail(nullptr, RAC_EINVAL, "max_ctas < 0");
   c->nccl_self = (o.flags & RAC_OPT_NCCL_SELF) != 0;
+  c->peer = (o.flags & RAC_OPT_PEER) != 0;
+  c->max_ctas = o.max_ctas;
   c->device = o.device;
   c->world = o.world < 1 ? 1 : o.world;
   c->rank = c->world > 1 ? o.rank : 0;
   c->vshards = (c->world == 1 && o.virtual_shards > 1) ? o.virtual_shards : 1;
-  if (c->world > 1 && (o.rank < 0 || o.rank >= c->world || !o.nccl_unique_id))
-    return fail(nullptr, RAC_EINVAL, "world > 1 needs 0 <= rank < world and nccl_unique_id");
+  if (c->world > 1 && (o.rank < 0 || o.rank >= c->world))
+    return fail(nullptr, RAC_EINVAL, "world > 1 needs 0 <= rank < world");
+  if (c->world > 1 && !c->peer && !o.nccl_unique_id)
+    return fail(nullptr, RAC_EINVAL, "world > 1 needs nccl_unique_id (or RAC_OPT_PEER)");
   if (c->vshards > n) c->vshards = n;
   c->n = n;
   c->dom.assign(dom, dom + n);
@@ -249,10 +273,12 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   CKC(cudaMemcpyAsync(c->dom_d, dom, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
   CKC(cudaMalloc(&c->dommask, (size_t)n * 8));
   CKC(cudaMemcpyAsync(c->dommask, c->dommask_h.data(), (size_t)n * 8, cudaMemcpyHostToDevice, c->stream));
-  CKC(cudaMalloc(&c->R3, (size_t)3 * n * 8));
-  CKC(cudaMemsetAsync(c->R3, 0, (size_t)3 * n * 8, c->stream));
+  CKC(cudaMalloc(&c->xr, xr_bytes(n)));
+  CKC(cudaMemsetAsync(c->xr, 0, xr_bytes(n), c->stream));
+  c->R3 = reinterpret_cast<unsigned long long*>(c->xr);
+  if (c->rank < RAC_MAX_RANKS) c->peer_base[c->rank] = c->xr;
   CKC(cudaMalloc(&c->bar, 64));
-  CKC(cudaMemsetAsync(c->bar, 0, 64, c->stream));  // [0..3] grid barrier, [4..6] row counters, [8..10] removal flags
+  CKC(cudaMemsetAsync(c->bar, 0, 64, c->stream));  // [0..3] grid barrier, [4..6] row counters, [12] peer error
   const size_t gtot = (size_t)c->world * c->blk;
   CKC(cudaMalloc(&c->sh.Dcur, (size_t)n * 8));
   CKC(cudaMalloc(&c->sh.Dg, gtot * 8));
@@ -286,6 +312,10 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   int pocc = 0;
   CKC(pass_occupancy(c->W, c->G, kernel_smem(c), &pocc));
   c->pass_grid = (int)std::max(1L, std::min((long)c->sm_count * std::max(1, pocc), want));
+  if (c->max_ctas > 0) {
+    c->fused_grid = std::min(c->fused_grid, c->max_ctas);
+    c->pass_grid = std::min(c->pass_grid, c->max_ctas);
+  }
   CKC(cudaStreamSynchronize(c->stream));
 #undef CKC
   return 0;
@@ -320,7 +350,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
                   int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
                   int n_seeds = 0) {
   FusedParams p{};
-  p.g = geom_for(c, 0, c->n);
+  p.g = geom_for(c, c->x_lo, c->x_hi);  // world == 1: every row
   p.dommask = c->dommask;
   p.d_in = d_in;
   p.d_out = d_out;
@@ -330,14 +360,30 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.R = c->R3;
   p.bar = c->bar;
   p.wctr = c->bar + 4;
-  p.rflag = c->bar + 8;
+  p.rflag = reinterpret_cast<unsigned*>(c->xr + xr_rflag_off(c->n));
+  p.seq = reinterpret_cast<unsigned long long*>(c->xr + xr_seq_off(c->n));
+  p.mir.world = c->peer ? c->world : 1;
+  p.mir.rank = c->rank;
+  p.mir.n = c->n;
+  p.xerr = reinterpret_cast<int32_t*>(c->bar + 12);
+  if (c->peer) {
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) continue;
+      p.mir.R[q] = reinterpret_cast<unsigned long long*>(c->peer_base[q]);
+      p.mir.flag[q] = reinterpret_cast<unsigned*>(c->peer_base[q] + xr_rflag_off(c->n));
+      p.peer_arrive[q] = reinterpret_cast<unsigned long long*>(c->peer_base[q] + xr_arrive_off(c->n));
+    }
+    p.arrive = reinterpret_cast<unsigned long long*>(c->xr + xr_arrive_off(c->n));
+    const char* to = getenv("RAC_PEER_TIMEOUT_MS");
+    p.timeout_ns = (unsigned long long)(to ? atoll(to) : 20000) * 1000000ull;
+  }
   p.flags = flags;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
   p.dbg = c->dbg;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
-  if (c->fused_grid == 1 && (seeds == nullptr || n_seeds == 1)) {
+  if (c->fused_grid == 1 && !c->peer && (seeds == nullptr || n_seeds == 1)) {
     // One CTA is enough: run the single-CTA variant (removal bits in shared
     // memory, __syncthreads as the pass barrier) -- the batched per-state
     // kernel with one state.
@@ -358,7 +404,10 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   // R[1] (pass 1's removal buffer) is clean: zeroed at create and by the last
   // CTA of every previous launch.
   static const bool no_coop = getenv("RAC_NO_COOP") != nullptr;  // A/B knob (tooling only)
-  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, kernel_smem(c), s, c->fused_grid > 1 && !no_coop));
+  // max_ctas > 0 (several ranks sharing a GPU): ordinary launch, co-residency
+  // is the caller's sizing
+  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, kernel_smem(c), s,
+                     c->fused_grid > 1 && !no_coop && c->max_ctas == 0));
   c->launches++;
   return 0;
 }
@@ -423,6 +472,12 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
+  if (c->peer) {
+    if (!c->connected) return fail(c, RAC_EINVAL, "RAC_OPT_PEER context: call rac_connect_peers first");
+    if (removed_at) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
+    return enforce_fused(c, d_in, d_out, iters, status, nullptr, flags, s, n_seeds >= 0 ? seeds : nullptr,
+                         n_seeds >= 0 ? n_seeds : 0);
+  }
   if (c->use_nccl() || c->vshards > 1) {
     // the sharded driver has no seeded pass 1: a full pass 1 is the superset
     // check (valid under the precondition; identical trajectory, Prop. 2)
@@ -445,6 +500,77 @@ void rac_default_options(rac_options* opt) {
   opt->world = 1;
   opt->rank = 0;
   opt->virtual_shards = 0;
+  opt->max_ctas = 0;
+}
+
+int rac_peer_region(const rac_ctx* c, void** region_dev) {
+  if (!c || !region_dev) return RAC_EINVAL;
+  *region_dev = c->xr;
+  return 0;
+}
+
+int rac_peer_handle(const rac_ctx* c, void* out) {
+  if (!c || !out) return RAC_EINVAL;
+  if (!c->peer) return RAC_EINVAL;
+  if (cudaSetDevice(c->device) != cudaSuccess) return RAC_ECUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, c->xr) != cudaSuccess) {
+    cudaGetLastError();
+    return RAC_ECUDA;
+  }
+  static_assert(sizeof(h) == RAC_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(out, &h, sizeof(h));
+  return 0;
+}
+
+int rac_connect_peers(rac_ctx* c, const void* handles) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (!handles || !c->peer) return fail(c, RAC_EINVAL, "rac_connect_peers needs a RAC_OPT_PEER context and handles");
+  if (c->connected) return fail(c, RAC_EINVAL, "peers already connected");
+  CK(c, cudaSetDevice(c->device));
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)q * RAC_IPC_HANDLE_BYTES, sizeof(h));
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, RAC_EPEER, std::string("cudaIpcOpenMemHandle(rank ") + std::to_string(q) +
+                                     "): " + cudaGetErrorString(e));
+    }
+    c->peer_base[q] = static_cast<uint8_t*>(ptr);
+    c->peer_ipc[q] = true;
+  }
+  c->connected = true;
+  return 0;
+}
+
+int rac_connect_peers_local(rac_ctx* c, void* const* regions, const int32_t* devices) {
+  int rc = check_usable(c);
+  if (rc) return rc;
+  if (!regions || !devices || !c->peer)
+    return fail(c, RAC_EINVAL, "rac_connect_peers_local needs a RAC_OPT_PEER context, regions and devices");
+  if (c->connected) return fail(c, RAC_EINVAL, "peers already connected");
+  if (regions[c->rank] != c->xr || devices[c->rank] != c->device)
+    return fail(c, RAC_EINVAL, "regions[rank] / devices[rank] must be this context's");
+  CK(c, cudaSetDevice(c->device));
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) continue;
+    if (!regions[q]) return fail(c, RAC_EINVAL, "NULL peer region");
+    if (devices[q] != c->device) {
+      int can = 0;
+      CK(c, cudaDeviceCanAccessPeer(&can, c->device, devices[q]));
+      if (!can) return fail(c, RAC_EUNSUPPORTED, "no peer access between the devices");
+      cudaError_t e = cudaDeviceEnablePeerAccess(devices[q], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else CK(c, e);
+    }
+    c->peer_base[q] = static_cast<uint8_t*>(regions[q]);
+  }
+  c->connected = true;
+  return 0;
 }
 
 int rac_shard_range(int32_t n_vars, int32_t world, int32_t rank, int32_t* x_lo, int32_t* x_hi) {
@@ -592,6 +718,7 @@ int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* i
   memcpy(d_out, c->h_out, nb);
   *iterations = c->h_scalars[0];
   const int st = c->h_scalars[1];
+  if (st == RAC_EPEER) return fail(c, RAC_EPEER, "peer exchange timed out (a rank did not arrive)");
   if (st != RAC_OK && st != RAC_WIPEOUT) return fail(c, RAC_ECUDA, "kernel did not report a status");
   return st;
 }
@@ -625,11 +752,6 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   const size_t nb = (size_t)c->n * 8;
   if ((size_t)n_seeds > c->seed_cap) {
     cudaFree(c->buf_seeds);
-  cudaFree(c->bs_X2);
-  cudaFree(c->bs_bar);
-  cudaFree(c->dbg);
-  cudaFree(c->bs_dbg);
-  cudaFree(c->eval_buf);
     c->buf_seeds = nullptr;
     CK(c, cudaMalloc(&c->buf_seeds, (size_t)n_seeds * 4));
     c->seed_cap = (size_t)n_seeds;
@@ -647,6 +769,7 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   memcpy(d_out, c->h_out, nb);
   *iterations = c->h_scalars[0];
   const int st = c->h_scalars[1];
+  if (st == RAC_EPEER) return fail(c, RAC_EPEER, "peer exchange timed out (a rank did not arrive)");
   if (st != RAC_OK && st != RAC_WIPEOUT) return fail(c, RAC_ECUDA, "kernel did not report a status");
   return st;
 }
@@ -701,9 +824,6 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     }
     if ((size_t)NWmax * 4 > c->bs_bar_cap) {
       cudaFree(c->bs_bar);
-  cudaFree(c->dbg);
-  cudaFree(c->bs_dbg);
-  cudaFree(c->eval_buf);
       c->bs_bar = nullptr;
       CK(c, cudaMalloc(&c->bs_bar, (size_t)NWmax * 16));
       CK(c, cudaMemsetAsync(c->bs_bar, 0, (size_t)NWmax * 16, st));
@@ -840,6 +960,7 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
   std::copy(root.begin(), root.end(), doms.begin());
   int depth = 0;
   frames[0].var = pick(doms.data());
+  if (frames[0].var < 0) return fail(c, RAC_EINVAL, "no variable to assign");
   frames[0].todo = doms[frames[0].var];
   assigned[frames[0].var] = 1;
   bool found = false;

@@ -66,6 +66,18 @@ struct PassGeom {
   int dbytes;             // bytes of D in smem (n*W rounded up to 16)
 };
 
+// Peer-memory exchange of the row-sharded fused kernel (world > 1, RAC_OPT_PEER):
+// after each pass a rank writes the removal words of its own rows into every
+// peer's removal buffer (NVLink P2P stores), so after the cross-rank barrier
+// each rank holds the complete R of the pass.  Entries of self are NULL.
+constexpr int kMaxRanks = 8;
+struct Mirror {
+  int world, rank;
+  int n;                               // words per removal buffer
+  unsigned long long* R[kMaxRanks];    // peer q's R[3][n]
+  unsigned* flag[kMaxRanks];           // peer q's per-pass removal flags [3]
+};
+
 struct FusedParams {
   PassGeom g;
   const uint64_t* dommask;  // [n]
@@ -82,6 +94,16 @@ struct FusedParams {
   int n_seeds;
   uint32_t flags;
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
+  // Global pass counter (persists across launches): pass t of this launch is
+  // pass *seq + t; it selects the rotating buffers and is the cross-rank
+  // barrier's sequence number.
+  unsigned long long* seq;
+  // world > 1 (peer exchange) only:
+  Mirror mir;
+  unsigned long long* arrive;                  // own arrival words [kMaxRanks] (written by peers)
+  unsigned long long* peer_arrive[kMaxRanks];  // peer q's arrival words (NULL for self)
+  unsigned long long timeout_ns;               // give up waiting for a peer after this long
+  int32_t* xerr;                               // set to 1 on a peer timeout
 };
 
 struct ShardState {
@@ -464,6 +486,16 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Software grid barrier for a co-resident (cooperative) grid.  bar[0] counts
 // arrivals over the whole launch, bar[1] is the released epoch.
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks, unsigned epoch) {
@@ -473,6 +505,44 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks, unsig
     unsigned prev = atomicAdd(&bar[0], 1u);
     if (prev + 1u == nblocks * epoch) {
       st_release_gpu(&bar[1], epoch);
+    } else {
+      while (ld_acquire_gpu(&bar[1]) < epoch) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The grid barrier extended across ranks (world > 1, peer exchange).  Every
+// CTA fences at system scope (covering its mirrored removals on the peers)
+// before it counts itself in; the CTA that completes the local count
+// publishes "this rank finished global pass seqv" on every peer and waits
+// for every peer's arrival before it releases the local grid.  The wait gives
+// up after p.timeout_ns (a peer that never launched) and sets *p.xerr.
+static __device__ __noinline__ void grid_sync_peer(unsigned* bar, unsigned nblocks, unsigned epoch, const FusedParams& p,
+                                               unsigned long long seqv) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const bool last = nblocks == 1 || atomicAdd(&bar[0], 1u) + 1u == nblocks * epoch;
+    if (last) {
+      __threadfence_system();  // acquire the other CTAs' arrivals before publishing ours
+      for (int q = 0; q < p.mir.world; ++q)
+        if (q != p.mir.rank) st_release_sys64(p.peer_arrive[q] + p.mir.rank, seqv);
+      const unsigned long long t0 = globaltimer();
+      for (int q = 0; q < p.mir.world; ++q) {
+        if (q == p.mir.rank) continue;
+        while (ld_acquire_sys64(p.arrive + q) < seqv) {
+          if (*reinterpret_cast<volatile int32_t*>(p.xerr)) break;
+          if (globaltimer() - t0 > p.timeout_ns) {
+            atomicExch(p.xerr, 1);
+            break;
+          }
+          __nanosleep(64);
+        }
+      }
+      __threadfence_system();
+      if (nblocks > 1) st_release_gpu(&bar[1], epoch);
     } else {
       while (ld_acquire_gpu(&bar[1]) < epoch) __nanosleep(32);
     }

@@ -39,6 +39,7 @@ namespace {
 
 constexpr uint32_t kFull = 1u;  // RAC_FULL_FIXPOINT
 constexpr int kOK = 0, kWIPEOUT = 1;
+constexpr int kPeerTimeout = -7;  // RAC_EPEER
 
 // Test the rows of variables [g.x_lo, g.x_hi) against the columns
 // cols[0, ncol) (cols == nullptr: columns 0..ncol-1) and OR removals into R.
@@ -254,7 +255,7 @@ __device__ __forceinline__ void stage_from_u64(uint8_t* Db, const uint64_t* src,
 
 // ---------------------------------------------------------------------------- fused
 template <int W, int G>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_constant__ FusedParams p) {
   extern __shared__ uint4 Ds[];
   __shared__ int scratch[kThreads / 32];
   __shared__ int s_last;
@@ -279,7 +280,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   const bool full = (p.flags & kFull) != 0;
   int t = 0, status = kOK, vcnt = g.n;
   unsigned epoch = 0;
-  long long live = count_live<W>(Db, 0, g.n, scratch);
+  long long live = count_live<W>(Db, g.x_lo, g.x_hi, scratch);  // this rank's rows
+  // Rotating buffers and the cross-rank sequence follow the global pass
+  // number base + t, which continues across launches: pass k clears the
+  // buffers of pass k+1, so no launch needs a cleanup phase and a peer that
+  // is already in the next launch only writes buffers this rank has cleared.
+  const unsigned long long base = *reinterpret_cast<volatile unsigned long long*>(p.seq);
+  const bool mg = p.mir.world > 1;
+  int bn = (int)(base % 3ull);  // buffer of global pass base + t, advanced each pass
   int has_empty = 0;  // some D(x) empty (block-uniform)
   for (int x = threadIdx.x; x < g.n; x += blockDim.x) has_empty |= load_w<W>(Db + x * W) == 0;
   has_empty = __syncthreads_or(has_empty);
@@ -301,35 +309,55 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   } else {
     for (;;) {
       ++t;
-      unsigned long long* Rc = p.R + (size_t)(t % 3) * g.n;
-      unsigned long long* Rn = p.R + (size_t)((t + 1) % 3) * g.n;
+      const int b = bn == 2 ? 0 : bn + 1;  // (base + t) % 3
+      bn = b == 2 ? 0 : b + 1;            // (base + t + 1) % 3
+      unsigned long long* Rc = p.R + (size_t)b * g.n;
+      unsigned long long* Rn = p.R + (size_t)bn * g.n;
       // R (and the row counter) of pass t+1 were last used before the
       // previous barrier: clear them now.
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
       if (blockIdx.x == 0 && threadIdx.x == 0) {
-        p.wctr[(t + 1) % 3] = 0u;
-        p.rflag[(t + 1) % 3] = 0u;
+        p.wctr[bn] = 0u;
+        p.rflag[bn] = 0u;
       }
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
       if (pick_rows(g, live, lst ? vcnt : g.n))
-        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr + (t % 3), p.rflag + (t % 3));
+        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr + b, p.rflag + b);
       else
         column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
-                        p.rflag + (t % 3));
+                        p.rflag + b);
       RAC_MARK();
       if (p.dbg != nullptr && t == 1) {  // block-uniform condition: the barrier is safe
         __syncthreads();
         if (dbg_cta) p.dbg[256 + 3 * blockIdx.x + 1] = globaltimer();
       }
       grid_sync(p.bar, gridDim.x, ++epoch);
+      if (mg) {
+        // Row-sharded exchange: R of this rank's rows is complete; copy its
+        // non-zero words into every peer's R (a peer's words for these rows are
+        // zero until then: cleared in its previous pass, written only here),
+        // raise the peers' removal flags, then the cross-rank barrier.
+        if (__ldcg(p.rflag + b) != 0u) {
+          for (int x = g.x_lo + blockIdx.x * blockDim.x + threadIdx.x; x < g.x_hi; x += gridDim.x * blockDim.x) {
+            const unsigned long long v = __ldcg(&Rc[x]);
+            if (v)
+              for (int q = 0; q < p.mir.world; ++q)
+                if (q != p.mir.rank) p.mir.R[q][(size_t)b * g.n + x] = v;
+          }
+          if (blockIdx.x == 0 && threadIdx.x == 0)
+            for (int q = 0; q < p.mir.world; ++q)
+              if (q != p.mir.rank) atomicOr_system(p.mir.flag[q] + b, 1u);
+        }
+        grid_sync_peer(p.bar, gridDim.x, ++epoch, p, base + (unsigned long long)t);
+      }
       RAC_MARK();
       // D_t = D_{t-1} & ~R (every CTA, redundantly); flags for Alg. 1's checks;
       // the changed variables are the next pass's columns.  A pass that
       // removed nothing (the per-pass flag is still 0) leaves D as it was:
       // changed = 0, wipe = "D already had an empty row", no R read.
       int changed = 0, wipe = 0;
-      if (__ldcg(p.rflag + (t % 3)) == 0u) {
+      if (__ldcg(p.rflag + b) == 0u) {
         wipe = has_empty;
       } else {
         for (int x0 = threadIdx.x; x0 < g.n; x0 += 4 * blockDim.x) {
@@ -360,21 +388,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
       if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
       if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
       vcnt = block_compact(vneed, vlist, g.n, scratch);        // next pass's columns
-      live = count_live<W>(Db, 0, g.n, scratch);
+      live = count_live<W>(Db, g.x_lo, g.x_hi, scratch);
       RAC_MARK();
     }
   }
   if (blockIdx.x == 0) {
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.d_out[x] = load_w<W>(Db + x * W);
-    if (threadIdx.x == 0) { *p.iters = t; *p.status = status; }
+    if (threadIdx.x == 0) {
+      *p.iters = t;
+      *p.status = (mg && *reinterpret_cast<volatile int32_t*>(p.xerr)) ? kPeerTimeout : status;
+      // every CTA read *p.seq before the first barrier
+      if (t > 0) *p.seq = base + (unsigned long long)t;
+    }
   }
   RAC_MARK();
   if (dbg) p.dbg[0] = nd;
   if (dbg_cta) p.dbg[256 + 3 * blockIdx.x + 2] = globaltimer();
 #undef RAC_MARK
-  // The last CTA out resets the barrier words and clears R[1] (the removal
-  // buffer pass 1 of the next launch writes): every other CTA has finished
-  // reading by the time it counts itself out.
+  // The last CTA out resets the barrier words: every other CTA has passed its
+  // last barrier by the time it counts itself out.
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = gridDim.x == 1 ? 1 : (atomicAdd(&p.bar[2], 1u) + 1u == gridDim.x);
@@ -382,11 +414,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(FusedParams p)
   __syncthreads();
   if (s_last) {
     __threadfence();
-    for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.R[(size_t)g.n + x] = 0ull;
-    if (threadIdx.x == 0) {
-      p.wctr[1] = 0u;
-      p.rflag[1] = 0u;
-    }
     if (threadIdx.x == 0 && gridDim.x > 1) {
       p.bar[0] = 0u;
       p.bar[1] = 0u;

@@ -1,8 +1,11 @@
 """Multi-process plumbing for the row-sharded path (one process per GPU).
 
-torch.distributed is used only to broadcast librac's NCCL unique id and to
-reduce timings; the per-pass exchange itself (ncclAllGather of the alive
-bitvector slices) happens inside librac (include/rac.h, "Multi-GPU").
+torch.distributed is used only to exchange librac's setup tokens (the NCCL
+unique id, or the peer regions' CUDA IPC handles) and to reduce timings; the
+per-pass exchange itself happens inside librac (include/rac.h, "Multi-GPU"):
+an ncclAllGather of the alive-bitvector slices (default), or, with
+``peer=True``, NVLink peer stores and a cross-rank barrier inside the one
+persistent enforcement kernel.
 """
 from __future__ import annotations
 
@@ -31,13 +34,28 @@ def max_over_ranks(value: float, group=None, device=None) -> float:
     return float(t.item())
 
 
+def connect_peers(ctx: rac.RacContext, group=None) -> None:
+    """All-gather every rank's IPC handle and open the peers' regions."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    handles = [None] * world
+    dist.all_gather_object(handles, ctx.peer_handle(), group=group)
+    ctx.connect_peers(handles)
+
+
 def create_sharded_random(n_vars: int, d: int, dens_q32: int, t_q16: int, seed: int, device: int,
-                          group=None, uid: Optional[bytes] = None) -> rac.RacContext:
+                          group=None, uid: Optional[bytes] = None, peer: bool = False) -> rac.RacContext:
     """Collective rac_create_random over the ranks of `group`: rank r keeps the
-    masks of variables rac_shard_range(n, world, r)."""
+    masks of variables rac_shard_range(n, world, r).  peer=True: exchange
+    through peer memory (RAC_OPT_PEER; IPC handles swapped here)."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if peer and world > 1:
+        ctx = rac.RacContext.create_random(n_vars, d, dens_q32, t_q16, seed, device=device, rank=rank, world=world,
+                                           peer=True)
+        connect_peers(ctx, group)
+        return ctx
     if uid is None:
         uid = nccl_unique_id(group) if world > 1 else None
     return rac.RacContext.create_random(n_vars, d, dens_q32, t_q16, seed, device=device, rank=rank, world=world,

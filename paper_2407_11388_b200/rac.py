@@ -29,13 +29,17 @@ RAC_ECUDA = -3
 RAC_ENCCL = -4
 RAC_ESTATE = -5
 RAC_EUNSUPPORTED = -6
+RAC_EPEER = -7
 RAC_FULL_FIXPOINT = 1
 RAC_OPT_NCCL_SELF = 1
+RAC_OPT_PEER = 2
 RAC_MAX_DOM = 64
 RAC_NCCL_ID_BYTES = 128
+RAC_MAX_RANKS = 8
+RAC_IPC_HANDLE_BYTES = 64
 
 _ERRNAMES = {RAC_EINVAL: "RAC_EINVAL", RAC_ENOMEM: "RAC_ENOMEM", RAC_ECUDA: "RAC_ECUDA", RAC_ENCCL: "RAC_ENCCL",
-             RAC_ESTATE: "RAC_ESTATE", RAC_EUNSUPPORTED: "RAC_EUNSUPPORTED"}
+             RAC_ESTATE: "RAC_ESTATE", RAC_EUNSUPPORTED: "RAC_EUNSUPPORTED", RAC_EPEER: "RAC_EPEER"}
 
 
 class RacError(RuntimeError):
@@ -56,7 +60,8 @@ class rac_search_stats(ctypes.Structure):
 
 class rac_options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
-                ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p), ("virtual_shards", ctypes.c_int32)]
+                ("world", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p), ("virtual_shards", ctypes.c_int32),
+                ("max_ctas", ctypes.c_int32)]
 
 
 # Every symbol include/rac.h declares (checked by tests/test_abi.py).
@@ -64,6 +69,7 @@ EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforc
            "rac_enforce_async", "rac_enforce_batch", "rac_enforce_seeded", "rac_enforce_seeded_async",
            "rac_enforce_batch_seeded", "rac_search", "rac_batch_pass_eval", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
            "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
+           "rac_peer_handle", "rac_connect_peers", "rac_peer_region", "rac_connect_peers_local",
            "rac_last_launch_count", "rac_last_error", "rac_destroy"]
 
 
@@ -99,6 +105,10 @@ def _load() -> ctypes.CDLL:
         "rac_local_range": (ctypes.c_int, [P, i32p, i32p]),
         "rac_read_row": (ctypes.c_int, [P, i32, i32, u64p, ctypes.POINTER(ctypes.c_uint8)]),
         "rac_get_nccl_unique_id": (ctypes.c_int, [P]),
+        "rac_peer_handle": (ctypes.c_int, [P, P]),
+        "rac_connect_peers": (ctypes.c_int, [P, P]),
+        "rac_peer_region": (ctypes.c_int, [P, ctypes.POINTER(P)]),
+        "rac_connect_peers_local": (ctypes.c_int, [P, ctypes.POINTER(P), i32p]),
         "rac_last_launch_count": (i64, [P]),
         "rac_last_error": (ctypes.c_char_p, [P]),
         "rac_destroy": (None, [P]),
@@ -145,11 +155,11 @@ def rac_get_nccl_unique_id() -> bytes:
 
 
 def make_options(device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
-                 virtual_shards: int = 0, nccl_self: bool = False):
+                 virtual_shards: int = 0, nccl_self: bool = False, peer: bool = False, max_ctas: int = 0):
     o = rac_options()
     lib.rac_default_options(ctypes.byref(o))
-    o.device, o.rank, o.world, o.virtual_shards = device, rank, world, virtual_shards
-    o.flags = RAC_OPT_NCCL_SELF if nccl_self else 0
+    o.device, o.rank, o.world, o.virtual_shards, o.max_ctas = device, rank, world, virtual_shards, max_ctas
+    o.flags = (RAC_OPT_NCCL_SELF if nccl_self else 0) | (RAC_OPT_PEER if peer else 0)
     keep = None
     if nccl_unique_id is not None:
         keep = ctypes.create_string_buffer(bytes(nccl_unique_id), RAC_NCCL_ID_BYTES)
@@ -189,7 +199,7 @@ class RacContext:
     @classmethod
     def create(cls, n_vars: int, dom_sizes, xs, ys, rows, device: int = 0, rank: int = 0, world: int = 1,
                nccl_unique_id: Optional[bytes] = None, virtual_shards: int = 0,
-               nccl_self: bool = False) -> "RacContext":
+               nccl_self: bool = False, peer: bool = False, max_ctas: int = 0) -> "RacContext":
         """rac_create from relation arrays: constraint k on (xs[k], ys[k]) with
         rows[k, a] = c_xy|(x,a) bitsets (uint64)."""
         dom = np.ascontiguousarray(dom_sizes, dtype=np.int32)
@@ -206,7 +216,7 @@ class RacContext:
             arr["x"] = xs
             arr["y"] = ys
             arr["rows"] = base + stride * np.arange(m, dtype=np.uint64)
-        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self)
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self, peer, max_ctas)
         h = ctypes.c_void_p()
         rc = lib.rac_create(n_vars, _i32p(dom), m, rel if m else None, ctypes.byref(opt), ctypes.byref(h))
         _check(rc)
@@ -220,8 +230,9 @@ class RacContext:
     @classmethod
     def create_random(cls, n_vars: int, d: int, dens_q32: int, t_q16: int, seed: int, device: int = 0,
                       rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
-                      virtual_shards: int = 0, nccl_self: bool = False) -> "RacContext":
-        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self)
+                      virtual_shards: int = 0, nccl_self: bool = False, peer: bool = False,
+                      max_ctas: int = 0) -> "RacContext":
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self, peer, max_ctas)
         h = ctypes.c_void_p()
         _check(lib.rac_create_random(n_vars, d, dens_q32, t_q16, seed, ctypes.byref(opt), ctypes.byref(h)))
         del keep
@@ -317,6 +328,29 @@ class RacContext:
         _check(lib.rac_enforce_batch(self._h, n_states, _ptr(d_in_dev), _ptr(d_out_dev), _ptr(iters_dev),
                                      _ptr(status_dev), RAC_FULL_FIXPOINT if full else 0, _stream_ptr(stream)),
                self._h)
+
+    # ---- peer-memory exchange (RAC_OPT_PEER)
+    def peer_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(RAC_IPC_HANDLE_BYTES)
+        _check(lib.rac_peer_handle(self._h, buf), self._h)
+        return buf.raw
+
+    def connect_peers(self, handles: Sequence[bytes]) -> None:
+        """handles[q] = rank q's peer_handle() (world entries, rank order)."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(lib.rac_connect_peers(self._h, buf), self._h)
+
+    def peer_region(self) -> int:
+        p = ctypes.c_void_p()
+        _check(lib.rac_peer_region(self._h, ctypes.byref(p)), self._h)
+        return int(p.value or 0)
+
+    def connect_peers_local(self, regions: Sequence[int], devices: Sequence[int]) -> None:
+        """Ranks driven by this one process: regions[q] = rank q's peer_region()."""
+        arr = (ctypes.c_void_p * len(regions))(*regions)
+        dev = np.ascontiguousarray(devices, dtype=np.int32)
+        _check(lib.rac_connect_peers_local(self._h, arr, _i32p(dev)), self._h)
 
     # ---- introspection
     @property

@@ -546,3 +546,35 @@ def test_batch_pass_eval_tc_and_bitsliced(rac):
             out = dout.cpu().numpy().view(np.uint64)
             for s in range(S):
                 assert np.array_equal(out[s], expect[s]), (ci, impl, s)
+
+
+def test_scratch_growth_interleaved(rac):
+    """Growing one scratch buffer (the seed list, the batch exchange buffers) must
+    leave the others intact: batched calls of growing size interleaved with seeded
+    calls of growing seed lists on ONE context, every result against the oracle,
+    then destroy (regression for a growth path that freed unrelated buffers)."""
+    import torch
+    inst = synth.random_csp(80, 10, 0.7, 0.4, 9)
+    orc = oracle.Oracle.from_instance(inst)
+    st0, root, _, _ = orc.rac(inst.full_domains())
+    assert st0 == oracle.OK
+    ctx = rac.RacContext.from_instance(inst)
+    rng = np.random.default_rng(4)
+    for rnd, (S, ns) in enumerate(((32, 1), (200, 7), (96, 40), (700, 80))):
+        states = np.stack([synth.w_rand(inst.dom, 0.8, seed=1000 * rnd + s) for s in range(S)])
+        din = torch.from_numpy(states.view(np.int64).copy()).cuda()
+        dout = torch.zeros_like(din)
+        its = torch.zeros(S, dtype=torch.int32, device="cuda")
+        sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+        ctx.enforce_batch(S, din, dout, its, sts)
+        torch.cuda.synchronize()
+        out, its, sts = dout.cpu().numpy().view(np.uint64), its.cpu().numpy(), sts.cpu().numpy()
+        for s in range(0, S, 7):
+            e = orc.rac(states[s], with_epochs=False)
+            assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (rnd, s)
+        seeds = rng.choice(inst.n, size=ns, replace=False).astype(np.int32)
+        d_in = synth.w_rand(inst.dom, 0.9, seed=rnd)
+        g = ctx.enforce_seeded(d_in, seeds)
+        o = orc.rac_seeded(d_in, seeds, with_epochs=False)
+        assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1]), ("seeded", rnd)
+    ctx.close()
