@@ -37,15 +37,29 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     if not force and out is None and not _stale():
         return LIB
     tmp = lib + ".tmp.%d" % os.getpid()
-    cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-o", tmp] + ["-D" + d for d in defines] + \
-        [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building librac.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+    objdir = tmp + ".obj"
+    os.makedirs(objdir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if verbose else "-O3"] + ["-D" + d for d in defines]
+    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+
+    def compile_one(i):
+        return subprocess.run([nvcc_path(), *flags, "-c", os.path.join(CSRC, SOURCES[i]), "-o", objs[i]],
+                              capture_output=True, text=True)
+
+    # one nvcc per translation unit, in parallel (rac_kernels.cu dominates)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, range(len(SOURCES))))
+    results.append(subprocess.run([nvcc_path(), *ARCH, "-shared", "-o", tmp] + objs + ["-ldl"],
+                                  capture_output=True, text=True))
+    shutil.rmtree(objdir, ignore_errors=True)
+    for res in results:
+        if res.returncode != 0:
+            sys.stderr.write(res.stdout + res.stderr)
+            raise RuntimeError("nvcc failed building librac.so")
+        if verbose:
+            sys.stderr.write(res.stderr)
     os.replace(tmp, lib)
     return lib
 

@@ -359,7 +359,8 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.removed_at = removed_at;
   p.R = c->R3;
   p.bar = c->bar;
-  p.wctr = c->bar + 4;
+  static const bool no_claim = getenv("RAC_NO_CLAIM") != nullptr;  // A/B knob (tooling only)
+  p.wctr = no_claim ? nullptr : c->bar + 4;
   p.rflag = reinterpret_cast<unsigned*>(c->xr + xr_rflag_off(c->n));
   p.seq = reinterpret_cast<unsigned long long*>(c->xr + xr_seq_off(c->n));
   p.mir.world = c->peer ? c->world : 1;

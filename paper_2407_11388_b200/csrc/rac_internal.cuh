@@ -341,7 +341,7 @@ __device__ __noinline__ bool vec_real_fail(uint4 m, uint4 d, int v, int n, const
     const int y = v * L + i;
     if (y >= n) break;
     uint64_t mi, di;
-    if (W == 8) {
+    if constexpr (W == 8) {
       mi = (uint64_t)mw[2 * i] | ((uint64_t)mw[2 * i + 1] << 32);
       di = (uint64_t)dw[2 * i] | ((uint64_t)dw[2 * i + 1] << 32);
     } else {

@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   // is already in the next launch only writes buffers this rank has cleared.
   const unsigned long long base = *reinterpret_cast<volatile unsigned long long*>(p.seq);
   const bool mg = p.mir.world > 1;
-  int bn = (int)(base % 3ull);  // buffer of global pass base + t, advanced each pass
+  int b = (int)(base % 3ull);  // buffer of global pass base + t, advanced each pass
   int has_empty = 0;  // some D(x) empty (block-uniform)
   for (int x = threadIdx.x; x < g.n; x += blockDim.x) has_empty |= load_w<W>(Db + x * W) == 0;
   has_empty = __syncthreads_or(has_empty);
@@ -309,21 +309,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   } else {
     for (;;) {
       ++t;
-      const int b = bn == 2 ? 0 : bn + 1;  // (base + t) % 3
-      bn = b == 2 ? 0 : b + 1;            // (base + t + 1) % 3
+      b = b == 2 ? 0 : b + 1;                   // (base + t) % 3
+      const int bn = b == 2 ? 0 : b + 1;        // (base + t + 1) % 3
       unsigned long long* Rc = p.R + (size_t)b * g.n;
       unsigned long long* Rn = p.R + (size_t)bn * g.n;
       // R (and the row counter) of pass t+1 were last used before the
       // previous barrier: clear them now.
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += gridDim.x * blockDim.x) Rn[i] = 0ull;
       if (blockIdx.x == 0 && threadIdx.x == 0) {
-        p.wctr[bn] = 0u;
+        if (p.wctr) p.wctr[bn] = 0u;
         p.rflag[bn] = 0u;
       }
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
       if (pick_rows(g, live, lst ? vcnt : g.n))
-        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr + b, p.rflag + b);
+        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b);
       else
         column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
                         p.rflag + b);

@@ -429,6 +429,29 @@ def test_forced_layouts(rac, layout, monkeypatch):
             assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1])
 
 
+@pytest.mark.parametrize("layout", ["auto", "rows"])
+def test_back_to_back_launches(rac, layout, monkeypatch):
+    """Many enforcements in a row on ONE context with pass counts 1, 2 and 3 mixed:
+    the per-pass buffers (removal vector, row-claim counter, removal flag) rotate
+    through three copies across launches, so every residue of the global pass
+    number mod 3 is exercised; every result keeps full epoch parity.  (A rotation
+    bug once left a stale row-claim counter that skipped rows: C2 W-seed.)"""
+    if layout != "auto":
+        monkeypatch.setenv("RAC_FORCE_LAYOUT", layout)
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.0119)
+    ctx = rac.RacContext.create_random(500, 20, dq, tq, 1)
+    orc = oracle.Oracle.from_synth(500, 20, dq, tq, 1)
+    root = synth.full_domains(np.full(500, 20))
+    o_root = orc.rac(root)
+    inputs = [root] + [synth.w_seed(o_root[1], 11, k)[0] for k in range(3)] + \
+        [synth.w_rand(np.full(500, 20), 0.9, 2)]
+    expect = [orc.rac(d) for d in inputs]
+    assert len({e[2] for e in expect}) >= 2
+    order = [0, 1, 1, 2, 4, 1, 3, 3, 0, 2, 2, 4, 4, 1, 0, 3, 2, 1, 4, 0, 3]
+    for i, k in enumerate(order):
+        assert_same(ctx.enforce(inputs[k], removed_at=True), expect[k], (layout, i, k))
+
+
 # ----------------------------------------------------------------------------- search (NEXT-2)
 def test_search_parity(rac):
     """rac_search (Alg. 2 with seeded enforcement per assignment) explores the
