@@ -596,7 +596,16 @@ def test_scratch_growth_interleaved(rac):
             e = orc.rac(states[s], with_epochs=False)
             assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (rnd, s)
         seeds = rng.choice(inst.n, size=ns, replace=False).astype(np.int32)
-        d_in = synth.w_rand(inst.dom, 0.9, seed=rnd)
+        # the seeded-call precondition (DESIGN R12): AC on every c_xy with y not a
+        # seed -- an AC state whose seed variables lost some values
+        st_ac, d_in, _, _ = orc.rac(synth.w_rand(inst.dom, 0.9, seed=rnd), with_epochs=False)
+        if st_ac != oracle.OK:
+            d_in = root.copy()
+        for x in seeds:
+            vals = [a for a in range(64) if (int(d_in[x]) >> a) & 1]
+            keep = rng.choice(vals, size=max(1, len(vals) - 1), replace=False)
+            d_in[x] = U64(sum(1 << int(a) for a in keep))
+        assert orc.rac(d_in, with_epochs=False)[2] == orc.rac_seeded(d_in, seeds, with_epochs=False)[2]
         g = ctx.enforce_seeded(d_in, seeds)
         o = orc.rac_seeded(d_in, seeds, with_epochs=False)
         assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1]), ("seeded", rnd)
