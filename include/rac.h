@@ -113,12 +113,26 @@ typedef struct {
 /* rac_options.flags: world > 1 exchanges through peer memory inside the fused
  * kernel instead of NCCL (see "Multi-GPU" above); 2 <= world <= RAC_MAX_RANKS. */
 #define RAC_OPT_PEER (1u << 1)
+/* rac_options.flags: relation layout (NEXT-3).  Dense (default for instances
+ * whose dense tensor is L2-sized or that are nearly complete): every (x,a) row
+ * holds n masks, absent pairs all-ones.  Sparse arc blocks: only declared arcs
+ * are stored -- block = the masks c_xy|(x,a) of one arc for all a, the blocks
+ * of column y contiguous (Cons[:, y]) -- so a pass reads only declared
+ * constraints (the paper's density grid 0.1-0.75).  Without either
+ * flag the library picks sparse on one GPU when the dense column tensor is
+ * >= 64 MB and the sparse one is <= 0.7 of it.  Sparse contexts need
+ * world == 1 without virtual shards / NCCL_SELF (RAC_EINVAL otherwise) and do
+ * not support the batched calls (RAC_EUNSUPPORTED); results are identical. */
+#define RAC_OPT_SPARSE (1u << 2)
+#define RAC_OPT_DENSE (1u << 3)
+#define RAC_LAYOUT_DENSE 0
+#define RAC_LAYOUT_SPARSE 1
 #define RAC_MAX_RANKS 8
 #define RAC_IPC_HANDLE_BYTES 64
 
 typedef struct {
   int32_t device;             /* CUDA device ordinal (rank's GPU)                     */
-  uint32_t flags;             /* 0 or RAC_OPT_NCCL_SELF                               */
+  uint32_t flags;             /* RAC_OPT_* bits (0: defaults)                         */
   int32_t rank, world;        /* world <= 1: single GPU                               */
   const void* nccl_unique_id; /* world > 1: RAC_NCCL_ID_BYTES bytes, identical on all
                                  ranks (from rac_get_nccl_unique_id on rank 0)        */
@@ -291,6 +305,8 @@ int rac_peer_handle(const rac_ctx* ctx, void* out /* RAC_IPC_HANDLE_BYTES */);
 int rac_connect_peers(rac_ctx* ctx, const void* handles /* world x RAC_IPC_HANDLE_BYTES */);
 int rac_peer_region(const rac_ctx* ctx, void** region_dev);
 int rac_connect_peers_local(rac_ctx* ctx, void* const* regions /* [world] */, const int32_t* devices /* [world] */);
+/* RAC_LAYOUT_DENSE or RAC_LAYOUT_SPARSE (see RAC_OPT_SPARSE). */
+int32_t rac_layout(const rac_ctx* ctx);
 /* Kernel launches enqueued by the last rac_enforce* call on this context. */
 int64_t rac_last_launch_count(const rac_ctx* ctx);
 

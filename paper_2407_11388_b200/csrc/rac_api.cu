@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/rac.h"
+#include "../../synth/csp_synth.h"  // presence of generated pairs (rac_create_random, sparse layout)
 #include "rac_internal.cuh"
 
 using namespace rac;
@@ -83,6 +84,14 @@ struct rac_ctx {
   int G = 1;                // lanes per row of the row-major sweep
   int force_layout = 0;     // RAC_FORCE_LAYOUT=rows|cols (testing knob)
   uint32_t* P = nullptr;
+  // Sparse arc-block layout (NEXT-3; rac.h RAC_OPT_SPARSE): only declared arcs
+  bool sparse = false;
+  uint8_t* S = nullptr;          // [s_nblk][s_bbytes]
+  uint32_t* s_off = nullptr;     // [n+1]
+  uint32_t* s_arc = nullptr;     // [s_nblk] x | y << 16
+  uint32_t s_nblk = 0;
+  int s_dpad = 0, s_bbytes = 0, s_vb = 0;
+  std::vector<uint32_t> s_off_h, s_arc_h;
   int32_t* dom_d = nullptr;
   uint64_t* dommask = nullptr;
   // Exchange region (one allocation so that one IPC handle maps it): the
@@ -153,6 +162,9 @@ void free_ctx(rac_ctx* c) {
     if (c->peer_ipc[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
   cudaFree(c->M);
   cudaFree(c->Mr);
+  cudaFree(c->S);
+  cudaFree(c->s_off);
+  cudaFree(c->s_arc);
   cudaFree(c->P);
   cudaFree(c->dom_d);
   cudaFree(c->dommask);
@@ -188,15 +200,27 @@ size_t xr_seq_off(int n) { return xr_arrive_off(n) + 8 * RAC_MAX_RANKS; }  // u6
 size_t xr_bytes(int n) { return xr_seq_off(n) + 8; }
 
 size_t kernel_smem(const rac_ctx* c) {
-  return fused_smem(c->dbytes, c->n);
+  return c->sparse ? sparse_smem(c->dbytes, c->n) : fused_smem(c->dbytes, c->n);
+}
+
+// Sparse arc-block geometry: dpad rows per block so that a block is a whole
+// number of 16-byte vectors.
+int sparse_dpad(int dmax, int W) {
+  const int L = 16 / W;
+  return (dmax + L - 1) / L * L;
 }
 
 // Common part of rac_create / rac_create_random up to (not including) packing.
-int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt) {
+int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt, double n_pairs) {
   rac_options o;
   rac_default_options(&o);
   if (opt) o = *opt;
-  if (o.flags & ~(RAC_OPT_NCCL_SELF | RAC_OPT_PEER)) return fail(nullptr, RAC_EINVAL, "unknown options.flags");
+  if (o.flags & ~(RAC_OPT_NCCL_SELF | RAC_OPT_PEER | RAC_OPT_SPARSE | RAC_OPT_DENSE))
+    return fail(nullptr, RAC_EINVAL, "unknown options.flags");
+  if ((o.flags & RAC_OPT_SPARSE) && (o.flags & RAC_OPT_DENSE))
+    return fail(nullptr, RAC_EINVAL, "RAC_OPT_SPARSE and RAC_OPT_DENSE together");
+  if ((o.flags & RAC_OPT_SPARSE) && (o.world > 1 || o.virtual_shards > 1 || (o.flags & RAC_OPT_NCCL_SELF)))
+    return fail(nullptr, RAC_EINVAL, "RAC_OPT_SPARSE needs world == 1 without virtual shards / NCCL_SELF");
   if ((o.flags & RAC_OPT_NCCL_SELF) && o.world > 1) return fail(nullptr, RAC_EINVAL, "RAC_OPT_NCCL_SELF needs world == 1");
   if ((o.flags & RAC_OPT_PEER) && (o.world < 2 || o.world > RAC_MAX_RANKS))
     return fail(nullptr, RAC_EINVAL, "RAC_OPT_PEER needs 2 <= world <= RAC_MAX_RANKS");
@@ -231,6 +255,26 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
     c->col_stride = (size_t)c->rows_pad * c->W;
   }
   if (n > 65535) return fail(nullptr, RAC_EUNSUPPORTED, "n_vars > 65535");
+  {
+    // Layout: the sparse arc-block tensor stores 2 * pairs blocks of dpad masks
+    // instead of n columns x rows_pad masks (twice, with the row-major copy).
+    // Auto: sparse on one GPU when the dense tensor would not be L2-resident
+    // and the sparse one is at most 0.7 of it.
+    const double dense_b = (double)n * (double)c->col_stride;
+    const int dpad = sparse_dpad(c->dmax, c->W);
+    const double sparse_b = 2.0 * n_pairs * dpad * c->W;
+    const bool single = c->world == 1 && c->vshards == 1 && !c->nccl_self;
+    if (o.flags & RAC_OPT_SPARSE) c->sparse = true;
+    else if (o.flags & RAC_OPT_DENSE) c->sparse = false;
+    else c->sparse = single && dense_b >= 64.0 * (1 << 20) && sparse_b <= 0.7 * dense_b;
+    if (c->sparse) {
+      c->s_dpad = dpad;
+      c->s_bbytes = dpad * c->W;
+      c->s_vb = c->s_bbytes / 16;
+      if (2.0 * n_pairs * c->s_vb >= 4294967295.0)
+        return fail(nullptr, RAC_EUNSUPPORTED, "sparse layout: more than 2^32 16-byte vectors");
+    }
+  }
 
   cudaError_t e = cudaSetDevice(c->device);
   if (e != cudaSuccess) return fail(nullptr, RAC_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
@@ -248,9 +292,9 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
       return fail(nullptr, e_ == cudaErrorMemoryAllocation ? RAC_ENOMEM : RAC_ECUDA,                \
                   std::string(#call) + ": " + cudaGetErrorString(e_));                              \
   } while (0)
-  CKC(cudaMalloc(&c->M, std::max<size_t>(mbytes, 16)));
-  CKC(cudaMemsetAsync(c->M, 0xFF, std::max<size_t>(mbytes, 16), c->stream));
-  {
+  CKC(cudaMalloc(&c->M, c->sparse ? 16 : std::max<size_t>(mbytes, 16)));
+  CKC(cudaMemsetAsync(c->M, 0xFF, c->sparse ? 16 : std::max<size_t>(mbytes, 16), c->stream));
+  if (!c->sparse) {
     // Row-major copy for full passes (dead-row skip, early exit).  Optional:
     // without room for it every pass uses the column-major tensor.
     const size_t rbytes = (size_t)c->rows_pad * c->dbytes;
@@ -302,7 +346,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt)
   // as many CTAs as fit, but no more than the work of a full pass can feed
   // (about 4 items of kUnroll columns x one 512-byte slab per warp).
   const long slabs = c->rows_pad / slab_rows(c->W);
-  const long items = slabs * ((n + kUnroll - 1) / kUnroll);
+  const long items = c->sparse ? (long)((2.0 * n_pairs * c->s_vb + 32.0 * kUnrollS - 1) / (32.0 * kUnrollS))
+                               : slabs * ((n + kUnroll - 1) / kUnroll);
   int occ = 0;
   CKC(fused_occupancy(c->W, c->G, kernel_smem(c), &occ));
   if (occ < 1) return fail(nullptr, RAC_EUNSUPPORTED, "support-pass kernel does not fit on an SM (n too large)");
@@ -335,7 +380,73 @@ PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi) {
   g.P = c->P;
   g.pw = c->pw;
   g.dbytes = c->dbytes;
+  g.S = c->S;
+  g.s_off = c->s_off;
+  g.s_arc = c->s_arc;
+  g.s_nblk = c->s_nblk;
+  g.s_vb = c->s_vb;
   return g;
+}
+
+// Sparse layout: order the arcs of the pairs (xs[r], ys[r]) by column then x,
+// upload the block index, pack the masks (host rows or the generator when
+// drows == nullptr) and set the presence bits.
+int build_sparse(rac_ctx* c, const std::vector<int32_t>& xs, const std::vector<int32_t>& ys, const uint64_t* drows,
+                 int row_words, int d, uint32_t t_q16, uint64_t seed) {
+  const long np = (long)xs.size();
+  const int n = c->n;
+  // arc key = column << 16 | x; value = r << 1 | (1 = the y -> x arc of pair r)
+  std::vector<std::pair<uint32_t, uint32_t>> arcs;
+  arcs.reserve(2 * np);
+  for (long r = 0; r < np; ++r) {
+    const uint32_t x = (uint32_t)xs[r], y = (uint32_t)ys[r];
+    arcs.push_back({(y << 16) | x, (uint32_t)(r << 1)});      // x -> y: rows of x, column y
+    arcs.push_back({(x << 16) | y, (uint32_t)(r << 1) | 1u}); // y -> x: rows of y, column x
+  }
+  std::sort(arcs.begin(), arcs.end());
+  c->s_nblk = (uint32_t)arcs.size();
+  c->s_off_h.assign(n + 1, 0u);
+  c->s_arc_h.resize(arcs.size());
+  std::vector<uint32_t> fwd(np), bwd(np);
+  std::vector<uint32_t> pres((size_t)n * c->pw, 0u);
+  for (size_t b = 0; b < arcs.size(); ++b) {
+    const uint32_t col = arcs[b].first >> 16, row = arcs[b].first & 0xffffu;
+    c->s_off_h[col + 1]++;
+    c->s_arc_h[b] = row | (col << 16);
+    const uint32_t r = arcs[b].second >> 1;
+    if (arcs[b].second & 1u) bwd[r] = (uint32_t)b; else fwd[r] = (uint32_t)b;
+    pres[(size_t)row * c->pw + (col >> 5)] |= 1u << (col & 31);
+  }
+  for (int y = 0; y < n; ++y) c->s_off_h[y + 1] += c->s_off_h[y];
+  const size_t sbytes = std::max<size_t>((size_t)c->s_nblk * c->s_bbytes, 16);
+  int32_t *dxs = nullptr, *dys = nullptr;
+  uint32_t *dfwd = nullptr, *dbwd = nullptr;
+  cudaError_t e = cudaMalloc(&c->S, sbytes);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->S, 0xFF, sbytes, c->stream);
+  if (e == cudaSuccess) e = cudaMalloc(&c->s_off, (size_t)(n + 1) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&c->s_arc, std::max<size_t>(arcs.size(), 1) * 4);
+  if (e == cudaSuccess && np > 0) e = cudaMalloc(&dxs, (size_t)np * 4);
+  if (e == cudaSuccess && np > 0) e = cudaMalloc(&dys, (size_t)np * 4);
+  if (e == cudaSuccess && np > 0) e = cudaMalloc(&dfwd, (size_t)np * 4);
+  if (e == cudaSuccess && np > 0) e = cudaMalloc(&dbwd, (size_t)np * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(c->s_off, c->s_off_h.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && np > 0) e = cudaMemcpy(c->s_arc, c->s_arc_h.data(), arcs.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dxs, xs.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dys, ys.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dfwd, fwd.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dbwd, bwd.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->P, pres.data(), pres.size() * 4, cudaMemcpyHostToDevice);
+  SparsePack g{c->S, c->s_bbytes, c->W, c->dom_d, n};
+  if (e == cudaSuccess) e = launch_pack_sparse(g, dxs, dys, drows, row_words, dfwd, dbwd, np, d, t_q16, seed, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(dxs);
+  cudaFree(dys);
+  cudaFree(dfwd);
+  cudaFree(dbwd);
+  if (e != cudaSuccess)
+    return fail(nullptr, e == cudaErrorMemoryAllocation ? RAC_ENOMEM : RAC_ECUDA,
+                std::string("sparse packing: ") + cudaGetErrorString(e));
+  return 0;
 }
 
 
@@ -384,7 +495,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
   p.dbg = c->dbg;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
-  if (c->fused_grid == 1 && !c->peer && (seeds == nullptr || n_seeds == 1)) {
+  if (c->fused_grid == 1 && !c->peer && !c->sparse && (seeds == nullptr || n_seeds == 1)) {
     // One CTA is enough: run the single-CTA variant (removal bits in shared
     // memory, __syncthreads as the pass barrier) -- the batched per-state
     // kernel with one state.
@@ -635,9 +746,21 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
       return fail(nullptr, RAC_EINVAL, "duplicate constraint on one unordered pair");
   }
   rac_ctx* c = new rac_ctx();
-  int rc = setup_ctx(c, n_vars, dom_sizes, opt);
+  int rc = setup_ctx(c, n_vars, dom_sizes, opt, (double)n_rel);
   if (rc) { free_ctx(c); return rc; }
-  if (n_rel > 0) {
+  if (c->sparse) {
+    uint64_t* drows = nullptr;
+    cudaError_t e = n_rel > 0 ? cudaMalloc(&drows, rows.size() * 8) : cudaSuccess;
+    if (e == cudaSuccess && n_rel > 0) e = cudaMemcpy(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(drows);
+      free_ctx(c);
+      return fail(nullptr, RAC_ENOMEM, std::string("relation upload: ") + cudaGetErrorString(e));
+    }
+    rc = build_sparse(c, xs, ys, drows, dmax, 0, 0u, 0ull);
+    cudaFree(drows);
+    if (rc) { free_ctx(c); return rc; }
+  } else if (n_rel > 0) {
     int32_t *dxs = nullptr, *dys = nullptr;
     uint64_t* drows = nullptr;
     cudaError_t e = cudaMalloc(&dxs, (size_t)n_rel * 4);
@@ -672,8 +795,27 @@ int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q
     return fail(nullptr, RAC_EINVAL, "bad generator parameters");
   std::vector<int32_t> dom(n_vars, d);
   rac_ctx* c = new rac_ctx();
-  int rc = setup_ctx(c, n_vars, dom.data(), opt);
+  const double est_pairs = (double)dens_q32 / 4294967296.0 * 0.5 * (double)n_vars * (double)(n_vars - 1);
+  int rc = setup_ctx(c, n_vars, dom.data(), opt, est_pairs);
   if (rc) { free_ctx(c); return rc; }
+  if (c->sparse) {
+    // the present pairs (x < y) from the generator's presence hash
+    std::vector<int32_t> xs, ys;
+    xs.reserve((size_t)(est_pairs * 1.05) + 16);
+    ys.reserve((size_t)(est_pairs * 1.05) + 16);
+    for (int x = 0; x < n_vars; ++x)
+      for (int y = x + 1; y < n_vars; ++y)
+        if (synth_present(seed, (uint32_t)n_vars, (uint32_t)x, (uint32_t)y, dens_q32)) {
+          xs.push_back(x);
+          ys.push_back(y);
+        }
+    rc = build_sparse(c, xs, ys, nullptr, 0, d, t_q16, seed);
+    if (rc) { free_ctx(c); return rc; }
+    rc = init_comm(c, opt);
+    if (rc) { free_ctx(c); return rc; }
+    *out = c;
+    return 0;
+  }
   PackGeom g{c->M, c->col_stride, c->Mr, (size_t)c->dbytes, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw,
                c->dom_d};
   cudaError_t e = launch_generate(g, d, dens_q32, t_q16, seed, c->stream);
@@ -799,6 +941,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   if (n_states < 0 || (n_states > 0 && (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev)))
     return fail(c, RAC_EINVAL, "bad batch arguments");
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
+  if (c->sparse) return fail(c, RAC_EUNSUPPORTED, "batched mode needs the dense layout (RAC_OPT_DENSE)");
   if (c->world > 1) return fail(c, RAC_EUNSUPPORTED, "batched mode runs per rank (world == 1 contexts)");
   c->launches = 0;
   if (n_states == 0) return 0;
@@ -890,6 +1033,7 @@ int rac_batch_pass_eval(rac_ctx* c, int32_t impl, int32_t n_states, const uint64
   if (rc) return rc;
   if (n_states < 1 || !d_in_dev || !d_out_dev || (impl != 0 && impl != 1)) return fail(c, RAC_EINVAL, "bad arguments");
   if (c->use_nccl() || c->x_lo != 0 || c->x_hi != c->n) return fail(c, RAC_EUNSUPPORTED, "single-GPU contexts only");
+  if (c->sparse) return fail(c, RAC_EUNSUPPORTED, "batched passes need the dense layout (RAC_OPT_DENSE)");
   if (impl == 1 && c->dmax > 16) return fail(c, RAC_EUNSUPPORTED, "tensor-core pass needs max dom <= 16");
   CK(c, cudaSetDevice(c->device));
   const int rows = c->n * c->dmax, rows4 = (rows + 3) & ~3, NW = (n_states + 31) / 32;
@@ -1013,8 +1157,11 @@ int32_t rac_n_vars(const rac_ctx* c) { return c ? c->n : RAC_EINVAL; }
 int32_t rac_max_dom(const rac_ctx* c) { return c ? c->dmax : RAC_EINVAL; }
 int32_t rac_mask_bytes(const rac_ctx* c) { return c ? c->W : RAC_EINVAL; }
 int64_t rac_relation_bytes(const rac_ctx* c) {
-  return c ? (int64_t)c->n * (int64_t)c->col_stride + (c->Mr ? (int64_t)c->rows_pad * c->dbytes : 0) : RAC_EINVAL;
+  if (!c) return RAC_EINVAL;
+  if (c->sparse) return (int64_t)c->s_nblk * c->s_bbytes;
+  return (int64_t)c->n * (int64_t)c->col_stride + (c->Mr ? (int64_t)c->rows_pad * c->dbytes : 0);
 }
+int32_t rac_layout(const rac_ctx* c) { return c ? (c->sparse ? RAC_LAYOUT_SPARSE : RAC_LAYOUT_DENSE) : RAC_EINVAL; }
 int64_t rac_last_launch_count(const rac_ctx* c) { return c ? c->launches : RAC_EINVAL; }
 
 int rac_local_range(const rac_ctx* c, int32_t* x_lo, int32_t* x_hi) {
@@ -1030,7 +1177,23 @@ int rac_read_row(const rac_ctx* cc, int32_t x, int32_t a, uint64_t* out_masks, u
   if (rc) return rc;
   if (x < c->x_lo || x >= c->x_hi || a < 0 || a >= c->dmax) return fail(c, RAC_EINVAL, "row not local");
   CK(c, cudaSetDevice(c->device));
-  if (out_masks) {
+  if (out_masks && c->sparse) {
+    // arc blocks: the block of arc x -> y in column y (sorted by x), else all ones
+    const uint64_t ones = c->W == 8 ? ~0ull : ((1ull << (8 * c->W)) - 1ull);
+    for (int y = 0; y < c->n; ++y) {
+      out_masks[y] = ones;
+      const uint32_t* b0 = c->s_arc_h.data() + c->s_off_h[y];
+      const uint32_t* b1 = c->s_arc_h.data() + c->s_off_h[y + 1];
+      const uint32_t key = (uint32_t)x | ((uint32_t)y << 16);
+      const uint32_t* it = std::lower_bound(b0, b1, key);
+      if (it != b1 && *it == key) {
+        uint64_t v = 0;
+        CK(c, cudaMemcpy(&v, c->S + (size_t)(it - c->s_arc_h.data()) * c->s_bbytes + (size_t)a * c->W, c->W,
+                         cudaMemcpyDeviceToHost));
+        out_masks[y] = v;
+      }
+    }
+  } else if (out_masks) {
     // column-major: the row's n masks are strided by col_stride
     std::vector<uint8_t> buf((size_t)c->n * c->W);
     const size_t r = (size_t)(x - c->x_lo) * c->dmax + a;

@@ -44,6 +44,10 @@ constexpr int kMinBlocks = RAC_MIN_BLOCKS;  // CTAs per SM the register budget i
 #endif
 constexpr int kUnroll = RAC_UNROLL_C;   // 16-byte column loads in flight per lane (contiguous columns)
 constexpr int kUnrollL = RAC_UNROLL_L;  // ... listed columns (an index each)
+#ifndef RAC_UNROLL_S
+#define RAC_UNROLL_S 8
+#endif
+constexpr int kUnrollS = RAC_UNROLL_S;  // 16-byte loads in flight per lane (sparse arc-block sweep)
 #ifndef RAC_UNROLL_R
 #define RAC_UNROLL_R 8
 #endif
@@ -64,6 +68,15 @@ struct PassGeom {
   const uint32_t* P;      // presence bits of variable x_lo_alloc onward
   int pw;                 // u32 words per presence row
   int dbytes;             // bytes of D in smem (n*W rounded up to 16)
+  // Sparse arc-block layout (S != nullptr; NEXT-3): only declared arcs are
+  // stored.  Block b = the dpad masks c_xy|(x,a), a < dpad, of one arc x -> y
+  // (16-byte multiple); the blocks of column y are contiguous (Cons[:, y] of
+  // Alg. 1), columns in order.
+  const uint8_t* S;
+  const uint32_t* s_off;  // [n+1] first block of column y
+  const uint32_t* s_arc;  // [nblk] x | y << 16
+  uint32_t s_nblk;        // blocks (local arcs)
+  int s_vb;               // 16-byte vectors per block
 };
 
 // Peer-memory exchange of the row-sharded fused kernel (world > 1, RAC_OPT_PEER):
@@ -182,6 +195,11 @@ __host__ __device__ constexpr size_t need_offset(int dbytes, int n) {
 __host__ __device__ constexpr size_t fused_smem(int dbytes, int n) {
   return need_offset(dbytes, n) + (((size_t)n + 15) & ~(size_t)15);
 }
+// Sparse layout: + the prefix of block counts over the listed columns (u32[n+1]).
+__host__ __device__ constexpr size_t pref_offset(int dbytes, int n) { return fused_smem(dbytes, n); }
+__host__ __device__ constexpr size_t sparse_smem(int dbytes, int n) {
+  return pref_offset(dbytes, n) + (((size_t)(n + 1) * 4 + 15) & ~(size_t)15);
+}
 
 // ---------------------------------------------------------------------------- host launchers
 // (defined in rac_kernels.cu / rac_pack.cu; return cudaError_t of the launch)
@@ -221,6 +239,20 @@ cudaError_t launch_pack_relations(const PackGeom& g, const int32_t* xs, const in
                                   int n_rel, int row_words, cudaStream_t s);
 cudaError_t launch_generate(const PackGeom& g, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed,
                             cudaStream_t s);
+// Sparse arc-block packer: pair r = (xs[r], ys[r]) (x < y for generated
+// instances); its forward masks c_xy|(x,a) go to block fwd[r], the transposed
+// masks c_yx|(y,b) to block bwd[r] (either may be UINT32_MAX: not local).
+// rows == nullptr: rows come from the seeded generator (d, t_q16, seed).
+struct SparsePack {
+  uint8_t* S;
+  int bbytes;             // bytes per block
+  int W;
+  const int32_t* dom;     // device [n]
+  int n;
+};
+cudaError_t launch_pack_sparse(const SparsePack& g, const int32_t* xs, const int32_t* ys, const uint64_t* rows,
+                               int row_words, const uint32_t* fwd, const uint32_t* bwd, long n_pairs, int d,
+                               uint32_t t_q16, uint64_t seed, cudaStream_t s);
 
 // ---------------------------------------------------------------------------- device helpers
 #ifdef __CUDACC__
@@ -426,6 +458,47 @@ __device__ __forceinline__ int block_compact(uint8_t* need, uint16_t* out, int c
     need[i] = 0;
   }
   const int total = scratch[(T >> 5) - 1];
+  __syncthreads();
+  return total;
+}
+
+// Sparse layout: pref[i] = blocks of the listed columns list[0..i) (exclusive
+// prefix of s_off[y+1] - s_off[y]), pref[cnt] = total.  Block-wide, every CTA
+// computes it redundantly from its own list; returns the total.
+__device__ __forceinline__ uint32_t block_prefix_blocks(const uint16_t* list, int cnt, const uint32_t* s_off,
+                                                        uint32_t* pref, int* scratch) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const int chunk = (cnt + T - 1) / T;
+  const int b = min(cnt, t * chunk), e = min(cnt, b + chunk);
+  uint32_t c = 0;
+  for (int i = b; i < e; ++i) c += __ldg(s_off + list[i] + 1) - __ldg(s_off + list[i]);
+  const int lane = t & 31, w = t >> 5;
+  uint32_t v = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  __syncthreads();  // scratch may still be read by a previous helper
+  if (lane == 31) scratch[w] = (int)v;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane < (T >> 5) ? (uint32_t)scratch[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += u;
+    }
+    if (lane < (T >> 5)) scratch[lane] = (int)s;
+  }
+  __syncthreads();
+  uint32_t pos = v - c + (w > 0 ? (uint32_t)scratch[w - 1] : 0u);
+  for (int i = b; i < e; ++i) {
+    pref[i] = pos;
+    pos += __ldg(s_off + list[i] + 1) - __ldg(s_off + list[i]);
+  }
+  const uint32_t total = (uint32_t)scratch[(T >> 5) - 1];
+  if (t == 0) pref[cnt] = total;
   __syncthreads();
   return total;
 }

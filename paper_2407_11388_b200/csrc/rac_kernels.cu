@@ -137,6 +137,76 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
   }
 }
 
+// Sparse arc-block sweep (NEXT-3): the tested columns' blocks form one flat
+// range of 16-byte vectors (all blocks in a full pass; the listed columns'
+// blocks, through the prefix `pref`, otherwise).  A warp item is 32 x kUnrollS
+// consecutive vectors: each lane issues its kUnrollS streaming loads first,
+// then per vector reads the arc (x, y) of its block, tests the 16/W rows
+// a0.. of x that are live against D(y) and ORs failures into R[x].  Only
+// declared arcs are stored, so no presence check is needed (reading R2).
+template <int W>
+__device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
+                                             int32_t* removed_at, int t, long warp0, long nwarps,
+                                             const uint16_t* cols, int ncol, const uint32_t* pref,
+                                             unsigned* rflag) {
+  constexpr int L = 16 / W, U = kUnrollS;
+  constexpr uint32_t LM = (L == 32) ? 0xffffffffu : ((1u << L) - 1u);
+  const int lane = threadIdx.x & 31;
+  const uint32_t VB = (uint32_t)g.s_vb;
+  const uint32_t nblk = cols ? pref[ncol] : g.s_nblk;
+  const uint32_t nvec = nblk * VB;
+  const uint32_t items = (nvec + 32u * U - 1u) / (32u * U);
+  const uint4* S4 = reinterpret_cast<const uint4*>(g.S);
+  int ci = 0;  // listed column of the lane's current vector (monotone within an item)
+  for (uint32_t it = (uint32_t)warp0; it < items; it += (uint32_t)nwarps) {
+    uint4 m[U];
+    uint32_t blk[U], part[U];
+    if (cols) {  // binary search for the first vector of the item, then walk
+      const uint32_t k0 = min((it * 32u * U + lane) / VB, nblk - 1u);
+      int lo = 0, hi = ncol - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pref[mid] <= k0) lo = mid; else hi = mid - 1;
+      }
+      ci = lo;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = it * 32u * U + (uint32_t)(u * 32 + lane);
+      blk[u] = 0xffffffffu;
+      if (v < nvec) {
+        const uint32_t k = v / VB;
+        part[u] = v - k * VB;
+        if (cols) {
+          while (pref[ci + 1] <= k) ++ci;
+          blk[u] = __ldg(g.s_off + cols[ci]) + (k - pref[ci]);
+        } else {
+          blk[u] = k;
+        }
+        m[u] = ldg_stream(S4 + (size_t)blk[u] * VB + part[u]);
+      }
+    }
+    uint32_t any = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (blk[u] != 0xffffffffu) {
+        const uint32_t arc = __ldg(g.s_arc + blk[u]);
+        const int x = (int)(arc & 0xffffu), y = (int)(arc >> 16);
+        const int a0 = (int)part[u] * L;
+        const uint32_t cand = (uint32_t)(load_w<W>(Db + x * W) >> a0) & LM;
+        const uint32_t f = zero_lanes<W>(and4(m[u], rep16<W>(load_w<W>(Db + y * W)))) & cand;
+        if (f) {
+          any = 1;
+          atomicOr(&R[x], (unsigned long long)f << a0);
+          if (removed_at)
+            for (uint32_t ff = f; ff; ff &= ff - 1u) removed_at[(size_t)x * 64 + a0 + __ffs(ff) - 1] = t;
+        }
+      }
+    }
+    if (any && rflag) atomicOr(rflag, 1u);  // this pass removed something
+  }
+}
+
 // Row-major sweep: every live row (x,a) of variables [g.x_lo, g.x_hi) is
 // streamed whole (all n columns) by a group of G lanes, with early exit on
 // the first failing column and dead-row skip.  Rows are split into n_seg
@@ -322,7 +392,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       }
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
-      if (pick_rows(g, live, lst ? vcnt : g.n))
+      if (g.S) {
+        const uint32_t* pref = reinterpret_cast<const uint32_t*>(Db + pref_offset(g.dbytes, g.n));
+        if (lst) block_prefix_blocks(vlist, vcnt, g.s_off, const_cast<uint32_t*>(pref), scratch);
+        sparse_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, vcnt, pref, p.rflag + b);
+      } else if (pick_rows(g, live, lst ? vcnt : g.n))
         row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b);
       else
         column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,

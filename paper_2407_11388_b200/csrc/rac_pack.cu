@@ -120,6 +120,64 @@ __global__ void generate_kernel(PackGeom g, int d, uint64_t dens_q32, uint32_t t
   }
 }
 
+// Sparse arc-block packer (NEXT-3): warp per pair, rows a = lane, lane + 32 of
+// rel(c_xy) from the host array or the generator; forward masks to block
+// fwd[r] (row a at byte a*W), the ballot-transposed masks c_yx|(y,b) to block
+// bwd[r].  Blocks were filled with 0xFF (rows a >= dom(x) are never live).
+__global__ void pack_sparse_kernel(SparsePack g, const int32_t* xs, const int32_t* ys, const uint64_t* rows,
+                                   int row_words, const uint32_t* fwd, const uint32_t* bwd, long n_pairs, int d,
+                                   uint32_t t_q16, uint64_t seed) {
+  const int lane = threadIdx.x & 31;
+  const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
+  for (long r = warp; r < n_pairs; r += nwarps) {
+    const int x = xs[r], y = ys[r];
+    const int dx = g.dom[x], dy = g.dom[y];
+    uint64_t row_lo = 0, row_hi = 0;
+    if (rows) {
+      const uint64_t* rr = rows + (size_t)r * row_words;
+      row_lo = lane < dx ? rr[lane] : 0ull;
+      row_hi = lane + 32 < dx ? rr[lane + 32] : 0ull;
+    } else {
+      const uint64_t pk = synth_pair_key(seed, (uint32_t)g.n, (uint32_t)x, (uint32_t)y);
+      const uint32_t q = (uint32_t)(d + 3) / 4u;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = lane + 32 * h;
+        if (a >= d) continue;
+        uint64_t row = 0;
+        for (uint32_t bq = 0; bq < q; ++bq) {
+          const uint64_t w = synth_cell_word_pk(pk, (uint32_t)d, (uint32_t)a, bq);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t b = bq * 4u + j;
+            if (b < (uint32_t)d && ((uint32_t)(w >> (16 * j)) & 0xFFFFu) >= t_q16) row |= 1ull << b;
+          }
+        }
+        if (h == 0) row_lo = row; else row_hi = row;
+      }
+    }
+    if (fwd[r] != 0xffffffffu) {
+      uint8_t* blk = g.S + (size_t)fwd[r] * g.bbytes;
+      if (lane < dx) put_w(blk + lane * g.W, g.W, row_lo);
+      if (lane + 32 < dx) put_w(blk + (lane + 32) * g.W, g.W, row_hi);
+    }
+    if (bwd[r] != 0xffffffffu) {
+      uint64_t col_lo = 0, col_hi = 0;  // column b = lane and b = lane + 32
+      for (int b = 0; b < dy; ++b) {
+        const uint32_t lo = __ballot_sync(0xffffffffu, (row_lo >> b) & 1ull);
+        const uint32_t hi = __ballot_sync(0xffffffffu, (row_hi >> b) & 1ull);
+        const uint64_t col = (uint64_t)lo | ((uint64_t)hi << 32);
+        if (b == lane) col_lo = col;
+        if (b == lane + 32) col_hi = col;
+      }
+      uint8_t* blk = g.S + (size_t)bwd[r] * g.bbytes;
+      if (lane < dy) put_w(blk + lane * g.W, g.W, col_lo);
+      if (lane + 32 < dy) put_w(blk + (lane + 32) * g.W, g.W, col_hi);
+    }
+  }
+}
+
 int grid_for(long work_warps) {
   long blocks = (work_warps * 32 + 255) / 256;
   if (blocks < 1) blocks = 1;
@@ -139,6 +197,14 @@ cudaError_t launch_pack_relations(const PackGeom& g, const int32_t* xs, const in
 cudaError_t launch_generate(const PackGeom& g, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed,
                             cudaStream_t s) {
   generate_kernel<<<grid_for((long)g.n * g.n), 256, 0, s>>>(g, d, dens_q32, t_q16, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_sparse(const SparsePack& g, const int32_t* xs, const int32_t* ys, const uint64_t* rows,
+                               int row_words, const uint32_t* fwd, const uint32_t* bwd, long n_pairs, int d,
+                               uint32_t t_q16, uint64_t seed, cudaStream_t s) {
+  if (n_pairs == 0) return cudaSuccess;
+  pack_sparse_kernel<<<grid_for(n_pairs), 256, 0, s>>>(g, xs, ys, rows, row_words, fwd, bwd, n_pairs, d, t_q16, seed);
   return cudaGetLastError();
 }
 

@@ -33,6 +33,10 @@ RAC_EPEER = -7
 RAC_FULL_FIXPOINT = 1
 RAC_OPT_NCCL_SELF = 1
 RAC_OPT_PEER = 2
+RAC_OPT_SPARSE = 4
+RAC_OPT_DENSE = 8
+RAC_LAYOUT_DENSE = 0
+RAC_LAYOUT_SPARSE = 1
 RAC_MAX_DOM = 64
 RAC_NCCL_ID_BYTES = 128
 RAC_MAX_RANKS = 8
@@ -68,7 +72,7 @@ class rac_options(ctypes.Structure):
 EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforce", "rac_enforce_ex",
            "rac_enforce_async", "rac_enforce_batch", "rac_enforce_seeded", "rac_enforce_seeded_async",
            "rac_enforce_batch_seeded", "rac_search", "rac_batch_pass_eval", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
-           "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
+           "rac_layout", "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
            "rac_peer_handle", "rac_connect_peers", "rac_peer_region", "rac_connect_peers_local",
            "rac_last_launch_count", "rac_last_error", "rac_destroy"]
 
@@ -100,6 +104,7 @@ def _load() -> ctypes.CDLL:
         "rac_n_vars": (i32, [P]),
         "rac_max_dom": (i32, [P]),
         "rac_mask_bytes": (i32, [P]),
+        "rac_layout": (i32, [P]),
         "rac_relation_bytes": (i64, [P]),
         "rac_shard_range": (ctypes.c_int, [i32, i32, i32, i32p, i32p]),
         "rac_local_range": (ctypes.c_int, [P, i32p, i32p]),
@@ -155,11 +160,13 @@ def rac_get_nccl_unique_id() -> bytes:
 
 
 def make_options(device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
-                 virtual_shards: int = 0, nccl_self: bool = False, peer: bool = False, max_ctas: int = 0):
+                 virtual_shards: int = 0, nccl_self: bool = False, peer: bool = False, max_ctas: int = 0,
+                 layout: str = "auto"):
     o = rac_options()
     lib.rac_default_options(ctypes.byref(o))
     o.device, o.rank, o.world, o.virtual_shards, o.max_ctas = device, rank, world, virtual_shards, max_ctas
-    o.flags = (RAC_OPT_NCCL_SELF if nccl_self else 0) | (RAC_OPT_PEER if peer else 0)
+    o.flags = (RAC_OPT_NCCL_SELF if nccl_self else 0) | (RAC_OPT_PEER if peer else 0) | \
+        {"auto": 0, "sparse": RAC_OPT_SPARSE, "dense": RAC_OPT_DENSE}[layout]
     keep = None
     if nccl_unique_id is not None:
         keep = ctypes.create_string_buffer(bytes(nccl_unique_id), RAC_NCCL_ID_BYTES)
@@ -199,7 +206,8 @@ class RacContext:
     @classmethod
     def create(cls, n_vars: int, dom_sizes, xs, ys, rows, device: int = 0, rank: int = 0, world: int = 1,
                nccl_unique_id: Optional[bytes] = None, virtual_shards: int = 0,
-               nccl_self: bool = False, peer: bool = False, max_ctas: int = 0) -> "RacContext":
+               nccl_self: bool = False, peer: bool = False, max_ctas: int = 0,
+               layout: str = "auto") -> "RacContext":
         """rac_create from relation arrays: constraint k on (xs[k], ys[k]) with
         rows[k, a] = c_xy|(x,a) bitsets (uint64)."""
         dom = np.ascontiguousarray(dom_sizes, dtype=np.int32)
@@ -216,7 +224,8 @@ class RacContext:
             arr["x"] = xs
             arr["y"] = ys
             arr["rows"] = base + stride * np.arange(m, dtype=np.uint64)
-        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self, peer, max_ctas)
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self, peer, max_ctas,
+                                 layout)
         h = ctypes.c_void_p()
         rc = lib.rac_create(n_vars, _i32p(dom), m, rel if m else None, ctypes.byref(opt), ctypes.byref(h))
         _check(rc)
@@ -231,8 +240,9 @@ class RacContext:
     def create_random(cls, n_vars: int, d: int, dens_q32: int, t_q16: int, seed: int, device: int = 0,
                       rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
                       virtual_shards: int = 0, nccl_self: bool = False, peer: bool = False,
-                      max_ctas: int = 0) -> "RacContext":
-        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self, peer, max_ctas)
+                      max_ctas: int = 0, layout: str = "auto") -> "RacContext":
+        opt, keep = make_options(device, rank, world, nccl_unique_id, virtual_shards, nccl_self, peer, max_ctas,
+                                 layout)
         h = ctypes.c_void_p()
         _check(lib.rac_create_random(n_vars, d, dens_q32, t_q16, seed, ctypes.byref(opt), ctypes.byref(h)))
         del keep
@@ -356,6 +366,11 @@ class RacContext:
     @property
     def mask_bytes(self) -> int:
         return int(lib.rac_mask_bytes(self._h))
+
+    @property
+    def layout(self) -> str:
+        """"dense" or "sparse" (arc blocks, rac.h RAC_OPT_SPARSE)."""
+        return "sparse" if int(lib.rac_layout(self._h)) == RAC_LAYOUT_SPARSE else "dense"
 
     @property
     def relation_bytes(self) -> int:

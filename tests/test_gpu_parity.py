@@ -610,3 +610,84 @@ def test_scratch_growth_interleaved(rac):
         o = orc.rac_seeded(d_in, seeds, with_epochs=False)
         assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1]), ("seeded", rnd)
     ctx.close()
+
+
+# ----------------------------------------------------------------------------- sparse layout (NEXT-3)
+@pytest.mark.parametrize("n,d,p,t", [(9, 3, 0.5, 0.3), (33, 8, 0.7, 0.4), (70, 17, 0.3, 0.5), (40, 64, 0.9, 0.6),
+                                     (17, 1, 1.0, 0.2), (50, 32, 0.2, 0.6)])
+def test_sparse_packer_matches_oracle(rac, n, d, p, t):
+    """Sparse arc blocks (RAC_OPT_SPARSE): every stored mask equals the oracle's
+    support set c_xy|(x,a), absent pairs read back as all ones, presence bits
+    match -- host-packed and generated instances."""
+    inst = synth.random_csp(n, d, p, t, seed=5)
+    orc = oracle.Oracle.from_instance(inst)
+    for ctx in (rac.RacContext.from_instance(inst, layout="sparse"),
+                rac.RacContext.create_random(n, d, synth.quant_density(p), synth.quant_tightness(t), 5,
+                                             layout="sparse")):
+        assert ctx.layout == "sparse"
+        allones = U64((1 << (8 * ctx.mask_bytes)) - 1)
+        for x in range(n):
+            for a in range(d):
+                masks, pres = ctx.read_row(x, a)
+                for y in range(n):
+                    present, s = orc.support(x, y, a)
+                    assert bool(pres[y]) == present
+                    assert masks[y] == (U64(s) if present else allones), (x, a, y)
+
+
+def test_sparse_corpus(rac):
+    """SPEC-corpus shapes and non-uniform domains through the sparse layout: full
+    epoch parity in stop and full-fixpoint modes, empty rows included."""
+    for k, inst in enumerate(I.random_corpus(300, seed0=77)):
+        ctx = rac.RacContext.from_instance(inst, layout="sparse")
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = inst.full_domains() if k % 3 == 0 else synth.w_rand(inst.dom, 0.85, seed=k)
+        if k % 7 == 0:
+            d_in[k % inst.n] = U64(0)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (k, full))
+
+
+@pytest.mark.parametrize("t,workload", [(0.5, "stream"), (0.74, "prop")])
+def test_sparse_c3_density(rac, t, workload):
+    """n=2000, d=32 at density 0.25 (the paper's density grid): the library
+    picks the sparse layout by itself; W-stream (1 pass) / W-prop (~23 passes) root,
+    W-rand, a W-seed seeded call and back-to-back launches all match the oracle;
+    the dense layout gives the same results."""
+    n, d = 2000, 32
+    dq, tq = synth.quant_density(0.25), synth.quant_tightness(t)
+    ctx = rac.RacContext.create_random(n, d, dq, tq, 1)
+    assert ctx.layout == "sparse"
+    assert ctx.relation_bytes < 0.3 * n * n * d * 4
+    orc = oracle.Oracle.from_synth(n, d, dq, tq, 1)
+    root = synth.full_domains(np.full(n, d))
+    o_root = orc.rac(root)
+    for rep in range(2):
+        assert_same(ctx.enforce(root, removed_at=True), o_root, (workload, "root", rep))
+    rnd = synth.w_rand(np.full(n, d), 0.9, 3)
+    assert_same(ctx.enforce(rnd, removed_at=True), orc.rac(rnd), (workload, "rand"))
+    if o_root[0] == oracle.OK:
+        s, x, v = synth.w_seed(o_root[1], 7)
+        g = ctx.enforce_seeded(s, [x])
+        o = orc.rac(s, with_epochs=False)
+        assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1])
+    dense = rac.RacContext.create_random(n, d, dq, tq, 1, layout="dense")
+    assert dense.layout == "dense"
+    assert_same(dense.enforce(root, removed_at=True), o_root, (workload, "dense"))
+
+
+def test_sparse_unsupported_and_invalid(rac):
+    """Sparse contexts refuse the batched calls (RAC_EUNSUPPORTED) and sparse with
+    virtual shards is rejected at create (RAC_EINVAL)."""
+    import torch
+    inst = synth.random_csp(30, 8, 0.5, 0.4, seed=2)
+    ctx = rac.RacContext.from_instance(inst, layout="sparse")
+    din = torch.zeros((4, 30), dtype=torch.int64, device="cuda")
+    i32 = torch.zeros(4, dtype=torch.int32, device="cuda")
+    with pytest.raises(rac.RacError) as e:
+        ctx.enforce_batch(4, din, din.clone(), i32, i32.clone())
+    assert e.value.code == rac.RAC_EUNSUPPORTED
+    with pytest.raises(rac.RacError) as e:
+        rac.RacContext.from_instance(inst, layout="sparse", virtual_shards=2)
+    assert e.value.code == rac.RAC_EINVAL
