@@ -54,6 +54,11 @@ WORKLOADS = {
     "c3-seed": (2000, 32, 1.0, 0.5, 1, "seed",
                 "C3 W-seed: n=2000, d=32, density 1.0, tightness 0.5; D_ac(root) with one seeded assignment, "
                 "seeded enforcement (Alg. 1 tensorAC(Vars, [idx]), P:392)"),
+    "c3s-stream": (4000, 32, 0.25, 0.5, 1, "root",
+                   "NEXT-3 sparse: n=4000, d=32, density 0.25 (paper's density grid P:236), tightness 0.5; root "
+                   "enforcement (1 pass; sparse arc blocks, 512 MB of declared masks vs 2 GB dense)"),
+    "c3s-prop": (4000, 32, 0.25, 0.72, 1, "root",
+                 "NEXT-3 sparse: n=4000, d=32, density 0.25, tightness 0.72; root enforcement (propagating)"),
     "c4-stream": (8000, 64, 1.0, 0.5, 1, "root",
                   "C4 W-stream: n=8000, d=64, density 1.0, tightness 0.5; root enforcement (32.8 GB of masks)"),
     "c5-batch": (200, 16, 0.8, 0.3, 1, "dive",
@@ -359,7 +364,8 @@ def run_gpu(args, rank, world, local_rank):
             roofline["frac"] = round(achieved / world / peak, 4)
     cfg = {"workload": args.workload + ": " + desc, "n": n, "d": d, "density": dens, "tightness": tight,
            "t_q16": tq, "seed": seed, "states": S if kind == "dive" else 1,
-           "l2": "inputs larger than L2 (no flush)" if n * n * d * d / 8 > 200e6 else
+           "layout": ctx.layout, "relation_bytes": ctx.relation_bytes,
+           "l2": "inputs larger than L2 (no flush)" if ctx.relation_bytes > 200e6 else
                  "relation L2-resident (warm; stated, not flushed)",
            "parallelism": ("row-sharded x%d (NCCL all-gather of D per pass)" % world) if world > 1 else "1 GPU",
            "instance_generation_s": round(gen_s, 3)}
