@@ -89,6 +89,7 @@ struct rac_ctx {
   uint8_t* S = nullptr;          // [s_nblk][s_bbytes]
   uint32_t* s_off = nullptr;     // [n+1]
   uint32_t* s_arc = nullptr;     // [s_nblk] x | y << 16
+  uint32_t* s_ipref = nullptr;   // [n+1] full-pass work-item prefix (sparse_sweep)
   uint32_t s_nblk = 0;
   int s_dpad = 0, s_bbytes = 0, s_vb = 0;
   std::vector<uint32_t> s_off_h, s_arc_h;
@@ -165,6 +166,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->S);
   cudaFree(c->s_off);
   cudaFree(c->s_arc);
+  cudaFree(c->s_ipref);
   cudaFree(c->P);
   cudaFree(c->dom_d);
   cudaFree(c->dommask);
@@ -349,7 +351,7 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
   const long items = c->sparse ? (long)((2.0 * n_pairs * c->s_vb + 32.0 * kUnrollS - 1) / (32.0 * kUnrollS))
                                : slabs * ((n + kUnroll - 1) / kUnroll);
   int occ = 0;
-  CKC(fused_occupancy(c->W, c->G, kernel_smem(c), &occ));
+  CKC(fused_occupancy(c->W, c->sparse ? 0 : c->G, kernel_smem(c), &occ));
   if (occ < 1) return fail(nullptr, RAC_EUNSUPPORTED, "support-pass kernel does not fit on an SM (n too large)");
   // about one item per warp (small problems are latency-bound: spread them)
   const long want = (items + (kThreads / 32) - 1) / (kThreads / 32);
@@ -383,6 +385,7 @@ PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi) {
   g.S = c->S;
   g.s_off = c->s_off;
   g.s_arc = c->s_arc;
+  g.s_ipref = c->s_ipref;
   g.s_nblk = c->s_nblk;
   g.s_vb = c->s_vb;
   return g;
@@ -418,6 +421,10 @@ int build_sparse(rac_ctx* c, const std::vector<int32_t>& xs, const std::vector<i
     pres[(size_t)row * c->pw + (col >> 5)] |= 1u << (col & 31);
   }
   for (int y = 0; y < n; ++y) c->s_off_h[y + 1] += c->s_off_h[y];
+  std::vector<uint32_t> ipref(n + 1, 0u);  // full-pass work items (32 x kUnrollS vectors, within a column)
+  const uint32_t per_item = 32u * kUnrollS;
+  for (int y = 0; y < n; ++y)
+    ipref[y + 1] = ipref[y] + ((c->s_off_h[y + 1] - c->s_off_h[y]) * (uint32_t)c->s_vb + per_item - 1u) / per_item;
   const size_t sbytes = std::max<size_t>((size_t)c->s_nblk * c->s_bbytes, 16);
   int32_t *dxs = nullptr, *dys = nullptr;
   uint32_t *dfwd = nullptr, *dbwd = nullptr;
@@ -425,6 +432,8 @@ int build_sparse(rac_ctx* c, const std::vector<int32_t>& xs, const std::vector<i
   if (e == cudaSuccess) e = cudaMemsetAsync(c->S, 0xFF, sbytes, c->stream);
   if (e == cudaSuccess) e = cudaMalloc(&c->s_off, (size_t)(n + 1) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->s_arc, std::max<size_t>(arcs.size(), 1) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&c->s_ipref, (size_t)(n + 1) * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(c->s_ipref, ipref.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && np > 0) e = cudaMalloc(&dxs, (size_t)np * 4);
   if (e == cudaSuccess && np > 0) e = cudaMalloc(&dys, (size_t)np * 4);
   if (e == cudaSuccess && np > 0) e = cudaMalloc(&dfwd, (size_t)np * 4);
@@ -518,7 +527,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   static const bool no_coop = getenv("RAC_NO_COOP") != nullptr;  // A/B knob (tooling only)
   // max_ctas > 0 (several ranks sharing a GPU): ordinary launch, co-residency
   // is the caller's sizing
-  CK(c, launch_fused(c->W, c->G, p, c->fused_grid, kernel_smem(c), s,
+  CK(c, launch_fused(c->W, c->sparse ? 0 : c->G, p, c->fused_grid, kernel_smem(c), s,
                      c->fused_grid > 1 && !no_coop && c->max_ctas == 0));
   c->launches++;
   return 0;

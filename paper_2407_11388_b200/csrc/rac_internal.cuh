@@ -44,8 +44,12 @@ constexpr int kMinBlocks = RAC_MIN_BLOCKS;  // CTAs per SM the register budget i
 #endif
 constexpr int kUnroll = RAC_UNROLL_C;   // 16-byte column loads in flight per lane (contiguous columns)
 constexpr int kUnrollL = RAC_UNROLL_L;  // ... listed columns (an index each)
+#ifndef RAC_COL_SLABS
+#define RAC_COL_SLABS 1
+#endif
+constexpr int kColSlabs = RAC_COL_SLABS;  // 512-byte slabs per warp item of the column sweep
 #ifndef RAC_UNROLL_S
-#define RAC_UNROLL_S 8
+#define RAC_UNROLL_S 16
 #endif
 constexpr int kUnrollS = RAC_UNROLL_S;  // 16-byte loads in flight per lane (sparse arc-block sweep)
 #ifndef RAC_UNROLL_R
@@ -75,6 +79,7 @@ struct PassGeom {
   const uint8_t* S;
   const uint32_t* s_off;  // [n+1] first block of column y
   const uint32_t* s_arc;  // [nblk] x | y << 16
+  const uint32_t* s_ipref;  // [n+1] work items of columns 0..y-1 (full-pass item prefix)
   uint32_t s_nblk;        // blocks (local arcs)
   int s_vb;               // 16-byte vectors per block
 };
@@ -195,7 +200,7 @@ __host__ __device__ constexpr size_t need_offset(int dbytes, int n) {
 __host__ __device__ constexpr size_t fused_smem(int dbytes, int n) {
   return need_offset(dbytes, n) + (((size_t)n + 15) & ~(size_t)15);
 }
-// Sparse layout: + the prefix of block counts over the listed columns (u32[n+1]).
+// Sparse layout: + the work-item prefix over the tested columns (u32[n+1]).
 __host__ __device__ constexpr size_t pref_offset(int dbytes, int n) { return fused_smem(dbytes, n); }
 __host__ __device__ constexpr size_t sparse_smem(int dbytes, int n) {
   return pref_offset(dbytes, n) + (((size_t)(n + 1) * 4 + 15) & ~(size_t)15);
@@ -462,16 +467,22 @@ __device__ __forceinline__ int block_compact(uint8_t* need, uint16_t* out, int c
   return total;
 }
 
-// Sparse layout: pref[i] = blocks of the listed columns list[0..i) (exclusive
-// prefix of s_off[y+1] - s_off[y]), pref[cnt] = total.  Block-wide, every CTA
-// computes it redundantly from its own list; returns the total.
-__device__ __forceinline__ uint32_t block_prefix_blocks(const uint16_t* list, int cnt, const uint32_t* s_off,
-                                                        uint32_t* pref, int* scratch) {
+// Sparse layout: ipref[i] = work items of the listed columns list[0..i)
+// (column y has ceil((s_off[y+1] - s_off[y]) * VB / per_item) items of
+// per_item vectors), ipref[cnt] = total.  Block-wide; every CTA computes it
+// redundantly from its own list; returns the total.
+__device__ __forceinline__ uint32_t block_prefix_items(const uint16_t* list, int cnt, const uint32_t* s_off,
+                                                       uint32_t VB, uint32_t per_item, uint32_t* ipref,
+                                                       int* scratch) {
   const int T = blockDim.x, t = threadIdx.x;
   const int chunk = (cnt + T - 1) / T;
   const int b = min(cnt, t * chunk), e = min(cnt, b + chunk);
+  auto items_of = [&](int i) {
+    const int y = list[i];
+    return ((__ldg(s_off + y + 1) - __ldg(s_off + y)) * VB + per_item - 1u) / per_item;
+  };
   uint32_t c = 0;
-  for (int i = b; i < e; ++i) c += __ldg(s_off + list[i] + 1) - __ldg(s_off + list[i]);
+  for (int i = b; i < e; ++i) c += items_of(i);
   const int lane = t & 31, w = t >> 5;
   uint32_t v = c;
 #pragma unroll
@@ -494,11 +505,11 @@ __device__ __forceinline__ uint32_t block_prefix_blocks(const uint16_t* list, in
   __syncthreads();
   uint32_t pos = v - c + (w > 0 ? (uint32_t)scratch[w - 1] : 0u);
   for (int i = b; i < e; ++i) {
-    pref[i] = pos;
-    pos += __ldg(s_off + list[i] + 1) - __ldg(s_off + list[i]);
+    ipref[i] = pos;
+    pos += items_of(i);
   }
   const uint32_t total = (uint32_t)scratch[(T >> 5) - 1];
-  if (t == 0) pref[cnt] = total;
+  if (t == 0) ipref[cnt] = total;
   __syncthreads();
   return total;
 }

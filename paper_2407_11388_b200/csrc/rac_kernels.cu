@@ -49,86 +49,108 @@ template <int W>
 __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                              int32_t* removed_at, int t, long warp0, long nwarps,
                                              const uint16_t* cols, int ncol, unsigned* rflag = nullptr) {
-  constexpr int RPL = 16 / W, RPW = 32 * RPL;
+  // SL slabs per item: a warp reads SL x 512 contiguous bytes of each column
+  // (lane l holds rows l*RPL.. of each slab); loads in flight per lane stay
+  // kUnroll (kUnroll/SL columns x SL slabs).
+  constexpr int SL = kColSlabs;
+  constexpr int RPL = 16 / W, RPW = 32 * RPL * SL;
+  constexpr int UC = kUnroll / SL > 0 ? kUnroll / SL : 1;
+  constexpr int ULc = kUnrollL / SL > 0 ? kUnrollL / SL : 1;
+  constexpr uint64_t LM = (RPL == 64) ? ~0ull : ((1ull << RPL) - 1ull);
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
   const int r_hi = (g.x_hi - g.x_lo_alloc) * g.dmax;
   if (r_hi <= r_lo || ncol <= 0) return;
   const int s_lo = r_lo / RPW, s_hi = (r_hi + RPW - 1) / RPW;
   const int nslab = s_hi - s_lo;
-  // about 4 items per warp, each at least kUnroll columns long (32-bit
+  // about 4 items per warp, each at least UC columns long (32-bit
   // arithmetic only: 64-bit division is a long software sequence)
   const int nw = (int)nwarps;
   int nchunk = (4 * nw + nslab - 1) / nslab;
-  const int maxchunk = (ncol + kUnroll - 1) / kUnroll;
+  const int maxchunk = (ncol + UC - 1) / UC;
   if (nchunk > maxchunk) nchunk = maxchunk;
   if (nchunk < 1) nchunk = 1;
   const int yc = (ncol + nchunk - 1) / nchunk;
   nchunk = (ncol + yc - 1) / yc;
   const int items = nslab * nchunk;
+  const size_t rows_alloc = g.col_stride / W;  // padded rows per column
   for (int it = (int)warp0; it < items; it += nw) {
     const int chunk = it / nslab;
     const int slab = s_lo + (it - chunk * nslab);
-    const int r0 = slab * RPW + lane * RPL;  // first local row of this lane
-    uint32_t cand = 0;                       // live rows of this lane
-    {
-      // walk (x, a) incrementally from one division
+    uint64_t cand = 0;  // live rows of this lane: bit j*RPL + i = row slab*RPW + j*32*RPL + lane*RPL + i
+#pragma unroll
+    for (int j = 0; j < SL; ++j) {
+      const int r0 = slab * RPW + j * 32 * RPL + lane * RPL;
       int xl = r0 / g.dmax, a = r0 - xl * g.dmax;
 #pragma unroll
       for (int i = 0; i < RPL; ++i) {
         const int r = r0 + i;
         if (r >= r_lo && r < r_hi) {
           const int x = g.x_lo_alloc + xl;
-          if ((Db[x * W + (a >> 3)] >> (a & 7)) & 1u) cand |= 1u << i;
+          if ((Db[x * W + (a >> 3)] >> (a & 7)) & 1u) cand |= 1ull << (j * RPL + i);
         }
         if (++a == g.dmax) { a = 0; ++xl; }
       }
     }
-    uint32_t fail = 0;
+    uint64_t fail = 0;
     const int c0 = chunk * yc, c1 = min(c0 + yc, ncol);
-    const uint8_t* base = g.M + (size_t)r0 * W;
+    const size_t rbase = (size_t)slab * RPW + (size_t)lane * RPL;
+    const bool tail = rbase + (size_t)(SL - 1) * 32 * RPL >= rows_alloc;  // last slabs past the padding
+    const uint8_t* base = g.M + rbase * W;
+    auto test = [&](const uint4* m, int y, uint64_t dv) {
+#pragma unroll
+      for (int j = 0; j < SL; ++j) {
+        const int r0 = slab * RPW + j * 32 * RPL + lane * RPL;
+        const uint32_t cj = (uint32_t)(((cand & ~fail) >> (j * RPL)) & LM);
+        if (cj) fail |= (uint64_t)column_fail<W>(m[j], dv, cj, y, r0, g.dmax, g.P, g.pw) << (j * RPL);
+      }
+    };
     if (cols == nullptr) {
-      // contiguous columns c0..c1-1: running pointer, no index array
       const uint8_t* pc = base + (size_t)c0 * g.col_stride;
-      for (int c = c0; c < c1 && fail != cand; c += kUnroll) {
-        uint4 m[kUnroll];
+      for (int c = c0; c < c1 && fail != cand; c += UC) {
+        uint4 m[UC][SL];
         const uint8_t* q = pc;
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          if (c + u < c1) m[u] = ldg_stream(reinterpret_cast<const uint4*>(q));
+        for (int u = 0; u < UC; ++u) {
+          if (c + u < c1)
+#pragma unroll
+            for (int j = 0; j < SL; ++j)
+              if (!tail || rbase + (size_t)j * 32 * RPL < rows_alloc)
+                m[u][j] = ldg_stream(reinterpret_cast<const uint4*>(q + (size_t)j * 32 * 16));
+              else
+                m[u][j] = make_uint4(~0u, ~0u, ~0u, ~0u);
           q += g.col_stride;
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          if (c + u < c1) {
-            const uint64_t d = load_w<W>(Db + (c + u) * W);
-            fail |= column_fail<W>(m[u], d, cand & ~fail, c + u, r0, g.dmax, g.P, g.pw);
-          }
-        }
+        for (int u = 0; u < UC; ++u)
+          if (c + u < c1) test(m[u], c + u, load_w<W>(Db + (c + u) * W));
         pc = q;
       }
     } else {
-      constexpr int UL = kUnrollL;  // listed columns: an index each
-      for (int c = c0; c < c1 && fail != cand; c += UL) {
-        uint4 m[UL];
-        int yy[UL];
+      for (int c = c0; c < c1 && fail != cand; c += ULc) {
+        uint4 m[ULc][SL];
+        int yy[ULc];
 #pragma unroll
-        for (int u = 0; u < UL; ++u) {
+        for (int u = 0; u < ULc; ++u) {
           yy[u] = c + u < c1 ? (int)cols[c + u] : -1;
-          if (yy[u] >= 0) m[u] = ldg_stream(reinterpret_cast<const uint4*>(base + (size_t)yy[u] * g.col_stride));
+          if (yy[u] >= 0)
+#pragma unroll
+            for (int j = 0; j < SL; ++j)
+              if (!tail || rbase + (size_t)j * 32 * RPL < rows_alloc)
+                m[u][j] = ldg_stream(
+                    reinterpret_cast<const uint4*>(base + (size_t)yy[u] * g.col_stride + (size_t)j * 32 * 16));
+              else
+                m[u][j] = make_uint4(~0u, ~0u, ~0u, ~0u);
         }
 #pragma unroll
-        for (int u = 0; u < UL; ++u) {
-          if (yy[u] >= 0) {
-            const uint64_t d = load_w<W>(Db + yy[u] * W);
-            fail |= column_fail<W>(m[u], d, cand & ~fail, yy[u], r0, g.dmax, g.P, g.pw);
-          }
-        }
+        for (int u = 0; u < ULc; ++u)
+          if (yy[u] >= 0) test(m[u], yy[u], load_w<W>(Db + yy[u] * W));
       }
     }
     if (fail && rflag) atomicOr(rflag, 1u);  // this pass removed something
-    for (uint32_t f = fail; f; f &= f - 1u) {
-      const int r = r0 + __ffs(f) - 1;
+    for (uint64_t f = fail; f; f &= f - 1ull) {
+      const int bit = __ffsll((long long)f) - 1;
+      const int r = slab * RPW + (bit / RPL) * 32 * RPL + lane * RPL + (bit % RPL);
       const int xl = r / g.dmax, a = r - xl * g.dmax;
       const int x = g.x_lo_alloc + xl;
       atomicOr(&R[x], 1ull << a);
@@ -137,69 +159,60 @@ __device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* D
   }
 }
 
-// Sparse arc-block sweep (NEXT-3): the tested columns' blocks form one flat
-// range of 16-byte vectors (all blocks in a full pass; the listed columns'
-// blocks, through the prefix `pref`, otherwise).  A warp item is 32 x kUnrollS
-// consecutive vectors: each lane issues its kUnrollS streaming loads first,
-// then per vector reads the arc (x, y) of its block, tests the 16/W rows
-// a0.. of x that are live against D(y) and ORs failures into R[x].  Only
+// Sparse arc-block sweep (NEXT-3).  Work item = (tested column y, chunk of
+// 32 x kUnrollS consecutive 16-byte vectors of column y's blocks); ipref[i] =
+// items before the i-th tested column (all columns in a full pass, the listed
+// ones otherwise).  Per item: one binary search in shared memory, D(y) read
+// once; each lane streams kUnrollS vectors and tests them against D(y) with a
+// zero-lane check.  Only a vector with some zero lane (rare) looks up its arc
+// (x, y) and the live rows of x, and ORs real failures into R[x].  Only
 // declared arcs are stored, so no presence check is needed (reading R2).
 template <int W>
 __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                              int32_t* removed_at, int t, long warp0, long nwarps,
-                                             const uint16_t* cols, int ncol, const uint32_t* pref,
+                                             const uint16_t* cols, int ncol, const uint32_t* ipref,
                                              unsigned* rflag) {
   constexpr int L = 16 / W, U = kUnrollS;
   constexpr uint32_t LM = (L == 32) ? 0xffffffffu : ((1u << L) - 1u);
   const int lane = threadIdx.x & 31;
   const uint32_t VB = (uint32_t)g.s_vb;
-  const uint32_t nblk = cols ? pref[ncol] : g.s_nblk;
-  const uint32_t nvec = nblk * VB;
-  const uint32_t items = (nvec + 32u * U - 1u) / (32u * U);
+  const uint32_t items = ipref[ncol];
   const uint4* S4 = reinterpret_cast<const uint4*>(g.S);
-  int ci = 0;  // listed column of the lane's current vector (monotone within an item)
+  int ci = 0;
   for (uint32_t it = (uint32_t)warp0; it < items; it += (uint32_t)nwarps) {
+    int hi = ncol - 1;  // last i with ipref[i] <= it (items increase: search from the previous ci)
+    while (ci < hi) {
+      const int mid = (ci + hi + 1) >> 1;
+      if (ipref[mid] <= it) ci = mid; else hi = mid - 1;
+    }
+    const int y = cols ? (int)cols[ci] : ci;
+    const uint32_t b0 = __ldg(g.s_off + y);
+    const uint32_t nv = (__ldg(g.s_off + y + 1) - b0) * VB;
+    const uint32_t v0 = (it - ipref[ci]) * 32u * U + (uint32_t)lane;
+    const uint4* col = S4 + (size_t)b0 * VB;
     uint4 m[U];
-    uint32_t blk[U], part[U];
-    if (cols) {  // binary search for the first vector of the item, then walk
-      const uint32_t k0 = min((it * 32u * U + lane) / VB, nblk - 1u);
-      int lo = 0, hi = ncol - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (pref[mid] <= k0) lo = mid; else hi = mid - 1;
-      }
-      ci = lo;
-    }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t v = it * 32u * U + (uint32_t)(u * 32 + lane);
-      blk[u] = 0xffffffffu;
-      if (v < nvec) {
-        const uint32_t k = v / VB;
-        part[u] = v - k * VB;
-        if (cols) {
-          while (pref[ci + 1] <= k) ++ci;
-          blk[u] = __ldg(g.s_off + cols[ci]) + (k - pref[ci]);
-        } else {
-          blk[u] = k;
-        }
-        m[u] = ldg_stream(S4 + (size_t)blk[u] * VB + part[u]);
-      }
-    }
+    for (int u = 0; u < U; ++u)
+      if (v0 + u * 32u < nv) m[u] = ldg_stream(col + v0 + u * 32u);
+    const uint4 dy = rep16<W>(load_w<W>(Db + y * W));
     uint32_t any = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      if (blk[u] != 0xffffffffu) {
-        const uint32_t arc = __ldg(g.s_arc + blk[u]);
-        const int x = (int)(arc & 0xffffu), y = (int)(arc >> 16);
-        const int a0 = (int)part[u] * L;
-        const uint32_t cand = (uint32_t)(load_w<W>(Db + x * W) >> a0) & LM;
-        const uint32_t f = zero_lanes<W>(and4(m[u], rep16<W>(load_w<W>(Db + y * W)))) & cand;
-        if (f) {
-          any = 1;
-          atomicOr(&R[x], (unsigned long long)f << a0);
-          if (removed_at)
-            for (uint32_t ff = f; ff; ff &= ff - 1u) removed_at[(size_t)x * 64 + a0 + __ffs(ff) - 1] = t;
+      const uint32_t v = v0 + u * 32u;
+      if (v < nv) {
+        const uint4 tv = and4(m[u], dy);
+        if (vec_any_zero<W>(tv)) {  // rare: some row of this vector may lose its support
+          const uint32_t k = v / VB, pp = v - k * VB;
+          const int x = (int)(__ldg(g.s_arc + b0 + k) & 0xffffu);
+          const int a0 = (int)pp * L;
+          const uint32_t cand = (uint32_t)(load_w<W>(Db + x * W) >> a0) & LM;
+          const uint32_t f = zero_lanes<W>(tv) & cand;
+          if (f) {
+            any = 1;
+            atomicOr(&R[x], (unsigned long long)f << a0);
+            if (removed_at)
+              for (uint32_t ff = f; ff; ff &= ff - 1u) removed_at[(size_t)x * 64 + a0 + __ffs(ff) - 1] = t;
+          }
         }
       }
     }
@@ -346,7 +359,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   RAC_MARK();
   const long warp0 = (long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const long nwarps = (long)gridDim.x * (blockDim.x / 32);
-  const long gidx = warp0 * (32 / G) + (threadIdx.x & 31) / G, ngroups = nwarps * (32 / G);
+  constexpr int GG = G == 0 ? 1 : G;  // G == 0: the sparse arc-block variant
+  const long gidx = warp0 * (32 / GG) + (threadIdx.x & 31) / GG, ngroups = nwarps * (32 / GG);
   const bool full = (p.flags & kFull) != 0;
   int t = 0, status = kOK, vcnt = g.n;
   unsigned epoch = 0;
@@ -392,15 +406,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       }
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
-      if (g.S) {
-        const uint32_t* pref = reinterpret_cast<const uint32_t*>(Db + pref_offset(g.dbytes, g.n));
-        if (lst) block_prefix_blocks(vlist, vcnt, g.s_off, const_cast<uint32_t*>(pref), scratch);
-        sparse_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, vcnt, pref, p.rflag + b);
-      } else if (pick_rows(g, live, lst ? vcnt : g.n))
-        row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b);
-      else
-        column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
+      if constexpr (G == 0) {
+        uint32_t* ipref = reinterpret_cast<uint32_t*>(Db + pref_offset(g.dbytes, g.n));
+        if (lst) {
+          block_prefix_items(vlist, vcnt, g.s_off, (uint32_t)g.s_vb, 32u * kUnrollS, ipref, scratch);
+        } else {  // every column: the item prefix precomputed at create
+          for (int i = threadIdx.x; i <= g.n; i += blockDim.x) ipref[i] = __ldg(g.s_ipref + i);
+          __syncthreads();
+        }
+        sparse_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ipref,
                         p.rflag + b);
+      } else {
+        if (pick_rows(g, live, lst ? vcnt : g.n))
+          row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b);
+        else
+          column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
+                          p.rflag + b);
+      }
       RAC_MARK();
       if (p.dbg != nullptr && t == 1) {  // block-uniform condition: the barrier is safe
         __syncthreads();
@@ -704,7 +726,7 @@ cudaError_t set_smem(K k, size_t smem) {
 }
 
 template <int W, int G>
-struct Launch {
+struct LaunchF {
   static cudaError_t fused(const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
     auto k = rac_fused<W, G>;
     cudaError_t e = set_smem(k, smem);
@@ -717,6 +739,16 @@ struct Launch {
     k<<<grid, kThreads, smem, s>>>(p);
     return cudaGetLastError();
   }
+  static cudaError_t occ_fused(size_t smem, int* out) {
+    const void* k = (const void*)rac_fused<W, G>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
+  }
+};
+
+template <int W, int G>
+struct Launch {
   static cudaError_t pass(const PassParams& p, int grid, size_t smem, cudaStream_t s) {
     auto k = rac_pass<W, G>;
     cudaError_t e = set_smem(k, smem);
@@ -732,8 +764,7 @@ struct Launch {
     return cudaGetLastError();
   }
   static cudaError_t occ(int which, size_t smem, int* out) {
-    const void* k = which == 0 ? (const void*)rac_fused<W, G>
-                    : which == 1 ? (const void*)rac_pass<W, G> : (const void*)rac_batch<W, G>;
+    const void* k = which == 1 ? (const void*)rac_pass<W, G> : (const void*)rac_batch<W, G>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, kThreads, smem);
@@ -750,6 +781,26 @@ struct Launch {
     case 8: return Launch<WW, 8>::CALL;                            \
     case 16: return Launch<WW, 16>::CALL;                          \
     case 32: return Launch<WW, 32>::CALL;                          \
+    default: return cudaErrorInvalidValue;                         \
+  }
+// fused kernel only: G == 0 selects the sparse arc-block variant
+#define RAC_G0_SWITCH(WW, G, CALL)                                 \
+  switch (G) {                                                     \
+    case 0: return LaunchF<WW, 0>::CALL;                           \
+    case 1: return LaunchF<WW, 1>::CALL;                           \
+    case 2: return LaunchF<WW, 2>::CALL;                           \
+    case 4: return LaunchF<WW, 4>::CALL;                           \
+    case 8: return LaunchF<WW, 8>::CALL;                           \
+    case 16: return LaunchF<WW, 16>::CALL;                         \
+    case 32: return LaunchF<WW, 32>::CALL;                         \
+    default: return cudaErrorInvalidValue;                         \
+  }
+#define RAC_WG0_SWITCH(W, G, CALL)                                 \
+  switch (W) {                                                     \
+    case 1: RAC_G0_SWITCH(1, G, CALL)                              \
+    case 2: RAC_G0_SWITCH(2, G, CALL)                              \
+    case 4: RAC_G0_SWITCH(4, G, CALL)                              \
+    case 8: RAC_G0_SWITCH(8, G, CALL)                              \
     default: return cudaErrorInvalidValue;                         \
   }
 #define RAC_WG_SWITCH(W, G, CALL)                                  \
@@ -769,9 +820,9 @@ int choose_group(int nvec) {
 }
 
 cudaError_t launch_fused(int W, int G, const FusedParams& p, int grid, size_t smem, cudaStream_t s, bool coop) {
-  RAC_WG_SWITCH(W, G, fused(p, grid, smem, s, coop))
+  RAC_WG0_SWITCH(W, G, fused(p, grid, smem, s, coop))
 }
-cudaError_t fused_occupancy(int W, int G, size_t smem, int* out) { RAC_WG_SWITCH(W, G, occ(0, smem, out)) }
+cudaError_t fused_occupancy(int W, int G, size_t smem, int* out) { RAC_WG0_SWITCH(W, G, occ_fused(smem, out)) }
 cudaError_t launch_pass(int W, int G, const PassParams& p, int grid, size_t smem, cudaStream_t s) {
   RAC_WG_SWITCH(W, G, pass(p, grid, smem, s))
 }

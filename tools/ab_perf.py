@@ -62,6 +62,18 @@ def batch(S=1024):
 
 
 tag = sys.argv[1] if len(sys.argv) > 1 else ""
+if os.environ.get("AB_SET") == "cols":  # column-sweep workloads only
+    os.environ["RAC_FORCE_LAYOUT"] = "cols"
+    print(tag, "cols:", single("c3stream", 2000, 32, 1.0, 0.5), single("c3prop", 2000, 32, 1.0, 0.70, reps=50),
+          single("c3seed", 2000, 32, 1.0, 0.5, "seed", 100), flush=True)
+    del os.environ["RAC_FORCE_LAYOUT"]
+    print(tag, "auto:", single("c3prop", 2000, 32, 1.0, 0.70, reps=50), single("c3seed", 2000, 32, 1.0, 0.5, "seed", 100),
+          single("c2", 500, 20, 1.0, 0.3, reps=1000), flush=True)
+    sys.exit(0)
+if os.environ.get("AB_SET") == "sparse":
+    print(tag, single("c3s_stream", 4000, 32, 0.25, 0.5, reps=100), single("c3s_prop", 4000, 32, 0.25, 0.72, reps=50),
+          flush=True)
+    sys.exit(0)
 print(tag, single("c1seed", 20, 8, 0.5, 0.4, "seed", 2000), single("c5single_seed", 200, 16, 0.8, 0.3, "seed", 1000),
       single("c2", 500, 20, 1.0, 0.3, reps=1000), single("c3stream", 2000, 32, 1.0, 0.5),
       single("c3prop", 2000, 32, 1.0, 0.70, reps=50), single("c3seed", 2000, 32, 1.0, 0.5, "seed", 100),
