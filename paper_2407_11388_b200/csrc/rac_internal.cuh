@@ -39,15 +39,7 @@ constexpr int kMinBlocks = RAC_MIN_BLOCKS;  // CTAs per SM the register budget i
 #ifndef RAC_UNROLL_C
 #define RAC_UNROLL_C 8
 #endif
-#ifndef RAC_UNROLL_L
-#define RAC_UNROLL_L 8
-#endif
-constexpr int kUnroll = RAC_UNROLL_C;   // 16-byte column loads in flight per lane (contiguous columns)
-constexpr int kUnrollL = RAC_UNROLL_L;  // ... listed columns (an index each)
-#ifndef RAC_COL_SLABS
-#define RAC_COL_SLABS 1
-#endif
-constexpr int kColSlabs = RAC_COL_SLABS;  // 512-byte slabs per warp item of the column sweep
+constexpr int kUnroll = RAC_UNROLL_C;   // 16-byte loads in flight per lane (column sweep)
 #ifndef RAC_UNROLL_S
 #define RAC_UNROLL_S 16
 #endif
@@ -352,6 +344,22 @@ __device__ __forceinline__ uint32_t column_fail(uint4 m, uint64_t d, uint32_t ca
   return f;
 }
 
+// column_fail with the AND already taken (t = mask & D(y) over the 16/W rows):
+// the rows among `cand` whose test failed on a declared c_xy.
+template <int W>
+__device__ __forceinline__ uint32_t column_fail_t(uint4 t, uint64_t d, uint32_t cand, int y, int r0, int dmax,
+                                                  const uint32_t* P, int pw) {
+  const uint32_t z = zero_lanes<W>(t) & cand;
+  if (z == 0u || d != 0ull) return z;
+  uint32_t f = 0;
+  for (uint32_t zz = z; zz; zz &= zz - 1u) {
+    const int i = __ffs(zz) - 1;
+    const int xl = (r0 + i) / dmax;
+    if ((P[(size_t)xl * pw + (y >> 5)] >> (y & 31)) & 1u) f |= 1u << i;
+  }
+  return f;
+}
+
 // ---- row-major sweep helpers
 // Does any W-byte lane of t equal zero?  (t = mask & D, 16 bytes = 16/W masks)
 template <int W>
@@ -467,23 +475,10 @@ __device__ __forceinline__ int block_compact(uint8_t* need, uint16_t* out, int c
   return total;
 }
 
-// Sparse layout: ipref[i] = work items of the listed columns list[0..i)
-// (column y has ceil((s_off[y+1] - s_off[y]) * VB / per_item) items of
-// per_item vectors), ipref[cnt] = total.  Block-wide; every CTA computes it
-// redundantly from its own list; returns the total.
-__device__ __forceinline__ uint32_t block_prefix_items(const uint16_t* list, int cnt, const uint32_t* s_off,
-                                                       uint32_t VB, uint32_t per_item, uint32_t* ipref,
-                                                       int* scratch) {
-  const int T = blockDim.x, t = threadIdx.x;
-  const int chunk = (cnt + T - 1) / T;
-  const int b = min(cnt, t * chunk), e = min(cnt, b + chunk);
-  auto items_of = [&](int i) {
-    const int y = list[i];
-    return ((__ldg(s_off + y + 1) - __ldg(s_off + y)) * VB + per_item - 1u) / per_item;
-  };
-  uint32_t c = 0;
-  for (int i = b; i < e; ++i) c += items_of(i);
-  const int lane = t & 31, w = t >> 5;
+// Block-wide inclusive scan of one u32 per thread (every thread gets its
+// exclusive prefix and the total).
+__device__ __forceinline__ uint32_t block_scan_u32(uint32_t c, uint32_t* total, int* scratch) {
+  const int T = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
   uint32_t v = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -503,15 +498,45 @@ __device__ __forceinline__ uint32_t block_prefix_items(const uint16_t* list, int
     if (lane < (T >> 5)) scratch[lane] = (int)s;
   }
   __syncthreads();
-  uint32_t pos = v - c + (w > 0 ? (uint32_t)scratch[w - 1] : 0u);
+  const uint32_t excl = v - c + (w > 0 ? (uint32_t)scratch[w - 1] : 0u);
+  *total = (uint32_t)scratch[(T >> 5) - 1];
+  __syncthreads();
+  return excl;
+}
+
+// Sparse layout, listed columns: choose the vectors per lane per item `upl`
+// (U, fewer when the pass is too small to give every warp an item) and write
+// ipref[i] = work items of list[0..i) (column y has ceil((s_off[y+1] -
+// s_off[y]) * VB / (32 upl)) items), ipref[cnt] = total.  Block-wide; every
+// CTA computes it redundantly from its own list.  Returns upl.
+__device__ __forceinline__ uint32_t block_prefix_items(const uint16_t* list, int cnt, const uint32_t* s_off,
+                                                       uint32_t VB, uint32_t U, long nwarps, uint32_t* ipref,
+                                                       int* scratch) {
+  const int T = blockDim.x, t = threadIdx.x;
+  const int chunk = (cnt + T - 1) / T;
+  const int b = min(cnt, t * chunk), e = min(cnt, b + chunk);
+  uint32_t c = 0;
+  for (int i = b; i < e; ++i) c += __ldg(s_off + list[i] + 1) - __ldg(s_off + list[i]);
+  uint32_t tot_blocks;
+  block_scan_u32(c, &tot_blocks, scratch);
+  const uint64_t upl64 = (uint64_t)tot_blocks * VB / (32ull * (uint64_t)nwarps);
+  const uint32_t upl = upl64 < 1 ? 1u : (upl64 > U ? U : (uint32_t)upl64);
+  const uint32_t per_item = 32u * upl;
+  auto items_of = [&](int i) {
+    const int y = list[i];
+    return ((__ldg(s_off + y + 1) - __ldg(s_off + y)) * VB + per_item - 1u) / per_item;
+  };
+  c = 0;
+  for (int i = b; i < e; ++i) c += items_of(i);
+  uint32_t total;
+  uint32_t pos = block_scan_u32(c, &total, scratch);
   for (int i = b; i < e; ++i) {
     ipref[i] = pos;
     pos += items_of(i);
   }
-  const uint32_t total = (uint32_t)scratch[(T >> 5) - 1];
   if (t == 0) ipref[cnt] = total;
   __syncthreads();
-  return total;
+  return upl;
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {

@@ -41,121 +41,68 @@ constexpr uint32_t kFull = 1u;  // RAC_FULL_FIXPOINT
 constexpr int kOK = 0, kWIPEOUT = 1;
 constexpr int kPeerTimeout = -7;  // RAC_EPEER
 
-// Test the rows of variables [g.x_lo, g.x_hi) against the columns
-// cols[0, ncol) (cols == nullptr: columns 0..ncol-1) and OR removals into R.
-// Work items = (slab of 32*(16/W) rows, chunk of columns), one warp per item,
-// static round-robin over the warps [warp0, warp0 + nwarps) of the launch.
+// Column sweep: test the rows of variables [g.x_lo, g.x_hi) against the
+// columns cols[0, ncol) (cols == nullptr: columns 0..ncol-1) and OR removals
+// into R.  Work item = (tested column y, chunk of 32 x kUnrollC consecutive
+// 16-byte vectors of column y's rows); the columns all have the same rows, so
+// item -> (column, chunk) is one division.  Per item D(y) is read once; each
+// lane streams kUnrollC vectors (16/W rows each) and tests them with a
+// zero-lane check; only a vector with a zero lane (rare) works out which of
+// its rows are live and declared-unsupported and ORs them into R.  Dead rows
+// are not skipped here: the per-pass layout choice (pick_rows) sends passes
+// with few live rows to the row-major sweep, which skips them.
 template <int W>
-__device__ __forceinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
-                                             int32_t* removed_at, int t, long warp0, long nwarps,
-                                             const uint16_t* cols, int ncol, unsigned* rflag = nullptr) {
-  // SL slabs per item: a warp reads SL x 512 contiguous bytes of each column
-  // (lane l holds rows l*RPL.. of each slab); loads in flight per lane stay
-  // kUnroll (kUnroll/SL columns x SL slabs).
-  constexpr int SL = kColSlabs;
-  constexpr int RPL = 16 / W, RPW = 32 * RPL * SL;
-  constexpr int UC = kUnroll / SL > 0 ? kUnroll / SL : 1;
-  constexpr int ULc = kUnrollL / SL > 0 ? kUnrollL / SL : 1;
-  constexpr uint64_t LM = (RPL == 64) ? ~0ull : ((1ull << RPL) - 1ull);
+__device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
+                                          int32_t* removed_at, int t, long warp0, long nwarps,
+                                          const uint16_t* cols, int ncol, unsigned* rflag = nullptr) {
+  constexpr int RPL = 16 / W, U = kUnroll;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
   const int r_hi = (g.x_hi - g.x_lo_alloc) * g.dmax;
   if (r_hi <= r_lo || ncol <= 0) return;
-  const int s_lo = r_lo / RPW, s_hi = (r_hi + RPW - 1) / RPW;
-  const int nslab = s_hi - s_lo;
-  // about 4 items per warp, each at least UC columns long (32-bit
-  // arithmetic only: 64-bit division is a long software sequence)
-  const int nw = (int)nwarps;
-  int nchunk = (4 * nw + nslab - 1) / nslab;
-  const int maxchunk = (ncol + UC - 1) / UC;
-  if (nchunk > maxchunk) nchunk = maxchunk;
-  if (nchunk < 1) nchunk = 1;
-  const int yc = (ncol + nchunk - 1) / nchunk;
-  nchunk = (ncol + yc - 1) / yc;
-  const int items = nslab * nchunk;
-  const size_t rows_alloc = g.col_stride / W;  // padded rows per column
-  for (int it = (int)warp0; it < items; it += nw) {
-    const int chunk = it / nslab;
-    const int slab = s_lo + (it - chunk * nslab);
-    uint64_t cand = 0;  // live rows of this lane: bit j*RPL + i = row slab*RPW + j*32*RPL + lane*RPL + i
+  const uint32_t v_lo = (uint32_t)r_lo / RPL, v_hi = ((uint32_t)r_hi + RPL - 1) / RPL;
+  // vectors per lane per item: U, fewer when the pass is too small to give
+  // every warp an item (latency-bound passes spread over more warps)
+  const uint64_t tot = (uint64_t)(v_hi - v_lo) * (uint32_t)ncol;
+  const uint64_t upl64 = tot / (32ull * (uint64_t)nwarps);
+  const uint32_t upl = upl64 < 1ull ? 1u : (upl64 > (uint64_t)U ? (uint32_t)U : (uint32_t)upl64);
+  const uint32_t ipc = (v_hi - v_lo + 32u * upl - 1u) / (32u * upl);  // items per column
+  const uint32_t items = ipc * (uint32_t)ncol;
+  for (uint32_t it = (uint32_t)warp0; it < items; it += (uint32_t)nwarps) {
+    const uint32_t c = it / ipc, chunk = it - c * ipc;
+    const int y = cols ? (int)cols[c] : (int)c;
+    const uint4* col = reinterpret_cast<const uint4*>(g.M + (size_t)y * g.col_stride);
+    const uint32_t v0 = v_lo + chunk * 32u * upl + (uint32_t)lane;
+    const uint32_t ve = min(v_hi, v0 - (uint32_t)lane + 32u * upl);
+    uint4 m[U];
 #pragma unroll
-    for (int j = 0; j < SL; ++j) {
-      const int r0 = slab * RPW + j * 32 * RPL + lane * RPL;
-      int xl = r0 / g.dmax, a = r0 - xl * g.dmax;
+    for (int u = 0; u < U; ++u)
+      if (v0 + u * 32u < ve) m[u] = ldg_stream(col + v0 + u * 32u);
+    const uint64_t dv = load_w<W>(Db + y * W);
+    const uint4 rd = rep16<W>(dv);
+    uint32_t any = 0;
 #pragma unroll
-      for (int i = 0; i < RPL; ++i) {
-        const int r = r0 + i;
-        if (r >= r_lo && r < r_hi) {
-          const int x = g.x_lo_alloc + xl;
-          if ((Db[x * W + (a >> 3)] >> (a & 7)) & 1u) cand |= 1ull << (j * RPL + i);
+    for (int u = 0; u < U; ++u) {
+      const uint32_t v = v0 + u * 32u;
+      if (v < ve) {
+        const uint4 tv = and4(m[u], rd);
+        if (vec_any_zero<W>(tv)) {  // rare: some row of this vector may lose its support
+          const uint32_t z = zero_lanes<W>(tv);
+          for (uint32_t zz = z; zz; zz &= zz - 1u) {
+            const int r = (int)v * RPL + __ffs(zz) - 1;
+            if (r < r_lo || r >= r_hi) continue;
+            const int xl = r / g.dmax, a = r - xl * g.dmax;
+            const int x = g.x_lo_alloc + xl;
+            if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;  // (x,a) not live
+            if (dv == 0ull && !((g.P[(size_t)xl * g.pw + (y >> 5)] >> (y & 31)) & 1u)) continue;  // R2
+            any = 1;
+            atomicOr(&R[x], 1ull << a);
+            if (removed_at) removed_at[(size_t)x * 64 + a] = t;
+          }
         }
-        if (++a == g.dmax) { a = 0; ++xl; }
       }
     }
-    uint64_t fail = 0;
-    const int c0 = chunk * yc, c1 = min(c0 + yc, ncol);
-    const size_t rbase = (size_t)slab * RPW + (size_t)lane * RPL;
-    const bool tail = rbase + (size_t)(SL - 1) * 32 * RPL >= rows_alloc;  // last slabs past the padding
-    const uint8_t* base = g.M + rbase * W;
-    auto test = [&](const uint4* m, int y, uint64_t dv) {
-#pragma unroll
-      for (int j = 0; j < SL; ++j) {
-        const int r0 = slab * RPW + j * 32 * RPL + lane * RPL;
-        const uint32_t cj = (uint32_t)(((cand & ~fail) >> (j * RPL)) & LM);
-        if (cj) fail |= (uint64_t)column_fail<W>(m[j], dv, cj, y, r0, g.dmax, g.P, g.pw) << (j * RPL);
-      }
-    };
-    if (cols == nullptr) {
-      const uint8_t* pc = base + (size_t)c0 * g.col_stride;
-      for (int c = c0; c < c1 && fail != cand; c += UC) {
-        uint4 m[UC][SL];
-        const uint8_t* q = pc;
-#pragma unroll
-        for (int u = 0; u < UC; ++u) {
-          if (c + u < c1)
-#pragma unroll
-            for (int j = 0; j < SL; ++j)
-              if (!tail || rbase + (size_t)j * 32 * RPL < rows_alloc)
-                m[u][j] = ldg_stream(reinterpret_cast<const uint4*>(q + (size_t)j * 32 * 16));
-              else
-                m[u][j] = make_uint4(~0u, ~0u, ~0u, ~0u);
-          q += g.col_stride;
-        }
-#pragma unroll
-        for (int u = 0; u < UC; ++u)
-          if (c + u < c1) test(m[u], c + u, load_w<W>(Db + (c + u) * W));
-        pc = q;
-      }
-    } else {
-      for (int c = c0; c < c1 && fail != cand; c += ULc) {
-        uint4 m[ULc][SL];
-        int yy[ULc];
-#pragma unroll
-        for (int u = 0; u < ULc; ++u) {
-          yy[u] = c + u < c1 ? (int)cols[c + u] : -1;
-          if (yy[u] >= 0)
-#pragma unroll
-            for (int j = 0; j < SL; ++j)
-              if (!tail || rbase + (size_t)j * 32 * RPL < rows_alloc)
-                m[u][j] = ldg_stream(
-                    reinterpret_cast<const uint4*>(base + (size_t)yy[u] * g.col_stride + (size_t)j * 32 * 16));
-              else
-                m[u][j] = make_uint4(~0u, ~0u, ~0u, ~0u);
-        }
-#pragma unroll
-        for (int u = 0; u < ULc; ++u)
-          if (yy[u] >= 0) test(m[u], yy[u], load_w<W>(Db + yy[u] * W));
-      }
-    }
-    if (fail && rflag) atomicOr(rflag, 1u);  // this pass removed something
-    for (uint64_t f = fail; f; f &= f - 1ull) {
-      const int bit = __ffsll((long long)f) - 1;
-      const int r = slab * RPW + (bit / RPL) * 32 * RPL + lane * RPL + (bit % RPL);
-      const int xl = r / g.dmax, a = r - xl * g.dmax;
-      const int x = g.x_lo_alloc + xl;
-      atomicOr(&R[x], 1ull << a);
-      if (removed_at) removed_at[(size_t)x * 64 + a] = t;
-    }
+    if (any && rflag) atomicOr(rflag, 1u);  // this pass removed something
   }
 }
 
@@ -171,7 +118,7 @@ template <int W>
 __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                              int32_t* removed_at, int t, long warp0, long nwarps,
                                              const uint16_t* cols, int ncol, const uint32_t* ipref,
-                                             unsigned* rflag) {
+                                             uint32_t upl, unsigned* rflag) {
   constexpr int L = 16 / W, U = kUnrollS;
   constexpr uint32_t LM = (L == 32) ? 0xffffffffu : ((1u << L) - 1u);
   const int lane = threadIdx.x & 31;
@@ -188,18 +135,19 @@ __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* D
     const int y = cols ? (int)cols[ci] : ci;
     const uint32_t b0 = __ldg(g.s_off + y);
     const uint32_t nv = (__ldg(g.s_off + y + 1) - b0) * VB;
-    const uint32_t v0 = (it - ipref[ci]) * 32u * U + (uint32_t)lane;
+    const uint32_t v0 = (it - ipref[ci]) * 32u * upl + (uint32_t)lane;
+    const uint32_t ve = min(nv, v0 - (uint32_t)lane + 32u * upl);
     const uint4* col = S4 + (size_t)b0 * VB;
     uint4 m[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (v0 + u * 32u < nv) m[u] = ldg_stream(col + v0 + u * 32u);
+      if (v0 + u * 32u < ve) m[u] = ldg_stream(col + v0 + u * 32u);
     const uint4 dy = rep16<W>(load_w<W>(Db + y * W));
     uint32_t any = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t v = v0 + u * 32u;
-      if (v < nv) {
+      if (v < ve) {
         const uint4 tv = and4(m[u], dy);
         if (vec_any_zero<W>(tv)) {  // rare: some row of this vector may lose its support
           const uint32_t k = v / VB, pp = v - k * VB;
@@ -225,7 +173,7 @@ __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* D
 // the first failing column and dead-row skip.  Rows are split into n_seg
 // segments so that every group gets several items.
 template <int W, int G>
-__device__ __forceinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
+__device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
                                           int32_t* removed_at, int t, long gidx, long ngroups,
                                           unsigned* wctr = nullptr, unsigned* rflag = nullptr) {
   const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
@@ -293,9 +241,9 @@ __device__ __forceinline__ bool pick_rows(const PassGeom& g, long long live, int
   const long long rows = (long long)(g.x_hi - g.x_lo) * g.dmax;
   // tiny tensors are latency-bound: whole rows are fewer, simpler work items
   if (rows * (long long)g.dbytes <= (256ll << 10)) return true;
-  // bytes of each layout, the column stream weighted by its measured rate
-  // (~3.7 vs ~6.5 TB/s at C3, profiles/r01d timeline): 7 col bytes ~ 4 row bytes
-  return 4 * live * (long long)g.n <= 7 * rows * (long long)ncol;
+  // bytes of each layout (both sweeps stream at about the same rate since the
+  // column sweep reads column-aligned 4 KB items, profiles/r01j)
+  return live * (long long)g.n < rows * (long long)ncol;
 }
 
 // Live rows (x,a) of variables [x_lo, x_hi) in D (every thread of the CTA gets it).
@@ -408,14 +356,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       RAC_MARK();
       if constexpr (G == 0) {
         uint32_t* ipref = reinterpret_cast<uint32_t*>(Db + pref_offset(g.dbytes, g.n));
+        uint32_t upl = kUnrollS;
         if (lst) {
-          block_prefix_items(vlist, vcnt, g.s_off, (uint32_t)g.s_vb, 32u * kUnrollS, ipref, scratch);
+          upl = block_prefix_items(vlist, vcnt, g.s_off, (uint32_t)g.s_vb, kUnrollS, nwarps, ipref, scratch);
         } else {  // every column: the item prefix precomputed at create
           for (int i = threadIdx.x; i <= g.n; i += blockDim.x) ipref[i] = __ldg(g.s_ipref + i);
           __syncthreads();
         }
         sparse_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ipref,
-                        p.rflag + b);
+                        upl, p.rflag + b);
       } else {
         if (pick_rows(g, live, lst ? vcnt : g.n))
           row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b);
