@@ -41,6 +41,49 @@ constexpr uint32_t kFull = 1u;  // RAC_FULL_FIXPOINT
 constexpr int kOK = 0, kWIPEOUT = 1;
 constexpr int kPeerTimeout = -7;  // RAC_EPEER
 
+// Work-item iterator of a warp: the first ~7/8 of the items are assigned
+// round robin, the rest are claimed one at a time from a per-pass counter
+// (the next claim in flight while the current item streams), so SMs that
+// drain HBM faster take more of the tail.  Without a counter: plain round
+// robin.  (Measured on the 4 KB items of the column and sparse sweeps: one
+// same-address atomic per item costs more than the imbalance it removes --
+// C3 W-stream 88.7 -> 92.1 us -- so those sweeps run round robin.)
+struct ItemIter {
+  uint32_t items, nw, per, S, k, pending;
+  unsigned* wctr;
+  int lane;
+  uint32_t warp0;
+  __device__ __forceinline__ ItemIter(uint32_t items_, long warp0_, long nwarps_, unsigned* wctr_)
+      : items(items_), nw((uint32_t)nwarps_), k(0), pending(0), wctr(wctr_), lane(threadIdx.x & 31),
+        warp0((uint32_t)warp0_) {
+    per = wctr ? (items - items / 8) / nw : (items + nw - 1) / nw;
+    S = wctr ? per * nw : items;
+    if (wctr && per == 0) pending = claim();
+  }
+  __device__ __forceinline__ uint32_t claim() {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(wctr, 1u);
+    return S + __shfl_sync(0xffffffffu, b, 0);
+  }
+  // next item of this warp (warp-uniform); false when done
+  __device__ __forceinline__ bool next(uint32_t& it) {
+    for (;;) {
+      if (k < per) {
+        it = warp0 + k * nw;
+        if (++k == per && wctr) pending = claim();
+        if (it < items) return true;
+      } else if (wctr) {
+        it = pending;
+        if (it >= items) return false;
+        pending = claim();
+        return true;
+      } else {
+        return false;
+      }
+    }
+  }
+};
+
 // Column sweep: test the rows of variables [g.x_lo, g.x_hi) against the
 // columns cols[0, ncol) (cols == nullptr: columns 0..ncol-1) and OR removals
 // into R.  Work item = (tested column y, chunk of 32 x kUnrollC consecutive
@@ -54,7 +97,8 @@ constexpr int kPeerTimeout = -7;  // RAC_EPEER
 template <int W>
 __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                           int32_t* removed_at, int t, long warp0, long nwarps,
-                                          const uint16_t* cols, int ncol, unsigned* rflag = nullptr) {
+                                          const uint16_t* cols, int ncol, unsigned* rflag = nullptr,
+                                          unsigned* wctr = nullptr) {
   constexpr int RPL = 16 / W, U = kUnroll;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
@@ -68,7 +112,8 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
   const uint32_t upl = upl64 < 1ull ? 1u : (upl64 > (uint64_t)U ? (uint32_t)U : (uint32_t)upl64);
   const uint32_t ipc = (v_hi - v_lo + 32u * upl - 1u) / (32u * upl);  // items per column
   const uint32_t items = ipc * (uint32_t)ncol;
-  for (uint32_t it = (uint32_t)warp0; it < items; it += (uint32_t)nwarps) {
+  ItemIter iter(items, warp0, nwarps, wctr);
+  for (uint32_t it; iter.next(it);) {
     const uint32_t c = it / ipc, chunk = it - c * ipc;
     const int y = cols ? (int)cols[c] : (int)c;
     const uint4* col = reinterpret_cast<const uint4*>(g.M + (size_t)y * g.col_stride);
@@ -118,7 +163,7 @@ template <int W>
 __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                              int32_t* removed_at, int t, long warp0, long nwarps,
                                              const uint16_t* cols, int ncol, const uint32_t* ipref,
-                                             uint32_t upl, unsigned* rflag) {
+                                             uint32_t upl, unsigned* rflag, unsigned* wctr) {
   constexpr int L = 16 / W, U = kUnrollS;
   constexpr uint32_t LM = (L == 32) ? 0xffffffffu : ((1u << L) - 1u);
   const int lane = threadIdx.x & 31;
@@ -126,7 +171,8 @@ __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* D
   const uint32_t items = ipref[ncol];
   const uint4* S4 = reinterpret_cast<const uint4*>(g.S);
   int ci = 0;
-  for (uint32_t it = (uint32_t)warp0; it < items; it += (uint32_t)nwarps) {
+  ItemIter iter(items, warp0, nwarps, wctr);
+  for (uint32_t it; iter.next(it);) {
     int hi = ncol - 1;  // last i with ipref[i] <= it (items increase: search from the previous ci)
     while (ci < hi) {
       const int mid = (ci + hi + 1) >> 1;
@@ -364,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
           __syncthreads();
         }
         sparse_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ipref,
-                        upl, p.rflag + b);
+                        upl, p.rflag + b, nullptr);
       } else {
         if (pick_rows(g, live, lst ? vcnt : g.n))
           row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b);

@@ -46,3 +46,4 @@ run("c5-single", 200, 16, 0.8, 0.3, "seed")
 run("c2-root", 500, 20, 1.0, 0.3)
 run("c3-stream", 2000, 32, 1.0, 0.5)
 run("c3-prop", 2000, 32, 1.0, 0.70)
+run("c3s-prop", 4000, 32, 0.25, 0.72)
