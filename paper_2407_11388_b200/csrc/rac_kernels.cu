@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   extern __shared__ uint4 Ds[];
   __shared__ int scratch[kThreads / 32];
   __shared__ int s_last;
+  __shared__ int s_red[2][2];  // per-pass-parity block reductions: [flags, removed live values]
   const PassGeom& g = p.g;
   uint8_t* Db = reinterpret_cast<uint8_t*>(Ds);
   uint16_t* vlist = reinterpret_cast<uint16_t*>(Db + list_offset(g.dbytes));
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   int t = 0, status = kOK, vcnt = g.n;
   unsigned epoch = 0;
   long long live = count_live<W>(Db, g.x_lo, g.x_hi, scratch);  // this rank's rows
+  if (threadIdx.x < 4) s_red[threadIdx.x >> 1][threadIdx.x & 1] = 0;  // (ordered by later barriers)
   // Rotating buffers and the cross-rank sequence follow the global pass
   // number base + t, which continues across launches: pass k clears the
   // buffers of pass k+1, so no launch needs a cleanup phase and a peer that
@@ -451,6 +453,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       if (__ldcg(p.rflag + b) == 0u) {
         wipe = has_empty;
       } else {
+        // one block barrier for the three reductions: flags (changed | wipe)
+        // and the live values of the local rows this pass removed
+        int nrm = 0;
+        const int par = t & 1;
+        if (threadIdx.x == 0) { s_red[par ^ 1][0] = 0; s_red[par ^ 1][1] = 0; }  // next pass's slots
         for (int x0 = threadIdx.x; x0 < g.n; x0 += 4 * blockDim.x) {
           uint64_t rv[4];
 #pragma unroll
@@ -469,17 +476,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
             changed |= chx;
             wipe |= nd == 0;
             if (chx) vneed[x] = 1;
+            if (x >= g.x_lo && x < g.x_hi) nrm += __popcll(dv & rv[k]);
           }
         }
+        const int fl = __reduce_or_sync(0xffffffffu, changed | (wipe << 1));
+        nrm = __reduce_add_sync(0xffffffffu, nrm);
+        if ((threadIdx.x & 31) == 0) {
+          if (fl) atomicOr_block(&s_red[par][0], fl);
+          if (nrm) atomicAdd_block(&s_red[par][1], nrm);
+        }
+        __syncthreads();
+        changed = s_red[par][0] & 1;
+        wipe = (s_red[par][0] >> 1) & 1;
+        live -= s_red[par][1];
       }
-      changed = __syncthreads_or(changed);
-      wipe = __syncthreads_or(wipe);
       has_empty = wipe;
       RAC_MARK();
       if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
       if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
       vcnt = block_compact(vneed, vlist, g.n, scratch);        // next pass's columns
-      live = count_live<W>(Db, g.x_lo, g.x_hi, scratch);
       RAC_MARK();
     }
   }
