@@ -155,13 +155,19 @@ def run_gpu(args, rank, world, local_rank):
     n, d, dens, tight, seed, kind, desc = WORKLOADS[args.workload]
     dq, tq = synth.quant_density(dens), synth.quant_tightness(tight)
     uid = None
-    if world > 1:
+    peer = world > 1 and args.exchange == "peer"
+    if world > 1 and not peer:
         obj = [rac.rac_get_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     t0 = time.time()
     ctx = rac.RacContext.create_random(n, d, dq, tq, seed, device=local_rank, rank=rank, world=world,
-                                       nccl_unique_id=uid)
+                                       nccl_unique_id=uid, peer=peer)
+    if peer:
+        # the regions' CUDA IPC handles travel over the process group; the
+        # per-pass exchange then runs inside the one persistent kernel
+        from paper_2407_11388_b200 import dist as rdist
+        rdist.connect_peers(ctx)
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     full = synth.full_domains(np.full(n, d))
@@ -355,7 +361,7 @@ def run_gpu(args, rank, world, local_rank):
                 traffic = None
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                    "kernel": "rac_fused" if world == 1 else "rac_pass (+ allgather)",
+                    "kernel": "rac_fused" if (world == 1 or peer) else "rac_pass (+ allgather)",
                     "algorithmic_bytes_per_launch": alg_bytes,
                     "launch_ms_median": round(kern_ms, 5),
                     "peak_source": peak_src + ("" if world == 1 else "; per-GPU bytes = total / N")}
@@ -367,7 +373,9 @@ def run_gpu(args, rank, world, local_rank):
            "layout": ctx.layout, "relation_bytes": ctx.relation_bytes,
            "l2": "inputs larger than L2 (no flush)" if ctx.relation_bytes > 200e6 else
                  "relation L2-resident (warm; stated, not flushed)",
-           "parallelism": ("row-sharded x%d (NCCL all-gather of D per pass)" % world) if world > 1 else "1 GPU",
+           "parallelism": (("row-sharded x%d (peer-memory removal exchange + cross-rank barrier inside the "
+                            "persistent kernel, NVLink P2P)" if peer else
+                            "row-sharded x%d (NCCL all-gather of D per pass)") % world) if world > 1 else "1 GPU",
            "instance_generation_s": round(gen_s, 3)}
     out = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -486,6 +494,9 @@ def main():
     ap.add_argument("--states", type=int, default=1024)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: per-pass exchange through peer memory inside the fused kernel (default) "
+                         "or an NCCL all-gather between per-pass launches")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:
