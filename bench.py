@@ -192,11 +192,30 @@ def run_gpu(args, rank, world, local_rank):
 
     # --- instrumentation run (outside the timed region): iterations, status, live rows per pass
     if kind == "dive":
-        res = [ctx.enforce(din_h[s]) for s in range(S)]
+        res = [ctx.enforce(din_h[s], removed_at=True) for s in range(S)]
         iters_list = [r[2] for r in res]
         instr = {"iterations_mean": float(np.mean(iters_list)), "iterations_max": int(np.max(iters_list)),
                  "wipeout_frac": float(np.mean([r[0] == 1 for r in res]))}
         alg_bytes = None
+        # Algorithmic support tests of Alg. 1 per state (seeded call):
+        # pass t tests every live (x,a) against the declared c_xy whose y changed in
+        # pass t-1 (the state's assigned variable in pass 1).  The removal epochs come
+        # from the plain recurrence, whose trajectory the seeded call follows (DESIGN R12).
+        xs_p, ys_p = synth.present_pairs(n, dq, seed)
+        alg_tests = 0
+        for s_i, r in enumerate(res):
+            remd = r[3][:, :d]
+            live0 = np.array([[(int(din_h[s_i][x]) >> a) & 1 for a in range(d)] for x in range(n)], dtype=bool)
+            chg = np.zeros(n, dtype=bool)
+            chg[seed_vars[s_i]] = True
+            for t in range(1, r[2] + 1):
+                lv = (live0 & ((remd == 0) | (remd >= t))).sum(axis=1)
+                nb = np.zeros(n, dtype=np.int64)
+                np.add.at(nb, xs_p, chg[ys_p].astype(np.int64))
+                np.add.at(nb, ys_p, chg[xs_p].astype(np.int64))
+                alg_tests += int((lv * nb).sum())
+                chg = (remd == t).any(axis=1)
+        instr["support_tests"] = alg_tests
     else:
         stt, dout, it, rem = (ctx.enforce(din_h[0], removed_at=True) if world == 1 else
                               (*ctx.enforce(din_h[0]), None))
@@ -349,6 +368,25 @@ def run_gpu(args, rank, world, local_rank):
 
     peak, peak_src = measured_peaks()
     roofline = None
+    if kind == "dive":
+        # Bit-sliced batched pass (rac_batch_bs): a support test of (x,a) against
+        # c_xy for 32 states is ceil(d/4) nibble-table lookups in shared memory;
+        # the LDS issue rate (32 lanes x 4 B per clock per SM) bounds it:
+        #   peak = 148 SM x 32 lookups/clk x f_max / ceil(d/4) x 32 states
+        kern_ms = statistics.median(per_step)
+        sm_mhz = 1965.0
+        try:
+            sm_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+        except Exception:
+            pass
+        peak_t = 148 * 32 * sm_mhz * 1e6 / ((d + 3) // 4) * 32 / 1e12
+        ach_t = instr["support_tests"] / (kern_ms / 1e3) / 1e12
+        roofline = {"bound": "alu", "achieved": round(ach_t, 4), "peak": round(peak_t, 2),
+                    "unit": "T support-tests/s (x,a,y,state)", "frac": round(ach_t / peak_t, 4),
+                    "traffic": None, "kernel": "rac_batch_bs",
+                    "algorithmic_tests_per_launch": instr["support_tests"], "launch_ms_median": round(kern_ms, 5),
+                    "peak_source": "derived: LDS lookups (148 SM x 32/clk x %.0f MHz) / ceil(d/4) lookups per "
+                                   "32-state test; DESIGN.md section 7" % sm_mhz}
     if alg_bytes is not None:
         kern_ms = statistics.median(per_step)
         achieved = alg_bytes / (kern_ms / 1e3) / 1e9
