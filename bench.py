@@ -161,8 +161,11 @@ def run_gpu(args, rank, world, local_rank):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     t0 = time.time()
+    max_ctas = 0
+    if os.environ.get("RAC_BENCH_SHARED_GPU") == "1" and world > 1:
+        max_ctas = max(1, torch.cuda.get_device_properties(local_rank).multi_processor_count // world)
     ctx = rac.RacContext.create_random(n, d, dq, tq, seed, device=local_rank, rank=rank, world=world,
-                                       nccl_unique_id=uid, peer=peer)
+                                       nccl_unique_id=uid, peer=peer, max_ctas=max_ctas)
     if peer:
         # the regions' CUDA IPC handles travel over the process group; the
         # per-pass exchange then runs inside the one persistent kernel
@@ -543,6 +546,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # Testing knob: RAC_BENCH_SHARED_GPU=1 runs every rank on cuda:0 (gloo process
+    # group, peer exchange, grids capped so they fit together) to exercise the N > 1
+    # code path on a one-GPU box.  Numbers from it are not throughput claims.
+    shared = os.environ.get("RAC_BENCH_SHARED_GPU") == "1" and world > 1
+    if shared:
+        local_rank = 0
 
     if args.impl == "reference":
         if rank != 0:
@@ -555,7 +564,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out, wl = run_gpu(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
