@@ -103,6 +103,7 @@ struct rac_ctx {
   uint8_t* peer_base[RAC_MAX_RANKS] = {};  // every rank's region as seen from this device (self = xr)
   bool peer_ipc[RAC_MAX_RANKS] = {};       // opened with cudaIpcOpenMemHandle (closed at destroy)
   unsigned* bar = nullptr;
+  uint32_t* clist = nullptr;  // fused path: per-pass change lists [3][n+1]
   ShardState sh{};
   uint64_t* buf_in = nullptr;   // blocking-API staging
   uint64_t* buf_out = nullptr;
@@ -172,6 +173,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->dommask);
   cudaFree(c->xr);
   cudaFree(c->bar);
+  cudaFree(c->clist);
   cudaFree(c->sh.Dcur);
   cudaFree(c->sh.Dg);
   cudaFree(c->sh.Dw);
@@ -323,6 +325,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
   CKC(cudaMemsetAsync(c->xr, 0, xr_bytes(n), c->stream));
   c->R3 = reinterpret_cast<unsigned long long*>(c->xr);
   if (c->rank < RAC_MAX_RANKS) c->peer_base[c->rank] = c->xr;
+  CKC(cudaMalloc(&c->clist, (size_t)3 * (n + 1) * 4));
+  CKC(cudaMemsetAsync(c->clist, 0, (size_t)3 * (n + 1) * 4, c->stream));
   CKC(cudaMalloc(&c->bar, 64));
   CKC(cudaMemsetAsync(c->bar, 0, 64, c->stream));  // [0..3] grid barrier, [4..6] row counters, [12] peer error
   const size_t gtot = (size_t)c->world * c->blk;
@@ -482,6 +486,8 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   static const bool no_claim = getenv("RAC_NO_CLAIM") != nullptr;  // A/B knob (tooling only)
   p.wctr = no_claim ? nullptr : c->bar + 4;
   p.rflag = reinterpret_cast<unsigned*>(c->xr + xr_rflag_off(c->n));
+  static const bool no_clist = getenv("RAC_NO_CLIST") != nullptr;  // A/B knob (tooling only)
+  p.clist = no_clist ? nullptr : c->clist;
   p.seq = reinterpret_cast<unsigned long long*>(c->xr + xr_seq_off(c->n));
   p.mir.world = c->peer ? c->world : 1;
   p.mir.rank = c->rank;

@@ -100,6 +100,7 @@ struct FusedParams {
   unsigned* bar;            // grid barrier words [4]
   unsigned* wctr;           // [3] per-pass dynamic row counters (rotating like R)
   unsigned* rflag;          // [3] per-pass "some value was removed" flags (rotating like R)
+  uint32_t* clist;          // nullable [3][n+1] per-pass change lists ([0] = count; rotating like R)
   const int32_t* seeds;     // nullable device [n_seeds]: Alg. 1 initial @changed
   int n_seeds;
   uint32_t flags;

@@ -41,6 +41,19 @@ constexpr uint32_t kFull = 1u;  // RAC_FULL_FIXPOINT
 constexpr int kOK = 0, kWIPEOUT = 1;
 constexpr int kPeerTimeout = -7;  // RAC_EPEER
 
+// OR removal bits into R[x]; with a change list `cl` ([0] = count, then the
+// variables), the first removal of x in the pass appends x -- after the grid
+// barrier only the listed words need to be read (and they are the next pass's
+// tested columns, Alg. 1's @changed).
+__device__ __forceinline__ void mark_removed(unsigned long long* R, int x, unsigned long long bits, uint32_t* cl) {
+  if (cl == nullptr) {
+    atomicOr(&R[x], bits);  // fire-and-forget reduction
+    return;
+  }
+  const unsigned long long old = atomicOr(&R[x], bits);
+  if (old == 0ull) cl[1 + atomicAdd(cl, 1u)] = (uint32_t)x;
+}
+
 // Work-item iterator of a warp: the first ~7/8 of the items are assigned
 // round robin, the rest are claimed one at a time from a per-pass counter
 // (the next claim in flight while the current item streams), so SMs that
@@ -48,6 +61,13 @@ constexpr int kPeerTimeout = -7;  // RAC_EPEER
 // robin.  (Measured on the 4 KB items of the column and sparse sweeps: one
 // same-address atomic per item costs more than the imbalance it removes --
 // C3 W-stream 88.7 -> 92.1 us -- so those sweeps run round robin.)
+#ifndef RAC_CLAIM_DIV
+#define RAC_CLAIM_DIV 8
+#endif
+constexpr uint32_t kClaimDiv = RAC_CLAIM_DIV;  // 1/kClaimDiv of the items are claimed dynamically
+#ifndef RAC_COL_CLAIM
+#define RAC_COL_CLAIM 0
+#endif
 struct ItemIter {
   uint32_t items, nw, per, S, k, pending;
   unsigned* wctr;
@@ -56,7 +76,7 @@ struct ItemIter {
   __device__ __forceinline__ ItemIter(uint32_t items_, long warp0_, long nwarps_, unsigned* wctr_)
       : items(items_), nw((uint32_t)nwarps_), k(0), pending(0), wctr(wctr_), lane(threadIdx.x & 31),
         warp0((uint32_t)warp0_) {
-    per = wctr ? (items - items / 8) / nw : (items + nw - 1) / nw;
+    per = wctr ? (items - items / kClaimDiv) / nw : (items + nw - 1) / nw;
     S = wctr ? per * nw : items;
     if (wctr && per == 0) pending = claim();
   }
@@ -98,7 +118,7 @@ template <int W>
 __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                           int32_t* removed_at, int t, long warp0, long nwarps,
                                           const uint16_t* cols, int ncol, unsigned* rflag = nullptr,
-                                          unsigned* wctr = nullptr) {
+                                          unsigned* wctr = nullptr, uint32_t* cl = nullptr) {
   constexpr int RPL = 16 / W, U = kUnroll;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
@@ -141,7 +161,7 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
             if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;  // (x,a) not live
             if (dv == 0ull && !((g.P[(size_t)xl * g.pw + (y >> 5)] >> (y & 31)) & 1u)) continue;  // R2
             any = 1;
-            atomicOr(&R[x], 1ull << a);
+            mark_removed(R, x, 1ull << a, cl);
             if (removed_at) removed_at[(size_t)x * 64 + a] = t;
           }
         }
@@ -163,7 +183,7 @@ template <int W>
 __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                              int32_t* removed_at, int t, long warp0, long nwarps,
                                              const uint16_t* cols, int ncol, const uint32_t* ipref,
-                                             uint32_t upl, unsigned* rflag, unsigned* wctr) {
+                                             uint32_t upl, unsigned* rflag, unsigned* wctr, uint32_t* cl) {
   constexpr int L = 16 / W, U = kUnrollS;
   constexpr uint32_t LM = (L == 32) ? 0xffffffffu : ((1u << L) - 1u);
   const int lane = threadIdx.x & 31;
@@ -203,7 +223,7 @@ __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* D
           const uint32_t f = zero_lanes<W>(tv) & cand;
           if (f) {
             any = 1;
-            atomicOr(&R[x], (unsigned long long)f << a0);
+            mark_removed(R, x, (unsigned long long)f << a0, cl);
             if (removed_at)
               for (uint32_t ff = f; ff; ff &= ff - 1u) removed_at[(size_t)x * 64 + a0 + __ffs(ff) - 1] = t;
           }
@@ -221,7 +241,8 @@ __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* D
 template <int W, int G>
 __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
                                           int32_t* removed_at, int t, long gidx, long ngroups,
-                                          unsigned* wctr = nullptr, unsigned* rflag = nullptr) {
+                                          unsigned* wctr = nullptr, unsigned* rflag = nullptr,
+                                          uint32_t* cl = nullptr) {
   const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
@@ -250,7 +271,7 @@ __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsig
     const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
     const int vb = sgi * seg, ve = min(vb + seg, nvec);
     if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
-      atomicOr(&R[x], 1ull << a);
+      mark_removed(R, x, 1ull << a, cl);
       if (rflag) atomicOr(rflag, 1u);  // this pass removed something
       if (removed_at) removed_at[(size_t)x * 64 + a] = t;
     }
@@ -367,6 +388,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   // is already in the next launch only writes buffers this rank has cleared.
   const unsigned long long base = *reinterpret_cast<volatile unsigned long long*>(p.seq);
   const bool mg = p.mir.world > 1;
+  // sparse layout, single rank: removals also go to a per-pass change list, so
+  // the tail of a pass reads only the changed variables' R words and needs no
+  // compaction.  (Measured on the dense layout it is a wash -- C3 W-prop
+  // 239 -> 235 us but W-seed 132 -> 143 us -- so dense passes keep the
+  // full-R apply; sparse W-prop 319 -> 304 us.)
+  const bool use_list = G == 0 && p.clist != nullptr && !mg;
   int b = (int)(base % 3ull);  // buffer of global pass base + t, advanced each pass
   int has_empty = 0;  // some D(x) empty (block-uniform)
   for (int x = threadIdx.x; x < g.n; x += blockDim.x) has_empty |= load_w<W>(Db + x * W) == 0;
@@ -399,7 +426,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (p.wctr) p.wctr[bn] = 0u;
         p.rflag[bn] = 0u;
+        if (use_list) p.clist[(size_t)bn * (g.n + 1)] = 0u;
       }
+      uint32_t* clc = use_list ? p.clist + (size_t)b * (g.n + 1) : nullptr;  // this pass's change list
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       RAC_MARK();
       if constexpr (G == 0) {
@@ -412,13 +441,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
           __syncthreads();
         }
         sparse_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ipref,
-                        upl, p.rflag + b, nullptr);
+                        upl, p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc);
       } else {
         if (pick_rows(g, live, lst ? vcnt : g.n))
-          row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b);
+          row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b,
+                          clc);
         else
           column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
-                          p.rflag + b);
+                          p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc);
       }
       RAC_MARK();
       if (p.dbg != nullptr && t == 1) {  // block-uniform condition: the barrier is safe
@@ -450,7 +480,40 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       // removed nothing (the per-pass flag is still 0) leaves D as it was:
       // changed = 0, wipe = "D already had an empty row", no R read.
       int changed = 0, wipe = 0;
-      if (__ldcg(p.rflag + b) == 0u) {
+      bool listed = false;  // vlist/vcnt already hold the next pass's columns
+      if (use_list) {
+        const int cnt = (int)__ldcg(clc);
+        if (cnt == 0) {
+          wipe = has_empty;
+        } else {
+          // every listed x lost a live value (marks are made for live rows only)
+          int wp = 0, nrm = 0;
+          const int par = t & 1;
+          if (threadIdx.x == 0) s_red[par ^ 1][0] = 0, s_red[par ^ 1][1] = 0;  // next pass's slots
+          for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            const int x = (int)__ldcg(clc + 1 + i);
+            const uint64_t rv = __ldcg(&Rc[x]);
+            const uint64_t dv = load_w<W>(Db + x * W);
+            const uint64_t nd = dv & ~rv;
+            store_w<W>(Db + x * W, nd);
+            wp |= nd == 0;
+            if (x >= g.x_lo && x < g.x_hi) nrm += __popcll(dv & rv);
+            vlist[i] = (uint16_t)x;
+          }
+          wp = __reduce_or_sync(0xffffffffu, wp);
+          nrm = __reduce_add_sync(0xffffffffu, nrm);
+          if ((threadIdx.x & 31) == 0) {
+            if (wp) atomicOr_block(&s_red[par][0], 2);
+            if (nrm) atomicAdd_block(&s_red[par][1], nrm);
+          }
+          __syncthreads();
+          changed = 1;
+          wipe = has_empty | ((s_red[par][0] >> 1) & 1);
+          live -= s_red[par][1];
+          vcnt = cnt;
+          listed = true;
+        }
+      } else if (__ldcg(p.rflag + b) == 0u) {
         wipe = has_empty;
       } else {
         // one block barrier for the three reductions: flags (changed | wipe)
@@ -494,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       RAC_MARK();
       if (wipe && !full) { status = kWIPEOUT; break; }          // Alg. 1
       if (!changed) { status = wipe ? kWIPEOUT : kOK; break; }  // Prop. 1 end condition
-      vcnt = block_compact(vneed, vlist, g.n, scratch);        // next pass's columns
+      if (!listed) vcnt = block_compact(vneed, vlist, g.n, scratch);  // next pass's columns
       RAC_MARK();
     }
   }
