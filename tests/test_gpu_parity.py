@@ -691,3 +691,50 @@ def test_sparse_unsupported_and_invalid(rac):
     with pytest.raises(rac.RacError) as e:
         rac.RacContext.from_instance(inst, layout="sparse", virtual_shards=2)
     assert e.value.code == rac.RAC_EINVAL
+
+
+@pytest.mark.parametrize("n,d,p,t", [(120, 16, 0.3, 0.6), (90, 40, 0.4, 0.8), (80, 64, 0.35, 0.9), (150, 5, 0.2, 0.2)])
+def test_sparse_mask_widths(rac, n, d, p, t):
+    """Sparse arc blocks at every mask width (W = 1, 2, 8 bytes; dpad padding at
+    d = 40 and d = 5), generated instances: W-root, W-rand and full-fixpoint mode
+    with epochs, seeded calls after an assignment -- all equal to the oracle."""
+    dq, tq = synth.quant_density(p), synth.quant_tightness(t)
+    ctx = rac.RacContext.create_random(n, d, dq, tq, 4, layout="sparse")
+    assert ctx.layout == "sparse"
+    orc = oracle.Oracle.from_synth(n, d, dq, tq, 4)
+    root = synth.full_domains(np.full(n, d))
+    o_root = orc.rac(root)
+    assert_same(ctx.enforce(root, removed_at=True), o_root, "root")
+    for k in range(4):
+        d_in = synth.w_rand(np.full(n, d), 0.85, 20 + k)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (k, full))
+    if o_root[0] == oracle.OK:
+        for k in range(4):
+            s, x, v = synth.w_seed(o_root[1], 9, k)
+            g = ctx.enforce_seeded(s, [x])
+            o = orc.rac(s, with_epochs=False)
+            assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1]), k
+
+
+def test_sparse_nonuniform_domains(rac):
+    """Per-variable domain sizes through the sparse layout (rows a >= dom(x) are
+    padding inside each block, never live)."""
+    rng = np.random.default_rng(8)
+    for k in range(60):
+        n = int(rng.integers(2, 40))
+        dom = rng.integers(1, 30, size=n)
+        cons = []
+        for x in range(n):
+            for y in range(x + 1, n):
+                if rng.random() < 0.4:
+                    allowed = [(a, b) for a in range(dom[x]) for b in range(dom[y]) if rng.random() > 0.3]
+                    cons.append((x, y, allowed))
+        inst = synth.from_constraints(n, dom, cons)
+        ctx = rac.RacContext.from_instance(inst, layout="sparse")
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = synth.w_rand(inst.dom, 0.85, seed=k)
+        for full in (False, True):
+            g, o = both(ctx, orc, d_in, full)
+            assert_same(g, o, (k, full))
