@@ -39,7 +39,7 @@ __device__ __forceinline__ void word_sync(unsigned* bar, unsigned nblocks, unsig
     if (prev + 1u == nblocks * epoch) {
       st_release_gpu(&bar[1], epoch);
     } else {
-      while (ld_acquire_gpu(&bar[1]) < epoch) __nanosleep(128);
+      while (ld_relaxed_gpu(&bar[1]) < epoch) __nanosleep(128);
     }
     __threadfence();
   }

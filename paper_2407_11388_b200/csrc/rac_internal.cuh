@@ -592,6 +592,21 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   return v;
 }
 
+// Spin-wait loads: relaxed (an acquire load invalidates the SM's L1 on every
+// poll -- CCTL.IVALL in the SASS -- which evicted the L1-cached operands of the
+// other CTAs sharing the SM); the fence after the loop gives the acquire.
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -616,7 +631,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks, unsig
     if (prev + 1u == nblocks * epoch) {
       st_release_gpu(&bar[1], epoch);
     } else {
-      while (ld_acquire_gpu(&bar[1]) < epoch) __nanosleep(32);
+      while (ld_relaxed_gpu(&bar[1]) < epoch) __nanosleep(32);
     }
     __threadfence();
   }
@@ -642,7 +657,7 @@ static __device__ __noinline__ void grid_sync_peer(unsigned* bar, unsigned nbloc
       const unsigned long long t0 = globaltimer();
       for (int q = 0; q < p.mir.world; ++q) {
         if (q == p.mir.rank) continue;
-        while (ld_acquire_sys64(p.arrive + q) < seqv) {
+        while (ld_relaxed_sys64(p.arrive + q) < seqv) {
           if (*reinterpret_cast<volatile int32_t*>(p.xerr)) break;
           if (globaltimer() - t0 > p.timeout_ns) {
             atomicExch(p.xerr, 1);
@@ -654,7 +669,7 @@ static __device__ __noinline__ void grid_sync_peer(unsigned* bar, unsigned nbloc
       __threadfence_system();
       if (nblocks > 1) st_release_gpu(&bar[1], epoch);
     } else {
-      while (ld_acquire_gpu(&bar[1]) < epoch) __nanosleep(32);
+      while (ld_relaxed_gpu(&bar[1]) < epoch) __nanosleep(32);
     }
     __threadfence();
   }
