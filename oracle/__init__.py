@@ -93,6 +93,21 @@ def _load():
         lib.orc_pass_block.argtypes = [P, u64p, ctypes.c_int, ctypes.c_int, u64p]
         lib.orc_domain_size.argtypes = [P, u64p]
         lib.orc_domain_size.restype = ctypes.c_int64
+        lib.orc_wbuild.restype = P
+        lib.orc_wbuild.argtypes = [ctypes.c_int, i32p, ctypes.c_int, i32p, i32p, u64p, ctypes.c_int]
+        lib.orc_wbuild_synth.restype = P
+        lib.orc_wbuild_synth.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
+                                         ctypes.c_uint64]
+        lib.orc_wfree.argtypes = [P]
+        lib.orc_wfree.restype = None
+        lib.orc_wq.argtypes = [P]
+        lib.orc_wq.restype = ctypes.c_int
+        lib.orc_rac_wide.argtypes = [P, u64p, u64p, i32p, i32p, ctypes.c_int]
+        lib.orc_rac_wide.restype = ctypes.c_int
+        lib.orc_wis_ac.argtypes = [P, u64p]
+        lib.orc_wis_ac.restype = ctypes.c_int
+        lib.orc_wac3.argtypes = [P, u64p, u64p]
+        lib.orc_wac3.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -223,6 +238,70 @@ class Oracle:
 
     def degree(self, x: int) -> int:
         return int(_load().orc_degree(self._h, x))
+
+
+class WideOracle:
+    """Wide-domain instance (NEXT-4, domains up to 256 values): domain states are
+    [n * wq] uint64 words, wq = ceil(max dom / 64); removal epochs [n, 64 * wq]."""
+
+    def __init__(self, handle, n: int, dom: np.ndarray):
+        self._h = handle
+        self.n = n
+        self.dom = dom
+        self.wq = int(_load().orc_wq(handle))
+
+    @classmethod
+    def from_instance(cls, inst) -> "WideOracle":
+        """inst.rows: uint64 [n_rel, max_dom, wq] (synth.wide_from_constraints / random_csp_wide)."""
+        lib = _load()
+        dom = np.ascontiguousarray(inst.dom, dtype=np.int32)
+        xs = np.ascontiguousarray(inst.xs, dtype=np.int32)
+        ys = np.ascontiguousarray(inst.ys, dtype=np.int32)
+        wq = max(1, (int(dom.max()) + 63) // 64)
+        rows = np.ascontiguousarray(inst.rows, dtype=np.uint64)
+        stride = rows.shape[1] if rows.ndim == 3 and rows.shape[0] else int(dom.max())
+        if rows.size == 0:
+            rows = np.zeros((1, stride, wq), dtype=np.uint64)
+        assert rows.shape[2] == wq, "rows must be [n_rel, max_dom, ceil(max_dom/64)]"
+        h = lib.orc_wbuild(inst.n, _i32p(dom), xs.shape[0], _i32p(xs), _i32p(ys), _u64p(rows), stride)
+        if not h:
+            raise ValueError("invalid instance")
+        return cls(h, inst.n, dom)
+
+    @classmethod
+    def from_synth(cls, n: int, d: int, dens_q32: int, t_q16: int, seed: int) -> "WideOracle":
+        h = _load().orc_wbuild_synth(n, d, dens_q32, t_q16, seed)
+        if not h:
+            raise ValueError("invalid generator parameters")
+        return cls(h, n, np.full(n, d, dtype=np.int32))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.orc_wfree(self._h)
+            self._h = None
+
+    def rac(self, d_in, full: bool = False, with_epochs: bool = True):
+        """O1w. Returns (status, d_out [n*wq], iterations, removed_at [n, 64*wq] or None)."""
+        lib = _load()
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
+        assert d_in.size == self.n * self.wq
+        d_out = np.zeros(self.n * self.wq, dtype=np.uint64)
+        it = np.zeros(1, dtype=np.int32)
+        rem = np.zeros(self.n * 64 * self.wq, dtype=np.int32) if with_epochs else None
+        st = lib.orc_rac_wide(self._h, _u64p(d_in), _u64p(d_out), _i32p(it),
+                              _i32p(rem) if rem is not None else None, 1 if full else 0)
+        return st, d_out, int(it[0]), (rem.reshape(self.n, 64 * self.wq) if rem is not None else None)
+
+    def is_ac(self, D) -> bool:
+        D = np.ascontiguousarray(D, dtype=np.uint64).reshape(-1)
+        return bool(_load().orc_wis_ac(self._h, _u64p(D)))
+
+    def ac3(self, d_in):
+        """AC-3 to the fixpoint on wide domains.  Returns (status, d_out)."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
+        d_out = np.zeros(self.n * self.wq, dtype=np.uint64)
+        st = _load().orc_wac3(self._h, _u64p(d_in), _u64p(d_out))
+        return st, d_out
 
 
 def row_supported_synth(n: int, d: int, dens_q32: int, t_q16: int, seed: int, x: int, a: int, D) -> bool:

@@ -668,3 +668,273 @@ int64_t orc_domain_size(const orc_csp *c, const uint64_t *D) {
   for (int x = 0; x < c->n; ++x) s += popc64(D[x] & dom_mask(c->dom[x]));
   return s;
 }
+
+/* ======================================================================== */
+/*
+ * Wide domains (d > 64, up to 256 values).
+ *
+ * The same recurrence, Eq. 1 with Alg. 1's loop
+ * (lines 198-210) and readings R1-R7, on domains wider than one machine word.
+ * The paper fixes no domain-size limit (its Cons is a dense [n,d,n,d] fp32
+ * tensor); only the bitset width changes here.  A domain state is
+ * wq = ceil(dmax/64) uint64 words per variable: bit a of variable x is bit
+ * (a % 64) of word D[x*wq + a/64].  Support sets c_xy|(x,a) are wq-word
+ * bitsets over dom(y).  removed_at has n * 64*wq entries, (x,a) at x*64*wq + a.
+ * Kept separate from the one-word functions above so that those stay exactly
+ * as pinned; the pins of these (tests/test_oracle.py "wide"): value
+ * duplication of a pinned one-word instance, the arc-consistency audit, the
+ * Lemma-1 certificate and AC-3 agreement (orc_wac3).
+ */
+typedef struct {
+  int n, wq;
+  int *dom;
+  int *deg;
+  int **nbr;       /* ascending */
+  uint64_t **sup;  /* sup[x][((size_t)k*dom[x] + a)*wq + w] */
+} orc_wcsp;
+
+void orc_wfree(orc_wcsp *c) {
+  if (!c) return;
+  for (int x = 0; x < c->n; ++x) {
+    if (c->nbr) free(c->nbr[x]);
+    if (c->sup) free(c->sup[x]);
+  }
+  free(c->nbr); free(c->sup); free(c->dom); free(c->deg);
+  free(c);
+}
+
+static int wbit(const uint64_t *v, int b) { return (int)((v[b >> 6] >> (b & 63)) & 1ULL); }
+static void wset(uint64_t *v, int b) { v[b >> 6] |= 1ULL << (b & 63); }
+
+static orc_wcsp *walloc(int n, const int *dom) {
+  int dmax = 1;
+  for (int x = 0; x < n; ++x) if (dom[x] > dmax) dmax = dom[x];
+  orc_wcsp *c = (orc_wcsp *)calloc(1, sizeof(orc_wcsp));
+  if (!c) return NULL;
+  c->n = n;
+  c->wq = (dmax + 63) / 64;
+  c->dom = (int *)calloc((size_t)n, sizeof(int));
+  c->deg = (int *)calloc((size_t)n, sizeof(int));
+  c->nbr = (int **)calloc((size_t)n, sizeof(int *));
+  c->sup = (uint64_t **)calloc((size_t)n, sizeof(uint64_t *));
+  if (!c->dom || !c->deg || !c->nbr || !c->sup) { orc_wfree(c); return NULL; }
+  for (int x = 0; x < n; ++x) c->dom[x] = dom[x];
+  return c;
+}
+
+static int walloc_arcs(orc_wcsp *c) {
+  for (int x = 0; x < c->n; ++x) {
+    size_t k = (size_t)(c->deg[x] > 0 ? c->deg[x] : 1);
+    c->nbr[x] = (int *)malloc(k * sizeof(int));
+    c->sup[x] = (uint64_t *)calloc(k * (size_t)c->dom[x] * (size_t)c->wq, sizeof(uint64_t));
+    if (!c->nbr[x] || !c->sup[x]) return -1;
+  }
+  return 0;
+}
+
+static int warc_index(const orc_wcsp *c, int x, int y) {
+  for (int k = 0; k < c->deg[x]; ++k) if (c->nbr[x][k] == y) return k;
+  return -1;
+}
+
+int orc_wq(const orc_wcsp *c) { return c->wq; }
+
+/*
+ * Explicit relations: constraint r on (xs[r], ys[r]); row a of rel(c_{xs,ys})
+ * is the wq-word bitset rows[(r*row_stride + a)*wq .. +wq) (bit b set iff
+ * (a,b) allowed), wq = ceil(max dom / 64).  Domain sizes 1..256.
+ */
+orc_wcsp *orc_wbuild(int n, const int *dom, int n_rel, const int *xs, const int *ys,
+                     const uint64_t *rows, int row_stride) {
+  if (n < 1) return NULL;
+  for (int x = 0; x < n; ++x)
+    if (dom[x] < 1 || dom[x] > 256) return NULL;
+  orc_wcsp *c = walloc(n, dom);
+  if (!c) return NULL;
+  const int wq = c->wq;
+  for (int r = 0; r < n_rel; ++r) {
+    int x = xs[r], y = ys[r];
+    if (x < 0 || y < 0 || x >= n || y >= n || x == y) { orc_wfree(c); return NULL; }
+    c->deg[x]++; c->deg[y]++;
+  }
+  if (walloc_arcs(c)) { orc_wfree(c); return NULL; }
+  int *fill = (int *)calloc((size_t)n, sizeof(int));
+  for (int r = 0; r < n_rel; ++r) {
+    c->nbr[xs[r]][fill[xs[r]]++] = ys[r];
+    c->nbr[ys[r]][fill[ys[r]]++] = xs[r];
+  }
+  free(fill);
+  for (int x = 0; x < n; ++x) {
+    qsort(c->nbr[x], (size_t)c->deg[x], sizeof(int), cmp_int);
+    for (int k = 1; k < c->deg[x]; ++k)
+      if (c->nbr[x][k] == c->nbr[x][k - 1]) { orc_wfree(c); return NULL; }
+  }
+  for (int r = 0; r < n_rel; ++r) {
+    int x = xs[r], y = ys[r];
+    int kx = warc_index(c, x, y), ky = warc_index(c, y, x);
+    for (int a = 0; a < row_stride; ++a) {
+      const uint64_t *row = rows + ((size_t)r * (size_t)row_stride + (size_t)a) * (size_t)wq;
+      for (int b = 0; b < 64 * wq; ++b) {
+        if (!wbit(row, b)) continue;
+        if (a >= dom[x] || b >= dom[y]) { orc_wfree(c); return NULL; } /* bits beyond the domains */
+        /* arc x -> y: c_xy|(x,a) = row a; arc y -> x: the transpose */
+        wset(c->sup[x] + ((size_t)kx * dom[x] + a) * wq, b);
+        wset(c->sup[y] + ((size_t)ky * dom[y] + b) * wq, a);
+      }
+    }
+  }
+  return c;
+}
+
+/* The seeded random instance of synth/csp_synth.h, uniform domain d <= 256. */
+orc_wcsp *orc_wbuild_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed) {
+  if (n < 1 || d < 1 || d > 256) return NULL;
+  int *dom = (int *)malloc((size_t)n * sizeof(int));
+  for (int x = 0; x < n; ++x) dom[x] = d;
+  orc_wcsp *c = walloc(n, dom);
+  free(dom);
+  if (!c) return NULL;
+  const int wq = c->wq;
+  for (int x = 0; x < n; ++x)
+    for (int y = x + 1; y < n; ++y)
+      if (synth_present(seed, (uint32_t)n, (uint32_t)x, (uint32_t)y, dens_q32)) { c->deg[x]++; c->deg[y]++; }
+  if (walloc_arcs(c)) { orc_wfree(c); return NULL; }
+  int *fill = (int *)calloc((size_t)n, sizeof(int));
+  for (int x = 0; x < n; ++x)
+    for (int y = 0; y < n; ++y) {
+      if (y == x) continue;
+      int lo = x < y ? x : y, hi = x < y ? y : x;
+      if (synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) c->nbr[x][fill[x]++] = y;
+    }
+  free(fill);
+  for (int x = 0; x < n; ++x)
+    for (int k = 0; k < c->deg[x]; ++k) {
+      int y = c->nbr[x][k];
+      for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) {
+          /* (a,b) in c_xy: for x < y the generator's cell; for x > y the transpose of c_yx */
+          int ok = x < y ? synth_allowed(seed, (uint32_t)n, (uint32_t)d, (uint32_t)x, (uint32_t)y, (uint32_t)a,
+                                         (uint32_t)b, t_q16)
+                         : synth_allowed(seed, (uint32_t)n, (uint32_t)d, (uint32_t)y, (uint32_t)x, (uint32_t)b,
+                                         (uint32_t)a, t_q16);
+          if (ok) wset(c->sup[x] + ((size_t)k * d + a) * wq, b);
+        }
+    }
+  return c;
+}
+
+/* c_xy|(x,a) ∩ D(y) ≠ ∅ over wq words. */
+static int wmeets(const uint64_t *s, const uint64_t *Dy, int wq) {
+  for (int w = 0; w < wq; ++w) if (s[w] & Dy[w]) return 1;
+  return 0;
+}
+
+static int wempty(const uint64_t *v, int wq) {
+  for (int w = 0; w < wq; ++w) if (v[w]) return 0;
+  return 1;
+}
+
+/* O1w: orc_rac with wq-word domains (same loop, same readings R1-R7). */
+int orc_rac_wide(const orc_wcsp *c, const uint64_t *d_in, uint64_t *d_out, int *iterations,
+                 int32_t *removed_at, int full) {
+  const int n = c->n, wq = c->wq;
+  const size_t nw = (size_t)n * wq;
+  uint64_t *prev = (uint64_t *)calloc(nw, sizeof(uint64_t));
+  uint64_t *next = (uint64_t *)calloc(nw, sizeof(uint64_t));
+  memcpy(prev, d_in, nw * sizeof(uint64_t));
+  if (removed_at) memset(removed_at, 0, (size_t)n * 64 * wq * sizeof(int32_t));
+  int k = 0, status = ORC_OK;
+  for (;;) {
+    ++k;
+    memcpy(next, prev, nw * sizeof(uint64_t));
+    for (int x = 0; x < n; ++x)
+      for (int a = 0; a < c->dom[x]; ++a) {
+        if (!wbit(prev + (size_t)x * wq, a)) continue;
+        for (int kk = 0; kk < c->deg[x]; ++kk) {
+          int y = c->nbr[x][kk];
+          const uint64_t *s = c->sup[x] + ((size_t)kk * c->dom[x] + a) * wq; /* c_xy|(x,a) */
+          if (!wmeets(s, prev + (size_t)y * wq, wq)) {                         /* ∩ D_{k-1}(y) = ∅ */
+            next[(size_t)x * wq + (a >> 6)] &= ~(1ULL << (a & 63));
+            if (removed_at) removed_at[(size_t)x * 64 * wq + a] = k;
+            break;
+          }
+        }
+      }
+    int wipe = 0, changed = 0;
+    for (int x = 0; x < n; ++x) {
+      if (wempty(next + (size_t)x * wq, wq)) wipe = 1;
+      for (int w = 0; w < wq; ++w) if (next[(size_t)x * wq + w] != prev[(size_t)x * wq + w]) changed = 1;
+    }
+    memcpy(prev, next, nw * sizeof(uint64_t));
+    if (wipe && !full) { status = ORC_WIPEOUT; break; } /* Alg. 1 */
+    if (!changed) { status = wipe ? ORC_WIPEOUT : ORC_OK; break; }
+  }
+  memcpy(d_out, prev, nw * sizeof(uint64_t));
+  *iterations = k;
+  free(prev); free(next);
+  return status;
+}
+
+/* Arc consistency by definition on wide domains: 1 iff AC and no empty domain. */
+int orc_wis_ac(const orc_wcsp *c, const uint64_t *D) {
+  const int wq = c->wq;
+  for (int x = 0; x < c->n; ++x) {
+    if (wempty(D + (size_t)x * wq, wq)) return 0;
+    for (int a = 0; a < c->dom[x]; ++a) {
+      if (!wbit(D + (size_t)x * wq, a)) continue;
+      for (int k = 0; k < c->deg[x]; ++k)
+        if (!wmeets(c->sup[x] + ((size_t)k * c->dom[x] + a) * wq, D + (size_t)c->nbr[x][k] * wq, wq)) return 0;
+    }
+  }
+  return 1;
+}
+
+/*
+ * Textbook AC-3 on wide domains: a FIFO of arcs (x, y); revising
+ * removes from D(x) every a with c_xy|(x,a) ∩ D(y) = ∅; a change re-queues
+ * every arc (z, x), z ≠ y.  Runs to the fixpoint (FULL semantics).
+ * Returns ORC_WIPEOUT if some domain ends empty.
+ */
+int orc_wac3(const orc_wcsp *c, const uint64_t *d_in, uint64_t *d_out) {
+  const int n = c->n, wq = c->wq;
+  memcpy(d_out, d_in, (size_t)n * wq * sizeof(uint64_t));
+  size_t narcs = 0;
+  for (int x = 0; x < n; ++x) narcs += (size_t)c->deg[x];
+  size_t cap = narcs + 1, head = 0, count = 0;
+  int *qx = (int *)malloc(cap * sizeof(int)), *qk = (int *)malloc(cap * sizeof(int));
+  char *inq = (char *)calloc(cap, 1);
+  size_t *base = (size_t *)calloc((size_t)n + 1, sizeof(size_t));
+  for (int x = 0; x < n; ++x) base[x + 1] = base[x] + (size_t)c->deg[x];
+  for (int x = 0; x < n; ++x)
+    for (int k = 0; k < c->deg[x]; ++k) {
+      qx[(head + count) % cap] = x; qk[(head + count) % cap] = k; ++count;
+      inq[base[x] + k] = 1;
+    }
+  while (count) {
+    int x = qx[head], k = qk[head];
+    head = (head + 1) % cap; --count;
+    inq[base[x] + k] = 0;
+    int y = c->nbr[x][k], changed = 0;
+    for (int a = 0; a < c->dom[x]; ++a) {
+      if (!wbit(d_out + (size_t)x * wq, a)) continue;
+      if (!wmeets(c->sup[x] + ((size_t)k * c->dom[x] + a) * wq, d_out + (size_t)y * wq, wq)) {
+        d_out[(size_t)x * wq + (a >> 6)] &= ~(1ULL << (a & 63));
+        changed = 1;
+      }
+    }
+    if (!changed) continue;
+    for (int j = 0; j < c->deg[x]; ++j) {
+      int z = c->nbr[x][j];
+      if (z == y) continue;
+      int kz = warc_index(c, z, x);
+      if (!inq[base[z] + kz]) {
+        qx[(head + count) % cap] = z; qk[(head + count) % cap] = kz; ++count;
+        inq[base[z] + kz] = 1;
+      }
+    }
+  }
+  free(qx); free(qk); free(inq); free(base);
+  for (int x = 0; x < n; ++x)
+    if (wempty(d_out + (size_t)x * wq, wq)) return ORC_WIPEOUT;
+  return ORC_OK;
+}

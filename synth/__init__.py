@@ -297,3 +297,99 @@ def dive_states(D_root: np.ndarray, enforce: Callable[[np.ndarray], Tuple[int, n
         status, out = enforce(s)
         cur = np.array(D_root if status != 0 else out, dtype=U64, copy=True)
     return (states, seeds) if return_seeds else states
+
+
+# ----------------------------------------------------------------------------- wide domains (NEXT-4)
+# Domains of up to 256 values: a domain state is wq = ceil(dmax/64) uint64
+# words per variable (bit a of x = bit a%64 of word x*wq + a//64), and
+# Instance.rows becomes uint64 [n_rel, max_dom, wq].  Same generator spec as
+# above (synth_allowed has no domain-size limit); input construction only.
+def words_per_var(dmax: int) -> int:
+    return max(1, (int(dmax) + 63) // 64)
+
+
+def wide_from_constraints(n: int, dom, constraints, wq: Optional[int] = None) -> Instance:
+    """Like from_constraints, rows as wq-word bitsets (wq defaults to ceil(max dom / 64))."""
+    if np.isscalar(dom):
+        dom = [int(dom)] * n
+    dom = np.asarray(dom, dtype=np.int32)
+    dmax = int(dom.max()) if n else 1
+    wq = wq or words_per_var(dmax)
+    xs, ys, rows = [], [], []
+    for (x, y, allowed) in constraints:
+        if x > y:
+            x, y = y, x
+            allowed = [(b, a) for (a, b) in allowed]
+        r = np.zeros((dmax, wq), dtype=U64)
+        for (a, b) in allowed:
+            if not (0 <= a < dom[x] and 0 <= b < dom[y]):
+                raise ValueError("value out of range")
+            r[a, b >> 6] |= U64(1) << U64(b & 63)
+        xs.append(x)
+        ys.append(y)
+        rows.append(r)
+    return Instance(n=n, dom=dom, xs=np.asarray(xs, dtype=np.int32), ys=np.asarray(ys, dtype=np.int32),
+                    rows=np.asarray(rows, dtype=U64).reshape(len(rows), dmax, wq))
+
+
+def relation_rows_wide(n: int, d: int, xs, ys, t_q16: int, seed: int) -> np.ndarray:
+    """rows[k, a, w] for pairs (xs[k] < ys[k]): csp_synth.h synth_allowed for any d."""
+    xs = np.asarray(xs, dtype=U64)
+    ys = np.asarray(ys, dtype=U64)
+    q = (d + 3) // 4
+    wq = words_per_var(d)
+    kc = U64(key(seed, TAG_CELL))
+    rows = np.zeros((xs.shape[0], d, wq), dtype=U64)
+    with np.errstate(over="ignore"):
+        pk = mix64(kc ^ mix64(xs * U64(n) + ys))
+        for a in range(d):
+            for bq in range(q):
+                h = mix64(pk + U64(a * q + bq + 1) * U64(GAMMA))
+                for j in range(4):
+                    b = bq * 4 + j
+                    if b >= d:
+                        break
+                    v = (h >> U64(16 * j)) & U64(0xFFFF)
+                    rows[:, a, b >> 6] |= (v >= U64(t_q16)).astype(U64) << U64(b & 63)
+    return rows
+
+
+def random_csp_wide(n: int, d: int, density: float, tightness: float, seed: int) -> Instance:
+    """The seeded random instance of csp_synth.h for 1 <= d <= 256 (rows [n_rel, d, wq])."""
+    if not (1 <= d <= 256):
+        raise ValueError("1 <= d <= 256")
+    dq, tq = quant_density(density), quant_tightness(tightness)
+    xs, ys = present_pairs(n, dq, seed)
+    rows = relation_rows_wide(n, d, xs, ys, tq, seed)
+    return Instance(n=n, dom=np.full(n, d, dtype=np.int32), xs=xs, ys=ys, rows=rows,
+                    gen={"n": n, "d": d, "density": density, "tightness": tightness,
+                         "dens_q32": dq, "t_q16": tq, "seed": seed, "prng": "splitmix64-counter-v1"})
+
+
+def full_domains_wide(dom, wq: Optional[int] = None) -> np.ndarray:
+    """W-root on wide domains: [n * wq] words, every value of dom(x) present."""
+    dom = np.asarray(dom, dtype=np.int64)
+    wq = wq or words_per_var(int(dom.max()) if dom.size else 1)
+    out = np.zeros((dom.shape[0], wq), dtype=U64)
+    for i, k in enumerate(dom):
+        for w in range(wq):
+            bits = min(64, max(0, int(k) - 64 * w))
+            out[i, w] = U64(M64) if bits == 64 else U64((1 << bits) - 1)
+    return out.reshape(-1)
+
+
+def w_rand_wide(dom, keep: float, seed: int, wq: Optional[int] = None) -> np.ndarray:
+    """W-rand on wide domains: value (x,a) kept with probability `keep`, hashed on x*256 + a."""
+    dom = np.asarray(dom, dtype=np.int64)
+    n = dom.shape[0]
+    wq = wq or words_per_var(int(dom.max()) if n else 1)
+    kq = U64(quant_keep(keep))
+    kk = U64(key(seed, TAG_KEEP))
+    out = np.zeros((n, wq), dtype=U64)
+    x = np.arange(n, dtype=U64)
+    with np.errstate(over="ignore"):
+        for a in range(int(dom.max()) if n else 0):
+            h = mix64(kk ^ mix64(x * U64(256) + U64(a)))
+            bit = ((h & U64(0xFFFF)) < kq) & (U64(a) < dom.astype(U64))
+            out[:, a >> 6] |= bit.astype(U64) << U64(a & 63)
+    return out.reshape(-1)

@@ -485,3 +485,151 @@ def test_search_hand_cases():
     free = synth.from_constraints(3, 2, [])
     r, sol, st = oracle.Oracle.from_instance(free).search(free.full_domains())
     assert r == 0 and list(sol) == [0, 0, 0] and st["assignments"] == 3
+
+
+# ----------------------------------------------------------------------------- wide domains (NEXT-4)
+from tests import _wide as WD  # noqa: E402
+
+
+def _narrow_cases():
+    inst = []
+    for i, (n, d, p, t) in enumerate([(12, 20, 0.6, 0.8), (9, 40, 1.0, 0.91), (15, 33, 0.4, 0.88),
+                                      (6, 50, 0.8, 0.93), (10, 7, 0.7, 0.45)]):
+        inst.append(synth.random_csp(n, d, p, t, seed=501 + i))
+    return inst
+
+
+@pytest.mark.parametrize("case", range(5))
+@pytest.mark.parametrize("k", [2, 4, 5])
+@pytest.mark.parametrize("masked", [False, True])
+def test_wide_value_duplication(case, k, masked):
+    """O1w pinned to the (pinned) one-word O1 by value duplication: copy j of
+    value a is value j*d + a and (a', b') is allowed iff (a' mod d, b' mod d) is.
+    Eq. 1's support test depends on D(y) only through the set of values
+    with a live copy, so the wide trajectory projects onto the narrow one run from
+    the projected D_in: same status, same iteration count, a copy removed at
+    epoch t iff its value is removed at t.  `masked` keeps random copies only, so
+    copies of one value sit in different words with different liveness (a test
+    that looked at one word of D(y) would fail)."""
+    narrow = _narrow_cases()[case]
+    if int(narrow.dom.max()) * k > 256:
+        pytest.skip("beyond 256 values")
+    rng = np.random.default_rng(case * 10 + k) if masked else None
+    n = narrow.n
+    d_in_n = synth.w_rand(narrow.dom, 0.9, seed=case + 3)
+    wide = WD.duplicate(narrow, k)
+    d_in_w = WD.duplicate_state(narrow, k, d_in_n, rng)
+    proj = WD.project(narrow, k, d_in_w)
+    for full in (False, True):
+        st_n, out_n, it_n, rem_n = oracle.Oracle.from_instance(narrow).rac(proj, full=full)
+        wo = oracle.WideOracle.from_instance(wide)
+        st_w, out_w, it_w, rem_w = wo.rac(d_in_w, full=full)
+        assert (st_w, it_w) == (st_n, it_n)
+        assert np.array_equal(WD.project(narrow, k, out_w), out_n)
+        win = WD.bits_of(d_in_w, n, wo.wq)
+        wout = WD.bits_of(out_w, n, wo.wq)
+        for x in range(n):
+            dx = int(narrow.dom[x])
+            for ap in range(dx * k):
+                a = ap % dx
+                if win[x, ap]:
+                    assert wout[x, ap] == bool((int(out_n[x]) >> a) & 1)
+                    assert rem_w[x, ap] == rem_n[x, a]
+                else:
+                    assert not wout[x, ap] and rem_w[x, ap] == 0
+
+
+def test_wide_one_word_equals_o1():
+    """With d <= 64 the wide oracle is O1 itself (wq = 1): identical outputs and epochs."""
+    for i, inst in enumerate(I.random_corpus(40, seed0=77, n_range=(2, 14), d_range=(1, 64))):
+        d_in = synth.w_rand(inst.dom, 0.8, seed=i)
+        rows3 = np.asarray(inst.rows, dtype=U64).reshape(inst.n_rel, int(inst.dom.max()), 1)
+        wi = synth.Instance(n=inst.n, dom=inst.dom, xs=inst.xs, ys=inst.ys, rows=rows3)
+        a = oracle.Oracle.from_instance(inst).rac(d_in)
+        b = oracle.WideOracle.from_instance(wi).rac(d_in)
+        assert a[0] == b[0] and a[2] == b[2] and np.array_equal(a[1], b[1]) and np.array_equal(a[3], b[3])
+
+
+def _wide_corpus(count, seed0):
+    rng = np.random.default_rng(seed0)
+    out = []
+    for i in range(count):
+        n = int(rng.integers(2, 12))
+        d = int(rng.integers(65, 257))
+        # tightness 1 - u/d: about u allowed values per row, so the recurrence propagates
+        out.append(synth.random_csp_wide(n, d, float(rng.uniform(0.2, 1.0)), 1.0 - float(rng.uniform(1.0, 4.0)) / d,
+                                         seed=seed0 * 1009 + i))
+    return out
+
+
+def _lemma1_certificate(wo, inst, d_in, d_out, rem):
+    """Lemma 1 (proof P:304-308) for every removal in epoch order:
+    (x,a) removed at epoch t has a declared c_xy whose supports in D_in were all
+    removed before t.  Written here from the definitions (independent of oracle.c)."""
+    n, wq = inst.n, wo.wq
+    win, wout = WD.bits_of(d_in, n, wq), WD.bits_of(d_out, n, wq)
+    arcs = {}
+    for r in range(inst.n_rel):
+        x, y = int(inst.xs[r]), int(inst.ys[r])
+        arcs.setdefault(x, []).append((y, r, False))
+        arcs.setdefault(y, []).append((x, r, True))
+    for x in range(n):
+        for a in range(int(inst.dom[x])):
+            if not win[x, a] or wout[x, a]:
+                continue
+            t = int(rem[x, a])
+            assert t >= 1
+            ok = False
+            for (y, r, rev) in arcs.get(x, []):
+                sup = [b for b in range(int(inst.dom[y]))
+                       if ((int(inst.rows[r, b, a >> 6]) >> (a & 63)) & 1 if rev
+                           else (int(inst.rows[r, a, b >> 6]) >> (b & 63)) & 1) and win[y, b]]
+                if all((not wout[y, b]) and 1 <= int(rem[y, b]) < t for b in sup):
+                    ok = True
+                    break
+            assert ok, (x, a, t)
+
+
+def test_wide_ac3_audit_certificate():
+    """Random wide instances (65..256 values): O1w in FULL mode equals AC-3 at the
+    fixpoint (AC-3 computes D_ac), the output passes the definitional AC
+    audit unless a domain is empty, and every removal carries a Lemma-1
+    certificate -- together D_out = D_ac."""
+    for i, inst in enumerate(_wide_corpus(30, 31)):
+        wo = oracle.WideOracle.from_instance(inst)
+        d_in = synth.w_rand_wide(inst.dom, 0.85, seed=i)
+        st, out, it, rem = wo.rac(d_in, full=True)
+        st3, out3 = wo.ac3(d_in)
+        assert np.array_equal(out, out3) and st == st3
+        if st == oracle.OK:
+            assert wo.is_ac(out)
+        _lemma1_certificate(wo, inst, d_in, out, rem)
+
+
+def test_wide_equality_chain_closed_form():
+    """x_i = x_{i+1} with dom 200 and D_in(x_0) = {150} (word 2 of 4): pass t
+    restricts x_t, so D_ac(x_i) = {150} for all i after n - 1 removing passes plus
+    the final unchanged one (iterations = n; Prop. 1)."""
+    n, d = 9, 200
+    inst = synth.wide_from_constraints(n, d, [(i, i + 1, [(a, a) for a in range(d)]) for i in range(n - 1)])
+    wo = oracle.WideOracle.from_instance(inst)
+    D = WD.bits_of(synth.full_domains_wide(inst.dom), n, wo.wq)
+    D[0, :] = False
+    D[0, 150] = True
+    st, out, it, rem = wo.rac(WD.words_of(D))
+    ob = WD.bits_of(out, n, wo.wq)
+    assert st == oracle.OK and it == n
+    assert all(ob[x].sum() == 1 and ob[x, 150] for x in range(n))
+    for x in range(1, n):
+        assert all(int(rem[x, a]) == x for a in range(d) if a != 150)
+
+
+def test_wide_synth_matches_numpy_generator():
+    """orc_wbuild_synth (C, csp_synth.h) and random_csp_wide (numpy) are the same instance."""
+    for (n, d, p, t, s) in [(14, 100, 0.5, 0.9, 3), (8, 256, 1.0, 0.97, 4), (20, 65, 0.3, 0.8, 5)]:
+        inst = synth.random_csp_wide(n, d, p, t, s)
+        a = oracle.WideOracle.from_instance(inst)
+        b = oracle.WideOracle.from_synth(n, d, synth.quant_density(p), synth.quant_tightness(t), s)
+        d_in = synth.w_rand_wide(inst.dom, 0.9, seed=s)
+        ra, rb = a.rac(d_in, full=True), b.rac(d_in, full=True)
+        assert ra[0] == rb[0] and ra[2] == rb[2] and np.array_equal(ra[1], rb[1])
