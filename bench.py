@@ -61,6 +61,15 @@ WORKLOADS = {
                  "NEXT-3 sparse: n=4000, d=32, density 0.25, tightness 0.72; root enforcement (propagating)"),
     "c4-stream": (8000, 64, 1.0, 0.5, 1, "root",
                   "C4 W-stream: n=8000, d=64, density 1.0, tightness 0.5; root enforcement (32.8 GB of masks)"),
+    "w128-stream": (2000, 128, 1.0, 0.5, 1, "root",
+                    "NEXT-4 wide domains: n=2000, d=128 (2 words per variable), density 1.0, tightness 0.5; root "
+                    "enforcement (1 pass over 8.19 GB of 16-byte masks)"),
+    "w128-prop": (2000, 128, 1.0, 0.93, 1, "root",
+                  "NEXT-4 wide domains: n=2000, d=128, density 1.0, tightness 0.93; root enforcement "
+                  "(propagating: wipeout after 3 passes)"),
+    "w256-stream": (1000, 256, 1.0, 0.5, 1, "root",
+                    "NEXT-4 wide domains: n=1000, d=256 (4 words per variable), density 1.0, tightness 0.5; root "
+                    "enforcement (1 pass over 8.19 GB of 32-byte masks)"),
     "c5-batch": (200, 16, 0.8, 0.3, 1, "dive",
                  "C5: 1024 W-dive states (search-tree nodes) on n=200, d=16, density 0.8, tightness 0.3; "
                  "one batched seeded enforcement per step (each state seeded with its assigned variable)"),
@@ -173,7 +182,7 @@ def run_gpu(args, rank, world, local_rank):
         rdist.connect_peers(ctx)
     torch.cuda.synchronize()
     gen_s = time.time() - t0
-    full = synth.full_domains(np.full(n, d))
+    full = synth.full_domains(np.full(n, d)) if d <= 64 else synth.full_domains_wide(np.full(n, d))
     stream = torch.cuda.current_stream()
 
     # --- D_in
@@ -230,7 +239,7 @@ def run_gpu(args, rank, world, local_rank):
         # (equal to SURVEY §8(d)'s full-check figure for one-pass workloads).
         if rem is not None:
             remd = rem[:, :d]
-            live0 = np.array([[(int(din_h[0][x]) >> a) & 1 for a in range(d)] for x in range(n)], dtype=bool)
+            live0 = _live_bits(din_h[0], n, d)
             if dens >= 1.0:
                 def nbr_count(chg):
                     return chg.sum() - chg.astype(np.int64)
@@ -255,7 +264,7 @@ def run_gpu(args, rank, world, local_rank):
                 alg_bytes += float((lv * nbr_count(chg)).sum()) * d / 8.0
                 chg = (remd == t).any(axis=1)
         else:
-            live_per_pass = [int(sum(bin(int(v)).count("1") for v in din_h[0]))] + [0] * (it - 1)
+            live_per_pass = [int(_live_bits(din_h[0], n, d).sum())] + [0] * (it - 1)
             alg_bytes = live_per_pass[0] * (n - 1) * d / 8.0 if it == 1 else None
         instr["live_rows_per_pass"] = live_per_pass
 
@@ -337,7 +346,8 @@ def run_gpu(args, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             wall_ms = float(t.item())
         e2e = {"value": reps / (wall_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": n * 8 + (4 if kind == "seed" else 0), "d2h_bytes_per_step": n * 8 + 8,
+               "h2d_bytes_per_step": n * ctx.wq * 8 + (4 if kind == "seed" else 0),
+               "d2h_bytes_per_step": n * ctx.wq * 8 + 8,
                "how": ("rac_enforce_seeded" if kind == "seed" else "rac_enforce") + " (host buffers; pinned staging, H2D + enforcement + D2H + sync per call), "
                       "host wall clock over %d calls, max over ranks" % reps}
     else:
@@ -421,7 +431,7 @@ def run_gpu(args, rank, world, local_rank):
     out = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-           "dtype": {1: "u8", 2: "u16", 4: "u32", 8: "u64"}[ctx.mask_bytes] + " bitmasks",
+           "dtype": {1: "u8", 2: "u16", 4: "u32", 8: "u64", 16: "2 x u64", 32: "4 x u64"}[ctx.mask_bytes] + " bitmasks",
            "data": "synthetic (seeded counter-based random CSP, synth/csp_synth.h)", "config": cfg,
            "gpu_launches": int(launches_per_step * args.steps), "clocks": clk, "e2e": e2e,
            "enforcement": instr, "roofline": roofline}
@@ -430,11 +440,44 @@ def run_gpu(args, rank, world, local_rank):
     return out, (n, d, dq, tq, seed, kind, din_h)
 
 
+def _live_bits(D, n, d):
+    """[n, d] bool: value a of x live in the domain state D ([n] or [n * wq] words)."""
+    D = np.asarray(D, dtype=np.uint64)
+    wq = D.size // n
+    W = D.reshape(n, wq)
+    out = np.zeros((n, d), dtype=bool)
+    for a in range(d):
+        out[:, a] = ((W[:, a >> 6] >> np.uint64(a & 63)) & np.uint64(1)).astype(bool)
+    return out
+
+
 # ----------------------------------------------------------------------------- CPU oracle
 def oracle_baseline(n, d, dq, tq, seed, kind, din_h, budget_s=20.0, passes=None):
     """The oracle as it stands (single-threaded C, oracle/oracle.c) on a bounded
     sample of the same workload, on this host."""
     import oracle
+    if d > 64:
+        # Wide domains (NEXT-4): the oracle's build is O(n^2 d^2) generator calls,
+        # so time one Eq. 1 step over the rows of a block of B variables (O1w's
+        # step, orc_wpass_block) and scale by n/B and the pass count.
+        B = max(1, min(n, int(4e6 / (n * d))))
+        t0 = time.time()
+        orc = oracle.WideOracle.from_synth_block(n, d, dq, tq, seed, 0, B)
+        build_s = time.time() - t0
+        reps, t1 = 0, time.perf_counter()
+        while True:
+            orc.pass_block(din_h[0], 0, B)
+            reps += 1
+            el = time.perf_counter() - t1
+            if el > budget_s / 3 or reps >= 20:
+                break
+        t_block = el / reps
+        npass = passes or 1
+        t_enf = t_block * (n / B) * npass
+        return {"value": 1.0 / t_enf, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": "pass over the rows of variables [0,%d) of %d (orc_wpass_block, the O1w step, 1 thread), "
+                          "%d reps, %.4f s each; scaled x n/B = %.1f and x %d pass(es); block build %.1f s excluded"
+                          % (B, n, reps, t_block, n / B, npass, build_s)}
     if kind != "dive" and float(n) * n * d * d / 8 > 2e9:
         # C4-size: the oracle's own instance would not fit / take minutes to build.
         # Sample: arcs of a block of B variables, one Eq. 1 step over its rows,
@@ -484,6 +527,19 @@ def run_reference(args):
     n, d, dens, tight, seed, kind, desc = WORKLOADS[args.workload]
     dq, tq = synth.quant_density(dens), synth.quant_tightness(tight)
     import oracle
+    if d > 64:
+        # Wide domains: the oracle instance is O(n^2 d^2) to build; each step is the
+        # block-sampled O1w estimate of one enforcement (see oracle_baseline).
+        full = synth.full_domains_wide(np.full(n, d))
+        cb = oracle_baseline(n, d, dq, tq, seed, kind, full[None, :], budget_s=min(60.0, 6.0 * max(1, args.steps)))
+        val = cb["value"]
+        return {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u64 bitsets", "data": "synthetic (seeded counter-based random CSP, "
+                "synth/csp_synth.h)", "config": {"workload": args.workload + ": " + desc, "n": n, "d": d,
+                                                 "density": dens, "tightness": tight, "seed": seed},
+                "impl": "reference", "cpu_baseline": cb,
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     if kind == "dive":
         inst = synth.random_csp(n, d, dens, tight, seed)
         orc = oracle.Oracle.from_instance(inst)

@@ -28,7 +28,17 @@
  *   Relation: for a constraint on (x, y), rows[a] (a < dom[x]) is a uint64_t
  *     whose bit b is set iff (a, b) ∈ rel(c_xy); i.e. rows[a] = c_xy|(x,a).
  *     Bits >= dom[y] must be 0.  The (y, x) orientation is derived (transpose).
- *   Domain sizes: 1 <= dom_sizes[x] <= 64 (RAC_MAX_DOM).
+ *   Domain sizes: 1 <= dom_sizes[x] <= 256 (RAC_MAX_DOM_WIDE).
+ *   Wide domains (max dom > 64; SURVEY §8(f) NEXT-4 -- the paper fixes no
+ *   domain-size limit, its Cons is a dense [n,d,n,d] tensor):
+ *     every domain state is wq = ceil(max dom / 64) words per variable
+ *     (rac_words_per_var): bit a of x is bit a%64 of word D[x*wq + a/64]; a
+ *     relation's rows are dom[x] x wq words (row a at rows + a*wq); removal
+ *     epochs are [n_vars * 64 * wq] (x,a) at x*64*wq + a.  With max dom <= 64,
+ *     wq = 1 and every format below is unchanged.  Wide contexts support
+ *     rac_create / rac_create_random / rac_enforce / rac_enforce_ex /
+ *     rac_enforce_async on one GPU (world == 1, dense layout); the seeded,
+ *     batched, search, sharded and peer calls return RAC_EUNSUPPORTED.
  *
  * Return values: every int-returning call returns >= 0 on success (RAC_OK or
  * RAC_WIPEOUT for enforcement calls) and a negative RAC_E* code on error.
@@ -94,7 +104,8 @@ extern "C" {
  * domain of the fixpoint is empty. */
 #define RAC_FULL_FIXPOINT (1u << 0)
 
-#define RAC_MAX_DOM 64
+#define RAC_MAX_DOM 64       /* one-word domains: every call                 */
+#define RAC_MAX_DOM_WIDE 256 /* multi-word domains: see "Wide domains" above */
 #define RAC_NCCL_ID_BYTES 128
 
 typedef struct rac_ctx rac_ctx;
@@ -154,7 +165,7 @@ void rac_default_options(rac_options* opt);
  * Create a context from explicit relations ("Prepare Cons"; Fig. 1).
  * Packs, on the device, every relation into per-(x,a) support masks (both
  * orientations) plus a constraint-presence bitmap.
- * RAC_EINVAL: n_vars < 1; dom size outside [1,64]; x == y or out of range;
+ * RAC_EINVAL: n_vars < 1; dom size outside [1,256]; x == y or out of range;
  * duplicate unordered pair; bits beyond the domain sizes; NULL pointers
  * (rels may be NULL iff n_rel == 0); bad options.
  */
@@ -271,8 +282,12 @@ int rac_search(rac_ctx* ctx, const uint64_t* d_in, int64_t max_assignments, uint
 /* ---- introspection ------------------------------------------------------ */
 int32_t rac_n_vars(const rac_ctx* ctx);
 int32_t rac_max_dom(const rac_ctx* ctx);
-/* Bytes per packed support mask (1, 2, 4 or 8: the smallest width >= max dom bits). */
+/* Bytes per packed support mask (1, 2, 4 or 8: the smallest width >= max dom bits;
+ * 16 or 32 for wide domains: max dom <= 128 or <= 256). */
 int32_t rac_mask_bytes(const rac_ctx* ctx);
+/* Words per variable of every domain state of this context: ceil(max dom / 64)
+ * (1 for max dom <= 64).  RAC_EINVAL if ctx is NULL. */
+int32_t rac_words_per_var(const rac_ctx* ctx);
 /* Bytes of packed support masks held by this rank (rows x row stride). */
 int64_t rac_relation_bytes(const rac_ctx* ctx);
 /* Row block [*x_lo, *x_hi) of variables owned by `rank` of `world` (host only,

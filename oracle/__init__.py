@@ -98,6 +98,11 @@ def _load():
         lib.orc_wbuild_synth.restype = P
         lib.orc_wbuild_synth.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
                                          ctypes.c_uint64]
+        lib.orc_wbuild_synth_block.restype = P
+        lib.orc_wbuild_synth_block.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
+                                               ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
+        lib.orc_wpass_block.restype = ctypes.c_int64
+        lib.orc_wpass_block.argtypes = [P, u64p, ctypes.c_int, ctypes.c_int, u64p]
         lib.orc_wfree.argtypes = [P]
         lib.orc_wfree.restype = None
         lib.orc_wq.argtypes = [P]
@@ -274,6 +279,21 @@ class WideOracle:
         if not h:
             raise ValueError("invalid generator parameters")
         return cls(h, n, np.full(n, d, dtype=np.int32))
+
+    @classmethod
+    def from_synth_block(cls, n: int, d: int, dens_q32: int, t_q16: int, seed: int, x_lo: int, x_hi: int):
+        """Arcs of the variables [x_lo, x_hi) only (sampled CPU timing; pass_block only)."""
+        h = _load().orc_wbuild_synth_block(n, d, dens_q32, t_q16, seed, x_lo, x_hi)
+        if not h:
+            raise ValueError("invalid generator parameters")
+        return cls(h, n, np.full(n, d, dtype=np.int32))
+
+    def pass_block(self, D, x_lo: int, x_hi: int):
+        """One Eq. 1 step over the rows of [x_lo, x_hi).  Returns (out [n*wq], removed)."""
+        D = np.ascontiguousarray(D, dtype=np.uint64).reshape(-1)
+        out = D.copy()
+        r = _load().orc_wpass_block(self._h, _u64p(D), x_lo, x_hi, _u64p(out))
+        return out, int(r)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:

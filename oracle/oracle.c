@@ -786,28 +786,36 @@ orc_wcsp *orc_wbuild(int n, const int *dom, int n_rel, const int *xs, const int 
   return c;
 }
 
-/* The seeded random instance of synth/csp_synth.h, uniform domain d <= 256. */
-orc_wcsp *orc_wbuild_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed) {
-  if (n < 1 || d < 1 || d > 256) return NULL;
+/*
+ * The seeded random instance of synth/csp_synth.h, uniform domain d <= 256,
+ * with arcs only for the variables x in [x_lo, x_hi) (all their neighbours y);
+ * the full instance is x_lo = 0, x_hi = n.  A partial build serves sampled CPU
+ * timing at sizes the full instance does not fit (orc_wpass_block only).
+ */
+orc_wcsp *orc_wbuild_synth_block(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed, int x_lo, int x_hi) {
+  if (n < 1 || d < 1 || d > 256 || x_lo < 0 || x_hi > n || x_lo > x_hi) return NULL;
   int *dom = (int *)malloc((size_t)n * sizeof(int));
   for (int x = 0; x < n; ++x) dom[x] = d;
   orc_wcsp *c = walloc(n, dom);
   free(dom);
   if (!c) return NULL;
   const int wq = c->wq;
-  for (int x = 0; x < n; ++x)
-    for (int y = x + 1; y < n; ++y)
-      if (synth_present(seed, (uint32_t)n, (uint32_t)x, (uint32_t)y, dens_q32)) { c->deg[x]++; c->deg[y]++; }
-  if (walloc_arcs(c)) { orc_wfree(c); return NULL; }
-  int *fill = (int *)calloc((size_t)n, sizeof(int));
-  for (int x = 0; x < n; ++x)
+  for (int x = x_lo; x < x_hi; ++x)
     for (int y = 0; y < n; ++y) {
       if (y == x) continue;
       int lo = x < y ? x : y, hi = x < y ? y : x;
-      if (synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) c->nbr[x][fill[x]++] = y;
+      if (synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) c->deg[x]++;
     }
-  free(fill);
-  for (int x = 0; x < n; ++x)
+  if (walloc_arcs(c)) { orc_wfree(c); return NULL; }
+  for (int x = x_lo; x < x_hi; ++x) {
+    int k = 0;
+    for (int y = 0; y < n; ++y) {
+      if (y == x) continue;
+      int lo = x < y ? x : y, hi = x < y ? y : x;
+      if (synth_present(seed, (uint32_t)n, (uint32_t)lo, (uint32_t)hi, dens_q32)) c->nbr[x][k++] = y;
+    }
+  }
+  for (int x = x_lo; x < x_hi; ++x)
     for (int k = 0; k < c->deg[x]; ++k) {
       int y = c->nbr[x][k];
       for (int a = 0; a < d; ++a)
@@ -821,6 +829,10 @@ orc_wcsp *orc_wbuild_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint
         }
     }
   return c;
+}
+
+orc_wcsp *orc_wbuild_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed) {
+  return orc_wbuild_synth_block(n, d, dens_q32, t_q16, seed, 0, n);
 }
 
 /* c_xy|(x,a) ∩ D(y) ≠ ∅ over wq words. */
@@ -937,4 +949,25 @@ int orc_wac3(const orc_wcsp *c, const uint64_t *d_in, uint64_t *d_out) {
   for (int x = 0; x < n; ++x)
     if (wempty(d_out + (size_t)x * wq, wq)) return ORC_WIPEOUT;
   return ORC_OK;
+}
+
+/* One Eq. 1 step over the rows of x in [x_lo, x_hi) against D:
+ * out[x*wq + w] = D(x) minus the values with an empty support on some c_xy.
+ * Returns the number of values removed. */
+int64_t orc_wpass_block(const orc_wcsp *c, const uint64_t *D, int x_lo, int x_hi, uint64_t *out) {
+  const int wq = c->wq;
+  int64_t removed = 0;
+  for (int x = x_lo; x < x_hi; ++x) {
+    for (int w = 0; w < wq; ++w) out[(size_t)x * wq + w] = D[(size_t)x * wq + w];
+    for (int a = 0; a < c->dom[x]; ++a) {
+      if (!wbit(D + (size_t)x * wq, a)) continue;
+      for (int k = 0; k < c->deg[x]; ++k)
+        if (!wmeets(c->sup[x] + ((size_t)k * c->dom[x] + a) * wq, D + (size_t)c->nbr[x][k] * wq, wq)) {
+          out[(size_t)x * wq + (a >> 6)] &= ~(1ULL << (a & 63));
+          ++removed;
+          break;
+        }
+    }
+  }
+  return removed;
 }

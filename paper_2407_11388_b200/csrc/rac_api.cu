@@ -128,6 +128,15 @@ struct rac_ctx {
   int fused_grid = 0;
   int pass_grid = 0;
   ncclComm_t comm = nullptr;
+  // Wide domains (NEXT-4, rac_wide.cu): dmax > 64.  M / P / dom_d / clist /
+  // staging buffers are shared with the one-word layout's fields.
+  bool wide = false;
+  int wq = 1, WS = 0;       // boundary words per variable, mask words per (x,a,y)
+  uint64_t* wD = nullptr;   // [n*WS] current state
+  uint64_t* wR = nullptr;   // [n*WS] removal bits
+  unsigned* wslots = nullptr;
+  int wide_grid = 0;
+  size_t wide_smem = 0;
   int64_t launches = 0;
   bool broken = false;
   std::string err;
@@ -190,6 +199,9 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->dbg);
   cudaFree(c->bs_dbg);
   cudaFree(c->eval_buf);
+  cudaFree(c->wD);
+  cudaFree(c->wR);
+  cudaFree(c->wslots);
   cudaFreeHost(c->h_in);
   cudaFreeHost(c->h_out);
   cudaFreeHost(c->h_scalars);
@@ -437,18 +449,18 @@ int build_sparse(rac_ctx* c, const std::vector<int32_t>& xs, const std::vector<i
   if (e == cudaSuccess) e = cudaMalloc(&c->s_off, (size_t)(n + 1) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->s_arc, std::max<size_t>(arcs.size(), 1) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->s_ipref, (size_t)(n + 1) * 4);
-  if (e == cudaSuccess) e = cudaMemcpy(c->s_ipref, ipref.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->s_ipref, ipref.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
   if (e == cudaSuccess && np > 0) e = cudaMalloc(&dxs, (size_t)np * 4);
   if (e == cudaSuccess && np > 0) e = cudaMalloc(&dys, (size_t)np * 4);
   if (e == cudaSuccess && np > 0) e = cudaMalloc(&dfwd, (size_t)np * 4);
   if (e == cudaSuccess && np > 0) e = cudaMalloc(&dbwd, (size_t)np * 4);
-  if (e == cudaSuccess) e = cudaMemcpy(c->s_off, c->s_off_h.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && np > 0) e = cudaMemcpy(c->s_arc, c->s_arc_h.data(), arcs.size() * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dxs, xs.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dys, ys.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dfwd, fwd.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && np > 0) e = cudaMemcpy(dbwd, bwd.data(), (size_t)np * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(c->P, pres.data(), pres.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->s_off, c->s_off_h.data(), (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+  if (e == cudaSuccess && np > 0) e = cudaMemcpyAsync(c->s_arc, c->s_arc_h.data(), arcs.size() * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+  if (e == cudaSuccess && np > 0) e = cudaMemcpyAsync(dxs, xs.data(), (size_t)np * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+  if (e == cudaSuccess && np > 0) e = cudaMemcpyAsync(dys, ys.data(), (size_t)np * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+  if (e == cudaSuccess && np > 0) e = cudaMemcpyAsync(dfwd, fwd.data(), (size_t)np * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+  if (e == cudaSuccess && np > 0) e = cudaMemcpyAsync(dbwd, bwd.data(), (size_t)np * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->P, pres.data(), pres.size() * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
   SparsePack g{c->S, c->s_bbytes, c->W, c->dom_d, n};
   if (e == cudaSuccess) e = launch_pack_sparse(g, dxs, dys, drows, row_words, dfwd, dbwd, np, d, t_q16, seed, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
@@ -463,6 +475,98 @@ int build_sparse(rac_ctx* c, const std::vector<int32_t>& xs, const std::vector<i
 }
 
 
+
+// Wide-domain context (NEXT-4): one GPU, dense row-major masks of WS words.
+int setup_wide(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt) {
+  rac_options o;
+  rac_default_options(&o);
+  if (opt) o = *opt;
+  if (o.flags & ~(RAC_OPT_NCCL_SELF | RAC_OPT_PEER | RAC_OPT_SPARSE | RAC_OPT_DENSE))
+    return fail(nullptr, RAC_EINVAL, "unknown options.flags");
+  if (o.world > 1 || o.virtual_shards > 1 || (o.flags & (RAC_OPT_NCCL_SELF | RAC_OPT_PEER | RAC_OPT_SPARSE)))
+    return fail(nullptr, RAC_EUNSUPPORTED, "domains > 64 values: single GPU, dense layout only");
+  if (o.max_ctas < 0) return fail(nullptr, RAC_EINVAL, "max_ctas < 0");
+  if (n > 65535) return fail(nullptr, RAC_EUNSUPPORTED, "n_vars > 65535");
+  c->wide = true;
+  c->device = o.device;
+  c->max_ctas = o.max_ctas;
+  c->n = n;
+  c->dom.assign(dom, dom + n);
+  c->dmax = 0;
+  for (int x = 0; x < n; ++x) c->dmax = std::max(c->dmax, (int)dom[x]);
+  c->wq = (c->dmax + 63) / 64;
+  c->WS = c->dmax <= 128 ? 2 : 4;
+  c->W = c->WS * 8;
+  c->pw = (n + 31) / 32;
+  c->x_lo = 0;
+  c->x_hi = n;
+  c->wide_smem = (size_t)n * c->WS * 8;
+  if (c->wide_smem > 200 * 1024) return fail(nullptr, RAC_EUNSUPPORTED, "n * mask words too large for the smem D");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return fail(nullptr, RAC_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  if (cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess)
+    return fail(nullptr, RAC_ECUDA, "cudaDeviceGetAttribute");
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(nullptr, RAC_ECUDA, "cudaStreamCreate");
+  const size_t mbytes = (size_t)n * c->dmax * n * c->WS * 8;
+  const size_t nw = (size_t)n * c->wq;
+#define CKC(call)                                                                                   \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess)                                                                          \
+      return fail(nullptr, e_ == cudaErrorMemoryAllocation ? RAC_ENOMEM : RAC_ECUDA,                \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                              \
+  } while (0)
+  CKC(cudaMalloc(&c->M, mbytes));
+  CKC(cudaMemsetAsync(c->M, 0xFF, mbytes, c->stream));  // absent pairs / diagonal: all ones, P = 0
+  CKC(cudaMalloc(&c->P, (size_t)n * c->pw * 4));
+  CKC(cudaMemsetAsync(c->P, 0, (size_t)n * c->pw * 4, c->stream));
+  CKC(cudaMalloc(&c->dom_d, (size_t)n * 4));
+  CKC(cudaMemcpyAsync(c->dom_d, dom, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+  CKC(cudaMalloc(&c->wD, (size_t)n * c->WS * 8));
+  CKC(cudaMalloc(&c->wR, (size_t)n * c->WS * 8));
+  CKC(cudaMalloc(&c->wslots, 64));
+  CKC(cudaMalloc(&c->clist, (size_t)3 * n * 4));
+  CKC(cudaMalloc(&c->buf_in, nw * 8));
+  CKC(cudaMalloc(&c->buf_out, nw * 8));
+  CKC(cudaMalloc(&c->buf_scalars, 16));
+  CKC(cudaMalloc(&c->buf_removed, nw * 64 * 4));
+  CKC(cudaMallocHost(&c->h_in, nw * 8));
+  CKC(cudaMallocHost(&c->h_out, nw * 8));
+  CKC(cudaMallocHost(&c->h_scalars, 16));
+  CKC(wide_fused_grid(c->WS, c->wide_smem, c->sm_count, &c->wide_grid));
+  // about four live rows per warp at most: small instances keep fewer CTAs
+  const long rows = (long)n * c->dmax;
+  c->wide_grid = (int)std::max(1L, std::min((long)c->wide_grid, (rows + 16 * 4 - 1) / (16 * 4)));
+  if (c->max_ctas > 0) c->wide_grid = std::min(c->wide_grid, c->max_ctas);
+  CKC(cudaStreamSynchronize(c->stream));
+#undef CKC
+  return 0;
+}
+
+WidePack wide_pack_geom(const rac_ctx* c, uint64_t dens_q32) {
+  return WidePack{reinterpret_cast<uint64_t*>(c->M), c->P, c->dom_d, c->n, c->dmax, c->wq, c->WS, c->pw, dens_q32};
+}
+
+int enforce_wide(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
+                 int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+  WideParams p{reinterpret_cast<const uint64_t*>(c->M), c->P, c->dom_d, c->n, c->dmax, c->wq, c->WS, c->pw,
+               (flags & RAC_FULL_FIXPOINT) ? 1 : 0, d_in, d_out, c->wD, c->wR, c->clist, c->wslots, removed_at,
+               iters, status};
+  CK(c, launch_wide_fused(p, c->wide_grid, c->wide_smem, s));
+  c->launches = 1;
+  return 0;
+}
+
+bool wide_bits_ok(const rac_ctx* c, const uint64_t* D) {
+  for (int x = 0; x < c->n; ++x)
+    for (int w = 0; w < c->wq; ++w) {
+      const int bits = std::min(64, std::max(0, c->dom[x] - 64 * w));
+      const uint64_t dm = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+      if (D[(size_t)x * c->wq + w] & ~dm) return false;
+    }
+  return true;
+}
 
 int check_usable(rac_ctx* c) {
   if (!c) return RAC_EINVAL;
@@ -599,6 +703,10 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
+  if (c->wide) {
+    if (n_seeds >= 0) return fail(c, RAC_EUNSUPPORTED, "seeded calls: domains <= 64 values only");
+    return enforce_wide(c, d_in, d_out, iters, status, removed_at, flags, s);
+  }
   if (c->peer) {
     if (!c->connected) return fail(c, RAC_EINVAL, "RAC_OPT_PEER context: call rac_connect_peers first");
     if (removed_at) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
@@ -615,6 +723,63 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
                        n_seeds >= 0 ? n_seeds : 0);
 }
 
+}  // namespace
+
+namespace {
+// rac_create with max dom > 64: rows of relation r are dom[x] x wq words
+// (wq = ceil(max dom / 64)); validated here, packed on the device.
+int create_wide(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const rac_relation* rels,
+                const rac_options* opt, rac_ctx** out) {
+  int dmax = 0;
+  for (int x = 0; x < n_vars; ++x) dmax = std::max(dmax, (int)dom_sizes[x]);
+  const int wq = (dmax + 63) / 64;
+  std::vector<int32_t> xs(n_rel), ys(n_rel);
+  std::vector<uint64_t> keys(n_rel);
+  std::vector<uint64_t> rows((size_t)std::max(n_rel, 1) * dmax * wq, 0ull);
+  for (int r = 0; r < n_rel; ++r) {
+    const int x = rels[r].x, y = rels[r].y;
+    if (x < 0 || y < 0 || x >= n_vars || y >= n_vars || x == y || !rels[r].rows)
+      return fail(nullptr, RAC_EINVAL, "relation " + std::to_string(r) + ": bad (x, y) or NULL rows");
+    for (int a = 0; a < dom_sizes[x]; ++a)
+      for (int w = 0; w < wq; ++w) {
+        const uint64_t v = rels[r].rows[(size_t)a * wq + w];
+        const int bits = std::min(64, std::max(0, dom_sizes[y] - 64 * w));
+        const uint64_t dm = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+        if (v & ~dm) return fail(nullptr, RAC_EINVAL, "relation " + std::to_string(r) + ": bits beyond dom(y)");
+        rows[((size_t)r * dmax + a) * wq + w] = v;
+      }
+    xs[r] = x;
+    ys[r] = y;
+    keys[r] = ((uint64_t)std::min(x, y) << 32) | (uint64_t)std::max(x, y);
+  }
+  std::sort(keys.begin(), keys.end());
+  if (std::adjacent_find(keys.begin(), keys.end()) != keys.end())
+    return fail(nullptr, RAC_EINVAL, "duplicate constraint on one unordered pair");
+  rac_ctx* c = new rac_ctx();
+  int rc = setup_wide(c, n_vars, dom_sizes, opt);
+  if (rc) { free_ctx(c); return rc; }
+  if (n_rel > 0) {
+    int32_t *dxs = nullptr, *dys = nullptr;
+    uint64_t* drows = nullptr;
+    cudaError_t e = cudaMalloc(&dxs, (size_t)n_rel * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&dys, (size_t)n_rel * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&drows, rows.size() * 8);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dxs, xs.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dys, ys.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+    if (e == cudaSuccess) e = launch_wide_pack(wide_pack_geom(c, 0), dxs, dys, drows, n_rel, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    cudaFree(dxs);
+    cudaFree(dys);
+    cudaFree(drows);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(nullptr, RAC_ECUDA, std::string("packing relations: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = c;
+  return 0;
+}
 }  // namespace
 
 // ----------------------------------------------------------------------------- C ABI
@@ -653,6 +818,7 @@ int rac_peer_handle(const rac_ctx* c, void* out) {
 int rac_connect_peers(rac_ctx* c, const void* handles) {
   int rc = check_usable(c);
   if (rc) return rc;
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
   if (!handles || !c->peer) return fail(c, RAC_EINVAL, "rac_connect_peers needs a RAC_OPT_PEER context and handles");
   if (c->connected) return fail(c, RAC_EINVAL, "peers already connected");
   CK(c, cudaSetDevice(c->device));
@@ -677,6 +843,7 @@ int rac_connect_peers(rac_ctx* c, const void* handles) {
 int rac_connect_peers_local(rac_ctx* c, void* const* regions, const int32_t* devices) {
   int rc = check_usable(c);
   if (rc) return rc;
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
   if (!regions || !devices || !c->peer)
     return fail(c, RAC_EINVAL, "rac_connect_peers_local needs a RAC_OPT_PEER context, regions and devices");
   if (c->connected) return fail(c, RAC_EINVAL, "peers already connected");
@@ -733,9 +900,11 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
   if (n_vars < 1 || !dom_sizes || n_rel < 0 || (n_rel > 0 && !rels))
     return fail(nullptr, RAC_EINVAL, "bad n_vars / dom_sizes / rels");
   for (int x = 0; x < n_vars; ++x)
-    if (dom_sizes[x] < 1 || dom_sizes[x] > RAC_MAX_DOM) return fail(nullptr, RAC_EINVAL, "dom size outside [1,64]");
+    if (dom_sizes[x] < 1 || dom_sizes[x] > RAC_MAX_DOM_WIDE)
+      return fail(nullptr, RAC_EINVAL, "dom size outside [1,256]");
   int dmax = 0;
   for (int x = 0; x < n_vars; ++x) dmax = std::max(dmax, (int)dom_sizes[x]);
+  if (dmax > RAC_MAX_DOM) return create_wide(n_vars, dom_sizes, n_rel, rels, opt, out);
   // validate relations: range, x != y, padding bits, duplicate unordered pairs
   std::vector<uint64_t> keys(n_rel);
   std::vector<int32_t> xs(n_rel), ys(n_rel);
@@ -766,7 +935,7 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
   if (c->sparse) {
     uint64_t* drows = nullptr;
     cudaError_t e = n_rel > 0 ? cudaMalloc(&drows, rows.size() * 8) : cudaSuccess;
-    if (e == cudaSuccess && n_rel > 0) e = cudaMemcpy(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n_rel > 0) e = cudaMemcpyAsync(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
     if (e != cudaSuccess) {
       cudaFree(drows);
       free_ctx(c);
@@ -781,9 +950,9 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
     cudaError_t e = cudaMalloc(&dxs, (size_t)n_rel * 4);
     if (e == cudaSuccess) e = cudaMalloc(&dys, (size_t)n_rel * 4);
     if (e == cudaSuccess) e = cudaMalloc(&drows, rows.size() * 8);
-    if (e == cudaSuccess) e = cudaMemcpy(dxs, xs.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(dys, ys.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dxs, xs.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dys, ys.data(), (size_t)n_rel * 4, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(drows, rows.data(), rows.size() * 8, cudaMemcpyHostToDevice, c->stream);  // stream-ordered (pageable H2D may outlive cudaMemcpy)
     PackGeom g{c->M, c->col_stride, c->Mr, (size_t)c->dbytes, c->W, c->n, c->dmax, c->x_lo, c->x_hi, c->P, c->pw,
                c->dom_d};
     if (e == cudaSuccess) e = launch_pack_relations(g, dxs, dys, drows, n_rel, dmax, c->stream);
@@ -806,9 +975,22 @@ int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q
                       const rac_options* opt, rac_ctx** out) {
   if (!out) return fail(nullptr, RAC_EINVAL, "out is NULL");
   *out = nullptr;
-  if (n_vars < 1 || d < 1 || d > RAC_MAX_DOM || dens_q32 > (1ull << 32) || t_q16 > 65536u)
+  if (n_vars < 1 || d < 1 || d > RAC_MAX_DOM_WIDE || dens_q32 > (1ull << 32) || t_q16 > 65536u)
     return fail(nullptr, RAC_EINVAL, "bad generator parameters");
   std::vector<int32_t> dom(n_vars, d);
+  if (d > RAC_MAX_DOM) {
+    rac_ctx* c = new rac_ctx();
+    int rc = setup_wide(c, n_vars, dom.data(), opt);
+    if (rc) { free_ctx(c); return rc; }
+    cudaError_t e = launch_wide_generate(wide_pack_geom(c, dens_q32), d, t_q16, seed, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      free_ctx(c);
+      return fail(nullptr, RAC_ECUDA, std::string("generating instance: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return 0;
+  }
   rac_ctx* c = new rac_ctx();
   const double est_pairs = (double)dens_q32 / 4294967296.0 * 0.5 * (double)n_vars * (double)(n_vars - 1);
   int rc = setup_ctx(c, n_vars, dom.data(), opt, est_pairs);
@@ -859,10 +1041,11 @@ int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* i
   int rc = check_usable(c);
   if (rc) return rc;
   if (!d_in || !d_out || !iterations) return fail(c, RAC_EINVAL, "NULL pointer");
-  for (int x = 0; x < c->n; ++x)
+  if (c->wide && !wide_bits_ok(c, d_in)) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
+  for (int x = 0; x < c->n && !c->wide; ++x)
     if (d_in[x] & ~c->dommask_h[x]) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
   CK(c, cudaSetDevice(c->device));
-  const size_t nb = (size_t)c->n * 8;
+  const size_t nb = (size_t)c->n * c->wq * 8;
   memcpy(c->h_in, d_in, nb);
   CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb, cudaMemcpyHostToDevice, c->stream));
   rc = enforce_async_impl(c, c->buf_in, c->buf_out, c->buf_scalars, c->buf_scalars + 1,
@@ -871,7 +1054,8 @@ int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* i
   CK(c, cudaMemcpyAsync(c->h_out, c->buf_out, nb, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaMemcpyAsync(c->h_scalars, c->buf_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
   if (removed_at)
-    CK(c, cudaMemcpyAsync(removed_at, c->buf_removed, (size_t)c->n * 64 * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaMemcpyAsync(removed_at, c->buf_removed, (size_t)c->n * 64 * c->wq * 4, cudaMemcpyDeviceToHost,
+                          c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   memcpy(d_out, c->h_out, nb);
   *iterations = c->h_scalars[0];
@@ -900,6 +1084,7 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
                        int32_t n_seeds, uint32_t flags) {
   int rc = check_usable(c);
   if (rc) return rc;
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "seeded calls: domains <= 64 values only");
   if (!d_in || !d_out || !iterations || n_seeds < 0 || (n_seeds > 0 && !seeds))
     return fail(c, RAC_EINVAL, "bad seeded-enforcement arguments");
   for (int i = 0; i < n_seeds; ++i)
@@ -953,6 +1138,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
                       void* stream) {
   int rc = check_usable(c);
   if (rc) return rc;
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
   if (n_states < 0 || (n_states > 0 && (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev)))
     return fail(c, RAC_EINVAL, "bad batch arguments");
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
@@ -1046,6 +1232,7 @@ int rac_batch_pass_eval(rac_ctx* c, int32_t impl, int32_t n_states, const uint64
                         void* stream) {
   int rc = check_usable(c);
   if (rc) return rc;
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
   if (n_states < 1 || !d_in_dev || !d_out_dev || (impl != 0 && impl != 1)) return fail(c, RAC_EINVAL, "bad arguments");
   if (c->use_nccl() || c->x_lo != 0 || c->x_hi != c->n) return fail(c, RAC_EUNSUPPORTED, "single-GPU contexts only");
   if (c->sparse) return fail(c, RAC_EUNSUPPORTED, "batched passes need the dense layout (RAC_OPT_DENSE)");
@@ -1081,6 +1268,7 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
                rac_search_stats* stats) {
   int rc = check_usable(c);
   if (rc) return rc;
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
   if (!d_in) return fail(c, RAC_EINVAL, "d_in is NULL");
   if (flags & ~(RAC_SEARCH_ALL | RAC_FULL_FIXPOINT)) return fail(c, RAC_EINVAL, "unknown flags");
   if (c->use_nccl() || c->vshards > 1) return fail(c, RAC_EUNSUPPORTED, "rac_search runs on fused single-GPU contexts");
@@ -1171,9 +1359,11 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
 int32_t rac_n_vars(const rac_ctx* c) { return c ? c->n : RAC_EINVAL; }
 int32_t rac_max_dom(const rac_ctx* c) { return c ? c->dmax : RAC_EINVAL; }
 int32_t rac_mask_bytes(const rac_ctx* c) { return c ? c->W : RAC_EINVAL; }
+int32_t rac_words_per_var(const rac_ctx* c) { return c ? c->wq : RAC_EINVAL; }
 int64_t rac_relation_bytes(const rac_ctx* c) {
   if (!c) return RAC_EINVAL;
   if (c->sparse) return (int64_t)c->s_nblk * c->s_bbytes;
+  if (c->wide) return (int64_t)c->n * c->dmax * c->n * c->WS * 8;
   return (int64_t)c->n * (int64_t)c->col_stride + (c->Mr ? (int64_t)c->rows_pad * c->dbytes : 0);
 }
 int32_t rac_layout(const rac_ctx* c) { return c ? (c->sparse ? RAC_LAYOUT_SPARSE : RAC_LAYOUT_DENSE) : RAC_EINVAL; }
@@ -1190,6 +1380,7 @@ int rac_read_row(const rac_ctx* cc, int32_t x, int32_t a, uint64_t* out_masks, u
   rac_ctx* c = const_cast<rac_ctx*>(cc);
   int rc = check_usable(c);
   if (rc) return rc;
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
   if (x < c->x_lo || x >= c->x_hi || a < 0 || a >= c->dmax) return fail(c, RAC_EINVAL, "row not local");
   CK(c, cudaSetDevice(c->device));
   if (out_masks && c->sparse) {
@@ -1269,3 +1460,15 @@ const char* rac_last_error(const rac_ctx* c) { return c ? c->err.c_str() : g_cre
 void rac_destroy(rac_ctx* c) { free_ctx(c); }
 
 }  // extern "C"
+
+// Tooling (not part of include/rac.h): copy a wide context's mask tensor and
+// presence bitmap to the host (tools/wide_debug.py).
+extern "C" int rac_debug_wide_dump(rac_ctx* c, uint64_t* M_out, uint32_t* P_out) {
+  if (!c || !c->wide) return RAC_EINVAL;
+  CK(c, cudaSetDevice(c->device));
+  CK(c, cudaStreamSynchronize(c->stream));
+  if (M_out)
+    CK(c, cudaMemcpy(M_out, c->M, (size_t)c->n * c->dmax * c->n * c->WS * 8, cudaMemcpyDeviceToHost));
+  if (P_out) CK(c, cudaMemcpy(P_out, c->P, (size_t)c->n * c->pw * 4, cudaMemcpyDeviceToHost));
+  return 0;
+}

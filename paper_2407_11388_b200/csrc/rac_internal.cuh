@@ -252,6 +252,39 @@ cudaError_t launch_pack_sparse(const SparsePack& g, const int32_t* xs, const int
                                int row_words, const uint32_t* fwd, const uint32_t* bwd, long n_pairs, int d,
                                uint32_t t_q16, uint64_t seed, cudaStream_t s);
 
+// ---------------------------------------------------------------------------- wide domains (rac_wide.cu)
+// NEXT-4: 65..256 values.  Masks WS = 2 or 4 words per (x,a,y), row-major
+// M[((x*dmax + a)*n + y)*WS]; boundary domain states n x wq words, wq = ceil(dmax/64).
+struct WideParams {
+  const uint64_t* M;
+  const uint32_t* P;       // presence bitmap [n][pw]
+  const int32_t* dom;      // device [n]
+  int n, dmax, wq, WS, pw;
+  int full;                // RAC_FULL_FIXPOINT
+  const uint64_t* d_in;    // [n * wq]
+  uint64_t* d_out;         // [n * wq]
+  uint64_t* D;             // [n * WS] current state
+  uint64_t* R;             // [n * WS] removal bits of the pass
+  uint32_t* clist;         // [3][n] change lists
+  unsigned* slots;         // [3][2] {count, wipe}
+  int32_t* removed_at;     // nullable [n * 64 * wq]
+  int32_t* iters;
+  int32_t* status;
+};
+struct WidePack {
+  uint64_t* M;
+  uint32_t* P;
+  const int32_t* dom;      // device [n]
+  int n, dmax, wq, WS, pw;
+  uint64_t dens_q32;
+};
+cudaError_t wide_fused_grid(int WS, size_t smem, int sm_count, int* grid);
+cudaError_t launch_wide_fused(const WideParams& p, int grid, size_t smem, cudaStream_t s);
+// rows: [n_rel][dmax][wq] (row a of rel(c_{xs[r] ys[r]}))
+cudaError_t launch_wide_pack(const WidePack& g, const int32_t* xs, const int32_t* ys, const uint64_t* rows,
+                             int n_rel, cudaStream_t s);
+cudaError_t launch_wide_generate(const WidePack& g, int d, uint32_t t_q16, uint64_t seed, cudaStream_t s);
+
 // ---------------------------------------------------------------------------- device helpers
 #ifdef __CUDACC__
 

@@ -38,6 +38,7 @@ RAC_OPT_DENSE = 8
 RAC_LAYOUT_DENSE = 0
 RAC_LAYOUT_SPARSE = 1
 RAC_MAX_DOM = 64
+RAC_MAX_DOM_WIDE = 256
 RAC_NCCL_ID_BYTES = 128
 RAC_MAX_RANKS = 8
 RAC_IPC_HANDLE_BYTES = 64
@@ -71,7 +72,7 @@ class rac_options(ctypes.Structure):
 # Every symbol include/rac.h declares (checked by tests/test_abi.py).
 EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforce", "rac_enforce_ex",
            "rac_enforce_async", "rac_enforce_batch", "rac_enforce_seeded", "rac_enforce_seeded_async",
-           "rac_enforce_batch_seeded", "rac_search", "rac_batch_pass_eval", "rac_n_vars", "rac_max_dom", "rac_mask_bytes",
+           "rac_enforce_batch_seeded", "rac_search", "rac_batch_pass_eval", "rac_n_vars", "rac_max_dom", "rac_mask_bytes", "rac_words_per_var",
            "rac_layout", "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
            "rac_peer_handle", "rac_connect_peers", "rac_peer_region", "rac_connect_peers_local",
            "rac_last_launch_count", "rac_last_error", "rac_destroy"]
@@ -104,6 +105,7 @@ def _load() -> ctypes.CDLL:
         "rac_n_vars": (i32, [P]),
         "rac_max_dom": (i32, [P]),
         "rac_mask_bytes": (i32, [P]),
+        "rac_words_per_var": (i32, [P]),
         "rac_layout": (i32, [P]),
         "rac_relation_bytes": (i64, [P]),
         "rac_shard_range": (ctypes.c_int, [i32, i32, i32, i32p, i32p]),
@@ -201,6 +203,7 @@ class RacContext:
         self._h = handle
         self.n = n
         self.dmax = dmax
+        self.wq = int(lib.rac_words_per_var(handle))  # words per variable of every domain state
 
     # ---- creation
     @classmethod
@@ -209,7 +212,8 @@ class RacContext:
                nccl_self: bool = False, peer: bool = False, max_ctas: int = 0,
                layout: str = "auto") -> "RacContext":
         """rac_create from relation arrays: constraint k on (xs[k], ys[k]) with
-        rows[k, a] = c_xy|(x,a) bitsets (uint64)."""
+        rows[k, a] = c_xy|(x,a) bitsets (uint64); wide domains (max dom > 64):
+        rows[k, a, w] = word w of the bitset, w < ceil(max dom / 64)."""
         dom = np.ascontiguousarray(dom_sizes, dtype=np.int32)
         xs = np.ascontiguousarray(xs, dtype=np.int32)
         ys = np.ascontiguousarray(ys, dtype=np.int32)
@@ -217,7 +221,7 @@ class RacContext:
         m = xs.shape[0]
         rel = (rac_relation * max(m, 1))()
         if m:
-            stride = rows.shape[1] * 8
+            stride = rows.strides[0]
             base = rows.ctypes.data
             arr = np.frombuffer(rel, dtype=np.dtype([("x", np.int32), ("y", np.int32), ("rows", np.uint64)]),
                                 count=m)
@@ -265,13 +269,14 @@ class RacContext:
     # ---- enforcement
     def enforce(self, d_in, full: bool = False, removed_at: bool = False):
         """rac_enforce / rac_enforce_ex with host buffers.
-        Returns (status, d_out, iterations[, removed_at[n,64]])."""
+        Returns (status, d_out, iterations[, removed_at[n, 64*wq]]); domain states
+        are [n_vars * wq] words (wq = 1 unless the domains are wider than 64)."""
         d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
-        if d_in.shape != (self.n,):
-            raise ValueError("d_in must have shape (n_vars,)")
-        d_out = np.zeros(self.n, dtype=np.uint64)
+        if d_in.shape != (self.n * self.wq,):
+            raise ValueError("d_in must have shape (n_vars * words_per_var,)")
+        d_out = np.zeros(self.n * self.wq, dtype=np.uint64)
         it = ctypes.c_int32(0)
-        rem = np.zeros(self.n * 64, dtype=np.int32) if removed_at else None
+        rem = np.zeros(self.n * 64 * self.wq, dtype=np.int32) if removed_at else None
         if full or removed_at:
             rc = lib.rac_enforce_ex(self._h, _u64p(d_in), _u64p(d_out), ctypes.byref(it),
                                     _i32p(rem) if rem is not None else None, RAC_FULL_FIXPOINT if full else 0)
@@ -279,7 +284,7 @@ class RacContext:
             rc = lib.rac_enforce(self._h, _u64p(d_in), _u64p(d_out), ctypes.byref(it))
         _check(rc, self._h)
         if removed_at:
-            return rc, d_out, it.value, rem.reshape(self.n, 64)
+            return rc, d_out, it.value, rem.reshape(self.n, 64 * self.wq)
         return rc, d_out, it.value
 
     def enforce_seeded(self, d_in, seeds, full: bool = False):

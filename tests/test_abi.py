@@ -61,7 +61,7 @@ def test_create_validation_errors():
         (3, [2, 2, 2], [0], [3], [[1, 2]]),                 # y out of range
         (3, [2, 2, 2], [0], [1], [[4, 2]]),                 # bit 2 beyond dom(y) = 2
         (3, [2, 0, 2], [], [], []),                         # dom size 0
-        (3, [2, 65, 2], [], [], []),                        # dom size > 64
+        (3, [2, 257, 2], [], [], []),                       # dom size > 256 (RAC_MAX_DOM_WIDE)
     ]
     for n, dom, xs, ys, rows in bad:
         rows = np.asarray(rows, dtype=np.uint64).reshape(len(xs), -1) if xs else np.zeros((0, 1), np.uint64)
@@ -75,7 +75,7 @@ def test_create_validation_errors():
 
 def test_create_random_validation():
     h = ctypes.c_void_p()
-    assert rac.lib.rac_create_random(10, 65, 1 << 31, 100, 1, None, ctypes.byref(h)) == rac.RAC_EINVAL
+    assert rac.lib.rac_create_random(10, 257, 1 << 31, 100, 1, None, ctypes.byref(h)) == rac.RAC_EINVAL
     assert rac.lib.rac_create_random(10, 8, (1 << 32) + 1, 100, 1, None, ctypes.byref(h)) == rac.RAC_EINVAL
     assert rac.lib.rac_create_random(10, 8, 1 << 31, 65537, 1, None, ctypes.byref(h)) == rac.RAC_EINVAL
     assert rac.lib.rac_create_random(0, 8, 1 << 31, 100, 1, None, ctypes.byref(h)) == rac.RAC_EINVAL

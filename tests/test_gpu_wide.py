@@ -1,0 +1,184 @@
+"""GPU parity for wide domains (65..256 values per
+variable): the CUDA path (rac_wide.cu through the C ABI) against the wide
+oracle O1w (oracle.WideOracle, pinned in tests/test_oracle.py) on the same
+seeded inputs.  Integer work: status, D_out, iteration count and removal
+epochs must be bit-exact.  Expected values come only from oracle/."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests import _wide as WD
+from tests.test_oracle import _narrow_cases, _wide_corpus
+
+pytestmark = pytest.mark.gpu
+
+U64 = np.uint64
+
+
+@pytest.fixture(scope="module")
+def rac():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2407_11388_b200 import rac as r
+    return r
+
+
+def same(ctx, wo, d_in, full=False, what=""):
+    g = ctx.enforce(d_in, full=full, removed_at=True)
+    o = wo.rac(d_in, full=full)
+    assert g[0] == o[0], (what, "status", g[0], o[0])
+    assert g[2] == o[2], (what, "iterations", g[2], o[2])
+    assert np.array_equal(g[1], o[1]), (what, "d_out")
+    assert np.array_equal(g[3], o[3]), (what, "removed_at")
+    return g
+
+
+def test_wide_corpus(rac):
+    """Random wide instances (65..256 values, density 0.2..1, propagating
+    tightness), W-root and W-rand, stop and FULL modes."""
+    for i, inst in enumerate(_wide_corpus(40, 91)):
+        ctx = rac.RacContext.from_instance(inst)
+        wo = oracle.WideOracle.from_instance(inst)
+        assert ctx.wq == wo.wq == synth.words_per_var(int(inst.dom.max()))
+        for d_in in (synth.full_domains_wide(inst.dom), synth.w_rand_wide(inst.dom, 0.8, seed=i)):
+            for full in (False, True):
+                same(ctx, wo, d_in, full, "corpus %d" % i)
+
+
+def test_wide_nonuniform_domains(rac):
+    """Domain sizes mixed across the one-word boundary (1..256 in one instance)."""
+    rng = np.random.default_rng(5)
+    for i in range(12):
+        n = int(rng.integers(3, 40))
+        dom = rng.integers(1, 257, size=n)
+        dom[int(rng.integers(n))] = int(rng.integers(65, 257))  # at least one wide domain
+        cons = []
+        for x in range(n):
+            for y in range(x + 1, n):
+                if rng.random() < 0.5:
+                    p = min(1.0, 3.0 / max(1, int(dom[y])))
+                    allowed = [(a, b) for a in range(int(dom[x])) for b in np.nonzero(rng.random(int(dom[y])) < p)[0]]
+                    cons.append((x, y, allowed))
+        inst = synth.wide_from_constraints(n, dom.astype(np.int32), cons)
+        ctx = rac.RacContext.from_instance(inst)
+        wo = oracle.WideOracle.from_instance(inst)
+        for d_in in (synth.full_domains_wide(inst.dom), synth.w_rand_wide(inst.dom, 0.7, seed=i)):
+            same(ctx, wo, d_in, False, "nonuniform %d" % i)
+            same(ctx, wo, d_in, True, "nonuniform %d full" % i)
+
+
+@pytest.mark.parametrize("k", [2, 4, 5])
+def test_wide_duplication(rac, k):
+    """Value-duplicated instances (tests/_wide.py) with random copy masks."""
+    for case, narrow in enumerate(_narrow_cases()):
+        if int(narrow.dom.max()) * k > 256 or int(narrow.dom.max()) * k <= 64:
+            continue
+        wide = WD.duplicate(narrow, k)
+        ctx = rac.RacContext.from_instance(wide)
+        wo = oracle.WideOracle.from_instance(wide)
+        d_in = WD.duplicate_state(narrow, k, synth.w_rand(narrow.dom, 0.9, seed=case),
+                                  np.random.default_rng(case))
+        same(ctx, wo, d_in, False, "dup %d" % case)
+        same(ctx, wo, d_in, True, "dup %d full" % case)
+
+
+def test_wide_equality_chain(rac):
+    n, d = 300, 200
+    inst = synth.wide_from_constraints(n, d, [(i, i + 1, [(a, a) for a in range(d)]) for i in range(n - 1)])
+    ctx = rac.RacContext.from_instance(inst)
+    wo = oracle.WideOracle.from_instance(inst)
+    D = WD.bits_of(synth.full_domains_wide(inst.dom), n, wo.wq)
+    D[0, :] = False
+    D[0, 150] = True
+    g = same(ctx, wo, WD.words_of(D), False, "chain")
+    assert g[0] == rac.RAC_OK and g[2] == n
+
+
+def test_wide_edge_cases(rac):
+    """Empty D_in row (reading R7: one pass, then WIPEOUT), all-empty D_in, no
+    constraints, a single variable, d_in bits beyond the domains rejected."""
+    inst = _wide_corpus(3, 17)[0]
+    ctx = rac.RacContext.from_instance(inst)
+    wo = oracle.WideOracle.from_instance(inst)
+    d_in = synth.full_domains_wide(inst.dom).reshape(inst.n, -1)
+    d_in[1, :] = 0
+    g = same(ctx, wo, d_in.reshape(-1), False, "empty row")
+    assert g[0] == rac.RAC_WIPEOUT and g[2] == 1
+    same(ctx, wo, d_in.reshape(-1), True, "empty row full")
+    same(ctx, wo, np.zeros_like(d_in).reshape(-1), False, "all empty")
+    free = synth.wide_from_constraints(5, 130, [])
+    cf, of = rac.RacContext.from_instance(free), oracle.WideOracle.from_instance(free)
+    g = same(cf, of, synth.full_domains_wide(free.dom), False, "no constraints")
+    assert g[0] == rac.RAC_OK and g[2] == 1
+    one = synth.wide_from_constraints(1, 256, [])
+    same(rac.RacContext.from_instance(one), oracle.WideOracle.from_instance(one),
+         synth.full_domains_wide(one.dom), False, "n=1")
+    bad = synth.full_domains_wide(free.dom).reshape(5, -1)
+    bad[0, -1] |= U64(1) << U64(63)  # value 191 of a 130-value domain
+    with pytest.raises(rac.RacError) as ei:
+        cf.enforce(bad.reshape(-1))
+    assert ei.value.code == rac.RAC_EINVAL
+    with pytest.raises(rac.RacError) as ei:
+        cf.enforce_seeded(synth.full_domains_wide(free.dom), [0])
+    assert ei.value.code == rac.RAC_EUNSUPPORTED
+
+
+@pytest.mark.parametrize("n,d,t", [(200, 128, 0.97), (120, 256, 0.985), (150, 100, 0.96), (90, 192, 0.98)])
+def test_wide_generator(rac, n, d, t):
+    """rac_create_random (device generator + packer) against the oracle's own
+    build of the same seeded instance; W-root and W-rand, stop and FULL."""
+    dq, tq = synth.quant_density(1.0 if d != 100 else 0.5), synth.quant_tightness(t)
+    ctx = rac.RacContext.create_random(n, d, dq, tq, 7)
+    wo = oracle.WideOracle.from_synth(n, d, dq, tq, 7)
+    dom = np.full(n, d)
+    for d_in in (synth.full_domains_wide(dom), synth.w_rand_wide(dom, 0.9, seed=3)):
+        for full in (False, True):
+            same(ctx, wo, d_in, full, "gen n=%d d=%d" % (n, d))
+
+
+def _sample_supported(n, d, dq, tq, seed, x, a, Dbits):
+    """Straight from the numpy generator: is (x,a) supported on every declared
+    c_xy against D?  (one step of Eq. 1 for one row)."""
+    px, py = synth.present_pairs(n, dq, seed)
+    sel = (px == x) | (py == x)
+    lo, hi = px[sel], py[sel]
+    rows = synth.relation_rows_wide(n, d, lo, hi, tq, seed)  # [pairs, d, wq] of c_{lo hi}
+    for k in range(lo.shape[0]):
+        if int(lo[k]) == x:   # c_xy is the pair's own orientation: row a
+            y = int(hi[k])
+            sup = [b for b in range(d) if (int(rows[k, a, b >> 6]) >> (b & 63)) & 1]
+        else:                 # c_xy = transpose of c_yx: column a
+            y = int(lo[k])
+            sup = [b for b in range(d) if (int(rows[k, b, a >> 6]) >> (a & 63)) & 1]
+        if not any(Dbits[y, b] for b in sup):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("n,d", [(2000, 128), (1000, 256)])
+def test_wide_bench_size_stream(rac, n, d):
+    """The bench's W-stream configurations at full size, in the bench's launch
+    configuration: every row supported -> one pass, D_out = D_in (checked on
+    sampled rows straight from the generator), status OK."""
+    import torch
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.5)
+    ctx = rac.RacContext.create_random(n, d, dq, tq, 1)
+    full = synth.full_domains_wide(np.full(n, d))
+    dev = torch.device("cuda", 0)
+    din = torch.from_numpy(full.view(np.int64).copy()).to(dev)
+    dout = torch.zeros_like(din)
+    its = torch.zeros(1, dtype=torch.int32, device=dev)
+    sts = torch.zeros(1, dtype=torch.int32, device=dev)
+    ctx.enforce_async(din, dout, its, sts)
+    torch.cuda.synchronize()
+    out = dout.cpu().numpy().view(np.uint64)
+    assert int(sts.item()) == rac.RAC_OK and int(its.item()) == 1
+    assert np.array_equal(out, full)
+    Dbits = WD.bits_of(full, n, ctx.wq)
+    rng = np.random.default_rng(0)
+    for _ in range(3):
+        x, a = int(rng.integers(n)), int(rng.integers(d))
+        assert _sample_supported(n, d, dq, tq, 1, x, a, Dbits)

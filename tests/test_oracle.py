@@ -633,3 +633,20 @@ def test_wide_synth_matches_numpy_generator():
         d_in = synth.w_rand_wide(inst.dom, 0.9, seed=s)
         ra, rb = a.rac(d_in, full=True), b.rac(d_in, full=True)
         assert ra[0] == rb[0] and ra[2] == rb[2] and np.array_equal(ra[1], rb[1])
+
+
+def test_wide_pass_block_matches_o1w():
+    """orc_wpass_block over every row block equals the first step of O1w (the
+    removal epochs equal to 1), and the block build agrees with the full build."""
+    n, d, dq, tq, seed = 24, 130, synth.quant_density(0.7), synth.quant_tightness(0.975), 9
+    full = oracle.WideOracle.from_synth(n, d, dq, tq, seed)
+    D = synth.w_rand_wide(np.full(n, d), 0.8, seed=1)
+    st, out, it, rem = full.rac(D, full=True)
+    exp = WD.bits_of(D, n, full.wq) & ~(rem == 1)
+    got = np.zeros_like(exp)
+    for lo in range(0, n, 5):
+        hi = min(n, lo + 5)
+        blk = oracle.WideOracle.from_synth_block(n, d, dq, tq, seed, lo, hi)
+        o, _ = blk.pass_block(D, lo, hi)
+        got[lo:hi] = WD.bits_of(o, n, full.wq)[lo:hi]
+    assert np.array_equal(got, exp)
