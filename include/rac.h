@@ -37,8 +37,9 @@
  *     epochs are [n_vars * 64 * wq] (x,a) at x*64*wq + a.  With max dom <= 64,
  *     wq = 1 and every format below is unchanged.  Wide contexts support
  *     rac_create / rac_create_random / rac_enforce / rac_enforce_ex /
- *     rac_enforce_async on one GPU (world == 1, dense layout); the seeded,
- *     batched, search, sharded and peer calls return RAC_EUNSUPPORTED.
+ *     rac_enforce_async / rac_enforce_seeded / rac_enforce_seeded_async on
+ *     one GPU (world == 1, dense layout); the batched, search, sharded and
+ *     peer calls return RAC_EUNSUPPORTED.
  *
  * Return values: every int-returning call returns >= 0 on success (RAC_OK or
  * RAC_WIPEOUT for enforcement calls) and a negative RAC_E* code on error.

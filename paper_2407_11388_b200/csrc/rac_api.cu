@@ -549,10 +549,11 @@ WidePack wide_pack_geom(const rac_ctx* c, uint64_t dens_q32) {
 }
 
 int enforce_wide(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
-                 int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+                 int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
+                 int n_seeds = -1) {
   WideParams p{reinterpret_cast<const uint64_t*>(c->M), c->P, c->dom_d, c->n, c->dmax, c->wq, c->WS, c->pw,
                (flags & RAC_FULL_FIXPOINT) ? 1 : 0, d_in, d_out, c->wD, c->wR, c->clist, c->wslots, removed_at,
-               iters, status};
+               iters, status, seeds, n_seeds};
   CK(c, launch_wide_fused(p, c->wide_grid, c->wide_smem, s));
   c->launches = 1;
   return 0;
@@ -703,10 +704,7 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
-  if (c->wide) {
-    if (n_seeds >= 0) return fail(c, RAC_EUNSUPPORTED, "seeded calls: domains <= 64 values only");
-    return enforce_wide(c, d_in, d_out, iters, status, removed_at, flags, s);
-  }
+  if (c->wide) return enforce_wide(c, d_in, d_out, iters, status, removed_at, flags, s, seeds, n_seeds);
   if (c->peer) {
     if (!c->connected) return fail(c, RAC_EINVAL, "RAC_OPT_PEER context: call rac_connect_peers first");
     if (removed_at) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
@@ -818,7 +816,7 @@ int rac_peer_handle(const rac_ctx* c, void* out) {
 int rac_connect_peers(rac_ctx* c, const void* handles) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (!handles || !c->peer) return fail(c, RAC_EINVAL, "rac_connect_peers needs a RAC_OPT_PEER context and handles");
   if (c->connected) return fail(c, RAC_EINVAL, "peers already connected");
   CK(c, cudaSetDevice(c->device));
@@ -843,7 +841,7 @@ int rac_connect_peers(rac_ctx* c, const void* handles) {
 int rac_connect_peers_local(rac_ctx* c, void* const* regions, const int32_t* devices) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (!regions || !devices || !c->peer)
     return fail(c, RAC_EINVAL, "rac_connect_peers_local needs a RAC_OPT_PEER context, regions and devices");
   if (c->connected) return fail(c, RAC_EINVAL, "peers already connected");
@@ -1084,15 +1082,15 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
                        int32_t n_seeds, uint32_t flags) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "seeded calls: domains <= 64 values only");
   if (!d_in || !d_out || !iterations || n_seeds < 0 || (n_seeds > 0 && !seeds))
     return fail(c, RAC_EINVAL, "bad seeded-enforcement arguments");
   for (int i = 0; i < n_seeds; ++i)
     if (seeds[i] < 0 || seeds[i] >= c->n) return fail(c, RAC_EINVAL, "seed out of range");
-  for (int x = 0; x < c->n; ++x)
+  if (c->wide && !wide_bits_ok(c, d_in)) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
+  for (int x = 0; x < c->n && !c->wide; ++x)
     if (d_in[x] & ~c->dommask_h[x]) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
   CK(c, cudaSetDevice(c->device));
-  const size_t nb = (size_t)c->n * 8;
+  const size_t nb = (size_t)c->n * c->wq * 8;
   if ((size_t)n_seeds > c->seed_cap) {
     cudaFree(c->buf_seeds);
     c->buf_seeds = nullptr;
@@ -1138,7 +1136,7 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
                       void* stream) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (n_states < 0 || (n_states > 0 && (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev)))
     return fail(c, RAC_EINVAL, "bad batch arguments");
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
@@ -1232,7 +1230,7 @@ int rac_batch_pass_eval(rac_ctx* c, int32_t impl, int32_t n_states, const uint64
                         void* stream) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (n_states < 1 || !d_in_dev || !d_out_dev || (impl != 0 && impl != 1)) return fail(c, RAC_EINVAL, "bad arguments");
   if (c->use_nccl() || c->x_lo != 0 || c->x_hi != c->n) return fail(c, RAC_EUNSUPPORTED, "single-GPU contexts only");
   if (c->sparse) return fail(c, RAC_EUNSUPPORTED, "batched passes need the dense layout (RAC_OPT_DENSE)");
@@ -1268,7 +1266,7 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
                rac_search_stats* stats) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (!d_in) return fail(c, RAC_EINVAL, "d_in is NULL");
   if (flags & ~(RAC_SEARCH_ALL | RAC_FULL_FIXPOINT)) return fail(c, RAC_EINVAL, "unknown flags");
   if (c->use_nccl() || c->vshards > 1) return fail(c, RAC_EUNSUPPORTED, "rac_search runs on fused single-GPU contexts");
@@ -1380,7 +1378,7 @@ int rac_read_row(const rac_ctx* cc, int32_t x, int32_t a, uint64_t* out_masks, u
   rac_ctx* c = const_cast<rac_ctx*>(cc);
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce / rac_enforce_ex / rac_enforce_async only");
+  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (x < c->x_lo || x >= c->x_hi || a < 0 || a >= c->dmax) return fail(c, RAC_EINVAL, "row not local");
   CK(c, cudaSetDevice(c->device));
   if (out_masks && c->sparse) {

@@ -270,6 +270,8 @@ struct WideParams {
   int32_t* removed_at;     // nullable [n * 64 * wq]
   int32_t* iters;
   int32_t* status;
+  const int32_t* seeds;    // device [n_seeds], each in [0, n) (seeded calls)
+  int n_seeds;             // -1: unseeded (pass 1 tests every column)
 };
 struct WidePack {
   uint64_t* M;

@@ -105,7 +105,21 @@ __global__ void __launch_bounds__(kWideThreads) wide_fused(WideParams p) {
   int status = RAC_OK;
   const uint32_t* cols = nullptr;  // nullptr: every column (pass 1)
   unsigned ncols = (unsigned)n;
-  for (;;) {
+  if (p.n_seeds >= 0) {  // seeded call: pass 1 tests Cons[:, seeds] (Alg. 1 @changed = seeds)
+    cols = reinterpret_cast<const uint32_t*>(p.seeds);  // duplicates re-test a column: same result
+    ncols = (unsigned)p.n_seeds;
+  }
+  if (p.n_seeds == 0) {  // empty @changed: no pass, status from D_in (include/rac.h)
+    for (size_t x = gtid; x < (size_t)n; x += gthreads) {
+      uint64_t v = 0;
+#pragma unroll
+      for (int w = 0; w < WS; ++w) v |= p.D[x * WS + w];
+      if (!v) atomicOr(&slots[0].wipe, 1u);
+    }
+    grid.sync();
+    status = *((volatile unsigned*)&slots[0].wipe) ? RAC_WIPEOUT : RAC_OK;
+  }
+  for (; p.n_seeds != 0;) {
     ++pass;
     const int s = pass % 3;
     for (int i = tid; i < n * WS; i += blockDim.x) sD[i] = __ldcg(p.D + i);  // L2: written by other SMs

@@ -290,9 +290,11 @@ class RacContext:
     def enforce_seeded(self, d_in, seeds, full: bool = False):
         """rac_enforce_seeded (Alg. 1 tensorAC(Vars, @changed = seeds)), host buffers.
         Returns (status, d_out, iterations)."""
-        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
+        if d_in.shape != (self.n * self.wq,):
+            raise ValueError("d_in must have shape (n_vars * words_per_var,)")
         seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.int32).reshape(-1))
-        d_out = np.zeros(self.n, dtype=np.uint64)
+        d_out = np.zeros(self.n * self.wq, dtype=np.uint64)
         it = ctypes.c_int32(0)
         rc = lib.rac_enforce_seeded(self._h, _u64p(d_in), _u64p(d_out), ctypes.byref(it),
                                     _i32p(seeds) if seeds.size else None, int(seeds.size),

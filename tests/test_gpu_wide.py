@@ -122,8 +122,63 @@ def test_wide_edge_cases(rac):
         cf.enforce(bad.reshape(-1))
     assert ei.value.code == rac.RAC_EINVAL
     with pytest.raises(rac.RacError) as ei:
-        cf.enforce_seeded(synth.full_domains_wide(free.dom), [0])
+        cf.search(synth.full_domains_wide(free.dom))
     assert ei.value.code == rac.RAC_EUNSUPPORTED
+    with pytest.raises(rac.RacError) as ei:
+        cf.enforce_seeded(bad.reshape(-1), [0])
+    assert ei.value.code == rac.RAC_EINVAL
+
+
+def _assignments(ctx, wo, n, wq, d_ac, rng, count):
+    """Alg. 2's per-assignment call on a wide context: from
+    the arc-consistent D_ac, x := a (D(x) = {a}), then tensorAC(Vars, [x]).  By
+    Prop. 2 the seeded result equals the full enforcement of the
+    assigned state, which the oracle computes from scratch."""
+    bits = WD.bits_of(d_ac, n, wq)
+    xs = [x for x in range(n) if bits[x].sum() >= 2]
+    for _ in range(min(count, len(xs))):
+        x = int(rng.choice(xs))
+        a = int(rng.choice(np.flatnonzero(bits[x])))
+        b2 = bits.copy()
+        b2[x, :] = False
+        b2[x, a] = True
+        d_in = WD.words_of(b2)
+        o = wo.rac(d_in)
+        for seeds in ([x], [x, x]):
+            g = ctx.enforce_seeded(d_in, seeds)
+            assert g[0] == o[0], ("status", x, a, g[0], o[0])
+            assert g[2] == o[2], ("iterations", x, a, g[2], o[2])
+            assert np.array_equal(g[1], o[1]), ("d_out", x, a)
+
+
+def test_wide_seeded(rac):
+    """Seeded wide enforcement (NEXT-1 on NEXT-4 contexts) against O1w on the
+    assigned state, on corpus instances and a generator instance; an empty
+    seed list is no pass (iterations 0, D_out = D_in, status from emptiness)."""
+    rng = np.random.default_rng(23)
+    cases = [(inst, rac.RacContext.from_instance(inst), oracle.WideOracle.from_instance(inst))
+             for inst in _wide_corpus(20, 57)]
+    checked = 0
+    for inst, ctx, wo in cases:
+        st, d_ac, _, _ = wo.rac(synth.full_domains_wide(inst.dom))
+        if st != rac.RAC_OK:
+            continue
+        _assignments(ctx, wo, inst.n, wo.wq, d_ac, rng, 4)
+        checked += 1
+        g = ctx.enforce_seeded(d_ac, [])
+        assert g[0] == rac.RAC_OK and g[2] == 0 and np.array_equal(g[1], d_ac)
+        e = d_ac.reshape(inst.n, -1).copy()
+        e[0, :] = 0
+        g = ctx.enforce_seeded(e.reshape(-1), [])
+        assert g[0] == rac.RAC_WIPEOUT and g[2] == 0
+    assert checked >= 5
+    n, d = 200, 128  # t = 0.93: root D_ac is OK after 5 passes (0.94 wipes out)
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.93)
+    ctx = rac.RacContext.create_random(n, d, dq, tq, 7)
+    wo = oracle.WideOracle.from_synth(n, d, dq, tq, 7)
+    st, d_ac, _, _ = wo.rac(synth.full_domains_wide(np.full(n, d)))
+    assert st == rac.RAC_OK
+    _assignments(ctx, wo, n, wo.wq, d_ac, rng, 6)
 
 
 @pytest.mark.parametrize("n,d,t", [(200, 128, 0.97), (120, 256, 0.985), (150, 100, 0.96), (90, 192, 0.98)])
