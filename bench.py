@@ -235,8 +235,14 @@ def run_gpu(args, rank, world, local_rank):
         # Algorithmic bytes of Alg. 1: pass t tests every live (x,a)
         # against the constraints c_xy with y changed in pass t-1 (all y in
         # pass 1 of a root call; the seed variables in pass 1 of a seeded call):
-        #   bytes_t = Σ_x |D_{t-1}(x)| · |{y ∈ C_x : y ∈ changed_{t-1}}| · d / 8
-        # (equal to SURVEY §8(d)'s full-check figure for one-pass workloads).
+        #   full_t = Σ_x |D_{t-1}(x)| · |{y ∈ C_x : y ∈ changed_{t-1}}| · d / 8
+        # (SURVEY §8(d)'s full-check figure).  The roofline charges the bytes a
+        # correct pass MUST read: a row kept by pass t reads every tested mask
+        # (any unread one could be the empty support set), a row removed at t
+        # needs only its witness (Lemma 1: one mask, d/8 bytes).  Both
+        # kernels stop reading a row at its first failed test, so the full figure
+        # over-counts removal passes (w128-prop: 18.3 GB full, 12.7 GB DRAM read).
+        # One-pass workloads remove nothing: both figures are the same.
         if rem is not None:
             remd = rem[:, :d]
             live0 = _live_bits(din_h[0], n, d)
@@ -256,13 +262,18 @@ def run_gpu(args, rank, world, local_rank):
                 chg[seed_vars] = True
             else:
                 chg[:] = True
-            live_per_pass, alg_bytes = [], 0.0
+            live_per_pass, alg_bytes, full_bytes = [], 0.0, 0.0
             for t in range(1, it + 1):
                 alive = live0 & ((remd == 0) | (remd >= t))
+                gone = live0 & (remd == t)
                 lv = alive.sum(axis=1)
+                nb = nbr_count(chg)
                 live_per_pass.append(int(lv.sum()))
-                alg_bytes += float((lv * nbr_count(chg)).sum()) * d / 8.0
+                full_bytes += float((lv * nb).sum()) * d / 8.0
+                alg_bytes += (float(((lv - gone.sum(axis=1)) * nb).sum()) +
+                              float((gone.sum(axis=1) * (nb > 0)).sum())) * d / 8.0
                 chg = (remd == t).any(axis=1)
+            instr["full_test_bytes"] = full_bytes
         else:
             live_per_pass = [int(_live_bits(din_h[0], n, d).sum())] + [0] * (it - 1)
             alg_bytes = live_per_pass[0] * (n - 1) * d / 8.0 if it == 1 else None
@@ -412,8 +423,10 @@ def run_gpu(args, rank, world, local_rank):
                 traffic = None
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(achieved / peak, 4), "traffic": traffic,
-                    "kernel": "rac_fused" if (world == 1 or peer) else "rac_pass (+ allgather)",
+                    "kernel": ("wide_fused" if d > 64 else "rac_fused") if (world == 1 or peer)
+                              else "rac_pass (+ allgather)",
                     "algorithmic_bytes_per_launch": alg_bytes,
+                    "algorithmic_bytes_rule": "kept rows: every tested mask; removed rows: one witness mask",
                     "launch_ms_median": round(kern_ms, 5),
                     "peak_source": peak_src + ("" if world == 1 else "; per-GPU bytes = total / N")}
         if world > 1:
