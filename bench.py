@@ -90,6 +90,25 @@ def measured_peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+def pass_bytes(live0, remd, iters, nbr_count, chg, d):
+    """Per-enforcement byte counts from the removal epochs (see the comment at
+    the call site).  live0: [n, d] bool live rows of D_in; remd: [n, d] epoch
+    of each removal (0 = kept); chg: [n] bool variables tested in pass 1;
+    nbr_count(chg) -> [n] count of declared c_xy with y in chg.  Returns
+    (live rows per pass, must-read bytes, full-check bytes)."""
+    live_per_pass, alg, full = [], 0.0, 0.0
+    for t in range(1, iters + 1):
+        alive = live0 & ((remd == 0) | (remd >= t))
+        gone = (live0 & (remd == t)).sum(axis=1)
+        lv = alive.sum(axis=1)
+        nb = nbr_count(chg)
+        live_per_pass.append(int(lv.sum()))
+        full += float((lv * nb).sum()) * d / 8.0
+        alg += (float(((lv - gone) * nb).sum()) + float((gone * (nb > 0)).sum())) * d / 8.0
+        chg = (remd == t).any(axis=1)
+    return live_per_pass, alg, full
+
+
 def algorithmic_bytes(n, d, density_present_deg, live_per_pass):
     """Σ_t Σ_x |D_{t-1}(x)| · Σ_{y∈C_x} d_y / 8; uniform d."""
     return sum(live * deg * d for live, deg in zip(live_per_pass, density_present_deg)) / 8.0
@@ -262,17 +281,7 @@ def run_gpu(args, rank, world, local_rank):
                 chg[seed_vars] = True
             else:
                 chg[:] = True
-            live_per_pass, alg_bytes, full_bytes = [], 0.0, 0.0
-            for t in range(1, it + 1):
-                alive = live0 & ((remd == 0) | (remd >= t))
-                gone = live0 & (remd == t)
-                lv = alive.sum(axis=1)
-                nb = nbr_count(chg)
-                live_per_pass.append(int(lv.sum()))
-                full_bytes += float((lv * nb).sum()) * d / 8.0
-                alg_bytes += (float(((lv - gone.sum(axis=1)) * nb).sum()) +
-                              float((gone.sum(axis=1) * (nb > 0)).sum())) * d / 8.0
-                chg = (remd == t).any(axis=1)
+            live_per_pass, alg_bytes, full_bytes = pass_bytes(live0, remd, it, nbr_count, chg, d)
             instr["full_test_bytes"] = full_bytes
         else:
             live_per_pass = [int(_live_bits(din_h[0], n, d).sum())] + [0] * (it - 1)
