@@ -19,7 +19,9 @@
 // by the previous pass afterwards (Alg. 1's Cons[:, @changed], Prop. 2) -- four
 // 16-byte loads in flight per lane, AND with D(y) from smem; a zero result on
 // a declared pair is a failure (warp vote, early exit) and sets the row's
-// removal bit R[x][a] (a4).  Grid barrier; one thread per variable applies
+// removal bit R[x][a] (a4).  A pass with at most kThreadRowCols tested
+// columns (a seeded pass 1, a late pass) gives each thread a row instead, so
+// rows are not serialised behind 31 idle lanes.  Grid barrier; one thread per variable applies
 // D_t = D_{t-1} & ~R, appends changed variables to the next column list,
 // records removal epochs, raises the wipeout flag (a5); grid barrier; every
 // thread reads the same flags and takes the same stop decision.
@@ -35,6 +37,7 @@ namespace rac {
 namespace {
 
 constexpr int kWideThreads = 512;
+constexpr unsigned kThreadRowCols = 8;  // tested columns at or below which a thread takes a row
 
 struct WideSlot {
   unsigned cnt;   // variables changed by the pass (length of the slot's column list)
@@ -127,6 +130,23 @@ __global__ void __launch_bounds__(kWideThreads) wide_fused(WideParams p) {
 
     // ---- a3/a4: support tests of the live rows against the tested columns
     const size_t rows = (size_t)n * dmax;
+    // Few tested columns (a seeded pass 1, a late pass): a thread per row, so the
+    // 31 idle lanes of the warp-per-row loop do not serialise the rows.
+    if (ncols <= kThreadRowCols) {
+      for (size_t r = gtid; r < rows; r += gthreads) {
+        const int x = (int)(r / dmax), a = (int)(r % dmax);
+        if (!((sD[(size_t)x * WS + (a >> 6)] >> (a & 63)) & 1ull)) continue;  // dead row
+        const uint64_t* row = p.M + r * (size_t)n * WS;
+        bool failed = false;
+        for (unsigned i = 0; i < ncols && !failed; ++i) {
+          const int y = cols ? (int)__ldcg(cols + i) : (int)i;
+          const Mask<WS> m = load_mask<WS>(row + (size_t)y * WS);
+          failed = !meets<WS>(m, sD + (size_t)y * WS) && present(p.P, p.pw, x, y);
+        }
+        if (failed) atomicOr(reinterpret_cast<unsigned long long*>(p.R) + (size_t)x * WS + (a >> 6),
+                             1ull << (a & 63));
+      }
+    } else
     for (size_t r = gwarp; r < rows; r += nwarps) {
       const int x = (int)(r / dmax), a = (int)(r % dmax);
       if (!((sD[(size_t)x * WS + (a >> 6)] >> (a & 63)) & 1ull)) continue;  // dead row
