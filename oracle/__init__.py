@@ -42,13 +42,34 @@ WIPEOUT = 1
 _lib = None
 
 
+_CFLAGS = ["-O2", "-std=c11", "-shared", "-fPIC", "-Wall", "-fopenmp"]
+
+
+def _source_hash() -> str:
+    """sha256 of the sources and flags; a library with another stamp is rebuilt
+    (file times are not trusted: the tree is copied between machines)."""
+    import hashlib
+    h = hashlib.sha256()
+    for p in (_SRC, os.path.join(_HERE, "..", "synth", "csp_synth.h")):
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(_CFLAGS).encode())
+    return h.hexdigest()
+
+
 def build(force: bool = False) -> str:
-    """Compile oracle.c -> liboracle.so with gcc (plain C, -O2, no SIMD intrinsics)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "..", "synth", "csp_synth.h"))):
+    """Compile oracle.c -> liboracle.so with gcc (plain C, -O2, no SIMD
+    intrinsics; OpenMP only for the independent per-variable loops of the
+    certificate and of the all-core timing leg)."""
+    stamp = _LIB + ".srchash"
+    want = _source_hash()
+    have = open(stamp).read().strip() if os.path.exists(stamp) else ""
+    if force or not os.path.exists(_LIB) or have != want:
         tmp = _LIB + ".tmp.%d" % os.getpid()
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", *_CFLAGS, "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
+        with open(stamp, "w") as f:
+            f.write(want + "\n")
     return _LIB
 
 
@@ -91,8 +112,14 @@ def _load():
                                               ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
         lib.orc_pass_block.restype = ctypes.c_int64
         lib.orc_pass_block.argtypes = [P, u64p, ctypes.c_int, ctypes.c_int, u64p]
-        lib.orc_domain_size.argtypes = [P, u64p]
-        lib.orc_domain_size.restype = ctypes.c_int64
+        lib.orc_certify_trajectory.argtypes = [P, u64p, u64p, i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.orc_certify_trajectory.restype = ctypes.c_int
+        lib.orc_wcertify_trajectory.argtypes = [P, u64p, u64p, i32p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+        lib.orc_wcertify_trajectory.restype = ctypes.c_int
+        lib.orc_certify_trajectory_synth.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
+                                                     ctypes.c_uint64, u64p, u64p, i32p, ctypes.c_int, ctypes.c_int,
+                                                     ctypes.c_int, ctypes.c_int]
+        lib.orc_certify_trajectory_synth.restype = ctypes.c_int
         lib.orc_wbuild.restype = P
         lib.orc_wbuild.argtypes = [ctypes.c_int, i32p, ctypes.c_int, i32p, i32p, u64p, ctypes.c_int]
         lib.orc_wbuild_synth.restype = P
@@ -236,6 +263,16 @@ class Oracle:
         rem = np.ascontiguousarray(np.asarray(removed_at, dtype=np.int32).reshape(-1))
         return int(_load().orc_certify(self._h, _u64p(d_in), _u64p(d_out), _i32p(rem), 1 if check_ac else 0))
 
+    def certify_trajectory(self, d_in, d_out, removed_at, iterations: int, status: int, full: bool = False) -> int:
+        """O7: 0 iff (status, d_out, iterations, removed_at) is exactly the RAC
+        recurrence's output on d_in (see oracle.c); else a reason code."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        d_out = np.ascontiguousarray(d_out, dtype=np.uint64)
+        rem = np.ascontiguousarray(np.asarray(removed_at, dtype=np.int32).reshape(-1))
+        assert rem.size == self.n * 64
+        return int(_load().orc_certify_trajectory(self._h, _u64p(d_in), _u64p(d_out), _i32p(rem), int(iterations),
+                                                  int(status), 1 if full else 0))
+
     def support(self, x: int, y: int, a: int) -> Tuple[bool, int]:
         p = ctypes.c_int32(0)
         s = _load().orc_support(self._h, x, y, a, ctypes.byref(p))
@@ -316,12 +353,36 @@ class WideOracle:
         D = np.ascontiguousarray(D, dtype=np.uint64).reshape(-1)
         return bool(_load().orc_wis_ac(self._h, _u64p(D)))
 
+    def certify_trajectory(self, d_in, d_out, removed_at, iterations: int, status: int, full: bool = False) -> int:
+        """O7 on wide domains: 0 iff the claim is exactly the recurrence's output."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
+        d_out = np.ascontiguousarray(d_out, dtype=np.uint64).reshape(-1)
+        rem = np.ascontiguousarray(np.asarray(removed_at, dtype=np.int32).reshape(-1))
+        assert rem.size == self.n * 64 * self.wq and d_in.size == self.n * self.wq
+        return int(_load().orc_wcertify_trajectory(self._h, _u64p(d_in), _u64p(d_out), _i32p(rem), int(iterations),
+                                                   int(status), 1 if full else 0))
+
     def ac3(self, d_in):
         """AC-3 to the fixpoint on wide domains.  Returns (status, d_out)."""
         d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
         d_out = np.zeros(self.n * self.wq, dtype=np.uint64)
         st = _load().orc_wac3(self._h, _u64p(d_in), _u64p(d_out))
         return st, d_out
+
+
+def certify_trajectory_synth(n: int, d: int, dens_q32: int, t_q16: int, seed: int, d_in, d_out, removed_at,
+                             iterations: int, status: int, full: bool = False, threads: int = 0) -> int:
+    """O7 on the seeded random instance (d <= 256), regenerating the support sets
+    of one variable at a time from synth/csp_synth.h (C4 / wide bench sizes).
+    Domain states [n * ceil(d/64)] words, epochs [n, 64 * ceil(d/64)]."""
+    wq = (d + 63) // 64
+    d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
+    d_out = np.ascontiguousarray(d_out, dtype=np.uint64).reshape(-1)
+    rem = np.ascontiguousarray(np.asarray(removed_at, dtype=np.int32).reshape(-1))
+    assert d_in.size == n * wq and d_out.size == n * wq and rem.size == n * 64 * wq
+    return int(_load().orc_certify_trajectory_synth(n, d, dens_q32, t_q16, seed, _u64p(d_in), _u64p(d_out),
+                                                    _i32p(rem), int(iterations), int(status), 1 if full else 0,
+                                                    int(threads)))
 
 
 def row_supported_synth(n: int, d: int, dens_q32: int, t_q16: int, seed: int, x: int, a: int, D) -> bool:

@@ -52,6 +52,10 @@
 
 #include "../synth/csp_synth.h"
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 #define ORC_OK 0
 #define ORC_WIPEOUT 1
 #define ORC_EINVAL (-1)
@@ -662,12 +666,6 @@ int orc_row_supported_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uin
   return 1;
 }
 
-/* Number of live values, summed (|D|). */
-int64_t orc_domain_size(const orc_csp *c, const uint64_t *D) {
-  int64_t s = 0;
-  for (int x = 0; x < c->n; ++x) s += popc64(D[x] & dom_mask(c->dom[x]));
-  return s;
-}
 
 /* ======================================================================== */
 /*
@@ -970,4 +968,276 @@ int64_t orc_wpass_block(const orc_wcsp *c, const uint64_t *D, int x_lo, int x_hi
     }
   }
   return removed;
+}
+
+/* ======================================================================== */
+/*
+ * O7: exact-trajectory certificate.  Given D_in, the
+ * claimed output D_out, the claimed removal epochs eps(x,a) (0 = kept), the
+ * claimed iteration count K and status, accept iff they are exactly what the
+ * RAC recurrence (Eq. 1, with Alg. 1's loop control,
+ * lines 198-210, readings R1-R7) produces -- without running the recurrence.
+ *
+ * The epochs define the claimed trajectory
+ *     D_s = { (y,b) in D_in : eps(y,b) = 0 or eps(y,b) > s },   s = 0..K
+ * (D_0 = D_in).  Eq. 1 removes (x,a) at pass t iff (x,a) in D_{t-1} and some
+ * declared c_xy in C_x has c_xy|(x,a) ∩ D_{t-1}(y) = ∅ (R1, R2).  So the claim is
+ * the recurrence's iff, for every (x,a) in D_in:
+ *   removed at e >= 1:  (L1) some declared c_xy has c_xy|(x,a) ∩ D_{e-1}(y) = ∅
+ *                            -- the Eq. 1 removal test at pass e; this is
+ *                            Lemma 1 (lines 79-82): all supports were removed
+ *                            before e;
+ *                       (P2) if e >= 2, every declared c_xy has
+ *                            c_xy|(x,a) ∩ D_{e-2}(y) ≠ ∅ -- (x,a) survived pass
+ *                            e-1, so it is removed exactly at e (Prop. 2, lines
+ *                            130-143: removals at step e are caused by removals
+ *                            at step e-1);
+ *   kept:               (AC) every declared c_xy has c_xy|(x,a) ∩ D_{K-1}(y) ≠ ∅
+ *                            (it survives the last pass; D is monotone, so
+ *                            every earlier pass too);
+ * and the loop control matches Alg. 1 (R3, R5):
+ *   every pass t < K removed something (otherwise the loop ends at t);
+ *   status OK:        D_K has no empty domain and pass K removed nothing
+ *                     (Prop. 1 end condition, line 125: D_K is arc consistent);
+ *   status WIPEOUT, stop mode: D_K has an empty domain and D_{K-1} has none
+ *                     unless K = 1 (an empty domain in D_in: one pass, R7);
+ *   status WIPEOUT, full mode: pass K removed nothing and D_K has an empty domain.
+ * Also D_out = D_K, epochs lie in [1, K] exactly on D_in \ D_out, D_out ⊆ D_in.
+ * By induction on t the set {eps = t} is determined by {eps < t}, so exactly
+ * one claim passes: the recurrence's own trajectory.
+ *
+ * Layout of the checks: for each y the level bitsets E[y][s] = D_s(y) (wq words
+ * each).  Domain states are wq words per variable (wq = 1: the one-word layout);
+ * epochs removed_at[x*64*wq + a].
+ *
+ * Return codes: 0 accepted; 2 D_out ⊄ D_in or bits beyond dom; 3 epochs
+ * inconsistent with D_in / D_out / K; 5 (L1) fails: a removal without an empty
+ * support set at its pass; 6 (P2) fails: the value should have gone one pass
+ * earlier; 7 (AC) fails: a kept value without support in D_{K-1}; 8 loop
+ * control (K, status) inconsistent; -1 bad arguments / out of memory.
+ */
+static int cert_word_bit(const uint64_t *v, int b) { return (int)((v[b >> 6] >> (b & 63)) & 1ULL); }
+
+/* Global part: epochs against D_in / D_out / K, the level bitsets E, and the
+ * loop-control rules.  E = [n][K+1][wq], allocated here. */
+static int cert_global(int n, const int *dom, int wq, const uint64_t *d_in, const uint64_t *d_out,
+                       const int32_t *eps, int K, int status, int full, uint64_t **E_out) {
+  *E_out = NULL;
+  if (K < 0 || (status != ORC_OK && status != ORC_WIPEOUT)) return 8;
+  const size_t nw = (size_t)n * wq;
+  for (size_t i = 0; i < nw; ++i)
+    if (d_out[i] & ~d_in[i]) return 2;
+  for (int x = 0; x < n; ++x)
+    for (int b = 0; b < 64 * wq; ++b) {
+      const int in = cert_word_bit(d_in + (size_t)x * wq, b), out = cert_word_bit(d_out + (size_t)x * wq, b);
+      const int32_t e = eps[(size_t)x * 64 * wq + b];
+      if (b >= dom[x] && (in || e != 0)) return 2;
+      if (in && !out) { if (e < 1 || e > K) return 3; }
+      else if (e != 0) return 3;
+    }
+  if (K == 0) return 8; /* every enforcement runs at least one pass (R3) */
+  uint64_t *E = (uint64_t *)calloc((size_t)n * (size_t)(K + 1) * wq, sizeof(uint64_t));
+  if (!E) return -1;
+  int *removed_at_t = (int *)calloc((size_t)K + 2, sizeof(int)); /* number of values with eps = t */
+  int *empty_at_s = (int *)calloc((size_t)K + 1, sizeof(int));   /* D_s has an empty domain */
+  if (!removed_at_t || !empty_at_s) { free(E); free(removed_at_t); free(empty_at_s); return -1; }
+  for (int y = 0; y < n; ++y)
+    for (int b = 0; b < dom[y]; ++b) {
+      if (!cert_word_bit(d_in + (size_t)y * wq, b)) continue;
+      const int32_t e = eps[(size_t)y * 64 * wq + b];
+      if (e > 0) removed_at_t[e]++;
+      for (int s = 0; s <= K; ++s)
+        if (e == 0 || e > s) E[((size_t)y * (K + 1) + s) * wq + (b >> 6)] |= 1ULL << (b & 63);
+    }
+  for (int s = 0; s <= K; ++s)
+    for (int y = 0; y < n; ++y) {
+      int any = 0;
+      for (int w = 0; w < wq; ++w) any |= E[((size_t)y * (K + 1) + s) * wq + w] != 0;
+      if (!any) { empty_at_s[s] = 1; break; }
+    }
+  int bad = 0;
+  for (int t = 1; t < K; ++t)
+    if (removed_at_t[t] == 0) bad = 1; /* the loop would have ended at t */
+  if (status == ORC_OK) {
+    if (empty_at_s[K] || removed_at_t[K] != 0) bad = 1;
+  } else if (!full) {
+    if (!empty_at_s[K] || (K > 1 && empty_at_s[K - 1])) bad = 1;
+  } else {
+    if (!empty_at_s[K] || removed_at_t[K] != 0) bad = 1;
+  }
+  free(removed_at_t);
+  free(empty_at_s);
+  if (bad) { free(E); return 8; }
+  *E_out = E;
+  return 0;
+}
+
+/* c_xy|(x,a) ∩ D_s(y) ≠ ∅ for the wq-word support set `sup`. */
+static int cert_meets(const uint64_t *sup, const uint64_t *E, int y, int K, int s, int wq) {
+  const uint64_t *Ds = E + ((size_t)y * (K + 1) + s) * wq;
+  for (int w = 0; w < wq; ++w)
+    if (sup[w] & Ds[w]) return 1;
+  return 0;
+}
+
+/* Per-variable part: every (x,a) in D_in against the (L1), (P2), (AC) rules.
+ * nbr[k] (k < deg) are the constrained neighbours of x, sup[((size_t)k*dom_x +
+ * a)*wq + w] the support sets c_{x,nbr[k]}|(x,a). */
+static int cert_var(int x, int dom_x, int deg, const int *nbr, const uint64_t *sup, int wq, const uint64_t *E,
+                    const uint64_t *d_in, const int32_t *eps, int K) {
+  for (int a = 0; a < dom_x; ++a) {
+    if (!cert_word_bit(d_in + (size_t)x * wq, a)) continue;
+    const int32_t e = eps[(size_t)x * 64 * wq + a];
+    if (e == 0) { /* kept: supported in D_{K-1} on every declared constraint */
+      for (int k = 0; k < deg; ++k)
+        if (!cert_meets(sup + ((size_t)k * dom_x + a) * wq, E, nbr[k], K, K - 1, wq)) return 7;
+    } else {
+      int l1 = 0;
+      for (int k = 0; k < deg; ++k) {
+        const uint64_t *s = sup + ((size_t)k * dom_x + a) * wq;
+        if (!cert_meets(s, E, nbr[k], K, e - 1, wq)) l1 = 1;                 /* (L1) */
+        if (e >= 2 && !cert_meets(s, E, nbr[k], K, e - 2, wq)) return 6;      /* (P2) */
+      }
+      if (!l1) return 5;
+    }
+  }
+  return 0;
+}
+
+int orc_certify_trajectory(const orc_csp *c, const uint64_t *d_in, const uint64_t *d_out, const int32_t *removed_at,
+                           int iterations, int status, int full) {
+  uint64_t *E = NULL;
+  int rc = cert_global(c->n, c->dom, 1, d_in, d_out, removed_at, iterations, status, full, &E);
+  if (rc) return rc;
+  for (int x = 0; x < c->n && rc == 0; ++x)
+    rc = cert_var(x, c->dom[x], c->deg[x], c->nbr[x], c->sup[x], 1, E, d_in, removed_at, iterations);
+  free(E);
+  return rc;
+}
+
+int orc_wcertify_trajectory(const orc_wcsp *c, const uint64_t *d_in, const uint64_t *d_out,
+                            const int32_t *removed_at, int iterations, int status, int full) {
+  uint64_t *E = NULL;
+  int rc = cert_global(c->n, c->dom, c->wq, d_in, d_out, removed_at, iterations, status, full, &E);
+  if (rc) return rc;
+  for (int x = 0; x < c->n && rc == 0; ++x)
+    rc = cert_var(x, c->dom[x], c->deg[x], c->nbr[x], c->sup[x], c->wq, E, d_in, removed_at, iterations);
+  free(E);
+  return rc;
+}
+
+/*
+ * The same certificate for the seeded random instance of synth/csp_synth.h
+ * (uniform d <= 256) at sizes where the oracle's instance does not fit in host
+ * memory (C4: 32.8 GB of support sets).  Each constrained pair {x < y} is
+ * regenerated once from the generator as its d x d cell matrix; its rows are the
+ * support sets c_xy|(x,a) and its columns the c_yx|(y,b).  The per-value rules
+ * are OR-reductions over the constraints, so every pair contributes flags
+ *   F_L1 : this constraint has c|(x,a) ∩ D_{e-1}(y) = ∅         (wanted for e >= 1)
+ *   F_P2 : this constraint has c|(x,a) ∩ D_{e-2}(y) = ∅         (forbidden for e >= 2)
+ *   F_AC : this constraint has c|(x,a) ∩ D_{K-1}(y) = ∅         (forbidden for kept)
+ * to both endpoints; the rules are checked once all pairs are in (the same
+ * rules as cert_var).  Pairs are spread over `threads` OpenMP threads (0 = all)
+ * with per-thread flag arrays OR-ed together, so the verdict does not depend on
+ * the thread count.
+ */
+#define CERT_F_L1 1
+#define CERT_F_P2 2
+#define CERT_F_AC 4
+
+static void cert_pair_side(const uint64_t *rowsup /* [d][wq] supports of the side's values */, int x, int y, int d,
+                           int wq, const uint64_t *E, const uint64_t *d_in, const int32_t *eps, int K,
+                           uint8_t *flags /* [n][64*wq] */) {
+  for (int a = 0; a < d; ++a) {
+    if (!cert_word_bit(d_in + (size_t)x * wq, a)) continue;
+    const int32_t e = eps[(size_t)x * 64 * wq + a];
+    const uint64_t *sp = rowsup + (size_t)a * wq;
+    uint8_t f = 0;
+    if (e == 0) {
+      if (!cert_meets(sp, E, y, K, K - 1, wq)) f |= CERT_F_AC;
+    } else {
+      if (!cert_meets(sp, E, y, K, e - 1, wq)) f |= CERT_F_L1;
+      if (e >= 2 && !cert_meets(sp, E, y, K, e - 2, wq)) f |= CERT_F_P2;
+    }
+    flags[(size_t)x * 64 * wq + a] |= f;
+  }
+}
+
+int orc_certify_trajectory_synth(int n, int d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed,
+                                 const uint64_t *d_in, const uint64_t *d_out, const int32_t *removed_at,
+                                 int iterations, int status, int full, int threads) {
+  if (n < 1 || d < 1 || d > 256) return -1;
+  const int wq = (d + 63) / 64, K = iterations;
+  int *dom = (int *)malloc((size_t)n * sizeof(int));
+  if (!dom) return -1;
+  for (int x = 0; x < n; ++x) dom[x] = d;
+  uint64_t *E = NULL;
+  int rc = cert_global(n, dom, wq, d_in, d_out, removed_at, iterations, status, full, &E);
+  free(dom);
+  if (rc) return rc;
+  const size_t nv = (size_t)n * 64 * wq;
+  uint8_t *flags = (uint8_t *)calloc(nv, 1);
+  if (!flags) { free(E); return -1; }
+  const int q = (d + 3) / 4;
+  int oom = 0;
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel
+#endif
+  {
+    uint8_t *fl = (uint8_t *)calloc(nv, 1);               /* this thread's flags */
+    uint64_t *fw = (uint64_t *)malloc((size_t)d * wq * 8); /* fw[a] = c_xy|(x,a) (rows)    */
+    uint64_t *bw = (uint64_t *)malloc((size_t)d * wq * 8); /* bw[b] = c_yx|(y,b) (columns) */
+    const int ok = fl && fw && bw;
+#ifdef _OPENMP
+#pragma omp for schedule(dynamic, 4)
+#endif
+    for (int x = 0; x < n; ++x) {
+      if (!ok) continue;
+      for (int y = x + 1; y < n; ++y) {
+        if (!synth_present(seed, (uint32_t)n, (uint32_t)x, (uint32_t)y, dens_q32)) continue;
+        memset(fw, 0, (size_t)d * wq * 8);
+        memset(bw, 0, (size_t)d * wq * 8);
+        const uint64_t pk = synth_pair_key(seed, (uint32_t)n, (uint32_t)x, (uint32_t)y);
+        for (int a = 0; a < d; ++a)
+          for (int bq = 0; bq < q; ++bq) {
+            const uint64_t h = synth_cell_word_pk(pk, (uint32_t)d, (uint32_t)a, (uint32_t)bq);
+            for (int j = 0; j < 4 && 4 * bq + j < d; ++j) {
+              const int b = 4 * bq + j;
+              const uint64_t allowed = ((h >> (16 * j)) & 0xFFFFULL) >= t_q16; /* (a,b) in rel(c_xy) */
+              fw[(size_t)a * wq + (b >> 6)] |= allowed << (b & 63);
+              bw[(size_t)b * wq + (a >> 6)] |= allowed << (a & 63);
+            }
+          }
+        cert_pair_side(fw, x, y, d, wq, E, d_in, removed_at, K, fl);
+        cert_pair_side(bw, y, x, d, wq, E, d_in, removed_at, K, fl);
+      }
+    }
+#ifdef _OPENMP
+#pragma omp critical
+#endif
+    {
+      if (!ok) oom = 1;
+      else
+        for (size_t i = 0; i < nv; ++i) flags[i] |= fl[i];
+    }
+    free(fl);
+    free(fw);
+    free(bw);
+  }
+  free(E);
+  if (oom) { free(flags); return -1; }
+  /* the per-value rules of cert_var, in the same order of precedence */
+  int err = 0;
+  for (int x = 0; x < n && !err; ++x)
+    for (int a = 0; a < d && !err; ++a) {
+      if (!cert_word_bit(d_in + (size_t)x * wq, a)) continue;
+      const int32_t e = removed_at[(size_t)x * 64 * wq + a];
+      const uint8_t f = flags[(size_t)x * 64 * wq + a];
+      if (e == 0) { if (f & CERT_F_AC) err = 7; }
+      else if (f & CERT_F_P2) err = 6;
+      else if (!(f & CERT_F_L1)) err = 5;
+    }
+  free(flags);
+  return err;
 }

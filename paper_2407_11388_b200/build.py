@@ -23,13 +23,31 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+def _source_hash(defines=()) -> str:
+    """sha256 over every source the library is built from, the nvcc flags and the
+    nvcc version.  Stored next to librac.so: a library whose stamp differs (or
+    is missing) is rebuilt, so a .so copied from another machine, or one older
+    than the sources whatever the file times say, is never used."""
+    import hashlib
+    h = hashlib.sha256()
     deps = [os.path.join(CSRC, f) for f in DEPS] + [os.path.join(ROOT, "include", "rac.h"),
                                                       os.path.join(ROOT, "synth", "csp_synth.h")]
-    return any(os.path.getmtime(d) > t for d in deps)
+    for d in deps:
+        with open(d, "rb") as f:
+            h.update(os.path.basename(d).encode() + b"\0" + f.read())
+    h.update(" ".join(ARCH + ["-O3", "-lineinfo"] + list(defines)).encode())
+    try:
+        h.update(subprocess.run([nvcc_path(), "--version"], capture_output=True, text=True).stdout.encode())
+    except Exception:
+        pass
+    return h.hexdigest()
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".srchash"):
+        return True
+    with open(LIB + ".srchash") as f:
+        return f.read().strip() != _source_hash()
 
 
 def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
@@ -61,6 +79,9 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         if verbose:
             sys.stderr.write(res.stderr)
     os.replace(tmp, lib)
+    if out is None and not defines:
+        with open(LIB + ".srchash", "w") as f:
+            f.write(_source_hash() + "\n")
     return lib
 
 

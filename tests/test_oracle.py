@@ -650,3 +650,179 @@ def test_wide_pass_block_matches_o1w():
         o, _ = blk.pass_block(D, lo, hi)
         got[lo:hi] = WD.bits_of(o, n, full.wq)[lo:hi]
     assert np.array_equal(got, exp)
+
+
+# ----------------------------------------------------------------------------- O7 exact-trajectory certificate
+def _perturbations(d_in, d_out, rem, it, st, n, rng, wq=1):
+    """Claims that differ from the recurrence's output (status, d_out, iterations,
+    epochs) in one plausible way each: (kind, d_out', rem', it', st')."""
+    out = []
+    nb = 64 * wq
+    din = np.asarray(d_in, dtype=U64).reshape(n, wq)
+    dout = np.asarray(d_out, dtype=U64).reshape(n, wq)
+
+    def bit(D, x, a):
+        return (int(D[x, a >> 6]) >> (a & 63)) & 1
+
+    def setb(D, x, a, v):
+        D = D.copy()
+        if v:
+            D[x, a >> 6] |= U64(1) << U64(a & 63)
+        else:
+            D[x, a >> 6] &= ~(U64(1) << U64(a & 63))
+        return D
+
+    removed = [(x, a) for x in range(n) for a in range(nb) if rem[x, a]]
+    kept = [(x, a) for x in range(n) for a in range(nb) if bit(dout, x, a)]
+    if removed:
+        x, a = removed[int(rng.integers(len(removed)))]
+        e = int(rem[x, a])
+        for de in (-1, +1):  # epoch one pass early / late, value still removed
+            if 1 <= e + de <= it:
+                r2 = rem.copy()
+                r2[x, a] = e + de
+                out.append(("epoch%+d" % de, dout.reshape(-1), r2, it, st))
+        r2 = rem.copy()  # under-pruned: the value put back
+        r2[x, a] = 0
+        out.append(("under", setb(dout, x, a, 1).reshape(-1), r2, it, st))
+    if kept:
+        x, a = kept[int(rng.integers(len(kept)))]
+        r2 = rem.copy()  # over-pruned: a kept value claimed removed
+        r2[x, a] = int(rng.integers(1, it + 1))
+        out.append(("over", setb(dout, x, a, 0).reshape(-1), r2, it, st))
+    out.append(("iters+1", dout.reshape(-1), rem, it + 1, st))
+    if it > 1:
+        out.append(("iters-1", dout.reshape(-1), rem, it - 1, st))
+    out.append(("status", dout.reshape(-1), rem, it, 1 - st))
+    return out
+
+
+def test_trajectory_certificate_accepts_recurrence_and_rejects_perturbations():
+    """O7 (oracle.c orc_certify_trajectory) accepts O1's output (O1 is pinned by
+    brute force, AC-3 and the hand traces above) in stop and full mode on W-root
+    and W-rand inputs, and rejects every one-step perturbation: an epoch moved one
+    pass (Prop. 2: a removal at k is caused at k-1), a value put back
+    (fails the AC rule), a kept value claimed removed (fails Lemma 1), a
+    wrong iteration count or status (Alg. 1 loop control).  O4 cannot
+    see epoch shifts that keep Lemma 1 true; O7 must."""
+    rng = np.random.default_rng(21)
+    counts = collections.Counter()
+    o4_blind = 0
+    for k, inst in enumerate(I.random_corpus(400, seed0=17) +
+                             [synth.random_csp(20, 8, 0.5, 0.4, s) for s in range(1, 101)]):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = inst.full_domains() if k % 2 == 0 else synth.w_rand(inst.dom, 0.85, seed=k)
+        for full in (False, True):
+            st, d_out, it, rem = orc.rac(d_in, full=full)
+            assert orc.certify_trajectory(d_in, d_out, rem, it, st, full) == 0, (k, full)
+            for kind, o2, r2, it2, st2 in _perturbations(d_in, d_out, rem, it, st, inst.n, rng):
+                assert orc.certify_trajectory(d_in, o2, r2, it2, st2, full) != 0, (k, full, kind)
+                counts[kind] += 1
+                if kind.startswith("epoch") and orc.certify(d_in, o2, r2, check_ac=(st == oracle.OK)) == 0:
+                    o4_blind += 1
+    for kind in ("epoch-1", "epoch+1", "under", "over", "iters+1", "iters-1", "status"):
+        assert counts[kind] > 40, counts
+    assert o4_blind > 10, o4_blind
+
+
+def test_trajectory_certificate_hand_traces():
+    """The hand traces: EQ2 / PATH3 / WIPE2 outputs are accepted with
+    their traced epochs and iteration counts; the PATH3 trace with its two
+    epochs swapped is rejected."""
+    for name in I.golden_names():
+        doc, inst = I.load_golden(name)
+        orc = oracle.Oracle.from_instance(inst)
+        exp = doc["expect"]
+        rem = np.zeros((inst.n, 64), dtype=np.int32)
+        for t, s in enumerate(exp["trace"], start=1):
+            for (x, a) in s:
+                rem[x, a] = t
+        st = oracle.OK if exp["status"] == "OK" else oracle.WIPEOUT
+        d_in = np.asarray(doc["d_in"], dtype=U64)
+        d_out = np.asarray(exp["d_out"], dtype=U64)
+        assert orc.certify_trajectory(d_in, d_out, rem, exp["iterations"], st) == 0, name
+        if name.startswith("path3"):
+            sw = rem.copy()
+            sw[rem == 1], sw[rem == 2] = 2, 1
+            assert orc.certify_trajectory(d_in, d_out, sw, exp["iterations"], st) != 0
+
+
+def test_trajectory_certificate_synth_streaming_matches():
+    """orc_certify_trajectory_synth (support sets regenerated per variable from
+    the generator, OpenMP over variables) gives the same verdicts as the
+    in-memory O7 on the same seeded instances, for 1 and 4 threads, one-word
+    and wide domains."""
+    rng = np.random.default_rng(5)
+    for (n, d, p, t, s) in [(60, 20, 1.0, 0.3, 1), (45, 64, 0.6, 0.75, 2), (30, 8, 0.5, 0.4, 3)]:
+        dq, tq = synth.quant_density(p), synth.quant_tightness(t)
+        orc = oracle.Oracle.from_synth(n, d, dq, tq, s)
+        d_in = synth.w_rand(np.full(n, d), 0.9, seed=s)
+        for full in (False, True):
+            st, d_out, it, rem = orc.rac(d_in, full=full)
+            for th in (1, 4):
+                assert oracle.certify_trajectory_synth(n, d, dq, tq, s, d_in, d_out, rem, it, st, full, th) == 0
+            for kind, o2, r2, it2, st2 in _perturbations(d_in, d_out, rem, it, st, n, rng):
+                a = orc.certify_trajectory(d_in, o2, r2, it2, st2, full)
+                b = oracle.certify_trajectory_synth(n, d, dq, tq, s, d_in, o2, r2, it2, st2, full, 4)
+                assert a != 0 and b != 0, (kind, a, b)  # codes may differ: first failing variable vs any
+    for (n, d, p, t, s) in [(24, 130, 0.7, 0.975, 9), (12, 256, 1.0, 0.985, 4)]:
+        dq, tq = synth.quant_density(p), synth.quant_tightness(t)
+        wo = oracle.WideOracle.from_synth(n, d, dq, tq, s)
+        d_in = synth.w_rand_wide(np.full(n, d), 0.8, seed=s)
+        for full in (False, True):
+            st, d_out, it, rem = wo.rac(d_in, full=full)
+            assert wo.certify_trajectory(d_in, d_out, rem, it, st, full) == 0
+            assert oracle.certify_trajectory_synth(n, d, dq, tq, s, d_in, d_out, rem, it, st, full, 2) == 0
+            for kind, o2, r2, it2, st2 in _perturbations(d_in, d_out, rem, it, st, n, rng, wo.wq):
+                a = wo.certify_trajectory(d_in, o2, r2, it2, st2, full)
+                b = oracle.certify_trajectory_synth(n, d, dq, tq, s, d_in, o2, r2, it2, st2, full, 2)
+                assert a != 0 and b != 0, (kind, a, b)  # codes may differ: first failing variable vs any
+
+
+def test_wide_trajectory_certificate_corpus():
+    """O7 on wide domains (wcertify): accepts O1w (pinned above by value
+    duplication and AC-3) on the random wide corpus, rejects the perturbations."""
+    rng = np.random.default_rng(8)
+    counts = collections.Counter()
+    for i, inst in enumerate(_wide_corpus(30, 77)):
+        wo = oracle.WideOracle.from_instance(inst)
+        d_in = synth.w_rand_wide(inst.dom, 0.85, seed=i)
+        for full in (False, True):
+            st, out, it, rem = wo.rac(d_in, full=full)
+            assert wo.certify_trajectory(d_in, out, rem, it, st, full) == 0
+            for kind, o2, r2, it2, st2 in _perturbations(d_in, out, rem, it, st, inst.n, rng, wo.wq):
+                assert wo.certify_trajectory(d_in, o2, r2, it2, st2, full) != 0, (i, kind)
+                counts[kind] += 1
+    assert counts["under"] > 10 and counts["over"] > 10 and counts["epoch+1"] + counts["epoch-1"] > 10
+
+
+def test_wide_is_ac_negative():
+    """orc_wis_ac is the AC definition plus "no empty domain": D_ac
+    (AC) is accepted; D_ac plus any one removed value of D_in is rejected (D_ac is
+    the largest AC subset, so a superset cannot be AC); emptying the
+    domain of a variable without constraints keeps the set AC by definition but
+    is rejected by the empty-domain clause."""
+    checked = 0
+    for i, inst in enumerate(_wide_corpus(30, 41)):
+        wo = oracle.WideOracle.from_instance(inst)
+        d_in = synth.w_rand_wide(inst.dom, 0.9, seed=i)
+        st, out, it, rem = wo.rac(d_in, full=True)
+        if st != oracle.OK:
+            continue
+        assert wo.is_ac(out)
+        ob = WD.bits_of(out, inst.n, wo.wq)
+        for (x, a) in list(zip(*np.nonzero(rem)))[:5]:
+            b2 = ob.copy()
+            b2[x, a] = True
+            assert not wo.is_ac(WD.words_of(b2)), (i, x, a)
+            checked += 1
+    assert checked > 20
+    # an isolated variable (no constraint): emptying it leaves an AC set with an empty domain
+    n, d = 4, 100
+    inst = synth.wide_from_constraints(n, d, [(0, 1, [(a, a) for a in range(d)]), (1, 2, [(a, a) for a in range(d)])])
+    wo = oracle.WideOracle.from_instance(inst)
+    D = synth.full_domains_wide(inst.dom)
+    assert wo.is_ac(D)
+    bits = WD.bits_of(D, n, wo.wq)
+    bits[3, :] = False
+    assert not wo.is_ac(WD.words_of(bits))
