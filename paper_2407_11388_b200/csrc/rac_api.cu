@@ -347,10 +347,11 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
   CKC(cudaMalloc(&c->sh.Dw, (size_t)c->dbytes));
   CKC(cudaMalloc(&c->sh.R, (size_t)n * 8));
   CKC(cudaMemsetAsync(c->sh.R, 0, (size_t)n * 8, c->stream));
-  CKC(cudaMalloc(&c->sh.iters, 16));
+  CKC(cudaMalloc(&c->sh.iters, 32));
   c->sh.status = c->sh.iters + 1;
   c->sh.done = c->sh.iters + 2;
   c->sh.vcnt = c->sh.iters + 3;
+  c->sh.seeded = c->sh.iters + 4;
   CKC(cudaMalloc(&c->sh.vlist, (size_t)n * 2 + 16));
   CKC(cudaMalloc(&c->buf_in, (size_t)n * 8));
   CKC(cudaMalloc(&c->buf_out, (size_t)n * 8));
@@ -575,9 +576,11 @@ int check_usable(rac_ctx* c) {
   return 0;
 }
 
+// n_seeds < 0: root call (every column in pass 1); >= 0: seeded call
+// (Alg. 1 @changed = seeds; 0 = empty @changed, no pass, whatever `seeds` is).
 int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
                   int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
-                  int n_seeds = 0) {
+                  int n_seeds = -1) {
   FusedParams p{};
   p.g = geom_for(c, c->x_lo, c->x_hi);  // world == 1: every row
   p.dommask = c->dommask;
@@ -615,7 +618,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
   p.dbg = c->dbg;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
-  if (c->fused_grid == 1 && !c->peer && !c->sparse && (seeds == nullptr || n_seeds == 1)) {
+  if (c->fused_grid == 1 && !c->peer && !c->sparse && (n_seeds < 0 || n_seeds == 1)) {
     // One CTA is enough: run the single-CTA variant (removal bits in shared
     // memory, __syncthreads as the pass barrier) -- the batched per-state
     // kernel with one state.
@@ -626,7 +629,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
     b.d_out = d_out;
     b.iters = iters;
     b.status = status;
-    b.seed_var = seeds;  // one seed (or NULL = root call)
+    b.seed_var = n_seeds == 1 ? seeds : nullptr;  // one seed (or NULL = root call)
     b.removed_at = removed_at;
     b.flags = flags;
     CK(c, launch_batch(c->W, c->G, b, 1, fused_smem(c->dbytes, c->n) + (size_t)c->n * 8, s));
@@ -645,12 +648,19 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
 }
 
 int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
-                    int32_t* removed_at, uint32_t flags, cudaStream_t s) {
+                    int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
+                    int n_seeds = -1) {
   if (removed_at && c->world > 1) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
   const int total_g = c->world * c->blk;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
   CK(c, launch_shard_init(c->sh, d_in, c->dommask, c->n, c->W, c->dbytes, total_g, s));
   c->launches++;
+  if (n_seeds >= 0) {
+    // seeded call: pass 1 tests Cons[:, seeds] (Alg. 1 @changed = seeds);
+    // an empty list marks the call done with no pass
+    CK(c, launch_shard_seed(c->sh, seeds, n_seeds, c->n, s));
+    c->launches++;
+  }
   const int nb = c->use_nccl() ? 1 : c->vshards;
   std::vector<PassParams> pp(nb);
   for (int b = 0; b < nb; ++b) {
@@ -708,17 +718,11 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   if (c->peer) {
     if (!c->connected) return fail(c, RAC_EINVAL, "RAC_OPT_PEER context: call rac_connect_peers first");
     if (removed_at) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
-    return enforce_fused(c, d_in, d_out, iters, status, nullptr, flags, s, n_seeds >= 0 ? seeds : nullptr,
-                         n_seeds >= 0 ? n_seeds : 0);
+    return enforce_fused(c, d_in, d_out, iters, status, nullptr, flags, s, seeds, n_seeds);
   }
-  if (c->use_nccl() || c->vshards > 1) {
-    // the sharded driver has no seeded pass 1: a full pass 1 is the superset
-    // check (valid under the precondition; identical trajectory, Prop. 2)
-    if (n_seeds == 0) return fail(c, RAC_EUNSUPPORTED, "empty seed list on the sharded path");
-    return enforce_sharded(c, d_in, d_out, iters, status, removed_at, flags, s);
-  }
-  return enforce_fused(c, d_in, d_out, iters, status, removed_at, flags, s, n_seeds >= 0 ? seeds : nullptr,
-                       n_seeds >= 0 ? n_seeds : 0);
+  if (c->use_nccl() || c->vshards > 1)
+    return enforce_sharded(c, d_in, d_out, iters, status, removed_at, flags, s, seeds, n_seeds);
+  return enforce_fused(c, d_in, d_out, iters, status, removed_at, flags, s, seeds, n_seeds);
 }
 
 }  // namespace

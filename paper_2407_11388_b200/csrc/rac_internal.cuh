@@ -101,8 +101,8 @@ struct FusedParams {
   unsigned* wctr;           // [3] per-pass dynamic row counters (rotating like R)
   unsigned* rflag;          // [3] per-pass "some value was removed" flags (rotating like R)
   uint32_t* clist;          // nullable [3][n+1] per-pass change lists ([0] = count; rotating like R)
-  const int32_t* seeds;     // nullable device [n_seeds]: Alg. 1 initial @changed
-  int n_seeds;
+  const int32_t* seeds;     // device [n_seeds]: Alg. 1 initial @changed (read only if n_seeds > 0)
+  int n_seeds;              // < 0: root call (every column in pass 1); 0: no pass
   uint32_t flags;
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
   // Global pass counter (persists across launches): pass t of this launch is
@@ -126,6 +126,7 @@ struct ShardState {
   int32_t* status;
   int32_t* done;
   int32_t* vcnt;             // length of vlist (variables changed in the last pass)
+  int32_t* seeded;           // 1: pass 1 tests vlist (a seeded call), 0: every column
   uint16_t* vlist;           // [n] Prop. 2 incremental column list
 };
 
@@ -208,6 +209,7 @@ cudaError_t launch_pass(int W, int G, const PassParams& p, int grid, size_t smem
 cudaError_t pass_occupancy(int W, int G, size_t smem, int* blocks_per_sm);
 cudaError_t launch_shard_init(const ShardState& s, const uint64_t* d_in, const uint64_t* dommask, int n, int W,
                               int dbytes, int total_g, cudaStream_t st);
+cudaError_t launch_shard_seed(const ShardState& s, const int32_t* seeds, int n_seeds, int n, cudaStream_t st);
 cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, cudaStream_t st);
 cudaError_t launch_shard_update(const ShardState& s, int n, int W, uint32_t flags, cudaStream_t st);
 cudaError_t launch_shard_finalize(const ShardState& s, int n, uint64_t* d_out, int32_t* iters, int32_t* status,

@@ -398,8 +398,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   int has_empty = 0;  // some D(x) empty (block-uniform)
   for (int x = threadIdx.x; x < g.n; x += blockDim.x) has_empty |= load_w<W>(Db + x * W) == 0;
   has_empty = __syncthreads_or(has_empty);
-  // Seeded call (Alg. 1 with @changed = seeds): pass 1 tests only the seed columns.
-  const bool seeded = p.seeds != nullptr;
+  // Seeded call (Alg. 1 with @changed = seeds): pass 1 tests only the seed
+  // columns.  n_seeds < 0: root call (every column); n_seeds == 0: empty
+  // @changed, no pass (the seeds pointer is not read).
+  const bool seeded = p.n_seeds >= 0;
   if (seeded) {
     for (int i = threadIdx.x; i < p.n_seeds; i += blockDim.x) {
       const int y = p.seeds[i];
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_pass(PassParams p) {
   tma_stage(Db, p.s.Dw, (uint32_t)p.g.dbytes, &mbar);
   const int t = *p.s.iters + 1;
   const int vcnt = *p.s.vcnt;
-  const bool lst = t > 1;
+  const bool lst = t > 1 || *p.s.seeded;
   uint16_t* vlist = reinterpret_cast<uint16_t*>(Db + list_offset(p.g.dbytes));
   if (lst) {
     for (int i = threadIdx.x; i < vcnt; i += blockDim.x) vlist[i] = p.s.vlist[i];
@@ -669,6 +671,35 @@ __global__ void rac_shard_init(ShardState s, const uint64_t* d_in, const uint64_
     *s.status = -1;
     *s.done = 0;
     *s.vcnt = 0;
+    *s.seeded = 0;
+  }
+}
+
+// Seeded call (Alg. 1 tensorAC(Vars, @changed = seeds)): pass 1 tests
+// the columns of the listed variables (out-of-range entries skipped,
+// duplicates once).  An empty list means no pass: done, iterations 0, status
+// from D_in.  One CTA; dynamic smem = n flag bytes.
+__global__ void __launch_bounds__(1024) rac_shard_seed(ShardState s, const int32_t* seeds, int n_seeds, int n) {
+  extern __shared__ uint8_t need[];
+  __shared__ int scratch[32];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) need[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_seeds; i += blockDim.x) {
+    const int y = seeds[i];
+    if (y >= 0 && y < n) need[y] = 1;
+  }
+  __syncthreads();
+  const int cnt = block_compact(need, s.vlist, n, scratch);
+  int wipe = 0;
+  for (int x = threadIdx.x; x < n; x += blockDim.x) wipe |= s.Dcur[x] == 0ull;
+  wipe = __syncthreads_or(wipe);
+  if (threadIdx.x == 0) {
+    *s.vcnt = cnt;
+    *s.seeded = 1;
+    if (cnt == 0) {
+      *s.status = wipe ? kWIPEOUT : kOK;
+      *s.done = 1;
+    }
   }
 }
 
@@ -911,6 +942,14 @@ cudaError_t launch_shard_init(const ShardState& s, const uint64_t* d_in, const u
   int grid = (work + 255) / 256;
   if (grid > 1024) grid = 1024;
   rac_shard_init<<<grid, 256, 0, st>>>(s, d_in, dommask, n, W, dbytes, total_g);
+  return cudaGetLastError();
+}
+cudaError_t launch_shard_seed(const ShardState& s, const int32_t* seeds, int n_seeds, int n, cudaStream_t st) {
+  if (n > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(rac_shard_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, n);
+    if (e != cudaSuccess) return e;
+  }
+  rac_shard_seed<<<1, 1024, n, st>>>(s, seeds, n_seeds, n);
   return cudaGetLastError();
 }
 cudaError_t launch_shard_slice(const ShardState& s, int x_lo, int x_hi, int n, cudaStream_t st) {

@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_fused(WideParams p) {
         bool failed = false;
         for (unsigned i = 0; i < ncols && !failed; ++i) {
           const int y = cols ? (int)__ldcg(cols + i) : (int)i;
+          if ((unsigned)y >= (unsigned)n) continue;  // a bad seed is skipped (as in rac_fused)
           const Mask<WS> m = load_mask<WS>(row + (size_t)y * WS);
           failed = !meets<WS>(m, sD + (size_t)y * WS) && present(p.P, p.pw, x, y);
         }
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_fused(WideParams p) {
         for (int u = 0; u < 4; ++u) {
           const unsigned i = base + (unsigned)u * 32u + (unsigned)lane;
           ys[u] = i < ncols ? (cols ? (int)__ldcg(cols + i) : (int)i) : -1;
+          if ((unsigned)ys[u] >= (unsigned)n) ys[u] = -1;  // a bad seed is skipped (as in rac_fused)
           if (ys[u] >= 0) m[u] = load_mask<WS>(row + (size_t)ys[u] * WS);
         }
         bool f = false;

@@ -1,0 +1,132 @@
+"""Small workloads for compute-sanitizer (memcheck / racecheck / synccheck /
+initcheck) over every enforcement kernel, each checked against the CPU oracle:
+
+  fused   -- multi-CTA rac_fused (C2 shape n=500 d=20 t=0.3: root, seeded, W-rand,
+             full mode) and a small C3-shaped propagating instance (n=600 d=32)
+  sparse  -- rac_fused<W,0> over the sparse arc-block layout (density 0.25)
+  vshard  -- rac_pass + rac_shard_{init,seed,slice,update,finalize} (3 row blocks)
+  wide    -- wide_fused (d=128, propagating), root + seeded
+  batch   -- rac_batch_bs (64 W-dive states) and the single-CTA rac_batch path
+  peer    -- one rank of a 2-process RAC_OPT_PEER group (run under torchrun)
+
+Exit status 0 iff every result equals the oracle's.
+usage: python tools/sanitize_cases.py CASE
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2407_11388_b200 import rac  # noqa: E402
+
+
+def same(g, o, what):
+    ok = g[0] == o[0] and g[2] == o[2] and np.array_equal(np.asarray(g[1]).reshape(-1), np.asarray(o[1]).reshape(-1))
+    if len(g) > 3 and g[3] is not None and o[3] is not None:
+        ok = ok and np.array_equal(np.asarray(g[3]), np.asarray(o[3]))
+    print(what, "OK" if ok else "MISMATCH", (g[0], g[2]), (o[0], o[2]), flush=True)
+    return ok
+
+
+def gen_case(n, d, p, t, seed, **kw):
+    dq, tq = synth.quant_density(p), synth.quant_tightness(t)
+    return rac.RacContext.create_random(n, d, dq, tq, seed, **kw), oracle.Oracle.from_synth(n, d, dq, tq, seed)
+
+
+def run_common(ctx, orc, n, d, tag):
+    ok = True
+    root = synth.full_domains(np.full(n, d))
+    o = orc.rac(root)
+    ok &= same(ctx.enforce(root, removed_at=True), o, tag + " root")
+    if o[0] == oracle.OK:
+        ds, x, _ = synth.w_seed(o[1], 5)
+        ok &= same(ctx.enforce_seeded(ds, [x]), orc.rac(ds, with_epochs=False), tag + " seeded")
+        ok &= same(ctx.enforce_seeded(ds, []), (0 if all(int(v) for v in ds) else 1, ds, 0), tag + " seeded-empty")
+    dr = synth.w_rand(np.full(n, d), 0.9, 3)
+    ok &= same(ctx.enforce(dr, removed_at=True), orc.rac(dr), tag + " rand")
+    ok &= same(ctx.enforce(dr, full=True, removed_at=True), orc.rac(dr, full=True), tag + " rand-full")
+    return ok
+
+
+def main(case):
+    import torch
+    torch.cuda.set_device(0)
+    ok = True
+    if case == "fused":
+        for (n, d, p, t) in ((500, 20, 1.0, 0.3), (600, 32, 1.0, 0.66)):
+            ctx, orc = gen_case(n, d, p, t, 1)
+            ok &= run_common(ctx, orc, n, d, "fused n=%d" % n)
+    elif case == "sparse":
+        ctx, orc = gen_case(800, 32, 0.25, 0.6, 2, layout="sparse")
+        assert ctx.layout == "sparse"
+        ok &= run_common(ctx, orc, 800, 32, "sparse")
+    elif case == "vshard":
+        ctx, orc = gen_case(500, 20, 1.0, 0.3, 1, virtual_shards=3)
+        ok &= run_common(ctx, orc, 500, 20, "vshard")
+    elif case == "wide":
+        n, d = 200, 128
+        dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.93)
+        ctx = rac.RacContext.create_random(n, d, dq, tq, 1)
+        wo = oracle.WideOracle.from_synth(n, d, dq, tq, 1)
+        full = synth.full_domains_wide(np.full(n, d))
+        o = wo.rac(full)
+        g = ctx.enforce(full, removed_at=True)
+        ok &= same(g, o, "wide root")
+        dr = synth.w_rand_wide(np.full(n, d), 0.9, 3)
+        ok &= same(ctx.enforce(dr, removed_at=True), wo.rac(dr), "wide rand")
+    elif case == "batch":
+        n, d, S = 200, 16, 64
+        inst = synth.random_csp(n, d, 0.8, 0.3, 1)
+        orc = oracle.Oracle.from_instance(inst)
+        _, root, _, _ = orc.rac(inst.full_domains())
+        states, svars = synth.dive_states(root, lambda D: orc.rac(D, with_epochs=False)[:2], S, seed=1,
+                                          return_seeds=True)
+        states = np.stack(states)
+        ctx = rac.RacContext.from_instance(inst)
+        din = torch.from_numpy(states.view(np.int64).copy()).cuda()
+        dout = torch.zeros_like(din)
+        its = torch.zeros(S, dtype=torch.int32, device="cuda")
+        sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+        sv = torch.from_numpy(np.asarray(svars, dtype=np.int32)).cuda()
+        for seeded in (False, True):
+            if seeded:
+                ctx.enforce_batch_seeded(S, din, dout, its, sts, sv)
+            else:
+                ctx.enforce_batch(S, din, dout, its, sts)
+            torch.cuda.synchronize()
+            out = dout.cpu().numpy().view(np.uint64)
+            for s in range(S):
+                o = orc.rac(states[s], with_epochs=False)
+                ok &= (int(sts[s]), int(its[s])) == (o[0], o[2]) and np.array_equal(out[s], o[1])
+            print("batch seeded=%s" % seeded, "OK" if ok else "MISMATCH", flush=True)
+        c1 = synth.random_csp(20, 8, 0.5, 0.4, 1)
+        ctx1, orc1 = rac.RacContext.from_instance(c1), oracle.Oracle.from_instance(c1)
+        ok &= same(ctx1.enforce(c1.full_domains(), removed_at=True), orc1.rac(c1.full_domains()), "single-cta C1")
+    elif case == "peer":
+        import torch.distributed as dist
+        from paper_2407_11388_b200 import dist as rdist
+        os.environ.setdefault("RAC_PEER_TIMEOUT_MS", "120000")
+        dist.init_process_group("gloo")
+        rank, world = dist.get_rank(), dist.get_world_size()
+        n, d, p, t = 300, 16, 0.5, 0.5
+        dq, tq = synth.quant_density(p), synth.quant_tightness(t)
+        ctx = rac.RacContext.create_random(n, d, dq, tq, 3, device=0, rank=rank, world=world, peer=True, max_ctas=8)
+        rdist.connect_peers(ctx)
+        orc = oracle.Oracle.from_synth(n, d, dq, tq, 3)
+        for k in range(2):
+            dr = synth.w_rand(np.full(n, d), 0.9, 10 + k)
+            ok &= same(ctx.enforce(dr), orc.rac(dr, with_epochs=False), "peer rank %d k=%d" % (rank, k))
+        dist.barrier()
+        ctx.close()
+        dist.destroy_process_group()
+    else:
+        raise SystemExit("unknown case " + case)
+    print("CASE", case, "PASS" if ok else "FAIL", flush=True)
+    return 0 if ok else 3
+
+
+if __name__ == "__main__":
+    sys.exit(main(sys.argv[1]))
