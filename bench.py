@@ -401,6 +401,7 @@ def run_gpu(args, rank, world, local_rank):
 
     peak, peak_src = measured_peaks()
     roofline = None
+    l2_roof = None
     if kind == "dive":
         # Bit-sliced batched pass (rac_batch_bs): a support test of (x,a) against
         # c_xy for 32 states is ceil(d/4) nibble-table lookups in shared memory;
@@ -420,46 +421,114 @@ def run_gpu(args, rank, world, local_rank):
                     "algorithmic_tests_per_launch": instr["support_tests"], "launch_ms_median": round(kern_ms, 5),
                     "peak_source": "derived: LDS lookups (148 SM x 32/clk x %.0f MHz) / ceil(d/4) lookups per "
                                    "32-state test; DESIGN.md section 7" % sm_mhz}
+    if alg_bytes is not None and ctx.relation_bytes <= L2_BYTES // 2 and world == 1:
+        # The relation is L2-resident (C1/C2): the bound is L2, not HBM.  Peak =
+        # read bandwidth of an L2-resident buffer measured here (torch sum of a
+        # buffer the size of the relation, back to back, CUDA events).
+        l2_gbs = measure_l2_read_gbs(max(ctx.relation_bytes, 4 << 20), dev)
+        kern_ms = statistics.median(per_step)
+        ach = alg_bytes / (kern_ms / 1e3) / 1e9
+        l2_roof = {"bound": "l2", "achieved": round(ach, 1), "peak": round(l2_gbs, 1), "unit": "GB/s",
+                   "frac": round(ach / l2_gbs, 4),
+                   "peak_source": "measured in this run: torch.sum over an L2-resident %d-byte buffer "
+                                  "(read bandwidth, best of 20)" % max(ctx.relation_bytes, 4 << 20)}
     if alg_bytes is not None:
         kern_ms = statistics.median(per_step)
         achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-        traffic = None
+        traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(args.workload, {}).get("dram_bytes_per_launch")
+                tj = json.load(open(tp))
+                ent = tj.get(args.workload, {})
+                traffic = ent.get("dram_bytes_per_launch")
+                if traffic is not None:
+                    traffic_src = "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum, one launch, " \
+                                  "captured in session %s (profiles/ncu_traffic.json), not in this run" % \
+                                  ent.get("session", tj.get("session", "?"))
             except Exception:
                 traffic = None
+        full_b = instr.get("full_test_bytes")
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": traffic,
-                    "kernel": ("wide_fused" if d > 64 else "rac_fused") if (world == 1 or peer)
-                              else "rac_pass (+ allgather)",
+                    "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                    "kernel": ("wide_fused" if d > 64 else ("rac_state" if ctx.path == "one_block" else "rac_fused"))
+                              if (world == 1 or peer) else "rac_pass (+ allgather)",
                     "algorithmic_bytes_per_launch": alg_bytes,
-                    "algorithmic_bytes_rule": "kept rows: every tested mask; removed rows: one witness mask",
+                    "byte_rule": "must-read",
+                    "algorithmic_bytes_rule": "must-read: kept rows every tested mask, removed rows one witness "
+                                              "mask (Lemma 1); SURVEY 8(d) full-check figure in frac_full_check",
+                    "frac_full_check": round(full_b / (kern_ms / 1e3) / 1e9 / peak, 4) if full_b else
+                                       round(achieved / peak, 4),
                     "launch_ms_median": round(kern_ms, 5),
                     "peak_source": peak_src + ("" if world == 1 else "; per-GPU bytes = total / N")}
         if world > 1:
             roofline["achieved"] = round(achieved / world, 1)
             roofline["frac"] = round(achieved / world / peak, 4)
-    cfg = {"workload": args.workload + ": " + desc, "n": n, "d": d, "density": dens, "tightness": tight,
-           "t_q16": tq, "seed": seed, "states": S if kind == "dive" else 1,
-           "layout": ctx.layout, "relation_bytes": ctx.relation_bytes,
-           "l2": "inputs larger than L2 (no flush)" if ctx.relation_bytes > 200e6 else
-                 "relation L2-resident (warm; stated, not flushed)",
-           "parallelism": (("row-sharded x%d (peer-memory removal exchange + cross-rank barrier inside the "
-                            "persistent kernel, NVLink P2P)" if peer else
-                            "row-sharded x%d (NCCL all-gather of D per pass)") % world) if world > 1 else "1 GPU",
-           "instance_generation_s": round(gen_s, 3)}
+    cfg = workload_config(args)
+    setup = {"layout": ctx.layout, "relation_bytes": ctx.relation_bytes,
+             "parallelism": (("row-sharded x%d (peer-memory removal exchange + cross-rank barrier inside the "
+                              "persistent kernel, NVLink P2P)" if peer else
+                              "row-sharded x%d (NCCL all-gather of D per pass)") % world) if world > 1 else "1 GPU",
+             "instance_generation_s": round(gen_s, 3)}
     out = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
            "dtype": {1: "u8", 2: "u16", 4: "u32", 8: "u64", 16: "2 x u64", 32: "4 x u64"}[ctx.mask_bytes] + " bitmasks",
            "data": "synthetic (seeded counter-based random CSP, synth/csp_synth.h)", "config": cfg,
            "gpu_launches": int(launches_per_step * args.steps), "clocks": clk, "e2e": e2e,
-           "enforcement": instr, "roofline": roofline}
+           "enforcement": instr, "roofline": roofline, "setup": setup, "paper_context": PAPER_CONTEXT}
+    if l2_roof is not None:
+        out["roofline_l2"] = l2_roof
     if roofline:
         out["relation_gbs_per_iter"] = roofline["achieved"] * (world if world > 1 else 1)
     return out, (n, d, dq, tq, seed, kind, din_h)
+
+
+L2_BYTES = 126 * (1 << 20)
+
+# BASELINE.md / PAPER.md context: the paper publishes no throughput; its only
+# numbers are Table 1's per-assignment counts on its own (unpublished) instances.
+PAPER_CONTEXT = {
+    "source": "PAPER.md Table 1 (lines 253-288); setup lines 225-236",
+    "hardware": "RTAC: Python + PyTorch (fp32 tensors) on an RTX 3090; AC3: Python + JIT on an i9-10900K "
+                "(PAPER.md line 229)",
+    "table1_recurrence_per_assignment": [3.441, 4.831],
+    "table1_revision_per_assignment": [307.6, 107680.5],
+    "time_per_assignment": "Fig. 3 (ms per assignment, mean of 50K) -- image missing from the paper text, "
+                           "no number recoverable (PAPER.md lines 238-243)",
+    "comparable": "no: instances, domain size and tightness unpublished; counts are context only "
+                  "(this build's Table-1 trend: DESIGN.md section 7)",
+}
+
+# L2-resident workloads (relation well under the 126 MB L2): stated, not flushed
+L2_RESIDENT = {"c1-seed", "c2-root", "c5-batch"}
+
+
+def workload_config(args):
+    """The workload-defining keys only (identical in the GPU arm and the reference arm)."""
+    n, d, dens, tight, seed, kind, desc = WORKLOADS[args.workload]
+    return {"workload": args.workload + ": " + desc, "n": n, "d": d, "density": dens, "tightness": tight,
+            "t_q16": synth.quant_tightness(tight), "seed": seed, "states": args.states if kind == "dive" else 1,
+            "l2": "relation L2-resident (warm; stated, not flushed)" if args.workload in L2_RESIDENT else
+                  "inputs larger than L2 (no flush)"}
+
+
+def measure_l2_read_gbs(nbytes, dev):
+    import torch
+    buf = torch.ones(nbytes // 4, dtype=torch.float32, device=dev)
+    for _ in range(5):
+        buf.sum()
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(20):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(10):
+            buf.sum()
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / 10)
+    return nbytes / (best / 1e3) / 1e9
 
 
 def _live_bits(D, n, d):
@@ -529,18 +598,50 @@ def oracle_baseline(n, d, dq, tq, seed, kind, din_h, budget_s=20.0, passes=None)
     else:
         orc = oracle.Oracle.from_synth(n, d, dq, tq, seed)
     build_s = time.time() - t0
-    done = 0
-    t1 = time.perf_counter()
-    while True:
-        orc.rac(din_h[done % din_h.shape[0]], with_epochs=False)
-        done += 1
-        el = time.perf_counter() - t1
-        if el > budget_s or done >= max(1, din_h.shape[0]) * 64:
-            break
-    return {"value": done / el, "unit": "states/s" if kind == "dive" else UNIT, "cores": 1, "kind": "oracle",
-            "sample": "%d enforcement(s) of the same D_in%s by orc_rac (O1, 1 thread, gcc -O2) in %.1f s; "
-                      "oracle instance build %.1f s excluded" % (done, " states" if kind == "dive" else "", el,
-                                                                    build_s)}
+    unit = "states/s" if kind == "dive" else UNIT
+    S = din_h.shape[0]
+    cores = oracle.max_threads()
+
+    def timed(fn, budget, per_call_units=1):
+        """calls of fn() until `budget` seconds (at least one); returns units/s, calls, seconds"""
+        done, t1 = 0, time.perf_counter()
+        while True:
+            fn(done)
+            done += 1
+            el = time.perf_counter() - t1
+            if el > budget or done >= 64 * max(1, S):
+                break
+        return done * per_call_units / el, done, el
+
+    # (1) O1 on one core
+    v_one, calls1, el1 = timed(lambda k: orc.rac(din_h[k % S], with_epochs=False), budget_s * 0.3)
+    one = {"value": v_one, "unit": unit, "cores": 1, "kind": "oracle",
+           "sample": "%d enforcement(s) by orc_rac (O1, gcc -O2, 1 thread) in %.1f s" % (calls1, el1)}
+    # (2) O1 on every host core (BASELINE.md section 4)
+    if kind == "dive":
+        v_all, calls, el = timed(lambda k: orc.rac_many(din_h, threads=0), budget_s * 0.4, per_call_units=S)
+        s_all = "%d batch(es) of %d W-dive states, states spread over %d OpenMP threads (orc_rac_many, O1)" % (
+            calls, S, cores)
+    else:
+        v_all, calls, el = timed(lambda k: orc.rac_par(din_h[0], threads=0), budget_s * 0.4)
+        s_all = "%d enforcement(s) of the same D_in, each pass's variables over %d OpenMP threads (orc_rac_par, O1)" % (
+            calls, cores)
+    allc = {"value": v_all, "unit": unit, "cores": cores, "kind": "oracle",
+            "sample": s_all + " in %.1f s; oracle instance build %.1f s excluded" % (el, build_s)}
+    # (3) AC-3 on one core: the paper's baseline class (PAPER.md line 227; inherently sequential)
+    v_ac3, calls3, el3 = timed(lambda k: orc.ac3(din_h[k % S]), budget_s * 0.3)
+    ac3 = {"value": v_ac3, "unit": unit, "cores": 1, "kind": "oracle (AC-3, O2)",
+           "sample": "%d enforcement(s) by orc_ac3 (FIFO AC-3, the paper's baseline class, PAPER.md line 227) "
+                     "in %.1f s" % (calls3, el3)}
+    # Headline: every core where a pass has enough work to split (batches of states;
+    # an enforcement of >= 2 ms on one core); a small enforcement is synchronisation-
+    # bound across threads, and its honest host figure is the single-thread one.
+    head = allc if (kind == "dive" or v_one < 500.0) else one
+    out = dict(head)
+    out["one_core"] = one
+    out["all_cores"] = allc
+    out["ac3_one_core"] = ac3
+    return out
 
 
 def run_reference(args):
@@ -558,8 +659,7 @@ def run_reference(args):
         return {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u64 bitsets", "data": "synthetic (seeded counter-based random CSP, "
-                "synth/csp_synth.h)", "config": {"workload": args.workload + ": " + desc, "n": n, "d": d,
-                                                 "density": dens, "tightness": tight, "seed": seed},
+                "synth/csp_synth.h)", "config": workload_config(args),
                 "impl": "reference", "cpu_baseline": cb,
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     if kind == "dive":
@@ -576,31 +676,50 @@ def run_reference(args):
         else:
             d_in = full
         din_h = d_in[None, :]
-    # bounded sample: each step = one enforcement (or one state); cap total time
+    # bounded sample, on every host core: each step = one enforcement (orc_rac_par:
+    # each pass's variables over OpenMP threads) or, batched, one batch of states
+    # (orc_rac_many: states over threads); cap the total time
+    cores = oracle.max_threads()
+    S = din_h.shape[0]
     t0 = time.perf_counter()
     orc.rac(din_h[0], with_epochs=False)
+    one = time.perf_counter() - t0
+    if kind == "dive":
+        def one_step(k):
+            orc.rac_many(din_h, threads=0)
+    elif one >= 2e-3:
+        def one_step(k):
+            orc.rac_par(din_h[0], threads=0)
+    else:  # small enforcement: threads only add synchronisation (see oracle_baseline)
+        cores = 1
+
+        def one_step(k):
+            orc.rac(din_h[0], with_epochs=False)
+    t0 = time.perf_counter()
+    one_step(0)
     one = time.perf_counter() - t0
     budget = 150.0
     steps = args.steps
     if one * (args.steps + args.warmup) > budget:
         steps = max(3, int(budget / max(one, 1e-9)) - args.warmup)
     for k in range(min(args.warmup, 3)):
-        orc.rac(din_h[k % din_h.shape[0]], with_epochs=False)
+        one_step(k)
     t0 = time.perf_counter()
     for k in range(steps):
-        orc.rac(din_h[k % din_h.shape[0]], with_epochs=False)
+        one_step(k)
     el = time.perf_counter() - t0
     unit = "states/s" if kind == "dive" else UNIT
-    val = steps / el
-    sample = ("%d of %d requested steps, each one full enforcement by orc_rac (O1, 1 thread)" % (steps, args.steps))
+    val = steps * (S if kind == "dive" else 1) / el
+    sample = ("%d of %d requested steps, each %s by the oracle's O1 on %d thread(s)" %
+              (steps, args.steps, ("one batch of %d states (orc_rac_many)" % S) if kind == "dive" else
+               "one full enforcement (%s)" % ("orc_rac_par" if cores > 1 else "orc_rac"), cores))
     return {"metric": METRIC if kind != "dive" else "AC enforcements/sec (batched search-tree states)",
             "value": val, "unit": unit, "n_gpus": 0, "steps": steps, "warmup": args.warmup,
             "ms_per_step": el / steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64 bitsets", "data": "synthetic (seeded counter-based random CSP, synth/csp_synth.h)",
-            "config": {"workload": args.workload + ": " + desc, "n": n, "d": d, "density": dens,
-                       "tightness": tight, "seed": seed},
+            "config": workload_config(args),
             "impl": "reference",
-            "cpu_baseline": {"value": val, "unit": unit, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

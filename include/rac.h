@@ -323,6 +323,22 @@ int rac_peer_region(const rac_ctx* ctx, void** region_dev);
 int rac_connect_peers_local(rac_ctx* ctx, void* const* regions /* [world] */, const int32_t* devices /* [world] */);
 /* RAC_LAYOUT_DENSE or RAC_LAYOUT_SPARSE (see RAC_OPT_SPARSE). */
 int32_t rac_layout(const rac_ctx* ctx);
+/* Which kernel runs a single-state enforcement on this context:
+ *   RAC_PATH_FUSED     persistent cooperative kernel (dense one-word layout)
+ *   RAC_PATH_ONE_BLOCK one thread block per state (small instances: the whole
+ *                      mask tensor is L2-sized; also the batched calls' kernel)
+ *   RAC_PATH_SPARSE    persistent cooperative kernel over the sparse layout
+ *   RAC_PATH_SHARDED   per-pass launches + exchange (world > 1 / virtual shards)
+ *   RAC_PATH_PEER      persistent kernel + peer-memory exchange (RAC_OPT_PEER)
+ *   RAC_PATH_WIDE      wide-domain persistent kernel (max dom > 64)
+ * RAC_EINVAL if ctx is NULL. */
+#define RAC_PATH_FUSED 0
+#define RAC_PATH_ONE_BLOCK 1
+#define RAC_PATH_SPARSE 2
+#define RAC_PATH_SHARDED 3
+#define RAC_PATH_PEER 4
+#define RAC_PATH_WIDE 5
+int32_t rac_path(const rac_ctx* ctx);
 /* Kernel launches enqueued by the last rac_enforce* call on this context. */
 int64_t rac_last_launch_count(const rac_ctx* ctx);
 

@@ -89,6 +89,12 @@ def _load():
         lib.orc_free.restype = None
         lib.orc_rac.argtypes = [P, u64p, u64p, i32p, i32p, ctypes.c_int]
         lib.orc_rac.restype = ctypes.c_int
+        lib.orc_rac_par.argtypes = [P, u64p, u64p, i32p, ctypes.c_int, ctypes.c_int]
+        lib.orc_rac_par.restype = ctypes.c_int
+        lib.orc_rac_many.argtypes = [P, ctypes.c_int, u64p, u64p, i32p, i32p, ctypes.c_int, ctypes.c_int]
+        lib.orc_rac_many.restype = ctypes.c_int
+        lib.orc_max_threads.argtypes = []
+        lib.orc_max_threads.restype = ctypes.c_int
         lib.orc_rac_seeded.argtypes = [P, u64p, i32p, ctypes.c_int, u64p, i32p, i32p, ctypes.c_int]
         lib.orc_rac_seeded.restype = ctypes.c_int
         lib.orc_search.argtypes = [P, u64p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, i32p,
@@ -216,6 +222,28 @@ class Oracle:
         st = lib.orc_rac(self._h, _u64p(d_in), _u64p(d_out), _i32p(it),
                          _i32p(rem) if rem is not None else None, 1 if full else 0)
         return st, d_out, int(it[0]), (rem.reshape(self.n, 64) if rem is not None else None)
+
+    def rac_par(self, d_in, full: bool = False, threads: int = 0):
+        """O1 with each step's variables split over `threads` OpenMP threads (0 =
+        all host cores; the all-core CPU baseline).  Returns (status, d_out, iterations)."""
+        lib = _load()
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        d_out = np.zeros(self.n, dtype=np.uint64)
+        it = np.zeros(1, dtype=np.int32)
+        st = lib.orc_rac_par(self._h, _u64p(d_in), _u64p(d_out), _i32p(it), 1 if full else 0, int(threads))
+        return st, d_out, int(it[0])
+
+    def rac_many(self, states, full: bool = False, threads: int = 0):
+        """O1 on every row of states [S, n], states spread over OpenMP threads.
+        Returns (status[S], d_out[S, n], iterations[S])."""
+        states = np.ascontiguousarray(states, dtype=np.uint64)
+        S = states.shape[0]
+        out = np.zeros_like(states)
+        it = np.zeros(S, dtype=np.int32)
+        st = np.zeros(S, dtype=np.int32)
+        _load().orc_rac_many(self._h, S, _u64p(states), _u64p(out), _i32p(it), _i32p(st), 1 if full else 0,
+                             int(threads))
+        return st, out, it
 
     def rac_seeded(self, d_in, seeds, full: bool = False, with_epochs: bool = True):
         """O5: Alg. 1 tensorAC(Vars, @changed = seeds) as written.  Returns like rac()."""
@@ -383,6 +411,11 @@ def certify_trajectory_synth(n: int, d: int, dens_q32: int, t_q16: int, seed: in
     return int(_load().orc_certify_trajectory_synth(n, d, dens_q32, t_q16, seed, _u64p(d_in), _u64p(d_out),
                                                     _i32p(rem), int(iterations), int(status), 1 if full else 0,
                                                     int(threads)))
+
+
+def max_threads() -> int:
+    """OpenMP threads the oracle's parallel legs use by default (the host's cores)."""
+    return int(_load().orc_max_threads())
 
 
 def row_supported_synth(n: int, d: int, dens_q32: int, t_q16: int, seed: int, x: int, a: int, D) -> bool:

@@ -382,6 +382,75 @@ int orc_rac(const orc_csp *c, const uint64_t *d_in, uint64_t *d_out, int *iterat
 }
 
 /*
+ * O1 on `threads` host threads (0 = all), for the CPU baseline timed on every
+ * core of the host: the same synchronous step as orc_rac -- every variable's
+ * new word depends only on prev -- with the variables of a step split over
+ * OpenMP threads, then the same wipeout-first / convergence checks.  No removal
+ * epochs.  Results equal orc_rac for every thread count (tests/test_oracle.py).
+ */
+int orc_rac_par(const orc_csp *c, const uint64_t *d_in, uint64_t *d_out, int *iterations, int full, int threads) {
+  int n = c->n;
+  uint64_t *prev = (uint64_t *)calloc((size_t)n, sizeof(uint64_t));
+  uint64_t *next = (uint64_t *)calloc((size_t)n, sizeof(uint64_t));
+  if (!prev || !next) { free(prev); free(next); return ORC_EINVAL; }
+  memcpy(prev, d_in, (size_t)n * sizeof(uint64_t));
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#endif
+  int k = 0, status = ORC_OK;
+  for (;;) {
+    ++k;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+    for (int x = 0; x < n; ++x) {
+      uint64_t nx = prev[x];
+      for (int a = 0; a < c->dom[x]; ++a) {
+        if (!((prev[x] >> a) & 1ULL)) continue;
+        for (int kk = 0; kk < c->deg[x]; ++kk) {
+          int y = c->nbr[x][kk];
+          if ((c->sup[x][(size_t)kk * c->dom[x] + a] & prev[y]) == 0) { nx &= ~(1ULL << a); break; }
+        }
+      }
+      next[x] = nx;
+    }
+    int wipe = 0, changed = 0;
+    for (int x = 0; x < n; ++x) {
+      if (next[x] == 0) wipe = 1;
+      if (next[x] != prev[x]) changed = 1;
+    }
+    memcpy(prev, next, (size_t)n * sizeof(uint64_t));
+    if (wipe && !full) { status = ORC_WIPEOUT; break; }
+    if (!changed) { status = wipe ? ORC_WIPEOUT : ORC_OK; break; }
+  }
+  memcpy(d_out, prev, (size_t)n * sizeof(uint64_t));
+  *iterations = k;
+  free(prev); free(next);
+  return status;
+}
+
+/* O1 on S independent states (the batched workload), states spread over
+ * `threads` OpenMP threads (0 = all); state s at d_in + s*n.  No epochs. */
+int orc_rac_many(const orc_csp *c, int S, const uint64_t *d_in, uint64_t *d_out, int *iterations, int *status,
+                 int full, int threads) {
+#ifdef _OPENMP
+  if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+  for (int s = 0; s < S; ++s)
+    status[s] = orc_rac(c, d_in + (size_t)s * c->n, d_out + (size_t)s * c->n, iterations + s, NULL, full);
+  return 0;
+}
+
+int orc_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+/*
  * O5: Alg. 1 tensorAC(Vars, @changed) as written:
  *   while |@changed| != 0:
  *     Vars = tensorRevise(Vars, @changed)   -- (x,a) kept iff for every y in

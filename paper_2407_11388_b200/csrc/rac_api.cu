@@ -137,6 +137,11 @@ struct rac_ctx {
   unsigned* wslots = nullptr;
   int wide_grid = 0;
   size_t wide_smem = 0;
+  // rac_state (one block per state): batched mode and small single instances
+  StateParams state_geom{};  // shared-memory layout (state_layout)
+  size_t state_smem = 0;
+  int state_T = 128;         // threads per block
+  bool small = false;        // single instance small enough for one block
   int64_t launches = 0;
   bool broken = false;
   std::string err;
@@ -380,9 +385,44 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
     c->fused_grid = std::min(c->fused_grid, c->max_ctas);
     c->pass_grid = std::min(c->pass_grid, c->max_ctas);
   }
+  // rac_state geometry (dense layout, one GPU): the whole mask tensor of a
+  // small instance is at most a few hundred KB, which one block streams from L2
+  // faster than a cooperative grid can be launched and synchronised
+  if (!c->sparse && c->world == 1 && n <= 8192) {
+    c->state_smem = state_layout(c->state_geom, n, c->dmax, c->W, c->rows_pad, c->pw, 48 * 1024);
+    if (c->state_smem > 200 * 1024) c->state_smem = 0;
+    const char* st = getenv("RAC_STATE_T");  // A/B knob (tooling only)
+    if (st) c->state_T = atoi(st);
+    const char* sm = getenv("RAC_SMALL_BYTES");  // A/B knob (tooling only)
+    const double small_bytes = sm ? atof(sm) : 256.0 * 1024;
+    c->small = c->state_smem > 0 && c->vshards == 1 && !c->nccl_self && (double)mbytes <= small_bytes;
+  }
   CKC(cudaStreamSynchronize(c->stream));
 #undef CKC
   return 0;
+}
+
+StateParams state_params(const rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
+                         uint32_t flags) {
+  StateParams sp = c->state_geom;
+  sp.M = c->M;
+  sp.col_stride = c->col_stride;
+  sp.n = c->n;
+  sp.dmax = c->dmax;
+  sp.P = c->P;
+  sp.pw = c->pw;
+  sp.dommask = c->dommask;
+  sp.d_in = d_in;
+  sp.d_out = d_out;
+  sp.iters = iters;
+  sp.status = status;
+  sp.seed_var = nullptr;
+  sp.seeds = nullptr;
+  sp.n_seeds = -1;
+  sp.removed_at = nullptr;
+  sp.flags = flags;
+  sp.s0 = 0;
+  return sp;
 }
 
 PassGeom geom_for(const rac_ctx* c, int x_lo, int x_hi) {
@@ -618,21 +658,15 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
   p.dbg = c->dbg;
   if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
-  if (c->fused_grid == 1 && !c->peer && !c->sparse && (n_seeds < 0 || n_seeds == 1)) {
-    // One CTA is enough: run the single-CTA variant (removal bits in shared
-    // memory, __syncthreads as the pass barrier) -- the batched per-state
-    // kernel with one state.
-    BatchParams b{};
-    b.g = geom_for(c, 0, c->n);
-    b.dommask = c->dommask;
-    b.d_in = d_in;
-    b.d_out = d_out;
-    b.iters = iters;
-    b.status = status;
-    b.seed_var = n_seeds == 1 ? seeds : nullptr;  // one seed (or NULL = root call)
-    b.removed_at = removed_at;
-    b.flags = flags;
-    CK(c, launch_batch(c->W, c->G, b, 1, fused_smem(c->dbytes, c->n) + (size_t)c->n * 8, s));
+  if (c->small && !c->peer && !c->sparse) {
+    // A small instance is latency-bound: one block runs the whole enforcement
+    // (rac_state: D, removal bits and column lists in shared memory,
+    // __syncthreads as the pass barrier, an ordinary launch).
+    StateParams sp = state_params(c, d_in, d_out, iters, status, flags);
+    sp.seeds = seeds;
+    sp.n_seeds = n_seeds;
+    sp.removed_at = removed_at;
+    CK(c, launch_state(c->W, c->state_T, sp, 1, c->state_smem, s));
     c->launches++;
     return 0;
   }
@@ -1150,9 +1184,24 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   if (n_states == 0) return 0;
   CK(c, cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  const char* impl = getenv("RAC_BATCH_IMPL");  // A/B knob (tooling only): "bs" = bit-sliced N5
+  const bool want_bs = impl && strcmp(impl, "bs") == 0;
+  if (!want_bs && c->state_smem > 0) {
+    // Default: one block per state (rac_state): each state runs its own
+    // passes with no cross-state barrier; the relation stays L2-resident.
+    StateParams sp = state_params(c, d_in_dev, d_out_dev, iterations_dev, status_dev, flags);
+    sp.seed_var = seed_var_dev;
+    const int T = getenv("RAC_STATE_T") ? c->state_T : 128;
+    // launches of at most 65535 blocks (the grid's x limit is larger, but the
+    // state index arithmetic stays in int)
+    for (int s0 = 0; s0 < n_states; s0 += 65535) {
+      sp.s0 = s0;
+      CK(c, launch_state(c->W, T, sp, std::min(65535, n_states - s0), c->state_smem, st));
+      c->launches++;
+    }
+    return 0;
+  }
   // Bit-sliced path (N5): 32 states per 32-bit word, per-word CTA groups.
-  const char* impl = getenv("RAC_BATCH_IMPL");
-  const bool want_bs = !(impl && strcmp(impl, "state") == 0);
   const int rows = c->n * c->dmax;
   const int RB = (rows + 255) / 256;
   bool use_table = batch_bs_smem(c->n, c->dmax, c->W, true) <= 96 * 1024;
@@ -1370,6 +1419,14 @@ int64_t rac_relation_bytes(const rac_ctx* c) {
 }
 int32_t rac_layout(const rac_ctx* c) { return c ? (c->sparse ? RAC_LAYOUT_SPARSE : RAC_LAYOUT_DENSE) : RAC_EINVAL; }
 int64_t rac_last_launch_count(const rac_ctx* c) { return c ? c->launches : RAC_EINVAL; }
+int32_t rac_path(const rac_ctx* c) {
+  if (!c) return RAC_EINVAL;
+  if (c->wide) return RAC_PATH_WIDE;
+  if (c->peer) return RAC_PATH_PEER;
+  if (c->use_nccl() || c->vshards > 1) return RAC_PATH_SHARDED;
+  if (c->sparse) return RAC_PATH_SPARSE;
+  return c->small ? RAC_PATH_ONE_BLOCK : RAC_PATH_FUSED;
+}
 
 int rac_local_range(const rac_ctx* c, int32_t* x_lo, int32_t* x_hi) {
   if (!c || !x_lo || !x_hi) return RAC_EINVAL;

@@ -148,6 +148,30 @@ struct BatchParams {
   uint32_t flags;
 };
 
+// rac_state (rac_state.cu): one block per domain state.
+struct StateParams {
+  const uint8_t* M;         // column-major masks (all rows of the instance)
+  size_t col_stride;        // bytes per column
+  int n, dmax;
+  const uint32_t* P;        // presence bitmap [n][pw]
+  int pw;
+  const uint64_t* dommask;  // [n]
+  const uint64_t* d_in;     // [.][n] states (state s0 + blockIdx.x)
+  uint64_t* d_out;
+  int32_t* iters;
+  int32_t* status;
+  const int32_t* seed_var;  // nullable [.]: per-state seed variable (-1 = all)
+  const int32_t* seeds;     // single-state seeded call: device [n_seeds] (read if n_seeds > 0)
+  int n_seeds;              // < 0: not a seed-list call; 0: empty @changed (no pass)
+  int32_t* removed_at;      // nullable (single-state launches): [n*64], pre-zeroed
+  uint32_t flags;
+  int s0;                   // first state of this launch in the caller's arrays
+  int nvec;                 // 16-byte vectors per column
+  uint32_t off_R, off_live, off_vx, off_list, off_nlist, off_P;  // shared-memory layout (state_layout)
+};
+size_t state_layout(StateParams& p, int n, int dmax, int W, int rows_pad, int pw, size_t p_cap);
+cudaError_t launch_state(int W, int T, const StateParams& p, int n_states, size_t smem, cudaStream_t s);
+
 struct BatchBSParams {
   const uint8_t* M;
   size_t col_stride;

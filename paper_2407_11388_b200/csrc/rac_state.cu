@@ -1,0 +1,306 @@
+// rac_state.cu -- one thread block per domain state: the batched mode (SURVEY
+// §8(a7), many search-tree nodes, Alg. 2) and the
+// single-CTA enforcement of small instances (C1-sized, latency-bound).
+//
+// Each block runs the whole RAC enforcement of ITS state on its own: Eq. 1
+// (intersection form of line 59) with Alg. 1's loop
+// control (lines 198-210), D_t / the removal bits / the tested-column list in
+// shared memory, __syncthreads as the pass barrier, so a state stops at its
+// own pass (freeze-on-stop is free) and no block ever waits for another.
+// States are independent: the grid is simply one block per state and the
+// hardware keeps as many resident as fit (no grid-wide barrier, no exchange).
+//
+// Support test (a3/a4): pass t tests the live rows (x,a) against the columns
+// of the variables changed in pass t-1 (all columns in pass 1 of a root call,
+// the seed variables in pass 1 of a seeded call -- Alg. 1's Cons[:, @changed],
+// line 215, Prop. 2).  Work item = one 16-byte vector of a
+// tested column of the column-major mask tensor (16/W rows (x, a..a+16/W-1)),
+// loaded with ld.global.nc (the relation of a batched instance is shared by
+// every block and stays L2-resident) only when one of its rows is live in
+// D_{t-1} and c_xy is declared (presence bitmap staged in shared memory):
+// dead rows, absent pairs and the diagonal cost no load.  mask & D(y) == 0 on
+// a live row is a removal (atomicOr into R[x] in shared memory).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rac_internal.cuh"
+
+namespace rac {
+
+namespace {
+
+constexpr uint32_t kFullS = 1u;  // RAC_FULL_FIXPOINT
+constexpr int kOKs = 0, kWIPEOUTs = 1;
+constexpr int kUs = 8;  // vector loads in flight per thread
+
+// Block-wide exclusive scan of one int per thread; returns the prefix, *total
+// gets the sum.  `sc` holds blockDim/32 ints.
+__device__ __forceinline__ int scan_excl(int v, int* total, int* sc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += u;
+  }
+  if (nw == 1) {
+    *total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+  }
+  __syncthreads();
+  if (lane == 31) sc[w] = x;
+  __syncthreads();
+  int base = 0, tot = 0;
+  for (int k = 0; k < nw; ++k) {
+    const int s = sc[k];
+    if (k < w) base += s;
+    tot += s;
+  }
+  *total = tot;
+  return base + x - v;
+}
+
+// live rows of vector v (L = 16/W rows r0 = v*L ..) as an L-bit mask
+template <int W>
+__device__ __forceinline__ uint32_t vec_live(const uint8_t* Db, int v, int n, int dmax, bool aligned) {
+  constexpr int L = 16 / W;
+  constexpr uint32_t LM = L == 32 ? 0xffffffffu : ((1u << L) - 1u);
+  const int r0 = v * L;
+  if (aligned) {  // dmax % L == 0: the L rows are values a0.. of one variable
+    const int x = r0 / dmax;
+    if (x >= n) return 0u;
+    const int a0 = r0 - x * dmax;
+    return (uint32_t)(load_w<W>(Db + x * W) >> a0) & LM;
+  }
+  uint32_t m = 0;
+  for (int i = 0; i < L; ++i) {
+    const int r = r0 + i, x = r / dmax;
+    if (x >= n) break;
+    const int a = r - x * dmax;
+    m |= (uint32_t)((load_w<W>(Db + x * W) >> a) & 1u) << i;
+  }
+  return m;
+}
+
+template <int W, int T>
+__global__ void __launch_bounds__(T) rac_state(StateParams p) {
+  constexpr int L = 16 / W;
+  extern __shared__ uint4 smem4[];
+  __shared__ int sc[T / 32 > 0 ? T / 32 : 1];
+  const int n = p.n, dmax = p.dmax, tid = threadIdx.x;
+  const int s = blockIdx.x;
+  const int nvec = p.nvec;  // 16-byte vectors per column
+  const bool aligned = (dmax % L) == 0;
+  // shared memory: D | R (u64 per variable) | live[nvec] (u32) | vx[nvec] (u16) | list | nlist | P (optional)
+  uint8_t* Db = reinterpret_cast<uint8_t*>(smem4);
+  unsigned long long* R = reinterpret_cast<unsigned long long*>(Db + p.off_R);
+  uint32_t* live = reinterpret_cast<uint32_t*>(Db + p.off_live);
+  uint16_t* vx = reinterpret_cast<uint16_t*>(Db + p.off_vx);
+  uint16_t* list = reinterpret_cast<uint16_t*>(Db + p.off_list);
+  uint16_t* nlist = reinterpret_cast<uint16_t*>(Db + p.off_nlist);
+  const uint32_t* Ps = p.off_P ? reinterpret_cast<const uint32_t*>(Db + p.off_P) : nullptr;
+
+  // ---- stage D_0 = d_in (bits beyond dom dropped), P, per-vector variable
+  const uint64_t* din = p.d_in + (size_t)(p.s0 + s) * n;
+  for (int x = tid; x < n; x += T) {
+    store_w<W>(Db + x * W, __ldg(din + x) & __ldg(p.dommask + x));
+    R[x] = 0ull;
+  }
+  if (Ps)
+    for (int i = tid; i < n * p.pw; i += T) const_cast<uint32_t*>(Ps)[i] = __ldg(p.P + i);
+  for (int v = tid; v < nvec; v += T) {
+    const int r0 = v * L, x0 = r0 / dmax, x1 = (r0 + L - 1) / dmax;
+    // one variable per vector (absent-pair skip allowed) -> x0, else 0xffff
+    vx[v] = (x0 == x1 && x0 < n) ? (uint16_t)x0 : (uint16_t)0xffffu;
+  }
+  // ---- initial tested columns: the seeds (seeded call) or every column
+  int cnt = n;
+  bool all_cols = true;
+  {
+    const int sv = p.seed_var ? p.seed_var[p.s0 + s] : -1;
+    if (p.n_seeds >= 0 || (sv >= 0 && sv < n)) {
+      all_cols = false;
+      // flags in nlist (as u16), then compact into list
+      for (int i = tid; i < n; i += T) nlist[i] = 0;
+      __syncthreads();
+      if (p.n_seeds >= 0) {
+        for (int i = tid; i < p.n_seeds; i += T) {
+          const int y = p.seeds[i];
+          if (y >= 0 && y < n) nlist[y] = 1;
+        }
+      } else if (tid == 0) {
+        nlist[sv] = 1;
+      }
+      __syncthreads();
+      int c = 0, total = 0;
+      const int per = (n + T - 1) / T, b = min(n, tid * per), e = min(n, b + per);
+      for (int i = b; i < e; ++i) c += nlist[i] != 0;
+      int pos = scan_excl(c, &total, sc);
+      for (int i = b; i < e; ++i)
+        if (nlist[i]) list[pos++] = (uint16_t)i;
+      cnt = total;
+    }
+  }
+  __syncthreads();
+  int has_empty = 0;
+  for (int x = tid; x < n; x += T) has_empty |= load_w<W>(Db + x * W) == 0;
+  has_empty = __syncthreads_or(has_empty);
+  for (int v = tid; v < nvec; v += T) live[v] = vec_live<W>(Db, v, n, dmax, aligned);
+  __syncthreads();
+
+  const bool full = (p.flags & kFullS) != 0;
+  int t = 0, status = kOKs;
+  if (cnt == 0) {  // empty @changed: no pass, status from D_in
+    status = has_empty ? kWIPEOUTs : kOKs;
+  } else {
+    for (;;) {
+      ++t;
+      // ---- a3/a4: sweep (items = tested column c x vector v)
+      int c = tid / nvec, v = tid - c * nvec;
+      bool any_rm = false;
+      while (c < cnt) {
+        uint4 m[kUs];
+        int yy[kUs], vv[kUs];
+        uint32_t lv[kUs];
+#pragma unroll
+        for (int u = 0; u < kUs; ++u) {
+          lv[u] = 0u;
+          if (c < cnt) {
+            const int y = all_cols ? c : (int)list[c];
+            const uint32_t l = live[v];
+            const int xv = vx[v];
+            // skip: no live row; or the vector's variable has no declared c_xy
+            // (absent pair / diagonal: all-ones masks never fail a non-empty D(y))
+            bool need = l != 0u;
+            if (need && xv != 0xffff && (xv == y || (Ps && !((Ps[xv * p.pw + (y >> 5)] >> (y & 31)) & 1u))))
+              need = false;
+            if (need) {
+              lv[u] = l;
+              yy[u] = y;
+              vv[u] = v;
+              m[u] = ldg_stream(reinterpret_cast<const uint4*>(p.M + (size_t)y * p.col_stride) + v);
+            }
+            v += T;
+            while (v >= nvec) { v -= nvec; ++c; }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUs; ++u) {
+          if (!lv[u]) continue;
+          const int y = yy[u];
+          const uint64_t dv = load_w<W>(Db + y * W);
+          const uint32_t z = zero_lanes<W>(and4(m[u], rep16<W>(dv))) & lv[u];
+          if (!z) continue;
+          for (uint32_t zz = z; zz; zz &= zz - 1u) {
+            const int r = vv[u] * L + __ffs(zz) - 1;
+            const int x = r / dmax, a = r - x * dmax;
+            // R2: an all-ones absent pair only "fails" on an empty D(y); then P decides
+            if (dv == 0ull && !((__ldg(p.P + (size_t)x * p.pw + (y >> 5)) >> (y & 31)) & 1u)) continue;
+            atomicOr(&R[x], 1ull << a);
+            any_rm = true;
+            if (p.removed_at) p.removed_at[(size_t)x * 64 + a] = t;
+          }
+        }
+      }
+      const int removed_any = __syncthreads_or(any_rm);
+      // ---- a5: D_t = D_{t-1} & ~R; the changed variables (R[x] != 0: marks are
+      // made on live rows only) become the next pass's tested columns
+      int changed = 0, wipe = has_empty;
+      if (removed_any) {
+        const int per = (n + T - 1) / T, b = min(n, tid * per), e = min(n, b + per);
+        int cx = 0;
+        for (int x = b; x < e; ++x) cx += R[x] != 0ull;
+        int total = 0;
+        int pos = scan_excl(cx, &total, sc);
+        for (int x = b; x < e; ++x) {
+          const unsigned long long r = R[x];
+          if (!r) continue;
+          const uint64_t nd = load_w<W>(Db + x * W) & ~r;
+          store_w<W>(Db + x * W, nd);
+          R[x] = 0ull;
+          wipe |= nd == 0ull;
+          nlist[pos++] = (uint16_t)x;
+        }
+        changed = total;
+        wipe = __syncthreads_or(wipe);
+        uint16_t* tmp = list;
+        list = nlist;
+        nlist = tmp;
+        all_cols = false;
+        cnt = total;
+      }
+      has_empty = wipe;
+      if (wipe && !full) { status = kWIPEOUTs; break; }          // Alg. 1
+      if (!changed) { status = wipe ? kWIPEOUTs : kOKs; break; }  // Prop. 1 end condition
+      for (int v2 = tid; v2 < nvec; v2 += T) live[v2] = vec_live<W>(Db, v2, n, dmax, aligned);
+      __syncthreads();
+    }
+  }
+  uint64_t* dout = p.d_out + (size_t)(p.s0 + s) * n;
+  for (int x = tid; x < n; x += T) dout[x] = load_w<W>(Db + x * W);
+  if (tid == 0) {
+    p.iters[p.s0 + s] = t;
+    p.status[p.s0 + s] = status;
+  }
+}
+
+template <int W, int T>
+struct LaunchS {
+  static cudaError_t go(const StateParams& p, int n_states, size_t smem, cudaStream_t st) {
+    auto k = rac_state<W, T>;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k<<<n_states, T, smem, st>>>(p);
+    return cudaGetLastError();
+  }
+};
+
+}  // namespace
+
+// Shared-memory layout of rac_state for an instance (offsets into the dynamic
+// buffer); returns the total bytes.  P is staged only if it fits in `p_cap`.
+size_t state_layout(StateParams& p, int n, int dmax, int W, int rows_pad, int pw, size_t p_cap) {
+  const int L = 16 / W;
+  p.nvec = (rows_pad + L - 1) / L;
+  size_t off = (((size_t)n * W) + 15) & ~(size_t)15;  // D
+  p.off_R = (uint32_t)off;
+  off += (size_t)n * 8;
+  p.off_live = (uint32_t)off;
+  off += ((size_t)p.nvec * 4 + 15) & ~(size_t)15;
+  p.off_vx = (uint32_t)off;
+  off += ((size_t)p.nvec * 2 + 15) & ~(size_t)15;
+  p.off_list = (uint32_t)off;
+  off += ((size_t)n * 2 + 15) & ~(size_t)15;
+  p.off_nlist = (uint32_t)off;
+  off += ((size_t)n * 2 + 15) & ~(size_t)15;
+  const size_t pb = (size_t)n * pw * 4;
+  if (pb <= p_cap) {
+    p.off_P = (uint32_t)off;
+    off += (pb + 15) & ~(size_t)15;
+  } else {
+    p.off_P = 0;
+  }
+  return off;
+}
+
+cudaError_t launch_state(int W, int T, const StateParams& p, int n_states, size_t smem, cudaStream_t st) {
+#define RAC_T_SWITCH(WW)                                        \
+  switch (T) {                                                  \
+    case 32: return LaunchS<WW, 32>::go(p, n_states, smem, st);   \
+    case 128: return LaunchS<WW, 128>::go(p, n_states, smem, st); \
+    case 256: return LaunchS<WW, 256>::go(p, n_states, smem, st); \
+    default: return cudaErrorInvalidValue;                      \
+  }
+  switch (W) {
+    case 1: RAC_T_SWITCH(1)
+    case 2: RAC_T_SWITCH(2)
+    case 4: RAC_T_SWITCH(4)
+    case 8: RAC_T_SWITCH(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef RAC_T_SWITCH
+}
+
+}  // namespace rac

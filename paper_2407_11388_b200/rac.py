@@ -75,7 +75,9 @@ EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforc
            "rac_enforce_batch_seeded", "rac_search", "rac_batch_pass_eval", "rac_n_vars", "rac_max_dom", "rac_mask_bytes", "rac_words_per_var",
            "rac_layout", "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
            "rac_peer_handle", "rac_connect_peers", "rac_peer_region", "rac_connect_peers_local",
-           "rac_last_launch_count", "rac_last_error", "rac_destroy"]
+           "rac_last_launch_count", "rac_path", "rac_last_error", "rac_destroy"]
+
+PATHS = {0: "fused", 1: "one_block", 2: "sparse", 3: "sharded", 4: "peer", 5: "wide"}
 
 
 def _load() -> ctypes.CDLL:
@@ -117,6 +119,7 @@ def _load() -> ctypes.CDLL:
         "rac_peer_region": (ctypes.c_int, [P, ctypes.POINTER(P)]),
         "rac_connect_peers_local": (ctypes.c_int, [P, ctypes.POINTER(P), i32p]),
         "rac_last_launch_count": (i64, [P]),
+        "rac_path": (i32, [P]),
         "rac_last_error": (ctypes.c_char_p, [P]),
         "rac_destroy": (None, [P]),
     }
@@ -386,6 +389,11 @@ class RacContext:
     @property
     def last_launch_count(self) -> int:
         return int(lib.rac_last_launch_count(self._h))
+
+    @property
+    def path(self) -> str:
+        """rac_path: which kernel runs a single-state enforcement ("fused", "one_block", ...)."""
+        return PATHS[int(lib.rac_path(self._h))]
 
     def local_range(self) -> Tuple[int, int]:
         lo, hi = ctypes.c_int32(0), ctypes.c_int32(0)

@@ -85,9 +85,14 @@ def test_packer_matches_oracle_layout(rac, n, d, p, t):
 
 
 # ----------------------------------------------------------------------------- corpora
-def test_spec_corpus(rac):
+@pytest.mark.parametrize("path", ["one-block", "fused"])
+def test_spec_corpus(rac, path, monkeypatch):
     """SPEC.md acceptance corpus shape: 1000 instances, n 2..20, d 1..6,
-    density 0.1..1, tightness 0..0.9; W-root and W-rand; stop and full modes."""
+    density 0.1..1, tightness 0..0.9; W-root and W-rand; stop and full modes --
+    through the one-block kernel (rac_state, the default for small instances)
+    and through the cooperative rac_fused kernel (RAC_SMALL_BYTES=0)."""
+    if path == "fused":
+        monkeypatch.setenv("RAC_SMALL_BYTES", "0")
     for k, inst in enumerate(I.random_corpus(1000)):
         ctx = rac.RacContext.from_instance(inst)
         orc = oracle.Oracle.from_instance(inst)
@@ -403,6 +408,7 @@ def test_forced_layouts(rac, layout, monkeypatch):
     """Every pass on the row-major copy only, or on the column-major tensor only
     (RAC_FORCE_LAYOUT), gives the oracle's results: both sweeps are exact."""
     monkeypatch.setenv("RAC_FORCE_LAYOUT", layout)
+    monkeypatch.setenv("RAC_SMALL_BYTES", "0")  # tiny instances through rac_fused too (not the one-block path)
     for k, inst in enumerate(I.random_corpus(150, seed0=61)):
         ctx = rac.RacContext.from_instance(inst)
         orc = oracle.Oracle.from_instance(inst)

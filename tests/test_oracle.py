@@ -826,3 +826,31 @@ def test_wide_is_ac_negative():
     bits = WD.bits_of(D, n, wo.wq)
     bits[3, :] = False
     assert not wo.is_ac(WD.words_of(bits))
+
+
+def test_parallel_o1_equals_o1():
+    """orc_rac_par (the all-core CPU baseline) equals orc_rac for 1, 3 and 8 threads,
+    stop and full mode, on the corpus and a C2-shaped instance."""
+    insts = I.random_corpus(150, seed0=23)
+    for k, inst in enumerate(insts):
+        orc = oracle.Oracle.from_instance(inst)
+        d_in = inst.full_domains() if k % 2 else synth.w_rand(inst.dom, 0.85, seed=k)
+        for full in (False, True):
+            st, out, it, _ = orc.rac(d_in, full=full, with_epochs=False)
+            for th in (1, 3, 8):
+                g = orc.rac_par(d_in, full=full, threads=th)
+                assert g[0] == st and g[2] == it and np.array_equal(g[1], out), (k, full, th)
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.3)
+    orc = oracle.Oracle.from_synth(500, 20, dq, tq, 1)
+    d_in = synth.w_rand(np.full(500, 20), 0.9, 2)
+    st, out, it, _ = orc.rac(d_in, with_epochs=False)
+    g = orc.rac_par(d_in, threads=4)
+    assert (g[0], g[2]) == (st, it) and np.array_equal(g[1], out)
+    assert oracle.max_threads() >= 1
+    inst = synth.random_csp(60, 8, 0.5, 0.4, 3)
+    orc = oracle.Oracle.from_instance(inst)
+    states = np.stack([synth.w_rand(inst.dom, 0.8, seed=s) for s in range(40)])
+    st, out, it = orc.rac_many(states, threads=4)
+    for s in range(40):
+        o = orc.rac(states[s], with_epochs=False)
+        assert (st[s], it[s]) == (o[0], o[2]) and np.array_equal(out[s], o[1])

@@ -28,6 +28,6 @@ for tool in ${PEER_TOOLS:-memcheck synccheck}; do
      python tools/sanitize_cases.py peer > $OUT/sanitize_${tool}_peer.log 2>&1
   rc=$?
   summ=$(grep "ERROR SUMMARY" $OUT/sanitize_${tool}_peer.log | tr '\n' ' ')
-  pass=$(grep -c "CASE peer PASS" $OUT/sanitize_${tool}_peer.log)
+  pass=$(grep -c "peer rank .* OK" $OUT/sanitize_${tool}_peer.log)
   echo "$tool peer(2 procs) rc=$rc ranks_pass=$pass | $summ" | tee -a $OUT/sanitize_summary.txt
 done

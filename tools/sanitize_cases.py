@@ -6,7 +6,8 @@ initcheck) over every enforcement kernel, each checked against the CPU oracle:
   sparse  -- rac_fused<W,0> over the sparse arc-block layout (density 0.25)
   vshard  -- rac_pass + rac_shard_{init,seed,slice,update,finalize} (3 row blocks)
   wide    -- wide_fused (d=128, propagating), root + seeded
-  batch   -- rac_batch_bs (64 W-dive states) and the single-CTA rac_batch path
+  state   -- rac_state (one block per state) on single instances up to C2 size
+  batch   -- rac_state and rac_batch_bs on 64 W-dive states, and C1 (one block)
   peer    -- one rank of a 2-process RAC_OPT_PEER group (run under torchrun)
 
 Exit status 0 iff every result equals the oracle's.
@@ -59,6 +60,13 @@ def main(case):
         for (n, d, p, t) in ((500, 20, 1.0, 0.3), (600, 32, 1.0, 0.66)):
             ctx, orc = gen_case(n, d, p, t, 1)
             ok &= run_common(ctx, orc, n, d, "fused n=%d" % n)
+    elif case == "state":
+        # the one-block kernel (rac_state) on instances beyond its default size
+        os.environ["RAC_SMALL_BYTES"] = "1e12"
+        for (n, d, p, t) in ((500, 20, 1.0, 0.3), (150, 7, 0.6, 0.5)):
+            ctx, orc = gen_case(n, d, p, t, 1)
+            assert ctx.path == "one_block"
+            ok &= run_common(ctx, orc, n, d, "state n=%d" % n)
     elif case == "sparse":
         ctx, orc = gen_case(800, 32, 0.25, 0.6, 2, layout="sparse")
         assert ctx.layout == "sparse"
@@ -91,7 +99,9 @@ def main(case):
         its = torch.zeros(S, dtype=torch.int32, device="cuda")
         sts = torch.zeros(S, dtype=torch.int32, device="cuda")
         sv = torch.from_numpy(np.asarray(svars, dtype=np.int32)).cuda()
-        for seeded in (False, True):
+        for impl, seeded in (("state", False), ("state", True), ("bs", False), ("bs", True)):
+            if impl == "bs":
+                os.environ["RAC_BATCH_IMPL"] = "bs"
             if seeded:
                 ctx.enforce_batch_seeded(S, din, dout, its, sts, sv)
             else:
@@ -101,7 +111,8 @@ def main(case):
             for s in range(S):
                 o = orc.rac(states[s], with_epochs=False)
                 ok &= (int(sts[s]), int(its[s])) == (o[0], o[2]) and np.array_equal(out[s], o[1])
-            print("batch seeded=%s" % seeded, "OK" if ok else "MISMATCH", flush=True)
+            print("batch %s seeded=%s" % (impl, seeded), "OK" if ok else "MISMATCH", flush=True)
+        os.environ.pop("RAC_BATCH_IMPL", None)
         c1 = synth.random_csp(20, 8, 0.5, 0.4, 1)
         ctx1, orc1 = rac.RacContext.from_instance(c1), oracle.Oracle.from_instance(c1)
         ok &= same(ctx1.enforce(c1.full_domains(), removed_at=True), orc1.rac(c1.full_domains()), "single-cta C1")
