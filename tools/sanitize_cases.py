@@ -60,6 +60,15 @@ def main(case):
         for (n, d, p, t) in ((500, 20, 1.0, 0.3), (600, 32, 1.0, 0.66)):
             ctx, orc = gen_case(n, d, p, t, 1)
             ok &= run_common(ctx, orc, n, d, "fused n=%d" % n)
+        # many passes (the rotating per-pass buffers, hundreds of grid barriers):
+        # an equality chain inside a complete graph takes exactly n passes
+        from tests import _instances as I
+        inst = I.equality_chain(300, 8, embed_complete=True)
+        ctx, orc = rac.RacContext.from_instance(inst), oracle.Oracle.from_instance(inst)
+        assert ctx.path == "fused"
+        d_in = inst.full_domains()
+        d_in[0] = np.uint64(1)
+        ok &= same(ctx.enforce(d_in, removed_at=True), orc.rac(d_in), "fused chain n=300")
     elif case == "state":
         # the one-block kernel (rac_state) on instances beyond its default size
         os.environ["RAC_SMALL_BYTES"] = "1e12"
