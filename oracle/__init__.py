@@ -144,6 +144,9 @@ def _load():
         lib.orc_rac_wide.restype = ctypes.c_int
         lib.orc_wis_ac.argtypes = [P, u64p]
         lib.orc_wis_ac.restype = ctypes.c_int
+        lib.orc_wsearch.argtypes = [P, u64p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, i32p,
+                                    ctypes.POINTER(ctypes.c_int64)]
+        lib.orc_wsearch.restype = ctypes.c_int
         lib.orc_wac3.argtypes = [P, u64p, u64p]
         lib.orc_wac3.restype = ctypes.c_int
         _lib = lib
@@ -389,6 +392,16 @@ class WideOracle:
         assert rem.size == self.n * 64 * self.wq and d_in.size == self.n * self.wq
         return int(_load().orc_wcertify_trajectory(self._h, _u64p(d_in), _u64p(d_out), _i32p(rem), int(iterations),
                                                    int(status), 1 if full else 0))
+
+    def search(self, d_in, max_assignments: int = 0, all_solutions: bool = False, full: bool = False):
+        """O6w: Alg. 2 backtracking search over O1w.  Returns (result, solution, stats) like Oracle.search."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
+        sol = np.full(self.n, -1, dtype=np.int32)
+        st = (ctypes.c_int64 * 6)()
+        r = _load().orc_wsearch(self._h, _u64p(d_in), int(max_assignments), 1 if all_solutions else 0,
+                                1 if full else 0, _i32p(sol), st)
+        keys = ["assignments", "recurrences", "wipeouts", "solutions", "max_depth", "root_iterations"]
+        return r, sol, dict(zip(keys, [int(v) for v in st]))
 
     def ac3(self, d_in):
         """AC-3 to the fixpoint on wide domains.  Returns (status, d_out)."""

@@ -954,6 +954,92 @@ int orc_rac_wide(const orc_wcsp *c, const uint64_t *d_in, uint64_t *d_out, int *
   return status;
 }
 
+/*
+ * O6w: Alg. 2 backtracking search on wide domains,
+ * the same recursion as orc_search over O1w (engine "full": by Prop. 2 the
+ * seeded call tensorAC(Vars, [idx]) of line 392 follows the same trajectory
+ * after an assignment on an arc-consistent state, reading R12): min-domain
+ * variable (lowest index on ties), ascending values, assignment on a copy of
+ * the parent's domains.  stats as orc_search; returns 0 solution, 1 unsat,
+ * 2 budget exhausted.
+ */
+typedef struct {
+  const orc_wcsp *c;
+  int64_t budget;
+  int all, full;
+  int64_t *stats;
+  int32_t *solution;
+  char *assigned;
+  int found, out_of_budget;
+} orc_wsearch_ctx;
+
+static int wcount(const uint64_t *v, int wq) {
+  int k = 0;
+  for (int w = 0; w < wq; ++w) k += popc64(v[w]);
+  return k;
+}
+
+static int orc_wdfs(orc_wsearch_ctx *s, const uint64_t *D, int level) {
+  const orc_wcsp *c = s->c;
+  const int n = c->n, wq = c->wq;
+  const size_t nw = (size_t)n * wq;
+  int idx = -1, best = 1 << 30;
+  for (int x = 0; x < n; ++x) {
+    if (s->assigned[x]) continue;
+    const int k = wcount(D + (size_t)x * wq, wq);
+    if (k < best) { best = k; idx = x; }
+  }
+  s->assigned[idx] = 1;
+  uint64_t *child = (uint64_t *)malloc(nw * sizeof(uint64_t));
+  uint64_t *out = (uint64_t *)malloc(nw * sizeof(uint64_t));
+  int stop = 0;
+  for (int v = 0; v < 64 * wq && !stop; ++v) {
+    if (!wbit(D + (size_t)idx * wq, v)) continue;
+    if (s->budget > 0 && s->stats[0] >= s->budget) { s->out_of_budget = 1; stop = 1; break; }
+    memcpy(child, D, nw * sizeof(uint64_t));
+    for (int w = 0; w < wq; ++w) child[(size_t)idx * wq + w] = 0;
+    wset(child + (size_t)idx * wq, v); /* assign, lines 410-416 */
+    int it = 0;
+    const int st = orc_rac_wide(c, child, out, &it, NULL, s->full);
+    s->stats[0]++;
+    s->stats[1] += it;
+    if (st == ORC_WIPEOUT) { s->stats[2]++; continue; }
+    if (level + 1 > s->stats[4]) s->stats[4] = level + 1;
+    if (level + 1 == n) {
+      s->stats[3]++;
+      if (!s->found && s->solution)
+        for (int x = 0; x < n; ++x)
+          for (int b = 0; b < 64 * wq; ++b)
+            if (wbit(out + (size_t)x * wq, b)) { s->solution[x] = b; break; }
+      s->found = 1;
+      if (!s->all) stop = 1;
+      continue;
+    }
+    if (orc_wdfs(s, out, level + 1)) stop = 1;
+  }
+  free(child); free(out);
+  s->assigned[idx] = 0;
+  return stop;
+}
+
+int orc_wsearch(const orc_wcsp *c, const uint64_t *d_in, int64_t max_assignments, int all, int full,
+                int32_t *solution, int64_t *stats) {
+  const int n = c->n;
+  for (int k = 0; k < 6; ++k) stats[k] = 0;
+  uint64_t *root = (uint64_t *)malloc((size_t)n * c->wq * sizeof(uint64_t));
+  int it = 0;
+  const int st = orc_rac_wide(c, d_in, root, &it, NULL, full);
+  stats[5] = it;
+  if (st == ORC_WIPEOUT) { free(root); return 1; }
+  orc_wsearch_ctx s = {c, max_assignments, all, full, stats, solution, NULL, 0, 0};
+  s.assigned = (char *)calloc((size_t)n, 1);
+  orc_wdfs(&s, root, 0);
+  free(s.assigned);
+  free(root);
+  if (s.out_of_budget) return 2;
+  return s.found ? 0 : 1;
+}
+
 /* Arc consistency by definition on wide domains: 1 iff AC and no empty domain. */
 int orc_wis_ac(const orc_wcsp *c, const uint64_t *D) {
   const int wq = c->wq;

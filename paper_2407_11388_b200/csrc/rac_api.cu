@@ -120,8 +120,9 @@ struct rac_ctx {
   uint32_t* eval_buf = nullptr;          // rac_batch_pass_eval scratch
   size_t eval_cap = 0;
   int bs_dbg_ctas = 0;
-  uint64_t* h_in = nullptr;        // pinned
-  uint64_t* h_out = nullptr;
+  uint64_t* h_in = nullptr;        // pinned staging: [d_in words | seeds (seed_cap int32)]
+  uint64_t* h_out = nullptr;       // pinned + mapped: [d_out words | iters, status] written by the kernel
+  uint64_t* d_hout = nullptr;      // device view of h_out (zero-copy: no D2H copy in the blocking API)
   int32_t* h_scalars = nullptr;    // pinned [iters, status, done]
   cudaStream_t stream = nullptr;
   int sm_count = 0;
@@ -170,6 +171,37 @@ uint64_t dom_mask(int k) { return k >= 64 ? ~0ull : ((1ull << k) - 1ull); }
 
 int mask_bytes(int dmax) { return dmax <= 8 ? 1 : dmax <= 16 ? 2 : dmax <= 32 ? 4 : 8; }
 
+// Blocking-API staging: pinned h_in / device buf_in hold [d_in | seeds] so one
+// H2D copy moves both; h_out is pinned AND mapped: the kernels write D_out and
+// [iters, status] straight into it (zero-copy), so no D2H copy is enqueued.
+// (Re)allocates the input staging with room for `seeds` seed entries.
+cudaError_t alloc_staging(rac_ctx* c, size_t nb, size_t seeds) {
+  cudaFree(c->buf_in);
+  cudaFreeHost(c->h_in);
+  c->buf_in = nullptr;
+  c->h_in = nullptr;
+  c->buf_seeds = nullptr;
+  c->seed_cap = 0;
+  cudaError_t e = cudaMalloc(&c->buf_in, nb + seeds * 4);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->h_in, nb + seeds * 4);
+  if (e != cudaSuccess) return e;
+  c->buf_seeds = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c->buf_in) + nb);
+  c->seed_cap = seeds;
+  if (!c->h_out) {
+    e = cudaHostAlloc(&c->h_out, nb + 16, cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_hout), c->h_out, 0);
+  }
+  return e;
+}
+
+// cudaSetDevice only when another device is current (the call is not free).
+cudaError_t ensure_device(const rac_ctx* c) {
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e == cudaSuccess && cur == c->device) return cudaSuccess;
+  return cudaSetDevice(c->device);
+}
+
 void free_ctx(rac_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
@@ -198,7 +230,6 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->buf_out);
   cudaFree(c->buf_scalars);
   cudaFree(c->buf_removed);
-  cudaFree(c->buf_seeds);
   cudaFree(c->bs_X2);
   cudaFree(c->bs_bar);
   cudaFree(c->dbg);
@@ -358,12 +389,10 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
   c->sh.vcnt = c->sh.iters + 3;
   c->sh.seeded = c->sh.iters + 4;
   CKC(cudaMalloc(&c->sh.vlist, (size_t)n * 2 + 16));
-  CKC(cudaMalloc(&c->buf_in, (size_t)n * 8));
   CKC(cudaMalloc(&c->buf_out, (size_t)n * 8));
   CKC(cudaMalloc(&c->buf_scalars, 16));
   CKC(cudaMalloc(&c->buf_removed, (size_t)n * 64 * 4));
-  CKC(cudaMallocHost(&c->h_in, (size_t)n * 8));
-  CKC(cudaMallocHost(&c->h_out, (size_t)n * 8));
+  CKC(alloc_staging(c, (size_t)n * 8, 64));
   CKC(cudaMallocHost(&c->h_scalars, 16));
 
   // Launch geometry.  Fused path: a co-resident grid (cooperative launch),
@@ -389,7 +418,7 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
   // small instance is at most a few hundred KB, which one block streams from L2
   // faster than a cooperative grid can be launched and synchronised
   if (!c->sparse && c->world == 1 && n <= 8192) {
-    c->state_smem = state_layout(c->state_geom, n, c->dmax, c->W, c->rows_pad, c->pw, 48 * 1024);
+    c->state_smem = state_layout(c->state_geom, n, c->dmax, c->W, c->rows_pad, c->pw, 48 * 1024, 96 * 1024);
     if (c->state_smem > 200 * 1024) c->state_smem = 0;
     const char* st = getenv("RAC_STATE_T");  // A/B knob (tooling only)
     if (st) c->state_T = atoi(st);
@@ -568,12 +597,10 @@ int setup_wide(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt
   CKC(cudaMalloc(&c->wR, (size_t)n * c->WS * 8));
   CKC(cudaMalloc(&c->wslots, 64));
   CKC(cudaMalloc(&c->clist, (size_t)3 * n * 4));
-  CKC(cudaMalloc(&c->buf_in, nw * 8));
   CKC(cudaMalloc(&c->buf_out, nw * 8));
   CKC(cudaMalloc(&c->buf_scalars, 16));
   CKC(cudaMalloc(&c->buf_removed, nw * 64 * 4));
-  CKC(cudaMallocHost(&c->h_in, nw * 8));
-  CKC(cudaMallocHost(&c->h_out, nw * 8));
+  CKC(alloc_staging(c, nw * 8, 64));
   CKC(cudaMallocHost(&c->h_scalars, 16));
   CKC(wide_fused_grid(c->WS, c->wide_smem, c->sm_count, &c->wide_grid));
   // about four live rows per warp at most: small instances keep fewer CTAs
@@ -608,6 +635,14 @@ bool wide_bits_ok(const rac_ctx* c, const uint64_t* D) {
       if (D[(size_t)x * c->wq + w] & ~dm) return false;
     }
   return true;
+}
+
+// Padding bits of a host domain state (bits at or beyond dom(x) must be 0).
+bool bits_ok(const rac_ctx* c, const uint64_t* D) {
+  if (c->wide) return wide_bits_ok(c, D);
+  uint64_t bad = 0;  // no early exit: a branch-free OR the compiler vectorises
+  for (int x = 0; x < c->n; ++x) bad |= D[x] & ~c->dommask_h[x];
+  return bad == 0;
 }
 
 int check_usable(rac_ctx* c) {
@@ -653,6 +688,8 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
     p.timeout_ns = (unsigned long long)(to ? atoll(to) : 20000) * 1000000ull;
   }
   p.flags = flags;
+  static const uint32_t ab = getenv("RAC_FUSED_AB") ? (uint32_t)atoi(getenv("RAC_FUSED_AB")) : 0u;  // tooling
+  p.ab = ab;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
@@ -746,7 +783,7 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
                        int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
                        int n_seeds = -1) {
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
-  CK(c, cudaSetDevice(c->device));
+  CK(c, ensure_device(c));
   c->launches = 0;
   if (c->wide) return enforce_wide(c, d_in, d_out, iters, status, removed_at, flags, s, seeds, n_seeds);
   if (c->peer) {
@@ -1077,25 +1114,24 @@ int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* i
   int rc = check_usable(c);
   if (rc) return rc;
   if (!d_in || !d_out || !iterations) return fail(c, RAC_EINVAL, "NULL pointer");
-  if (c->wide && !wide_bits_ok(c, d_in)) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
-  for (int x = 0; x < c->n && !c->wide; ++x)
-    if (d_in[x] & ~c->dommask_h[x]) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
-  CK(c, cudaSetDevice(c->device));
-  const size_t nb = (size_t)c->n * c->wq * 8;
+  if (!bits_ok(c, d_in)) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
+  CK(c, ensure_device(c));
+  const size_t nw = (size_t)c->n * c->wq, nb = nw * 8;
   memcpy(c->h_in, d_in, nb);
   CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb, cudaMemcpyHostToDevice, c->stream));
-  rc = enforce_async_impl(c, c->buf_in, c->buf_out, c->buf_scalars, c->buf_scalars + 1,
-                          removed_at ? c->buf_removed : nullptr, flags, c->stream);
+  int32_t* h_res = reinterpret_cast<int32_t*>(c->h_out + nw);
+  int32_t* d_res = reinterpret_cast<int32_t*>(c->d_hout + nw);
+  h_res[1] = -99;  // "no status reported" until the kernel writes one
+  rc = enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, removed_at ? c->buf_removed : nullptr, flags,
+                          c->stream);
   if (rc) return rc;
-  CK(c, cudaMemcpyAsync(c->h_out, c->buf_out, nb, cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaMemcpyAsync(c->h_scalars, c->buf_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
   if (removed_at)
     CK(c, cudaMemcpyAsync(removed_at, c->buf_removed, (size_t)c->n * 64 * c->wq * 4, cudaMemcpyDeviceToHost,
                           c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   memcpy(d_out, c->h_out, nb);
-  *iterations = c->h_scalars[0];
-  const int st = c->h_scalars[1];
+  *iterations = h_res[0];
+  const int st = h_res[1];
   if (st == RAC_EPEER) return fail(c, RAC_EPEER, "peer exchange timed out (a rank did not arrive)");
   if (st != RAC_OK && st != RAC_WIPEOUT) return fail(c, RAC_ECUDA, "kernel did not report a status");
   return st;
@@ -1124,30 +1160,26 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
     return fail(c, RAC_EINVAL, "bad seeded-enforcement arguments");
   for (int i = 0; i < n_seeds; ++i)
     if (seeds[i] < 0 || seeds[i] >= c->n) return fail(c, RAC_EINVAL, "seed out of range");
-  if (c->wide && !wide_bits_ok(c, d_in)) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
-  for (int x = 0; x < c->n && !c->wide; ++x)
-    if (d_in[x] & ~c->dommask_h[x]) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
-  CK(c, cudaSetDevice(c->device));
-  const size_t nb = (size_t)c->n * c->wq * 8;
+  if (!bits_ok(c, d_in)) return fail(c, RAC_EINVAL, "d_in has bits beyond dom sizes");
+  CK(c, ensure_device(c));
+  const size_t nw = (size_t)c->n * c->wq, nb = nw * 8;
   if ((size_t)n_seeds > c->seed_cap) {
-    cudaFree(c->buf_seeds);
-    c->buf_seeds = nullptr;
-    CK(c, cudaMalloc(&c->buf_seeds, (size_t)n_seeds * 4));
-    c->seed_cap = (size_t)n_seeds;
+    CK(c, cudaStreamSynchronize(c->stream));  // the staging buffers may still be in use
+    CK(c, alloc_staging(c, nb, std::max<size_t>((size_t)n_seeds, 2 * c->seed_cap)));
   }
   memcpy(c->h_in, d_in, nb);
-  CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb, cudaMemcpyHostToDevice, c->stream));
-  if (n_seeds > 0)
-    CK(c, cudaMemcpyAsync(c->buf_seeds, seeds, (size_t)n_seeds * 4, cudaMemcpyHostToDevice, c->stream));
-  rc = enforce_async_impl(c, c->buf_in, c->buf_out, c->buf_scalars, c->buf_scalars + 1, nullptr, flags, c->stream,
-                          c->buf_seeds, n_seeds);
+  if (n_seeds > 0) memcpy(reinterpret_cast<uint8_t*>(c->h_in) + nb, seeds, (size_t)n_seeds * 4);
+  CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb + (size_t)n_seeds * 4, cudaMemcpyHostToDevice, c->stream));
+  int32_t* h_res = reinterpret_cast<int32_t*>(c->h_out + nw);
+  int32_t* d_res = reinterpret_cast<int32_t*>(c->d_hout + nw);
+  h_res[1] = -99;
+  rc = enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, c->buf_seeds,
+                          n_seeds);
   if (rc) return rc;
-  CK(c, cudaMemcpyAsync(c->h_out, c->buf_out, nb, cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaMemcpyAsync(c->h_scalars, c->buf_scalars, 8, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   memcpy(d_out, c->h_out, nb);
-  *iterations = c->h_scalars[0];
-  const int st = c->h_scalars[1];
+  *iterations = h_res[0];
+  const int st = h_res[1];
   if (st == RAC_EPEER) return fail(c, RAC_EPEER, "peer exchange timed out (a rank did not arrive)");
   if (st != RAC_OK && st != RAC_WIPEOUT) return fail(c, RAC_ECUDA, "kernel did not report a status");
   return st;
@@ -1184,11 +1216,13 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
   if (n_states == 0) return 0;
   CK(c, cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
-  const char* impl = getenv("RAC_BATCH_IMPL");  // A/B knob (tooling only): "bs" = bit-sliced N5
-  const bool want_bs = impl && strcmp(impl, "bs") == 0;
-  if (!want_bs && c->state_smem > 0) {
-    // Default: one block per state (rac_state): each state runs its own
-    // passes with no cross-state barrier; the relation stays L2-resident.
+  const char* impl = getenv("RAC_BATCH_IMPL");  // A/B knob (tooling only): "state" = one block per state
+  const bool want_state = impl && strcmp(impl, "state") == 0;
+  if (want_state && c->state_smem > 0) {
+    // One block per state (rac_state): no cross-state barrier, but every state
+    // reads its own masks from L2 -- measured 1.2 ms vs 0.68 ms for the
+    // bit-sliced kernel at C5 (profiles/r02b/ab_state.log), which shares each
+    // mask load among 32 states.
     StateParams sp = state_params(c, d_in_dev, d_out_dev, iterations_dev, status_dev, flags);
     sp.seed_var = seed_var_dev;
     const int T = getenv("RAC_STATE_T") ? c->state_T : 128;
@@ -1201,7 +1235,8 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     }
     return 0;
   }
-  // Bit-sliced path (N5): 32 states per 32-bit word, per-word CTA groups.
+  // Bit-sliced path (N5, default): 32 states per 32-bit word, per-word CTA groups.
+  const bool want_bs = true;
   const int rows = c->n * c->dmax;
   const int RB = (rows + 255) / 256;
   bool use_table = batch_bs_smem(c->n, c->dmax, c->W, true) <= 96 * 1024;
@@ -1319,16 +1354,16 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
                rac_search_stats* stats) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (!d_in) return fail(c, RAC_EINVAL, "d_in is NULL");
   if (flags & ~(RAC_SEARCH_ALL | RAC_FULL_FIXPOINT)) return fail(c, RAC_EINVAL, "unknown flags");
   if (c->use_nccl() || c->vshards > 1) return fail(c, RAC_EUNSUPPORTED, "rac_search runs on fused single-GPU contexts");
-  const int n = c->n;
+  const int n = c->n, wq = c->wq;  // domain states are n x wq words (wq > 1: wide domains, NEXT-4)
+  const size_t nw = (size_t)n * wq;
   rac_search_stats st;
   memset(&st, 0, sizeof(st));
   const uint32_t ef = flags & RAC_FULL_FIXPOINT;
   // root: tensorAC(Vars, [0 : |Vars|])
-  std::vector<uint64_t> root(n);
+  std::vector<uint64_t> root(nw);
   int32_t it = 0;
   rc = rac_enforce_ex(c, d_in, root.data(), &it, nullptr, ef);
   if (rc < 0) return rc;
@@ -1339,46 +1374,58 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
     return RAC_WIPEOUT;
   }
   // explicit DFS stack: frame k holds the domains of depth k and the variable
-  // chosen there with its untried values
-  struct Frame {
-    int var;
-    uint64_t todo;
-  };
-  std::vector<uint64_t> doms((size_t)(n + 1) * n);
-  std::vector<Frame> frames(n + 1);
+  // chosen there with its untried values (wq words)
+  std::vector<uint64_t> doms((size_t)(n + 1) * nw);
+  std::vector<int> fvar(n + 1);
+  std::vector<uint64_t> ftodo((size_t)(n + 1) * wq);
   std::vector<char> assigned(n, 0);
+  auto count = [&](const uint64_t* v) {
+    int k = 0;
+    for (int w = 0; w < wq; ++w) k += __builtin_popcountll(v[w]);
+    return k;
+  };
+  auto first = [&](const uint64_t* v) {
+    for (int w = 0; w < wq; ++w)
+      if (v[w]) return 64 * w + __builtin_ctzll(v[w]);
+    return -1;
+  };
   auto pick = [&](const uint64_t* D) {
-    int best = -1, bc = 65;
+    int best = -1, bc = 1 << 30;
     for (int x = 0; x < n; ++x) {
       if (assigned[x]) continue;
-      const int cnt = __builtin_popcountll(D[x]);
+      const int cnt = count(D + (size_t)x * wq);
       if (cnt < bc) { bc = cnt; best = x; }
     }
     return best;
   };
+  auto open_frame = [&](int depth, const uint64_t* D) {
+    fvar[depth] = pick(D);
+    std::copy(D + (size_t)fvar[depth] * wq, D + (size_t)fvar[depth] * wq + wq, ftodo.begin() + (size_t)depth * wq);
+    assigned[fvar[depth]] = 1;
+  };
   std::copy(root.begin(), root.end(), doms.begin());
   int depth = 0;
-  frames[0].var = pick(doms.data());
-  if (frames[0].var < 0) return fail(c, RAC_EINVAL, "no variable to assign");
-  frames[0].todo = doms[frames[0].var];
-  assigned[frames[0].var] = 1;
+  if (pick(doms.data()) < 0) return fail(c, RAC_EINVAL, "no variable to assign");
+  open_frame(0, doms.data());
   bool found = false;
   int result = RAC_WIPEOUT;
-  std::vector<uint64_t> child(n);
+  std::vector<uint64_t> child(nw);
   while (depth >= 0) {
-    Frame& f = frames[depth];
-    if (f.todo == 0) {  // all values of f.var tried: backtrack
-      assigned[f.var] = 0;
+    uint64_t* todo = ftodo.data() + (size_t)depth * wq;
+    const int var = fvar[depth];
+    const int val = first(todo);
+    if (val < 0) {  // all values of var tried: backtrack
+      assigned[var] = 0;
       --depth;
       continue;
     }
     if (max_assignments > 0 && st.assignments >= max_assignments) { result = RAC_BUDGET; break; }
-    const int val = __builtin_ctzll(f.todo);
-    f.todo &= f.todo - 1;
-    const uint64_t* parent = doms.data() + (size_t)depth * n;
-    std::copy(parent, parent + n, child.begin());
-    child[f.var] = 1ull << val;  // assign: row overwrite
-    int32_t seed = f.var;
+    todo[val >> 6] &= ~(1ull << (val & 63));
+    const uint64_t* parent = doms.data() + (size_t)depth * nw;
+    std::copy(parent, parent + nw, child.begin());
+    for (int w = 0; w < wq; ++w) child[(size_t)var * wq + w] = 0;
+    child[(size_t)var * wq + (val >> 6)] = 1ull << (val & 63);  // assign: row overwrite
+    int32_t seed = var;
     int32_t cit = 0;
     const auto t0 = std::chrono::steady_clock::now();
     rc = rac_enforce_seeded(c, child.data(), child.data(), &cit, &seed, 1, ef);
@@ -1391,16 +1438,14 @@ int rac_search(rac_ctx* c, const uint64_t* d_in, int64_t max_assignments, uint32
     if (depth + 1 == n) {  // every variable assigned: a solution (Alg. 2 "find answer")
       st.solutions++;
       if (!found && solution)
-        for (int x = 0; x < n; ++x) solution[x] = __builtin_ctzll(child[x]);
+        for (int x = 0; x < n; ++x) solution[x] = first(child.data() + (size_t)x * wq);
       found = true;
       if (!(flags & RAC_SEARCH_ALL)) { result = RAC_OK; break; }
       continue;
     }
     ++depth;
-    std::copy(child.begin(), child.end(), doms.begin() + (size_t)depth * n);
-    frames[depth].var = pick(child.data());
-    frames[depth].todo = child[frames[depth].var];
-    assigned[frames[depth].var] = 1;
+    std::copy(child.begin(), child.end(), doms.begin() + (size_t)depth * nw);
+    open_frame(depth, child.data());
   }
   if (result != RAC_BUDGET && found) result = RAC_OK;
   if (stats) *stats = st;

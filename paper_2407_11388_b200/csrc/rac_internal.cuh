@@ -104,6 +104,7 @@ struct FusedParams {
   const int32_t* seeds;     // device [n_seeds]: Alg. 1 initial @changed (read only if n_seeds > 0)
   int n_seeds;              // < 0: root call (every column in pass 1); 0: no pass
   uint32_t flags;
+  uint32_t ab;              // A/B knobs (tooling, RAC_FUSED_AB): bit 0 legacy grid barrier, bit 1 legacy compaction
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
   // Global pass counter (persists across launches): pass t of this launch is
   // pass *seq + t; it selects the rotating buffers and is the cross-rank
@@ -167,9 +168,11 @@ struct StateParams {
   uint32_t flags;
   int s0;                   // first state of this launch in the caller's arrays
   int nvec;                 // 16-byte vectors per column
-  uint32_t off_R, off_live, off_vx, off_list, off_nlist, off_P;  // shared-memory layout (state_layout)
+  uint32_t off_R, off_live, off_vx, off_list, off_nlist, off_P, off_M;  // shared-memory layout (state_layout)
 };
-size_t state_layout(StateParams& p, int n, int dmax, int W, int rows_pad, int pw, size_t p_cap);
+// Offsets of rac_state's shared memory; P staged if <= p_cap bytes, the whole
+// mask tensor if <= m_cap bytes (0 = not staged).  Returns the total bytes.
+size_t state_layout(StateParams& p, int n, int dmax, int W, int rows_pad, int pw, size_t p_cap, size_t m_cap);
 cudaError_t launch_state(int W, int T, const StateParams& p, int n_states, size_t smem, cudaStream_t s);
 
 struct BatchBSParams {
@@ -682,9 +685,30 @@ __device__ __forceinline__ void st_release_sys64(unsigned long long* p, unsigned
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void red_release_add_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Software grid barrier for a co-resident (cooperative) grid.  bar[0] counts
-// arrivals over the whole launch, bar[1] is the released epoch.
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks, unsigned epoch) {
+// arrivals over the whole launch.  Each CTA arrives with a release reduction
+// (no return value, no separate fence) and polls the counter itself until all
+// nblocks * epoch arrivals are in (relaxed polls, one fence after: an acquire
+// load per poll would invalidate the SM's L1 every time), so the release does
+// not wait for a last arriver to publish a flag.  legacy != 0: the previous
+// form (fenced atomicAdd; the last arriver releases bar[1]) for A/B runs.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks, unsigned epoch, int legacy = 0) {
+  if (!legacy) {
+    __syncthreads();
+    if (nblocks > 1 && threadIdx.x == 0) {
+      red_release_add_gpu(&bar[0], 1u);
+      const unsigned target = nblocks * epoch;
+      while (ld_relaxed_gpu(&bar[0]) < target) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    return;
+  }
   __syncthreads();
   if (nblocks > 1 && threadIdx.x == 0) {
     __threadfence();

@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
         __syncthreads();
         if (dbg_cta) p.dbg[256 + 3 * blockIdx.x + 1] = globaltimer();
       }
-      grid_sync(p.bar, gridDim.x, ++epoch);
+      grid_sync(p.bar, gridDim.x, ++epoch, (int)(p.ab & 1u));
       if (mg) {
         // Row-sharded exchange: R of this rank's rows is complete; copy its
         // non-zero words into every peer's R (a peer's words for these rows are
@@ -517,6 +517,47 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
         }
       } else if (__ldcg(p.rflag + b) == 0u) {
         wipe = has_empty;
+      } else if (!(p.ab & 2u)) {
+        // D_t = D_{t-1} & ~R, with the next pass's column list built in the same
+        // sweep: thread i owns the contiguous variables [i*chunk, (i+1)*chunk), so
+        // a block scan of the per-thread change counts gives every CTA the same
+        // ascending list (the item -> column mapping must agree across CTAs).
+        const int T = blockDim.x, chunk = (g.n + T - 1) / T;  // <= 128 (n <= 65535)
+        const int xb = min(g.n, (int)threadIdx.x * chunk), xe = min(g.n, xb + chunk);
+        const int par = t & 1;
+        if (threadIdx.x == 0) s_red[par ^ 1][1] = 0;  // next pass's slot
+        uint32_t cm[4] = {0u, 0u, 0u, 0u};
+        int nrm = 0, wl = 0, cnt = 0;
+        for (int x0 = xb; x0 < xe; x0 += 4) {
+          uint64_t rv[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) rv[k] = x0 + k < xe ? __ldcg(&Rc[x0 + k]) : 0ull;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int x = x0 + k;
+            if (x >= xe) break;
+            const uint64_t dv = load_w<W>(Db + x * W);
+            const uint64_t nd = dv & ~rv[k];
+            if ((dv & rv[k]) != 0) {
+              store_w<W>(Db + x * W, nd);
+              cm[(x - xb) >> 5] |= 1u << ((x - xb) & 31);
+              ++cnt;
+              wl |= nd == 0;
+              if (x >= g.x_lo && x < g.x_hi) nrm += __popcll(dv & rv[k]);
+            }
+          }
+        }
+        nrm = __reduce_add_sync(0xffffffffu, nrm);
+        if ((threadIdx.x & 31) == 0 && nrm) atomicAdd_block(&s_red[par][1], nrm);
+        uint32_t total = 0;
+        uint32_t pos = block_scan_u32((uint32_t)cnt, &total, scratch);  // barriers inside
+        for (int w = 0; w < 4; ++w)
+          for (uint32_t m = cm[w]; m; m &= m - 1u) vlist[pos++] = (uint16_t)(xb + 32 * w + __ffs(m) - 1);
+        wipe = has_empty | __syncthreads_or(wl);  // also publishes vlist
+        changed = total > 0;
+        live -= s_red[par][1];
+        vcnt = (int)total;
+        listed = true;
       } else {
         // one block barrier for the three reductions: flags (changed | wipe)
         // and the live values of the local rows this pass removed

@@ -320,8 +320,9 @@ class RacContext:
 
     def search(self, d_in, max_assignments: int = 0, all_solutions: bool = False, full: bool = False):
         """rac_search: Alg. 2 backtracking search with seeded enforcement per assignment.
-        Returns (result, solution or None, stats dict)."""
-        d_in = np.ascontiguousarray(d_in, dtype=np.uint64)
+        Returns (result, solution or None, stats dict).  Domain states of wide
+        contexts are [n_vars * words_per_var] words."""
+        d_in = np.ascontiguousarray(d_in, dtype=np.uint64).reshape(-1)
         sol = np.full(self.n, -1, dtype=np.int32)
         st = rac_search_stats()
         flags = (RAC_SEARCH_ALL if all_solutions else 0) | (RAC_FULL_FIXPOINT if full else 0)

@@ -191,12 +191,12 @@ def test_seeded_lists_sharded_and_small(rac):
 def test_wide_seeded_many_seeds(rac):
     """Wide seeded calls with more than 8 seeds (pass 1 takes the warp-per-row
     branch of wide_fused) and an out-of-range seed on the device path (skipped,
-    as in rac_fused), at n=600, d=100: equal to O1w's full recurrence on the
-    assigned state (Prop. 2)."""
+    as in rac_fused), at n=300, d=100 (t=0.9: a 4-pass consistent root): equal
+    to O1w's full recurrence on the assigned state (Prop. 2)."""
     import torch
     from tests import _wide as WD
-    n, d = 600, 100
-    dq, tq = synth.quant_density(0.5), synth.quant_tightness(0.96)
+    n, d = 300, 100
+    dq, tq = synth.quant_density(0.5), synth.quant_tightness(0.9)
     ctx = rac.RacContext.create_random(n, d, dq, tq, 2)
     wo = oracle.WideOracle.from_synth(n, d, dq, tq, 2)
     full = synth.full_domains_wide(np.full(n, d))

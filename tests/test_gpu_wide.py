@@ -122,9 +122,6 @@ def test_wide_edge_cases(rac):
         cf.enforce(bad.reshape(-1))
     assert ei.value.code == rac.RAC_EINVAL
     with pytest.raises(rac.RacError) as ei:
-        cf.search(synth.full_domains_wide(free.dom))
-    assert ei.value.code == rac.RAC_EUNSUPPORTED
-    with pytest.raises(rac.RacError) as ei:
         cf.enforce_seeded(bad.reshape(-1), [0])
     assert ei.value.code == rac.RAC_EINVAL
 
@@ -232,8 +229,41 @@ def test_wide_bench_size_stream(rac, n, d):
     out = dout.cpu().numpy().view(np.uint64)
     assert int(sts.item()) == rac.RAC_OK and int(its.item()) == 1
     assert np.array_equal(out, full)
-    Dbits = WD.bits_of(full, n, ctx.wq)
-    rng = np.random.default_rng(0)
-    for _ in range(3):
-        x, a = int(rng.integers(n)), int(rng.integers(d))
-        assert _sample_supported(n, d, dq, tq, 1, x, a, Dbits)
+    # the whole output certified by the oracle's O7 (every row's support on every
+    # column regenerated from the generator), not a sample
+    g = ctx.enforce(full, removed_at=True)
+    assert oracle.certify_trajectory_synth(n, d, dq, tq, 1, full, g[1], g[3], g[2], g[0]) == 0
+
+
+def test_wide_search_parity(rac):
+    """rac_search on wide contexts (Alg. 2, seeded enforcement per
+    assignment) explores the same tree as the wide oracle O6w: same verdict,
+    first solution and statistics (assignments, #Recurrence, wipeouts,
+    solutions, depth) -- whole trees on small wide instances (all solutions),
+    and a budgeted search on a 60-variable generator instance."""
+    checked = 0
+    for k, inst in enumerate(_wide_corpus(12, 71)):
+        if inst.n > 7:
+            continue
+        ctx = rac.RacContext.from_instance(inst)
+        wo = oracle.WideOracle.from_instance(inst)
+        d_in = synth.full_domains_wide(inst.dom)
+        r, sol, st = ctx.search(d_in, all_solutions=True)
+        ro, solo, sto = wo.search(d_in, all_solutions=True)
+        assert r == (rac.RAC_OK if ro == 0 else rac.RAC_WIPEOUT), (k, r, ro)
+        for key in ("assignments", "recurrences", "wipeouts", "solutions", "max_depth"):
+            assert st[key] == sto[key], (k, key, st[key], sto[key])
+        if r == rac.RAC_OK:
+            assert np.array_equal(sol, solo), k
+        checked += 1
+    assert checked >= 4
+    n, d = 60, 100
+    dq, tq = synth.quant_density(0.5), synth.quant_tightness(0.95)
+    ctx = rac.RacContext.create_random(n, d, dq, tq, 3)
+    wo = oracle.WideOracle.from_synth(n, d, dq, tq, 3)
+    d_in = synth.full_domains_wide(np.full(n, d))
+    r, sol, st = ctx.search(d_in, max_assignments=300)
+    ro, solo, sto = wo.search(d_in, max_assignments=300)
+    assert {0: rac.RAC_OK, 1: rac.RAC_WIPEOUT, 2: rac.RAC_BUDGET}[ro] == r
+    for key in ("assignments", "recurrences", "wipeouts", "solutions", "max_depth"):
+        assert st[key] == sto[key], (key, st[key], sto[key])

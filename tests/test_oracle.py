@@ -854,3 +854,57 @@ def test_parallel_o1_equals_o1():
     for s in range(40):
         o = orc.rac(states[s], with_epochs=False)
         assert (st[s], it[s]) == (o[0], o[2]) and np.array_equal(out[s], o[1])
+
+
+def test_wide_search_equals_one_word_search():
+    """O6w on instances whose domains fit one word (wq = 1) explores exactly O6's
+    tree with the full-recurrence engine (same verdict, first solution and
+    statistics), on tiny corpus instances with all solutions counted."""
+    for k, inst in enumerate(I.random_corpus(60, seed0=97, n_range=(2, 9), d_range=(1, 5))):
+        orc = oracle.Oracle.from_instance(inst)
+        cons = []
+        for r in range(inst.n_rel):
+            x, y = int(inst.xs[r]), int(inst.ys[r])
+            cons.append((x, y, [(a, b) for a in range(int(inst.dom[x])) for b in range(int(inst.dom[y]))
+                                if (int(inst.rows[r, a]) >> b) & 1]))
+        wide = synth.wide_from_constraints(inst.n, np.asarray(inst.dom), cons)
+        wo = oracle.WideOracle.from_instance(wide)
+        assert wo.wq == 1
+        d_in = inst.full_domains()
+        a = orc.search(d_in, engine="full", all_solutions=True)
+        b = wo.search(d_in, all_solutions=True)
+        assert a[0] == b[0] and a[2] == b[2] and np.array_equal(a[1], b[1]), k
+
+
+def test_wide_search_solution_counts_by_enumeration():
+    """O6w with all solutions on tiny wide instances (n = 3, domains 65..100
+    values, several words): the solution count equals brute-force enumeration of
+    every complete assignment, and the first solution satisfies every
+    constraint."""
+    rng = np.random.default_rng(4)
+    for k in range(6):
+        n = 3
+        dom = rng.integers(65, 101, size=n)
+        cons = []
+        for x in range(n):
+            for y in range(x + 1, n):
+                allowed = [(a, b) for a in range(int(dom[x])) for b in range(int(dom[y]))
+                           if (a * 7 + b * 3 + k) % 11 == 0 or a == b]
+                cons.append((x, y, allowed))
+        inst = synth.wide_from_constraints(n, dom.astype(np.int32), cons)
+        wo = oracle.WideOracle.from_instance(inst)
+        rel = {(x, y): set(al) for (x, y, al) in cons}
+        count = 0
+        for a0 in range(int(dom[0])):
+            for a1 in range(int(dom[1])):
+                if (a0, a1) not in rel[(0, 1)]:
+                    continue
+                for a2 in range(int(dom[2])):
+                    if (a0, a2) in rel[(0, 2)] and (a1, a2) in rel[(1, 2)]:
+                        count += 1
+        r, sol, stats = wo.search(synth.full_domains_wide(inst.dom), all_solutions=True)
+        assert stats["solutions"] == count, (k, stats, count)
+        assert (r == 0) == (count > 0)
+        if count:
+            assert (sol[0], sol[1]) in rel[(0, 1)] and (sol[0], sol[2]) in rel[(0, 2)] and \
+                (sol[1], sol[2]) in rel[(1, 2)]
