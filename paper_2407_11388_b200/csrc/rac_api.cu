@@ -1235,7 +1235,45 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     }
     return 0;
   }
-  // Bit-sliced path (N5, default): 32 states per 32-bit word, per-word CTA groups.
+  // Default for d <= 32: one bit-sliced 32-state word per thread-block cluster
+  // (rac_batch_cl): cluster barriers and DSMEM exchange between the word's CTAs.
+  const bool want_old_bs = impl && strcmp(impl, "bs") == 0;
+  if (!want_old_bs && c->W <= 4) {
+    const int rows_all = c->n * c->dmax;
+    const char* ce = getenv("RAC_BATCH_CL");  // A/B knob (tooling only): cluster size
+    int C = ce ? atoi(ce) : 4;
+    C = std::max(1, std::min(C, (rows_all + 255) / 256));
+    int RPC = (rows_all + C - 1) / C;
+    RPC = (RPC + c->dmax - 1) / c->dmax * c->dmax;
+    C = (rows_all + RPC - 1) / RPC;
+    const int threads = std::min(1024, (RPC + 31) / 32 * 32);
+    const size_t smem = batch_cl_smem(c->n, c->dmax, c->W);
+    int maxcl = 0;
+    if (smem <= 200 * 1024) CK(c, batch_cl_max_clusters(c->W, C, threads, smem, &maxcl));
+    if (maxcl >= 1) {
+      BatchCLParams b{};
+      b.M = c->M;
+      b.col_stride = c->col_stride;
+      b.n = c->n;
+      b.dmax = c->dmax;
+      b.P = c->P;
+      b.pw = c->pw;
+      b.dommask = c->dommask;
+      b.d_in = d_in_dev;
+      b.d_out = d_out_dev;
+      b.iters = iterations_dev;
+      b.status = status_dev;
+      b.seed_var = seed_var_dev;
+      b.S = n_states;
+      b.RPC = RPC;
+      b.flags = flags;
+      const int NW = (n_states + 31) / 32;
+      CK(c, launch_batch_cl(c->W, b, std::min(NW, maxcl), C, threads, smem, st));
+      c->launches++;
+      return 0;
+    }
+  }
+  // Bit-sliced path (N5, r01 design): 32 states per 32-bit word, per-word CTA groups.
   const bool want_bs = true;
   const int rows = c->n * c->dmax;
   const int RB = (rows + 255) / 256;

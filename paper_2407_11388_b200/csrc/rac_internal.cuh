@@ -175,6 +175,28 @@ struct StateParams {
 size_t state_layout(StateParams& p, int n, int dmax, int W, int rows_pad, int pw, size_t p_cap, size_t m_cap);
 cudaError_t launch_state(int W, int T, const StateParams& p, int n_states, size_t smem, cudaStream_t s);
 
+// rac_batch_cl (rac_batch_cl.cu): one 32-state bit-sliced word per cluster.
+struct BatchCLParams {
+  const uint8_t* M;         // column-major masks
+  size_t col_stride;
+  int n, dmax;
+  const uint32_t* P;
+  int pw;
+  const uint64_t* dommask;
+  const uint64_t* d_in;     // [S][n]
+  uint64_t* d_out;
+  int32_t* iters;           // [S]
+  int32_t* status;          // [S]
+  const int32_t* seed_var;  // nullable [S]
+  int S;
+  int RPC;                  // rows per CTA of a cluster (a multiple of dmax)
+  uint32_t flags;
+};
+size_t batch_cl_smem(int n, int dmax, int W);
+cudaError_t launch_batch_cl(int W, const BatchCLParams& p, int clusters, int C, int threads, size_t smem,
+                            cudaStream_t s);
+cudaError_t batch_cl_max_clusters(int W, int C, int threads, size_t smem, int* out);
+
 struct BatchBSParams {
   const uint8_t* M;
   size_t col_stride;

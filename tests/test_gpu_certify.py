@@ -226,14 +226,17 @@ def test_wide_seeded_many_seeds(rac):
         assert np.array_equal(dout.cpu().numpy().view(np.uint64), o[1])
 
 
-@pytest.mark.parametrize("impl", ["state", "bs"])
+@pytest.mark.parametrize("impl", ["cluster", "cluster1", "bs", "state"])
 def test_batched_impls_corpus(rac, impl, monkeypatch):
-    """Both batched kernels -- one block per state (default) and the bit-sliced
-    32-states-per-word kernel (RAC_BATCH_IMPL=bs) -- equal the oracle state by
-    state on mixed corpora (W-rand states, stop and full modes, empty rows)."""
+    """Every batched kernel -- one 32-state word per cluster (default, cluster
+    sizes 4 and 1), the r01 bit-sliced kernel (RAC_BATCH_IMPL=bs) and one block
+    per state (RAC_BATCH_IMPL=state) -- equals the oracle state by state on
+    mixed corpora (W-rand states, stop and full modes, empty rows)."""
     import torch
-    if impl == "bs":
-        monkeypatch.setenv("RAC_BATCH_IMPL", "bs")
+    if impl in ("bs", "state"):
+        monkeypatch.setenv("RAC_BATCH_IMPL", impl)
+    if impl == "cluster1":
+        monkeypatch.setenv("RAC_BATCH_CL", "1")
     for k, inst in enumerate(I.random_corpus(40, seed0=301, n_range=(5, 60), d_range=(1, 16))):
         orc = oracle.Oracle.from_instance(inst)
         ctx = rac.RacContext.from_instance(inst)

@@ -70,6 +70,9 @@ if os.environ.get("AB_SET") == "cols":  # column-sweep workloads only
     print(tag, "auto:", single("c3prop", 2000, 32, 1.0, 0.70, reps=50), single("c3seed", 2000, 32, 1.0, 0.5, "seed", 100),
           single("c2", 500, 20, 1.0, 0.3, reps=1000), flush=True)
     sys.exit(0)
+if os.environ.get("AB_SET") == "batch":
+    print(tag, batch(), flush=True)
+    sys.exit(0)
 if os.environ.get("AB_SET") == "sparse":
     print(tag, single("c3s_stream", 4000, 32, 0.25, 0.5, reps=100), single("c3s_prop", 4000, 32, 0.25, 0.72, reps=50),
           flush=True)
