@@ -248,8 +248,8 @@ def run_gpu(args, rank, world, local_rank):
                 chg = (remd == t).any(axis=1)
         instr["support_tests"] = alg_tests
     else:
-        stt, dout, it, rem = (ctx.enforce(din_h[0], removed_at=True) if world == 1 else
-                              (*ctx.enforce(din_h[0]), None))
+        # removal epochs on every rank (with world > 1 they are gathered with the exchange)
+        stt, dout, it, rem = ctx.enforce(din_h[0], removed_at=True)
         instr = {"iterations": it, "status": "OK" if stt == 0 else "WIPEOUT"}
         # Algorithmic bytes of Alg. 1: pass t tests every live (x,a)
         # against the constraints c_xy with y changed in pass t-1 (all y in

@@ -37,9 +37,9 @@
  *     epochs are [n_vars * 64 * wq] (x,a) at x*64*wq + a.  With max dom <= 64,
  *     wq = 1 and every format below is unchanged.  Wide contexts support
  *     rac_create / rac_create_random / rac_enforce / rac_enforce_ex /
- *     rac_enforce_async / rac_enforce_seeded / rac_enforce_seeded_async on
- *     one GPU (world == 1, dense layout); the batched, search, sharded and
- *     peer calls return RAC_EUNSUPPORTED.
+ *     rac_enforce_async / rac_enforce_seeded / rac_enforce_seeded_async /
+ *     rac_search on one GPU (world == 1, dense layout); the sharded and peer
+ *     calls return RAC_EUNSUPPORTED.
  *
  * Return values: every int-returning call returns >= 0 on success (RAC_OK or
  * RAC_WIPEOUT for enforcement calls) and a negative RAC_E* code on error.
@@ -183,22 +183,27 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
 int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q16, uint64_t seed,
                       const rac_options* opt, rac_ctx** out);
 
-/* Blocking enforcement, host buffers: d_in, d_out = uint64_t[n_vars].
+/* Blocking enforcement, host buffers: d_in, d_out = uint64_t[n_vars * wq]
+ * (wq = rac_words_per_var(ctx): 1 unless the domains are wider than 64 values;
+ * bit a of x is bit a%64 of word x*wq + a/64).
  * Returns RAC_OK / RAC_WIPEOUT (and *iterations) or an error.
  * RAC_EINVAL: NULL pointers; bits of d_in beyond dom sizes. */
 int rac_enforce(rac_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations);
 
 /* As rac_enforce, plus flags (RAC_FULL_FIXPOINT) and, if removed_at != NULL,
- * removed_at[x*64 + a] = the pass that removed (x,a), 0 if kept or absent
- * (the per-step sets V^(k) of Prop. 2).  removed_at needs world == 1. */
+ * removed_at[x*64*wq + a] (int32_t[n_vars * 64 * wq]) = the pass that removed
+ * (x,a), 0 if kept or absent (the per-step sets V^(k) of Prop. 2).
+ * With world > 1 every rank receives all epochs (gathered with the exchange);
+ * removed_at is then collective: all ranks pass it or none does. */
 int rac_enforce_ex(rac_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations,
                    int32_t* removed_at, uint32_t flags);
 
-/* Asynchronous enforcement, DEVICE buffers, enqueued on `stream`
- * (a cudaStream_t; NULL = legacy default stream).  Writes *status_dev
- * (RAC_OK / RAC_WIPEOUT) and *iterations_dev on the device; returns 0 once
- * enqueued.  Bits of d_in beyond dom sizes are ignored.  removed_at_dev is
- * nullable ([n_vars*64] int32, world == 1 only).  On the single-GPU fused path
+/* Asynchronous enforcement, DEVICE buffers (d_in_dev / d_out_dev:
+ * uint64_t[n_vars * wq]), enqueued on `stream` (a cudaStream_t; NULL = legacy
+ * default stream).  Writes *status_dev (RAC_OK / RAC_WIPEOUT) and
+ * *iterations_dev on the device; returns 0 once enqueued.  Bits of d_in
+ * beyond dom sizes are ignored.  removed_at_dev is nullable
+ * (int32_t[n_vars * 64 * wq], as in rac_enforce_ex).  On the single-GPU fused path
  * the host is not involved per iteration; on the sharded path (world > 1 or
  * virtual_shards > 1) the host reads a device flag once per chunk of passes. */
 int rac_enforce_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d_out_dev,
@@ -206,7 +211,7 @@ int rac_enforce_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d_out_de
                       uint32_t flags, void* stream);
 
 /* Batched enforcement of n_states independent domain states (search-tree nodes)
- * on one instance, DEVICE buffers: d_in_dev/d_out_dev = uint64_t[n_states][n_vars],
+ * on one instance, DEVICE buffers: d_in_dev/d_out_dev = uint64_t[n_states][n_vars * wq],
  * iterations_dev/status_dev = int32_t[n_states].  State s's results are exactly
  * those of rac_enforce on state s alone (each state stops at its own pass).
  * world == 1 only (batches are sharded by the caller). */
@@ -223,12 +228,15 @@ int rac_enforce_batch(rac_ctx* ctx, int32_t n_states, const uint64_t* d_in_dev, 
  * variables instead of the whole relation tensor.  Without the precondition the
  * result is sound (every removal is justified by Lemma 1) but may keep values
  * D_ac removes.  n_seeds == 0: no pass, iterations = 0, status RAC_WIPEOUT iff
- * some domain of d_in is empty.  seeds: host int32[n_seeds], each in [0, n). */
+ * some domain of d_in is empty.  seeds: host int32[n_seeds], each in [0, n)
+ * (RAC_EINVAL otherwise).  d_in, d_out: uint64_t[n_vars * wq]. */
 int rac_enforce_seeded(rac_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations,
                        const int32_t* seeds, int32_t n_seeds, uint32_t flags);
 
-/* As rac_enforce_seeded, device buffers (seeds_dev: device int32[n_seeds]),
- * asynchronous on `stream` like rac_enforce_async. */
+/* As rac_enforce_seeded, device buffers (seeds_dev: device int32[n_seeds];
+ * NULL allowed when n_seeds == 0), asynchronous on `stream` like
+ * rac_enforce_async.  Out-of-range entries of seeds_dev are skipped (the
+ * device cannot report them); duplicates test their column once. */
 int rac_enforce_seeded_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d_out_dev, int32_t* iterations_dev,
                              int32_t* status_dev, const int32_t* seeds_dev, int32_t n_seeds, uint32_t flags,
                              void* stream);

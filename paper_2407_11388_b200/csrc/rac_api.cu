@@ -28,6 +28,7 @@ typedef int ncclResult_t;
 typedef void* ncclComm_t;
 typedef struct { char internal[RAC_NCCL_ID_BYTES]; } ncclUniqueId;
 constexpr int kNcclUint64 = 5;  // ncclUint64 in nccl.h
+constexpr int kNcclInt32 = 2;   // ncclInt32
 
 struct NcclApi {
   bool loaded = false;
@@ -109,6 +110,7 @@ struct rac_ctx {
   uint64_t* buf_out = nullptr;
   int32_t* buf_scalars = nullptr;  // [iters, status]
   int32_t* buf_removed = nullptr;  // [n*64]
+  int32_t* ra_g = nullptr;         // world > 1 (NCCL): padded epoch all-gather buffer
   int32_t* buf_seeds = nullptr;    // [seed_cap]
   size_t seed_cap = 0;
   uint32_t* bs_X2 = nullptr;       // bit-sliced batch exchange buffers
@@ -230,6 +232,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->buf_out);
   cudaFree(c->buf_scalars);
   cudaFree(c->buf_removed);
+  cudaFree(c->ra_g);
   cudaFree(c->bs_X2);
   cudaFree(c->bs_bar);
   cudaFree(c->dbg);
@@ -249,7 +252,9 @@ void free_ctx(rac_ctx* c) {
 size_t xr_rflag_off(int n) { return (size_t)3 * n * 8; }                 // u32[4]
 size_t xr_arrive_off(int n) { return xr_rflag_off(n) + 16; }             // u64[RAC_MAX_RANKS]
 size_t xr_seq_off(int n) { return xr_arrive_off(n) + 8 * RAC_MAX_RANKS; }  // u64
-size_t xr_bytes(int n) { return xr_seq_off(n) + 8; }
+size_t xr_calls_off(int n) { return xr_seq_off(n) + 8; }                     // u64: calls with removal epochs
+size_t xr_epoch_off(int n) { return xr_calls_off(n) + 8; }                   // int32 [2][n*64]
+size_t xr_bytes(int n) { return xr_epoch_off(n) + (size_t)2 * n * 64 * 4; }
 
 size_t kernel_smem(const rac_ctx* c) {
   return c->sparse ? sparse_smem(c->dbytes, c->n) : fused_smem(c->dbytes, c->n);
@@ -684,6 +689,10 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
       p.peer_arrive[q] = reinterpret_cast<unsigned long long*>(c->peer_base[q] + xr_arrive_off(c->n));
     }
     p.arrive = reinterpret_cast<unsigned long long*>(c->xr + xr_arrive_off(c->n));
+    p.E = reinterpret_cast<int32_t*>(c->xr + xr_epoch_off(c->n));
+    p.calls = reinterpret_cast<unsigned long long*>(c->xr + xr_calls_off(c->n));
+    for (int q = 0; q < c->world; ++q)
+      if (q != c->rank) p.Epeer[q] = reinterpret_cast<int32_t*>(c->peer_base[q] + xr_epoch_off(c->n));
     const char* to = getenv("RAC_PEER_TIMEOUT_MS");
     p.timeout_ns = (unsigned long long)(to ? atoll(to) : 20000) * 1000000ull;
   }
@@ -721,9 +730,17 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
 int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iters, int32_t* status,
                     int32_t* removed_at, uint32_t flags, cudaStream_t s, const int32_t* seeds = nullptr,
                     int n_seeds = -1) {
-  if (removed_at && c->world > 1) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
   const int total_g = c->world * c->blk;
-  if (removed_at) CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
+  // world > 1: each rank's passes write the epochs of its own rows into a
+  // padded [world*blk][64] buffer, all-gathered after the loop (collective)
+  int32_t* ra = removed_at;
+  if (removed_at && c->world > 1) {
+    if (!c->ra_g) CK(c, cudaMalloc(&c->ra_g, (size_t)total_g * 64 * 4));
+    ra = c->ra_g;
+    CK(c, cudaMemsetAsync(ra, 0, (size_t)total_g * 64 * 4, s));
+  } else if (removed_at) {
+    CK(c, cudaMemsetAsync(removed_at, 0, (size_t)c->n * 64 * 4, s));
+  }
   CK(c, launch_shard_init(c->sh, d_in, c->dommask, c->n, c->W, c->dbytes, total_g, s));
   c->launches++;
   if (n_seeds >= 0) {
@@ -740,7 +757,7 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
     else rac_shard_range(c->n, c->vshards, b, &lo, &hi);
     pp[b].g = geom_for(c, lo, std::min(hi, c->n));
     pp[b].s = c->sh;
-    pp[b].removed_at = removed_at;
+    pp[b].removed_at = ra;
   }
   const long max_passes = (long)c->n * c->dmax + 2;
   long enq = 0;
@@ -776,6 +793,14 @@ int enforce_sharded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* 
   }
   CK(c, launch_shard_finalize(c->sh, c->n, d_out, iters, status, s));
   c->launches++;
+  if (removed_at && c->world > 1) {
+    ncclResult_t r = nccl().AllGather(ra + (size_t)c->rank * c->blk * 64, ra, (size_t)c->blk * 64, kNcclInt32, c->comm,
+                                      s);
+    if (r != 0)
+      return fail(c, RAC_ENCCL, std::string("ncclAllGather(epochs): ") +
+                                    (nccl().GetErrorString ? nccl().GetErrorString(r) : "error"));
+    CK(c, cudaMemcpyAsync(removed_at, ra, (size_t)c->n * 64 * 4, cudaMemcpyDeviceToDevice, s));
+  }
   return 0;
 }
 
@@ -788,8 +813,9 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   if (c->wide) return enforce_wide(c, d_in, d_out, iters, status, removed_at, flags, s, seeds, n_seeds);
   if (c->peer) {
     if (!c->connected) return fail(c, RAC_EINVAL, "RAC_OPT_PEER context: call rac_connect_peers first");
-    if (removed_at) return fail(c, RAC_EUNSUPPORTED, "removed_at needs world == 1");
-    return enforce_fused(c, d_in, d_out, iters, status, nullptr, flags, s, seeds, n_seeds);
+    // removal epochs are exchanged through the peers' epoch arrays (collective:
+    // every rank passes removed_at or none does)
+    return enforce_fused(c, d_in, d_out, iters, status, removed_at, flags, s, seeds, n_seeds);
   }
   if (c->use_nccl() || c->vshards > 1)
     return enforce_sharded(c, d_in, d_out, iters, status, removed_at, flags, s, seeds, n_seeds);

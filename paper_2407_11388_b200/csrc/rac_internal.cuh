@@ -88,6 +88,21 @@ struct Mirror {
   unsigned* flag[kMaxRanks];           // peer q's per-pass removal flags [3]
 };
 
+// Removal epochs mirrored to the peers (peer path with removed_at): an epoch
+// written for a local row is also stored into every peer's epoch array of the
+// call, so after the last cross-rank barrier every rank holds all epochs.
+struct EpochMirror {
+  int world, rank;
+  int32_t* E[kMaxRanks];  // peer q's epoch array of this call (NULL for self)
+};
+
+__device__ __forceinline__ void put_epoch(int32_t* ra, const EpochMirror* em, size_t i, int t) {
+  ra[i] = t;
+  if (em)
+    for (int q = 0; q < em->world; ++q)
+      if (q != em->rank) em->E[q][i] = t;
+}
+
 struct FusedParams {
   PassGeom g;
   const uint64_t* dommask;  // [n]
@@ -116,6 +131,11 @@ struct FusedParams {
   unsigned long long* peer_arrive[kMaxRanks];  // peer q's arrival words (NULL for self)
   unsigned long long timeout_ns;               // give up waiting for a peer after this long
   int32_t* xerr;                               // set to 1 on a peer timeout
+  // world > 1 with removed_at: epoch arrays [2][n*64] in every rank's exchange
+  // region (double-buffered by the parity of *calls, the count of such calls)
+  int32_t* E;                                  // own
+  int32_t* Epeer[kMaxRanks];                   // peer q's (NULL for self)
+  unsigned long long* calls;
 };
 
 struct ShardState {

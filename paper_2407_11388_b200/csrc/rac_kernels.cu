@@ -118,7 +118,8 @@ template <int W>
 __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, unsigned long long* R,
                                           int32_t* removed_at, int t, long warp0, long nwarps,
                                           const uint16_t* cols, int ncol, unsigned* rflag = nullptr,
-                                          unsigned* wctr = nullptr, uint32_t* cl = nullptr) {
+                                          unsigned* wctr = nullptr, uint32_t* cl = nullptr,
+                                          const EpochMirror* em = nullptr) {
   constexpr int RPL = 16 / W, U = kUnroll;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
@@ -162,7 +163,7 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
             if (dv == 0ull && !((g.P[(size_t)xl * g.pw + (y >> 5)] >> (y & 31)) & 1u)) continue;  // R2
             any = 1;
             mark_removed(R, x, 1ull << a, cl);
-            if (removed_at) removed_at[(size_t)x * 64 + a] = t;
+            if (removed_at) put_epoch(removed_at, em, (size_t)x * 64 + a, t);
           }
         }
       }
@@ -242,7 +243,7 @@ template <int W, int G>
 __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
                                           int32_t* removed_at, int t, long gidx, long ngroups,
                                           unsigned* wctr = nullptr, unsigned* rflag = nullptr,
-                                          uint32_t* cl = nullptr) {
+                                          uint32_t* cl = nullptr, const EpochMirror* em = nullptr) {
   const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
@@ -273,7 +274,7 @@ __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsig
     if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
       mark_removed(R, x, 1ull << a, cl);
       if (rflag) atomicOr(rflag, 1u);  // this pass removed something
-      if (removed_at) removed_at[(size_t)x * 64 + a] = t;
+      if (removed_at) put_epoch(removed_at, em, (size_t)x * 64 + a, t);
     }
   };
   const int per = wctr ? (items - items / 8) / ng : (items + ng - 1) / ng;
@@ -388,6 +389,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   // is already in the next launch only writes buffers this rank has cleared.
   const unsigned long long base = *reinterpret_cast<volatile unsigned long long*>(p.seq);
   const bool mg = p.mir.world > 1;
+  // Removal epochs: written straight to p.removed_at on one rank; with peers,
+  // into this call's epoch array E[calls % 2] of every rank (put_epoch), the
+  // other array cleared for the next such call, and copied out at the end.
+  int32_t* ep = p.removed_at;
+  EpochMirror em{};
+  const EpochMirror* emp = nullptr;
+  unsigned long long calls0 = 0;
+  if (mg && p.removed_at) {
+    calls0 = *reinterpret_cast<volatile unsigned long long*>(p.calls);
+    const size_t ne = (size_t)g.n * 64, par = (size_t)(calls0 & 1ull);
+    ep = p.E + par * ne;
+    int32_t* enext = p.E + (par ^ 1) * ne;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += (size_t)gridDim.x * blockDim.x)
+      enext[i] = 0;
+    em.world = p.mir.world;
+    em.rank = p.mir.rank;
+    for (int q = 0; q < p.mir.world && q < kMaxRanks; ++q) em.E[q] = q == p.mir.rank ? nullptr : p.Epeer[q] + par * ne;
+    emp = &em;
+  }
   // sparse layout, single rank: removals also go to a per-pass change list, so
   // the tail of a pass reads only the changed variables' R words and needs no
   // compaction.  (Measured on the dense layout it is a wash -- C3 W-prop
@@ -442,15 +462,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
           for (int i = threadIdx.x; i <= g.n; i += blockDim.x) ipref[i] = __ldg(g.s_ipref + i);
           __syncthreads();
         }
-        sparse_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ipref,
+        sparse_sweep<W>(g, Db, Rc, ep, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ipref,
                         upl, p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc);
       } else {
         if (pick_rows(g, live, lst ? vcnt : g.n))
-          row_sweep<W, G>(g, Ds, Rc, p.removed_at, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b,
-                          clc);
+          row_sweep<W, G>(g, Ds, Rc, ep, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b,
+                          clc, emp);
         else
-          column_sweep<W>(g, Db, Rc, p.removed_at, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
-                          p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc);
+          column_sweep<W>(g, Db, Rc, ep, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
+                          p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc, emp);
       }
       RAC_MARK();
       if (p.dbg != nullptr && t == 1) {  // block-uniform condition: the barrier is safe
@@ -604,9 +624,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       RAC_MARK();
     }
   }
+  if (emp && t > 0) {
+    // every rank's epochs arrived before the last cross-rank barrier
+    const size_t ne = (size_t)g.n * 64;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += (size_t)gridDim.x * blockDim.x)
+      p.removed_at[i] = __ldcv(ep + i);
+  }
   if (blockIdx.x == 0) {
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.d_out[x] = load_w<W>(Db + x * W);
     if (threadIdx.x == 0) {
+      if (emp && t > 0) *p.calls = calls0 + 1ull;  // every CTA read *calls before the first barrier
       *p.iters = t;
       *p.status = (mg && *reinterpret_cast<volatile int32_t*>(p.xerr)) ? kPeerTimeout : status;
       // every CTA read *p.seq before the first barrier

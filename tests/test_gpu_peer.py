@@ -67,6 +67,25 @@ def run_group(ctxs, d_in, full=False, seeds=None):
             for r in range(len(ctxs))]
 
 
+def run_group_epochs(ctxs, d_in, full=False):
+    """As run_group, with every rank asking for the removal epochs."""
+    import torch
+    n = ctxs[0].n
+    streams = [torch.cuda.Stream() for _ in ctxs]
+    src = torch.from_numpy(np.ascontiguousarray(d_in, dtype=np.uint64).view(np.int64).copy()).cuda()
+    ins = [src.clone() for _ in ctxs]
+    outs = [torch.zeros_like(src) for _ in ctxs]
+    its = [torch.full((1,), -9, dtype=torch.int32, device="cuda") for _ in ctxs]
+    sts = [torch.full((1,), -9, dtype=torch.int32, device="cuda") for _ in ctxs]
+    rems = [torch.full((n * 64,), -9, dtype=torch.int32, device="cuda") for _ in ctxs]
+    torch.cuda.synchronize()
+    for r, c in enumerate(ctxs):
+        c.enforce_async(ins[r], outs[r], its[r], sts[r], rems[r], full=full, stream=streams[r])
+    torch.cuda.synchronize()
+    return [(int(sts[r].item()), outs[r].cpu().numpy().view(np.uint64).copy(), int(its[r].item()),
+             rems[r].cpu().numpy().reshape(n, 64)) for r in range(len(ctxs))]
+
+
 def check(res, o, what):
     for r, g in enumerate(res):
         assert g[0] == o[0], (what, r, "status", g[0], o[0])
@@ -149,3 +168,31 @@ def test_peer_timeout_reports_epeer(rac, monkeypatch):
     with pytest.raises(rac.RacError) as ei:
         c0.enforce(inst.full_domains())
     assert ei.value.code == rac.RAC_ESTATE
+
+
+def test_peer_removal_epochs(rac):
+    """Removal epochs on the peer path (include/rac.h rac_enforce_ex: with world > 1
+    every rank receives all epochs): each rank's epochs equal the oracle's, for
+    2, 3 and 4 ranks, stop and full modes, with calls that do and do not ask for
+    epochs interleaved (the double-buffered epoch arrays switch parity only on
+    calls that ask)."""
+    for k, inst in enumerate(I.random_corpus(18, seed0=307, n_range=(8, 40), d_range=(2, 10))):
+        world = 2 + k % 3
+        orc = oracle.Oracle.from_instance(inst)
+        ctxs = make_group(rac, world, lambda r, w, m: rac.RacContext.from_instance(
+            inst, rank=r, world=w, peer=True, max_ctas=m), max_ctas=4)
+        for j in range(3):
+            d_in = synth.w_rand(inst.dom, 0.85, seed=100 * k + j)
+            full = j == 1
+            o = orc.rac(d_in, full=full)
+            for r, g in enumerate(run_group_epochs(ctxs, d_in, full)):
+                assert (g[0], g[2]) == (o[0], o[2]) and np.array_equal(g[1], o[1]), (k, j, r)
+                assert np.array_equal(g[3], o[3]), (k, j, r, "epochs")
+            check(run_group(ctxs, d_in), orc.rac(d_in, with_epochs=False), (k, j, "no epochs"))
+    # C3 shape, 13 passes, 2 ranks: certified epochs on every rank
+    dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.70)
+    ctxs = make_group(rac, 2, lambda r, w, m: rac.RacContext.create_random(
+        2000, 32, dq, tq, 1, rank=r, world=w, peer=True, max_ctas=m), max_ctas=64)
+    root = synth.full_domains(np.full(2000, 32))
+    for g in run_group_epochs(ctxs, root):
+        assert oracle.certify_trajectory_synth(2000, 32, dq, tq, 1, root, g[1], g[3], g[2], g[0]) == 0
