@@ -1232,10 +1232,26 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
                       void* stream) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
   if (n_states < 0 || (n_states > 0 && (!d_in_dev || !d_out_dev || !iterations_dev || !status_dev)))
     return fail(c, RAC_EINVAL, "bad batch arguments");
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
+  if (c->wide) {
+    // wide domains (NEXT-4): one block per state (wide_state)
+    c->launches = 0;
+    if (n_states == 0) return 0;
+    if (wide_state_smem(c->n, c->WS) > 200 * 1024)
+      return fail(c, RAC_EUNSUPPORTED, "wide batched mode: n too large for the per-state shared memory");
+    CK(c, ensure_device(c));
+    WideStateParams w{reinterpret_cast<const uint64_t*>(c->M), c->P, c->dom_d, c->n, c->dmax, c->wq, c->WS, c->pw,
+                      (flags & RAC_FULL_FIXPOINT) ? 1 : 0, d_in_dev, d_out_dev, iterations_dev, status_dev,
+                      seed_var_dev, 0};
+    for (int s0 = 0; s0 < n_states; s0 += 65535) {
+      w.s0 = s0;
+      CK(c, launch_wide_state(w, std::min(65535, n_states - s0), (cudaStream_t)stream));
+      c->launches++;
+    }
+    return 0;
+  }
   if (c->sparse) return fail(c, RAC_EUNSUPPORTED, "batched mode needs the dense layout (RAC_OPT_DENSE)");
   if (c->world > 1) return fail(c, RAC_EUNSUPPORTED, "batched mode runs per rank (world == 1 contexts)");
   c->launches = 0;

@@ -351,6 +351,21 @@ struct WidePack {
   int n, dmax, wq, WS, pw;
   uint64_t dens_q32;
 };
+struct WideStateParams {  // wide_state: one block per domain state
+  const uint64_t* M;
+  const uint32_t* P;
+  const int32_t* dom;
+  int n, dmax, wq, WS, pw;
+  int full;
+  const uint64_t* d_in;     // [S][n * wq]
+  uint64_t* d_out;
+  int32_t* iters;
+  int32_t* status;
+  const int32_t* seed_var;  // nullable [S]
+  int s0;                   // first state of this launch
+};
+size_t wide_state_smem(int n, int WS);
+cudaError_t launch_wide_state(const WideStateParams& p, int n_states, cudaStream_t s);
 cudaError_t wide_fused_grid(int WS, size_t smem, int sm_count, int* grid);
 cudaError_t launch_wide_fused(const WideParams& p, int grid, size_t smem, cudaStream_t s);
 // rows: [n_rel][dmax][wq] (row a of rel(c_{xs[r] ys[r]}))

@@ -222,6 +222,147 @@ __global__ void __launch_bounds__(kWideThreads) wide_fused(WideParams p) {
   }
 }
 
+// ---- a7 on wide domains: one thread block per domain state (batched mode,
+// search-tree nodes, Alg. 2).  The block runs its
+// state's whole enforcement -- Eq. 1 with Alg. 1's loop control, D / removal
+// bits / tested-column list in shared memory, __syncthreads as the pass
+// barrier -- so each state stops at its own pass; no cross-state barrier.
+// Pass t: every live row (x,a) (thread-strided) is tested against the tested
+// columns (the seed variable in pass 1 of a seeded state, all columns in pass 1
+// of a root state, then the variables changed in pass t-1; Prop. 2), four
+// masks in flight, early exit at the first declared c_xy with an empty
+// support set.
+template <int WS>
+__global__ void __launch_bounds__(256) wide_state(WideStateParams p) {
+  extern __shared__ uint64_t wsm[];
+  __shared__ unsigned sc[256 / 32];
+  const int n = p.n, dmax = p.dmax, wq = p.wq, tid = threadIdx.x, T = blockDim.x;
+  const int s = p.s0 + blockIdx.x;
+  uint64_t* D = wsm;                                          // [n*WS]
+  unsigned long long* R = reinterpret_cast<unsigned long long*>(D + (size_t)n * WS);  // [n*WS]
+  uint32_t* list = reinterpret_cast<uint32_t*>(R + (size_t)n * WS);                  // [n]
+  uint32_t* nlist = list + n;                                                          // [n]
+  const uint64_t* din = p.d_in + (size_t)s * n * wq;
+  for (int i = tid; i < n * WS; i += T) {
+    const int x = i / WS, w = i % WS;
+    uint64_t v = 0;
+    if (w < wq) {
+      const int bits = min(64, max(0, p.dom[x] - 64 * w));
+      v = din[(size_t)x * wq + w] & (bits >= 64 ? ~0ull : ((1ull << bits) - 1ull));
+    }
+    D[i] = v;
+    R[i] = 0ull;
+  }
+  const int sv = p.seed_var ? p.seed_var[s] : -1;
+  bool all_cols = !(sv >= 0 && sv < n);
+  int cnt = all_cols ? n : 1;
+  if (!all_cols && tid == 0) list[0] = (uint32_t)sv;
+  __syncthreads();
+  int has_empty = 0;
+  for (int x = tid; x < n; x += T) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int w = 0; w < WS; ++w) v |= D[x * WS + w];
+    has_empty |= v == 0ull;
+  }
+  has_empty = __syncthreads_or(has_empty);
+  const int rows = n * dmax;
+  int t = 0, status = RAC_OK;
+  for (;;) {
+    ++t;
+    // a3/a4: live rows against the tested columns
+    int any = 0;
+    for (int r = tid; r < rows; r += T) {
+      const int x = r / dmax, a = r - x * dmax;
+      if (!((D[x * WS + (a >> 6)] >> (a & 63)) & 1ull)) continue;  // dead row
+      const uint64_t* row = p.M + (size_t)r * n * WS;
+      bool failed = false;
+      for (int c0 = 0; c0 < cnt && !failed; c0 += 4) {
+        Mask<WS> m[4];
+        int yv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          yv[u] = c0 + u < cnt ? (all_cols ? c0 + u : (int)list[c0 + u]) : -1;
+          if (yv[u] >= 0) m[u] = load_mask<WS>(row + (size_t)yv[u] * WS);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (yv[u] >= 0 && !failed && !meets<WS>(m[u], D + (size_t)yv[u] * WS) && present(p.P, p.pw, x, yv[u]))
+            failed = true;
+      }
+      if (failed) {
+        atomicOr(&R[x * WS + (a >> 6)], 1ull << (a & 63));
+        any = 1;
+      }
+    }
+    if (!__syncthreads_or(any)) {  // nothing removed: D_t = D_{t-1}
+      status = has_empty ? RAC_WIPEOUT : RAC_OK;
+      break;
+    }
+    // a5: D_t = D_{t-1} & ~R; changed variables (ascending) -> next columns
+    const int per = (n + T - 1) / T, xb = min(n, tid * per), xe = min(n, xb + per);
+    unsigned c = 0;
+    for (int x = xb; x < xe; ++x) {
+      unsigned long long rr = 0;
+#pragma unroll
+      for (int w = 0; w < WS; ++w) rr |= R[x * WS + w];
+      c += rr != 0ull;
+    }
+    unsigned total = 0;
+    {
+      // block exclusive scan of c
+      const int lane = tid & 31, wp = tid >> 5, nw = T >> 5;
+      unsigned v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane == 31) sc[wp] = v;
+      __syncthreads();
+      unsigned base = 0;
+      for (int k = 0; k < nw; ++k) {
+        if (k < wp) base += sc[k];
+        total += sc[k];
+      }
+      c = base + v - c;  // exclusive prefix
+    }
+    int wipe = has_empty;
+    for (int x = xb; x < xe; ++x) {
+      bool chx = false, empty = true;
+#pragma unroll
+      for (int w = 0; w < WS; ++w) {
+        const unsigned long long rr = R[x * WS + w];
+        if (rr) {
+          chx = true;
+          D[x * WS + w] &= ~rr;
+          R[x * WS + w] = 0ull;
+        }
+        if (D[x * WS + w]) empty = false;
+      }
+      if (chx) {
+        nlist[c++] = (uint32_t)x;
+        wipe |= empty;
+      }
+    }
+    wipe = __syncthreads_or(wipe);
+    uint32_t* tmp = list;
+    list = nlist;
+    nlist = tmp;
+    all_cols = false;
+    cnt = (int)total;
+    has_empty = wipe;
+    if (wipe && !p.full) { status = RAC_WIPEOUT; break; }  // Alg. 1, checked first
+    if (cnt == 0) { status = wipe ? RAC_WIPEOUT : RAC_OK; break; }
+  }
+  uint64_t* dout = p.d_out + (size_t)s * n * wq;
+  for (int i = tid; i < n * wq; i += T) dout[i] = D[(size_t)(i / wq) * WS + (i % wq)];
+  if (tid == 0) {
+    p.iters[s] = t;
+    p.status[s] = status;
+  }
+}
+
 // ---- a1: packing.  One CTA per constrained pair: the d x d relation bit matrix
 // in smem (rows a, words of b), its transpose, both orientations written.
 template <bool GEN>
@@ -308,6 +449,18 @@ cudaError_t wide_fused_grid(int WS, size_t smem, int sm_count, int* grid) {
   if (e != cudaSuccess) return e;
   *grid = per_sm * sm_count;
   return *grid > 0 ? cudaSuccess : cudaErrorInvalidConfiguration;
+}
+
+size_t wide_state_smem(int n, int WS) { return (size_t)n * WS * 16 + (size_t)n * 8; }
+
+cudaError_t launch_wide_state(const WideStateParams& p, int n_states, cudaStream_t s) {
+  const size_t smem = wide_state_smem(p.n, p.WS);
+  const void* k = p.WS == 2 ? (const void*)wide_state<2> : (const void*)wide_state<4>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (p.WS == 2) wide_state<2><<<n_states, 256, smem, s>>>(p);
+  else wide_state<4><<<n_states, 256, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_wide_pack(const WidePack& g, const int32_t* xs, const int32_t* ys, const uint64_t* rows,

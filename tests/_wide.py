@@ -91,3 +91,20 @@ def project(inst, k, D_wide):
             if any(wb[x, j * int(dom[x]) + a] for j in range(k)):
                 out[x] |= U64(1) << U64(a)
     return out
+
+
+def restrict_domains(inst, dom):
+    """The same instance with per-variable domain sizes dom[x] <= inst's: rows
+    a >= dom[x] and columns b >= dom[y] of every relation dropped (input
+    construction: no method arithmetic)."""
+    dom = np.asarray(dom, dtype=np.int32)
+    rows = np.array(inst.rows, dtype=U64, copy=True)
+    nrel, dmax, wq = rows.shape
+    for k in range(nrel):
+        x, y = int(inst.xs[k]), int(inst.ys[k])
+        rows[k, int(dom[x]):, :] = 0
+        for w in range(wq):
+            bits = min(64, max(0, int(dom[y]) - 64 * w))
+            keep = U64(0xFFFFFFFFFFFFFFFF) if bits == 64 else U64((1 << bits) - 1)
+            rows[k, :, w] &= keep
+    return synth.Instance(n=inst.n, dom=dom, xs=inst.xs, ys=inst.ys, rows=rows)

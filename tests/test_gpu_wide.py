@@ -267,3 +267,77 @@ def test_wide_search_parity(rac):
     assert {0: rac.RAC_OK, 1: rac.RAC_WIPEOUT, 2: rac.RAC_BUDGET}[ro] == r
     for key in ("assignments", "recurrences", "wipeouts", "solutions", "max_depth"):
         assert st[key] == sto[key], (key, st[key], sto[key])
+
+
+def test_wide_nonuniform_domains_at_scale(rac):
+    """Non-uniform wide domains at n = 1000 (NEXT-4): domain sizes 16..200 drawn
+    per variable (four words per variable; domains inside one word and across
+    word boundaries), density 0.02, tightness 0.75 (3-4 removing passes);
+    root and W-rand enforcements in stop and full mode equal O1w (status, D_out,
+    iterations, epochs) and are accepted by the O7 certificate."""
+    n, d = 1000, 200
+    rng = np.random.default_rng(12)
+    dom = rng.integers(16, d + 1, size=n).astype(np.int32)
+    base = synth.random_csp_wide(n, d, 0.02, 0.75, seed=8)
+    inst = WD.restrict_domains(base, dom)
+    ctx = rac.RacContext.from_instance(inst)
+    wo = oracle.WideOracle.from_instance(inst)
+    assert ctx.wq == 4 or ctx.wq == wo.wq
+    for k, d_in in enumerate((synth.full_domains_wide(inst.dom), synth.w_rand_wide(inst.dom, 0.8, seed=3))):
+        for full in (False, True):
+            g = same(ctx, wo, d_in, full, (k, full))
+            assert wo.certify_trajectory(d_in, g[1], g[3], g[2], g[0], full) == 0
+
+
+def test_wide_batched(rac):
+    """Batched enforcement on wide contexts (one block per state, wide_state):
+    every state's (status, D_out, iterations) equals O1w on that state alone --
+    W-rand states in stop and full mode, and assigned states (x := a on the
+    root D_ac) with their assigned variable as the per-state seed (Prop. 2)."""
+    import torch
+    rng = np.random.default_rng(31)
+    for k, inst in enumerate(_wide_corpus(10, 91)):
+        ctx = rac.RacContext.from_instance(inst)
+        wo = oracle.WideOracle.from_instance(inst)
+        S = 40 + k
+        states = np.stack([synth.w_rand_wide(inst.dom, 0.85, seed=1000 * k + s) for s in range(S)])
+        din = torch.from_numpy(states.view(np.int64).copy()).cuda()
+        for full in (False, True):
+            dout = torch.zeros_like(din)
+            its = torch.zeros(S, dtype=torch.int32, device="cuda")
+            sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+            ctx.enforce_batch(S, din, dout, its, sts, full=full)
+            torch.cuda.synchronize()
+            out = dout.cpu().numpy().view(np.uint64)
+            for s in range(S):
+                o = wo.rac(states[s], full=full, with_epochs=False)
+                assert (int(sts[s]), int(its[s])) == (o[0], o[2]), (k, s, full)
+                assert np.array_equal(out[s], o[1]), (k, s, full)
+        st, root, _, _ = wo.rac(synth.full_domains_wide(inst.dom), with_epochs=False)
+        if st != oracle.OK:
+            continue
+        bits = WD.bits_of(root, inst.n, wo.wq)
+        xs = [x for x in range(inst.n) if bits[x].sum() >= 2]
+        if not xs:
+            continue
+        seeds, sts_ = [], []
+        for s in range(24):
+            x = int(rng.choice(xs))
+            a = int(rng.choice(np.flatnonzero(bits[x])))
+            b2 = bits.copy()
+            b2[x, :] = False
+            b2[x, a] = True
+            sts_.append(WD.words_of(b2))
+            seeds.append(x)
+        states = np.stack(sts_)
+        din = torch.from_numpy(states.view(np.int64).copy()).cuda()
+        dout = torch.zeros_like(din)
+        its = torch.zeros(24, dtype=torch.int32, device="cuda")
+        sts = torch.zeros(24, dtype=torch.int32, device="cuda")
+        sv = torch.from_numpy(np.asarray(seeds, dtype=np.int32)).cuda()
+        ctx.enforce_batch_seeded(24, din, dout, its, sts, sv)
+        torch.cuda.synchronize()
+        out = dout.cpu().numpy().view(np.uint64)
+        for s in range(24):
+            o = wo.rac(states[s], with_epochs=False)
+            assert (int(sts[s]), int(its[s])) == (o[0], o[2]) and np.array_equal(out[s], o[1]), (k, s, "seeded")
