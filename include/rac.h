@@ -251,11 +251,14 @@ int rac_enforce_batch_seeded(rac_ctx* ctx, int32_t n_states, const uint64_t* d_i
 
 /* Measurement of the batched contraction alone: ONE pass of Eq. 1 (every
  * column tested, no loop control) for n_states device states, d_out[s] = D_1.
- * impl 0 = bit-sliced ALU pass (32 states per u32 OR); impl 1 = tcgen05
- * tensor-core pass (tcgen05.mma.kind::f16: per column y, 128 rows x 16 mask
- * bits times 16 values x 256 states, fp32 counts in TMEM, count > 0 tested in
- * the epilogue).  impl 1 needs max dom <= 16.  world == 1 only.  This is the
- * A/B behind the batched-mode choice, not an enforcement API. */
+ * One-word contexts: impl 0 = bit-sliced ALU pass (32 states per u32 OR);
+ * impl 1 = tcgen05 tensor-core pass (tcgen05.mma.kind::f16: per column y, 128
+ * rows x 16 mask bits times 16 values x 256 states, fp32 counts in TMEM, count
+ * > 0 tested in the epilogue; max dom <= 16).  Wide contexts (max dom > 64):
+ * impl 2 = bit-sliced byte-table pass; impl 3 = pipelined tcgen05 pass (K =
+ * 128 per column as 8 MMAs, two TMEM accumulators, producer / MMA / epilogue
+ * warps; max dom <= 128).  world == 1 only.  This is the A/B behind the
+ * batched-mode choice, not an enforcement API. */
 int rac_batch_pass_eval(rac_ctx* ctx, int32_t impl, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                         void* stream);
 

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librac.so")
-SOURCES = ["rac_api.cu", "rac_kernels.cu", "rac_pack.cu", "rac_batch.cu", "rac_batch_tc.cu", "rac_wide.cu", "rac_state.cu", "rac_batch_cl.cu"]
+SOURCES = ["rac_api.cu", "rac_kernels.cu", "rac_pack.cu", "rac_batch.cu", "rac_batch_tc.cu", "rac_wide.cu", "rac_state.cu", "rac_batch_cl.cu", "rac_wide_tc.cu"]
 DEPS = SOURCES + ["rac_internal.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1398,7 +1398,25 @@ int rac_batch_pass_eval(rac_ctx* c, int32_t impl, int32_t n_states, const uint64
                         void* stream) {
   int rc = check_usable(c);
   if (rc) return rc;
-  if (c->wide) return fail(c, RAC_EUNSUPPORTED, "domains > 64 values: rac_enforce[_ex / _async / _seeded / _seeded_async] only");
+  if (c->wide) {
+    // wide domains: impl 2 = bit-sliced byte-table pass, impl 3 = tcgen05 pass (d <= 128)
+    if (n_states < 1 || !d_in_dev || !d_out_dev || (impl != 2 && impl != 3)) return fail(c, RAC_EINVAL, "bad arguments");
+    if (impl == 3 && c->dmax > 128) return fail(c, RAC_EUNSUPPORTED, "tensor-core wide pass needs max dom <= 128");
+    CK(c, ensure_device(c));
+    const int rows = c->n * c->dmax, rows4 = (rows + 3) & ~3, NW = (n_states + 31) / 32;
+    const size_t need = (size_t)2 * NW * rows4 * 4;
+    if (need > c->eval_cap) {
+      cudaFree(c->eval_buf);
+      c->eval_buf = nullptr;
+      CK(c, cudaMalloc(&c->eval_buf, need));
+      c->eval_cap = need;
+    }
+    WideTcParams w{reinterpret_cast<const uint64_t*>(c->M), c->P, c->pw, c->dom_d, c->n, c->dmax, c->wq, c->WS,
+                   n_states, d_in_dev, d_out_dev, c->eval_buf, c->eval_buf + (size_t)NW * rows4, rows4, NW};
+    CK(c, launch_wide_pass_eval(impl, w, (cudaStream_t)stream));
+    c->launches = impl == 2 ? 3 : 2;
+    return 0;
+  }
   if (n_states < 1 || !d_in_dev || !d_out_dev || (impl != 0 && impl != 1)) return fail(c, RAC_EINVAL, "bad arguments");
   if (c->use_nccl() || c->x_lo != 0 || c->x_hi != c->n) return fail(c, RAC_EUNSUPPORTED, "single-GPU contexts only");
   if (c->sparse) return fail(c, RAC_EUNSUPPORTED, "batched passes need the dense layout (RAC_OPT_DENSE)");

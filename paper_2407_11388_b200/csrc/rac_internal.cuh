@@ -364,6 +364,22 @@ struct WideStateParams {  // wide_state: one block per domain state
   const int32_t* seed_var;  // nullable [S]
   int s0;                   // first state of this launch
 };
+// rac_wide_tc.cu: one batched pass on wide domains, bit-sliced (impl 2) or
+// tcgen05 (impl 3, d <= 128), for the A/B of rac_batch_pass_eval.
+struct WideTcParams {
+  const uint64_t* M;        // wide row-major masks
+  const uint32_t* P;
+  int pw;
+  const int32_t* dom;       // device [n]
+  int n, dmax, wq, WS;
+  int S;                    // states
+  const uint64_t* d_in;     // [S][n * wq]
+  uint64_t* d_out;          // [S][n * wq]
+  const uint32_t* Xin;      // [NW][rows4] state slices (impl 2)
+  uint32_t* Xout;           // [NW][rows4] rows kept per state
+  int rows4, NW;
+};
+cudaError_t launch_wide_pass_eval(int impl, const WideTcParams& p, cudaStream_t st);
 size_t wide_state_smem(int n, int WS);
 cudaError_t launch_wide_state(const WideStateParams& p, int n_states, cudaStream_t s);
 cudaError_t wide_fused_grid(int WS, size_t smem, int sm_count, int* grid);

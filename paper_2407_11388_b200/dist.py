@@ -3,9 +3,11 @@
 torch.distributed is used only to exchange librac's setup tokens (the NCCL
 unique id, or the peer regions' CUDA IPC handles) and to reduce timings; the
 per-pass exchange itself happens inside librac (include/rac.h, "Multi-GPU"):
-an ncclAllGather of the alive-bitvector slices (default), or, with
-``peer=True``, NVLink peer stores and a cross-rank barrier inside the one
-persistent enforcement kernel.
+without RAC_OPT_PEER (the library's default for world > 1) an ncclAllGather of
+the alive-bitvector slices between per-pass launches; with ``peer=True``
+(RAC_OPT_PEER -- what ``bench.py --gpus N`` uses unless ``--exchange nccl``)
+NVLink peer stores and a cross-rank barrier inside the one persistent
+enforcement kernel.
 """
 from __future__ import annotations
 

@@ -341,3 +341,32 @@ def test_wide_batched(rac):
         for s in range(24):
             o = wo.rac(states[s], with_epochs=False)
             assert (int(sts[s]), int(its[s])) == (o[0], o[2]) and np.array_equal(out[s], o[1]), (k, s, "seeded")
+
+
+@pytest.mark.parametrize("impl", [2, 3])
+def test_wide_pass_eval_bitsliced_and_tcgen05(rac, impl):
+    """The wide batched-pass A/B kernels (rac_batch_pass_eval impl 2 = bit-sliced
+    byte tables, impl 3 = pipelined tcgen05 f16 MMA with TMEM accumulators):
+    ONE step of Eq. 1 for every state, D_1 = D_0 minus the values O1w removes
+    in its first pass (removal epoch 1), on instances with 65..128 values
+    (non-uniform included) and 300 states spanning several 256-state tiles."""
+    import torch
+    cases = [synth.random_csp_wide(40, 128, 0.6, 1.0 - 3.0 / 128, 7),
+             synth.random_csp_wide(33, 100, 0.9, 0.95, 8)]
+    rng = np.random.default_rng(2)
+    dom = rng.integers(65, 129, size=50).astype(np.int32)
+    cases.append(WD.restrict_domains(synth.random_csp_wide(50, 128, 0.5, 0.9, 9), dom))
+    for k, inst in enumerate(cases):
+        ctx = rac.RacContext.from_instance(inst)
+        wo = oracle.WideOracle.from_instance(inst)
+        S = 300
+        states = np.stack([synth.w_rand_wide(inst.dom, 0.7, seed=50 * k + s) for s in range(S)])
+        din = torch.from_numpy(states.view(np.int64).copy()).cuda()
+        dout = torch.zeros_like(din)
+        ctx.batch_pass_eval(impl, S, din, dout)
+        torch.cuda.synchronize()
+        out = dout.cpu().numpy().view(np.uint64)
+        for s in range(S):
+            _, _, _, rem = wo.rac(states[s])
+            exp = WD.words_of(WD.bits_of(states[s], inst.n, wo.wq) & (rem != 1))
+            assert np.array_equal(out[s], exp), (k, s)
