@@ -192,8 +192,11 @@ def run_gpu(args, rank, world, local_rank):
     max_ctas = 0
     if os.environ.get("RAC_BENCH_SHARED_GPU") == "1" and world > 1:
         max_ctas = max(1, torch.cuda.get_device_properties(local_rank).multi_processor_count // world)
-    ctx = rac.RacContext.create_random(n, d, dq, tq, seed, device=local_rank, rank=rank, world=world,
-                                       nccl_unique_id=uid, peer=peer, max_ctas=max_ctas)
+    def make_ctx():
+        return rac.RacContext.create_random(n, d, dq, tq, seed, device=local_rank, rank=rank, world=world,
+                                            nccl_unique_id=uid, peer=peer, max_ctas=max_ctas)
+
+    ctx = make_ctx()
     if peer:
         # the regions' CUDA IPC handles travel over the process group; the
         # per-pass exchange then runs inside the one persistent kernel
@@ -295,40 +298,81 @@ def run_gpu(args, rank, world, local_rank):
     sts = torch.zeros(S, dtype=torch.int32, device=dev)
     sv = torch.from_numpy(seed_vars).to(dev) if seed_vars is not None else None
 
-    def step():
+    def step(st=None):
+        st = st if st is not None else stream
         if kind == "dive":
-            ctx.enforce_batch_seeded(S, din, dout, its, sts, sv, stream=stream)
+            ctx.enforce_batch_seeded(S, din, dout, its, sts, sv, stream=st)
         elif kind == "seed":
-            ctx.enforce_seeded_async(din, dout, its, sts, sv, 1, stream=stream)
+            ctx.enforce_seeded_async(din, dout, its, sts, sv, 1, stream=st)
         else:
-            ctx.enforce_async(din, dout, its, sts, stream=stream)
+            ctx.enforce_async(din, dout, its, sts, stream=st)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches_per_step = ctx.last_launch_count
+    ref = (dout.clone(), its.clone(), sts.clone())
+
+    # Single-GPU paths with no host loop are captured into a CUDA graph of G
+    # steps (G divides K), so small enforcements are timed without the host's
+    # per-call launch overhead (the launch-bound inner loop in a graph); the
+    # graph's results are checked against the eager ones.  Multi-GPU paths (and
+    # any path whose capture fails) run eagerly.
+    graph, G, launch_mode = None, 1, "eager"
+    if world == 1 and ctx.path not in ("sharded", "peer") and os.environ.get("RAC_BENCH_GRAPH", "1") == "1":
+        G = max(g for g in range(1, min(args.steps, 50) + 1) if args.steps % g == 0)
+        try:
+            cs = torch.cuda.Stream()
+            cs.wait_stream(stream)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=cs):
+                for _ in range(G):
+                    step(cs)
+            for _ in range(max(1, args.warmup // G)):
+                gr.replay()
+            torch.cuda.synchronize()
+            if not (torch.equal(dout, ref[0]) and torch.equal(its, ref[1]) and torch.equal(sts, ref[2])):
+                raise RuntimeError("graph replay differs from the eager result")
+            graph, launch_mode = gr, "CUDA graph of %d steps (captured async calls; results checked)" % G
+        except Exception as e:  # report, and run eagerly
+            launch_mode = "eager (graph capture failed: %s)" % (repr(e)[:120],)
+            graph, G = None, 1
+            torch.cuda.synchronize()
+            if isinstance(e, rac.RacError):  # a CUDA error inside librac leaves the context unusable
+                ctx.close()
+                ctx = make_ctx()
+                for _ in range(args.warmup):
+                    step()
+                torch.cuda.synchronize()
 
     clocks = ClockSampler(local_rank)
     clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    R = args.steps // G
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(R + 1)]
     evs[0].record(stream)
-    for k in range(args.steps):
-        step()
+    for k in range(R):
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
         evs[k + 1].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    per_step = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    per_step = [evs[k].elapsed_time(evs[k + 1]) / G for k in range(R)]
     total_ms = evs[0].elapsed_time(evs[-1])
     # clocks: keep the sampler running for at least ~1.5 s of the same step loop
     soak = 0
     while time.time() - clocks.t0 < 1.5:
-        step()
-        soak += 1
-        if soak % 64 == 0:
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
+        soak += G
+        if soak % 64 < G:
             torch.cuda.synchronize()
     torch.cuda.synchronize()
     crow = clocks.stop()
@@ -465,7 +509,8 @@ def run_gpu(args, rank, world, local_rank):
             roofline["achieved"] = round(achieved / world, 1)
             roofline["frac"] = round(achieved / world / peak, 4)
     cfg = workload_config(args)
-    setup = {"layout": ctx.layout, "relation_bytes": ctx.relation_bytes,
+    setup = {"layout": ctx.layout, "relation_bytes": ctx.relation_bytes, "kernel_path": ctx.path,
+             "launch": launch_mode,
              "parallelism": (("row-sharded x%d (peer-memory removal exchange + cross-rank barrier inside the "
                               "persistent kernel, NVLink P2P)" if peer else
                               "row-sharded x%d (NCCL all-gather of D per pass)") % world) if world > 1 else "1 GPU",

@@ -537,11 +537,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
         }
       } else if (__ldcg(p.rflag + b) == 0u) {
         wipe = has_empty;
-      } else if (!(p.ab & 2u)) {
-        // D_t = D_{t-1} & ~R, with the next pass's column list built in the same
-        // sweep: thread i owns the contiguous variables [i*chunk, (i+1)*chunk), so
-        // a block scan of the per-thread change counts gives every CTA the same
-        // ascending list (the item -> column mapping must agree across CTAs).
+      } else if (p.ab & 2u) {
+        // A/B variant (RAC_FUSED_AB bit 1; measured slightly slower than the
+        // separate compaction below, profiles/r02c/ab_fused.log): D_t = D_{t-1} &
+        // ~R with the next pass's column list built in the same sweep: thread i
+        // owns the contiguous variables [i*chunk, (i+1)*chunk), so a block scan of
+        // the per-thread change counts gives every CTA the same ascending list
+        // (the item -> column mapping must agree across CTAs).
         const int T = blockDim.x, chunk = (g.n + T - 1) / T;  // <= 128 (n <= 65535)
         const int xb = min(g.n, (int)threadIdx.x * chunk), xe = min(g.n, xb + chunk);
         const int par = t & 1;
