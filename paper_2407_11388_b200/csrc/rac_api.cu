@@ -699,6 +699,11 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.flags = flags;
   static const uint32_t ab = getenv("RAC_FUSED_AB") ? (uint32_t)atoi(getenv("RAC_FUSED_AB")) : 0u;  // tooling
   p.ab = ab;
+  // tail of a column pass claimed in chunks (A/B knobs RAC_CLAIM_DIV / RAC_CLAIM_CH)
+  static const uint32_t cdiv = getenv("RAC_CLAIM_DIV") ? (uint32_t)atoi(getenv("RAC_CLAIM_DIV")) : 16u;
+  static const uint32_t cch = getenv("RAC_CLAIM_CH") ? (uint32_t)atoi(getenv("RAC_CLAIM_CH")) : 0u;
+  p.claim_div = cdiv;
+  p.claim_ch = cch;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));

@@ -120,6 +120,8 @@ struct FusedParams {
   int n_seeds;              // < 0: root call (every column in pass 1); 0: no pass
   uint32_t flags;
   uint32_t ab;              // A/B knobs (tooling, RAC_FUSED_AB): bit 0 legacy grid barrier, bit 1 listed apply
+  uint32_t claim_div;       // column sweep: 1/claim_div of a pass's items claimed dynamically...
+  uint32_t claim_ch;        // ...in chunks of claim_ch items (0: static round robin only)
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
   // Global pass counter (persists across launches): pass t of this launch is
   // pass *seq + t; it selects the rotating buffers and is the cross-rank
