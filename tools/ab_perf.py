@@ -70,6 +70,11 @@ if os.environ.get("AB_SET") == "cols":  # column-sweep workloads only
     print(tag, "auto:", single("c3prop", 2000, 32, 1.0, 0.70, reps=50), single("c3seed", 2000, 32, 1.0, 0.5, "seed", 100),
           single("c2", 500, 20, 1.0, 0.3, reps=1000), flush=True)
     sys.exit(0)
+if os.environ.get("AB_SET") == "fused":
+    print(tag, single("c2", 500, 20, 1.0, 0.3, reps=1000), single("c3stream", 2000, 32, 1.0, 0.5, reps=200),
+          single("c3prop", 2000, 32, 1.0, 0.70, reps=100), single("c3seed", 2000, 32, 1.0, 0.5, "seed", 200),
+          single("c4stream", 8000, 64, 1.0, 0.5, reps=10), flush=True)
+    sys.exit(0)
 if os.environ.get("AB_SET") == "batch":
     print(tag, batch(), flush=True)
     sys.exit(0)

@@ -4,6 +4,6 @@ OUT=gpurun_out/r02f
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1; tail -1 $OUT/smoke.log
 for v in "" "RAC_CLAIM_CH=4 RAC_CLAIM_DIV=16" "RAC_CLAIM_CH=8 RAC_CLAIM_DIV=16" "RAC_CLAIM_CH=8 RAC_CLAIM_DIV=8" "RAC_CLAIM_CH=16 RAC_CLAIM_DIV=8" "RAC_CLAIM_CH=4 RAC_CLAIM_DIV=32"; do
-  env $v AB_SET=cols timeout 300 python tools/ab_perf.py "[$v]" >> $OUT/ab_claim.log 2>&1
+  env $v AB_SET=fused timeout 300 python tools/ab_perf.py "[$v]" >> $OUT/ab_claim.log 2>&1
 done
 cat $OUT/ab_claim.log
