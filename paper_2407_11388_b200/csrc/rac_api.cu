@@ -455,6 +455,7 @@ StateParams state_params(const rac_ctx* c, const uint64_t* d_in, uint64_t* d_out
   sp.n_seeds = -1;
   sp.removed_at = nullptr;
   sp.flags = flags;
+  sp.dbg = nullptr;
   sp.s0 = 0;
   return sp;
 }
@@ -717,6 +718,8 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
     sp.seeds = seeds;
     sp.n_seeds = n_seeds;
     sp.removed_at = removed_at;
+    if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
+    sp.dbg = c->dbg;
     CK(c, launch_state(c->W, c->state_T, sp, 1, c->state_smem, s));
     c->launches++;
     return 0;

@@ -191,6 +191,7 @@ struct StateParams {
   int s0;                   // first state of this launch in the caller's arrays
   int nvec;                 // 16-byte vectors per column
   uint32_t off_R, off_live, off_vx, off_list, off_nlist, off_P, off_M;  // shared-memory layout (state_layout)
+  unsigned long long* dbg;  // nullable: phase stamps of block 0 (RAC_DEBUG_TIMELINE)
 };
 // Offsets of rac_state's shared memory; P staged if <= p_cap bytes, the whole
 // mask tensor if <= m_cap bytes (0 = not staged).  Returns the total bytes.

@@ -89,6 +89,11 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
   __shared__ int sc[T / 32 > 0 ? T / 32 : 1];
   const int n = p.n, dmax = p.dmax, tid = threadIdx.x;
   const int s = blockIdx.x;
+  // phase stamps (tooling, RAC_DEBUG_TIMELINE): thread 0 of block 0
+  int nd = 0;
+  const bool dbg = p.dbg != nullptr && blockIdx.x == 0 && tid == 0;
+#define RAC_SMARK() do { if (dbg && nd < 255) p.dbg[1 + nd++] = globaltimer(); } while (0)
+  RAC_SMARK();
   const int nvec = p.nvec;  // 16-byte vectors per column
   const bool aligned = (dmax % L) == 0;
   // shared memory: D | R (u64 per variable) | live[nvec] (u32) | vx[nvec] (u16) | list | nlist | P (optional)
@@ -152,6 +157,7 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
     }
   }
   __syncthreads();
+  RAC_SMARK();
   int has_empty = 0;
   for (int x = tid; x < n; x += T) has_empty |= load_w<W>(Db + x * W) == 0;
   has_empty = __syncthreads_or(has_empty);
@@ -163,6 +169,7 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
   if (cnt == 0) {  // empty @changed: no pass, status from D_in
     status = has_empty ? kWIPEOUTs : kOKs;
   } else {
+    RAC_SMARK();
     for (;;) {
       ++t;
       // ---- a3/a4: sweep (items = tested column c x vector v)
@@ -214,6 +221,7 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
         }
       }
       const int removed_any = __syncthreads_or(any_rm);
+      RAC_SMARK();
       // ---- a5: D_t = D_{t-1} & ~R; the changed variables (R[x] != 0: marks are
       // made on live rows only) become the next pass's tested columns
       int changed = 0, wipe = has_empty;
@@ -243,16 +251,22 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
       has_empty = wipe;
       if (wipe && !full) { status = kWIPEOUTs; break; }          // Alg. 1
       if (!changed) { status = wipe ? kWIPEOUTs : kOKs; break; }  // Prop. 1 end condition
+      RAC_SMARK();
       for (int v2 = tid; v2 < nvec; v2 += T) live[v2] = vec_live<W>(Db, v2, n, dmax, aligned);
       __syncthreads();
+      RAC_SMARK();
     }
   }
+  RAC_SMARK();
   uint64_t* dout = p.d_out + (size_t)(p.s0 + s) * n;
   for (int x = tid; x < n; x += T) dout[x] = load_w<W>(Db + x * W);
   if (tid == 0) {
     p.iters[p.s0 + s] = t;
     p.status[p.s0 + s] = status;
   }
+  RAC_SMARK();
+  if (dbg) p.dbg[0] = nd;
+#undef RAC_SMARK
 }
 
 template <int W, int T>

@@ -70,6 +70,10 @@ if os.environ.get("AB_SET") == "cols":  # column-sweep workloads only
     print(tag, "auto:", single("c3prop", 2000, 32, 1.0, 0.70, reps=50), single("c3seed", 2000, 32, 1.0, 0.5, "seed", 100),
           single("c2", 500, 20, 1.0, 0.3, reps=1000), flush=True)
     sys.exit(0)
+if os.environ.get("AB_SET") == "small":
+    print(tag, single("c1seed", 20, 8, 0.5, 0.4, "seed", 2000), single("c1root", 20, 8, 0.5, 0.4, "root", 2000),
+          flush=True)
+    sys.exit(0)
 if os.environ.get("AB_SET") == "fused":
     print(tag, single("c2", 500, 20, 1.0, 0.3, reps=1000), single("c3stream", 2000, 32, 1.0, 0.5, reps=200),
           single("c3prop", 2000, 32, 1.0, 0.70, reps=100), single("c3seed", 2000, 32, 1.0, 0.5, "seed", 200),

@@ -35,10 +35,10 @@ def run(name, n, d, p, t, kind="root"):
     k = lib.rac_debug_timeline(ctx._h, buf, 256)
     ts = [buf[i] for i in range(k)]
     if len(ts) < 2:
-        print(f"{name}: single-CTA path (no fused-kernel timeline)", flush=True)
+        print(f"{name}: no timeline", flush=True)
         return
     d_ns = [ts[i + 1] - ts[i] for i in range(k - 1)]
-    print(f"{name}: iters={it.item()} total={ts[-1]-ts[0]} ns  phases(ns)={d_ns}", flush=True)
+    print(f"{name} [{ctx.path}]: iters={it.item()} total={ts[-1]-ts[0]} ns  phases(ns)={d_ns}", flush=True)
 
 
 run("c1-seed", 20, 8, 0.5, 0.4, "seed")
