@@ -145,6 +145,7 @@ struct rac_ctx {
   size_t state_smem = 0;
   int state_T = 128;         // threads per block
   bool small = false;        // single instance small enough for one block
+  bool tiny = false;         // ... and for one warp (n <= 64): rac_tiny
   int64_t launches = 0;
   bool broken = false;
   std::string err;
@@ -430,6 +431,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
     const char* sm = getenv("RAC_SMALL_BYTES");  // A/B knob (tooling only)
     const double small_bytes = sm ? atof(sm) : 256.0 * 1024;
     c->small = c->state_smem > 0 && c->vshards == 1 && !c->nccl_self && (double)mbytes <= small_bytes;
+    const char* tn = getenv("RAC_NO_TINY");  // A/B knob (tooling only)
+    c->tiny = c->small && n <= 64 && c->pw <= 2 && tiny_smem(n, c->col_stride) <= 96 * 1024 && !(tn && *tn == '1');
   }
   CKC(cudaStreamSynchronize(c->stream));
 #undef CKC
@@ -700,11 +703,6 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.flags = flags;
   static const uint32_t ab = getenv("RAC_FUSED_AB") ? (uint32_t)atoi(getenv("RAC_FUSED_AB")) : 0u;  // tooling
   p.ab = ab;
-  // tail of a column pass claimed in chunks (A/B knobs RAC_CLAIM_DIV / RAC_CLAIM_CH)
-  static const uint32_t cdiv = getenv("RAC_CLAIM_DIV") ? (uint32_t)atoi(getenv("RAC_CLAIM_DIV")) : 16u;
-  static const uint32_t cch = getenv("RAC_CLAIM_CH") ? (uint32_t)atoi(getenv("RAC_CLAIM_CH")) : 0u;
-  p.claim_div = cdiv;
-  p.claim_ch = cch;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
@@ -720,7 +718,8 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
     sp.removed_at = removed_at;
     if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
     sp.dbg = c->dbg;
-    CK(c, launch_state(c->W, c->state_T, sp, 1, c->state_smem, s));
+    if (c->tiny) CK(c, launch_tiny(c->W, sp, 1, tiny_smem(c->n, c->col_stride), s));
+    else CK(c, launch_state(c->W, c->state_T, sp, 1, c->state_smem, s));
     c->launches++;
     return 0;
   }

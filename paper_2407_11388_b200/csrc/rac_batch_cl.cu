@@ -48,6 +48,56 @@ __device__ __forceinline__ uint32_t mask_at(const uint8_t* p) {
   else return __ldg(p);
 }
 
+// The support test of my rows against the pass's tested columns.  ci[c] =
+// {byte offset of column c's masks, word offset of its nibble tables}; the
+// list is padded to a multiple of 8 with copies of its last column (a column
+// tested twice gives the same answer), so the 8-wide inner loop has no bounds
+// checks.  CP: some active state has an empty domain (pass 1 of an input with
+// an empty row, or full mode), so an all-ones mask of an absent pair could
+// "fail" and the presence bit must decide (reading R2); otherwise no absent
+// pair can fail and the presence test is skipped.
+template <int W, bool CP>
+__device__ __forceinline__ uint32_t sweep_rows(const uint8_t* __restrict__ M, const uint32_t* __restrict__ P, int pw,
+                                               uint32_t* X, const uint32_t* Tb, const uint2* ci, int cnt8, int r0,
+                                               int r1, int dmax, uint32_t active, uint32_t* chgn) {
+  constexpr int NQ = 2 * W;
+  uint32_t my_or = 0u;
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
+    const uint32_t cur = X[r];
+    const uint32_t live = cur & active;
+    if (!live) continue;
+    const uint8_t* Mrow = M + (size_t)r * W;
+    const int x = r / dmax;
+    uint32_t acc = 0xffffffffu;
+    for (int c0 = 0; c0 < cnt8 && (acc & live) != 0u; c0 += 8) {
+      uint32_t mv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mv[u] = mask_at<W>(Mrow + ci[c0 + u].x);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t* Ty = Tb + ci[c0 + u].y;
+        uint32_t sup = 0u;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) sup |= Ty[q * 16 + ((mv[u] >> (4 * q)) & 15u)];
+        if constexpr (CP) {
+          if ((sup & live) != live) {
+            const int y = (int)(ci[c0 + u].y / (NQ * 16));
+            if (!((__ldg(P + (size_t)x * pw + (y >> 5)) >> (y & 31)) & 1u)) sup = 0xffffffffu;
+          }
+        }
+        acc &= sup;
+      }
+    }
+    const uint32_t nb = cur & (acc | ~active);
+    if (nb != cur) {
+      X[r] = nb;
+      atomicOr(&chgn[x], cur ^ nb);
+      my_or |= cur ^ nb;
+    }
+  }
+  return my_or;
+}
+
 }  // namespace
 
 // Shared memory (dynamic): X [rows4] u32 | T [n][NQ][16] u32 | chg [n] u32 |
@@ -71,6 +121,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   uint32_t* chg = Tb + (size_t)n * NQ * 16;
   uint32_t* chgn = chg + n;
   uint16_t* list = reinterpret_cast<uint16_t*>(chgn + n);
+  uint2* ci = reinterpret_cast<uint2*>(list + (((size_t)n + 7) & ~(size_t)7));  // [n + 8] column info
   const int r0 = k * p.RPC, r1 = min(rows, r0 + p.RPC);  // my rows
   const int x0 = r0 / dmax, x1 = (r1 + dmax - 1) / dmax;  // my variables
   const bool full = (p.flags & kFullCL) != 0;
@@ -112,6 +163,23 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         for (int x = tid; x < n; x += T) chg[x] |= roots;
       __syncthreads();
     }
+    // lanes whose every domain is non-empty at the start of the pass (an empty
+    // one can only come from the input or, in full mode, from a wipeout)
+    uint32_t allne0;
+    {
+      uint32_t ne_all = 0xffffffffu;
+      for (int x = tid; x < n; x += T) {
+        uint32_t ne = 0u;
+        for (int a = 0; a < dmax; ++a) ne |= X[x * dmax + a];
+        ne_all &= ne;
+      }
+      ne_all = __reduce_and_sync(0xffffffffu, ne_all);
+      if (lane == 0) sc[warp] = (int)ne_all;
+      __syncthreads();
+      allne0 = 0xffffffffu;
+      for (int w2 = 0; w2 < nwarps; ++w2) allne0 &= (uint32_t)sc[w2];
+      __syncthreads();
+    }
     int t = 0;
     for (;;) {
       ++t;
@@ -128,7 +196,12 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         cnt = (int)total;
       }
       __syncthreads();
-      // ---- nibble tables of the tested columns
+      // ---- per-column offsets (the list padded to a multiple of 8) and nibble tables
+      const int cnt8 = (cnt + 7) & ~7;
+      for (int c = tid; c < cnt8; c += T) {
+        const int y = list[min(c, cnt - 1)];
+        ci[c] = make_uint2((uint32_t)((size_t)y * p.col_stride), (uint32_t)(y * NQ * 16));
+      }
       for (int i = tid; i < cnt * NQ; i += T) {
         const int c = i / NQ, q = i - c * NQ;
         const int y = list[c];
@@ -145,44 +218,9 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       }
       __syncthreads();
       // ---- a3/a4: my rows against the tested columns, 32 states at a time
-      uint32_t my_or = 0u;
-      for (int r = r0 + tid; r < r1; r += T) {
-        const uint32_t cur = X[r];
-        const uint32_t live = cur & active;
-        if (!live) continue;
-        const int x = r / dmax;
-        const uint8_t* Mrow = p.M + (size_t)r * W;
-        const uint32_t* Prow = p.P + (size_t)x * p.pw;
-        uint32_t acc = 0xffffffffu;
-        for (int c0 = 0; c0 < cnt && (acc & live) != 0u; c0 += 8) {
-          uint32_t mv[8];
-          int yv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            yv[u] = c0 + u < cnt ? (int)list[c0 + u] : -1;
-            mv[u] = yv[u] >= 0 ? mask_at<W>(Mrow + (size_t)yv[u] * p.col_stride) : 0u;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int y = yv[u];
-            if (y < 0) continue;
-            const uint32_t* Ty = Tb + (size_t)y * NQ * 16;
-            uint32_t sup = 0u;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) sup |= Ty[q * 16 + ((mv[u] >> (4 * q)) & 15u)];
-            // some live state lost support on c_xy: only a declared c_xy removes
-            // (absent pairs and y == x store all-ones masks; reading R2)
-            if ((sup & live) != live && !((__ldg(Prow + (y >> 5)) >> (y & 31)) & 1u)) sup = 0xffffffffu;
-            acc &= sup;
-          }
-        }
-        const uint32_t nb = cur & (acc | ~active);
-        if (nb != cur) {
-          X[r] = nb;
-          atomicOr(&chgn[x], cur ^ nb);
-          my_or |= cur ^ nb;
-        }
-      }
+      uint32_t my_or = (~allne0 & active)
+                                 ? sweep_rows<W, true>(p.M, p.P, p.pw, X, Tb, ci, cnt8, r0, r1, dmax, active, chgn)
+                                 : sweep_rows<W, false>(p.M, p.P, p.pw, X, Tb, ci, cnt8, r0, r1, dmax, active, chgn);
       // this CTA's partials: lanes that changed; lanes with every variable non-empty
       uint32_t my_ne = 0xffffffffu;
       __syncthreads();
@@ -235,6 +273,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         if (stop_conv & bit) s_status[tid] = (wipe & bit) ? 1 : 0;
       }
       active &= ~(stop_wipe | stop_conv);
+      allne0 = allne;
       __syncthreads();
       if (active == 0u) break;
     }
@@ -254,7 +293,8 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
 
 size_t batch_cl_smem(int n, int dmax, int W) {
   const size_t rows4 = (((size_t)n * dmax) + 3) & ~(size_t)3;
-  return rows4 * 4 + (size_t)n * (2 * W) * 16 * 4 + (size_t)n * 8 + (((size_t)n * 2 + 15) & ~(size_t)15);
+  return rows4 * 4 + (size_t)n * (2 * W) * 16 * 4 + (size_t)n * 8 + (((size_t)n + 7) & ~(size_t)7) * 2 +
+         ((size_t)n + 8) * 8;
 }
 
 cudaError_t launch_batch_cl(int W, const BatchCLParams& p, int clusters, int C, int threads, size_t smem,

@@ -120,8 +120,6 @@ struct FusedParams {
   int n_seeds;              // < 0: root call (every column in pass 1); 0: no pass
   uint32_t flags;
   uint32_t ab;              // A/B knobs (tooling, RAC_FUSED_AB): bit 0 legacy grid barrier, bit 1 listed apply
-  uint32_t claim_div;       // column sweep: 1/claim_div of a pass's items claimed dynamically...
-  uint32_t claim_ch;        // ...in chunks of claim_ch items (0: static round robin only)
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
   // Global pass counter (persists across launches): pass t of this launch is
   // pass *seq + t; it selects the rotating buffers and is the cross-rank
@@ -197,6 +195,9 @@ struct StateParams {
 // mask tensor if <= m_cap bytes (0 = not staged).  Returns the total bytes.
 size_t state_layout(StateParams& p, int n, int dmax, int W, int rows_pad, int pw, size_t p_cap, size_t m_cap);
 cudaError_t launch_state(int W, int T, const StateParams& p, int n_states, size_t smem, cudaStream_t s);
+// rac_tiny: one warp per state for n <= 64 (the mask tensor in shared memory)
+size_t tiny_smem(int n, size_t col_stride);
+cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, cudaStream_t s);
 
 // rac_batch_cl (rac_batch_cl.cu): one 32-state bit-sliced word per cluster.
 struct BatchCLParams {

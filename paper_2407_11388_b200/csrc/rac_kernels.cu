@@ -54,55 +54,55 @@ __device__ __forceinline__ void mark_removed(unsigned long long* R, int x, unsig
   if (old == 0ull) cl[1 + atomicAdd(cl, 1u)] = (uint32_t)x;
 }
 
-// Work-item iterator of a warp.  Without a counter: plain round robin.  With
-// one: the first (1 - 1/div) of the items are assigned round robin, the rest
-// are claimed from a per-pass counter in chunks of `ch` consecutive items (the
-// next chunk's claim is in flight while the current chunk streams), so SMs that
-// drain HBM faster take more of the tail.  (Measured on the 4 KB items of the
-// column and sparse sweeps: claims of ONE item, one same-address atomic per
-// 4 KB, cost more than the imbalance they remove -- C3 W-stream 88.7 -> 92.1 us;
-// chunked claims cut the atomics by `ch`.)
+// Work-item iterator of a warp: the first ~7/8 of the items are assigned
+// round robin, the rest are claimed one at a time from a per-pass counter
+// (the next claim in flight while the current item streams), so SMs that
+// drain HBM faster take more of the tail.  Without a counter: plain round
+// robin.  (Measured on the 4 KB items of the column and sparse sweeps: one
+// same-address atomic per item costs more than the imbalance it removes --
+// C3 W-stream 88.7 -> 92.1 us -- so those sweeps run round robin.  Claims of
+// 4..16 items per atomic were no better (profiles/r02f/ab_claim.log, c3-prop
+// 288 -> 344..575 us), and the generalised iterator alone slowed the static
+// column sweep 88 -> 112 us on the same box (profiles/r02g): removed.)
+#ifndef RAC_CLAIM_DIV
+#define RAC_CLAIM_DIV 8
+#endif
+constexpr uint32_t kClaimDiv = RAC_CLAIM_DIV;  // 1/kClaimDiv of the items are claimed dynamically
+#ifndef RAC_COL_CLAIM
+#define RAC_COL_CLAIM 0
+#endif
 struct ItemIter {
-  uint32_t items, nw, per, S, k, ch, pend, cur, left;
+  uint32_t items, nw, per, S, k, pending;
   unsigned* wctr;
   int lane;
   uint32_t warp0;
-  __device__ __forceinline__ ItemIter(uint32_t items_, long warp0_, long nwarps_, unsigned* wctr_, uint32_t div = 8,
-                                      uint32_t ch_ = 1)
-      : items(items_), nw((uint32_t)nwarps_), k(0), ch(ch_ ? ch_ : 1u), pend(0), cur(0), left(0), wctr(wctr_),
-        lane(threadIdx.x & 31), warp0((uint32_t)warp0_) {
-    const uint32_t dv = div < 2 ? 2u : div;
-    per = wctr ? (items - items / dv) / nw : (items + nw - 1) / nw;
+  __device__ __forceinline__ ItemIter(uint32_t items_, long warp0_, long nwarps_, unsigned* wctr_)
+      : items(items_), nw((uint32_t)nwarps_), k(0), pending(0), wctr(wctr_), lane(threadIdx.x & 31),
+        warp0((uint32_t)warp0_) {
+    per = wctr ? (items - items / kClaimDiv) / nw : (items + nw - 1) / nw;
     S = wctr ? per * nw : items;
-    if (wctr && per == 0) pend = claim();
+    if (wctr && per == 0) pending = claim();
   }
   __device__ __forceinline__ uint32_t claim() {
     uint32_t b = 0;
     if (lane == 0) b = atomicAdd(wctr, 1u);
-    return S + __shfl_sync(0xffffffffu, b, 0) * ch;
+    return S + __shfl_sync(0xffffffffu, b, 0);
   }
   // next item of this warp (warp-uniform); false when done
   __device__ __forceinline__ bool next(uint32_t& it) {
-    if (k < per) {
-      for (; k < per;) {
-        it = warp0 + k * nw;
-        if (++k == per && wctr) pend = claim();
-        if (it < items) return true;
-      }
-      if (!wctr) return false;
-    }
-    if (!wctr) return false;
     for (;;) {
-      if (left == 0) {
-        cur = pend;
-        if (cur >= items) return false;
-        left = ch;
-        pend = claim();
+      if (k < per) {
+        it = warp0 + k * nw;
+        if (++k == per && wctr) pending = claim();
+        if (it < items) return true;
+      } else if (wctr) {
+        it = pending;
+        if (it >= items) return false;
+        pending = claim();
+        return true;
+      } else {
+        return false;
       }
-      it = cur++;
-      --left;
-      if (it < items) return true;
-      left = 0;  // the chunk ran past the last item: the next claim is past it too
     }
   }
 };
@@ -122,8 +122,7 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
                                           int32_t* removed_at, int t, long warp0, long nwarps,
                                           const uint16_t* cols, int ncol, unsigned* rflag = nullptr,
                                           unsigned* wctr = nullptr, uint32_t* cl = nullptr,
-                                          const EpochMirror* em = nullptr, uint32_t claim_div = 8,
-                                          uint32_t claim_ch = 1) {
+                                          const EpochMirror* em = nullptr) {
   constexpr int RPL = 16 / W, U = kUnroll;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
@@ -137,7 +136,7 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
   const uint32_t upl = upl64 < 1ull ? 1u : (upl64 > (uint64_t)U ? (uint32_t)U : (uint32_t)upl64);
   const uint32_t ipc = (v_hi - v_lo + 32u * upl - 1u) / (32u * upl);  // items per column
   const uint32_t items = ipc * (uint32_t)ncol;
-  ItemIter iter(items, warp0, nwarps, wctr, claim_div, claim_ch);
+  ItemIter iter(items, warp0, nwarps, wctr);
   for (uint32_t it; iter.next(it);) {
     const uint32_t c = it / ipc, chunk = it - c * ipc;
     const int y = cols ? (int)cols[c] : (int)c;
@@ -467,15 +466,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
           __syncthreads();
         }
         sparse_sweep<W>(g, Db, Rc, ep, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n, ipref,
-                        upl, p.rflag + b, nullptr, clc);
+                        upl, p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc);
       } else {
         if (pick_rows(g, live, lst ? vcnt : g.n))
           row_sweep<W, G>(g, Ds, Rc, ep, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b,
                           clc, emp);
         else
           column_sweep<W>(g, Db, Rc, ep, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
-                          p.rflag + b, (p.claim_ch && p.wctr) ? p.wctr + b : nullptr, clc, emp, p.claim_div,
-                          p.claim_ch);
+                          p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc, emp);
       }
       RAC_MARK();
       if (p.dbg != nullptr && t == 1) {  // block-uniform condition: the barrier is safe

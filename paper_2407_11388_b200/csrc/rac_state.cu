@@ -269,6 +269,123 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
 #undef RAC_SMARK
 }
 
+// ---------------------------------------------------------------------------- rac_tiny
+// One WARP runs the whole enforcement of a tiny instance (n <= 64 variables,
+// the mask tensor staged in shared memory): lane-per-row support tests over
+// the tested columns that are declared for the row's variable (reading R2: an
+// absent pair never removes), __syncwarp as the pass barrier, ballots for the
+// loop control (Alg. 1: wipeout checked first, then changed).
+// The column sets are 64-bit masks, so a pass is a few hundred instructions
+// per lane; C1 (n = 20, d = 8) runs in a few microseconds.
+template <int W>
+__global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
+  extern __shared__ uint4 tsm4[];
+  const int n = p.n, dmax = p.dmax, lane = threadIdx.x;
+  uint8_t* Ms = reinterpret_cast<uint8_t*>(tsm4);                          // n * col_stride bytes
+  unsigned long long* D = reinterpret_cast<unsigned long long*>(Ms + (((size_t)n * p.col_stride + 15) & ~(size_t)15));
+  unsigned long long* R = D + 64;
+  unsigned long long* Pm = R + 64;  // Pm[x]: bit y set iff c_xy is declared
+  const int s = p.s0 + blockIdx.x;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(p.M);
+    uint4* dst = reinterpret_cast<uint4*>(Ms);
+    const int nv = (int)((size_t)n * p.col_stride / 16);
+    for (int i = lane; i < nv; i += 32) dst[i] = ldg_stream(src + i);
+  }
+  for (int x = lane; x < 64; x += 32) {
+    D[x] = x < n ? __ldg(p.d_in + (size_t)s * n + x) & __ldg(p.dommask + x) : ~0ull;
+    R[x] = 0ull;
+    unsigned long long pm = 0;
+    if (x < n) {
+      pm = __ldg(p.P + (size_t)x * p.pw);
+      if (p.pw > 1) pm |= (unsigned long long)__ldg(p.P + (size_t)x * p.pw + 1) << 32;
+    }
+    Pm[x] = pm;
+  }
+  unsigned long long T = n >= 64 ? ~0ull : ((1ull << n) - 1ull);  // tested columns: every column (root call)
+  const int sv = p.seed_var ? p.seed_var[s] : -1;
+  if (p.n_seeds >= 0) {
+    unsigned long long m = 0;
+    for (int i = lane; i < p.n_seeds; i += 32) {
+      const int y = p.seeds[i];
+      if (y >= 0 && y < n) m |= 1ull << y;
+    }
+    for (int o = 16; o; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+    T = m;
+  } else if (sv >= 0 && sv < n) {
+    T = 1ull << sv;
+  }
+  __syncwarp();
+  bool has_empty = __any_sync(0xffffffffu, (lane < n && D[lane] == 0ull) || (lane + 32 < n && D[lane + 32] == 0ull));
+  const bool full = (p.flags & 1u) != 0;
+  const int rows = n * dmax;
+  int t = 0, status = 0;
+  if (T == 0ull) {
+    status = has_empty ? 1 : 0;  // empty @changed: no pass
+  } else {
+    for (;;) {
+      ++t;
+      bool any = false;
+      for (int r = lane; r < rows; r += 32) {
+        const int x = r / dmax, a = r - x * dmax;
+        if (!((D[x] >> a) & 1ull)) continue;  // dead row
+        for (unsigned long long cols = T & Pm[x]; cols; cols &= cols - 1ull) {
+          const int y = __ffsll((long long)cols) - 1;
+          if ((load_w<W>(Ms + (size_t)y * p.col_stride + (size_t)r * W) & D[y]) == 0ull) {
+            atomicOr(&R[x], 1ull << a);
+            if (p.removed_at) p.removed_at[(size_t)x * 64 + a] = t;
+            any = true;
+            break;
+          }
+        }
+      }
+      __syncwarp();
+      if (!__any_sync(0xffffffffu, any)) {  // nothing removed: D_t = D_{t-1}
+        status = has_empty ? 1 : 0;
+        break;
+      }
+      unsigned long long C = 0;
+      bool wl = false;
+      for (int x = lane; x < n; x += 32) {
+        const unsigned long long rr = R[x];
+        if (rr) {
+          const unsigned long long nd = D[x] & ~rr;
+          D[x] = nd;
+          R[x] = 0ull;
+          C |= 1ull << x;
+          wl |= nd == 0ull;
+        }
+      }
+      for (int o = 16; o; o >>= 1) C |= __shfl_xor_sync(0xffffffffu, C, o);
+      const bool wipe = has_empty | __any_sync(0xffffffffu, wl);
+      __syncwarp();
+      has_empty = wipe;
+      if (wipe && !full) { status = 1; break; }   // Alg. 1
+      if (C == 0ull) { status = wipe ? 1 : 0; break; }
+      T = C;  // the changed variables are the next pass's columns (Prop. 2)
+    }
+  }
+  for (int x = lane; x < n; x += 32) p.d_out[(size_t)s * n + x] = D[x];
+  if (lane == 0) {
+    p.iters[s] = t;
+    p.status[s] = status;
+  }
+}
+
+size_t tiny_smem(int n, size_t col_stride) { return (((size_t)n * col_stride + 15) & ~(size_t)15) + 3 * 64 * 8; }
+
+cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, cudaStream_t st) {
+  const void* k = W == 1 ? (const void*)rac_tiny<1> : W == 2 ? (const void*)rac_tiny<2> : W == 4 ? (const void*)rac_tiny<4>
+                                                                                                  : (const void*)rac_tiny<8>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  StateParams pp = p;
+  void* args[] = {&pp};
+  return cudaLaunchKernel(k, dim3(n_states), dim3(32), args, smem, st);
+}
+
 template <int W, int T>
 struct LaunchS {
   static cudaError_t go(const StateParams& p, int n_states, size_t smem, cudaStream_t st) {

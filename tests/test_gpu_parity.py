@@ -85,14 +85,17 @@ def test_packer_matches_oracle_layout(rac, n, d, p, t):
 
 
 # ----------------------------------------------------------------------------- corpora
-@pytest.mark.parametrize("path", ["one-block", "fused"])
+@pytest.mark.parametrize("path", ["one-warp", "one-block", "fused"])
 def test_spec_corpus(rac, path, monkeypatch):
     """SPEC.md acceptance corpus shape: 1000 instances, n 2..20, d 1..6,
     density 0.1..1, tightness 0..0.9; W-root and W-rand; stop and full modes --
-    through the one-block kernel (rac_state, the default for small instances)
-    and through the cooperative rac_fused kernel (RAC_SMALL_BYTES=0)."""
+    through the one-warp kernel (rac_tiny, the default for n <= 64), the
+    one-block kernel (rac_state, RAC_NO_TINY=1) and the cooperative rac_fused
+    kernel (RAC_SMALL_BYTES=0)."""
     if path == "fused":
         monkeypatch.setenv("RAC_SMALL_BYTES", "0")
+    if path == "one-block":
+        monkeypatch.setenv("RAC_NO_TINY", "1")
     for k, inst in enumerate(I.random_corpus(1000)):
         ctx = rac.RacContext.from_instance(inst)
         orc = oracle.Oracle.from_instance(inst)
