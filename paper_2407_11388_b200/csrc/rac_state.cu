@@ -372,20 +372,6 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
   }
 }
 
-size_t tiny_smem(int n, size_t col_stride) { return (((size_t)n * col_stride + 15) & ~(size_t)15) + 3 * 64 * 8; }
-
-cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, cudaStream_t st) {
-  const void* k = W == 1 ? (const void*)rac_tiny<1> : W == 2 ? (const void*)rac_tiny<2> : W == 4 ? (const void*)rac_tiny<4>
-                                                                                                  : (const void*)rac_tiny<8>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  StateParams pp = p;
-  void* args[] = {&pp};
-  return cudaLaunchKernel(k, dim3(n_states), dim3(32), args, smem, st);
-}
-
 template <int W, int T>
 struct LaunchS {
   static cudaError_t go(const StateParams& p, int n_states, size_t smem, cudaStream_t st) {
@@ -400,6 +386,20 @@ struct LaunchS {
 };
 
 }  // namespace
+
+size_t tiny_smem(int n, size_t col_stride) { return (((size_t)n * col_stride + 15) & ~(size_t)15) + 3 * 64 * 8; }
+
+cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, cudaStream_t st) {
+  const void* k = W == 1 ? (const void*)rac_tiny<1> : W == 2 ? (const void*)rac_tiny<2> : W == 4 ? (const void*)rac_tiny<4>
+                                                                                                  : (const void*)rac_tiny<8>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  StateParams pp = p;
+  void* args[] = {&pp};
+  return cudaLaunchKernel(k, dim3(n_states), dim3(32), args, smem, st);
+}
 
 // Shared-memory layout of rac_state for an instance (offsets into the dynamic
 // buffer); returns the total bytes.  P is staged only if it fits in `p_cap`.
