@@ -713,6 +713,35 @@ __device__ __forceinline__ void bulk_copy_512(void* dst, const void* src, uint64
       : "memory");
 }
 
+// Stage `bytes` (a multiple of 16, both addresses 16-byte aligned) from global
+// into shared memory with bulk copies (TMA engine): thread 0 initialises the
+// mbarrier, arms it with the byte count and issues <= 32 KB copies; every
+// thread then calls bulk_stage_wait (phase 0).  The mbarrier must not be
+// reused within the launch.
+__device__ __forceinline__ void bulk_stage_start(void* dst, const void* src, uint32_t bytes, uint64_t* mb) {
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mb);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(m));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
+    const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst);
+    for (uint32_t off = 0; off < bytes; off += 32768u) {
+      const uint32_t sz = bytes - off < 32768u ? bytes - off : 32768u;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d0 + off),
+          "l"(static_cast<const uint8_t*>(src) + off), "r"(sz), "r"(m)
+          : "memory");
+    }
+  }
+}
+__device__ __forceinline__ void bulk_stage_wait(uint64_t* mb) {
+  __syncwarp();
+  // thread 0 initialised the barrier before any thread can observe phase 0 complete
+  if (blockDim.x > 32) __syncthreads();
+  mbar_wait(mb, 0);
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
                : "memory");

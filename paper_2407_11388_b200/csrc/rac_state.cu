@@ -117,12 +117,8 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
   }
   if (Ps)
     for (int i = tid; i < n * p.pw; i += T) const_cast<uint32_t*>(Ps)[i] = __ldg(p.P + i);
-  if (Ms) {
-    const uint4* src = reinterpret_cast<const uint4*>(p.M);
-    uint4* dst = const_cast<uint4*>(Ms);
-    const int nv = (int)((size_t)n * cs16);
-    for (int i = tid; i < nv; i += T) dst[i] = ldg_stream(src + i);
-  }
+  __shared__ alignas(8) uint64_t mbar;
+  if (Ms) bulk_stage_start(const_cast<uint4*>(Ms), p.M, (uint32_t)((size_t)n * p.col_stride), &mbar);
   for (int v = tid; v < nvec; v += T) {
     const int r0 = v * L, x0 = r0 / dmax, x1 = (r0 + L - 1) / dmax;
     // one variable per vector (absent-pair skip allowed) -> x0, else 0xffff
@@ -156,6 +152,7 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
       cnt = total;
     }
   }
+  if (Ms) bulk_stage_wait(&mbar);
   __syncthreads();
   RAC_SMARK();
   int has_empty = 0;
@@ -286,12 +283,11 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
   unsigned long long* R = D + 64;
   unsigned long long* Pm = R + 64;  // Pm[x]: bit y set iff c_xy is declared
   const int s = p.s0 + blockIdx.x;
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(p.M);
-    uint4* dst = reinterpret_cast<uint4*>(Ms);
-    const int nv = (int)((size_t)n * p.col_stride / 16);
-    for (int i = lane; i < nv; i += 32) dst[i] = ldg_stream(src + i);
-  }
+  __shared__ alignas(8) uint64_t mbar;
+  // the whole mask tensor in one bulk copy (TMA engine, one round trip) while
+  // the lanes load D and the presence words
+  const uint32_t mbytes = (uint32_t)((size_t)n * p.col_stride);
+  bulk_stage_start(Ms, p.M, mbytes, &mbar);
   for (int x = lane; x < 64; x += 32) {
     D[x] = x < n ? __ldg(p.d_in + (size_t)s * n + x) & __ldg(p.dommask + x) : ~0ull;
     R[x] = 0ull;
@@ -302,6 +298,7 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
     }
     Pm[x] = pm;
   }
+  bulk_stage_wait(&mbar);
   unsigned long long T = n >= 64 ? ~0ull : ((1ull << n) - 1ull);  // tested columns: every column (root call)
   const int sv = p.seed_var ? p.seed_var[s] : -1;
   if (p.n_seeds >= 0) {
