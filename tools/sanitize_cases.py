@@ -5,9 +5,11 @@ initcheck) over every enforcement kernel, each checked against the CPU oracle:
              full mode) and a small C3-shaped propagating instance (n=600 d=32)
   sparse  -- rac_fused<W,0> over the sparse arc-block layout (density 0.25)
   vshard  -- rac_pass + rac_shard_{init,seed,slice,update,finalize} (3 row blocks)
-  wide    -- wide_fused (d=128, propagating), root + seeded
+  wide    -- wide_fused (d=128, propagating), wide_state (batched), wide_bs_pass / wide_tc_pass
+             (tcgen05), the wide search
   state   -- rac_state (one block per state) on single instances up to C2 size
-  batch   -- rac_state and rac_batch_bs on 64 W-dive states, and C1 (one block)
+  batch   -- rac_batch_cl (clusters), rac_batch_bs and rac_state on 64 W-dive states, and C1
+             (one warp: rac_tiny)
   peer    -- one rank of a 2-process RAC_OPT_PEER group (run under torchrun)
 
 Exit status 0 iff every result equals the oracle's.
@@ -94,6 +96,33 @@ def main(case):
         ok &= same(g, o, "wide root")
         dr = synth.w_rand_wide(np.full(n, d), 0.9, 3)
         ok &= same(ctx.enforce(dr, removed_at=True), wo.rac(dr), "wide rand")
+        # batched (wide_state) and the batched-pass A/B kernels (bit-sliced, tcgen05)
+        S = 40
+        states = np.stack([synth.w_rand_wide(np.full(n, d), 0.8, seed=100 + k) for k in range(S)])
+        din = torch.from_numpy(states.view(np.int64).copy()).cuda()
+        dout = torch.zeros_like(din)
+        its = torch.zeros(S, dtype=torch.int32, device="cuda")
+        sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+        ctx.enforce_batch(S, din, dout, its, sts)
+        torch.cuda.synchronize()
+        out = dout.cpu().numpy().view(np.uint64)
+        for k in range(S):
+            o = wo.rac(states[k], with_epochs=False)
+            ok &= (int(sts[k]), int(its[k])) == (o[0], o[2]) and np.array_equal(out[k], o[1])
+        print("wide batched", "OK" if ok else "MISMATCH", flush=True)
+        from tests import _wide as WD
+        for impl in (2, 3):
+            ctx.batch_pass_eval(impl, S, din, dout)
+            torch.cuda.synchronize()
+            out = dout.cpu().numpy().view(np.uint64)
+            for k in range(S):
+                _, _, _, rem = wo.rac(states[k])
+                ok &= np.array_equal(out[k], WD.words_of(WD.bits_of(states[k], n, wo.wq) & (rem != 1)))
+            print("wide pass impl %d" % impl, "OK" if ok else "MISMATCH", flush=True)
+        r, sol, st = ctx.search(full, max_assignments=200)
+        ro, solo, sto = wo.search(full, max_assignments=200)
+        ok &= all(st[k] == sto[k] for k in ("assignments", "recurrences", "wipeouts", "solutions"))
+        print("wide search", "OK" if ok else "MISMATCH", flush=True)
     elif case == "batch":
         n, d, S = 200, 16, 64
         inst = synth.random_csp(n, d, 0.8, 0.3, 1)
@@ -108,9 +137,9 @@ def main(case):
         its = torch.zeros(S, dtype=torch.int32, device="cuda")
         sts = torch.zeros(S, dtype=torch.int32, device="cuda")
         sv = torch.from_numpy(np.asarray(svars, dtype=np.int32)).cuda()
-        for impl, seeded in (("state", False), ("state", True), ("bs", False), ("bs", True)):
-            if impl == "bs":
-                os.environ["RAC_BATCH_IMPL"] = "bs"
+        for impl, seeded in (("cluster", False), ("cluster", True), ("bs", False), ("bs", True), ("state", True)):
+            if impl in ("bs", "state"):
+                os.environ["RAC_BATCH_IMPL"] = impl
             if seeded:
                 ctx.enforce_batch_seeded(S, din, dout, its, sts, sv)
             else:
