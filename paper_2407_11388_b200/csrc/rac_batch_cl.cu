@@ -56,11 +56,21 @@ __device__ __forceinline__ uint32_t mask_at(const uint8_t* p) {
 // an empty row, or full mode), so an all-ones mask of an absent pair could
 // "fail" and the presence bit must decide (reading R2); otherwise no absent
 // pair can fail and the presence test is skipped.
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 template <int W, bool CP>
 __device__ __forceinline__ uint32_t sweep_rows(const uint8_t* __restrict__ M, const uint32_t* __restrict__ P, int pw,
                                                uint32_t* X, const uint32_t* Tb, const uint2* ci, int cnt8, int r0,
                                                int r1, int dmax, uint32_t active, uint32_t* chgn) {
   constexpr int NQ = 2 * W;
+  // nibble tables addressed with 32-bit shared-memory addresses: ci[c].y is the
+  // byte offset of column c's tables, the nibble q of the mask selects the
+  // word (v << 2) of its 16-entry table at byte q * 64
+  const uint32_t tb0 = (uint32_t)__cvta_generic_to_shared(Tb);
   uint32_t my_or = 0u;
   for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
     const uint32_t cur = X[r];
@@ -75,13 +85,14 @@ __device__ __forceinline__ uint32_t sweep_rows(const uint8_t* __restrict__ M, co
       for (int u = 0; u < 8; ++u) mv[u] = mask_at<W>(Mrow + ci[c0 + u].x);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint32_t* Ty = Tb + ci[c0 + u].y;
-        uint32_t sup = 0u;
+        const uint32_t ty = tb0 + ci[c0 + u].y;
+        const uint32_t m = mv[u];
+        uint32_t sup = lds32(ty + ((m << 2) & 0x3Cu));
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) sup |= Ty[q * 16 + ((mv[u] >> (4 * q)) & 15u)];
+        for (int q = 1; q < NQ; ++q) sup |= lds32(ty + 64u * q + ((m >> (4 * q - 2)) & 0x3Cu));
         if constexpr (CP) {
           if ((sup & live) != live) {
-            const int y = (int)(ci[c0 + u].y / (NQ * 16));
+            const int y = (int)(ci[c0 + u].y / (NQ * 64));
             if (!((__ldg(P + (size_t)x * pw + (y >> 5)) >> (y & 31)) & 1u)) sup = 0xffffffffu;
           }
         }
@@ -200,7 +211,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       const int cnt8 = (cnt + 7) & ~7;
       for (int c = tid; c < cnt8; c += T) {
         const int y = list[min(c, cnt - 1)];
-        ci[c] = make_uint2((uint32_t)((size_t)y * p.col_stride), (uint32_t)(y * NQ * 16));
+        ci[c] = make_uint2((uint32_t)((size_t)y * p.col_stride), (uint32_t)(y * NQ * 64));  // {mask bytes, table bytes}
       }
       for (int i = tid; i < cnt * NQ; i += T) {
         const int c = i / NQ, q = i - c * NQ;

@@ -211,7 +211,8 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
             const int x = r / dmax, a = r - x * dmax;
             // R2: an all-ones absent pair only "fails" on an empty D(y); then P decides
             if (dv == 0ull && !((__ldg(p.P + (size_t)x * p.pw + (y >> 5)) >> (y & 31)) & 1u)) continue;
-            atomicOr(&R[x], 1ull << a);
+            // 32-bit shared atomic (native; a 64-bit one compiles to a CAS spin loop)
+            atomicOr(reinterpret_cast<unsigned*>(&R[x]) + (a >> 5), 1u << (a & 31));
             any_rm = true;
             if (p.removed_at) p.removed_at[(size_t)x * 64 + a] = t;
           }
@@ -329,7 +330,8 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
         for (unsigned long long cols = T & Pm[x]; cols; cols &= cols - 1ull) {
           const int y = __ffsll((long long)cols) - 1;
           if ((load_w<W>(Ms + (size_t)y * p.col_stride + (size_t)r * W) & D[y]) == 0ull) {
-            atomicOr(&R[x], 1ull << a);
+            // 32-bit shared atomic (native; a 64-bit one compiles to a CAS spin loop)
+            atomicOr(reinterpret_cast<unsigned*>(&R[x]) + (a >> 5), 1u << (a & 31));
             if (p.removed_at) p.removed_at[(size_t)x * 64 + a] = t;
             any = true;
             break;

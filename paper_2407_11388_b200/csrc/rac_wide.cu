@@ -291,7 +291,8 @@ __global__ void __launch_bounds__(256) wide_state(WideStateParams p) {
             failed = true;
       }
       if (failed) {
-        atomicOr(&R[x * WS + (a >> 6)], 1ull << (a & 63));
+        // 32-bit shared atomic (native; a 64-bit one compiles to a CAS spin loop)
+        atomicOr(reinterpret_cast<unsigned*>(&R[x * WS + (a >> 6)]) + ((a >> 5) & 1), 1u << (a & 31));
         any = 1;
       }
     }
