@@ -146,6 +146,15 @@ struct rac_ctx {
   int state_T = 128;         // threads per block
   bool small = false;        // single instance small enough for one block
   bool tiny = false;         // ... and for one warp (n <= 64): rac_tiny
+  // Blocking calls on small instances: [H2D of d_in (+ seeds), kernel] replayed
+  // as one CUDA graph per (seed count, flags) -- one launch instead of a copy
+  // and a kernel launch (graphs[] keyed by gkey[]; cleared when the staging
+  // buffers move).
+  static constexpr int kGraphs = 8;
+  cudaGraphExec_t graphs[kGraphs] = {};
+  int64_t gkey[kGraphs] = {};
+  int ngraphs = 0;
+  bool graphs_off = false;
   int64_t launches = 0;
   bool broken = false;
   std::string err;
@@ -178,7 +187,10 @@ int mask_bytes(int dmax) { return dmax <= 8 ? 1 : dmax <= 16 ? 2 : dmax <= 32 ? 
 // H2D copy moves both; h_out is pinned AND mapped: the kernels write D_out and
 // [iters, status] straight into it (zero-copy), so no D2H copy is enqueued.
 // (Re)allocates the input staging with room for `seeds` seed entries.
+void drop_graphs(rac_ctx* c);
+
 cudaError_t alloc_staging(rac_ctx* c, size_t nb, size_t seeds) {
+  drop_graphs(c);  // captured graphs point at the old buffers
   cudaFree(c->buf_in);
   cudaFreeHost(c->h_in);
   c->buf_in = nullptr;
@@ -205,9 +217,16 @@ cudaError_t ensure_device(const rac_ctx* c) {
   return cudaSetDevice(c->device);
 }
 
+void drop_graphs(rac_ctx* c) {
+  for (int i = 0; i < c->ngraphs; ++i)
+    if (c->graphs[i]) cudaGraphExecDestroy(c->graphs[i]);
+  c->ngraphs = 0;
+}
+
 void free_ctx(rac_ctx* c) {
   if (!c) return;
   if (c->device >= 0) cudaSetDevice(c->device);
+  drop_graphs(c);
   if (c->comm && nccl().loaded) nccl().CommDestroy(c->comm);
   for (int q = 0; q < RAC_MAX_RANKS; ++q)
     if (c->peer_ipc[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
@@ -1142,6 +1161,8 @@ int rac_enforce_async(rac_ctx* c, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                             (cudaStream_t)stream);
 }
 
+static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags);
+
 int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations, int32_t* removed_at,
                    uint32_t flags) {
   int rc = check_usable(c);
@@ -1151,12 +1172,15 @@ int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* i
   CK(c, ensure_device(c));
   const size_t nw = (size_t)c->n * c->wq, nb = nw * 8;
   memcpy(c->h_in, d_in, nb);
-  CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb, cudaMemcpyHostToDevice, c->stream));
   int32_t* h_res = reinterpret_cast<int32_t*>(c->h_out + nw);
   int32_t* d_res = reinterpret_cast<int32_t*>(c->d_hout + nw);
   h_res[1] = -99;  // "no status reported" until the kernel writes one
-  rc = enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, removed_at ? c->buf_removed : nullptr, flags,
-                          c->stream);
+  if (removed_at) {
+    CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb, cudaMemcpyHostToDevice, c->stream));
+    rc = enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, c->buf_removed, flags, c->stream);
+  } else {
+    rc = enqueue_blocking(c, nb, -1, flags);
+  }
   if (rc) return rc;
   if (removed_at)
     CK(c, cudaMemcpyAsync(removed_at, c->buf_removed, (size_t)c->n * 64 * c->wq * 4, cudaMemcpyDeviceToHost,
@@ -1185,6 +1209,63 @@ int rac_enforce_seeded_async(rac_ctx* c, const uint64_t* d_in_dev, uint64_t* d_o
                             (cudaStream_t)stream, seeds_dev, n_seeds);
 }
 
+// Enqueue the blocking API's H2D copy (d_in words + n_seeds seeds, already in
+// h_in) and the enforcement writing into the mapped output.  Small instances
+// (the one-warp / one-block kernels, where the launch cost is comparable to the
+// kernel) replay a cached CUDA graph of the two; everything else enqueues them.
+static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags) {
+  const size_t nw = (size_t)c->n * c->wq;
+  int32_t* d_res = reinterpret_cast<int32_t*>(c->d_hout + nw);
+  const int32_t* seeds = n_seeds >= 0 ? c->buf_seeds : nullptr;
+  const size_t bytes = nb + (size_t)std::max(0, n_seeds) * 4;
+  static const bool no_graph = getenv("RAC_NO_BLOCKING_GRAPH") != nullptr;  // A/B knob (tooling only)
+  if (!c->small || c->peer || c->wide || c->graphs_off || no_graph) {
+    CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream));
+    return enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
+  }
+  const int64_t key = ((int64_t)n_seeds << 8) | (int64_t)flags;
+  for (int i = 0; i < c->ngraphs; ++i)
+    if (c->gkey[i] == key) {
+      CK(c, cudaGraphLaunch(c->graphs[i], c->stream));
+      c->launches = 1;
+      return 0;
+    }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed);
+  int rc = 0;
+  if (e == cudaSuccess) {
+    e = cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream);
+    if (e == cudaSuccess)
+      rc = enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
+    cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (rc == 0 && e == cudaSuccess) e = cudaGraphInstantiate(&ex, g, 0);
+  if (g) cudaGraphDestroy(g);
+  if (rc != 0 || e != cudaSuccess) {
+    // capture not possible here: remember, and run this call directly
+    cudaGetLastError();
+    c->broken = false;
+    c->graphs_off = true;
+    CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream));
+    return enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
+  }
+  if (c->ngraphs == rac_ctx::kGraphs) {
+    cudaGraphExecDestroy(c->graphs[0]);
+    for (int i = 1; i < c->ngraphs; ++i) {
+      c->graphs[i - 1] = c->graphs[i];
+      c->gkey[i - 1] = c->gkey[i];
+    }
+    --c->ngraphs;
+  }
+  c->graphs[c->ngraphs] = ex;
+  c->gkey[c->ngraphs++] = key;
+  CK(c, cudaGraphLaunch(ex, c->stream));
+  c->launches = 1;
+  return 0;
+}
+
 int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations, const int32_t* seeds,
                        int32_t n_seeds, uint32_t flags) {
   int rc = check_usable(c);
@@ -1202,12 +1283,9 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   }
   memcpy(c->h_in, d_in, nb);
   if (n_seeds > 0) memcpy(reinterpret_cast<uint8_t*>(c->h_in) + nb, seeds, (size_t)n_seeds * 4);
-  CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, nb + (size_t)n_seeds * 4, cudaMemcpyHostToDevice, c->stream));
   int32_t* h_res = reinterpret_cast<int32_t*>(c->h_out + nw);
-  int32_t* d_res = reinterpret_cast<int32_t*>(c->d_hout + nw);
   h_res[1] = -99;
-  rc = enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, c->buf_seeds,
-                          n_seeds);
+  rc = enqueue_blocking(c, nb, n_seeds, flags);
   if (rc) return rc;
   CK(c, cudaStreamSynchronize(c->stream));
   memcpy(d_out, c->h_out, nb);

@@ -285,6 +285,10 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
   unsigned long long* Pm = R + 64;  // Pm[x]: bit y set iff c_xy is declared
   const int s = p.s0 + blockIdx.x;
   __shared__ alignas(8) uint64_t mbar;
+  int nd = 0;  // phase stamps (tooling, RAC_DEBUG_TIMELINE): lane 0 of block 0
+  const bool dbg = p.dbg != nullptr && blockIdx.x == 0 && lane == 0;
+#define RAC_TMARK() do { if (dbg && nd < 255) p.dbg[1 + nd++] = globaltimer(); } while (0)
+  RAC_TMARK();
   // the whole mask tensor in one bulk copy (TMA engine, one round trip) while
   // the lanes load D and the presence words
   const uint32_t mbytes = (uint32_t)((size_t)n * p.col_stride);
@@ -300,6 +304,7 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
     Pm[x] = pm;
   }
   bulk_stage_wait(&mbar);
+  RAC_TMARK();
   unsigned long long T = n >= 64 ? ~0ull : ((1ull << n) - 1ull);  // tested columns: every column (root call)
   const int sv = p.seed_var ? p.seed_var[s] : -1;
   if (p.n_seeds >= 0) {
@@ -339,6 +344,7 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
         }
       }
       __syncwarp();
+      RAC_TMARK();
       if (!__any_sync(0xffffffffu, any)) {  // nothing removed: D_t = D_{t-1}
         status = has_empty ? 1 : 0;
         break;
@@ -362,6 +368,7 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
       if (wipe && !full) { status = 1; break; }   // Alg. 1
       if (C == 0ull) { status = wipe ? 1 : 0; break; }
       T = C;  // the changed variables are the next pass's columns (Prop. 2)
+      RAC_TMARK();
     }
   }
   for (int x = lane; x < n; x += 32) p.d_out[(size_t)s * n + x] = D[x];
@@ -369,6 +376,9 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
     p.iters[s] = t;
     p.status[s] = status;
   }
+  RAC_TMARK();
+  if (dbg) p.dbg[0] = nd;
+#undef RAC_TMARK
 }
 
 template <int W, int T>
