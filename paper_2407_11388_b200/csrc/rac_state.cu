@@ -268,32 +268,35 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
 }
 
 // ---------------------------------------------------------------------------- rac_tiny
-// One WARP runs the whole enforcement of a tiny instance (n <= 64 variables,
-// the mask tensor staged in shared memory): lane-per-row support tests over
-// the tested columns that are declared for the row's variable (reading R2: an
-// absent pair never removes), __syncwarp as the pass barrier, ballots for the
-// loop control (Alg. 1: wipeout checked first, then changed).
-// The column sets are 64-bit masks, so a pass is a few hundred instructions
-// per lane; C1 (n = 20, d = 8) runs in a few microseconds.
+// One small BLOCK (kTinyT threads) runs the whole enforcement of a tiny
+// instance (n <= 64 variables; the mask tensor staged in shared memory by one
+// bulk copy): thread per row (x,a), the row's tested-and-declared columns as a
+// 64-bit set (reading R2: an absent pair never removes) taken four at a time so
+// the shared-memory loads overlap, early exit on the first empty support set;
+// __syncthreads as the pass barrier, block-wide OR reductions for Alg. 1's loop
+// control (lines 198-210: wipeout checked first, then "changed").  C1 (n = 20,
+// d = 8: 160 rows) is one row per thread.
+constexpr int kTinyT = 256;
+
 template <int W>
-__global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
+__global__ void __launch_bounds__(kTinyT) rac_tiny(StateParams p) {
   extern __shared__ uint4 tsm4[];
-  const int n = p.n, dmax = p.dmax, lane = threadIdx.x;
-  uint8_t* Ms = reinterpret_cast<uint8_t*>(tsm4);                          // n * col_stride bytes
+  __shared__ alignas(8) uint64_t mbar;
+  __shared__ unsigned s_or[2];  // the pass's changed variables (low / high word)
+  const int n = p.n, dmax = p.dmax, tid = threadIdx.x;
+  uint8_t* Ms = reinterpret_cast<uint8_t*>(tsm4);  // n * col_stride bytes
   unsigned long long* D = reinterpret_cast<unsigned long long*>(Ms + (((size_t)n * p.col_stride + 15) & ~(size_t)15));
   unsigned long long* R = D + 64;
   unsigned long long* Pm = R + 64;  // Pm[x]: bit y set iff c_xy is declared
   const int s = p.s0 + blockIdx.x;
-  __shared__ alignas(8) uint64_t mbar;
-  int nd = 0;  // phase stamps (tooling, RAC_DEBUG_TIMELINE): lane 0 of block 0
-  const bool dbg = p.dbg != nullptr && blockIdx.x == 0 && lane == 0;
+  int nd = 0;  // phase stamps (tooling, RAC_DEBUG_TIMELINE): thread 0 of block 0
+  const bool dbg = p.dbg != nullptr && blockIdx.x == 0 && tid == 0;
 #define RAC_TMARK() do { if (dbg && nd < 255) p.dbg[1 + nd++] = globaltimer(); } while (0)
   RAC_TMARK();
-  // the whole mask tensor in one bulk copy (TMA engine, one round trip) while
-  // the lanes load D and the presence words
-  const uint32_t mbytes = (uint32_t)((size_t)n * p.col_stride);
-  bulk_stage_start(Ms, p.M, mbytes, &mbar);
-  for (int x = lane; x < 64; x += 32) {
+  // the whole mask tensor in one bulk copy (TMA engine) while D and P load
+  bulk_stage_start(Ms, p.M, (uint32_t)((size_t)n * p.col_stride), &mbar);
+  if (tid < 64) {
+    const int x = tid;
     D[x] = x < n ? __ldg(p.d_in + (size_t)s * n + x) & __ldg(p.dommask + x) : ~0ull;
     R[x] = 0ull;
     unsigned long long pm = 0;
@@ -303,13 +306,13 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
     }
     Pm[x] = pm;
   }
-  bulk_stage_wait(&mbar);
-  RAC_TMARK();
-  unsigned long long T = n >= 64 ? ~0ull : ((1ull << n) - 1ull);  // tested columns: every column (root call)
+  if (tid < 2) s_or[tid] = 0u;
+  // tested columns of pass 1: the seeds (seeded call), else every column
+  unsigned long long T = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
   const int sv = p.seed_var ? p.seed_var[s] : -1;
   if (p.n_seeds >= 0) {
     unsigned long long m = 0;
-    for (int i = lane; i < p.n_seeds; i += 32) {
+    for (int i = tid & 31; i < p.n_seeds; i += 32) {  // every warp computes the same set
       const int y = p.seeds[i];
       if (y >= 0 && y < n) m |= 1ull << y;
     }
@@ -318,8 +321,9 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
   } else if (sv >= 0 && sv < n) {
     T = 1ull << sv;
   }
-  __syncwarp();
-  bool has_empty = __any_sync(0xffffffffu, (lane < n && D[lane] == 0ull) || (lane + 32 < n && D[lane + 32] == 0ull));
+  bulk_stage_wait(&mbar);  // includes a __syncthreads: D, P visible
+  RAC_TMARK();
+  int has_empty = __syncthreads_or(tid < n && D[tid] == 0ull);
   const bool full = (p.flags & 1u) != 0;
   const int rows = n * dmax;
   int t = 0, status = 0;
@@ -329,41 +333,53 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
     for (;;) {
       ++t;
       bool any = false;
-      for (int r = lane; r < rows; r += 32) {
+      for (int r = tid; r < rows; r += kTinyT) {
         const int x = r / dmax, a = r - x * dmax;
         if (!((D[x] >> a) & 1ull)) continue;  // dead row
-        for (unsigned long long cols = T & Pm[x]; cols; cols &= cols - 1ull) {
-          const int y = __ffsll((long long)cols) - 1;
-          if ((load_w<W>(Ms + (size_t)y * p.col_stride + (size_t)r * W) & D[y]) == 0ull) {
-            // 32-bit shared atomic (native; a 64-bit one compiles to a CAS spin loop)
-            atomicOr(reinterpret_cast<unsigned*>(&R[x]) + (a >> 5), 1u << (a & 31));
-            if (p.removed_at) p.removed_at[(size_t)x * 64 + a] = t;
-            any = true;
-            break;
+        const uint8_t* mrow = Ms + (size_t)r * W;
+        bool failed = false;
+        for (unsigned long long cols = T & Pm[x]; cols && !failed;) {
+          int yv[4];
+          uint64_t mv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            yv[u] = cols ? __ffsll((long long)cols) - 1 : -1;
+            cols &= cols - 1ull;
+            if (yv[u] >= 0) mv[u] = load_w<W>(mrow + (size_t)yv[u] * p.col_stride);
           }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (yv[u] >= 0 && (mv[u] & D[yv[u]]) == 0ull) failed = true;
+        }
+        if (failed) {
+          // 32-bit shared atomic (native; a 64-bit one compiles to a CAS spin loop)
+          atomicOr(reinterpret_cast<unsigned*>(&R[x]) + (a >> 5), 1u << (a & 31));
+          if (p.removed_at) p.removed_at[(size_t)x * 64 + a] = t;
+          any = true;
         }
       }
-      __syncwarp();
-      RAC_TMARK();
-      if (!__any_sync(0xffffffffu, any)) {  // nothing removed: D_t = D_{t-1}
+      if (!__syncthreads_or(any)) {  // nothing removed: D_t = D_{t-1}
+        RAC_TMARK();
         status = has_empty ? 1 : 0;
         break;
       }
-      unsigned long long C = 0;
-      bool wl = false;
-      for (int x = lane; x < n; x += 32) {
+      RAC_TMARK();
+      int wl = 0;
+      if (tid < n) {
+        const int x = tid;
         const unsigned long long rr = R[x];
         if (rr) {
-          const unsigned long long nd = D[x] & ~rr;
-          D[x] = nd;
+          const unsigned long long nd2 = D[x] & ~rr;
+          D[x] = nd2;
           R[x] = 0ull;
-          C |= 1ull << x;
-          wl |= nd == 0ull;
+          atomicOr(&s_or[x >> 5], 1u << (x & 31));
+          wl = nd2 == 0ull;
         }
       }
-      for (int o = 16; o; o >>= 1) C |= __shfl_xor_sync(0xffffffffu, C, o);
-      const bool wipe = has_empty | __any_sync(0xffffffffu, wl);
-      __syncwarp();
+      const int wipe = has_empty | __syncthreads_or(wl);
+      const unsigned long long C = ((unsigned long long)s_or[1] << 32) | s_or[0];
+      __syncthreads();
+      if (tid < 2) s_or[tid] = 0u;  // ordered before the next pass's atomics by its barrier
       has_empty = wipe;
       if (wipe && !full) { status = 1; break; }   // Alg. 1
       if (C == 0ull) { status = wipe ? 1 : 0; break; }
@@ -371,8 +387,8 @@ __global__ void __launch_bounds__(32) rac_tiny(StateParams p) {
       RAC_TMARK();
     }
   }
-  for (int x = lane; x < n; x += 32) p.d_out[(size_t)s * n + x] = D[x];
-  if (lane == 0) {
+  if (tid < n) p.d_out[(size_t)s * n + tid] = D[tid];
+  if (tid == 0) {
     p.iters[s] = t;
     p.status[s] = status;
   }
@@ -407,7 +423,7 @@ cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, 
   }
   StateParams pp = p;
   void* args[] = {&pp};
-  return cudaLaunchKernel(k, dim3(n_states), dim3(32), args, smem, st);
+  return cudaLaunchKernel(k, dim3(n_states), dim3(kTinyT), args, smem, st);
 }
 
 // Shared-memory layout of rac_state for an instance (offsets into the dynamic
