@@ -38,3 +38,19 @@ for impl in (2, 3):
                       "ms": round(med, 4), "T_tests_per_s": round(tests / med / 1e9, 3),
                       "mma_TFLOPs_if_tc": round(flops / med / 1e9, 1)}), flush=True)
 print(json.dumps({"same_result": bool(np.array_equal(outs[2], outs[3]))}))
+# the product batched enforcement on the same states (wide_state, one block per
+# state, every pass to each state's own fixpoint), for scale
+dout = torch.zeros_like(din)
+its = torch.zeros(S, dtype=torch.int32, device="cuda")
+sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+for _ in range(2):
+    ctx.enforce_batch(S, din, dout, its, sts)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+for _ in range(3):
+    ctx.enforce_batch(S, din, dout, its, sts)
+b.record()
+torch.cuda.synchronize()
+print(json.dumps({"wide_state_enforcement_ms": round(a.elapsed_time(b) / 3, 4),
+                  "mean_iterations": float(its.float().mean().item()), "max_iterations": int(its.max().item())}))
