@@ -256,8 +256,9 @@ int rac_enforce_batch_seeded(rac_ctx* ctx, int32_t n_states, const uint64_t* d_i
  * rows x 16 mask bits times 16 values x 256 states, fp32 counts in TMEM, count
  * > 0 tested in the epilogue; max dom <= 16).  Wide contexts (max dom > 64):
  * impl 2 = bit-sliced byte-table pass; impl 3 = pipelined tcgen05 pass (K =
- * 128 per column as 8 MMAs, two TMEM accumulators, producer / MMA / epilogue
- * warps; max dom <= 128).  world == 1 only.  This is the A/B behind the
+ * 128 per column as 8 kind::f16 MMAs, two TMEM accumulators, producer / MMA /
+ * epilogue warps; max dom <= 128); impl 4 = the same with fp8 (e4m3) 0/1
+ * operands (kind::f8f6f4, 4 MMAs of K = 32 per column, half the operand bytes).  world == 1 only.  This is the A/B behind the
  * batched-mode choice, not an enforcement API. */
 int rac_batch_pass_eval(rac_ctx* ctx, int32_t impl, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                         void* stream);

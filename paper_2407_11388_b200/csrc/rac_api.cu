@@ -1485,8 +1485,8 @@ int rac_batch_pass_eval(rac_ctx* c, int32_t impl, int32_t n_states, const uint64
   if (rc) return rc;
   if (c->wide) {
     // wide domains: impl 2 = bit-sliced byte-table pass, impl 3 = tcgen05 pass (d <= 128)
-    if (n_states < 1 || !d_in_dev || !d_out_dev || (impl != 2 && impl != 3)) return fail(c, RAC_EINVAL, "bad arguments");
-    if (impl == 3 && c->dmax > 128) return fail(c, RAC_EUNSUPPORTED, "tensor-core wide pass needs max dom <= 128");
+    if (n_states < 1 || !d_in_dev || !d_out_dev || impl < 2 || impl > 4) return fail(c, RAC_EINVAL, "bad arguments");
+    if (impl >= 3 && c->dmax > 128) return fail(c, RAC_EUNSUPPORTED, "tensor-core wide pass needs max dom <= 128");
     CK(c, ensure_device(c));
     const int rows = c->n * c->dmax, rows4 = (rows + 3) & ~3, NW = (n_states + 31) / 32;
     const size_t need = (size_t)2 * NW * rows4 * 4;

@@ -119,8 +119,13 @@ constexpr int kTN = 256;     // states per tile (MMA N)
 constexpr int kK = 128;      // values of y per column (K), 8 MMAs of K = 16
 constexpr int kSlabA = kTM * 32;  // bytes of one K = 16 slab of A (128 rows x 16 f16)
 constexpr int kSlabB = kTN * 32;
-constexpr int kStageA = kSlabA * (kK / 16);  // 32 KB
-constexpr int kStageB = kSlabB * (kK / 16);  // 64 KB
+// f16 operands: K = 16 per MMA, 8 slabs per column; fp8 (e4m3): K = 32 per MMA,
+// 4 slabs.  A slab row is 32 bytes either way.
+template <bool F8> __host__ __device__ constexpr int slabs() { return F8 ? kK / 32 : kK / 16; }
+template <bool F8> __host__ __device__ constexpr int stageA() { return kSlabA * slabs<F8>(); }  // 32 KB f16, 16 KB fp8
+template <bool F8> __host__ __device__ constexpr int stageB() { return kSlabB * slabs<F8>(); }  // 64 KB f16, 32 KB fp8
+constexpr int kStageA = kSlabA * (kK / 16);
+constexpr int kStageB = kSlabB * (kK / 16);
 // K-major, no-swizzle canonical layout inside a slab: core matrices of 8 rows x
 // 16 bytes; row i, K-chunk j (8 f16) at (i/8)*256 + j*128 + (i%8)*16 bytes.
 constexpr uint32_t kLBO = 128, kSBO = 256;
@@ -158,6 +163,28 @@ __device__ __forceinline__ void put_row(uint8_t* base, int slab_bytes, int i, ui
   }
 }
 
+// fp8 (e4m3, 1.0 = 0x38): 128 bits -> row i, 4 K-slabs of 32 elements, each two
+// 16-element chunks; byte -> 8 fp8 from a 256-entry u64 table
+__device__ __forceinline__ void put_row8(uint8_t* base, int slab_bytes, int i, uint64_t lo, uint64_t hi,
+                                         const unsigned long long* lut8) {
+  uint8_t* p = base + (i >> 3) * kSBO + (i & 7) * 16;
+#pragma unroll
+  for (int sl = 0; sl < kK / 32; ++sl) {
+    const uint32_t b32 = (uint32_t)((sl < 2 ? lo : hi) >> (32 * (sl & 1)));
+    *reinterpret_cast<ulonglong2*>(p + sl * slab_bytes) = make_ulonglong2(lut8[b32 & 255u], lut8[(b32 >> 8) & 255u]);
+    *reinterpret_cast<ulonglong2*>(p + sl * slab_bytes + kLBO) =
+        make_ulonglong2(lut8[(b32 >> 16) & 255u], lut8[b32 >> 24]);
+  }
+}
+
+__device__ __forceinline__ unsigned long long fp8x8(uint32_t bits) {
+  unsigned long long v = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if ((bits >> j) & 1u) v |= 0x38ull << (8 * j);
+  return v;
+}
+
 __device__ __forceinline__ void mbar_init1(uint64_t* mb, unsigned cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(mb)), "r"(cnt));
 }
@@ -183,17 +210,20 @@ __device__ __forceinline__ void mbar_wait1(uint64_t* mb, uint32_t parity) {
 // 288 threads: warps 0-3 producers (thread i = row i of the tile and states
 // 2i, 2i+1), warps 4-7 epilogue (thread = row = TMEM lane), warp 8 lane 0 issues
 // the MMAs.  Dynamic smem: 2 stages x (A 32 KB + B 64 KB).
+template <bool F8>
 __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   __shared__ alignas(8) uint64_t full_bar[2], done_bar[2], free_bar[2];
   __shared__ uint32_t tmem_base_s;
-  __shared__ uint4 lut[256];  // byte -> 8 f16 (0 or 1.0)
+  __shared__ uint4 lut[256];                // byte -> 8 f16 (0 or 1.0)
+  __shared__ unsigned long long lut8[256];  // byte -> 8 fp8 e4m3 (0 or 1.0)
   const int tid = threadIdx.x, warp = tid >> 5;
   const int rows = p.n * p.dmax;
   const int row0 = blockIdx.x * kTM;
   const int s0 = blockIdx.y * kTN;
-  uint8_t* sA[2] = {tsm, tsm + kStageA + kStageB};
-  uint8_t* sB[2] = {tsm + kStageA, tsm + 2 * kStageA + kStageB};
+  constexpr int SA = stageA<F8>(), SB = stageB<F8>();
+  uint8_t* sA[2] = {tsm, tsm + SA + SB};
+  uint8_t* sB[2] = {tsm + SA, tsm + 2 * SA + SB};
   if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tmem_base_s)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -206,7 +236,10 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  for (int v = tid; v < 256; v += blockDim.x) lut[v] = f16x8((uint32_t)v);
+  for (int v = tid; v < 256; v += blockDim.x) {
+    if (F8) lut8[v] = fp8x8((uint32_t)v);
+    else lut[v] = f16x8((uint32_t)v);
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -225,7 +258,8 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
         lo = __ldg(mp);
         hi = __ldg(mp + 1);
       }
-      put_row(sA[st], kSlabA, i, lo, hi, lut);
+      if constexpr (F8) put_row8(sA[st], kSlabA, i, lo, hi, lut8);
+      else put_row(sA[st], kSlabA, i, lo, hi, lut);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int s = s0 + 2 * i + h;
@@ -237,7 +271,8 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
           a = __ldg(dp);
           b = p.wq > 1 ? __ldg(dp + 1) : 0ull;
         }
-        put_row(sB[st], kSlabB, 2 * i + h, a, b, lut);
+        if constexpr (F8) put_row8(sB[st], kSlabB, 2 * i + h, a, b, lut8);
+        else put_row(sB[st], kSlabB, 2 * i + h, a, b, lut);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core
       mbar_arrive1(&full_bar[st]);
@@ -293,14 +328,22 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t d_tmem = tmem + (uint32_t)(st * kTN);
 #pragma unroll
-      for (int sl = 0; sl < kK / 16; ++sl) {
+      for (int sl = 0; sl < slabs<F8>(); ++sl) {
         const uint64_t adesc = make_desc(su32(sA[st] + sl * kSlabA));
         const uint64_t bdesc = make_desc(su32(sB[st] + sl * kSlabB));
         const uint32_t accum = sl > 0 ? 1u : 0u;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+        if constexpr (F8) {
+          // e4m3 x e4m3 -> f32: the a/b format fields of idesc are 0 (E4M3) as for f16
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+              "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+        } else {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+              "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+        }
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           su32(&done_bar[st])));
@@ -311,7 +354,7 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-size_t wide_tc_smem() { return (size_t)2 * (kStageA + kStageB); }
+size_t wide_tc_smem(bool f8) { return (size_t)2 * (f8 ? stageA<true>() + stageB<true>() : kStageA + kStageB); }
 
 cudaError_t launch_wide_pass_eval(int impl, const WideTcParams& p, cudaStream_t st) {
   const int rows = p.n * p.dmax;
@@ -326,11 +369,14 @@ cudaError_t launch_wide_pass_eval(int impl, const WideTcParams& p, cudaStream_t 
     if (p.WS == 2) wide_bs_pass<2><<<grid, 1024, 0, st>>>(p);
     else wide_bs_pass<4><<<grid, 1024, 0, st>>>(p);
   } else {
-    const size_t smem = wide_tc_smem();
-    cudaError_t e = cudaFuncSetAttribute(wide_tc_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool f8 = impl == 4;
+    const size_t smem = wide_tc_smem(f8);
+    const void* k = f8 ? (const void*)wide_tc_pass<true> : (const void*)wide_tc_pass<false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((rows + kTM - 1) / kTM, (p.S + kTN - 1) / kTN);
-    wide_tc_pass<<<grid, 288, smem, st>>>(p);
+    if (f8) wide_tc_pass<true><<<grid, 288, smem, st>>>(p);
+    else wide_tc_pass<false><<<grid, 288, smem, st>>>(p);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -343,10 +343,11 @@ def test_wide_batched(rac):
             assert (int(sts[s]), int(its[s])) == (o[0], o[2]) and np.array_equal(out[s], o[1]), (k, s, "seeded")
 
 
-@pytest.mark.parametrize("impl", [2, 3])
+@pytest.mark.parametrize("impl", [2, 3, 4])
 def test_wide_pass_eval_bitsliced_and_tcgen05(rac, impl):
     """The wide batched-pass A/B kernels (rac_batch_pass_eval impl 2 = bit-sliced
-    byte tables, impl 3 = pipelined tcgen05 f16 MMA with TMEM accumulators):
+    byte tables, impl 3 = pipelined tcgen05 f16 MMA with TMEM accumulators,
+    impl 4 = the same with fp8 e4m3 0/1 operands, kind::f8f6f4):
     ONE step of Eq. 1 for every state, D_1 = D_0 minus the values O1w removes
     in its first pass (removal epoch 1), on instances with 65..128 values
     (non-uniform included) and 300 states spanning several 256-state tiles."""

@@ -17,7 +17,7 @@ ctx = rac.RacContext.create_random(n, d, synth.quant_density(0.8), synth.quant_t
 states = np.stack([synth.w_rand_wide(np.full(n, d), 0.8, seed=s) for s in range(S)])
 din = torch.from_numpy(states.view(np.int64).copy()).cuda()
 outs = {}
-for impl in (2, 3):
+for impl in (2, 3, 4):
     dout = torch.zeros_like(din)
     for _ in range(3):
         ctx.batch_pass_eval(impl, S, din, dout)
@@ -34,10 +34,10 @@ for impl in (2, 3):
     tests = n * d * (n - 1) * 0.8 * S  # (x,a,y,state) support tests of one full pass
     flops = 2.0 * n * d * n * 128 * S  # the dense MMA work of impl 3 (every column, K = 128)
     med = float(np.median(ms))
-    print(json.dumps({"impl": impl, "name": "bit-sliced" if impl == 2 else "tcgen05", "n": n, "d": d, "S": S,
+    print(json.dumps({"impl": impl, "name": {2: "bit-sliced", 3: "tcgen05 f16", 4: "tcgen05 fp8"}[impl], "n": n, "d": d, "S": S,
                       "ms": round(med, 4), "T_tests_per_s": round(tests / med / 1e9, 3),
                       "mma_TFLOPs_if_tc": round(flops / med / 1e9, 1)}), flush=True)
-print(json.dumps({"same_result": bool(np.array_equal(outs[2], outs[3]))}))
+print(json.dumps({"same_result": bool(np.array_equal(outs[2], outs[3]) and np.array_equal(outs[2], outs[4]))}))
 # the product batched enforcement on the same states (wide_state, one block per
 # state, every pass to each state's own fixpoint), for scale
 dout = torch.zeros_like(din)
