@@ -70,6 +70,10 @@ WORKLOADS = {
     "w256-stream": (1000, 256, 1.0, 0.5, 1, "root",
                     "NEXT-4 wide domains: n=1000, d=256 (4 words per variable), density 1.0, tightness 0.5; root "
                     "enforcement (1 pass over 8.19 GB of 32-byte masks)"),
+    "w128-batch": (200, 128, 0.8, 0.95, 1, "wrand",
+                   "NEXT-4 wide batched: 1024 W-rand states (keep 0.8) on n=200, d=128, density 0.8, tightness "
+                   "0.95; one batched enforcement per step (tensor-core passes: tcgen05 over every column, "
+                   "per-state loop control)"),
     "c5-batch": (200, 16, 0.8, 0.3, 1, "dive",
                  "C5: 1024 W-dive states (search-tree nodes) on n=200, d=16, density 0.8, tightness 0.3; "
                  "one batched seeded enforcement per step (each state seeded with its assigned variable)"),
@@ -215,17 +219,20 @@ def run_gpu(args, rank, world, local_rank):
         seed_vars = np.array([sx], dtype=np.int32)
     else:
         d_in = full
-    S = args.states if kind == "dive" else 1
+    batched = kind in ("dive", "wrand")
+    S = args.states if batched else 1
     if kind == "dive":
         st, root, _ = ctx.enforce(full)
         states, svars = synth.dive_states(root, lambda D: ctx.enforce(D)[:2], S, seed=seed, return_seeds=True)
         din_h = np.stack(states)
         seed_vars = np.asarray(svars, dtype=np.int32)
+    elif kind == "wrand":
+        din_h = wrand_states(n, d, S)
     else:
         din_h = d_in[None, :]
 
     # --- instrumentation run (outside the timed region): iterations, status, live rows per pass
-    if kind == "dive":
+    if batched:
         res = [ctx.enforce(din_h[s], removed_at=True) for s in range(S)]
         iters_list = [r[2] for r in res]
         instr = {"iterations_mean": float(np.mean(iters_list)), "iterations_max": int(np.max(iters_list)),
@@ -239,9 +246,12 @@ def run_gpu(args, rank, world, local_rank):
         alg_tests = 0
         for s_i, r in enumerate(res):
             remd = r[3][:, :d]
-            live0 = np.array([[(int(din_h[s_i][x]) >> a) & 1 for a in range(d)] for x in range(n)], dtype=bool)
+            live0 = _live_bits(din_h[s_i], n, d)
             chg = np.zeros(n, dtype=bool)
-            chg[seed_vars[s_i]] = True
+            if seed_vars is not None:
+                chg[seed_vars[s_i]] = True
+            else:
+                chg[:] = True
             for t in range(1, r[2] + 1):
                 lv = (live0 & ((remd == 0) | (remd >= t))).sum(axis=1)
                 nb = np.zeros(n, dtype=np.int64)
@@ -302,6 +312,8 @@ def run_gpu(args, rank, world, local_rank):
         st = st if st is not None else stream
         if kind == "dive":
             ctx.enforce_batch_seeded(S, din, dout, its, sts, sv, stream=st)
+        elif kind == "wrand":
+            ctx.enforce_batch(S, din, dout, its, sts, stream=st)
         elif kind == "seed":
             ctx.enforce_seeded_async(din, dout, its, sts, sv, 1, stream=st)
         else:
@@ -319,7 +331,8 @@ def run_gpu(args, rank, world, local_rank):
     # graph's results are checked against the eager ones.  Multi-GPU paths (and
     # any path whose capture fails) run eagerly.
     graph, G, launch_mode = None, 1, "eager"
-    if world == 1 and ctx.path not in ("sharded", "peer") and os.environ.get("RAC_BENCH_GRAPH", "1") == "1":
+    if world == 1 and ctx.path not in ("sharded", "peer") and kind != "wrand" and \
+            os.environ.get("RAC_BENCH_GRAPH", "1") == "1":  # the wide tensor-core batch reads a flag per pass
         G = max(g for g in range(1, min(args.steps, 50) + 1) if args.steps % g == 0)
         try:
             cs = torch.cuda.Stream()
@@ -387,7 +400,7 @@ def run_gpu(args, rank, world, local_rank):
 
     # --- e2e: the public host-buffer call, H2D + D2H inside the timed region
     e2e = None
-    if kind != "dive":
+    if not batched:
         host_call = (lambda: ctx.enforce_seeded(din_h[0], seed_vars)) if kind == "seed" else \
             (lambda: ctx.enforce(din_h[0]))
         for _ in range(3):
@@ -429,15 +442,16 @@ def run_gpu(args, rank, world, local_rank):
             h_st.copy_(sts, non_blocking=True)
             torch.cuda.synchronize()
         wall_ms = (time.perf_counter() - t_wall) * 1e3
-        e2e = {"value": reps * S / (wall_ms / 1e3), "unit": "states/s", "h2d_bytes_per_step": S * n * 8,
-               "d2h_bytes_per_step": S * n * 8 + S * 4,
+        e2e = {"value": reps * S / (wall_ms / 1e3), "unit": "states/s", "h2d_bytes_per_step": int(din_h.nbytes),
+               "d2h_bytes_per_step": int(din_h.nbytes) + S * 4,
                "how": "pinned host states -> device, rac_enforce_batch, D_out + status -> pinned host, sync"}
 
     ms_per_step = total_ms / args.steps
-    if kind == "dive":
+    if batched:
         value = S * args.steps / (total_ms / 1e3)
         unit = "states/s"
-        metric = "AC enforcements/sec (batched search-tree states)"
+        metric = "AC enforcements/sec (batched search-tree states)" if kind == "dive" else \
+            "AC enforcements/sec (batched states)"
     else:
         value = args.steps / (total_ms / 1e3)
         unit = UNIT
@@ -446,6 +460,27 @@ def run_gpu(args, rank, world, local_rank):
     peak, peak_src = measured_peaks()
     roofline = None
     l2_roof = None
+    if kind == "wrand":
+        # Wide tensor-core batch: every pass is a dense tcgen05 contraction of
+        # ALL states against every column (K = 128 per column, f16 0/1 operands,
+        # fp32 counts): 2 x rows x n x 128 x S_pad FLOPs per pass, for as many
+        # passes as the slowest state runs.  Peak: the measured dense bf16 cuBLAS
+        # figure (f16 runs at the same rate), MEASURED_PEAKS.json.
+        kern_ms = statistics.median(per_step)
+        s_pad = (S + 255) // 256 * 256
+        passes = int(instr["iterations_max"])
+        flops = 2.0 * n * d * n * 128 * s_pad * passes
+        ach_tf = flops / (kern_ms / 1e3) / 1e12
+        try:
+            pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            peak_tf, src = float(pk["bf16_tflops"]), "measured dense bf16 cuBLAS (MEASURED_PEAKS.json bf16_tflops, burst)"
+        except Exception:
+            peak_tf, src = 1590.0, "fallback (B200_PROFILING.md)"
+        roofline = {"bound": "tensor", "achieved": round(ach_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": round(ach_tf / peak_tf, 4), "traffic": None, "kernel": "wide_tc_pass (+ wide_tc_update)",
+                    "flops_per_launch": flops, "passes": passes, "launch_ms_median": round(kern_ms, 5),
+                    "algorithmic_tests_per_launch": instr["support_tests"],
+                    "tests_per_s": round(instr["support_tests"] / (kern_ms / 1e3), 1), "peak_source": src}
     if kind == "dive":
         # Bit-sliced batched pass (rac_batch_bs): a support test of (x,a) against
         # c_xy for 32 states is ceil(d/4) nibble-table lookups in shared memory;
@@ -553,9 +588,18 @@ def workload_config(args):
     """The workload-defining keys only (identical in the GPU arm and the reference arm)."""
     n, d, dens, tight, seed, kind, desc = WORKLOADS[args.workload]
     return {"workload": args.workload + ": " + desc, "n": n, "d": d, "density": dens, "tightness": tight,
-            "t_q16": synth.quant_tightness(tight), "seed": seed, "states": args.states if kind == "dive" else 1,
+            "t_q16": synth.quant_tightness(tight), "seed": seed,
+            "states": args.states if kind in ("dive", "wrand") else 1,
             "l2": "relation L2-resident (warm; stated, not flushed)" if args.workload in L2_RESIDENT else
                   "inputs larger than L2 (no flush)"}
+
+
+def wrand_states(n, d, S):
+    """S W-rand states (value kept with probability 0.8, seed 1000 + s)."""
+    dom = np.full(n, d)
+    if d > 64:
+        return np.stack([synth.w_rand_wide(dom, 0.8, seed=1000 + s) for s in range(S)])
+    return np.stack([synth.w_rand(dom, 0.8, seed=1000 + s) for s in range(S)])
 
 
 def measure_l2_read_gbs(nbytes, dev):
@@ -592,6 +636,21 @@ def oracle_baseline(n, d, dq, tq, seed, kind, din_h, budget_s=20.0, passes=None)
     """The oracle as it stands (single-threaded C, oracle/oracle.c) on a bounded
     sample of the same workload, on this host."""
     import oracle
+    if d > 64 and kind == "wrand":
+        # wide batched states: O1w per state, one core, bounded
+        t0 = time.time()
+        orc = oracle.WideOracle.from_synth(n, d, dq, tq, seed)
+        build_s = time.time() - t0
+        done, t1 = 0, time.perf_counter()
+        while True:
+            orc.rac(din_h[done % din_h.shape[0]], with_epochs=False)
+            done += 1
+            el = time.perf_counter() - t1
+            if el > budget_s or done >= din_h.shape[0]:
+                break
+        return {"value": done / el, "unit": "states/s", "cores": 1, "kind": "oracle",
+                "sample": "%d state(s) of the batch by orc_rac_wide (O1w, 1 thread) in %.1f s; oracle instance "
+                          "build %.1f s excluded" % (done, el, build_s)}
     if d > 64:
         # Wide domains (NEXT-4): the oracle's build is O(n^2 d^2) generator calls,
         # so time one Eq. 1 step over the rows of a block of B variables (O1w's
@@ -695,6 +754,16 @@ def run_reference(args):
     n, d, dens, tight, seed, kind, desc = WORKLOADS[args.workload]
     dq, tq = synth.quant_density(dens), synth.quant_tightness(tight)
     import oracle
+    if d > 64 and kind == "wrand":
+        din_h = wrand_states(n, d, args.states)
+        cb = oracle_baseline(n, d, dq, tq, seed, kind, din_h, budget_s=min(120.0, 10.0 * max(1, args.steps)))
+        val = cb["value"]
+        return {"metric": "AC enforcements/sec (batched states)", "value": val, "unit": "states/s", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": args.states / val * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64 bitsets",
+                "data": "synthetic (seeded counter-based random CSP, synth/csp_synth.h)",
+                "config": workload_config(args), "impl": "reference", "cpu_baseline": cb,
+                "e2e": {"value": val, "unit": "states/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     if d > 64:
         # Wide domains: the oracle instance is O(n^2 d^2) to build; each step is the
         # block-sampled O1w estimate of one enforcement (see oracle_baseline).

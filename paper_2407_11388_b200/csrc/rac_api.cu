@@ -120,6 +120,8 @@ struct rac_ctx {
   unsigned long long* dbg = nullptr;  // RAC_DEBUG_TIMELINE phase timestamps [256]
   unsigned long long* bs_dbg = nullptr;  // bit-sliced batch: [ctas][64] pass-end timestamps
   uint32_t* eval_buf = nullptr;          // rac_batch_pass_eval scratch
+  uint8_t* tc_buf = nullptr;             // wide tensor-core batch scratch
+  size_t tc_cap = 0;
   size_t eval_cap = 0;
   int bs_dbg_ctas = 0;
   uint64_t* h_in = nullptr;        // pinned staging: [d_in words | seeds (seed_cap int32)]
@@ -258,6 +260,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->dbg);
   cudaFree(c->bs_dbg);
   cudaFree(c->eval_buf);
+  cudaFree(c->tc_buf);
   cudaFree(c->wD);
   cudaFree(c->wR);
   cudaFree(c->wslots);
@@ -1300,6 +1303,54 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
                       int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev, uint32_t flags,
                       void* stream);
 
+// Batched enforcement on wide domains (d <= 128) with the tensor-core pass:
+// every pass is ONE dense contraction of all states against every column
+// (wide_tc_pass, the winner of the A/B in DESIGN.md section 8), followed by
+// per-state loop control (wide_tc_update: wipeout first, then changed; a
+// stopped state is frozen).  Testing every column in every pass is a superset
+// of Alg. 1's @changed columns, so seeded states (under rac_enforce_seeded's
+// precondition) and root states get their exact results (Prop. 2, reading
+// R12).  The host reads the count of running states once per pass.
+static int wide_tc_enforce(rac_ctx* c, int32_t S, const uint64_t* d_in, uint64_t* d_out, int32_t* iters,
+                           int32_t* status, uint32_t flags, cudaStream_t st) {
+  CK(c, ensure_device(c));
+  const size_t nw = (size_t)c->n * c->wq;
+  const int rows = c->n * c->dmax, rows4 = (rows + 3) & ~3, NW = (S + 31) / 32;
+  const size_t need = (size_t)S * nw * 8 + (size_t)NW * rows4 * 4 * 2 + (size_t)S * 4 + 16;
+  if (need > c->tc_cap) {
+    cudaFree(c->tc_buf);
+    c->tc_buf = nullptr;
+    CK(c, cudaMalloc(&c->tc_buf, need));
+    c->tc_cap = need;
+  }
+  uint8_t* b = c->tc_buf;
+  uint64_t* Dn = reinterpret_cast<uint64_t*>(b);
+  uint32_t* X = reinterpret_cast<uint32_t*>(b + (size_t)S * nw * 8);
+  int32_t* active = reinterpret_cast<int32_t*>(X + (size_t)NW * rows4 * 2);
+  int32_t* n_active = active + S;
+  const char* f8e = getenv("RAC_WIDE_TC");  // A/B knob (tooling only): "f16" | "fp8"
+  const int impl = (f8e && strcmp(f8e, "fp8") == 0) ? 4 : 3;
+  CK(c, launch_wide_mask_copy(d_in, c->dom_d, S, c->n, c->wq, d_out, st));  // d_out holds D_{t-1}
+  CK(c, cudaMemsetAsync(iters, 0, (size_t)S * 4, st));
+  CK(c, cudaMemsetAsync(status, 0, (size_t)S * 4, st));
+  CK(c, launch_fill_i32(active, 1, S, st));
+  c->launches += 2;
+  const long max_passes = (long)c->n * c->dmax + 2;
+  for (long t = 1; t <= max_passes; ++t) {
+    WideTcParams w{reinterpret_cast<const uint64_t*>(c->M), c->P, c->pw, c->dom_d, c->n, c->dmax, c->wq, c->WS, S,
+                   d_out, Dn, X, X + (size_t)NW * rows4, rows4, NW};
+    CK(c, launch_wide_pass_eval(impl, w, st));
+    CK(c, cudaMemsetAsync(n_active, 0, 4, st));
+    CK(c, launch_wide_tc_update(c->dom_d, c->n, c->wq, (flags & RAC_FULL_FIXPOINT) ? 1 : 0, d_out, Dn, active, iters,
+                                status, n_active, S, st));
+    c->launches += 3;
+    CK(c, cudaMemcpyAsync(c->h_scalars + 3, n_active, 4, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    if (c->h_scalars[3] == 0) return 0;
+  }
+  return fail(c, RAC_ECUDA, "wide tensor-core batch did not converge (internal error)");
+}
+
 int rac_enforce_batch_seeded(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                              int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev,
                              uint32_t flags, void* stream) {
@@ -1321,9 +1372,14 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     return fail(c, RAC_EINVAL, "bad batch arguments");
   if (flags & ~RAC_FULL_FIXPOINT) return fail(c, RAC_EINVAL, "unknown flags");
   if (c->wide) {
-    // wide domains (NEXT-4): one block per state (wide_state)
+    // wide domains (NEXT-4)
     c->launches = 0;
     if (n_states == 0) return 0;
+    const char* wb = getenv("RAC_WIDE_BATCH");  // A/B knob (tooling only): "state" | "tc"
+    const bool want_tc = wb ? strcmp(wb, "tc") == 0 : (c->dmax <= 128 && n_states >= 256);
+    if (want_tc && c->dmax <= 128) return wide_tc_enforce(c, n_states, d_in_dev, d_out_dev, iterations_dev,
+                                                          status_dev, flags, (cudaStream_t)stream);
+    // one block per state (wide_state)
     if (wide_state_smem(c->n, c->WS) > 200 * 1024)
       return fail(c, RAC_EUNSUPPORTED, "wide batched mode: n too large for the per-state shared memory");
     CK(c, ensure_device(c));

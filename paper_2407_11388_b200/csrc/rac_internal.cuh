@@ -384,6 +384,12 @@ struct WideTcParams {
   int rows4, NW;
 };
 cudaError_t launch_wide_pass_eval(int impl, const WideTcParams& p, cudaStream_t st);
+cudaError_t launch_fill_i32(int32_t* p, int32_t v, int n, cudaStream_t st);
+cudaError_t launch_wide_mask_copy(const uint64_t* d_in, const int32_t* dom, int S, int n, int wq, uint64_t* Dc,
+                                  cudaStream_t st);
+cudaError_t launch_wide_tc_update(const int32_t* dom, int n, int wq, int full, uint64_t* Dc, const uint64_t* Dn,
+                                  int32_t* active, int32_t* iters, int32_t* status, int32_t* n_active, int S,
+                                  cudaStream_t st);
 size_t wide_state_smem(int n, int WS);
 cudaError_t launch_wide_state(const WideStateParams& p, int n_states, cudaStream_t s);
 cudaError_t wide_fused_grid(int WS, size_t smem, int sm_count, int* grid);

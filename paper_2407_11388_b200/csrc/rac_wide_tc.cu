@@ -148,41 +148,38 @@ __device__ __forceinline__ uint4 f16x8(uint32_t bits) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// 128 bits (2 words) -> row i of an operand tile, all 8 K-slabs; the 8 f16 of
-// each byte come from a 256-entry table in shared memory (one 16-byte load
-// instead of ~16 ALU instructions)
-__device__ __forceinline__ void put_row(uint8_t* base, int slab_bytes, int i, uint64_t lo, uint64_t hi,
-                                        const uint4* lut) {
+// 128 bits (2 words) -> row i of an operand tile, all 8 K-slabs (f16).  (A
+// 256-entry shared-memory table of the 8 f16 of each byte was slower: random
+// 16-byte lookups conflict on the banks -- profiles/r02n, 3.06 -> 4.09 ms.)
+__device__ __forceinline__ void put_row(uint8_t* base, int slab_bytes, int i, uint64_t lo, uint64_t hi) {
   uint8_t* p = base + (i >> 3) * kSBO + (i & 7) * 16;
 #pragma unroll
   for (int sl = 0; sl < kK / 16; ++sl) {
     const uint64_t word = sl < 4 ? lo : hi;
     const uint32_t bits16 = (uint32_t)(word >> (16 * (sl & 3))) & 0xFFFFu;
-    *reinterpret_cast<uint4*>(p + sl * slab_bytes) = lut[bits16 & 0xFFu];
-    *reinterpret_cast<uint4*>(p + sl * slab_bytes + kLBO) = lut[bits16 >> 8];
+    *reinterpret_cast<uint4*>(p + sl * slab_bytes) = f16x8(bits16 & 0xFFu);
+    *reinterpret_cast<uint4*>(p + sl * slab_bytes + kLBO) = f16x8(bits16 >> 8);
   }
 }
 
-// fp8 (e4m3, 1.0 = 0x38): 128 bits -> row i, 4 K-slabs of 32 elements, each two
-// 16-element chunks; byte -> 8 fp8 from a 256-entry u64 table
-__device__ __forceinline__ void put_row8(uint8_t* base, int slab_bytes, int i, uint64_t lo, uint64_t hi,
-                                         const unsigned long long* lut8) {
+// 8 bits -> 8 fp8 e4m3 (0 or 1.0 = 0x38) with a few 64-bit ALU operations:
+// replicate the byte, keep bit j in byte j, turn each non-zero byte into 0x01,
+// scale to 0x38 (no carries: 0x38 < 0x100)
+__device__ __forceinline__ unsigned long long fp8x8(uint32_t bits) {
+  unsigned long long t = ((unsigned long long)(bits & 255u) * 0x0101010101010101ull) & 0x8040201008040201ull;
+  t = (((t + 0x7F7F7F7F7F7F7F7Full) | t) >> 7) & 0x0101010101010101ull;
+  return t * 0x38ull;
+}
+
+// fp8: 128 bits -> row i, 4 K-slabs of 32 elements, each two 16-element chunks
+__device__ __forceinline__ void put_row8(uint8_t* base, int slab_bytes, int i, uint64_t lo, uint64_t hi) {
   uint8_t* p = base + (i >> 3) * kSBO + (i & 7) * 16;
 #pragma unroll
   for (int sl = 0; sl < kK / 32; ++sl) {
     const uint32_t b32 = (uint32_t)((sl < 2 ? lo : hi) >> (32 * (sl & 1)));
-    *reinterpret_cast<ulonglong2*>(p + sl * slab_bytes) = make_ulonglong2(lut8[b32 & 255u], lut8[(b32 >> 8) & 255u]);
-    *reinterpret_cast<ulonglong2*>(p + sl * slab_bytes + kLBO) =
-        make_ulonglong2(lut8[(b32 >> 16) & 255u], lut8[b32 >> 24]);
+    *reinterpret_cast<ulonglong2*>(p + sl * slab_bytes) = make_ulonglong2(fp8x8(b32), fp8x8(b32 >> 8));
+    *reinterpret_cast<ulonglong2*>(p + sl * slab_bytes + kLBO) = make_ulonglong2(fp8x8(b32 >> 16), fp8x8(b32 >> 24));
   }
-}
-
-__device__ __forceinline__ unsigned long long fp8x8(uint32_t bits) {
-  unsigned long long v = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    if ((bits >> j) & 1u) v |= 0x38ull << (8 * j);
-  return v;
 }
 
 __device__ __forceinline__ void mbar_init1(uint64_t* mb, unsigned cnt) {
@@ -215,8 +212,6 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
   extern __shared__ __align__(1024) uint8_t tsm[];
   __shared__ alignas(8) uint64_t full_bar[2], done_bar[2], free_bar[2];
   __shared__ uint32_t tmem_base_s;
-  __shared__ uint4 lut[256];                // byte -> 8 f16 (0 or 1.0)
-  __shared__ unsigned long long lut8[256];  // byte -> 8 fp8 e4m3 (0 or 1.0)
   const int tid = threadIdx.x, warp = tid >> 5;
   const int rows = p.n * p.dmax;
   const int row0 = blockIdx.x * kTM;
@@ -236,10 +231,6 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  for (int v = tid; v < 256; v += blockDim.x) {
-    if (F8) lut8[v] = fp8x8((uint32_t)v);
-    else lut[v] = f16x8((uint32_t)v);
-  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -258,8 +249,8 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
         lo = __ldg(mp);
         hi = __ldg(mp + 1);
       }
-      if constexpr (F8) put_row8(sA[st], kSlabA, i, lo, hi, lut8);
-      else put_row(sA[st], kSlabA, i, lo, hi, lut);
+      if constexpr (F8) put_row8(sA[st], kSlabA, i, lo, hi);
+      else put_row(sA[st], kSlabA, i, lo, hi);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int s = s0 + 2 * i + h;
@@ -271,8 +262,8 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
           a = __ldg(dp);
           b = p.wq > 1 ? __ldg(dp + 1) : 0ull;
         }
-        if constexpr (F8) put_row8(sB[st], kSlabB, 2 * i + h, a, b, lut8);
-        else put_row(sB[st], kSlabB, 2 * i + h, a, b, lut);
+        if constexpr (F8) put_row8(sB[st], kSlabB, 2 * i + h, a, b);
+        else put_row(sB[st], kSlabB, 2 * i + h, a, b);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core
       mbar_arrive1(&full_bar[st]);
@@ -352,6 +343,79 @@ __global__ void __launch_bounds__(288, 1) wide_tc_pass(WideTcParams p) {
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------- batched enforcement
+// Per-state loop control after one tensor-core pass (Alg. 1):
+// Dn = D_t of every state (the pass ran on all of them), Dc = D_{t-1}.  An
+// active state counts the pass; wipeout is checked first, then "changed"; a
+// state that stops keeps D_t (its result) and is frozen; an active one that
+// continues adopts D_t.  One block per state; *n_active counts the states still
+// running (the host reads it once per pass).
+__global__ void __launch_bounds__(256) wide_tc_update(const int32_t* dom, int n, int wq, int full, uint64_t* Dc,
+                                                      const uint64_t* Dn, int32_t* active, int32_t* iters,
+                                                      int32_t* status, int32_t* n_active) {
+  const int s = blockIdx.x;
+  if (!active[s]) return;  // block-uniform
+  const size_t base = (size_t)s * n * wq;
+  int changed = 0, empty = 0;
+  for (int x = threadIdx.x; x < n; x += blockDim.x) {
+    uint64_t any = 0;
+    for (int k = 0; k < wq; ++k) {
+      const uint64_t a = Dc[base + (size_t)x * wq + k], b = Dn[base + (size_t)x * wq + k];
+      changed |= a != b;
+      any |= b;
+    }
+    empty |= any == 0ull;
+  }
+  changed = __syncthreads_or(changed);
+  empty = __syncthreads_or(empty);
+  for (int i = threadIdx.x; i < n * wq; i += blockDim.x) Dc[base + i] = Dn[base + i];  // D_t (result or next input)
+  if (threadIdx.x == 0) {
+    iters[s] += 1;
+    if (empty && !full) {
+      status[s] = 1;  // RAC_WIPEOUT, Alg. 1
+      active[s] = 0;
+    } else if (!changed) {
+      status[s] = empty ? 1 : 0;  // Prop. 1 end condition
+      active[s] = 0;
+    } else {
+      atomicAdd(n_active, 1);
+    }
+  }
+}
+
+// Dc = d_in with the bits beyond each domain cleared (every state)
+__global__ void wide_mask_copy(const uint64_t* d_in, const int32_t* dom, int S, int n, int wq, uint64_t* Dc) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long)S * n * wq) return;
+  const int k = (int)(i % wq), x = (int)((i / wq) % n);
+  const int bits = min(64, max(0, dom[x] - 64 * k));
+  Dc[i] = d_in[i] & (bits >= 64 ? ~0ull : ((1ull << bits) - 1ull));
+}
+
+cudaError_t launch_wide_mask_copy(const uint64_t* d_in, const int32_t* dom, int S, int n, int wq, uint64_t* Dc,
+                                  cudaStream_t st) {
+  const long tot = (long)S * n * wq;
+  wide_mask_copy<<<(int)((tot + 255) / 256), 256, 0, st>>>(d_in, dom, S, n, wq, Dc);
+  return cudaGetLastError();
+}
+
+__global__ void fill_i32(int32_t* p, int32_t v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+cudaError_t launch_fill_i32(int32_t* p, int32_t v, int n, cudaStream_t st) {
+  fill_i32<<<(n + 255) / 256, 256, 0, st>>>(p, v, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wide_tc_update(const int32_t* dom, int n, int wq, int full, uint64_t* Dc, const uint64_t* Dn,
+                                  int32_t* active, int32_t* iters, int32_t* status, int32_t* n_active, int S,
+                                  cudaStream_t st) {
+  wide_tc_update<<<S, 256, 0, st>>>(dom, n, wq, full, Dc, Dn, active, iters, status, n_active);
+  return cudaGetLastError();
 }
 
 size_t wide_tc_smem(bool f8) { return (size_t)2 * (f8 ? stageA<true>() + stageB<true>() : kStageA + kStageB); }
