@@ -72,7 +72,7 @@ WORKLOADS = {
                     "enforcement (1 pass over 8.19 GB of 32-byte masks)"),
     "w128-batch": (200, 128, 0.8, 0.95, 1, "wrand",
                    "NEXT-4 wide batched: 1024 W-rand states (keep 0.8) on n=200, d=128, density 0.8, tightness "
-                   "0.95; one batched enforcement per step (tensor-core passes: tcgen05 over every column, "
+                   "0.95; one batched enforcement per step (tensor-core passes: tcgen05 fp8 over every column, "
                    "per-state loop control)"),
     "c5-batch": (200, 16, 0.8, 0.3, 1, "dive",
                  "C5: 1024 W-dive states (search-tree nodes) on n=200, d=16, density 0.8, tightness 0.3; "
@@ -462,20 +462,23 @@ def run_gpu(args, rank, world, local_rank):
     l2_roof = None
     if kind == "wrand":
         # Wide tensor-core batch: every pass is a dense tcgen05 contraction of
-        # ALL states against every column (K = 128 per column, f16 0/1 operands,
-        # fp32 counts): 2 x rows x n x 128 x S_pad FLOPs per pass, for as many
-        # passes as the slowest state runs.  Peak: the measured dense bf16 cuBLAS
-        # figure (f16 runs at the same rate), MEASURED_PEAKS.json.
+        # ALL states against every column (K = 128 per column, fp8 e4m3 0/1
+        # operands by default, fp32 counts): 2 x rows x n x 128 x S_pad FLOPs per
+        # pass, for as many passes as the slowest state runs.  Peak: the measured
+        # dense bf16 cuBLAS figure x 2 for fp8 (x 1 for f16), MEASURED_PEAKS.json.
         kern_ms = statistics.median(per_step)
         s_pad = (S + 255) // 256 * 256
         passes = int(instr["iterations_max"])
         flops = 2.0 * n * d * n * 128 * s_pad * passes
         ach_tf = flops / (kern_ms / 1e3) / 1e12
+        f16 = os.environ.get("RAC_WIDE_TC") == "f16"  # fp8 e4m3 operands by default (librac)
         try:
             pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
             peak_tf, src = float(pk["bf16_tflops"]), "measured dense bf16 cuBLAS (MEASURED_PEAKS.json bf16_tflops, burst)"
         except Exception:
             peak_tf, src = 1590.0, "fallback (B200_PROFILING.md)"
+        if not f16:  # fp8: the measured bf16 figure x the nominal fp8 / bf16 ratio (4.5 / 2.25)
+            peak_tf, src = 2.0 * peak_tf, src + " x 2 (nominal dense fp8 / bf16 ratio, B200_PROFILING.md)"
         roofline = {"bound": "tensor", "achieved": round(ach_tf, 1), "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": round(ach_tf / peak_tf, 4), "traffic": None, "kernel": "wide_tc_pass (+ wide_tc_update)",
                     "flops_per_launch": flops, "passes": passes, "launch_ms_median": round(kern_ms, 5),
@@ -524,7 +527,7 @@ def run_gpu(args, rank, world, local_rank):
                 if traffic is not None:
                     traffic_src = "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum, one launch, " \
                                   "captured in session %s (profiles/ncu_traffic.json), not in this run" % \
-                                  ent.get("session", tj.get("session", "?"))
+                                  ent.get("round", "?")
             except Exception:
                 traffic = None
         full_b = instr.get("full_test_bytes")
