@@ -1453,7 +1453,14 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       b.RPC = RPC;
       b.flags = flags;
       const int NW = (n_states + 31) / 32;
-      CK(c, launch_batch_cl(c->W, b, std::min(NW, maxcl), C, threads, smem, st));
+      const int ncl = std::min(NW, maxcl);
+      if (getenv("RAC_DEBUG_TIMELINE")) {
+        if (!c->bs_dbg) CK(c, cudaMalloc(&c->bs_dbg, (size_t)4096 * 64 * 8));
+        CK(c, cudaMemsetAsync(c->bs_dbg, 0, (size_t)4096 * 64 * 8, st));
+        b.dbg = ncl <= 1024 ? c->bs_dbg : nullptr;
+        c->bs_dbg_ctas = ncl * 4;  // 256 stamps per cluster
+      }
+      CK(c, launch_batch_cl(c->W, b, ncl, C, threads, smem, st));
       c->launches++;
       return 0;
     }

@@ -137,9 +137,14 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   const int x0 = r0 / dmax, x1 = (r1 + dmax - 1) / dmax;  // my variables
   const bool full = (p.flags & kFullCL) != 0;
   const int NW = (p.S + 31) / 32;
+  // debug stamps: per word [start, staged, per pass: list, tables, sweep, A, B], end
+  int nd = 0;
+  const bool dbg = p.dbg != nullptr && k == 0 && tid == 0;
+#define CL_MARK() do { if (dbg && nd < 255) p.dbg[(size_t)g * 256 + nd++] = globaltimer(); } while (0)
 
   for (int w = g; w < NW; w += G) {
     const int s0 = 32 * w, nst = min(32, p.S - s0);
+    CL_MARK();
     // ---- the word's states -> bit slices (every CTA, all rows); seeds -> chg
     for (int x = warp; x < n; x += nwarps) {
       const uint64_t v = lane < nst ? __ldg(p.d_in + (size_t)(s0 + lane) * n + x) & __ldg(p.dommask + x) : 0ull;
@@ -192,6 +197,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       __syncthreads();
     }
     int t = 0;
+    CL_MARK();
     for (;;) {
       ++t;
       // ---- tested columns U = { y : chg[y] & active } (ascending, block scan)
@@ -207,6 +213,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         cnt = (int)total;
       }
       __syncthreads();
+      CL_MARK();
       // ---- per-column offsets (the list padded to a multiple of 8) and nibble tables
       const int cnt8 = (cnt + 7) & ~7;
       for (int c = tid; c < cnt8; c += T) {
@@ -228,10 +235,12 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         for (int v = 0; v < 16; v += 4) dst[v >> 2] = make_uint4(tv[v], tv[v + 1], tv[v + 2], tv[v + 3]);
       }
       __syncthreads();
+      CL_MARK();
       // ---- a3/a4: my rows against the tested columns, 32 states at a time
       uint32_t my_or = (~allne0 & active)
                                  ? sweep_rows<W, true>(p.M, p.P, p.pw, X, Tb, ci, cnt8, r0, r1, dmax, active, chgn)
                                  : sweep_rows<W, false>(p.M, p.P, p.pw, X, Tb, ci, cnt8, r0, r1, dmax, active, chgn);
+      CL_MARK();
       // this CTA's partials: lanes that changed; lanes with every variable non-empty
       uint32_t my_ne = 0xffffffffu;
       __syncthreads();
@@ -252,6 +261,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         if (my_ne != 0xffffffffu) atomicAnd(&s_part[1], my_ne);
       }
       cluster.sync();  // [A] every CTA's rows, change masks and partials are final
+      CL_MARK();
       // ---- exchange: change masks of every variable from its owner, the rows of
       // the variables that changed, and the partials
       uint32_t changed = 0u, allne = 0xffffffffu;
@@ -272,6 +282,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         if (owner != k) X[i] = *cluster.map_shared_rank(X + i, owner);
       }
       cluster.sync();  // [B] nobody rewrites its rows / chgn before the others read them
+      CL_MARK();
       for (int x = x0 + tid; x < x1; x += T) chgn[x] = 0u;
       // ---- per-state loop control (Alg. 1): wipeout first, then "changed"
       const uint32_t wipe = ~allne;
@@ -299,7 +310,9 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       p.status[s0 + tid] = s_status[tid];
     }
     cluster.sync();  // the next word reuses every CTA's shared memory
+    CL_MARK();
   }
+#undef CL_MARK
 }
 
 size_t batch_cl_smem(int n, int dmax, int W) {

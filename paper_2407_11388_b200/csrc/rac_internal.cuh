@@ -119,7 +119,7 @@ struct FusedParams {
   const int32_t* seeds;     // device [n_seeds]: Alg. 1 initial @changed (read only if n_seeds > 0)
   int n_seeds;              // < 0: root call (every column in pass 1); 0: no pass
   uint32_t flags;
-  uint32_t ab;              // A/B knobs (tooling, RAC_FUSED_AB): bit 0 legacy grid barrier, bit 1 listed apply
+  uint32_t ab;              // A/B knobs (tooling, RAC_FUSED_AB): bit 0 legacy grid barrier, bit 1 listed apply, bit 2 no removal-flag check before the R read
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
   // Global pass counter (persists across launches): pass t of this launch is
   // pass *seq + t; it selects the rotating buffers and is the cross-rank
@@ -215,6 +215,7 @@ struct BatchCLParams {
   int S;
   int RPC;                  // rows per CTA of a cluster (a multiple of dmax)
   uint32_t flags;
+  unsigned long long* dbg;  // nullable (RAC_DEBUG_TIMELINE): [clusters][256] %globaltimer stamps
 };
 size_t batch_cl_smem(int n, int dmax, int W);
 cudaError_t launch_batch_cl(int W, const BatchCLParams& p, int clusters, int C, int threads, size_t smem,

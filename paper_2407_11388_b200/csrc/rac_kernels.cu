@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
           vcnt = cnt;
           listed = true;
         }
-      } else if (__ldcg(p.rflag + b) == 0u) {
+      } else if (!(p.ab & 4u) && __ldcg(p.rflag + b) == 0u) {  // ab bit 2: read R unconditionally
         wipe = has_empty;
       } else if (p.ab & 2u) {
         // A/B variant (RAC_FUSED_AB bit 1; measured slightly slower than the

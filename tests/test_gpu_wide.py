@@ -289,19 +289,18 @@ def test_wide_nonuniform_domains_at_scale(rac):
             assert wo.certify_trajectory(d_in, g[1], g[3], g[2], g[0], full) == 0
 
 
-@pytest.mark.parametrize("impl", ["state", "tc", "tc-fp8"])
+@pytest.mark.parametrize("impl", ["state", "tc-f16", "tc-fp8"])
 def test_wide_batched(rac, impl, monkeypatch):
     """Batched enforcement on wide contexts -- one block per state (wide_state),
     and the tensor-core batch (every pass one dense tcgen05 contraction of all
-    states, f16 or fp8 operands, then per-state loop control; d <= 128, other
+    states, fp8 (default) or f16 operands, then per-state loop control; d <= 128, other
     instances fall back to wide_state): every state's (status, D_out,
     iterations) equals O1w on that state alone -- W-rand states in stop and full
     mode, and assigned states (x := a on the root D_ac) with their assigned
     variable as the per-state seed (Prop. 2)."""
     import torch
     monkeypatch.setenv("RAC_WIDE_BATCH", "state" if impl == "state" else "tc")
-    if impl == "tc-fp8":
-        monkeypatch.setenv("RAC_WIDE_TC", "fp8")
+    monkeypatch.setenv("RAC_WIDE_TC", "f16" if impl == "tc-f16" else "fp8")
     rng = np.random.default_rng(31)
     for k, inst in enumerate(_wide_corpus(10, 91)):
         ctx = rac.RacContext.from_instance(inst)
