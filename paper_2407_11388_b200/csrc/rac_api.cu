@@ -1212,20 +1212,35 @@ int rac_enforce_seeded_async(rac_ctx* c, const uint64_t* d_in_dev, uint64_t* d_o
                             (cudaStream_t)stream, seeds_dev, n_seeds);
 }
 
-// Enqueue the blocking API's H2D copy (d_in words + n_seeds seeds, already in
-// h_in) and the enforcement writing into the mapped output.  Small instances
-// (the one-warp / one-block kernels, where the launch cost is comparable to the
-// kernel) replay a cached CUDA graph of the two; everything else enqueues them.
+// Enqueue the blocking API's input and the enforcement writing into the mapped
+// output, as a cached CUDA graph (per seed count and flags; dropped when the
+// staging moves).  Small instances (the one-warp / one-block kernels, whose
+// launch cost is comparable to the kernel) read d_in and the seeds straight
+// from the pinned staging (zero-copy: no copy-engine transfer in the graph);
+// larger ones stage them with one H2D copy, since every CTA of the persistent
+// kernel reads d_in.
 static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags) {
   const size_t nw = (size_t)c->n * c->wq;
   int32_t* d_res = reinterpret_cast<int32_t*>(c->d_hout + nw);
-  const int32_t* seeds = n_seeds >= 0 ? c->buf_seeds : nullptr;
+  static const char* bg = getenv("RAC_BLOCKING_GRAPH");  // A/B knob (tooling only): "0" = no graph, "small"
+  const bool no_graph = bg && strcmp(bg, "0") == 0;
+  const bool small_only = bg && strcmp(bg, "small") == 0;
+  static const bool h2d_small = getenv("RAC_BLOCKING_H2D") != nullptr;  // A/B knob: small instances copy too
+  const bool zc = c->small && !c->peer && !c->wide && !h2d_small;
+  const uint64_t* din = zc ? c->h_in : c->buf_in;  // pinned host memory is device-accessible (UVA)
+  const int32_t* seeds =
+      n_seeds >= 0 ? (zc ? reinterpret_cast<const int32_t*>(reinterpret_cast<const uint8_t*>(c->h_in) + nb)
+                         : c->buf_seeds)
+                   : nullptr;
   const size_t bytes = nb + (size_t)std::max(0, n_seeds) * 4;
-  static const bool no_graph = getenv("RAC_NO_BLOCKING_GRAPH") != nullptr;  // A/B knob (tooling only)
-  if (!c->small || c->peer || c->wide || c->graphs_off || no_graph) {
-    CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream));
-    return enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
-  }
+  auto enqueue = [&]() -> int {
+    if (!zc) {
+      cudaError_t e = cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream);
+      if (e != cudaSuccess) return fail(c, RAC_ECUDA, std::string("cudaMemcpyAsync: ") + cudaGetErrorString(e));
+    }
+    return enforce_async_impl(c, din, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
+  };
+  if (c->peer || c->wide || c->graphs_off || no_graph || (small_only && !c->small)) return enqueue();
   const int64_t key = ((int64_t)n_seeds << 8) | (int64_t)flags;
   for (int i = 0; i < c->ngraphs; ++i)
     if (c->gkey[i] == key) {
@@ -1238,9 +1253,7 @@ static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags) 
   cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed);
   int rc = 0;
   if (e == cudaSuccess) {
-    e = cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream);
-    if (e == cudaSuccess)
-      rc = enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
+    rc = enqueue();
     cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
     if (e == cudaSuccess) e = e2;
   }
@@ -1251,8 +1264,7 @@ static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags) 
     cudaGetLastError();
     c->broken = false;
     c->graphs_off = true;
-    CK(c, cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream));
-    return enforce_async_impl(c, c->buf_in, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
+    return enqueue();
   }
   if (c->ngraphs == rac_ctx::kGraphs) {
     cudaGraphExecDestroy(c->graphs[0]);
@@ -1439,6 +1451,17 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       BatchCLParams b{};
       b.M = c->M;
       b.col_stride = c->col_stride;
+      b.Mr = c->Mr;
+      b.dbytes = c->dbytes;
+      // every column through the row-major copy when >= 4/5 of them are tested
+      // (A/B knob RAC_BATCH_FULL="num/den", "0" = column lists only)
+      b.full_num = 4;
+      b.full_den = 5;
+      if (const char* fe = getenv("RAC_BATCH_FULL")) {
+        int a = 0, d = 1;
+        if (sscanf(fe, "%d/%d", &a, &d) >= 1 && a > 0) { b.full_num = a; b.full_den = std::max(1, d); }
+        else b.Mr = nullptr;
+      }
       b.n = c->n;
       b.dmax = c->dmax;
       b.P = c->P;

@@ -2,33 +2,40 @@
 // per bit-sliced word, each word owned by ONE thread-block cluster.
 //
 // Many search-tree nodes (Alg. 2) on one instance.
-// As in rac_batch.cu the states are bit-sliced: for a word of 32 states,
-// X[(x,a)] is a u32 whose bit j says (x,a) ∈ D_j, and one pass of Eq. 1
-// (lines 89-99) for all 32 states is
-//   X'[(x,a)] = X[(x,a)] & AND_{y ∈ C_x} ( OR_{b ∈ c_xy|(x,a)} X[(y,b)] )
-// with the OR over b read from per-pass nibble tables
-//   T[y][q][v] = OR_{j : bit j of v} X[(y, 4q+j)]     (ceil(d/4) lookups per mask).
-// Per-state loop control (Alg. 1): wipeout first, then
-// "changed", each state frozen at its own pass.  The tested columns of a pass
-// are the union over the word's active states of the variables that changed
-// for them in the previous pass (the seed variable of a seeded state in pass 1;
-// Prop. 2, lines 130-143 -- testing a column that did not change for a state
-// re-passes, so the union is exact).
+// The states are bit-sliced: for a word of 32 states, X[(x,a)] is a u32 whose
+// bit j says (x,a) ∈ D_j, and one pass of Eq. 1 (lines 89-99) for all 32
+// states is
+//   X'[(x,a)] = X[(x,a)] & AND_{y tested} ( OR_{b ∈ c_xy|(x,a)} X[(y,b)]  |  ~tst[y] )
+// where tst[y] = the active states for which y changed in the previous pass
+// (the seed variable of a seeded state in pass 1, every variable of a root
+// state): Alg. 1's Cons[:, @changed] (line 215) per state, so every state
+// follows its own Alg. 1 trajectory exactly.  The OR over b comes from
+// per-column chunk tables in shared memory,
+//   T[y][q][v] = OR_{j : bit j of v} X[(y, shift_q + j)],
+// one lookup per chunk of the mask (W=2: chunks of 6+5+5 bits, 3 lookups per
+// mask; W=1: 2 nibbles; W=4: 8 nibbles).  A table is rebuilt only when its
+// column's rows changed.  Per-state loop control (Alg. 1):
+// wipeout first, then "changed", each state frozen at its own pass.
 //
-// What is different from rac_batch.cu (the r01 design measured at 0.68 ms per
-// C5 batch: 13 CTAs per word meeting at a global atomic barrier and exchanging
-// their rows through a global double buffer):
-//   * the word's CTAs form ONE cluster (C <= 8 CTAs, rows split between them);
-//     passes are separated by cluster barriers (barrier.cluster) and the new
-//     rows are exchanged through distributed shared memory -- no global
-//     barrier, no global exchange buffer;
-//   * every CTA keeps the whole word's slices in its shared memory and copies
-//     from the other CTAs only the rows of variables that changed;
-//   * a row takes one 16/W-byte... (column-major mask loads, 8 in flight per
-//     thread) and stops as soon as none of its live states is supported.
+// Cluster organisation: the word's CTAs form ONE cluster, each owning a block
+// of rows (whole variables) and keeping the whole word's slices X in shared
+// memory.  Per pass:
+//   prep   tst / the tested-column list (warp 0) and the tables of changed
+//          columns (the other warps); then a split cluster barrier ARRIVE
+//          ("I have read everybody's rows");
+//   sweep  my rows against the tested columns: either the column list
+//          (column-major masks, one 2/4-byte load per tested column) or, when
+//          most columns are tested, every column through the row-major copy
+//          (one 16-byte load per 16/W columns); a row stops as soon as none of
+//          its live states is supported;
+//   push   split barrier WAIT, then DSMEM stores of my changed rows, my change
+//          masks and my [changed, emptied] lanes into every CTA of the cluster;
+//   sync   one full cluster barrier; every CTA derives the same loop control.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <utility>
 
 #include "rac_internal.cuh"
 
@@ -40,6 +47,93 @@ namespace {
 
 constexpr uint32_t kFullCL = 1u;  // RAC_FULL_FIXPOINT
 constexpr int kMaxT = 1024;
+constexpr int kMaxC = 16;
+
+// Chunk tables per mask width W: chunk q covers values [shift(q), shift(q) +
+// bits(q)) of the mask; its table (2^bits(q) words) sits at byte off(q) of the
+// column's TSB-byte table block.  TSB exceeds every chunk's largest byte
+// offset, so (column base | entry offset) is an OR of disjoint bits.
+template <int W>
+struct Lut;
+template <>
+struct Lut<1> {
+  static constexpr int NCH = 2, TSB = 128, NI = 2;
+  __host__ __device__ static constexpr int bits(int) { return 4; }
+  __host__ __device__ static constexpr int shift(int q) { return 4 * q; }
+  __host__ __device__ static constexpr int off(int q) { return 64 * q; }
+};
+template <>
+struct Lut<2> {
+  static constexpr int NCH = 3, TSB = 512, NI = 8;
+  __host__ __device__ static constexpr int bits(int q) { return q == 0 ? 6 : 5; }
+  __host__ __device__ static constexpr int shift(int q) { return q == 0 ? 0 : (q == 1 ? 6 : 11); }
+  __host__ __device__ static constexpr int off(int q) { return q == 0 ? 0 : (q == 1 ? 256 : 384); }
+};
+template <>
+struct Lut<4> {
+  static constexpr int NCH = 8, TSB = 512, NI = 8;
+  __host__ __device__ static constexpr int bits(int) { return 4; }
+  __host__ __device__ static constexpr int shift(int q) { return 4 * q; }
+  __host__ __device__ static constexpr int off(int q) { return 64 * q; }
+};
+
+template <int IMM>
+__device__ __forceinline__ uint32_t lds_imm(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(IMM));
+  return v;
+}
+
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Byte offset of the table entry of chunk Q for the mask at bit SH of w.
+template <int W, int Q, int SH>
+__device__ __forceinline__ uint32_t lut_off(uint32_t w) {
+  constexpr int S = Lut<W>::shift(Q) + SH;
+  constexpr uint32_t MSK = ((1u << Lut<W>::bits(Q)) - 1u) << 2;
+  if constexpr (S >= 2) return (w >> (S - 2)) & MSK;
+  else return (w << (2 - S)) & MSK;
+}
+
+// OR over the mask's values of X[(y, b)]: one shared-memory lookup per chunk,
+// address (cb | entry offset) + IMM + off(q): cb = the shared-memory address of
+// a TSB-aligned table block, IMM = the column's block relative to cb.
+template <int W, int SH, int IMM, int Q = 0>
+__device__ __forceinline__ uint32_t sup_lookup(uint32_t w, uint32_t cb) {
+  const uint32_t s = lds_imm<IMM + Lut<W>::off(Q)>(cb | lut_off<W, Q, SH>(w));
+  if constexpr (Q + 1 < Lut<W>::NCH) return s | sup_lookup<W, SH, IMM, Q + 1>(w, cb);
+  else return s;
+}
+
+// Table item i of column y: chunk q, block bi of 16 entries.
+template <int W>
+__device__ __forceinline__ void build_item(uint8_t* Tb, const uint32_t* X, int y, int i, int dmax) {
+  int q = 0, bi = i;
+  while (bi >= (1 << (Lut<W>::bits(q) - 4))) {
+    bi -= 1 << (Lut<W>::bits(q) - 4);
+    ++q;
+  }
+  const int b0 = Lut<W>::shift(q), nb = Lut<W>::bits(q);
+  const uint32_t* Xy = X + (size_t)y * dmax;
+  uint32_t xb[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) xb[j] = b0 + j < dmax ? Xy[b0 + j] : 0u;
+  uint32_t hi = 0u;
+  for (int k = 0; k < nb - 4; ++k)
+    if (((bi >> k) & 1) && b0 + 4 + k < dmax) hi |= Xy[b0 + 4 + k];
+  uint32_t tv[16];
+  tv[0] = hi;
+#pragma unroll
+  for (int v = 1; v < 16; ++v) tv[v] = tv[v & (v - 1)] | xb[__ffs(v) - 1];
+  uint4* dst = reinterpret_cast<uint4*>(Tb + (size_t)y * Lut<W>::TSB + Lut<W>::off(q) + bi * 64);
+#pragma unroll
+  for (int v = 0; v < 16; v += 4) dst[v >> 2] = make_uint4(tv[v], tv[v + 1], tv[v + 2], tv[v + 3]);
+}
 
 template <int W>
 __device__ __forceinline__ uint32_t mask_at(const uint8_t* p) {
@@ -48,29 +142,29 @@ __device__ __forceinline__ uint32_t mask_at(const uint8_t* p) {
   else return __ldg(p);
 }
 
-// The support test of my rows against the pass's tested columns.  ci[c] =
-// {byte offset of column c's masks, word offset of its nibble tables}; the
-// list is padded to a multiple of 8 with copies of its last column (a column
-// tested twice gives the same answer), so the 8-wide inner loop has no bounds
-// checks.  CP: some active state has an empty domain (pass 1 of an input with
-// an empty row, or full mode), so an all-ones mask of an absent pair could
-// "fail" and the presence bit must decide (reading R2); otherwise no absent
-// pair can fail and the presence test is skipped.
-__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
-  uint32_t v;
-  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
+// Presence (R2): an absent pair's mask is all ones, so it can only "fail" for
+// a state whose D(y) is empty; such a lane is kept by the presence bit.
+__device__ __forceinline__ bool present(const uint32_t* P, int pw, int x, int y) {
+  return (__ldg(P + (size_t)x * pw + (y >> 5)) >> (y & 31)) & 1u;
 }
 
+// One column's test: acc &= sup | ~t (t = lanes that test this column).
+template <bool CP>
+__device__ __forceinline__ void apply_col(uint32_t& acc, uint32_t s, uint32_t t, uint32_t live, const uint32_t* P,
+                                          int pw, int x, int y) {
+  if constexpr (CP) {
+    if ((s & live & t) != (live & t) && !present(P, pw, x, y)) s = 0xffffffffu;
+  }
+  acc &= s | ~t;
+}
+
+// Listed columns: ci[c] = {byte offset of column c's masks, byte offset of its
+// table block}, ctst[c] = the lanes that test it; the list is padded to a
+// multiple of 8 with entries that test no lane.
 template <int W, bool CP>
-__device__ __forceinline__ uint32_t sweep_rows(const uint8_t* __restrict__ M, const uint32_t* __restrict__ P, int pw,
-                                               uint32_t* X, const uint32_t* Tb, const uint2* ci, int cnt8, int r0,
-                                               int r1, int dmax, uint32_t active, uint32_t* chgn) {
-  constexpr int NQ = 2 * W;
-  // nibble tables addressed with 32-bit shared-memory addresses: ci[c].y is the
-  // byte offset of column c's tables, the nibble q of the mask selects the
-  // word (v << 2) of its 16-entry table at byte q * 64
-  const uint32_t tb0 = (uint32_t)__cvta_generic_to_shared(Tb);
+__device__ __forceinline__ uint32_t sweep_list(const uint8_t* __restrict__ M, const uint32_t* __restrict__ P, int pw,
+                                               uint32_t* X, uint32_t tb0, const uint2* ci, const uint32_t* ctst,
+                                               int cnt8, int r0, int r1, int dmax, uint32_t active, uint32_t* chgn) {
   uint32_t my_or = 0u;
   for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
     const uint32_t cur = X[r];
@@ -80,24 +174,83 @@ __device__ __forceinline__ uint32_t sweep_rows(const uint8_t* __restrict__ M, co
     const int x = r / dmax;
     uint32_t acc = 0xffffffffu;
     for (int c0 = 0; c0 < cnt8 && (acc & live) != 0u; c0 += 8) {
+      uint2 cc[8];
       uint32_t mv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) mv[u] = mask_at<W>(Mrow + ci[c0 + u].x);
+      for (int u = 0; u < 8; ++u) cc[u] = ci[c0 + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mv[u] = mask_at<W>(Mrow + cc[u].x);
+      const uint4 ta = *reinterpret_cast<const uint4*>(ctst + c0);
+      const uint4 tb = *reinterpret_cast<const uint4*>(ctst + c0 + 4);
+      const uint32_t tz[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint32_t ty = tb0 + ci[c0 + u].y;
-        const uint32_t m = mv[u];
-        uint32_t sup = lds32(ty + ((m << 2) & 0x3Cu));
-#pragma unroll
-        for (int q = 1; q < NQ; ++q) sup |= lds32(ty + 64u * q + ((m >> (4 * q - 2)) & 0x3Cu));
-        if constexpr (CP) {
-          if ((sup & live) != live) {
-            const int y = (int)(ci[c0 + u].y / (NQ * 64));
-            if (!((__ldg(P + (size_t)x * pw + (y >> 5)) >> (y & 31)) & 1u)) sup = 0xffffffffu;
-          }
-        }
-        acc &= sup;
+        const uint32_t s = sup_lookup<W, 0, 0>(mv[u], tb0 + cc[u].y);
+        apply_col<CP>(acc, s, tz[u], live, P, pw, x, (int)(cc[u].y / Lut<W>::TSB));
       }
+    }
+    const uint32_t nb = cur & (acc | ~active);
+    if (nb != cur) {
+      X[r] = nb;
+      atomicOr(&chgn[x], cur ^ nb);
+      my_or |= cur ^ nb;
+    }
+  }
+  return my_or;
+}
+
+// Every column through the row-major copy: one 16-byte load per 16/W columns
+// (two groups per iteration, the next pair in flight); tst[] covers npad
+// columns (0 beyond n, so padding columns test no lane).
+template <int W, bool CP, int U>
+__device__ __forceinline__ void full_col(uint32_t& acc, const uint32_t (&wv)[8], uint32_t t, uint32_t cb,
+                                         uint32_t live, const uint32_t* P, int pw, int x, int y0) {
+  constexpr int MPW = 4 / W;
+  const uint32_t s = sup_lookup<W, 8 * W * (U % MPW), U * Lut<W>::TSB>(wv[U / MPW], cb);
+  apply_col<CP>(acc, s, t, live, P, pw, x, y0 + U);
+}
+template <int W, bool CP, int K4>
+__device__ __forceinline__ void full_quad(uint32_t& acc, const uint32_t (&wv)[8], const uint4* tq, uint32_t cb,
+                                          uint32_t live, const uint32_t* P, int pw, int x, int y0) {
+  const uint4 t4 = tq[K4];
+  full_col<W, CP, 4 * K4>(acc, wv, t4.x, cb, live, P, pw, x, y0);
+  full_col<W, CP, 4 * K4 + 1>(acc, wv, t4.y, cb, live, P, pw, x, y0);
+  full_col<W, CP, 4 * K4 + 2>(acc, wv, t4.z, cb, live, P, pw, x, y0);
+  full_col<W, CP, 4 * K4 + 3>(acc, wv, t4.w, cb, live, P, pw, x, y0);
+}
+template <int W, bool CP, int... K4s>
+__device__ __forceinline__ void full_cols(std::integer_sequence<int, K4s...>, uint32_t& acc, const uint32_t (&wv)[8],
+                                          const uint4* tq, uint32_t cb, uint32_t live, const uint32_t* P, int pw,
+                                          int x, int y0) {
+  (full_quad<W, CP, K4s>(acc, wv, tq, cb, live, P, pw, x, y0), ...);
+}
+
+template <int W, bool CP>
+__device__ __forceinline__ uint32_t sweep_full(const uint8_t* __restrict__ Mr, int dbytes,
+                                               const uint32_t* __restrict__ P, int pw, uint32_t* X, uint32_t tb0,
+                                               const uint32_t* tst, int npair, int ng, int r0, int r1, int dmax,
+                                               uint32_t active, uint32_t* chgn) {
+  constexpr int CPI = 32 / W;  // columns per iteration (two 16-byte groups)
+  uint32_t my_or = 0u;
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
+    const uint32_t cur = X[r];
+    const uint32_t live = cur & active;
+    if (!live) continue;
+    const uint4* row = reinterpret_cast<const uint4*>(Mr + (size_t)r * dbytes);
+    const int x = r / dmax;
+    uint32_t acc = 0xffffffffu;
+    const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);  // beyond the row: columns >= n test no lane
+    uint4 n0 = __ldg(row), n1 = ng > 1 ? __ldg(row + 1) : ones;
+    for (int g2 = 0; g2 < npair; ++g2) {
+      const uint32_t wv[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+      if (g2 + 1 < npair) {
+        n0 = __ldg(row + 2 * g2 + 2);
+        n1 = 2 * g2 + 3 < ng ? __ldg(row + 2 * g2 + 3) : ones;
+      }
+      full_cols<W, CP>(std::make_integer_sequence<int, CPI / 4>{}, acc, wv,
+                       reinterpret_cast<const uint4*>(tst + g2 * CPI), tb0 + (uint32_t)(g2 * CPI * Lut<W>::TSB),
+                       live, P, pw, x, g2 * CPI);
+      if ((acc & live) == 0u) break;
     }
     const uint32_t nb = cur & (acc | ~active);
     if (nb != cur) {
@@ -111,33 +264,47 @@ __device__ __forceinline__ uint32_t sweep_rows(const uint8_t* __restrict__ M, co
 
 }  // namespace
 
-// Shared memory (dynamic): X [rows4] u32 | T [n][NQ][16] u32 | chg [n] u32 |
-// chgn [n] u32 | list [n] u16.  Cluster rank k owns rows [k*RPC, (k+1)*RPC),
-// RPC a multiple of dmax, so every variable's rows live in one CTA.
+// Shared memory (dynamic), byte offsets from the TSB-aligned start:
+//   Tb [npad][TSB] | X [rows4] u32 | tst [npad] u32 | chg [n4] | chgn [n4] |
+//   chg_in [n4] | ctst [n + 8] u32 | ci [n + 8] uint2.
+// Cluster rank k owns rows [k*RPC, (k+1)*RPC), RPC a multiple of dmax, so
+// every variable's rows live in one CTA.
+extern __shared__ __align__(16) uint8_t cl_smem[];
+
 template <int W>
 __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
-  constexpr int NQ = 2 * W;  // nibbles per mask (d <= 8W <= 32)
-  extern __shared__ uint32_t sm[];
-  __shared__ uint32_t s_part[2];   // this CTA's [changed lanes OR, non-empty lanes AND]
-  __shared__ int sc[kMaxT / 32];
+  using L = Lut<W>;
+  constexpr int CPI = 32 / W;
+  __shared__ uint32_t s_red[2][2];             // per pass parity: this CTA's [changed lanes, emptied lanes]
+  __shared__ uint32_t s_part[2][kMaxC][2];     // per pass parity: every CTA's partial (pushed to all)
+  __shared__ int s_cnt;
+  __shared__ uint32_t s_empty0;
   __shared__ int s_iters[32], s_status[32];
   cg::cluster_group cluster = cg::this_cluster();
   const int C = (int)cluster.num_blocks();
   const int k = (int)cluster.block_rank();
   const int g = blockIdx.x / C, G = gridDim.x / C;
   const int n = p.n, dmax = p.dmax, rows = n * dmax, rows4 = (rows + 3) & ~3;
+  const int npad = (n + CPI - 1) / CPI * CPI, n4 = (n + 3) & ~3;
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = T >> 5;
-  uint32_t* X = sm;
-  uint32_t* Tb = X + rows4;
-  uint32_t* chg = Tb + (size_t)n * NQ * 16;
-  uint32_t* chgn = chg + n;
-  uint16_t* list = reinterpret_cast<uint16_t*>(chgn + n);
-  uint2* ci = reinterpret_cast<uint2*>(list + (((size_t)n + 7) & ~(size_t)7));  // [n + 8] column info
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(cl_smem);
+  const uint32_t pad = (uint32_t)(L::TSB - (base & (L::TSB - 1))) & (L::TSB - 1);
+  uint8_t* Tb = cl_smem + pad;
+  const uint32_t tb0 = base + pad;  // shared-memory address, TSB-aligned
+  uint32_t* X = reinterpret_cast<uint32_t*>(Tb + (size_t)npad * L::TSB);
+  uint32_t* tst = X + rows4;
+  uint32_t* chg = tst + npad;
+  uint32_t* chgn = chg + n4;
+  uint32_t* chg_in = chgn + n4;
+  uint32_t* ctst = chg_in + n4;
+  uint2* ci = reinterpret_cast<uint2*>(ctst + ((n + 8 + 3) & ~3));
   const int r0 = k * p.RPC, r1 = min(rows, r0 + p.RPC);  // my rows
   const int x0 = r0 / dmax, x1 = (r1 + dmax - 1) / dmax;  // my variables
   const bool full = (p.flags & kFullCL) != 0;
+  const bool rowmajor = p.Mr != nullptr;
+  const int ng = p.dbytes / 16, npair = npad / CPI;
   const int NW = (p.S + 31) / 32;
-  // debug stamps: per word [start, staged, per pass: list, tables, sweep, A, B], end
+  // debug stamps: per word [start, staged, per pass: prep, sweep, push, sync, control], end
   int nd = 0;
   const bool dbg = p.dbg != nullptr && k == 0 && tid == 0;
 #define CL_MARK() do { if (dbg && nd < 255) p.dbg[(size_t)g * 256 + nd++] = globaltimer(); } while (0)
@@ -145,15 +312,11 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   for (int w = g; w < NW; w += G) {
     const int s0 = 32 * w, nst = min(32, p.S - s0);
     CL_MARK();
-    // ---- the word's states -> bit slices (every CTA, all rows); seeds -> chg
-    for (int x = warp; x < n; x += nwarps) {
-      const uint64_t v = lane < nst ? __ldg(p.d_in + (size_t)(s0 + lane) * n + x) & __ldg(p.dommask + x) : 0ull;
-      for (int a = 0; a < dmax; ++a) {
-        const uint32_t b = __ballot_sync(0xffffffffu, (v >> a) & 1ull);
-        if (lane == 0) X[x * dmax + a] = b;
-      }
-    }
-    for (int x = tid; x < n; x += T) {
+    // ---- the word's states -> bit slices (every CTA, all rows); lanes with an
+    // empty input domain; seeds -> chg
+    if (tid == 0) s_empty0 = 0u;
+    for (int y = tid; y < npad; y += T) tst[y] = 0u;
+    for (int x = tid; x < n4; x += T) {
       chg[x] = 0u;
       chgn[x] = 0u;
     }
@@ -161,142 +324,167 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       s_iters[tid] = 0;
       s_status[tid] = 0;
     }
-    uint32_t active = nst >= 32 ? 0xffffffffu : ((1u << nst) - 1u);
     __syncthreads();
     {
-      // a root state (no seed) tests every column in pass 1
+      uint32_t emp = 0u;
+      for (int xb = warp; xb < n; xb += 4 * nwarps) {
+        uint64_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int x = xb + j * nwarps;
+          v[j] = (x < n && lane < nst) ? __ldg(p.d_in + (size_t)(s0 + lane) * n + x) & __ldg(p.dommask + x) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int x = xb + j * nwarps;
+          if (x >= n) break;
+          emp |= __ballot_sync(0xffffffffu, v[j] == 0ull);
+          uint32_t mine = 0u;
+          for (int a = 0; a < dmax; ++a) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (v[j] >> a) & 1ull);
+            if (lane == a) mine = b;
+          }
+          if (lane < dmax) X[x * dmax + lane] = mine;
+        }
+      }
+      if (lane == 0 && emp) atomicOr(&s_empty0, emp);
       uint32_t rootl = 0;
       if (tid < nst) {
         const int sv = p.seed_var ? p.seed_var[s0 + tid] : -1;
         if (sv >= 0 && sv < n) atomicOr(&chg[sv], 1u << tid);
         else rootl = 1u << tid;
       }
-      rootl = __reduce_or_sync(0xffffffffu, rootl);  // lanes 0..31 are warp 0
-      if (warp == 0) sc[0] = (int)rootl;
+      if (warp == 0) {
+        rootl = __reduce_or_sync(0xffffffffu, rootl);
+        if (lane == 0) s_cnt = (int)rootl;
+      }
       __syncthreads();
-      const uint32_t roots = (uint32_t)sc[0];
+      const uint32_t roots = (uint32_t)s_cnt;
       if (roots)
         for (int x = tid; x < n; x += T) chg[x] |= roots;
-      __syncthreads();
     }
-    // lanes whose every domain is non-empty at the start of the pass (an empty
-    // one can only come from the input or, in full mode, from a wipeout)
-    uint32_t allne0;
-    {
-      uint32_t ne_all = 0xffffffffu;
-      for (int x = tid; x < n; x += T) {
-        uint32_t ne = 0u;
-        for (int a = 0; a < dmax; ++a) ne |= X[x * dmax + a];
-        ne_all &= ne;
-      }
-      ne_all = __reduce_and_sync(0xffffffffu, ne_all);
-      if (lane == 0) sc[warp] = (int)ne_all;
-      __syncthreads();
-      allne0 = 0xffffffffu;
-      for (int w2 = 0; w2 < nwarps; ++w2) allne0 &= (uint32_t)sc[w2];
-      __syncthreads();
-    }
+    uint32_t active = nst >= 32 ? 0xffffffffu : ((1u << nst) - 1u);
+    uint32_t E = s_empty0;  // lanes with some empty domain (cumulative)
     int t = 0;
+    __syncthreads();
     CL_MARK();
     for (;;) {
       ++t;
-      // ---- tested columns U = { y : chg[y] & active } (ascending, block scan)
-      int cnt;
-      {
-        const int per = (n + T - 1) / T, b = min(n, tid * per), e = min(n, b + per);
-        uint32_t c = 0;
-        for (int i = b; i < e; ++i) c += (chg[i] & active) != 0u;
-        uint32_t total;
-        uint32_t pos = block_scan_u32(c, &total, sc);
-        for (int i = b; i < e; ++i)
-          if (chg[i] & active) list[pos++] = (uint16_t)i;
-        cnt = (int)total;
-      }
-      __syncthreads();
-      CL_MARK();
-      // ---- per-column offsets (the list padded to a multiple of 8) and nibble tables
-      const int cnt8 = (cnt + 7) & ~7;
-      for (int c = tid; c < cnt8; c += T) {
-        const int y = list[min(c, cnt - 1)];
-        ci[c] = make_uint2((uint32_t)((size_t)y * p.col_stride), (uint32_t)(y * NQ * 64));  // {mask bytes, table bytes}
-      }
-      for (int i = tid; i < cnt * NQ; i += T) {
-        const int c = i / NQ, q = i - c * NQ;
-        const int y = list[c];
-        uint32_t xb[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) xb[j] = (4 * q + j < dmax) ? X[y * dmax + 4 * q + j] : 0u;
-        uint32_t tv[16];
-        tv[0] = 0u;
-#pragma unroll
-        for (int v = 1; v < 16; ++v) tv[v] = tv[v & (v - 1)] | xb[__ffs(v) - 1];
-        uint4* dst = reinterpret_cast<uint4*>(Tb + ((size_t)y * NQ + q) * 16);
-#pragma unroll
-        for (int v = 0; v < 16; v += 4) dst[v >> 2] = make_uint4(tv[v], tv[v + 1], tv[v + 2], tv[v + 3]);
-      }
-      __syncthreads();
-      CL_MARK();
-      // ---- a3/a4: my rows against the tested columns, 32 states at a time
-      uint32_t my_or = (~allne0 & active)
-                                 ? sweep_rows<W, true>(p.M, p.P, p.pw, X, Tb, ci, cnt8, r0, r1, dmax, active, chgn)
-                                 : sweep_rows<W, false>(p.M, p.P, p.pw, X, Tb, ci, cnt8, r0, r1, dmax, active, chgn);
-      CL_MARK();
-      // this CTA's partials: lanes that changed; lanes with every variable non-empty
-      uint32_t my_ne = 0xffffffffu;
-      __syncthreads();
-      for (int x = x0 + tid; x < x1; x += T) {
-        uint32_t ne = 0u;
-        for (int a = 0; a < dmax; ++a) ne |= X[x * dmax + a];
-        my_ne &= ne;
-      }
-      my_or = __reduce_or_sync(0xffffffffu, my_or);
-      my_ne = __reduce_and_sync(0xffffffffu, my_ne);
+      const int par = t & 1;
+      // ---- prep: tst / the column list (warp 0), tables of the changed columns
+      // (every column in pass 1) by the other warps
       if (tid == 0) {
-        s_part[0] = 0u;
-        s_part[1] = 0xffffffffu;
+        s_red[par][0] = 0u;
+        s_red[par][1] = 0u;
+      }
+      if (warp == 0) {
+        int cnt = 0;
+        for (int yb = 0; yb < n; yb += 32) {
+          const int y = yb + lane;
+          const uint32_t ty = y < n ? chg[y] & active : 0u;
+          if (y < n) tst[y] = ty;
+          const uint32_t bal = __ballot_sync(0xffffffffu, ty != 0u);
+          if (ty) {
+            const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
+            ci[pos] = make_uint2((uint32_t)((size_t)y * p.col_stride), (uint32_t)(y * L::TSB));
+            ctst[pos] = ty;
+          }
+          cnt += __popc(bal);
+        }
+        const int cnt8 = (cnt + 7) & ~7;
+        if (cnt + lane < cnt8) {  // padding: tests no lane
+          ci[cnt + lane] = make_uint2(0u, 0u);
+          ctst[cnt + lane] = 0u;
+        }
+        if (lane == 0) s_cnt = cnt;
+      }
+      if (nwarps == 1) __syncwarp();
+      {
+        const int tb = nwarps > 1 ? tid - 32 : tid, TT = nwarps > 1 ? T - 32 : T;
+        if (tb >= 0)
+          for (int i = tb; i < n * L::NI; i += TT) {
+            const int y = i / L::NI;
+            if (t == 1 || chg[y] != 0u) build_item<W>(Tb, X, y, i - y * L::NI, dmax);
+          }
       }
       __syncthreads();
-      if (lane == 0) {
-        if (my_or) atomicOr(&s_part[0], my_or);
-        if (my_ne != 0xffffffffu) atomicAnd(&s_part[1], my_ne);
-      }
-      cluster.sync();  // [A] every CTA's rows, change masks and partials are final
+      const int cnt = s_cnt;
+      // everybody's rows and my chg_in are read: peers may overwrite them once
+      // they have waited on this arrival
+      cluster_arrive_release();
       CL_MARK();
-      // ---- exchange: change masks of every variable from its owner, the rows of
-      // the variables that changed, and the partials
-      uint32_t changed = 0u, allne = 0xffffffffu;
-      for (int q = 0; q < C; ++q) {
-        const uint32_t* rp = cluster.map_shared_rank(s_part, q);
-        changed |= rp[0];
-        allne &= rp[1];
+      // ---- sweep: my rows against the tested columns
+      const bool cp = (E & active) != 0u;  // some active state has an empty domain
+      const bool use_full = rowmajor && (long)cnt * p.full_den >= (long)n * p.full_num;
+      uint32_t my_or;
+      if (use_full)
+        my_or = cp ? sweep_full<W, true>(p.Mr, p.dbytes, p.P, p.pw, X, tb0, tst, npair, ng, r0, r1, dmax, active, chgn)
+                   : sweep_full<W, false>(p.Mr, p.dbytes, p.P, p.pw, X, tb0, tst, npair, ng, r0, r1, dmax, active, chgn);
+      else
+        my_or = cp ? sweep_list<W, true>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn)
+                   : sweep_list<W, false>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn);
+      my_or = __reduce_or_sync(0xffffffffu, my_or);
+      if (lane == 0 && my_or) atomicOr(&s_red[par][0], my_or);
+      __syncthreads();  // my rows and change masks are final
+      CL_MARK();
+      // ---- push: wait until every CTA has read the old rows, then store my
+      // changed rows and my change masks into every other CTA
+      cluster_wait_acquire();
+      uint32_t emp = 0u;
+      for (int x = x0 + tid; x < x1; x += T) {
+        const uint32_t c = chgn[x];
+        for (int q = 0; q < C; ++q)
+          if (q != k) *cluster.map_shared_rank(chg_in + x, q) = c;
+        if (c) {
+          uint32_t ne = 0u;
+          for (int a = 0; a < dmax; ++a) ne |= X[x * dmax + a];
+          emp |= ~ne;
+        }
       }
-      for (int x = tid; x < n; x += T) {
-        const int owner = min(C - 1, (x * dmax) / p.RPC);
-        chg[x] = owner == k ? chgn[x] : *cluster.map_shared_rank(chgn + x, owner);
+      for (int r = r0 + tid; r < r1; r += T) {
+        if (!chgn[r / dmax]) continue;
+        const uint32_t v = X[r];
+        for (int q = 0; q < C; ++q)
+          if (q != k) *cluster.map_shared_rank(X + r, q) = v;
       }
+      emp = __reduce_or_sync(0xffffffffu, emp);
+      if (lane == 0 && emp) atomicOr(&s_red[par][1], emp);
       __syncthreads();
-      for (int i = tid; i < n * dmax; i += T) {
-        const int x = i / dmax;
-        if (!chg[x]) continue;
-        const int owner = min(C - 1, i / p.RPC);
-        if (owner != k) X[i] = *cluster.map_shared_rank(X + i, owner);
+      if (tid < C) {
+        uint32_t* dst = cluster.map_shared_rank(&s_part[par][k][0], tid);
+        dst[0] = s_red[par][0];
+        dst[1] = s_red[par][1];
       }
-      cluster.sync();  // [B] nobody rewrites its rows / chgn before the others read them
       CL_MARK();
-      for (int x = x0 + tid; x < x1; x += T) chgn[x] = 0u;
+      cluster_arrive_release();
+      cluster_wait_acquire();
+      CL_MARK();
       // ---- per-state loop control (Alg. 1): wipeout first, then "changed"
-      const uint32_t wipe = ~allne;
-      const uint32_t stop_wipe = full ? 0u : (wipe & active);
+      uint32_t changed = 0u;
+      for (int q = 0; q < C; ++q) {
+        changed |= s_part[par][q][0];
+        E |= s_part[par][q][1];
+      }
+      const uint32_t stop_wipe = full ? 0u : (E & active);
       const uint32_t stop_conv = ~changed & active & ~stop_wipe;
       if (tid < 32) {
         const uint32_t bit = 1u << tid;
         if (active & bit) s_iters[tid] = t;
         if (stop_wipe & bit) s_status[tid] = 1;
-        if (stop_conv & bit) s_status[tid] = (wipe & bit) ? 1 : 0;
+        if (stop_conv & bit) s_status[tid] = (E & bit) ? 1 : 0;
       }
       active &= ~(stop_wipe | stop_conv);
-      allne0 = allne;
+      // next pass's change masks: mine from chgn, the others' as pushed
+      for (int x = tid; x < n; x += T) {
+        if (x >= x0 && x < x1) {
+          chg[x] = chgn[x];
+          chgn[x] = 0u;
+        } else {
+          chg[x] = chg_in[x];
+        }
+      }
       __syncthreads();
+      CL_MARK();
       if (active == 0u) break;
     }
     // ---- outputs: each CTA writes its own variables; rank 0 the counters
@@ -315,9 +503,13 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
 #undef CL_MARK
 }
 
+
 size_t batch_cl_smem(int n, int dmax, int W) {
+  const int TSB = W == 1 ? Lut<1>::TSB : W == 2 ? Lut<2>::TSB : Lut<4>::TSB;
+  const size_t CPI = 32 / W;
+  const size_t npad = (n + CPI - 1) / CPI * CPI, n4 = ((size_t)n + 3) & ~(size_t)3;
   const size_t rows4 = (((size_t)n * dmax) + 3) & ~(size_t)3;
-  return rows4 * 4 + (size_t)n * (2 * W) * 16 * 4 + (size_t)n * 8 + (((size_t)n + 7) & ~(size_t)7) * 2 +
+  return (size_t)TSB + npad * TSB + rows4 * 4 + npad * 4 + 3 * n4 * 4 + ((((size_t)n + 8 + 3) & ~(size_t)3) * 4) +
          ((size_t)n + 8) * 8;
 }
 
@@ -330,6 +522,7 @@ cudaError_t launch_batch_cl(int W, const BatchCLParams& p, int clusters, int C, 
     case 4: k = (const void*)rac_batch_cl<4>; break;
     default: return cudaErrorInvalidValue;
   }
+  if (C > kMaxC) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (C > 8) {
@@ -359,6 +552,10 @@ cudaError_t batch_cl_max_clusters(int W, int C, int threads, size_t smem, int* o
                                                                    : (const void*)rac_batch_cl<4>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (C > 8) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
   cfg.blockDim = dim3(threads);

@@ -203,6 +203,9 @@ cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, 
 struct BatchCLParams {
   const uint8_t* M;         // column-major masks
   size_t col_stride;
+  const uint8_t* Mr;        // nullable: row-major copy (row stride dbytes)
+  int dbytes;
+  int full_num, full_den;   // test every column through Mr when cnt * full_den >= n * full_num
   int n, dmax;
   const uint32_t* P;
   int pw;

@@ -524,6 +524,71 @@ def test_batched_corpus(rac):
             os.environ.pop("RAC_BATCH_IMPL", None)
 
 
+@pytest.mark.parametrize("full", ["0", "1/1000", None])
+def test_batched_sweep_modes(rac, full, monkeypatch):
+    """The cluster batch kernel's two sweeps -- tested-column lists over the column-major
+    masks (RAC_BATCH_FULL=0) and every column through the row-major copy (1/1000: nearly
+    every pass) -- and the default choice give the oracle's results: C5 dive states seeded
+    with their assigned variable (O1, the precondition holds), and seeded calls on W-rand
+    states, where the precondition of Alg. 1's seeded call does not hold, against O5
+    (tensorAC(Vars, @changed = seeds) as written): every state follows its own
+    Alg. 1 trajectory, not the union of its word's columns."""
+    import torch
+    if full is not None:
+        monkeypatch.setenv("RAC_BATCH_FULL", full)
+    n, d, S = 200, 16, 512
+    inst = synth.random_csp(n, d, 0.8, 0.3, 1)
+    orc = oracle.Oracle.from_instance(inst)
+    _, root, _, _ = orc.rac(inst.full_domains())
+
+    def enf(D):
+        s, out, _, _ = orc.rac(D, with_epochs=False)
+        return s, out
+
+    states, seeds = synth.dive_states(root, enf, S, seed=3, return_seeds=True)
+    states = np.stack(states)
+    seeds = np.asarray(seeds, dtype=np.int32)
+    seeds[::5] = -1
+    # the second half: W-rand states (not arc consistent) with random seed lists of one variable
+    rng = np.random.default_rng(11)
+    for s in range(S // 2, S):
+        states[s] = synth.w_rand(inst.dom, 0.9, seed=500 + s)
+        seeds[s] = int(rng.integers(0, n))
+    ctx = rac.RacContext.from_instance(inst)
+    din = torch.from_numpy(states.view(np.int64)).cuda()
+    dout = torch.zeros_like(din)
+    its = torch.zeros(S, dtype=torch.int32, device="cuda")
+    sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+    ctx.enforce_batch_seeded(S, din, dout, its, sts, torch.from_numpy(seeds).cuda())
+    torch.cuda.synchronize()
+    out = dout.cpu().numpy().view(np.uint64)
+    its, sts = its.cpu().numpy(), sts.cpu().numpy()
+    for s in range(S):
+        if seeds[s] < 0:
+            e = orc.rac(states[s], with_epochs=False)
+        else:
+            e = orc.rac_seeded(states[s], [int(seeds[s])], with_epochs=False)
+        assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (s, seeds[s], full)
+    for k, inst in enumerate(I.random_corpus(30, seed0=191, n_range=(2, 40), d_range=(1, 32))):
+        orc = oracle.Oracle.from_instance(inst)
+        S2 = int(rng.integers(1, 80))
+        st2 = np.stack([synth.w_rand(inst.dom, 0.85, seed=1000 * k + s) for s in range(S2)])
+        sd2 = rng.integers(-1, inst.n, size=S2).astype(np.int32)
+        ctx = rac.RacContext.from_instance(inst)
+        din = torch.from_numpy(st2.view(np.int64)).cuda()
+        dout = torch.zeros_like(din)
+        its = torch.zeros(S2, dtype=torch.int32, device="cuda")
+        sts = torch.zeros(S2, dtype=torch.int32, device="cuda")
+        ctx.enforce_batch_seeded(S2, din, dout, its, sts, torch.from_numpy(sd2).cuda())
+        torch.cuda.synchronize()
+        out = dout.cpu().numpy().view(np.uint64)
+        it_h, st_h = its.cpu().numpy(), sts.cpu().numpy()
+        for s in range(S2):
+            e = (orc.rac(st2[s], with_epochs=False) if sd2[s] < 0
+                 else orc.rac_seeded(st2[s], [int(sd2[s])], with_epochs=False))
+            assert (st_h[s], it_h[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (k, s, full)
+
+
 def test_nccl_exchange_leg_single_rank(rac):
     """The multi-GPU path with its real NCCL all-gather (a one-rank communicator,
     RAC_OPT_NCCL_SELF) gives the oracle's results: exercises dlopen of libnccl, comm init,

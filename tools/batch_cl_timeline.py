@@ -1,7 +1,8 @@
 """Per-word pass timeline of the cluster batch kernel rac_batch_cl at C5
 (RAC_DEBUG_TIMELINE=1): for every cluster (one 32-state word), %globaltimer at
-word start, after staging, and per pass after [list, tables, sweep, barrier A,
-exchange + barrier B]."""
+word start, after staging, and per pass after [prep (column list + tables),
+sweep, push (split-barrier wait + DSMEM stores), full cluster barrier, loop
+control]."""
 import ctypes
 import json
 import os
@@ -55,7 +56,7 @@ print("state iterations histogram:", np.bincount(its.cpu().numpy()).tolist())
 for w in words[-3:]:
     print("slow word g=%d passes=%d end=%d stage=%d" % (w["g"], w["passes"], w["end"], w["stage"]))
     for i, pp in enumerate(w["per_pass"]):
-        print("   pass %2d  list %5d tables %5d sweep %6d A %5d B %5d" % (i + 1, *pp))
+        print("   pass %2d  prep %5d sweep %6d push %5d sync %5d control %5d" % (i + 1, *pp))
 allp = [pp for w in words for pp in w["per_pass"]]
 print("phase totals over all passes of all words (ns): list %d tables %d sweep %d A %d B %d" %
       tuple(np.sum(allp, axis=0)))
