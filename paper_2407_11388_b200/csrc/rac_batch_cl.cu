@@ -84,11 +84,62 @@ __device__ __forceinline__ uint32_t lds_imm(uint32_t addr) {
   return v;
 }
 
-__device__ __forceinline__ void cluster_arrive_release() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+// Split cluster barrier.  The arrive is relaxed: what it announces ("I have
+// read the peers' rows and my chg_in") needs no memory release -- those loads
+// were consumed into shared-memory stores before the preceding __syncthreads --
+// and a release arrive costs a MEMBAR.ALL.GPU per pass.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void cluster_wait_acquire() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// DSMEM pushes: st.async stores into a peer CTA's shared memory that complete
+// bytes on the peer's mbarrier (the peer's wait on its own mbarrier is the
+// only synchronisation the data needs).
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+               :: "r"(raddr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void st_async_b32(uint32_t raddr, uint32_t v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+               :: "r"(raddr), "r"(v), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t a, uint32_t b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];"
+               :: "r"(raddr), "r"(a), "r"(b), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; "
+                 "selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+}
+
+// Bytes CTA k receives per pass: from every other rank q, its rows (16-byte
+// stores, rounded up), its change masks and its two-word partial.
+__device__ __forceinline__ uint32_t incoming_bytes(int k, int C, int RPC, int rows, int dmax) {
+  uint32_t b = 0;
+  for (int q = 0; q < C; ++q) {
+    if (q == k) continue;
+    const int a0 = q * RPC, a1 = min(rows, a0 + RPC);
+    if (a1 <= a0) continue;
+    b += 16u * (uint32_t)((a1 - a0 + 3) / 4) + 4u * (uint32_t)(a1 / dmax - a0 / dmax) + 8u;
+  }
+  return b;
 }
 
 // Byte offset of the table entry of chunk Q for the mask at bit SH of w.
@@ -276,7 +327,8 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   using L = Lut<W>;
   constexpr int CPI = 32 / W;
   __shared__ uint32_t s_red[2][2];             // per pass parity: this CTA's [changed lanes, emptied lanes]
-  __shared__ uint32_t s_part[2][kMaxC][2];     // per pass parity: every CTA's partial (pushed to all)
+  __shared__ __align__(8) uint32_t s_part[2][kMaxC][2];  // per pass parity: every CTA's partial (pushed to all)
+  __shared__ __align__(8) uint64_t s_mbar;     // incoming pushes of the current pass
   __shared__ int s_cnt;
   __shared__ uint32_t s_empty0;
   __shared__ int s_iters[32], s_status[32];
@@ -308,6 +360,15 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   int nd = 0;
   const bool dbg = p.dbg != nullptr && k == 0 && tid == 0;
 #define CL_MARK() do { if (dbg && nd < 255) p.dbg[(size_t)g * 256 + nd++] = globaltimer(); } while (0)
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  const uint32_t in_bytes = incoming_bytes(k, C, p.RPC, rows, dmax);
+  uint32_t ph = 0;  // parity of the mbarrier phase of the current pass
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (C > 1) mbar_expect_tx(mbar, in_bytes);  // pass 1 of the first word
+  }
+  cluster.sync();  // every peer's mbarrier is initialised before anybody pushes
 
   for (int w = g; w < NW; w += G) {
     const int s0 = 32 * w, nst = min(32, p.S - s0);
@@ -411,7 +472,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       const int cnt = s_cnt;
       // everybody's rows and my chg_in are read: peers may overwrite them once
       // they have waited on this arrival
-      cluster_arrive_release();
+      cluster_arrive_relaxed();
       CL_MARK();
       // ---- sweep: my rows against the tested columns
       const bool cp = (E & active) != 0u;  // some active state has an empty domain
@@ -426,38 +487,48 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       my_or = __reduce_or_sync(0xffffffffu, my_or);
       if (lane == 0 && my_or) atomicOr(&s_red[par][0], my_or);
       __syncthreads();  // my rows and change masks are final
-      CL_MARK();
-      // ---- push: wait until every CTA has read the old rows, then store my
-      // changed rows and my change masks into every other CTA
-      cluster_wait_acquire();
-      uint32_t emp = 0u;
-      for (int x = x0 + tid; x < x1; x += T) {
-        const uint32_t c = chgn[x];
-        for (int q = 0; q < C; ++q)
-          if (q != k) *cluster.map_shared_rank(chg_in + x, q) = c;
-        if (c) {
+      {
+        // lanes in which one of my variables became empty (only changed ones can)
+        uint32_t emp = 0u;
+        for (int x = x0 + tid; x < x1; x += T) {
+          if (!chgn[x]) continue;
           uint32_t ne = 0u;
           for (int a = 0; a < dmax; ++a) ne |= X[x * dmax + a];
           emp |= ~ne;
         }
+        emp = __reduce_or_sync(0xffffffffu, emp);
+        if (lane == 0 && emp) atomicOr(&s_red[par][1], emp);
       }
-      for (int r = r0 + tid; r < r1; r += T) {
-        if (!chgn[r / dmax]) continue;
-        const uint32_t v = X[r];
-        for (int q = 0; q < C; ++q)
-          if (q != k) *cluster.map_shared_rank(X + r, q) = v;
-      }
-      emp = __reduce_or_sync(0xffffffffu, emp);
-      if (lane == 0 && emp) atomicOr(&s_red[par][1], emp);
       __syncthreads();
-      if (tid < C) {
-        uint32_t* dst = cluster.map_shared_rank(&s_part[par][k][0], tid);
-        dst[0] = s_red[par][0];
-        dst[1] = s_red[par][1];
+      CL_MARK();
+      // ---- push: wait until every CTA has read the old rows, then store my
+      // rows, my change masks and my partial into every other CTA (fixed sizes:
+      // each peer's mbarrier expects exactly these bytes)
+      cluster_wait();
+      if (C > 1) {
+        // same layout in every CTA: the peer address is mapa(local address, q)
+        const uint32_t xs = (uint32_t)__cvta_generic_to_shared(X + r0), cs = (uint32_t)__cvta_generic_to_shared(chg_in);
+        const uint32_t ps = (uint32_t)__cvta_generic_to_shared(&s_part[par][k][0]);
+        const int nv4 = (r1 - r0 + 3) / 4;
+        for (int q = 0; q < C; ++q) {
+          if (q == k) continue;
+          const uint32_t bq = mapa(mbar, (uint32_t)q);
+          for (int i = tid; i < nv4; i += T)
+            st_async_v4(mapa(xs + 16u * (uint32_t)i, (uint32_t)q), *reinterpret_cast<const uint4*>(X + r0 + 4 * i), bq);
+          for (int x = x0 + tid; x < x1; x += T) st_async_b32(mapa(cs + 4u * (uint32_t)x, (uint32_t)q), chgn[x], bq);
+          if (tid == 0) st_async_v2(mapa(ps, (uint32_t)q), s_red[par][0], s_red[par][1], bq);
+        }
+      }
+      if (tid == 0) {
+        s_part[par][k][0] = s_red[par][0];
+        s_part[par][k][1] = s_red[par][1];
       }
       CL_MARK();
-      cluster_arrive_release();
-      cluster_wait_acquire();
+      if (C > 1) mbar_wait(mbar, ph);
+      ph ^= 1u;
+      __syncthreads();  // s_part[par][k] (own slot) for everybody
+      // the next pass's incoming bytes (peers push them only after my next arrival)
+      if (C > 1 && tid == 0) mbar_expect_tx(mbar, in_bytes);
       CL_MARK();
       // ---- per-state loop control (Alg. 1): wipeout first, then "changed"
       uint32_t changed = 0u;

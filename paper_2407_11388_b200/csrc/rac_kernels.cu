@@ -637,9 +637,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   }
   if (blockIdx.x == 0) {
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.d_out[x] = load_w<W>(Db + x * W);
+    // status last, after D_out and iterations are visible system-wide: a blocking
+    // host call polls the mapped status word instead of synchronising the stream
+    __threadfence_system();
+    __syncthreads();
     if (threadIdx.x == 0) {
       if (emp && t > 0) *p.calls = calls0 + 1ull;  // every CTA read *calls before the first barrier
       *p.iters = t;
+      __threadfence_system();
       *p.status = (mg && *reinterpret_cast<volatile int32_t*>(p.xerr)) ? kPeerTimeout : status;
       // every CTA read *p.seq before the first barrier
       if (t > 0) *p.seq = base + (unsigned long long)t;
