@@ -727,6 +727,10 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   p.flags = flags;
   static const uint32_t ab = getenv("RAC_FUSED_AB") ? (uint32_t)atoi(getenv("RAC_FUSED_AB")) : 0u;  // tooling
   p.ab = ab;
+  // passes t > 1 testing <= 16 columns keep a change list (c3-prop 281 -> 277 us,
+  // profiles/r02v; A/B knob RAC_LIST_MAX, 0 = off)
+  static const int list_max = getenv("RAC_LIST_MAX") ? atoi(getenv("RAC_LIST_MAX")) : 16;
+  p.list_max = list_max;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));
@@ -1168,30 +1172,6 @@ int rac_enforce_async(rac_ctx* c, const uint64_t* d_in_dev, uint64_t* d_out_dev,
 
 static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags);
 
-// Blocking calls: wait for the kernel's status word in mapped host memory (the
-// kernels write D_out and the iteration count first, then the status; see
-// rac_fused / rac_state) instead of synchronising the stream, which adds the
-// driver's completion signalling to every call.  Falls back to a stream
-// synchronise for the multi-kernel paths and surfaces launch errors through
-// periodic cudaStreamQuery.
-static int wait_blocking(rac_ctx* c, volatile int32_t* status) {
-  static const bool no_poll = getenv("RAC_NO_STATUS_POLL") != nullptr;  // A/B knob (tooling only)
-  if (no_poll || c->peer || c->wide || c->use_nccl() || c->vshards > 1) {
-    CK(c, cudaStreamSynchronize(c->stream));
-    return 0;
-  }
-  for (unsigned i = 1;; ++i) {
-    if (*status != -99) return 0;
-    if ((i & 1023u) == 0u) {
-      const cudaError_t q = cudaStreamQuery(c->stream);
-      if (q == cudaSuccess) break;
-      if (q != cudaErrorNotReady) return fail(c, RAC_ECUDA, std::string("kernel: ") + cudaGetErrorString(q));
-    }
-  }
-  CK(c, cudaStreamSynchronize(c->stream));  // stream idle without a status: the checks below report it
-  return 0;
-}
-
 int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* iterations, int32_t* removed_at,
                    uint32_t flags) {
   int rc = check_usable(c);
@@ -1211,14 +1191,13 @@ int rac_enforce_ex(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* i
     rc = enqueue_blocking(c, nb, -1, flags);
   }
   if (rc) return rc;
-  if (removed_at) {
+  if (removed_at)
     CK(c, cudaMemcpyAsync(removed_at, c->buf_removed, (size_t)c->n * 64 * c->wq * 4, cudaMemcpyDeviceToHost,
                           c->stream));
-    CK(c, cudaStreamSynchronize(c->stream));
-  } else {
-    rc = wait_blocking(c, h_res + 1);
-    if (rc) return rc;
-  }
+  // (Polling the mapped status word instead was measured: the system-scope
+  // fences it needs in the kernels cost more than the synchronise saves --
+  // C1 W-seed device time 5.8 -> 9.8 us, profiles/r02u.)
+  CK(c, cudaStreamSynchronize(c->stream));
   memcpy(d_out, c->h_out, nb);
   *iterations = h_res[0];
   const int st = h_res[1];
@@ -1332,8 +1311,7 @@ int rac_enforce_seeded(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
   h_res[1] = -99;
   rc = enqueue_blocking(c, nb, n_seeds, flags);
   if (rc) return rc;
-  rc = wait_blocking(c, h_res + 1);
-  if (rc) return rc;
+  CK(c, cudaStreamSynchronize(c->stream));
   memcpy(d_out, c->h_out, nb);
   *iterations = h_res[0];
   const int st = h_res[1];
@@ -1471,12 +1449,15 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
     const char* ce = getenv("RAC_BATCH_CL");  // A/B knob (tooling only): cluster size
     int C = ce ? atoi(ce) : 4;
     C = std::max(1, std::min(C, (rows_all + 255) / 256));
+    // a thread per row: enough CTAs that a CTA's rows fit its kBatchClThreads
+    // threads (up to 16 per cluster; beyond that threads take several rows)
+    C = std::min(16, std::max(C, (rows_all + kBatchClThreads - 1) / kBatchClThreads));
     // rows per CTA: whole variables, a multiple of 4 rows (16-byte DSMEM pushes)
     const int unit = c->dmax * 4 / std::gcd(c->dmax, 4);
     int RPC = (rows_all + C - 1) / C;
     RPC = (RPC + unit - 1) / unit * unit;
     C = (rows_all + RPC - 1) / RPC;
-    const int threads = std::min(1024, (RPC + 31) / 32 * 32);
+    const int threads = std::min(kBatchClThreads, (RPC + 31) / 32 * 32);
     const size_t smem = batch_cl_smem(c->n, c->dmax, c->W);
     int maxcl = 0;
     if (smem <= 200 * 1024) CK(c, batch_cl_max_clusters(c->W, C, threads, smem, &maxcl));
@@ -1484,23 +1465,6 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       BatchCLParams b{};
       b.M = c->M;
       b.col_stride = c->col_stride;
-      b.Mr = c->Mr;
-      b.dbytes = c->dbytes;
-      // Tested-column lists over the column-major masks.  Testing every column
-      // through the row-major copy (A/B knob RAC_BATCH_FULL="num/den": when
-      // cnt * den >= n * num) measured slower at C5 even for the passes that
-      // test nearly every column (0.240 vs 0.234 ms, profiles/r02t).
-      b.Mr = nullptr;
-      b.full_num = 1;
-      b.full_den = 1;
-      if (const char* fe = getenv("RAC_BATCH_FULL")) {
-        int a = 0, d = 1;
-        if (sscanf(fe, "%d/%d", &a, &d) >= 1 && a > 0) {
-          b.Mr = c->Mr;
-          b.full_num = a;
-          b.full_den = std::max(1, d);
-        }
-      }
       b.n = c->n;
       b.dmax = c->dmax;
       b.P = c->P;

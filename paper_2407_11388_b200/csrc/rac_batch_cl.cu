@@ -23,11 +23,11 @@
 //   prep   tst / the tested-column list (warp 0) and the tables of changed
 //          columns (the other warps); then a split cluster barrier ARRIVE
 //          ("I have read everybody's rows");
-//   sweep  my rows against the tested columns: either the column list
-//          (column-major masks, one 2/4-byte load per tested column) or, when
-//          most columns are tested, every column through the row-major copy
-//          (one 16-byte load per 16/W columns); a row stops as soon as none of
-//          its live states is supported;
+//   sweep  my rows against the tested-column list (column-major masks, one
+//          2/4-byte load per tested column, 8 in flight); a row stops as soon
+//          as none of its live states is supported.  (Testing every column
+//          through the row-major copy, one 16-byte load per 16/W columns, was
+//          measured slower: a warp's 16-byte row loads touch 32 lines.)
 //   push   split barrier WAIT, then DSMEM stores of my changed rows, my change
 //          masks and my [changed, emptied] lanes into every CTA of the cluster;
 //   sync   one full cluster barrier; every CTA derives the same loop control.
@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <utility>
 
 #include "rac_internal.cuh"
@@ -45,8 +46,22 @@ namespace rac {
 
 namespace {
 
+// build-time A/B variants (tools/session scripts build them with -D)
+// (profiles/r02aa, same box: item tables 242 -> 234 us per C5 batch, global
+// staging 242 -> 240, both 232; the alternatives stay selectable with -D...=0)
+#ifndef RAC_CL_ITEM_TABLES
+#define RAC_CL_ITEM_TABLES 1  // 1: tables built one 16-entry block per thread; 0: one warp per column
+#endif
+#ifndef RAC_CL_ITEM_ROT
+#define RAC_CL_ITEM_ROT 0  // 1: item stores rotated by item index (bank-conflict-free, SEL-selected quads)
+#endif
+#ifndef RAC_CL_GLOBAL_STAGE
+#define RAC_CL_GLOBAL_STAGE 1  // 1: the word's states transposed by ballots straight from global memory;
+                               // 0: staged through shared memory by coalesced loads first
+#endif
+
 constexpr uint32_t kFullCL = 1u;  // RAC_FULL_FIXPOINT
-constexpr int kMaxT = 1024;
+constexpr int kMaxT = kBatchClThreads;
 constexpr int kMaxC = 16;
 
 // Chunk tables per mask width W: chunk q covers values [shift(q), shift(q) +
@@ -161,7 +176,36 @@ __device__ __forceinline__ uint32_t sup_lookup(uint32_t w, uint32_t cb) {
   else return s;
 }
 
-// Table item i of column y: chunk q, block bi of 16 entries.
+// The chunk tables of column y, built by one warp: lane l computes the entries
+// e = l, l + 32, ... of the column's TSB / 4 words (entry e of chunk q holds
+// OR_{bit k of v} X[(y, shift(q) + k)], v = e - off(q) / 4).  The X words are
+// read as broadcasts (every lane of a chunk reads the same address) and the
+// stores are consecutive words (conflict-free).
+template <int W>
+__device__ __forceinline__ void build_column(uint8_t* Tb, const uint32_t* X, int y, int dmax, int lane) {
+  const uint32_t* Xy = X + (size_t)y * dmax;
+  uint32_t* Ty = reinterpret_cast<uint32_t*>(Tb + (size_t)y * Lut<W>::TSB);
+#pragma unroll
+  for (int e0 = 0; e0 < Lut<W>::TSB / 4; e0 += 32) {
+    const int e = e0 + lane;
+    int q = 0;
+#pragma unroll
+    for (int qq = 1; qq < Lut<W>::NCH; ++qq)
+      if (e >= Lut<W>::off(qq) / 4) q = qq;
+    const int v = e - Lut<W>::off(q) / 4, b0 = Lut<W>::shift(q), nb = Lut<W>::bits(q);
+    uint32_t acc = 0u;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int b = b0 + k;
+      if (k < nb && b < dmax && ((v >> k) & 1)) acc |= Xy[b];
+    }
+    Ty[e] = acc;
+  }
+}
+
+#if RAC_CL_ITEM_TABLES
+// A/B variant (build-time): one thread per 16-entry block (item i of column y:
+// chunk q, block bi), the block built in registers and stored as 4 x 16 bytes.
 template <int W>
 __device__ __forceinline__ void build_item(uint8_t* Tb, const uint32_t* X, int y, int i, int dmax) {
   int q = 0, bi = i;
@@ -180,11 +224,29 @@ __device__ __forceinline__ void build_item(uint8_t* Tb, const uint32_t* X, int y
   uint32_t tv[16];
   tv[0] = hi;
 #pragma unroll
-  for (int v = 1; v < 16; ++v) tv[v] = tv[v & (v - 1)] | xb[__ffs(v) - 1];
+  for (int v = 1; v < 16; ++v) {
+    const int lb = (v & 1) ? 0 : (v & 2) ? 1 : (v & 4) ? 2 : 3;  // lowest set bit (folds; __ffs would not)
+    tv[v] = tv[v & (v - 1)] | xb[lb];
+  }
   uint4* dst = reinterpret_cast<uint4*>(Tb + (size_t)y * Lut<W>::TSB + Lut<W>::off(q) + bi * 64);
+#if RAC_CL_ITEM_ROT
+  // consecutive items are consecutive 64-byte blocks: item i stores its quads
+  // starting at quad i % 4, so one store instruction of a warp covers all banks
+  const uint4 q4[4] = {make_uint4(tv[0], tv[1], tv[2], tv[3]), make_uint4(tv[4], tv[5], tv[6], tv[7]),
+                       make_uint4(tv[8], tv[9], tv[10], tv[11]), make_uint4(tv[12], tv[13], tv[14], tv[15])};
+  const int rot = i & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int k = (j + rot) & 3;
+    const uint4 a = (k & 1) ? q4[1] : q4[0], b = (k & 1) ? q4[3] : q4[2];
+    dst[k] = (k & 2) ? b : a;
+  }
+#else
 #pragma unroll
   for (int v = 0; v < 16; v += 4) dst[v >> 2] = make_uint4(tv[v], tv[v + 1], tv[v + 2], tv[v + 3]);
+#endif
 }
+#endif
 
 template <int W>
 __device__ __forceinline__ uint32_t mask_at(const uint8_t* p) {
@@ -250,73 +312,10 @@ __device__ __forceinline__ uint32_t sweep_list(const uint8_t* __restrict__ M, co
   return my_or;
 }
 
-// Every column through the row-major copy: one 16-byte load per 16/W columns
-// (two groups per iteration, the next pair in flight); tst[] covers npad
-// columns (0 beyond n, so padding columns test no lane).
-template <int W, bool CP, int U>
-__device__ __forceinline__ void full_col(uint32_t& acc, const uint32_t (&wv)[8], uint32_t t, uint32_t cb,
-                                         uint32_t live, const uint32_t* P, int pw, int x, int y0) {
-  constexpr int MPW = 4 / W;
-  const uint32_t s = sup_lookup<W, 8 * W * (U % MPW), U * Lut<W>::TSB>(wv[U / MPW], cb);
-  apply_col<CP>(acc, s, t, live, P, pw, x, y0 + U);
-}
-template <int W, bool CP, int K4>
-__device__ __forceinline__ void full_quad(uint32_t& acc, const uint32_t (&wv)[8], const uint4* tq, uint32_t cb,
-                                          uint32_t live, const uint32_t* P, int pw, int x, int y0) {
-  const uint4 t4 = tq[K4];
-  full_col<W, CP, 4 * K4>(acc, wv, t4.x, cb, live, P, pw, x, y0);
-  full_col<W, CP, 4 * K4 + 1>(acc, wv, t4.y, cb, live, P, pw, x, y0);
-  full_col<W, CP, 4 * K4 + 2>(acc, wv, t4.z, cb, live, P, pw, x, y0);
-  full_col<W, CP, 4 * K4 + 3>(acc, wv, t4.w, cb, live, P, pw, x, y0);
-}
-template <int W, bool CP, int... K4s>
-__device__ __forceinline__ void full_cols(std::integer_sequence<int, K4s...>, uint32_t& acc, const uint32_t (&wv)[8],
-                                          const uint4* tq, uint32_t cb, uint32_t live, const uint32_t* P, int pw,
-                                          int x, int y0) {
-  (full_quad<W, CP, K4s>(acc, wv, tq, cb, live, P, pw, x, y0), ...);
-}
-
-template <int W, bool CP>
-__device__ __forceinline__ uint32_t sweep_full(const uint8_t* __restrict__ Mr, int dbytes,
-                                               const uint32_t* __restrict__ P, int pw, uint32_t* X, uint32_t tb0,
-                                               const uint32_t* tst, int npair, int ng, int r0, int r1, int dmax,
-                                               uint32_t active, uint32_t* chgn) {
-  constexpr int CPI = 32 / W;  // columns per iteration (two 16-byte groups)
-  uint32_t my_or = 0u;
-  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
-    const uint32_t cur = X[r];
-    const uint32_t live = cur & active;
-    if (!live) continue;
-    const uint4* row = reinterpret_cast<const uint4*>(Mr + (size_t)r * dbytes);
-    const int x = r / dmax;
-    uint32_t acc = 0xffffffffu;
-    const uint4 ones = make_uint4(~0u, ~0u, ~0u, ~0u);  // beyond the row: columns >= n test no lane
-    uint4 n0 = __ldg(row), n1 = ng > 1 ? __ldg(row + 1) : ones;
-    for (int g2 = 0; g2 < npair; ++g2) {
-      const uint32_t wv[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
-      if (g2 + 1 < npair) {
-        n0 = __ldg(row + 2 * g2 + 2);
-        n1 = 2 * g2 + 3 < ng ? __ldg(row + 2 * g2 + 3) : ones;
-      }
-      full_cols<W, CP>(std::make_integer_sequence<int, CPI / 4>{}, acc, wv,
-                       reinterpret_cast<const uint4*>(tst + g2 * CPI), tb0 + (uint32_t)(g2 * CPI * Lut<W>::TSB),
-                       live, P, pw, x, g2 * CPI);
-      if ((acc & live) == 0u) break;
-    }
-    const uint32_t nb = cur & (acc | ~active);
-    if (nb != cur) {
-      X[r] = nb;
-      atomicOr(&chgn[x], cur ^ nb);
-      my_or |= cur ^ nb;
-    }
-  }
-  return my_or;
-}
-
 }  // namespace
 
 // Shared memory (dynamic), byte offsets from the TSB-aligned start:
-//   Tb [npad][TSB] | X [rows4] u32 | tst [npad] u32 | chg [n4] | chgn [n4] |
+//   Tb [npad][TSB] (or the staged d_in block) | X [rows4] u32 | chg [n4] | chgn [n4] |
 //   chg_in [n4] | ctst [n + 8] u32 | ci [n + 8] uint2.
 // Cluster rank k owns rows [k*RPC, (k+1)*RPC), RPC a multiple of dmax, so
 // every variable's rows live in one CTA.
@@ -343,9 +342,9 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   const uint32_t pad = (uint32_t)(L::TSB - (base & (L::TSB - 1))) & (L::TSB - 1);
   uint8_t* Tb = cl_smem + pad;
   const uint32_t tb0 = base + pad;  // shared-memory address, TSB-aligned
-  uint32_t* X = reinterpret_cast<uint32_t*>(Tb + (size_t)npad * L::TSB);
-  uint32_t* tst = X + rows4;
-  uint32_t* chg = tst + npad;
+  const size_t tb_bytes = max((size_t)npad * L::TSB, (size_t)32 * (n + 1) * 8);  // tables / staged d_in
+  uint32_t* X = reinterpret_cast<uint32_t*>(Tb + tb_bytes);
+  uint32_t* chg = X + rows4;
   uint32_t* chgn = chg + n4;
   uint32_t* chg_in = chgn + n4;
   uint32_t* ctst = chg_in + n4;
@@ -353,8 +352,6 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   const int r0 = k * p.RPC, r1 = min(rows, r0 + p.RPC);  // my rows
   const int x0 = r0 / dmax, x1 = (r1 + dmax - 1) / dmax;  // my variables
   const bool full = (p.flags & kFullCL) != 0;
-  const bool rowmajor = p.Mr != nullptr;
-  const int ng = p.dbytes / 16, npair = npad / CPI;
   const int NW = (p.S + 31) / 32;
   // debug stamps: per word [start, staged, per pass: prep, sweep, push, sync, control], end
   int nd = 0;
@@ -376,7 +373,6 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
     // ---- the word's states -> bit slices (every CTA, all rows); lanes with an
     // empty input domain; seeds -> chg
     if (tid == 0) s_empty0 = 0u;
-    for (int y = tid; y < npad; y += T) tst[y] = 0u;
     for (int x = tid; x < n4; x += T) {
       chg[x] = 0u;
       chgn[x] = 0u;
@@ -385,6 +381,8 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       s_iters[tid] = 0;
       s_status[tid] = 0;
     }
+#if RAC_CL_GLOBAL_STAGE
+    // A/B variant (build-time): ballots straight from global memory, 4 variables in flight per warp
     __syncthreads();
     {
       uint32_t emp = 0u;
@@ -408,6 +406,42 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
           if (lane < dmax) X[x * dmax + lane] = mine;
         }
       }
+#else
+    // the word's d_in block (nst x n contiguous words) -> shared memory with
+    // coalesced loads, rows padded to n + 1 words (the transposing reads below
+    // then hit distinct banks); it lives in the table area, built afterwards
+    uint64_t* stg = reinterpret_cast<uint64_t*>(Tb);
+    {
+      const uint64_t* src = p.d_in + (size_t)s0 * n;
+      const int tot = nst * n;
+      for (int i0 = tid; i0 < tot; i0 += 8 * T) {
+        uint64_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = i0 + j * T;
+          v[j] = i < tot ? __ldg(src + i) & __ldg(p.dommask + (i % n)) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = i0 + j * T;
+          if (i < tot) stg[i + i / n] = v[j];  // row s = i / n at s * (n + 1)
+        }
+      }
+    }
+    __syncthreads();
+    {
+      uint32_t emp = 0u;
+      for (int x = warp; x < n; x += nwarps) {
+        const uint64_t v = lane < nst ? stg[(size_t)lane * (n + 1) + x] : 0ull;
+        emp |= __ballot_sync(0xffffffffu, v == 0ull);
+        uint32_t mine = 0u;
+        for (int a = 0; a < dmax; ++a) {
+          const uint32_t b = __ballot_sync(0xffffffffu, (v >> a) & 1ull);
+          if (lane == a) mine = b;
+        }
+        if (lane < dmax) X[x * dmax + lane] = mine;
+      }
+#endif
       if (lane == 0 && emp) atomicOr(&s_empty0, emp);
       uint32_t rootl = 0;
       if (tid < nst) {
@@ -443,7 +477,6 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         for (int yb = 0; yb < n; yb += 32) {
           const int y = yb + lane;
           const uint32_t ty = y < n ? chg[y] & active : 0u;
-          if (y < n) tst[y] = ty;
           const uint32_t bal = __ballot_sync(0xffffffffu, ty != 0u);
           if (ty) {
             const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
@@ -460,14 +493,25 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         if (lane == 0) s_cnt = cnt;
       }
       if (nwarps == 1) __syncwarp();
+#if RAC_CL_ITEM_TABLES
       {
+        constexpr int NI = L::TSB / 64;  // 16-entry blocks per column
         const int tb = nwarps > 1 ? tid - 32 : tid, TT = nwarps > 1 ? T - 32 : T;
         if (tb >= 0)
-          for (int i = tb; i < n * L::NI; i += TT) {
-            const int y = i / L::NI;
-            if (t == 1 || chg[y] != 0u) build_item<W>(Tb, X, y, i - y * L::NI, dmax);
+          for (int i = tb; i < n * NI; i += TT) {
+            const int y = i / NI;
+            if (t == 1 || chg[y] != 0u) build_item<W>(Tb, X, y, i - y * NI, dmax);
           }
       }
+#else
+      {
+        // one warp per rebuilt column (warps 1.. while warp 0 builds the list)
+        const int wb = nwarps > 1 ? warp - 1 : warp, NWB = nwarps > 1 ? nwarps - 1 : nwarps;
+        if (wb >= 0)
+          for (int y = wb; y < n; y += NWB)
+            if (t == 1 || chg[y] != 0u) build_column<W>(Tb, X, y, dmax, lane);
+      }
+#endif
       __syncthreads();
       const int cnt = s_cnt;
       // everybody's rows and my chg_in are read: peers may overwrite them once
@@ -476,15 +520,10 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       CL_MARK();
       // ---- sweep: my rows against the tested columns
       const bool cp = (E & active) != 0u;  // some active state has an empty domain
-      const bool use_full = rowmajor && (long)cnt * p.full_den >= (long)n * p.full_num;
-      uint32_t my_or;
-      if (use_full)
-        my_or = cp ? sweep_full<W, true>(p.Mr, p.dbytes, p.P, p.pw, X, tb0, tst, npair, ng, r0, r1, dmax, active, chgn)
-                   : sweep_full<W, false>(p.Mr, p.dbytes, p.P, p.pw, X, tb0, tst, npair, ng, r0, r1, dmax, active, chgn);
-      else
-        my_or = cp ? sweep_list<W, true>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn)
-                   : sweep_list<W, false>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn);
-      my_or = __reduce_or_sync(0xffffffffu, my_or);
+      const uint32_t my_or0 =
+          cp ? sweep_list<W, true>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn)
+             : sweep_list<W, false>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn);
+      const uint32_t my_or = __reduce_or_sync(0xffffffffu, my_or0);
       if (lane == 0 && my_or) atomicOr(&s_red[par][0], my_or);
       __syncthreads();  // my rows and change masks are final
       {
@@ -580,7 +619,8 @@ size_t batch_cl_smem(int n, int dmax, int W) {
   const size_t CPI = 32 / W;
   const size_t npad = (n + CPI - 1) / CPI * CPI, n4 = ((size_t)n + 3) & ~(size_t)3;
   const size_t rows4 = (((size_t)n * dmax) + 3) & ~(size_t)3;
-  return (size_t)TSB + npad * TSB + rows4 * 4 + npad * 4 + 3 * n4 * 4 + ((((size_t)n + 8 + 3) & ~(size_t)3) * 4) +
+  const size_t tb_bytes = std::max(npad * TSB, (size_t)32 * (n + 1) * 8);  // tables, or the staged d_in block
+  return (size_t)TSB + tb_bytes + rows4 * 4 + 3 * n4 * 4 + ((((size_t)n + 8 + 3) & ~(size_t)3) * 4) +
          ((size_t)n + 8) * 8;
 }
 

@@ -120,6 +120,7 @@ struct FusedParams {
   int n_seeds;              // < 0: root call (every column in pass 1); 0: no pass
   uint32_t flags;
   uint32_t ab;              // A/B knobs (tooling, RAC_FUSED_AB): bit 0 legacy grid barrier, bit 1 listed apply, bit 2 no removal-flag check before the R read
+  int list_max;             // dense layout: passes testing <= list_max columns keep a change list (apply reads only its R words, no compaction)
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
   // Global pass counter (persists across launches): pass t of this launch is
   // pass *seq + t; it selects the rotating buffers and is the cross-rank
@@ -203,9 +204,6 @@ cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, 
 struct BatchCLParams {
   const uint8_t* M;         // column-major masks
   size_t col_stride;
-  const uint8_t* Mr;        // nullable: row-major copy (row stride dbytes)
-  int dbytes;
-  int full_num, full_den;   // test every column through Mr when cnt * full_den >= n * full_num
   int n, dmax;
   const uint32_t* P;
   int pw;
@@ -220,6 +218,9 @@ struct BatchCLParams {
   uint32_t flags;
   unsigned long long* dbg;  // nullable (RAC_DEBUG_TIMELINE): [clusters][256] %globaltimer stamps
 };
+// CTA size cap of rac_batch_cl: 800 threads = 25 warps, so ptxas may use 80
+// registers (the software-pipelined sweep needs ~70; at 1024 threads it spilled).
+constexpr int kBatchClThreads = 800;
 size_t batch_cl_smem(int n, int dmax, int W);
 cudaError_t launch_batch_cl(int W, const BatchCLParams& p, int clusters, int C, int threads, size_t smem,
                             cudaStream_t s);

@@ -417,6 +417,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   // 239 -> 235 us but W-seed 132 -> 143 us -- so dense passes keep the
   // full-R apply; sparse W-prop 319 -> 304 us.)
   const bool use_list = G == 0 && p.clist != nullptr && !mg;
+  // dense layout: small late passes (few tested columns, so few removals) keep the
+  // change list too -- its atomics are cheap there, and the pass tail then
+  // reads only the listed R words and needs no compaction; large passes keep
+  // the full-R apply (the list's atomics cost more than they save there)
+  const bool list_ok = G > 0 && p.clist != nullptr && !mg;
   int b = (int)(base % 3ull);  // buffer of global pass base + t, advanced each pass
   int has_empty = 0;  // some D(x) empty (block-uniform)
   for (int x = threadIdx.x; x < g.n; x += blockDim.x) has_empty |= load_w<W>(Db + x * W) == 0;
@@ -451,10 +456,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (p.wctr) p.wctr[bn] = 0u;
         p.rflag[bn] = 0u;
-        if (use_list) p.clist[(size_t)bn * (g.n + 1)] = 0u;
+        if (use_list || list_ok) p.clist[(size_t)bn * (g.n + 1)] = 0u;
       }
-      uint32_t* clc = use_list ? p.clist + (size_t)b * (g.n + 1) : nullptr;  // this pass's change list
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
+      // (not pass 1: one seed column can still remove values of most variables)
+      const bool lp = use_list || (list_ok && t > 1 && vcnt <= p.list_max);  // this pass keeps a change list
+      uint32_t* clc = lp ? p.clist + (size_t)b * (g.n + 1) : nullptr;  // this pass's change list
       RAC_MARK();
       if constexpr (G == 0) {
         uint32_t* ipref = reinterpret_cast<uint32_t*>(Db + pref_offset(g.dbytes, g.n));
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       // changed = 0, wipe = "D already had an empty row", no R read.
       int changed = 0, wipe = 0;
       bool listed = false;  // vlist/vcnt already hold the next pass's columns
-      if (use_list) {
+      if (lp) {
         const int cnt = (int)__ldcg(clc);
         if (cnt == 0) {
           wipe = has_empty;
@@ -637,14 +644,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   }
   if (blockIdx.x == 0) {
     for (int x = threadIdx.x; x < g.n; x += blockDim.x) p.d_out[x] = load_w<W>(Db + x * W);
-    // status last, after D_out and iterations are visible system-wide: a blocking
-    // host call polls the mapped status word instead of synchronising the stream
-    __threadfence_system();
-    __syncthreads();
     if (threadIdx.x == 0) {
       if (emp && t > 0) *p.calls = calls0 + 1ull;  // every CTA read *calls before the first barrier
       *p.iters = t;
-      __threadfence_system();
       *p.status = (mg && *reinterpret_cast<volatile int32_t*>(p.xerr)) ? kPeerTimeout : status;
       // every CTA read *p.seq before the first barrier
       if (t > 0) *p.seq = base + (unsigned long long)t;

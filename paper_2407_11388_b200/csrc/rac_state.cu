@@ -258,13 +258,8 @@ __global__ void __launch_bounds__(T) rac_state(StateParams p) {
   RAC_SMARK();
   uint64_t* dout = p.d_out + (size_t)(p.s0 + s) * n;
   for (int x = tid; x < n; x += T) dout[x] = load_w<W>(Db + x * W);
-  // status last, after D_out and iterations are visible system-wide: a blocking
-  // host call polls the mapped status word instead of synchronising the stream
-  __threadfence_system();
-  __syncthreads();
   if (tid == 0) {
     p.iters[p.s0 + s] = t;
-    __threadfence_system();
     p.status[p.s0 + s] = status;
   }
   RAC_SMARK();
@@ -393,11 +388,8 @@ __global__ void __launch_bounds__(kTinyT) rac_tiny(StateParams p) {
     }
   }
   if (tid < n) p.d_out[(size_t)s * n + tid] = D[tid];
-  __threadfence_system();  // status last (see rac_state)
-  __syncthreads();
   if (tid == 0) {
     p.iters[s] = t;
-    __threadfence_system();
     p.status[s] = status;
   }
   RAC_TMARK();

@@ -204,7 +204,9 @@ def test_c3(rac, t, workload):
 
 def test_c3_virtual_shards(rac):
     """The sharded per-pass path (row blocks, TMA-staged D, gather by device copy)
-    gives bit-identical results for 1, 2, 3 and 8 blocks at C3 shape."""
+    at C3 shape (W-prop, 13 passes): every block count's (status, D_out, iterations,
+    removal epochs) is certified by the oracle's exact-trajectory certificate O7
+    (the recurrence's own output, pass by pass), and equals the fused path's."""
     dq, tq = synth.quant_density(1.0), synth.quant_tightness(0.70)
     ref = rac.RacContext.create_random(2000, 32, dq, tq, 1)
     root = synth.full_domains(np.full(2000, 32))
@@ -212,6 +214,7 @@ def test_c3_virtual_shards(rac):
     for v in (2, 3, 8):
         ctx = rac.RacContext.create_random(2000, 32, dq, tq, 1, virtual_shards=v)
         r = ctx.enforce(root, removed_at=True)
+        assert oracle.certify_trajectory_synth(2000, 32, dq, tq, 1, root, r[1], r[3], r[2], r[0]) == 0, v
         assert_same(r, r0, v)
 
 
@@ -524,18 +527,16 @@ def test_batched_corpus(rac):
             os.environ.pop("RAC_BATCH_IMPL", None)
 
 
-@pytest.mark.parametrize("full", ["0", "1/1000", None])
-def test_batched_sweep_modes(rac, full, monkeypatch):
-    """The cluster batch kernel's two sweeps -- tested-column lists over the column-major
-    masks (RAC_BATCH_FULL=0) and every column through the row-major copy (1/1000: nearly
-    every pass) -- and the default choice give the oracle's results: C5 dive states seeded
-    with their assigned variable (O1, the precondition holds), and seeded calls on W-rand
-    states, where the precondition of Alg. 1's seeded call does not hold, against O5
-    (tensorAC(Vars, @changed = seeds) as written): every state follows its own
-    Alg. 1 trajectory, not the union of its word's columns."""
+def test_batched_exact_columns(rac):
+    """The cluster batch kernel tests, per state, only the columns that changed for
+    that state (Alg. 1's Cons[:, @changed]): C5 dive states seeded with their
+    assigned variable (O1, the seeded call's precondition holds), and seeded calls on
+    W-rand states, where the precondition does not hold, against O5
+    (tensorAC(Vars, @changed = seeds) as written) -- every state follows its own
+    Alg. 1 trajectory, not the union of its word's columns; plus a corpus with every
+    mask width (d up to 32, W = 1, 2, 4)."""
     import torch
-    if full is not None:
-        monkeypatch.setenv("RAC_BATCH_FULL", full)
+    full = None
     n, d, S = 200, 16, 512
     inst = synth.random_csp(n, d, 0.8, 0.3, 1)
     orc = oracle.Oracle.from_instance(inst)
