@@ -76,6 +76,7 @@ struct rac_ctx {
   int n = 0, dmax = 0, W = 0;
   int rows_pad = 0;        // local rows padded to a warp slab
   size_t col_stride = 0;   // bytes per column of the mask tensor
+  uint8_t* Mg = nullptr;   // batched mode: 8-byte column groups of the mask tensor (built on first use)
   int dbytes = 0;          // bytes of D in smem
   int x_lo = 0, x_hi = 0, blk = 0;
   int pw = 0;
@@ -236,6 +237,7 @@ void free_ctx(rac_ctx* c) {
     if (c->peer_ipc[q]) cudaIpcCloseMemHandle(c->peer_base[q]);
   cudaFree(c->M);
   cudaFree(c->Mr);
+  cudaFree(c->Mg);
   cudaFree(c->S);
   cudaFree(c->s_off);
   cudaFree(c->s_arc);
@@ -1465,6 +1467,24 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       BatchCLParams b{};
       b.M = c->M;
       b.col_stride = c->col_stride;
+      // Per-column masks by default.  A/B knob RAC_CL_GROUPS=1: 8-byte column
+      // groups (one coalesced 8-byte load per row tests 8/W columns), built from
+      // the column-major tensor on the first such call -- measured slower at C5
+      // (242 vs 232 us, profiles/r02ac: the heavy sweeps gain 3 %, the light
+      // passes lose more testing whole groups for one listed column).
+      const bool no_groups = !(getenv("RAC_CL_GROUPS") && atoi(getenv("RAC_CL_GROUPS")) == 1);  // per call
+      const int cpg = 8 / c->W, ngr = (c->n + cpg - 1) / cpg;
+      const size_t gbytes = (size_t)ngr * c->rows_pad * 8;
+      if (!no_groups && !c->Mg && gbytes <= ((size_t)1 << 30)) {
+        if (cudaMalloc(&c->Mg, gbytes) != cudaSuccess) {
+          cudaGetLastError();
+          c->Mg = nullptr;
+        } else {
+          CK(c, launch_pack_groups(c->M, c->col_stride, c->n, c->W, c->rows_pad, c->Mg, st));
+        }
+      }
+      b.Mg = no_groups ? nullptr : c->Mg;
+      b.gstride = (size_t)c->rows_pad * 8;
       b.n = c->n;
       b.dmax = c->dmax;
       b.P = c->P;

@@ -312,11 +312,76 @@ __device__ __forceinline__ uint32_t sweep_list(const uint8_t* __restrict__ M, co
   return my_or;
 }
 
+// Listed column GROUPS (column-group layout Mg: one 8-byte load per row gives
+// the masks of the 8/W columns g*8/W ..): cgrp[k] = the group, gtst[k*CPG + j]
+// = the lanes that test its column j (0: the column is not tested -- a
+// warp-uniform skip).  The list is padded to a multiple of 4 with groups that
+// test nothing.
+template <int W, bool CP, int J>
+__device__ __forceinline__ void group_col(uint32_t& acc, uint2 mv, uint32_t t, uint32_t cb, uint32_t live,
+                                          const uint32_t* P, int pw, int x, int y0) {
+  if (!t) return;
+  constexpr int MPW = 4 / W;  // masks per 32-bit word
+  const uint32_t w = (J / MPW) == 0 ? mv.x : mv.y;
+  const uint32_t s = sup_lookup<W, 8 * W * (J % MPW), J * Lut<W>::TSB>(w, cb);
+  apply_col<CP>(acc, s, t, live, P, pw, x, y0 + J);
+}
+template <int W, bool CP, int... Js>
+__device__ __forceinline__ void group_cols(std::integer_sequence<int, Js...>, uint32_t& acc, uint2 mv,
+                                           const uint32_t* tq, uint32_t cb, uint32_t live, const uint32_t* P,
+                                           int pw, int x, int y0) {
+  (group_col<W, CP, Js>(acc, mv, tq[Js], cb, live, P, pw, x, y0), ...);
+}
+
+template <int W, bool CP>
+__device__ __forceinline__ uint32_t sweep_groups(const uint8_t* __restrict__ Mg, size_t gstride,
+                                                 const uint32_t* __restrict__ P, int pw, uint32_t* X, uint32_t tb0,
+                                                 const uint32_t* cgrp, const uint32_t* gtst, int gcnt4, int r0,
+                                                 int r1, int dmax, uint32_t active, uint32_t* chgn) {
+  constexpr int CPG = 8 / W;
+  uint32_t my_or = 0u;
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
+    const uint32_t cur = X[r];
+    const uint32_t live = cur & active;
+    if (!live) continue;
+    const uint8_t* Mrow = Mg + (size_t)r * 8;
+    const int x = r / dmax;
+    uint32_t acc = 0xffffffffu;
+    for (int g0 = 0; g0 < gcnt4 && (acc & live) != 0u; g0 += 4) {
+      const uint4 g4 = *reinterpret_cast<const uint4*>(cgrp + g0);
+      const uint32_t gi[4] = {g4.x, g4.y, g4.z, g4.w};
+      uint2 mv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) mv[u] = __ldg(reinterpret_cast<const uint2*>(Mrow + (size_t)gi[u] * gstride));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t tq[CPG];
+#pragma unroll
+        for (int j = 0; j < CPG; j += 2) {
+          const uint2 t2 = *reinterpret_cast<const uint2*>(gtst + (g0 + u) * CPG + j);
+          tq[j] = t2.x;
+          tq[j + 1] = t2.y;
+        }
+        group_cols<W, CP>(std::make_integer_sequence<int, CPG>{}, acc, mv[u], tq,
+                          tb0 + gi[u] * (uint32_t)(CPG * Lut<W>::TSB), live, P, pw, x, (int)gi[u] * CPG);
+      }
+    }
+    const uint32_t nb = cur & (acc | ~active);
+    if (nb != cur) {
+      X[r] = nb;
+      atomicOr(&chgn[x], cur ^ nb);
+      my_or |= cur ^ nb;
+    }
+  }
+  return my_or;
+}
+
 }  // namespace
 
 // Shared memory (dynamic), byte offsets from the TSB-aligned start:
 //   Tb [npad][TSB] (or the staged d_in block) | X [rows4] u32 | chg [n4] | chgn [n4] |
-//   chg_in [n4] | ctst [n + 8] u32 | ci [n + 8] uint2.
+//   chg_in [n4] | ctst [n + 8] u32 | ci [n + 8] uint2 | gtst [(ng + 4) * 8/W] u32 |
+//   cgrp [ng + 4] u32  (ng = column groups).
 // Cluster rank k owns rows [k*RPC, (k+1)*RPC), RPC a multiple of dmax, so
 // every variable's rows live in one CTA.
 extern __shared__ __align__(16) uint8_t cl_smem[];
@@ -349,6 +414,11 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   uint32_t* chg_in = chgn + n4;
   uint32_t* ctst = chg_in + n4;
   uint2* ci = reinterpret_cast<uint2*>(ctst + ((n + 8 + 3) & ~3));
+  constexpr int CPG = 8 / W;  // columns per 8-byte group
+  const int ngr = (n + CPG - 1) / CPG;
+  uint32_t* gtst = reinterpret_cast<uint32_t*>(ci + ((n + 8 + 1) & ~1));          // 16-byte aligned
+  uint32_t* cgrp = gtst + (((size_t)(ngr + 4) * CPG + 3) & ~(size_t)3);          // 16-byte aligned
+  const bool groups = p.Mg != nullptr;
   const int r0 = k * p.RPC, r1 = min(rows, r0 + p.RPC);  // my rows
   const int x0 = r0 / dmax, x1 = (r1 + dmax - 1) / dmax;  // my variables
   const bool full = (p.flags & kFullCL) != 0;
@@ -472,7 +542,35 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         s_red[par][0] = 0u;
         s_red[par][1] = 0u;
       }
-      if (warp == 0) {
+      if (warp == 0 && groups) {
+        // lane = one column group: listed when one of its columns is tested
+        int cnt = 0;
+        for (int gb = 0; gb < ngr; gb += 32) {
+          const int g = gb + lane;
+          uint32_t tj[CPG], any = 0u;
+#pragma unroll
+          for (int j = 0; j < CPG; ++j) {
+            const int y = g * CPG + j;
+            tj[j] = (g < ngr && y < n) ? chg[y] & active : 0u;
+            any |= tj[j];
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, any != 0u);
+          if (any) {
+            const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
+            cgrp[pos] = (uint32_t)g;
+#pragma unroll
+            for (int j = 0; j < CPG; ++j) gtst[pos * CPG + j] = tj[j];
+          }
+          cnt += __popc(bal);
+        }
+        const int cnt4 = (cnt + 3) & ~3;
+        if (cnt + lane < cnt4) {  // padding: tests nothing
+          cgrp[cnt + lane] = 0u;
+#pragma unroll
+          for (int j = 0; j < CPG; ++j) gtst[(cnt + lane) * CPG + j] = 0u;
+        }
+        if (lane == 0) s_cnt = cnt;
+      } else if (warp == 0) {
         int cnt = 0;
         for (int yb = 0; yb < n; yb += 32) {
           const int y = yb + lane;
@@ -520,9 +618,15 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       CL_MARK();
       // ---- sweep: my rows against the tested columns
       const bool cp = (E & active) != 0u;  // some active state has an empty domain
-      const uint32_t my_or0 =
-          cp ? sweep_list<W, true>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn)
-             : sweep_list<W, false>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn);
+      uint32_t my_or0;
+      if (groups)
+        my_or0 = cp ? sweep_groups<W, true>(p.Mg, p.gstride, p.P, p.pw, X, tb0, cgrp, gtst, (cnt + 3) & ~3, r0, r1,
+                                            dmax, active, chgn)
+                    : sweep_groups<W, false>(p.Mg, p.gstride, p.P, p.pw, X, tb0, cgrp, gtst, (cnt + 3) & ~3, r0, r1,
+                                             dmax, active, chgn);
+      else
+        my_or0 = cp ? sweep_list<W, true>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn)
+                    : sweep_list<W, false>(p.M, p.P, p.pw, X, tb0, ci, ctst, (cnt + 7) & ~7, r0, r1, dmax, active, chgn);
       const uint32_t my_or = __reduce_or_sync(0xffffffffu, my_or0);
       if (lane == 0 && my_or) atomicOr(&s_red[par][0], my_or);
       __syncthreads();  // my rows and change masks are final
@@ -621,7 +725,38 @@ size_t batch_cl_smem(int n, int dmax, int W) {
   const size_t rows4 = (((size_t)n * dmax) + 3) & ~(size_t)3;
   const size_t tb_bytes = std::max(npad * TSB, (size_t)32 * (n + 1) * 8);  // tables, or the staged d_in block
   return (size_t)TSB + tb_bytes + rows4 * 4 + 3 * n4 * 4 + ((((size_t)n + 8 + 3) & ~(size_t)3) * 4) +
-         ((size_t)n + 8) * 8;
+         (((size_t)n + 8 + 1) & ~(size_t)1) * 8 +
+         ((((size_t)n + 8 / W - 1) / (8 / W) + 4) * (8 / W) + 3) / 4 * 16 + (((size_t)n + 8 / W - 1) / (8 / W) + 4) * 4;
+}
+
+// Column groups for the batched sweep: Mg[g][r] = the 8 bytes of masks of columns
+// g*8/W .. g*8/W + 8/W - 1 at row r (columns >= n: all ones -- never tested).
+__global__ void pack_groups_kernel(const uint8_t* __restrict__ M, size_t col_stride, int n, int W, int rows_pad,
+                                   uint8_t* __restrict__ Mg) {
+  const int cpg = 8 / W, ngr = (n + cpg - 1) / cpg;
+  const size_t total = (size_t)ngr * rows_pad;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i / rows_pad), r = (int)(i - (size_t)g * rows_pad);
+    uint8_t b[8];
+    for (int j = 0; j < cpg; ++j) {
+      const int y = g * cpg + j;
+      for (int k = 0; k < W; ++k) b[j * W + k] = y < n ? M[(size_t)y * col_stride + (size_t)r * W + k] : 0xFF;
+    }
+    uint2 v;
+    v.x = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+    v.y = (uint32_t)b[4] | ((uint32_t)b[5] << 8) | ((uint32_t)b[6] << 16) | ((uint32_t)b[7] << 24);
+    *reinterpret_cast<uint2*>(Mg + i * 8) = v;
+  }
+}
+
+cudaError_t launch_pack_groups(const uint8_t* M, size_t col_stride, int n, int W, int rows_pad, uint8_t* Mg,
+                               cudaStream_t s) {
+  if (W != 1 && W != 2 && W != 4) return cudaErrorInvalidValue;
+  const int cpg = 8 / W;
+  const size_t total = (size_t)((n + cpg - 1) / cpg) * rows_pad;
+  const int blocks = (int)std::min<size_t>(4096, (total + 255) / 256);
+  pack_groups_kernel<<<blocks, 256, 0, s>>>(M, col_stride, n, W, rows_pad, Mg);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_batch_cl(int W, const BatchCLParams& p, int clusters, int C, int threads, size_t smem,

@@ -204,6 +204,8 @@ cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, 
 struct BatchCLParams {
   const uint8_t* M;         // column-major masks
   size_t col_stride;
+  const uint8_t* Mg;        // nullable: 8-byte column groups, Mg + g*gstride + r*8 = masks of columns g*8/W.. of row r
+  size_t gstride;
   int n, dmax;
   const uint32_t* P;
   int pw;
@@ -222,6 +224,8 @@ struct BatchCLParams {
 // registers (the software-pipelined sweep needs ~70; at 1024 threads it spilled).
 constexpr int kBatchClThreads = 800;
 size_t batch_cl_smem(int n, int dmax, int W);
+cudaError_t launch_pack_groups(const uint8_t* M, size_t col_stride, int n, int W, int rows_pad, uint8_t* Mg,
+                               cudaStream_t s);
 cudaError_t launch_batch_cl(int W, const BatchCLParams& p, int clusters, int C, int threads, size_t smem,
                             cudaStream_t s);
 cudaError_t batch_cl_max_clusters(int W, int C, int threads, size_t smem, int* out);

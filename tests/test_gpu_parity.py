@@ -527,7 +527,8 @@ def test_batched_corpus(rac):
             os.environ.pop("RAC_BATCH_IMPL", None)
 
 
-def test_batched_exact_columns(rac):
+@pytest.mark.parametrize("groups", ["1", "0"])
+def test_batched_exact_columns(rac, groups, monkeypatch):
     """The cluster batch kernel tests, per state, only the columns that changed for
     that state (Alg. 1's Cons[:, @changed]): C5 dive states seeded with their
     assigned variable (O1, the seeded call's precondition holds), and seeded calls on
@@ -536,7 +537,7 @@ def test_batched_exact_columns(rac):
     Alg. 1 trajectory, not the union of its word's columns; plus a corpus with every
     mask width (d up to 32, W = 1, 2, 4)."""
     import torch
-    full = None
+    monkeypatch.setenv("RAC_CL_GROUPS", groups)  # 8-byte column-group loads (A/B path), or per-column masks
     n, d, S = 200, 16, 512
     inst = synth.random_csp(n, d, 0.8, 0.3, 1)
     orc = oracle.Oracle.from_instance(inst)
@@ -569,7 +570,7 @@ def test_batched_exact_columns(rac):
             e = orc.rac(states[s], with_epochs=False)
         else:
             e = orc.rac_seeded(states[s], [int(seeds[s])], with_epochs=False)
-        assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (s, seeds[s], full)
+        assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (s, seeds[s], groups)
     for k, inst in enumerate(I.random_corpus(30, seed0=191, n_range=(2, 40), d_range=(1, 32))):
         orc = oracle.Oracle.from_instance(inst)
         S2 = int(rng.integers(1, 80))
@@ -587,7 +588,7 @@ def test_batched_exact_columns(rac):
         for s in range(S2):
             e = (orc.rac(st2[s], with_epochs=False) if sd2[s] < 0
                  else orc.rac_seeded(st2[s], [int(sd2[s])], with_epochs=False))
-            assert (st_h[s], it_h[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (k, s, full)
+            assert (st_h[s], it_h[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (k, s, groups)
 
 
 def test_nccl_exchange_leg_single_rank(rac):
