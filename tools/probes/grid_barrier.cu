@@ -72,7 +72,7 @@ int main() {
   unsigned long long* out;
   cudaMalloc(&bar, 32 * 32 * 4);
   cudaMalloc(&out, 64);
-  for (int grid : {148, 296, 592}) {
+  for (int grid : {8, 16, 32, 64, 148, 296, 592}) {
     for (int mode = 0; mode < 3; ++mode) {
       for (int K : {4, 8, 16}) {
         if (mode != 1 && K != 8) continue;
