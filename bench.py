@@ -485,7 +485,7 @@ def run_gpu(args, rank, world, local_rank):
                     "algorithmic_tests_per_launch": instr["support_tests"],
                     "tests_per_s": round(instr["support_tests"] / (kern_ms / 1e3), 1), "peak_source": src}
     if kind == "dive":
-        # Bit-sliced batched pass (rac_batch_bs): a support test of (x,a) against
+        # Bit-sliced batched pass (rac_batch_cl; rac_batch_bs in r01): a support test of (x,a) against
         # c_xy for 32 states is ceil(d/4) nibble-table lookups in shared memory;
         # the LDS issue rate (32 lanes x 4 B per clock per SM) bounds it:
         #   peak = 148 SM x 32 lookups/clk x f_max / ceil(d/4) x 32 states
@@ -499,7 +499,7 @@ def run_gpu(args, rank, world, local_rank):
         ach_t = instr["support_tests"] / (kern_ms / 1e3) / 1e12
         roofline = {"bound": "alu", "achieved": round(ach_t, 4), "peak": round(peak_t, 2),
                     "unit": "T support-tests/s (x,a,y,state)", "frac": round(ach_t / peak_t, 4),
-                    "traffic": None, "kernel": "rac_batch_bs",
+                    "traffic": None, "kernel": "rac_batch_cl",
                     "algorithmic_tests_per_launch": instr["support_tests"], "launch_ms_median": round(kern_ms, 5),
                     "peak_source": "derived: LDS lookups (148 SM x 32/clk x %.0f MHz) / ceil(d/4) lookups per "
                                    "32-state test; DESIGN.md section 7" % sm_mhz}
