@@ -77,6 +77,7 @@ struct rac_ctx {
   int rows_pad = 0;        // local rows padded to a warp slab
   size_t col_stride = 0;   // bytes per column of the mask tensor
   uint8_t* Mg = nullptr;   // batched mode: 8-byte column groups of the mask tensor (built on first use)
+  unsigned* cctr = nullptr;  // partitioned tail-claim counters of the column sweep [3][32][32]
   int dbytes = 0;          // bytes of D in smem
   int x_lo = 0, x_hi = 0, blk = 0;
   int pw = 0;
@@ -238,6 +239,7 @@ void free_ctx(rac_ctx* c) {
   cudaFree(c->M);
   cudaFree(c->Mr);
   cudaFree(c->Mg);
+  cudaFree(c->cctr);
   cudaFree(c->S);
   cudaFree(c->s_off);
   cudaFree(c->s_arc);
@@ -406,6 +408,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
   c->R3 = reinterpret_cast<unsigned long long*>(c->xr);
   if (c->rank < RAC_MAX_RANKS) c->peer_base[c->rank] = c->xr;
   CKC(cudaMalloc(&c->clist, (size_t)3 * (n + 1) * 4));
+  CKC(cudaMalloc(&c->cctr, (size_t)3 * 32 * 32 * 4));
+  CKC(cudaMemsetAsync(c->cctr, 0, (size_t)3 * 32 * 32 * 4, c->stream));
   CKC(cudaMemsetAsync(c->clist, 0, (size_t)3 * (n + 1) * 4, c->stream));
   CKC(cudaMalloc(&c->bar, 64));
   CKC(cudaMemsetAsync(c->bar, 0, 64, c->stream));  // [0..3] grid barrier, [4..6] row counters, [12] peer error
@@ -733,6 +737,8 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   // profiles/r02v; A/B knob RAC_LIST_MAX, 0 = off)
   static const int list_max = getenv("RAC_LIST_MAX") ? atoi(getenv("RAC_LIST_MAX")) : 16;
   p.list_max = list_max;
+  static const bool no_cclaim = getenv("RAC_NO_CCLAIM") != nullptr;  // A/B knob (tooling only)
+  p.cctr = no_cclaim ? nullptr : c->cctr;
   p.seeds = seeds;
   p.n_seeds = n_seeds;
   if (getenv("RAC_DEBUG_TIMELINE") && !c->dbg) CK(c, cudaMalloc(&c->dbg, (256 + 3000) * 8));

@@ -107,6 +107,41 @@ struct ItemIter {
   }
 };
 
+// Partitioned tail claims (RAC_COL_CLAIM == 2, A/B): the last 1/kClaimDiv of a
+// pass's items is split into kClaimParts contiguous partitions, each with its
+// own counter on its own 128-byte line (ctr[j * 32]); a warp claims from
+// partition warp0 % kClaimParts and moves to the next one when it runs dry, so
+// each counter sees ~1/kClaimParts of the warps (one same-address counter for
+// every warp serialised the tail: profiles/r02f).  Lane 0 claims; returns the
+// item or ~0u when every partition is exhausted.
+#ifndef RAC_CLAIM_PARTS
+#define RAC_CLAIM_PARTS 32
+#endif
+constexpr uint32_t kClaimParts = RAC_CLAIM_PARTS;
+struct TailClaim {
+  uint32_t S, L, items, part, tries;
+  unsigned* ctr;
+  __device__ __forceinline__ TailClaim(uint32_t S_, uint32_t items_, uint32_t warp0, unsigned* ctr_)
+      : S(S_), L((items_ - S_ + kClaimParts - 1) / kClaimParts), items(items_), part(warp0 % kClaimParts),
+        tries(0), ctr(ctr_) {}
+  __device__ __noinline__ uint32_t claim() {
+    uint32_t r = ~0u, tr = tries;
+    if ((threadIdx.x & 31) == 0) {
+      while (tr < kClaimParts) {
+        const uint32_t j = (part + tr) % kClaimParts;
+        const uint32_t b = S + j * L, e = min(items, b + L);
+        if (b < e) {
+          const uint32_t i = atomicAdd(ctr + j * 32, 1u);
+          if (b + i < e) { r = b + i; break; }
+        }
+        ++tr;
+      }
+    }
+    tries = __shfl_sync(0xffffffffu, tr, 0);
+    return __shfl_sync(0xffffffffu, r, 0);
+  }
+};
+
 // Column sweep: test the rows of variables [g.x_lo, g.x_hi) against the
 // columns cols[0, ncol) (cols == nullptr: columns 0..ncol-1) and OR removals
 // into R.  Work item = (tested column y, chunk of 32 x kUnrollC consecutive
@@ -122,7 +157,7 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
                                           int32_t* removed_at, int t, long warp0, long nwarps,
                                           const uint16_t* cols, int ncol, unsigned* rflag = nullptr,
                                           unsigned* wctr = nullptr, uint32_t* cl = nullptr,
-                                          const EpochMirror* em = nullptr) {
+                                          const EpochMirror* em = nullptr, unsigned* cctr = nullptr) {
   constexpr int RPL = 16 / W, U = kUnroll;
   const int lane = threadIdx.x & 31;
   const int r_lo = (g.x_lo - g.x_lo_alloc) * g.dmax;
@@ -136,8 +171,30 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
   const uint32_t upl = upl64 < 1ull ? 1u : (upl64 > (uint64_t)U ? (uint32_t)U : (uint32_t)upl64);
   const uint32_t ipc = (v_hi - v_lo + 32u * upl - 1u) / (32u * upl);  // items per column
   const uint32_t items = ipc * (uint32_t)ncol;
+#if RAC_COL_CLAIM == 2
+  // static round robin for the first items, then partitioned claims (cctr)
+  const uint32_t per = cctr ? (items - items / kClaimDiv) / (uint32_t)nwarps
+                            : (items + (uint32_t)nwarps - 1) / (uint32_t)nwarps;
+  const uint32_t Sst = cctr ? per * (uint32_t)nwarps : items;
+  TailClaim tc(Sst, items, (uint32_t)warp0, cctr);
+  uint32_t kk = 0, pend = (cctr && per == 0) ? tc.claim() : ~0u;
+  for (;;) {
+    uint32_t it;
+    if (kk < per) {
+      it = (uint32_t)warp0 + kk * (uint32_t)nwarps;
+      if (++kk == per && cctr) pend = tc.claim();
+      if (it >= Sst) continue;
+    } else if (cctr) {
+      if (pend == ~0u) break;
+      it = pend;
+      pend = tc.claim();
+    } else {
+      break;
+    }
+#else
   ItemIter iter(items, warp0, nwarps, wctr);
   for (uint32_t it; iter.next(it);) {
+#endif
     const uint32_t c = it / ipc, chunk = it - c * ipc;
     const int y = cols ? (int)cols[c] : (int)c;
     const uint4* col = reinterpret_cast<const uint4*>(g.M + (size_t)y * g.col_stride);
@@ -458,6 +515,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
         p.rflag[bn] = 0u;
         if (use_list || list_ok) p.clist[(size_t)bn * (g.n + 1)] = 0u;
       }
+      if (p.cctr && blockIdx.x == 0 && threadIdx.x < kClaimParts) p.cctr[((size_t)bn * kClaimParts + threadIdx.x) * 32] = 0u;
       const bool lst = seeded || t > 1;  // pass 1 of a root call tests every column
       // (not pass 1: one seed column can still remove values of most variables)
       const bool lp = use_list || (list_ok && t > 1 && vcnt <= p.list_max);  // this pass keeps a change list
@@ -480,7 +538,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
                           clc, emp);
         else
           column_sweep<W>(g, Db, Rc, ep, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
-                          p.rflag + b, (RAC_COL_CLAIM && p.wctr) ? p.wctr + b : nullptr, clc, emp);
+                          p.rflag + b, (RAC_COL_CLAIM == 1 && p.wctr) ? p.wctr + b : nullptr, clc, emp,
+                          p.cctr ? p.cctr + (size_t)b * kClaimParts * 32 : nullptr);
       }
       RAC_MARK();
       if (p.dbg != nullptr && t == 1) {  // block-uniform condition: the barrier is safe
