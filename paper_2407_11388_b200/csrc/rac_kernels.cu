@@ -107,37 +107,35 @@ struct ItemIter {
   }
 };
 
+// (Measured, profiles/r02ag, same box: C3 W-stream 110.4 -> 107.5-108.4 us, but
+// C2 14.3 -> 16.1 us, C3 W-prop 275 -> 280 us and C4 W-stream 5.7 -> 6.7 ms: off.)
 // Partitioned tail claims (RAC_COL_CLAIM == 2, A/B): the last 1/kClaimDiv of a
 // pass's items is split into kClaimParts contiguous partitions, each with its
-// own counter on its own 128-byte line (ctr[j * 32]); a warp claims from
-// partition warp0 % kClaimParts and moves to the next one when it runs dry, so
-// each counter sees ~1/kClaimParts of the warps (one same-address counter for
-// every warp serialised the tail: profiles/r02f).  Lane 0 claims; returns the
-// item or ~0u when every partition is exhausted.
+// own counter on its own 128-byte line (ctr[j * 32]); a warp claims only from
+// partition warp0 % kClaimParts (every partition has ~nwarps/kClaimParts warps,
+// so each is drained by its own warps; walking the other partitions to detect
+// the end cost one atomic round trip per partition -- c2 14 -> 30 us,
+// profiles/r02af).  One same-address counter for every warp serialised the
+// tail (profiles/r02f).  Lane 0 claims; returns the item or ~0u.
 #ifndef RAC_CLAIM_PARTS
 #define RAC_CLAIM_PARTS 32
 #endif
 constexpr uint32_t kClaimParts = RAC_CLAIM_PARTS;
 struct TailClaim {
-  uint32_t S, L, items, part, tries;
+  uint32_t b, e;
   unsigned* ctr;
-  __device__ __forceinline__ TailClaim(uint32_t S_, uint32_t items_, uint32_t warp0, unsigned* ctr_)
-      : S(S_), L((items_ - S_ + kClaimParts - 1) / kClaimParts), items(items_), part(warp0 % kClaimParts),
-        tries(0), ctr(ctr_) {}
-  __device__ __noinline__ uint32_t claim() {
-    uint32_t r = ~0u, tr = tries;
-    if ((threadIdx.x & 31) == 0) {
-      while (tr < kClaimParts) {
-        const uint32_t j = (part + tr) % kClaimParts;
-        const uint32_t b = S + j * L, e = min(items, b + L);
-        if (b < e) {
-          const uint32_t i = atomicAdd(ctr + j * 32, 1u);
-          if (b + i < e) { r = b + i; break; }
-        }
-        ++tr;
-      }
+  __device__ __forceinline__ TailClaim(uint32_t S, uint32_t items, uint32_t warp0, unsigned* ctr_) {
+    const uint32_t L = (items - S + kClaimParts - 1) / kClaimParts, j = warp0 % kClaimParts;
+    b = S + j * L;
+    e = min(items, b + L);
+    ctr = ctr_ + j * 32;
+  }
+  __device__ __forceinline__ uint32_t claim() {
+    uint32_t r = ~0u;
+    if ((threadIdx.x & 31) == 0 && b < e) {
+      const uint32_t i = atomicAdd(ctr, 1u);
+      if (b + i < e) r = b + i;
     }
-    tries = __shfl_sync(0xffffffffu, tr, 0);
     return __shfl_sync(0xffffffffu, r, 0);
   }
 };
