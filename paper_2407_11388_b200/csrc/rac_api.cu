@@ -1250,10 +1250,13 @@ static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags) 
                          : c->buf_seeds)
                    : nullptr;
   const size_t bytes = nb + (size_t)std::max(0, n_seeds) * 4;
+  static const bool stage_kernel = getenv("RAC_BLOCKING_STAGE_KERNEL") != nullptr;  // A/B knob (tooling only)
   auto enqueue = [&]() -> int {
     if (!zc) {
-      cudaError_t e = cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream);
-      if (e != cudaSuccess) return fail(c, RAC_ECUDA, std::string("cudaMemcpyAsync: ") + cudaGetErrorString(e));
+      // (bytes is a multiple of 4: 8-byte words, then 4-byte seeds)
+      cudaError_t e = stage_kernel ? launch_stage_copy(c->h_in, c->buf_in, bytes, c->stream)
+                                   : cudaMemcpyAsync(c->buf_in, c->h_in, bytes, cudaMemcpyHostToDevice, c->stream);
+      if (e != cudaSuccess) return fail(c, RAC_ECUDA, std::string("input staging: ") + cudaGetErrorString(e));
     }
     return enforce_async_impl(c, din, c->d_hout, d_res, d_res + 1, nullptr, flags, c->stream, seeds, n_seeds);
   };

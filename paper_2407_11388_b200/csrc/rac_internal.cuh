@@ -200,6 +200,9 @@ cudaError_t launch_state(int W, int T, const StateParams& p, int n_states, size_
 // rac_tiny: one warp per state for n <= 64 (the mask tensor in shared memory)
 size_t tiny_smem(int n, size_t col_stride);
 cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, cudaStream_t s);
+// Blocking calls: copy the pinned host staging (d_in | seeds) into device memory
+// with one small kernel reading host memory (instead of a copy-engine transfer).
+cudaError_t launch_stage_copy(const void* host_src, void* dev_dst, size_t bytes, cudaStream_t s);
 
 // rac_batch_cl (rac_batch_cl.cu): one 32-state bit-sliced word per cluster.
 struct BatchCLParams {

@@ -414,6 +414,32 @@ struct LaunchS {
 
 size_t tiny_smem(int n, size_t col_stride) { return (((size_t)n * col_stride + 15) & ~(size_t)15) + 3 * 64 * 8; }
 
+// One block; 16-byte loads of pinned host memory, all in flight at once (the
+// staging is 16-byte aligned and padded: d_in words then the seeds).
+__global__ void __launch_bounds__(512) stage_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                         uint32_t n16, const uint32_t* __restrict__ tsrc,
+                                                         uint32_t* __restrict__ tdst, uint32_t ntail) {
+  for (uint32_t i0 = threadIdx.x; i0 < n16; i0 += 4 * blockDim.x) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k * blockDim.x < n16) v[k] = src[i0 + k * blockDim.x];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i0 + k * blockDim.x < n16) dst[i0 + k * blockDim.x] = v[k];
+  }
+  if (threadIdx.x < ntail) tdst[threadIdx.x] = tsrc[threadIdx.x];
+}
+
+cudaError_t launch_stage_copy(const void* host_src, void* dev_dst, size_t bytes, cudaStream_t s) {
+  if (((uintptr_t)host_src | (uintptr_t)dev_dst) & 15) return cudaErrorInvalidValue;
+  const uint32_t n16 = (uint32_t)(bytes / 16), ntail = (uint32_t)((bytes - (size_t)n16 * 16) / 4);
+  stage_copy_kernel<<<1, 512, 0, s>>>(reinterpret_cast<const uint4*>(host_src), reinterpret_cast<uint4*>(dev_dst),
+                                      n16, reinterpret_cast<const uint32_t*>(host_src) + n16 * 4,
+                                      reinterpret_cast<uint32_t*>(dev_dst) + n16 * 4, ntail);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tiny(int W, const StateParams& p, int n_states, size_t smem, cudaStream_t st) {
   const void* k = W == 1 ? (const void*)rac_tiny<1> : W == 2 ? (const void*)rac_tiny<2> : W == 4 ? (const void*)rac_tiny<4>
                                                                                                   : (const void*)rac_tiny<8>;
