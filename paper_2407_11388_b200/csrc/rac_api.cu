@@ -1250,7 +1250,10 @@ static int enqueue_blocking(rac_ctx* c, size_t nb, int n_seeds, uint32_t flags) 
                          : c->buf_seeds)
                    : nullptr;
   const size_t bytes = nb + (size_t)std::max(0, n_seeds) * 4;
-  static const bool stage_kernel = getenv("RAC_BLOCKING_STAGE_KERNEL") != nullptr;  // A/B knob (tooling only)
+  // d_in (+ seeds) reach device memory through a one-block kernel reading the
+  // pinned staging: C3 W-stream blocking call 128.4 -> 122.7 us against the
+  // copy-engine transfer (profiles/r02aj; A/B knob RAC_BLOCKING_COPY_ENGINE)
+  static const bool stage_kernel = getenv("RAC_BLOCKING_COPY_ENGINE") == nullptr;
   auto enqueue = [&]() -> int {
     if (!zc) {
       // (bytes is a multiple of 4: 8-byte words, then 4-byte seeds)

@@ -527,6 +527,38 @@ def test_batched_corpus(rac):
             os.environ.pop("RAC_BATCH_IMPL", None)
 
 
+def test_c5_batched_many_words(rac):
+    """More words than co-resident clusters (C5 shape, 5000 states = 157 words, the last one
+    partial): every cluster runs several words back to back (per-word re-staging, mbarrier
+    phases continuing across words) -- each state equals the oracle's single-state result."""
+    import torch
+    n, d, S = 200, 16, 5000
+    inst = synth.random_csp(n, d, 0.8, 0.3, 1)
+    orc = oracle.Oracle.from_instance(inst)
+    _, root, _, _ = orc.rac(inst.full_domains(), with_epochs=False)
+
+    def enf(D):
+        st, out, _, _ = orc.rac(D, with_epochs=False)
+        return st, out
+
+    states, seeds = synth.dive_states(root, enf, S, seed=4, return_seeds=True)
+    states = np.stack(states)
+    seeds = np.asarray(seeds, dtype=np.int32)
+    seeds[::3] = -1
+    ctx = rac.RacContext.from_instance(inst)
+    din = torch.from_numpy(states.view(np.int64)).cuda()
+    dout = torch.zeros_like(din)
+    its = torch.zeros(S, dtype=torch.int32, device="cuda")
+    sts = torch.zeros(S, dtype=torch.int32, device="cuda")
+    ctx.enforce_batch_seeded(S, din, dout, its, sts, torch.from_numpy(seeds).cuda())
+    torch.cuda.synchronize()
+    out = dout.cpu().numpy().view(np.uint64)
+    its, sts = its.cpu().numpy(), sts.cpu().numpy()
+    for s in range(S):
+        e = orc.rac(states[s], with_epochs=False)
+        assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), s
+
+
 @pytest.mark.parametrize("groups", ["1", "0"])
 def test_batched_exact_columns(rac, groups, monkeypatch):
     """The cluster batch kernel tests, per state, only the columns that changed for
