@@ -543,6 +543,16 @@ def run_gpu(args, rank, world, local_rank):
                                        round(achieved / peak, 4),
                     "launch_ms_median": round(kern_ms, 5),
                     "peak_source": peak_src + ("" if world == 1 else "; per-GPU bytes = total / N")}
+        if ctx.relation_bytes > L2_BYTES:
+            # context only (the peak stays MEASURED_PEAKS.json): this box's copy bandwidth,
+            # measured here the way the driver measures hbm_gbs -- pool boxes differ
+            try:
+                roofline["box_copy_gbs"] = round(measure_copy_gbs(dev), 1)
+                roofline["box_copy_note"] = ("this box, measured in this run (torch copy of 1 GiB of bf16, "
+                                             "read+write bytes, best of 10); context for box-to-box variance, "
+                                             "not the roofline denominator")
+            except Exception:
+                pass
         if world > 1:
             roofline["achieved"] = round(achieved / world, 1)
             roofline["frac"] = round(achieved / world / peak, 4)
@@ -603,6 +613,26 @@ def wrand_states(n, d, S):
     if d > 64:
         return np.stack([synth.w_rand_wide(dom, 0.8, seed=1000 + s) for s in range(S)])
     return np.stack([synth.w_rand(dom, 0.8, seed=1000 + s) for s in range(S)])
+
+
+def measure_copy_gbs(dev):
+    import torch
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    for _ in range(3):
+        b.copy_(a)
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2.0 * (1 << 30) * 2 / (best / 1e3) / 1e9
 
 
 def measure_l2_read_gbs(nbytes, dev):

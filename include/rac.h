@@ -244,7 +244,12 @@ int rac_enforce_seeded_async(rac_ctx* ctx, const uint64_t* d_in_dev, uint64_t* d
 /* Batched seeded enforcement: state s is seeded with the single variable
  * seed_var_dev[s] (device int32[n_states]; -1 = all variables, i.e. a root
  * call), under the precondition above (search-tree children after one
- * assignment each).  Results equal rac_enforce of each state alone. */
+ * assignment each).  Results equal rac_enforce of each state alone.  Off the
+ * precondition, the one-word kernels (max dom <= 32: 32-state words per
+ * thread-block cluster, every state gated to its own changed columns) and the
+ * per-state kernels give exactly rac_enforce_seeded(state, [seed]); the wide
+ * tensor-core pass (max dom 65..128, >= 256 states) tests every column in every
+ * pass, which agrees under the precondition. */
 int rac_enforce_batch_seeded(rac_ctx* ctx, int32_t n_states, const uint64_t* d_in_dev, uint64_t* d_out_dev,
                              int32_t* iterations_dev, int32_t* status_dev, const int32_t* seed_var_dev,
                              uint32_t flags, void* stream);
