@@ -1497,6 +1497,12 @@ static int batch_impl(rac_ctx* c, int32_t n_states, const uint64_t* d_in_dev, ui
       }
       b.Mg = no_groups ? nullptr : c->Mg;
       b.gstride = (size_t)c->rows_pad * 8;
+      // A/B knob (per call) RAC_CL_PS: per-state sweep for words with <= 8 active
+      // states, 1 = when cheaper by a test count, 2 = always.  Off: measured 1.8x
+      // slower at C5 (232 vs 421 us, profiles/r02al) -- each state pays its own
+      // mask loads, which the 32-state union sweep shares.
+      const char* pse = getenv("RAC_CL_PS");
+      b.ps_mode = pse ? atoi(pse) : 0;
       b.n = c->n;
       b.dmax = c->dmax;
       b.P = c->P;

@@ -312,6 +312,63 @@ __device__ __forceinline__ uint32_t sweep_list(const uint8_t* __restrict__ M, co
   return my_or;
 }
 
+// Per-state sweep (few active states): state s of slot k tests its own changed
+// columns psl[k][0..psc[k]) against its own D_s(y) (psd[k][.], W-bit values
+// extracted from the bit slices), one mask load and one AND per test instead
+// of the word's union of columns through the chunk tables.  A failing test
+// clears the row's lane s; an absent pair never fails (its mask is all ones,
+// so m & D_s(y) == 0 only when D_s(y) is empty: then the presence bit decides).
+constexpr int kPsMax = 8;  // per-state mode when at most this many states are active
+template <int W, bool CP>
+__device__ __forceinline__ uint32_t sweep_states(const uint8_t* __restrict__ M, size_t col_stride,
+                                                 const uint32_t* __restrict__ P, int pw, uint32_t* X,
+                                                 const uint16_t* psl, const uint32_t* psd, const int* psc,
+                                                 const int* pslane, int nps, int stride, int r0, int r1, int dmax,
+                                                 uint32_t active, uint32_t* chgn) {
+  uint32_t my_or = 0u;
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += blockDim.x) {
+    const uint32_t cur = X[r];
+    const uint32_t live = cur & active;
+    if (!live) continue;
+    const uint8_t* Mrow = M + (size_t)r * W;
+    const int x = r / dmax;
+    uint32_t fail = 0u;
+    for (int k = 0; k < nps; ++k) {
+      const int sl = pslane[k];
+      if (!((live >> sl) & 1u)) continue;
+      const uint16_t* L = psl + (size_t)k * stride;
+      const uint32_t* Dv = psd + (size_t)k * stride;
+      const int cntk = psc[k];
+      bool f = false;
+      for (int c0 = 0; c0 < cntk && !f; c0 += 8) {
+        uint32_t mv[8];
+        int yv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          yv[u] = c0 + u < cntk ? (int)L[c0 + u] : -1;
+          mv[u] = yv[u] >= 0 ? mask_at<W>(Mrow + (size_t)yv[u] * col_stride) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (yv[u] < 0) continue;
+          const uint32_t d = Dv[c0 + u];
+          if ((mv[u] & d) == 0u) {
+            if (d != 0u || !CP || present(P, pw, x, yv[u])) f = true;
+          }
+        }
+      }
+      if (f) fail |= 1u << sl;
+    }
+    const uint32_t nb = cur & ~fail;
+    if (nb != cur) {
+      X[r] = nb;
+      atomicOr(&chgn[x], cur ^ nb);
+      my_or |= cur ^ nb;
+    }
+  }
+  return my_or;
+}
+
 // Listed column GROUPS (column-group layout Mg: one 8-byte load per row gives
 // the masks of the 8/W columns g*8/W ..): cgrp[k] = the group, gtst[k*CPG + j]
 // = the lanes that test its column j (0: the column is not tested -- a
@@ -394,6 +451,8 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   __shared__ __align__(8) uint32_t s_part[2][kMaxC][2];  // per pass parity: every CTA's partial (pushed to all)
   __shared__ __align__(8) uint64_t s_mbar;     // incoming pushes of the current pass
   __shared__ int s_cnt;
+  __shared__ int s_ps;                               // this pass runs the per-state sweep (nps slots)
+  __shared__ int s_psc[kPsMax], s_pslane[kPsMax];    // per slot: column count, state lane
   __shared__ uint32_t s_empty0;
   __shared__ int s_iters[32], s_status[32];
   cg::cluster_group cluster = cg::this_cluster();
@@ -419,6 +478,9 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   uint32_t* gtst = reinterpret_cast<uint32_t*>(ci + ((n + 8 + 1) & ~1));          // 16-byte aligned
   uint32_t* cgrp = gtst + (((size_t)(ngr + 4) * CPG + 3) & ~(size_t)3);          // 16-byte aligned
   const bool groups = p.Mg != nullptr;
+  const int ps_stride = ((n + 8) + 7) & ~7;  // per-slot list stride (u16 / u32 entries)
+  uint16_t* psl = reinterpret_cast<uint16_t*>(cgrp + ((ngr + 4 + 3) & ~3));          // [kPsMax][ps_stride]
+  uint32_t* psd = reinterpret_cast<uint32_t*>(psl + (size_t)kPsMax * ps_stride);    // [kPsMax][ps_stride]
   const int r0 = k * p.RPC, r1 = min(rows, r0 + p.RPC);  // my rows
   const int x0 = r0 / dmax, x1 = (r1 + dmax - 1) / dmax;  // my variables
   const bool full = (p.flags & kFullCL) != 0;
@@ -588,7 +650,33 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
           ci[cnt + lane] = make_uint2(0u, 0u);
           ctst[cnt + lane] = 0u;
         }
-        if (lane == 0) s_cnt = cnt;
+        // few active states: each one's own changed columns, and the choice of sweep
+        // (per-state tests cost ~1/3 of a union-column test through the tables)
+        int nps = 0;
+        if (p.ps_mode && __popc(active) <= kPsMax && cnt > 0) {
+          int sum = 0;
+          for (uint32_t a = active; a; a &= a - 1u, ++nps) {
+            const int sl = __ffs(a) - 1;
+            int ck = 0;
+            for (int yb = 0; yb < n; yb += 32) {
+              const int y = yb + lane;
+              const bool in = y < n && ((chg[y] >> sl) & 1u);
+              const uint32_t bal = __ballot_sync(0xffffffffu, in);
+              if (in) psl[(size_t)nps * ps_stride + ck + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)y;
+              ck += __popc(bal);
+            }
+            if (lane == 0) {
+              s_psc[nps] = ck;
+              s_pslane[nps] = sl;
+            }
+            sum += ck;
+          }
+          if (!(p.ps_mode == 2 || sum < 3 * cnt)) nps = 0;
+        }
+        if (lane == 0) {
+          s_cnt = cnt;
+          s_ps = nps;
+        }
       }
       if (nwarps == 1) __syncwarp();
 #if RAC_CL_ITEM_TABLES
@@ -612,6 +700,21 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
 #endif
       __syncthreads();
       const int cnt = s_cnt;
+      const int nps = groups ? 0 : s_ps;
+      if (nps) {
+        // D_s(y) of every listed (state, column): one warp per entry, lane b reads
+        // X[(y, b)] and a ballot of bit s gives the W-bit domain
+        for (int k = 0; k < nps; ++k) {
+          const int ck = s_psc[k], sl = s_pslane[k];
+          for (int i = warp; i < ck; i += nwarps) {
+            const int y = psl[(size_t)k * ps_stride + i];
+            const bool bit = lane < dmax && ((X[y * dmax + lane] >> sl) & 1u);
+            const uint32_t dv = __ballot_sync(0xffffffffu, bit);
+            if (lane == 0) psd[(size_t)k * ps_stride + i] = dv;
+          }
+        }
+        __syncthreads();
+      }
       // everybody's rows and my chg_in are read: peers may overwrite them once
       // they have waited on this arrival
       cluster_arrive_relaxed();
@@ -619,7 +722,12 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       // ---- sweep: my rows against the tested columns
       const bool cp = (E & active) != 0u;  // some active state has an empty domain
       uint32_t my_or0;
-      if (groups)
+      if (nps)
+        my_or0 = cp ? sweep_states<W, true>(p.M, p.col_stride, p.P, p.pw, X, psl, psd, s_psc, s_pslane, nps,
+                                            ps_stride, r0, r1, dmax, active, chgn)
+                    : sweep_states<W, false>(p.M, p.col_stride, p.P, p.pw, X, psl, psd, s_psc, s_pslane, nps,
+                                             ps_stride, r0, r1, dmax, active, chgn);
+      else if (groups)
         my_or0 = cp ? sweep_groups<W, true>(p.Mg, p.gstride, p.P, p.pw, X, tb0, cgrp, gtst, (cnt + 3) & ~3, r0, r1,
                                             dmax, active, chgn)
                     : sweep_groups<W, false>(p.Mg, p.gstride, p.P, p.pw, X, tb0, cgrp, gtst, (cnt + 3) & ~3, r0, r1,
@@ -726,7 +834,9 @@ size_t batch_cl_smem(int n, int dmax, int W) {
   const size_t tb_bytes = std::max(npad * TSB, (size_t)32 * (n + 1) * 8);  // tables, or the staged d_in block
   return (size_t)TSB + tb_bytes + rows4 * 4 + 3 * n4 * 4 + ((((size_t)n + 8 + 3) & ~(size_t)3) * 4) +
          (((size_t)n + 8 + 1) & ~(size_t)1) * 8 +
-         ((((size_t)n + 8 / W - 1) / (8 / W) + 4) * (8 / W) + 3) / 4 * 16 + (((size_t)n + 8 / W - 1) / (8 / W) + 4) * 4;
+         ((((size_t)n + 8 / W - 1) / (8 / W) + 4) * (8 / W) + 3) / 4 * 16 +
+         ((((size_t)n + 8 / W - 1) / (8 / W) + 4 + 3) & ~(size_t)3) * 4 +
+         (size_t)kPsMax * ((((size_t)n + 8) + 7) & ~(size_t)7) * 6 + 16;
 }
 
 // Column groups for the batched sweep: Mg[g][r] = the 8 bytes of masks of columns

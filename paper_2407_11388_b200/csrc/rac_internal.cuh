@@ -210,6 +210,7 @@ struct BatchCLParams {
   size_t col_stride;
   const uint8_t* Mg;        // nullable: 8-byte column groups, Mg + g*gstride + r*8 = masks of columns g*8/W.. of row r
   size_t gstride;
+  int ps_mode;              // 0: union sweep only; 1: per-state sweep when <= 8 states are active and cheaper; 2: always when <= 8
   int n, dmax;
   const uint32_t* P;
   int pw;

@@ -559,8 +559,8 @@ def test_c5_batched_many_words(rac):
         assert (sts[s], its[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), s
 
 
-@pytest.mark.parametrize("groups", ["1", "0"])
-def test_batched_exact_columns(rac, groups, monkeypatch):
+@pytest.mark.parametrize("mode", ["default", "per_state", "groups"])
+def test_batched_exact_columns(rac, mode, monkeypatch):
     """The cluster batch kernel tests, per state, only the columns that changed for
     that state (Alg. 1's Cons[:, @changed]): C5 dive states seeded with their
     assigned variable (O1, the seeded call's precondition holds), and seeded calls on
@@ -569,7 +569,11 @@ def test_batched_exact_columns(rac, groups, monkeypatch):
     Alg. 1 trajectory, not the union of its word's columns; plus a corpus with every
     mask width (d up to 32, W = 1, 2, 4)."""
     import torch
-    monkeypatch.setenv("RAC_CL_GROUPS", groups)  # 8-byte column-group loads (A/B path), or per-column masks
+    # sweeps: union columns through chunk tables (per-column masks, or the 8-byte column-group
+    # A/B layout), and the per-state sweep for <= 8 active states (auto, or forced)
+    monkeypatch.setenv("RAC_CL_GROUPS", "1" if mode == "groups" else "0")
+    monkeypatch.setenv("RAC_CL_PS", {"default": "0", "per_state": "2", "union_only": "0", "groups": "0"}[mode])
+    groups = mode
     n, d, S = 200, 16, 512
     inst = synth.random_csp(n, d, 0.8, 0.3, 1)
     orc = oracle.Oracle.from_instance(inst)
