@@ -48,12 +48,11 @@ namespace {
 
 // build-time A/B variants (tools/session scripts build them with -D)
 // (profiles/r02aa, same box: item tables 242 -> 234 us per C5 batch, global
-// staging 242 -> 240, both 232; the alternatives stay selectable with -D...=0)
+// staging 242 -> 240, both 232; the alternatives stay selectable with -D...=0.
+// Also measured, no gain: rotated conflict-free table stores (r02ab), a u32
+// column list with 8 or 16 masks in flight per row (r02am: 232 / 236 us).)
 #ifndef RAC_CL_ITEM_TABLES
 #define RAC_CL_ITEM_TABLES 1  // 1: tables built one 16-entry block per thread; 0: one warp per column
-#endif
-#ifndef RAC_CL_ITEM_ROT
-#define RAC_CL_ITEM_ROT 0  // 1: item stores rotated by item index (bank-conflict-free, SEL-selected quads)
 #endif
 #ifndef RAC_CL_GLOBAL_STAGE
 #define RAC_CL_GLOBAL_STAGE 1  // 1: the word's states transposed by ballots straight from global memory;
@@ -229,22 +228,8 @@ __device__ __forceinline__ void build_item(uint8_t* Tb, const uint32_t* X, int y
     tv[v] = tv[v & (v - 1)] | xb[lb];
   }
   uint4* dst = reinterpret_cast<uint4*>(Tb + (size_t)y * Lut<W>::TSB + Lut<W>::off(q) + bi * 64);
-#if RAC_CL_ITEM_ROT
-  // consecutive items are consecutive 64-byte blocks: item i stores its quads
-  // starting at quad i % 4, so one store instruction of a warp covers all banks
-  const uint4 q4[4] = {make_uint4(tv[0], tv[1], tv[2], tv[3]), make_uint4(tv[4], tv[5], tv[6], tv[7]),
-                       make_uint4(tv[8], tv[9], tv[10], tv[11]), make_uint4(tv[12], tv[13], tv[14], tv[15])};
-  const int rot = i & 3;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int k = (j + rot) & 3;
-    const uint4 a = (k & 1) ? q4[1] : q4[0], b = (k & 1) ? q4[3] : q4[2];
-    dst[k] = (k & 2) ? b : a;
-  }
-#else
 #pragma unroll
   for (int v = 0; v < 16; v += 4) dst[v >> 2] = make_uint4(tv[v], tv[v + 1], tv[v + 2], tv[v + 3]);
-#endif
 }
 #endif
 
