@@ -385,7 +385,8 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
     // without room for it every pass uses the column-major tensor.
     const size_t rbytes = (size_t)c->rows_pad * c->dbytes;
     const char* fl = getenv("RAC_FORCE_LAYOUT");
-    c->force_layout = fl ? (strcmp(fl, "rows") == 0 ? 1 : strcmp(fl, "cols") == 0 ? 2 : 0) : 0;
+    c->force_layout = fl ? (strcmp(fl, "rows") == 0 ? 1 : strcmp(fl, "cols") == 0 ? 2
+                                : strcmp(fl, "tiecols") == 0 ? 3 : 0) : 0;
     const char* nr = getenv("RAC_NO_ROW_LAYOUT");
     if (!(nr && *nr && strcmp(nr, "0") != 0) && c->force_layout != 2) {
       if (cudaMalloc(&c->Mr, rbytes) != cudaSuccess) {

@@ -367,9 +367,15 @@ __device__ __forceinline__ bool pick_rows(const PassGeom& g, long long live, int
   const long long rows = (long long)(g.x_hi - g.x_lo) * g.dmax;
   // tiny tensors are latency-bound: whole rows are fewer, simpler work items
   if (rows * (long long)g.dbytes <= (256ll << 10)) return true;
-  // bytes of each layout (both sweeps stream at about the same rate since the
-  // column sweep reads column-aligned 4 KB items, profiles/r01j)
-  return live * (long long)g.n < rows * (long long)ncol;
+  // bytes of each layout; a tie (a full pass over live rows: C3 / C4 W-stream,
+  // pass 1 of a root call) goes to the row sweep: on some pool boxes the column
+  // sweep streams ~20 % slower (C3 W-stream 110 vs 90 us, C4 5.75 vs 4.99 ms on
+  // one box, profiles/r02an) while the row sweep runs ~90 us on every box
+  // measured.  L2-resident tensors keep the column sweep for ties (C2: 14.4 vs
+  // 16.3 us); force == 3 (RAC_FORCE_LAYOUT=tiecols) keeps it for every tie.
+  const bool hbm = rows * (long long)g.dbytes > (64ll << 20);
+  if (g.force == 3 || !hbm) return live * (long long)g.n < rows * (long long)ncol;
+  return live * (long long)g.n <= rows * (long long)ncol;
 }
 
 // Live rows (x,a) of variables [x_lo, x_hi) in D (every thread of the CTA gets it).
