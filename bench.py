@@ -563,6 +563,11 @@ def run_gpu(args, rank, world, local_rank):
                               "persistent kernel, NVLink P2P)" if peer else
                               "row-sharded x%d (NCCL all-gather of D per pass)") % world) if world > 1 else "1 GPU",
              "instance_generation_s": round(gen_s, 3)}
+    if ctx.wq == 1 and ctx.layout == "dense":
+        lay, ms_c, ms_r = ctx.full_pass_layout
+        setup["full_pass_sweep"] = {"sweep": lay, "calibration_ms_columns": ms_c, "calibration_ms_rows": ms_r,
+                                    "how": "rac_create times one root enforcement with full passes on each dense "
+                                           "sweep and keeps the faster (0 = not measured)"}
     out = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,

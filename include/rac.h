@@ -358,6 +358,12 @@ int32_t rac_layout(const rac_ctx* ctx);
 int32_t rac_path(const rac_ctx* ctx);
 /* Kernel launches enqueued by the last rac_enforce* call on this context. */
 int64_t rac_last_launch_count(const rac_ctx* ctx);
+/* Sweep used for full passes (every live row against every column: pass 1 of a
+ * root call) of a dense single-GPU context: 0 = row-major sweep, 1 = column
+ * sweep.  Both read the same bytes; HBM-resident contexts time one root
+ * enforcement with each at rac_create and keep the faster (*ms_cols, *ms_rows:
+ * best times in ms, 0 when not measured; either pointer may be NULL). */
+int32_t rac_full_pass_layout(const rac_ctx* ctx, float* ms_cols, float* ms_rows);
 
 const char* rac_last_error(const rac_ctx* ctx);
 void rac_destroy(rac_ctx* ctx);

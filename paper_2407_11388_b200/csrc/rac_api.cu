@@ -87,7 +87,8 @@ struct rac_ctx {
   uint8_t* M = nullptr;     // column-major masks
   uint8_t* Mr = nullptr;    // row-major copy (nullable)
   int G = 1;                // lanes per row of the row-major sweep
-  int force_layout = 0;     // RAC_FORCE_LAYOUT=rows|cols (testing knob)
+  int force_layout = 0;     // RAC_FORCE_LAYOUT=rows|cols|tiecols (testing knob); 3 after calibrate_tie picks columns
+  float tie_ms[2] = {0.f, 0.f};  // calibrate_tie: best root enforcement with ties to columns / rows
   uint32_t* P = nullptr;
   // Sparse arc-block layout (NEXT-3; rac.h RAC_OPT_SPARSE): only declared arcs
   bool sparse = false;
@@ -869,6 +870,50 @@ int enforce_async_impl(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_
 }  // namespace
 
 namespace {
+// Full passes over every live row read the same bytes in either dense sweep, and
+// which one streams faster depends on the box (profiles/r02an/r02ao: column
+// sweep 88 vs row sweep 92 us on one B200, 110 vs 90 us on another, same C3
+// W-stream).  So an HBM-resident single-GPU context times both once at create
+// -- a root enforcement from full domains with ties sent to columns, then to
+// rows, best of three -- and keeps the faster for ties (RAC_FORCE_LAYOUT
+// overrides; RAC_NO_TIE_CALIB=1 keeps the row sweep without measuring).
+void calibrate_tie(rac_ctx* c) {
+  if (c->sparse || c->world > 1 || c->vshards > 1 || c->nccl_self || c->peer || !c->Mr || c->small ||
+      c->force_layout != 0 || (double)c->rows_pad * c->dbytes <= 64.0 * (1 << 20))
+    return;
+  if (getenv("RAC_NO_TIE_CALIB")) return;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  float best[2] = {1e30f, 1e30f};  // [0] ties -> columns (force 3), [1] ties -> rows (force 0)
+  int32_t* res = reinterpret_cast<int32_t*>(c->buf_scalars);
+  for (int rep = 0; rep < 4; ++rep)
+    for (int v = 0; v < 2; ++v) {
+      c->force_layout = v == 0 ? 3 : 0;
+      cudaEventRecord(e0, c->stream);
+      if (enforce_fused(c, c->dommask, c->buf_out, res, res + 1, nullptr, 0u, c->stream) != 0) {
+        c->force_layout = 0;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGetLastError();
+        c->broken = false;
+        return;
+      }
+      cudaEventRecord(e1, c->stream);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0 && ms < best[v]) best[v] = ms;  // rep 0 warms up both
+    }
+  c->force_layout = best[0] < best[1] ? 3 : 0;
+  c->tie_ms[0] = best[0];
+  c->tie_ms[1] = best[1];
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 // rac_create with max dom > 64: rows of relation r are dom[x] x wq words
 // (wq = ceil(max dom / 64)); validated here, packed on the device.
 int create_wide(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const rac_relation* rels,
@@ -1110,6 +1155,7 @@ int rac_create(int32_t n_vars, const int32_t* dom_sizes, int32_t n_rel, const ra
   }
   rc = init_comm(c, opt);
   if (rc) { free_ctx(c); return rc; }
+  calibrate_tie(c);
   *out = c;
   return 0;
 }
@@ -1166,6 +1212,7 @@ int rac_create_random(int32_t n_vars, int32_t d, uint64_t dens_q32, uint32_t t_q
   }
   rc = init_comm(c, opt);
   if (rc) { free_ctx(c); return rc; }
+  calibrate_tie(c);
   *out = c;
   return 0;
 }
@@ -1777,6 +1824,12 @@ int64_t rac_relation_bytes(const rac_ctx* c) {
 }
 int32_t rac_layout(const rac_ctx* c) { return c ? (c->sparse ? RAC_LAYOUT_SPARSE : RAC_LAYOUT_DENSE) : RAC_EINVAL; }
 int64_t rac_last_launch_count(const rac_ctx* c) { return c ? c->launches : RAC_EINVAL; }
+int32_t rac_full_pass_layout(const rac_ctx* c, float* ms_cols, float* ms_rows) {
+  if (!c) return RAC_EINVAL;
+  if (ms_cols) *ms_cols = c->tie_ms[0];
+  if (ms_rows) *ms_rows = c->tie_ms[1];
+  return (c->force_layout == 2 || c->force_layout == 3 || !c->Mr) ? 1 : 0;
+}
 int32_t rac_path(const rac_ctx* c) {
   if (!c) return RAC_EINVAL;
   if (c->wide) return RAC_PATH_WIDE;

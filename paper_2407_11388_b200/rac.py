@@ -75,7 +75,7 @@ EXPORTS = ["rac_default_options", "rac_create", "rac_create_random", "rac_enforc
            "rac_enforce_batch_seeded", "rac_search", "rac_batch_pass_eval", "rac_n_vars", "rac_max_dom", "rac_mask_bytes", "rac_words_per_var",
            "rac_layout", "rac_relation_bytes", "rac_shard_range", "rac_local_range", "rac_read_row", "rac_get_nccl_unique_id",
            "rac_peer_handle", "rac_connect_peers", "rac_peer_region", "rac_connect_peers_local",
-           "rac_last_launch_count", "rac_path", "rac_last_error", "rac_destroy"]
+           "rac_last_launch_count", "rac_full_pass_layout", "rac_path", "rac_last_error", "rac_destroy"]
 
 PATHS = {0: "fused", 1: "one_block", 2: "sparse", 3: "sharded", 4: "peer", 5: "wide"}
 
@@ -120,6 +120,7 @@ def _load() -> ctypes.CDLL:
         "rac_peer_region": (ctypes.c_int, [P, ctypes.POINTER(P)]),
         "rac_connect_peers_local": (ctypes.c_int, [P, ctypes.POINTER(P), i32p]),
         "rac_last_launch_count": (i64, [P]),
+        "rac_full_pass_layout": (i32, [P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]),
         "rac_path": (i32, [P]),
         "rac_last_error": (ctypes.c_char_p, [P]),
         "rac_destroy": (None, [P]),
@@ -280,6 +281,14 @@ class RacContext:
         _check(lib.rac_create_random(n_vars, d, dens_q32, t_q16, seed, ctypes.byref(opt), ctypes.byref(h)))
         del keep
         return cls(h, n_vars, d)
+
+    @property
+    def full_pass_layout(self):
+        """(layout, ms_columns, ms_rows): the sweep of full passes ("rows" / "columns") and the
+        create-time calibration times (0 when not measured)."""
+        a, b = ctypes.c_float(0), ctypes.c_float(0)
+        r = int(lib.rac_full_pass_layout(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return ("columns" if r == 1 else "rows"), round(a.value, 5), round(b.value, 5)
 
     def close(self):
         if getattr(self, "_h", None) and lib is not None:
