@@ -71,21 +71,21 @@ template <int W>
 struct Lut;
 template <>
 struct Lut<1> {
-  static constexpr int NCH = 2, TSB = 128, NI = 2;
+  static constexpr int NCH = 2, TSB = 128;
   __host__ __device__ static constexpr int bits(int) { return 4; }
   __host__ __device__ static constexpr int shift(int q) { return 4 * q; }
   __host__ __device__ static constexpr int off(int q) { return 64 * q; }
 };
 template <>
 struct Lut<2> {
-  static constexpr int NCH = 3, TSB = 512, NI = 8;
+  static constexpr int NCH = 3, TSB = 512;
   __host__ __device__ static constexpr int bits(int q) { return q == 0 ? 6 : 5; }
   __host__ __device__ static constexpr int shift(int q) { return q == 0 ? 0 : (q == 1 ? 6 : 11); }
   __host__ __device__ static constexpr int off(int q) { return q == 0 ? 0 : (q == 1 ? 256 : 384); }
 };
 template <>
 struct Lut<4> {
-  static constexpr int NCH = 8, TSB = 512, NI = 8;
+  static constexpr int NCH = 8, TSB = 512;
   __host__ __device__ static constexpr int bits(int) { return 4; }
   __host__ __device__ static constexpr int shift(int q) { return 4 * q; }
   __host__ __device__ static constexpr int off(int q) { return 64 * q; }

@@ -121,6 +121,7 @@ struct ItemIter {
 #define RAC_CLAIM_PARTS 32
 #endif
 constexpr uint32_t kClaimParts = RAC_CLAIM_PARTS;
+#if RAC_COL_CLAIM == 2
 struct TailClaim {
   uint32_t b, e;
   unsigned* ctr;
@@ -139,6 +140,7 @@ struct TailClaim {
     return __shfl_sync(0xffffffffu, r, 0);
   }
 };
+#endif
 
 // Column sweep: test the rows of variables [g.x_lo, g.x_hi) against the
 // columns cols[0, ncol) (cols == nullptr: columns 0..ncol-1) and OR removals
