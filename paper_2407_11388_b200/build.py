@@ -50,8 +50,10 @@ def _stale() -> bool:
         return f.read().strip() != _source_hash()
 
 
-def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=(), src_dir: str = None) -> str:
+    """src_dir (A/B tooling, with `out`): build from another copy of csrc/ (e.g. an older revision)."""
     lib = out or LIB
+    csrc = src_dir or CSRC
     if not force and out is None and not _stale():
         return LIB
     tmp = lib + ".tmp.%d" % os.getpid()
@@ -62,7 +64,8 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
 
     def compile_one(i):
-        return subprocess.run([nvcc_path(), *flags, "-c", os.path.join(CSRC, SOURCES[i]), "-o", objs[i]],
+        return subprocess.run([nvcc_path(), *flags, "-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(ROOT, "synth"),
+                               "-c", os.path.join(csrc, SOURCES[i]), "-o", objs[i]],
                               capture_output=True, text=True)
 
     # one nvcc per translation unit, in parallel (rac_kernels.cu dominates)
@@ -79,7 +82,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
         if verbose:
             sys.stderr.write(res.stderr)
     os.replace(tmp, lib)
-    if out is None and not defines:
+    if out is None and not defines and src_dir is None:
         with open(LIB + ".srchash", "w") as f:
             f.write(_source_hash() + "\n")
     return lib

@@ -171,6 +171,7 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
   const uint32_t upl = upl64 < 1ull ? 1u : (upl64 > (uint64_t)U ? (uint32_t)U : (uint32_t)upl64);
   const uint32_t ipc = (v_hi - v_lo + 32u * upl - 1u) / (32u * upl);  // items per column
   const uint32_t items = ipc * (uint32_t)ncol;
+  bool flagged = false;  // this warp has raised the pass's removal flag
 #if RAC_COL_CLAIM == 2
   // static round robin for the first items, then partitioned claims (cctr)
   const uint32_t per = cctr ? (items - items / kClaimDiv) / (uint32_t)nwarps
@@ -206,10 +207,13 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
       if (v0 + u * 32u < ve) m[u] = ldg_stream(col + v0 + u * 32u);
     const uint64_t dv = load_w<W>(Db + y * W);
     const uint4 rd = rep16<W>(dv);
-    uint32_t any = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t v = v0 + u * 32u;
+      // failing live rows of this lane's vector, as (variable, value bits): the
+      // RPL rows of a vector span two variables at most when dmax >= RPL
+      int x1 = -1, x2 = -1;
+      unsigned long long b1 = 0ull, b2 = 0ull;
       if (v < ve) {
         const uint4 tv = and4(m[u], rd);
         if (vec_any_zero<W>(tv)) {  // rare: some row of this vector may lose its support
@@ -221,14 +225,26 @@ __device__ __noinline__ void column_sweep(const PassGeom& g, const uint8_t* Db, 
             const int x = g.x_lo_alloc + xl;
             if (!((Db[x * W + (a >> 3)] >> (a & 7)) & 1u)) continue;  // (x,a) not live
             if (dv == 0ull && !((g.P[(size_t)xl * g.pw + (y >> 5)] >> (y & 31)) & 1u)) continue;  // R2
-            any = 1;
-            mark_removed(R, x, 1ull << a, cl);
+            if (x1 < 0 || x1 == x) { x1 = x; b1 |= 1ull << a; }
+            else if (x2 < 0 || x2 == x) { x2 = x; b2 |= 1ull << a; }
+            else mark_removed(R, x, 1ull << a, cl);  // a third variable (dmax < RPL): direct
             if (removed_at) put_epoch(removed_at, em, (size_t)x * 64 + a, t);
           }
         }
       }
+      // one atomic per (lane, variable) instead of per row; the removal flag is
+      // a plain store (same-address atomics from every failing lane serialised the
+      // tail of removal-heavy passes, r02ar; a warp-wide merge of the atomics cost
+      // more in the stream than it saved, r02as)
+      if (x1 >= 0) {
+        mark_removed(R, x1, b1, cl);
+        if (x2 >= 0) mark_removed(R, x2, b2, cl);
+        if (rflag && !flagged) {
+          *reinterpret_cast<volatile unsigned*>(rflag) = 1u;
+          flagged = true;
+        }
+      }
     }
-    if (any && rflag) atomicOr(rflag, 1u);  // this pass removed something
   }
 }
 
@@ -252,6 +268,7 @@ __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* D
   const uint32_t items = ipref[ncol];
   const uint4* S4 = reinterpret_cast<const uint4*>(g.S);
   int ci = 0;
+  bool flagged = false;
   ItemIter iter(items, warp0, nwarps, wctr);
   for (uint32_t it; iter.next(it);) {
     int hi = ncol - 1;  // last i with ipref[i] <= it (items increase: search from the previous ci)
@@ -291,7 +308,11 @@ __device__ __forceinline__ void sparse_sweep(const PassGeom& g, const uint8_t* D
         }
       }
     }
-    if (any && rflag) atomicOr(rflag, 1u);  // this pass removed something
+    // this pass removed something: a plain store, once per lane and sweep
+    if (any && rflag && !flagged) {
+      *reinterpret_cast<volatile unsigned*>(rflag) = 1u;
+      flagged = true;
+    }
   }
 }
 
@@ -322,6 +343,7 @@ __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsig
   // claim in flight while the current item streams), so SMs that drain HBM
   // faster take more of the tail and the pass ends within about one row.
   const int gpw = 32 / G, gw = lane / G;
+  bool flagged = false;
   auto process = [&](int it) {
     int r = it, sgi = 0;
     if (n_seg > 1) { r = it / n_seg; sgi = it - r * n_seg; }
@@ -333,7 +355,10 @@ __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsig
     const int vb = sgi * seg, ve = min(vb + seg, nvec);
     if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
       mark_removed(R, x, 1ull << a, cl);
-      if (rflag) atomicOr(rflag, 1u);  // this pass removed something
+      if (rflag && !flagged) {  // this pass removed something: a plain store, once per group and sweep
+        *reinterpret_cast<volatile unsigned*>(rflag) = 1u;
+        flagged = true;
+      }
       if (removed_at) put_epoch(removed_at, em, (size_t)x * 64 + a, t);
     }
   };
