@@ -68,6 +68,10 @@ __device__ __forceinline__ void mark_removed(unsigned long long* R, int x, unsig
 #define RAC_CLAIM_DIV 8
 #endif
 constexpr uint32_t kClaimDiv = RAC_CLAIM_DIV;  // 1/kClaimDiv of the items are claimed dynamically
+#ifndef RAC_ROW_CLAIM_DIV
+#define RAC_ROW_CLAIM_DIV 8
+#endif
+constexpr int kRowClaimDiv = RAC_ROW_CLAIM_DIV;  // row sweep: 1/kRowClaimDiv of the rows are claimed
 #ifndef RAC_COL_CLAIM
 #define RAC_COL_CLAIM 0
 #endif
@@ -362,7 +366,7 @@ __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsig
       if (removed_at) put_epoch(removed_at, em, (size_t)x * 64 + a, t);
     }
   };
-  const int per = wctr ? (items - items / 8) / ng : (items + ng - 1) / ng;
+  const int per = wctr ? (items - items / kRowClaimDiv) / ng : (items + ng - 1) / ng;
   const int S = wctr ? per * ng : items;
   auto claim = [&]() {
     unsigned b = 0;
