@@ -88,6 +88,7 @@ struct rac_ctx {
   uint8_t* Mr = nullptr;    // row-major copy (nullable)
   int G = 1;                // lanes per row of the row-major sweep
   int force_layout = 0;     // RAC_FORCE_LAYOUT=rows|cols|tiecols (testing knob); 3 after calibrate_tie picks columns
+  bool row_agg = false;     // row sweep aggregates removals per CTA in shared memory (dense, when n words fit)
   float tie_ms[2] = {0.f, 0.f};  // calibrate_tie: best root enforcement with ties to columns / rows
   uint32_t* P = nullptr;
   // Sparse arc-block layout (NEXT-3; rac.h RAC_OPT_SPARSE): only declared arcs
@@ -287,7 +288,8 @@ size_t xr_epoch_off(int n) { return xr_calls_off(n) + 8; }                   // 
 size_t xr_bytes(int n) { return xr_epoch_off(n) + (size_t)2 * n * 64 * 4; }
 
 size_t kernel_smem(const rac_ctx* c) {
-  return c->sparse ? sparse_smem(c->dbytes, c->n) : fused_smem(c->dbytes, c->n);
+  return c->sparse ? sparse_smem(c->dbytes, c->n)
+                   : fused_smem(c->dbytes, c->n) + (c->row_agg ? (((size_t)c->n * 8 + 15) & ~(size_t)15) : 0);
 }
 
 // Sparse arc-block geometry: dpad rows per block so that a block is a whole
@@ -433,6 +435,11 @@ int setup_ctx(rac_ctx* c, int32_t n, const int32_t* dom, const rac_options* opt,
   CKC(alloc_staging(c, (size_t)n * 8, 64));
   CKC(cudaMallocHost(&c->h_scalars, 16));
 
+  // A/B knob RAC_ROW_AGG=1: row-sweep removals aggregated per CTA in shared memory
+  // (one atomic per (CTA, variable) instead of one per failing row).  Off: it
+  // shortened the barrier waits of C3 W-seed's removal-heavy passes (8.6 / 13.3 ->
+  // 3.6 / 4.3 us) but lengthened their sweeps as much (119.2 vs 120.2 us, r02aw).
+  c->row_agg = !c->sparse && fused_smem(c->dbytes, n) + (size_t)n * 8 <= 160 * 1024 && getenv("RAC_ROW_AGG") != nullptr;
   // Launch geometry.  Fused path: a co-resident grid (cooperative launch),
   // as many CTAs as fit, but no more than the work of a full pass can feed
   // (about 4 items of kUnroll columns x one 512-byte slab per warp).
@@ -739,6 +746,7 @@ int enforce_fused(rac_ctx* c, const uint64_t* d_in, uint64_t* d_out, int32_t* it
   // profiles/r02v; A/B knob RAC_LIST_MAX, 0 = off)
   static const int list_max = getenv("RAC_LIST_MAX") ? atoi(getenv("RAC_LIST_MAX")) : 16;
   p.list_max = list_max;
+  p.row_agg = c->row_agg ? 1 : 0;
   static const bool no_cclaim = getenv("RAC_NO_CCLAIM") != nullptr;  // A/B knob (tooling only)
   p.cctr = no_cclaim ? nullptr : c->cctr;
   p.seeds = seeds;

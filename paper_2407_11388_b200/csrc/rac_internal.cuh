@@ -121,6 +121,8 @@ struct FusedParams {
   uint32_t flags;
   uint32_t ab;              // A/B knobs (tooling, RAC_FUSED_AB): bit 0 legacy grid barrier, bit 1 listed apply, bit 2 no removal-flag check before the R read
   int list_max;             // dense layout: passes testing <= list_max columns keep a change list (apply reads only its R words, no compaction)
+  int row_agg;              // dense: the row sweep ORs removals into a per-CTA copy of R in shared memory (after the
+                            // fused_smem region, n words) and flushes one atomic per (CTA, variable)
   unsigned* cctr;           // nullable [3][32 parts][32]: partitioned tail-claim counters of the column sweep (RAC_COL_CLAIM == 2 builds)
   unsigned long long* dbg;  // nullable: phase timestamps of CTA 0 (RAC_DEBUG_TIMELINE)
   // Global pass counter (persists across launches): pass t of this launch is

@@ -328,7 +328,8 @@ template <int W, int G>
 __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsigned long long* R,
                                           int32_t* removed_at, int t, long gidx, long ngroups,
                                           unsigned* wctr = nullptr, unsigned* rflag = nullptr,
-                                          uint32_t* cl = nullptr, const EpochMirror* em = nullptr) {
+                                          uint32_t* cl = nullptr, const EpochMirror* em = nullptr,
+                                          unsigned long long* Rs = nullptr) {
   const uint8_t* Db = reinterpret_cast<const uint8_t*>(Ds);
   const int lane = threadIdx.x & 31;
   const int gl = lane % G;
@@ -358,7 +359,8 @@ __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsig
     const uint32_t* Prow = g.P + (size_t)(x - g.x_lo_alloc) * g.pw;
     const int vb = sgi * seg, ve = min(vb + seg, nvec);
     if (row_fails<W, G>(row, Ds, vb, ve, gl, gmask, g.n, Prow) && gl == 0) {
-      mark_removed(R, x, 1ull << a, cl);
+      if (Rs) atomicOr(reinterpret_cast<unsigned*>(&Rs[x]) + (a >> 5), 1u << (a & 31));  // shared (native)
+      else mark_removed(R, x, 1ull << a, cl);
       if (rflag && !flagged) {  // this pass removed something: a plain store, once per group and sweep
         *reinterpret_cast<volatile unsigned*>(rflag) = 1u;
         flagged = true;
@@ -387,6 +389,18 @@ __device__ __noinline__ void row_sweep(const PassGeom& g, const uint4* Ds, unsig
       break;
     }
     if (it < items) process(it);
+  }
+  if (Rs) {
+    // one atomic per (CTA, variable): the rows of a variable sit in neighbouring
+    // groups, so per-row atomics made chains of ~dmax on one R word (r02aw)
+    __syncthreads();
+    for (int x = g.x_lo + (int)threadIdx.x; x < g.x_hi; x += (int)blockDim.x) {
+      const unsigned long long v = Rs[x];
+      if (v) {
+        Rs[x] = 0ull;
+        mark_removed(R, x, v, cl);
+      }
+    }
   }
 }
 
@@ -467,6 +481,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
   if (dbg_cta) p.dbg[256 + 3 * blockIdx.x] = globaltimer();
   RAC_MARK();
   for (int i = threadIdx.x; i < g.n; i += blockDim.x) vneed[i] = 0;
+  unsigned long long* Rs = (G > 0 && p.row_agg) ? reinterpret_cast<unsigned long long*>(Db + fused_smem(g.dbytes, g.n))
+                                                : nullptr;  // per-CTA removal bits of the row sweep
+  if (Rs)
+    for (int i = threadIdx.x; i < g.n; i += blockDim.x) Rs[i] = 0ull;
   stage_from_u64<W>(Db, p.d_in, p.dommask, g.n, g.dbytes);
   RAC_MARK();
   const long warp0 = (long)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -570,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) rac_fused(const __grid_c
       } else {
         if (pick_rows(g, live, lst ? vcnt : g.n))
           row_sweep<W, G>(g, Ds, Rc, ep, t, gidx, ngroups, p.wctr ? p.wctr + b : nullptr, p.rflag + b,
-                          clc, emp);
+                          clc, emp, Rs);
         else
           column_sweep<W>(g, Db, Rc, ep, t, warp0, nwarps, lst ? vlist : nullptr, lst ? vcnt : g.n,
                           p.rflag + b, (RAC_COL_CLAIM == 1 && p.wctr) ? p.wctr + b : nullptr, clc, emp,
