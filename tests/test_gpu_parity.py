@@ -627,6 +627,33 @@ def test_batched_exact_columns(rac, mode, monkeypatch):
             assert (st_h[s], it_h[s]) == (e[0], e[2]) and np.array_equal(out[s], e[1]), (k, s, groups)
 
 
+@pytest.mark.parametrize("variant", ["row_agg", "tiecols", "rows"])
+def test_dense_sweep_variants(rac, variant, monkeypatch):
+    """The dense persistent kernel's A/B variants give the oracle's exact trajectory (O7 at C3
+    W-prop and W-seed): per-CTA shared-memory aggregation of the row sweep's removals
+    (RAC_ROW_AGG), full passes on the column sweep (tiecols) or the row sweep (rows); and the
+    create-time calibration reports its choice."""
+    env = {"row_agg": ("RAC_ROW_AGG", "1"), "tiecols": ("RAC_FORCE_LAYOUT", "tiecols"),
+           "rows": ("RAC_FORCE_LAYOUT", "rows")}[variant]
+    monkeypatch.setenv(*env)
+    dq = synth.quant_density(1.0)
+    for t in (0.70, 0.5):
+        tq = synth.quant_tightness(t)
+        ctx = rac.RacContext.create_random(2000, 32, dq, tq, 1)
+        root = synth.full_domains(np.full(2000, 32))
+        g = ctx.enforce(root, removed_at=True)
+        assert oracle.certify_trajectory_synth(2000, 32, dq, tq, 1, root, g[1], g[3], g[2], g[0]) == 0, (variant, t)
+        if g[0] == oracle.OK and t == 0.5:
+            ds, x, _ = synth.w_seed(g[1], 1)
+            gs = ctx.enforce(ds, removed_at=True)  # a root call on the W-seed state: multi-pass, removal-heavy
+            assert oracle.certify_trajectory_synth(2000, 32, dq, tq, 1, ds, gs[1], gs[3], gs[2], gs[0]) == 0
+        lay, ms_c, ms_r = ctx.full_pass_layout
+        if variant == "row_agg":
+            assert lay in ("rows", "columns") and ms_c > 0 and ms_r > 0
+        else:
+            assert lay == ("columns" if variant == "tiecols" else "rows")
+
+
 def test_nccl_exchange_leg_single_rank(rac):
     """The multi-GPU path with its real NCCL all-gather (a one-rank communicator,
     RAC_OPT_NCCL_SELF) gives the oracle's results: exercises dlopen of libnccl, comm init,
