@@ -453,9 +453,9 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
   const uint32_t tb0 = base + pad;  // shared-memory address, TSB-aligned
   const size_t tb_bytes = max((size_t)npad * L::TSB, (size_t)32 * (n + 1) * 8);  // tables / staged d_in
   uint32_t* X = reinterpret_cast<uint32_t*>(Tb + tb_bytes);
-  uint32_t* chg = X + rows4;
-  uint32_t* chgn = chg + n4;
-  uint32_t* chg_in = chgn + n4;
+  uint32_t* chg = X + rows4;       // pass 1's tested lanes per column (seeds / roots)
+  uint32_t* chgn2 = chg + n4;      // [2][n4] my variables' changed lanes, by pass parity
+  uint32_t* chg_in = chgn2 + 2 * n4;
   uint32_t* ctst = chg_in + n4;
   uint2* ci = reinterpret_cast<uint2*>(ctst + ((n + 8 + 3) & ~3));
   constexpr int CPG = 8 / W;  // columns per 8-byte group
@@ -492,7 +492,8 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
     if (tid == 0) s_empty0 = 0u;
     for (int x = tid; x < n4; x += T) {
       chg[x] = 0u;
-      chgn[x] = 0u;
+      chgn2[x] = 0u;
+      chgn2[n4 + x] = 0u;
     }
     if (tid < 32) {
       s_iters[tid] = 0;
@@ -583,6 +584,10 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
     for (;;) {
       ++t;
       const int par = t & 1;
+      uint32_t* chgn = chgn2 + (size_t)par * n4;               // this pass's changed lanes (my variables)
+      const uint32_t* chgp = chgn2 + (size_t)(par ^ 1) * n4;   // the previous pass's
+      // lanes for which y changed in the previous pass (pass 1: the seeds / roots)
+      auto chgof = [&](int y) -> uint32_t { return t == 1 ? chg[y] : (y >= x0 && y < x1 ? chgp[y] : chg_in[y]); };
       // ---- prep: tst / the column list (warp 0), tables of the changed columns
       // (every column in pass 1) by the other warps
       if (tid == 0) {
@@ -598,7 +603,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
 #pragma unroll
           for (int j = 0; j < CPG; ++j) {
             const int y = g * CPG + j;
-            tj[j] = (g < ngr && y < n) ? chg[y] & active : 0u;
+            tj[j] = (g < ngr && y < n) ? chgof(y) & active : 0u;
             any |= tj[j];
           }
           const uint32_t bal = __ballot_sync(0xffffffffu, any != 0u);
@@ -621,7 +626,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         int cnt = 0;
         for (int yb = 0; yb < n; yb += 32) {
           const int y = yb + lane;
-          const uint32_t ty = y < n ? chg[y] & active : 0u;
+          const uint32_t ty = y < n ? chgof(y) & active : 0u;
           const uint32_t bal = __ballot_sync(0xffffffffu, ty != 0u);
           if (ty) {
             const int pos = cnt + __popc(bal & ((1u << lane) - 1u));
@@ -645,7 +650,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
             int ck = 0;
             for (int yb = 0; yb < n; yb += 32) {
               const int y = yb + lane;
-              const bool in = y < n && ((chg[y] >> sl) & 1u);
+              const bool in = y < n && ((chgof(y) >> sl) & 1u);
               const uint32_t bal = __ballot_sync(0xffffffffu, in);
               if (in) psl[(size_t)nps * ps_stride + ck + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)y;
               ck += __popc(bal);
@@ -671,7 +676,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         if (tb >= 0)
           for (int i = tb; i < n * NI; i += TT) {
             const int y = i / NI;
-            if (t == 1 || chg[y] != 0u) build_item<W>(Tb, X, y, i - y * NI, dmax);
+            if (t == 1 || chgof(y) != 0u) build_item<W>(Tb, X, y, i - y * NI, dmax);
           }
       }
 #else
@@ -680,7 +685,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         const int wb = nwarps > 1 ? warp - 1 : warp, NWB = nwarps > 1 ? nwarps - 1 : nwarps;
         if (wb >= 0)
           for (int y = wb; y < n; y += NWB)
-            if (t == 1 || chg[y] != 0u) build_column<W>(Tb, X, y, dmax, lane);
+            if (t == 1 || chgof(y) != 0u) build_column<W>(Tb, X, y, dmax, lane);
       }
 #endif
       __syncthreads();
@@ -741,6 +746,7 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       // rows, my change masks and my partial into every other CTA (fixed sizes:
       // each peer's mbarrier expects exactly these bytes)
       cluster_wait();
+      for (int x = x0 + tid; x < x1; x += T) chgn2[(size_t)(par ^ 1) * n4 + x] = 0u;  // read by this pass's prep only
       if (C > 1) {
         // same layout in every CTA: the peer address is mapa(local address, q)
         const uint32_t xs = (uint32_t)__cvta_generic_to_shared(X + r0), cs = (uint32_t)__cvta_generic_to_shared(chg_in);
@@ -781,16 +787,8 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
         if (stop_conv & bit) s_status[tid] = (E & bit) ? 1 : 0;
       }
       active &= ~(stop_wipe | stop_conv);
-      // next pass's change masks: mine from chgn, the others' as pushed
-      for (int x = tid; x < n; x += T) {
-        if (x >= x0 && x < x1) {
-          chg[x] = chgn[x];
-          chgn[x] = 0u;
-        } else {
-          chg[x] = chg_in[x];
-        }
-      }
-      __syncthreads();
+      // (the next pass's prep reads the change masks in place -- mine from chgn,
+      // the others' from chg_in -- so no copy and no block barrier here)
       CL_MARK();
       if (active == 0u) break;
     }
@@ -817,7 +815,7 @@ size_t batch_cl_smem(int n, int dmax, int W) {
   const size_t npad = (n + CPI - 1) / CPI * CPI, n4 = ((size_t)n + 3) & ~(size_t)3;
   const size_t rows4 = (((size_t)n * dmax) + 3) & ~(size_t)3;
   const size_t tb_bytes = std::max(npad * TSB, (size_t)32 * (n + 1) * 8);  // tables, or the staged d_in block
-  return (size_t)TSB + tb_bytes + rows4 * 4 + 3 * n4 * 4 + ((((size_t)n + 8 + 3) & ~(size_t)3) * 4) +
+  return (size_t)TSB + tb_bytes + rows4 * 4 + 4 * n4 * 4 + ((((size_t)n + 8 + 3) & ~(size_t)3) * 4) +
          (((size_t)n + 8 + 1) & ~(size_t)1) * 8 +
          ((((size_t)n + 8 / W - 1) / (8 / W) + 4) * (8 / W) + 3) / 4 * 16 +
          ((((size_t)n + 8 / W - 1) / (8 / W) + 4 + 3) & ~(size_t)3) * 4 +
