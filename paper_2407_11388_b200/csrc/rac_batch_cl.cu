@@ -54,6 +54,9 @@ namespace {
 #ifndef RAC_CL_ITEM_TABLES
 #define RAC_CL_ITEM_TABLES 1  // 1: tables built one 16-entry block per thread; 0: one warp per column
 #endif
+#ifndef RAC_CL_STAGE_IF
+#define RAC_CL_STAGE_IF 8  // variables whose 32 states a warp loads at once when staging a word (4 or 8: same, r02ba)
+#endif
 #ifndef RAC_CL_GLOBAL_STAGE
 #define RAC_CL_GLOBAL_STAGE 1  // 1: the word's states transposed by ballots straight from global memory;
                                // 0: staged through shared memory by coalesced loads first
@@ -500,19 +503,20 @@ __global__ void __launch_bounds__(kMaxT, 1) rac_batch_cl(BatchCLParams p) {
       s_status[tid] = 0;
     }
 #if RAC_CL_GLOBAL_STAGE
-    // A/B variant (build-time): ballots straight from global memory, 4 variables in flight per warp
+    // ballots straight from global memory, RAC_CL_STAGE_IF variables in flight per
+    // warp (C5: 8 variables per warp = one load round trip per word)
     __syncthreads();
     {
       uint32_t emp = 0u;
-      for (int xb = warp; xb < n; xb += 4 * nwarps) {
-        uint64_t v[4];
+      for (int xb = warp; xb < n; xb += RAC_CL_STAGE_IF * nwarps) {
+        uint64_t v[RAC_CL_STAGE_IF];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < RAC_CL_STAGE_IF; ++j) {
           const int x = xb + j * nwarps;
           v[j] = (x < n && lane < nst) ? __ldg(p.d_in + (size_t)(s0 + lane) * n + x) & __ldg(p.dommask + x) : 0ull;
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < RAC_CL_STAGE_IF; ++j) {
           const int x = xb + j * nwarps;
           if (x >= n) break;
           emp |= __ballot_sync(0xffffffffu, v[j] == 0ull);
